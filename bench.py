@@ -1,0 +1,486 @@
+#!/usr/bin/env python
+"""bench.py — config evals/s (batched select_config) + controller decisions/s
+(batched control_step replay) on B200, beside the reference's CPU path.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Headline (`value`): cfg2 of BASELINE.json — llama2-7b-like (+tp8), 64 caps x 256
+batches x TP{1,2,4,8} = 65,536 configs, 1e4 QoS throughput targets evaluated and
+selected in one pass. A step = evaluate the grid (FP64, bit-exact), build the
+rank tables, decide all queries; inputs resident in HBM. Unit: (config, query)
+pairs actually scanned per second (queries decided without a scan are not
+counted). `decisions` (same line): cfg4 — 1e6 traces x 3600 control intervals
+through control_step + the fluid plant, one thread per trace.
+
+Multi-GPU (torchrun): weak scaling — every rank runs its own shard of the same
+per-GPU workload (queries/traces offset by rank), no collective on the data
+path; per-step device time is max-reduced over ranks and rank 0 prints.
+`--impl reference`: the reference's own CPU implementation (oracle/_ref, the
+unmodified headers) on all host threads, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "config evals/sec + controller decisions/sec at 1/2/4/8 B200 vs CPU reference"
+SELECT_WORKLOAD = ("cfg2: llama2-7b-like (+tp8 comm), caps 100+300i/63 x batch 1..256 x "
+                   "tp{1,2,4,8} = 65536 configs, 1e4 QoS targets per GPU, eval+rank+select "
+                   "per step")
+REPLAY_WORKLOAD = ("cfg4: 1e6 fluid-plant traces x 3600 control intervals per GPU, 8 calibrated "
+                   "profiles, 6x6 candidates each, QoS/budget-throughput 50/50")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--queries", type=int, default=10_000)
+    ap.add_argument("--traces", type=int, default=1_000_000)
+    ap.add_argument("--trace-steps", type=int, default=3600)
+    ap.add_argument("--replay-steps", type=int, default=None,
+                    help="timed replay steps (default: min(steps, 5))")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="target CPU time per reference sample")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- helpers --
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+
+    def init(self, backend):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.init_process_group(backend)
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, x: float) -> float:
+        return self._reduce(x, "max")
+
+    def sum(self, x: float) -> float:
+        return self._reduce(x, "sum")
+
+    def _reduce(self, x, op):
+        if not self.pg:
+            return x
+        import torch
+        dev = "cuda" if torch.cuda.is_available() else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX if op == "max" else self.pg.ReduceOp.SUM)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+class Clocks:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.index)], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    mx.append(float(parts[2]))
+                except ValueError:
+                    continue
+                for n, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        os.unlink(self.path)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no-samples"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks_json():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def ncu_traffic(kernel: str):
+    """Per-launch DRAM bytes of a kernel from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            return json.load(f).get(kernel, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------- our arm --
+def run_ours(args, dist: Dist):
+    import torch
+
+    from paper_2605_21427_b200 import workloads
+    from paper_2605_21427_b200.abi import QUERY_DT, SUMMARY_DT
+    from paper_2605_21427_b200.wattserve import (AnalyticModel, Context, Grid, Plan,
+                                                 measure_peaks, replay, replay_device)
+
+    torch.cuda.set_device(dist.local)
+    dist.init("nccl")
+    stream = torch.cuda.current_stream()
+    ctx = Context(dist.local)
+    ctx.set_stream(stream.cuda_stream)
+    int_peak, fp64_peak = measure_peaks(ctx)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    def l2_flush():
+        flush.zero_()
+
+    # ---------------- cfg2 select ----------------
+    cfg = workloads.cfg2(args.queries)
+    plan = Plan(AnalyticModel(ctx, cfg["profile"], cfg["gpu"]), Grid(ctx, cfg["points"]),
+                cfg["coeffs"])
+    n_cfg = len(cfg["points"])
+    th, _, _ = plan.scores()
+    tref = float(th.max())
+    nq = args.queries
+    q = workloads.gen_queries(nq, cfg["seed"], tref, "qos", first=dist.rank * nq)
+    d_q = torch.from_numpy(q.view(np.uint8).copy()).cuda()
+    d_idx = torch.empty(nq, dtype=torch.int32, device="cuda")
+    d_rs = torch.empty(nq, dtype=torch.uint8, device="cuda")
+
+    def select_step():
+        plan.prepare()
+        plan.select_device(d_q.data_ptr(), nq, d_idx.data_ptr(), d_rs.data_ptr())
+
+    for _ in range(args.warmup):
+        l2_flush()
+        select_step()
+    torch.cuda.synchronize()
+    counts = plan.stats()
+    scanned_q = int(counts[0] + counts[1] + counts[2])
+    pairs_step = scanned_q * n_cfg
+    int_ops_step = (2 * counts[0] + 4 * counts[1] + 2 * counts[2]) * n_cfg
+    plan.time_scan(True)
+    clocks = Clocks(dist.local)
+    clocks.start()
+    launches0 = ctx.launches
+    step_ms, scan_ms = [], []
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    dist.barrier()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        l2_flush()
+        ev[k][0].record(stream)
+        select_step()
+        ev[k][1].record(stream)
+        scan_ms.append(plan.scan_ms())  # syncs on the scan's end event (outside the step)
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches = ctx.launches - launches0
+    plan.time_scan(False)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    exact_q = int(plan.stats()[5])
+    t_rank = float(np.sum(step_ms))
+    t_max = dist.max(t_rank)
+    pairs_total = dist.sum(float(pairs_step)) * args.steps
+    value = pairs_total / (t_max * 1e-3)
+
+    # e2e through the public host-buffer API (pinned host queries -> H2D -> eval+rank+select
+    # -> D2H index/reason)
+    h_q = torch.empty(nq * QUERY_DT.itemsize, dtype=torch.uint8, pin_memory=True)
+    h_qn = h_q.numpy().view(QUERY_DT)
+    h_qn[:] = q
+    h_idx = torch.empty(nq, dtype=torch.int32, pin_memory=True).numpy()
+    h_rs = torch.empty(nq, dtype=torch.uint8, pin_memory=True).numpy()
+    from paper_2605_21427_b200.abi import ptr
+    lib = ctx.lib
+
+    def e2e_step():
+        rc = lib.pals_select(plan.h, ptr(h_qn), nq, ptr(h_idx), ptr(h_rs))
+        assert rc == 0, lib.pals_last_error()
+
+    for _ in range(args.warmup):
+        e2e_step()
+    e2e_ms = []
+    for _ in range(args.steps):
+        l2_flush()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        e2e_step()
+        b.record(stream)
+        b.synchronize()
+        e2e_ms.append(a.elapsed_time(b))
+    e2e_max = dist.max(float(np.sum(e2e_ms)))
+    e2e_value = pairs_total / (e2e_max * 1e-3)
+
+    scan_avg = float(np.mean(scan_ms))
+    roof = {"bound": "alu", "kernel": "k_scan<uint32_t>",
+            "achieved": int_ops_step / (scan_avg * 1e-3) / 1e12,
+            "peak": int_peak / 1e12, "unit": "Tops/s",
+            "frac": (int_ops_step / (scan_avg * 1e-3)) / int_peak,
+            "traffic": ncu_traffic("k_scan"),
+            "algorithmic": "2 int ops (compare, min) per scanned (config, query) pair; 4 for "
+                           "QoS+budget queries",
+            "peak_source": "measured here: pals_measure_peaks ISETP+VIMNMX chains",
+            "scan_share_of_step": scan_avg / float(np.mean(step_ms))}
+
+    # ---------------- cfg4 replay ----------------
+    s = workloads.cfg4_setup()
+    models = [AnalyticModel(ctx, p, s["gpu"]) for p in s["profiles"]]
+    nt = args.traces
+    spec = workloads.replay_spec(nt, n_steps=args.trace_steps, seed=2605, first=dist.rank * nt)
+    d_sum = torch.empty(nt * SUMMARY_DT.itemsize, dtype=torch.uint8, device="cuda")
+    rsteps = args.replay_steps or min(args.steps, 5)
+    for _ in range(max(1, min(args.warmup, 2))):
+        replay_device(ctx, models, s["profiles"], s["gpu"], s["coeffs"], s["caps"],
+                      s["batches"], s["cfg"], spec, d_sum.data_ptr())
+    torch.cuda.synchronize()
+    rev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(rsteps)]
+    dist.barrier()
+    rl0 = ctx.launches
+    for k in range(rsteps):
+        l2_flush()
+        rev[k][0].record(stream)
+        replay_device(ctx, models, s["profiles"], s["gpu"], s["coeffs"], s["caps"],
+                      s["batches"], s["cfg"], spec, d_sum.data_ptr())
+        rev[k][1].record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    rlaunches = ctx.launches - rl0
+    r_ms = [a.elapsed_time(b) for a, b in rev]
+    clk = clocks.stop()
+    r_max = dist.max(float(np.sum(r_ms)))
+    dec_total = dist.sum(float(nt) * args.trace_steps) * rsteps
+    dec_value = dec_total / (r_max * 1e-3)
+    # e2e: host summaries (D2H 48 B/trace); inputs are generated from (seed, index) on the device
+    re2e = []
+    for _ in range(min(rsteps, 3)):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        replay(ctx, models, s["profiles"], s["gpu"], s["coeffs"], s["caps"], s["batches"],
+               s["cfg"], spec)
+        b.record(stream)
+        b.synchronize()
+        re2e.append(a.elapsed_time(b))
+    re2e_max = dist.max(float(np.mean(re2e)))
+    dec_e2e = dist.sum(float(nt) * args.trace_steps) / (re2e_max * 1e-3)
+    # FP64 work per decision in the replay kernel: PID 15 flops (2 div),
+    # plant noise/min/energy/tokens 10, target test + Kt search ~2*log2(nd_t)+4
+    fp64_per_dec = 40.0
+    dec_roof = {"bound": "fp64", "kernel": "k_replay",
+                "achieved": dec_value / dist.world * fp64_per_dec / 1e12,
+                "peak": fp64_peak / 1e12, "unit": "TFLOP/s",
+                "frac": dec_value / dist.world * fp64_per_dec / fp64_peak,
+                "traffic": ncu_traffic("k_replay"),
+                "algorithmic": f"{fp64_per_dec:.0f} FP64 ops per decision (counted in DESIGN.md "
+                               "§4); the kernel is latency-bound, not FP64-throughput-bound",
+                "peak_source": "measured here: pals_measure_peaks DFMA chains"}
+
+    out = {
+        "metric": METRIC, "value": value, "unit": "config evals/s",
+        "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": SELECT_WORKLOAD, "queries_per_gpu": nq, "configs": n_cfg,
+                   "scanned_queries_per_gpu": scanned_q, "exact_fold_queries": exact_q,
+                   "global_batch": nq * dist.world, "parallelism": f"shard{dist.world}",
+                   "l2": "flushed between steps (256 MiB device write)"},
+        "e2e": {"value": e2e_value, "unit": "config evals/s",
+                "h2d_bytes_per_step": nq * QUERY_DT.itemsize,
+                "d2h_bytes_per_step": nq * 5,
+                "api": "pals_select (C ABI, pinned host buffers; includes eval+rank)"},
+        "roofline": roof,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "decisions": {
+            "metric": "controller decisions/s", "value": dec_value, "unit": "decisions/s",
+            "ms_per_step": r_max / rsteps, "steps": rsteps, "workload": REPLAY_WORKLOAD,
+            "traces_per_gpu": nt, "trace_steps": args.trace_steps,
+            "e2e": {"value": dec_e2e, "unit": "decisions/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": nt * SUMMARY_DT.itemsize,
+                    "api": "pals_replay (C ABI, host summaries)"},
+            "roofline": dec_roof, "gpu_launches": int(rlaunches)},
+        "peaks": {"int_ops_per_s": int_peak, "fp64_flops_per_s": fp64_peak,
+                  "hbm_gbs_measured": measured_peaks_json().get("hbm_gbs")},
+    }
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"], out["decisions"]["cpu_baseline"] = cpu_baselines(args, cfg, tref)
+    if dist.rank == 0:
+        print(json.dumps(out), flush=True)
+    dist.close()
+
+
+# ---------------------------------------------------------- CPU reference --
+def _reference_backend():
+    """The reference build (oracle/_ref) when present, else the C restatement."""
+    from oracle.oracle import Oracle, Reference
+    if Reference.available():
+        return "reference", Reference()
+    return "port", Oracle()
+
+
+def cpu_select(args, cfg, tref, seconds):
+    """select_config + analytic_scorer over cfg2 queries on all host threads."""
+    from paper_2605_21427_b200 import workloads
+    kind, ref = _reference_backend()
+    threads = os.cpu_count() or 1
+    n = len(cfg["points"])
+    if kind == "reference":
+        q = workloads.gen_queries(max(threads, 4 * threads), cfg["seed"], tref, "qos")
+        t, _, _ = ref.bench_select(cfg["profile"], cfg["gpu"], cfg["points"], cfg["coeffs"], q,
+                                   threads, want_results=False)
+        rate = len(q) * n / t
+        nq = int(min(args.queries, max(threads, rate * seconds / n)))
+        q = workloads.gen_queries(nq, cfg["seed"], tref, "qos")
+        t, _, _ = ref.bench_select(cfg["profile"], cfg["gpu"], cfg["points"], cfg["coeffs"], q,
+                                   threads, want_results=False)
+        return {"value": nq * n / t, "unit": "config evals/s", "cores": threads,
+                "kind": "reference",
+                "sample": f"{nq} cfg2 queries x {n} configs through the unmodified "
+                          f"select_config+analytic_scorer, {threads} threads, {t:.1f} s"}
+    # the C port is single threaded
+    T, P, _ = ref.eval(cfg["profile"], cfg["gpu"], cfg["points"])
+    q = workloads.gen_queries(50, cfg["seed"], tref, "qos")
+    t0 = time.perf_counter()
+    ref.select(cfg["points"], T, P, cfg["coeffs"], q)
+    t = time.perf_counter() - t0
+    return {"value": len(q) * n / t, "unit": "config evals/s", "cores": 1, "kind": "port",
+            "sample": f"{len(q)} cfg2 queries, C restatement, 1 thread"}
+
+
+def cpu_replay(args, seconds):
+    from paper_2605_21427_b200 import workloads
+    kind, ref = _reference_backend()
+    s = workloads.cfg4_setup()
+    threads = os.cpu_count() or 1
+    if kind == "reference":
+        probe = workloads.replay_spec(threads * 4, n_steps=args.trace_steps, seed=2605)
+        t, _ = ref.bench_replay(s["profiles"], s["gpu"], s["coeffs"], s["caps"], s["batches"],
+                                s["cfg"], probe, threads)
+        rate = probe.n_traces * args.trace_steps / t
+        ntr = int(max(threads, min(args.traces, rate * seconds / args.trace_steps)))
+        spec = workloads.replay_spec(ntr, n_steps=args.trace_steps, seed=2605)
+        t, _ = ref.bench_replay(s["profiles"], s["gpu"], s["coeffs"], s["caps"], s["batches"],
+                                s["cfg"], spec, threads)
+        return {"value": ntr * args.trace_steps / t, "unit": "decisions/s", "cores": threads,
+                "kind": "reference",
+                "sample": f"{ntr} cfg4 traces x {args.trace_steps} steps through the unmodified "
+                          f"control_step (detail::cached analytic scorer), {threads} threads, "
+                          f"{t:.1f} s"}
+    spec = workloads.replay_spec(8, n_steps=args.trace_steps, seed=2605)
+    t0 = time.perf_counter()
+    ref.replay(s["profiles"], s["gpu"], s["coeffs"], s["caps"], s["batches"], s["cfg"], spec)
+    t = time.perf_counter() - t0
+    return {"value": 8 * args.trace_steps / t, "unit": "decisions/s", "cores": 1, "kind": "port",
+            "sample": f"8 cfg4 traces, C restatement, 1 thread"}
+
+
+def cpu_baselines(args, cfg, tref):
+    return cpu_select(args, cfg, tref, args.cpu_seconds), cpu_replay(args, args.cpu_seconds)
+
+
+def run_reference(args, dist: Dist):
+    """The reference's own CPU implementation of the path, all host threads, rank 0."""
+    if dist.rank != 0:
+        return
+    from paper_2605_21427_b200 import workloads
+    from oracle.oracle import Reference
+    if not Reference.available():
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref/libwsref.so not built (needs /root/reference at build)"}))
+        return
+    cfg = workloads.cfg2(args.queries)
+    ref = Reference()
+    T, P, _ = ref.eval(cfg["profile"], cfg["gpu"], cfg["points"])
+    tref = float(np.max(T * cfg["points"]["dp"]))
+    per_step = max(2.0, 60.0 / max(1, args.steps + args.warmup))
+    vals = []
+    for k in range(args.warmup + args.steps):
+        b = cpu_select(args, cfg, tref, per_step)
+        if k >= args.warmup:
+            vals.append(b)
+    v = float(np.mean([b["value"] for b in vals]))
+    dec = cpu_replay(args, per_step)
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "config evals/s",
+           "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": SELECT_WORKLOAD, "queries_per_gpu": args.queries},
+           "cpu_baseline": vals[-1],
+           "e2e": {"value": v, "unit": "config evals/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0},
+           "decisions": {"metric": "controller decisions/s", "value": dec["value"],
+                         "unit": "decisions/s", "workload": REPLAY_WORKLOAD,
+                         "cpu_baseline": dec,
+                         "e2e": {"value": dec["value"], "unit": "decisions/s",
+                                 "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    dist = Dist()
+    if args.impl == "reference":
+        run_reference(args, dist)
+    else:
+        run_ours(args, dist)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,336 @@
+/*
+ * pals_gpu.h — C ABI of the B200 hot path for the PALS / wattserve reference.
+ *
+ * This is the drop-in boundary. Every entry point below replaces one call
+ * site of the reference's header-only C++ API (paths relative to
+ * /root/reference/proj/include/wattserve/):
+ *
+ *   pals_eval            throughput() + avg_gpu_power()           model.hpp:72-84
+ *   pals_select          select_config() over many Targets         controller.hpp:132-201
+ *   pals_select_one      select_config(), one call                 controller.hpp:132-201
+ *   pals_control_step_one control_step(), one call                 controller.hpp:210-267
+ *   pals_replay          control_step() replayed over traces       controller.hpp:210-267
+ *                        driven by the fluid plant of DESIGN.md §4 (sim.hpp:195-205, 431-472)
+ *   pals_model_analytic  analytic_scorer(profile, gpu)              controller.hpp:107-111
+ *   pals_model_table     TableScorer (test fake)                    tests/test_controller.cpp:17-29
+ *   pals_model_forest    predictor_scorer(bundle, model_id)         controller.hpp:100-105,
+ *                                                                    forest.hpp:227-235
+ *
+ * Plain C types only: pointers, sizes, POD structs. No torch, no C++.
+ * Errors follow the reference's exception taxonomy (types.hpp:13-23):
+ *   PALS_ECONFIG  <-> wattserve::config_error
+ *   PALS_EDATA    <-> wattserve::data_error
+ *   PALS_ERANGE   <-> std::out_of_range
+ *   PALS_ERUNTIME  CUDA / allocation failures (no reference counterpart)
+ * The message of the last failing call on the calling thread is returned by
+ * pals_last_error(); messages start with the reference's own text where one
+ * exists (e.g. "select_config: empty candidate list").
+ *
+ * Threading: calls on different contexts are independent; calls on one
+ * context are serialised by the caller (one host thread per GPU).
+ */
+#ifndef PALS_GPU_H
+#define PALS_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PALS_ABI_VERSION 1
+
+#define PALS_OK 0
+#define PALS_ECONFIG 2
+#define PALS_EDATA 3
+#define PALS_ERUNTIME 4
+#define PALS_ERANGE 5
+
+/* Objective (controller.hpp:17) */
+#define PALS_OBJ_QOS 0    /* Objective::QosMaxEfficiency   */
+#define PALS_OBJ_BUDGET 1 /* Objective::BudgetMaxThroughput */
+
+/* DecisionReason (controller.hpp:65-71), same numeric order */
+#define PALS_REASON_QOS_FEASIBLE 0
+#define PALS_REASON_FALLBACK_MAX_T 1
+#define PALS_REASON_BUDGET_MAX_T 2
+#define PALS_REASON_HOLD 3
+#define PALS_REASON_ORACLE 4
+
+#define PALS_MAX_TP_KEYS 8
+
+/* GpuSpec (types.hpp:27-39) */
+typedef struct {
+    double idle_watts;
+    double min_cap_watts;
+    double max_cap_watts;
+    double max_frequency;
+} pals_gpu_spec;
+
+/* SystemPowerCoeffs (types.hpp:42-49) */
+typedef struct {
+    double alpha;
+    double beta_watts;
+} pals_coeffs;
+
+/* ModelProfile (types.hpp:66-107), flattened: comm_fixed_by_tp becomes
+ * the parallel arrays tp_keys[n_tp] / comm_fixed[n_tp]. */
+typedef struct {
+    char name[64];
+    double compute_fixed;
+    double compute_per_seq;
+    double comm_per_seq;
+    double internode_factor;
+    double knee_watts;
+    double compute_power_base;
+    double compute_power_per_seq;
+    double comm_power;
+    double overlap;
+    double comm_fixed[PALS_MAX_TP_KEYS];
+    double total_params_b;
+    double active_params_b;
+    int32_t tp_keys[PALS_MAX_TP_KEYS];
+    int32_t n_tp;
+    int32_t num_experts;
+    int32_t top_k;
+    int32_t deploy_tp;
+    int32_t deploy_ep;
+    int32_t deploy_dp;
+} pals_profile;
+
+/* OperatingPoint (types.hpp:110-116) */
+typedef struct {
+    double cap_watts;
+    int32_t batch;
+    int32_t tp;
+    int32_t ep;
+    int32_t dp;
+} pals_point;
+
+/* One select_config() call's non-candidate arguments (controller.hpp:132-135):
+ * Targets{throughput_tps, power_budget_w, objective} plus bias, headroom, margin.
+ * has_budget == 0 is std::nullopt. */
+typedef struct {
+    double throughput_tps;
+    double power_budget_w;
+    double bias;
+    double target_headroom;
+    double budget_margin;
+    int32_t objective;
+    int32_t has_budget;
+} pals_query;
+
+/* Targets (controller.hpp:19-29) */
+typedef struct {
+    double throughput_tps;
+    double power_budget_w;
+    double epsilon;
+    int32_t has_budget;
+    int32_t objective;
+} pals_targets;
+
+/* ControllerConfig (controller.hpp:37-53) with PidGains (:31-35) inlined */
+typedef struct {
+    double kp;
+    double ki;
+    double kd;
+    double integral_clamp;
+    double bias_min;
+    double bias_max;
+    double interval_s;
+    double target_headroom;
+    double budget_margin;
+    int32_t sustain_intervals;
+    int32_t _pad;
+} pals_ctrl_cfg;
+
+/* ControllerState (controller.hpp:55-63); last_targets.has_value() is has_last_targets */
+typedef struct {
+    double bias;
+    double integral;
+    double prev_error;
+    pals_point current;
+    pals_targets last_targets;
+    int32_t has_prev_error;
+    int32_t sustain_count;
+    int32_t has_last_targets;
+    int32_t _pad;
+} pals_ctrl_state;
+
+/* Decision (controller.hpp:85-89) */
+typedef struct {
+    pals_point point;
+    int32_t applied;
+    int32_t reason;
+} pals_decision;
+
+/* TelemetryInput (controller.hpp:203-206) */
+typedef struct {
+    double t_s;
+    double throughput_tps;
+} pals_telemetry;
+
+/* Synthetic fluid-plant replay workload. Every trace is a pure
+ * function of (seed, global trace index), so shards need no input transfer. */
+typedef struct {
+    uint64_t seed;
+    int64_t first_trace;      /* global index of this shard's first trace */
+    int64_t n_traces;
+    int32_t n_steps;          /* control intervals per trace */
+    int32_t objective_mode;   /* 0 all QoS, 1 all budget-throughput, 2 mixed 50/50 */
+    double interval_s;
+    double qos_frac_lo, qos_frac_hi;   /* target = U(lo,hi) * unconstrained T */
+    double load_lo, load_hi;           /* offered load = U(lo,hi) * unconstrained T */
+    double noise_amp;                  /* measured *= 1 + amp*U(-1,1) */
+    double budget_lo_frac, budget_hi_frac; /* budget = U(lo*min p_node, hi*max p_node) */
+    double epsilon;                    /* Targets::epsilon */
+    int32_t seg_min, seg_max;          /* segment length U{min..max} steps */
+    int32_t budget_mode;               /* 0 unbudgeted, 1 piecewise-constant budget */
+    int32_t n_log_traces;              /* first n traces log every step */
+} pals_replay_spec;
+
+/* Per-trace replay result */
+typedef struct {
+    uint64_t digest;      /* FNV-1a over per-step (idx, applied, reason) words + final state */
+    double final_bias;
+    double energy_j;      /* sum of cluster_system_power * interval */
+    double tokens;        /* sum of measured tps * interval */
+    int32_t n_applied;
+    int32_t final_idx;
+    int32_t model;
+    int32_t objective;
+} pals_trace_summary;
+
+/* Per-step decision log record (metrics.hpp:145-156 fields that vary) */
+typedef struct {
+    int32_t idx;       /* candidate index of Decision::point */
+    uint8_t applied;
+    uint8_t reason;
+    uint16_t cap_tenths; /* enforced cap * 10 after the breaker walk */
+} pals_step_log;
+
+typedef struct pals_ctx pals_ctx;
+typedef struct pals_model pals_model;
+typedef struct pals_grid pals_grid;
+typedef struct pals_plan pals_plan;
+
+const char* pals_last_error(void);
+int pals_abi_version(void);
+
+/* ---- context ---------------------------------------------------------- */
+int pals_ctx_create(int device, pals_ctx** out);
+int pals_ctx_destroy(pals_ctx* ctx);
+/* Use an external cudaStream_t (e.g. torch's current stream); NULL restores
+ * the context's own stream. */
+int pals_ctx_set_stream(pals_ctx* ctx, void* cuda_stream);
+void* pals_ctx_stream(pals_ctx* ctx);
+int pals_ctx_sync(pals_ctx* ctx);
+/* Number of kernels this context has launched so far. */
+int64_t pals_ctx_launch_count(pals_ctx* ctx);
+
+/* ---- models (the three concrete Scorer kinds) ------------------------- */
+/* analytic_scorer(profile, gpu): validates like ModelProfile::validate (types.hpp:88-106) */
+int pals_model_analytic(pals_ctx* ctx, const pals_profile* profile, const pals_gpu_spec* gpu,
+                        pals_model** out);
+/* TableScorer: scores looked up by point value, first match wins */
+int pals_model_table(pals_ctx* ctx, const pals_point* points, const double* throughput_tps,
+                     const double* gpu_power_w, int64_t n, pals_model** out);
+/* predictor_scorer(bundle, model_id): one tree ensemble per target, SoA nodes.
+ * Trees of one forest are concatenated; tree t spans [tree_offset[t], tree_offset[t+1]).
+ * child indices are tree-local (forest.hpp:62-68). model_index is the one-hot slot
+ * FeatureSchema::model_index(model_id) (forest.hpp:34-39); n_features = 5 + n_models. */
+int pals_model_forest(pals_ctx* ctx, int32_t n_models, int32_t model_index,
+                      const pals_coeffs* coeffs,
+                      int32_t t_n_trees, const int64_t* t_tree_offset, const int32_t* t_feature,
+                      const double* t_threshold, const int32_t* t_left, const int32_t* t_right,
+                      const double* t_value,
+                      int32_t p_n_trees, const int64_t* p_tree_offset, const int32_t* p_feature,
+                      const double* p_threshold, const int32_t* p_left, const int32_t* p_right,
+                      const double* p_value, pals_model** out);
+int pals_model_destroy(pals_model* m);
+
+/* ---- candidate grids -------------------------------------------------- */
+int pals_grid_points(pals_ctx* ctx, const pals_point* points, int64_t n, pals_grid** out);
+/* Canonical sweep nesting cap -> batch -> tp -> ep -> dp (sweep.hpp:134-138) */
+int pals_grid_axes(pals_ctx* ctx, const double* caps, int32_t n_caps, const int32_t* batches,
+                   int32_t n_batches, const int32_t* tps, int32_t n_tps, const int32_t* eps,
+                   int32_t n_eps, const int32_t* dps, int32_t n_dps, pals_grid** out);
+int64_t pals_grid_size(const pals_grid* g);
+int pals_grid_destroy(pals_grid* g);
+
+/* ---- evaluation: Scorer(point) for every grid point ------------------- */
+/* Host outputs: throughput_tps and gpu_power_w per point (CandidateScore). */
+int pals_eval(pals_ctx* ctx, const pals_model* m, const pals_grid* g, double* throughput_tps,
+              double* gpu_power_w);
+
+/* ---- selection plans: model x grid x coeffs --------------------------- */
+int pals_plan_create(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
+                     const pals_coeffs* coeffs, pals_plan** out);
+int pals_plan_destroy(pals_plan* p);
+/* Async on the context stream: evaluate the grid and build the rank tables. */
+int pals_plan_prepare(pals_plan* p);
+/* Async: select for n queries resident in device memory. */
+int pals_plan_select_device(pals_plan* p, const pals_query* d_queries, int64_t n,
+                            int32_t* d_index, uint8_t* d_reason);
+/* Host buffers in and out: prepare + H2D + select + D2H, synchronous.
+ * The batched equivalent of n calls to select_config (controller.hpp:132). */
+int pals_select(pals_plan* p, const pals_query* queries, int64_t n, int32_t* index,
+                uint8_t* reason);
+/* Host copies of the per-point scores the plan selected on:
+ * t_hat = dp*T, p_node = dp*(alpha*4*P+beta), eff = t_hat/p_node (controller.hpp:147-150,163) */
+int pals_plan_scores(pals_plan* p, double* t_hat, double* p_node, double* eff);
+/* Diagnostics of the last select: queries resolved by the exact sequential fold. */
+int64_t pals_plan_last_exact_count(const pals_plan* p);
+/* Force every query through the exact sequential fold (testing). */
+int pals_plan_set_force_exact(pals_plan* p, int force);
+/* Synchronises, then reports the last select's per-class query counts:
+ * class_counts[0..3] = QoS-no-budget / QoS+budget / budget-only scans / no-scan,
+ * class_counts[4] = forced exact, class_counts[5] = queries decided by the exact fold.
+ * Scanned (query, point) pairs = (c[0]+c[1]+c[2]) * grid size. */
+int pals_plan_stats(pals_plan* p, int64_t* class_counts6);
+
+/* ---- measurement helpers (bench.py) ----------------------------------- */
+/* When enabled, the select path records CUDA events around its pair-scan kernel
+ * on the context stream; pals_plan_scan_ms() synchronises on the end event and
+ * returns that kernel's duration in the last select (ms, < 0 if unavailable). */
+int pals_plan_time_scan(pals_plan* p, int enable);
+double pals_plan_scan_ms(pals_plan* p);
+/* Peak integer compare+min rate (ops/s) and FP64 FMA rate (flop/s) of this device. */
+int pals_measure_peaks(pals_ctx* ctx, double* int_ops_per_s, double* fp64_flops_per_s);
+
+/* ---- single-call mirrors (the C++ adapter uses these) ----------------- */
+int pals_select_one(pals_ctx* ctx, const pals_model* m, const pals_point* candidates, int64_t n,
+                    const pals_targets* targets, const pals_coeffs* coeffs, double bias,
+                    double target_headroom, double budget_margin, pals_decision* out);
+int pals_control_step_one(pals_ctx* ctx, const pals_model* m, const pals_telemetry* telemetry,
+                          double now_s, const pals_targets* targets,
+                          const pals_point* candidates, int64_t n, const pals_coeffs* coeffs,
+                          const pals_ctrl_state* state, const pals_ctrl_cfg* cfg,
+                          pals_decision* out_decision, pals_ctrl_state* out_state);
+
+/* ---- batched controller replay --------------------------------------- */
+/* models[k] scores candidate grid k (the scenario grid caps x batches at
+ * profile k's deployment tp/ep/dp, built by build_candidates order sim.hpp:293-308);
+ * plant[k] is the analytic profile the fluid plant runs (the "true" system).
+ * Trace i uses model splitmix64(seed ^ i) % n_models. summaries: n_traces
+ * entries (host). logs: n_log_traces * n_steps entries (host) or NULL. */
+int pals_replay(pals_ctx* ctx, int32_t n_models, pals_model* const* models,
+                const pals_profile* plant, const pals_gpu_spec* gpu, const pals_coeffs* coeffs,
+                const double* caps, int32_t n_caps, const int32_t* batches, int32_t n_batches,
+                const pals_ctrl_cfg* cfg, const pals_replay_spec* spec,
+                pals_trace_summary* summaries, pals_step_log* logs);
+
+/* Replay with device-resident outputs (bench: no host copies in the timed region).
+ * Plans are built once per (models, caps, batches) and cached in the context. */
+int pals_replay_device(pals_ctx* ctx, int32_t n_models, pals_model* const* models,
+                       const pals_profile* plant, const pals_gpu_spec* gpu,
+                       const pals_coeffs* coeffs, const double* caps, int32_t n_caps,
+                       const int32_t* batches, int32_t n_batches, const pals_ctrl_cfg* cfg,
+                       const pals_replay_spec* spec, pals_trace_summary* d_summaries,
+                       pals_step_log* d_logs);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PALS_GPU_H */

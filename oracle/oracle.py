@@ -1,0 +1,256 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes front-end to the two CPU checkers.
+
+* ``Oracle``: the plain-C restatement (oracle/liboracle.so, pals_oracle.c).
+* ``Reference``: the unmodified reference headers behind oracle/ref_harness.cpp
+  (oracle/_ref/libwsref.so). Built here from /root/reference by oracle/Makefile;
+  shipped prebuilt to the GPU box.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+arm may import this module. The product (paper_2605_21427_b200) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+from paper_2605_21427_b200.abi import (POINT_DT, QUERY_DT, STEPLOG_DT, SUMMARY_DT, Coeffs,
+                                       CtrlCfg, CtrlState, Decision, GpuSpec, Profile,
+                                       ReplaySpec, Targets, Telemetry, ptr)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libwsref.so")
+
+_VP = C.c_void_p
+_P = C.POINTER
+
+
+def build(quiet: bool = True) -> None:
+    """Compile both checkers (the reference one only where /root/reference exists)."""
+    out = subprocess.run(["make", "-C", HERE], capture_output=True, text=True)
+    if out.returncode != 0:
+        raise RuntimeError("oracle build failed:\n" + out.stdout + out.stderr)
+    if not quiet:
+        print(out.stdout)
+
+
+def _load(path: str) -> C.CDLL:
+    if not os.path.exists(path):
+        build()
+    return C.CDLL(path)
+
+
+class Oracle:
+    """Plain-C restatement of the reference hot path (pals_oracle.c)."""
+
+    def __init__(self, path: str = ORACLE_SO):
+        L = self.lib = _load(path)
+        L.or_splitmix64.restype = C.c_uint64
+        L.or_splitmix64.argtypes = [C.c_uint64]
+        L.or_effective_frequency.restype = C.c_double
+        L.or_effective_frequency.argtypes = [C.c_double, _VP, _VP, _P(C.c_int)]
+        L.or_eval.argtypes = [_VP, _VP, _VP, C.c_int64, _VP, _VP, _VP]
+        L.or_select_scored.argtypes = [_VP, C.c_int64, _VP, _VP, _VP, _VP, _VP, _VP]
+        L.or_control_step_scored.argtypes = [_VP, C.c_int64, _VP, _VP, C.c_double, C.c_int,
+                                             _VP, C.c_double, _VP, _VP, _VP, _VP, _VP, _VP]
+        L.or_replay.argtypes = [C.c_int, _VP, _VP, _VP, _VP, C.c_int, _VP, C.c_int, _VP, _VP,
+                                _VP, _VP]
+
+    def splitmix64(self, x: int) -> int:
+        return self.lib.or_splitmix64(x)
+
+    def effective_frequency(self, cap, prof: Profile, gpu: GpuSpec):
+        e = C.c_int(0)
+        f = self.lib.or_effective_frequency(cap, C.byref(prof), C.byref(gpu), C.byref(e))
+        return f, e.value
+
+    def eval(self, prof: Profile, gpu: GpuSpec, pts: np.ndarray):
+        n = len(pts)
+        T = np.empty(n, np.float64)
+        P = np.empty(n, np.float64)
+        err = np.empty(n, np.int32)
+        self.lib.or_eval(C.byref(prof), C.byref(gpu), ptr(pts), n, ptr(T), ptr(P), ptr(err))
+        return T, P, err
+
+    def select(self, pts: np.ndarray, T: np.ndarray, P: np.ndarray, coeffs: Coeffs,
+               queries: np.ndarray):
+        """select_config per query over pre-scored candidates; returns (idx, reason, rc)."""
+        pts = np.ascontiguousarray(pts, dtype=POINT_DT)
+        T = np.ascontiguousarray(T, np.float64)
+        P = np.ascontiguousarray(P, np.float64)
+        nq = len(queries)
+        idx = np.empty(nq, np.int32)
+        rs = np.empty(nq, np.uint8)
+        rc = 0
+        for j in range(nq):
+            q = np.ascontiguousarray(queries[j:j + 1], dtype=QUERY_DT)
+            rc = self.lib.or_select_scored(ptr(pts), len(pts), ptr(T), ptr(P), C.byref(coeffs),
+                                           ptr(q), ptr(idx[j:]), ptr(rs[j:]))
+            if rc:
+                return idx, rs, rc
+        return idx, rs, rc
+
+    def control_step(self, pts, T, P, cur_T, cur_ok, tel: Telemetry, now, tg: Targets,
+                     coeffs: Coeffs, st: CtrlState, cfg: CtrlCfg):
+        d = Decision()
+        st2 = CtrlState()
+        rc = self.lib.or_control_step_scored(ptr(pts), len(pts), ptr(T), ptr(P), cur_T,
+                                             int(cur_ok), C.byref(tel), now, C.byref(tg),
+                                             C.byref(coeffs), C.byref(st), C.byref(cfg),
+                                             C.byref(d), C.byref(st2))
+        return d, st2, rc
+
+    def replay(self, plant, gpu, coeffs, caps, batches, cfg: CtrlCfg, spec: ReplaySpec):
+        profs = (Profile * len(plant))(*plant)
+        caps = np.ascontiguousarray(caps, np.float64)
+        batches = np.ascontiguousarray(batches, np.int32)
+        summ = np.zeros(spec.n_traces, SUMMARY_DT)
+        logs = np.zeros(max(1, spec.n_log_traces * spec.n_steps), STEPLOG_DT)
+        rc = self.lib.or_replay(len(plant), profs, C.byref(gpu), C.byref(coeffs), ptr(caps),
+                                len(caps), ptr(batches), len(batches), C.byref(cfg),
+                                C.byref(spec), ptr(summ), ptr(logs))
+        if rc:
+            raise RuntimeError(f"or_replay rc={rc}")
+        return summ, logs[: spec.n_log_traces * spec.n_steps]
+
+
+class Reference:
+    """The unmodified reference (oracle/_ref/libwsref.so)."""
+
+    @staticmethod
+    def available() -> bool:
+        return os.path.exists(REF_SO)
+
+    def __init__(self, path: str = REF_SO):
+        if not os.path.exists(path):
+            build()
+        if not os.path.exists(path):
+            raise FileNotFoundError(path)
+        L = self.lib = C.CDLL(path)
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_splitmix64.restype = C.c_uint64
+        L.ref_splitmix64.argtypes = [C.c_uint64]
+        L.ref_eval.argtypes = [_VP, _VP, _VP, C.c_int64, _VP, _VP, _VP]
+        L.ref_effective_frequency.restype = C.c_double
+        L.ref_effective_frequency.argtypes = [C.c_double, _VP, _VP, _P(C.c_int)]
+        L.ref_validate.argtypes = [_VP, _VP]
+        L.ref_select_analytic.argtypes = [_VP, _VP, _VP, C.c_int64, _VP, _VP, C.c_int64, _VP,
+                                          _VP]
+        L.ref_select_table.argtypes = [_VP, C.c_int64, _VP, _VP, _VP, _VP, C.c_int64, _VP, _VP]
+        L.ref_control_step_table.argtypes = [_VP, C.c_int64, _VP, _VP, _VP, C.c_double, _VP,
+                                             _VP, _VP, _VP, _VP, _VP]
+        L.ref_control_step_analytic.argtypes = [_VP, _VP, _VP, C.c_int64, _VP, C.c_double, _VP,
+                                                _VP, _VP, _VP, _VP, _VP]
+        L.ref_replay.argtypes = [C.c_int, _VP, _VP, _VP, _VP, C.c_int, _VP, C.c_int, _VP, _VP,
+                                 _VP, _VP]
+        L.ref_bench_select.restype = C.c_double
+        L.ref_bench_select.argtypes = [_VP, _VP, _VP, C.c_int64, _VP, _VP, C.c_int64, C.c_int,
+                                       _VP, _VP]
+        L.ref_bench_replay.restype = C.c_double
+        L.ref_bench_replay.argtypes = [C.c_int, _VP, _VP, _VP, _VP, C.c_int, _VP, C.c_int, _VP,
+                                       _VP, C.c_int, _VP]
+        L.ref_load_profile.argtypes = [C.c_char_p, _VP]
+        L.ref_load_platform.argtypes = [C.c_char_p, _VP, _VP]
+
+    def last_error(self) -> str:
+        return self.lib.ref_last_error().decode()
+
+    def eval(self, prof: Profile, gpu: GpuSpec, pts: np.ndarray):
+        n = len(pts)
+        T = np.empty(n, np.float64)
+        P = np.empty(n, np.float64)
+        err = np.empty(n, np.int32)
+        self.lib.ref_eval(C.byref(prof), C.byref(gpu), ptr(pts), n, ptr(T), ptr(P), ptr(err))
+        return T, P, err
+
+    def effective_frequency(self, cap, prof: Profile, gpu: GpuSpec):
+        e = C.c_int(0)
+        f = self.lib.ref_effective_frequency(cap, C.byref(prof), C.byref(gpu), C.byref(e))
+        return f, e.value
+
+    def select_analytic(self, prof, gpu, pts, coeffs, queries):
+        nq = len(queries)
+        idx = np.empty(nq, np.int32)
+        rs = np.empty(nq, np.uint8)
+        q = np.ascontiguousarray(queries, dtype=QUERY_DT)
+        rc = self.lib.ref_select_analytic(C.byref(prof), C.byref(gpu), ptr(pts), len(pts),
+                                          C.byref(coeffs), ptr(q), nq, ptr(idx), ptr(rs))
+        return idx, rs, rc
+
+    def select_table(self, pts, T, P, coeffs, queries):
+        nq = len(queries)
+        idx = np.empty(nq, np.int32)
+        rs = np.empty(nq, np.uint8)
+        q = np.ascontiguousarray(queries, dtype=QUERY_DT)
+        T = np.ascontiguousarray(T, np.float64)
+        P = np.ascontiguousarray(P, np.float64)
+        rc = self.lib.ref_select_table(ptr(pts), len(pts), ptr(T), ptr(P), C.byref(coeffs),
+                                       ptr(q), nq, ptr(idx), ptr(rs))
+        return idx, rs, rc
+
+    def control_step_table(self, pts, T, P, tel, now, tg, coeffs, st, cfg):
+        d = Decision()
+        st2 = CtrlState()
+        rc = self.lib.ref_control_step_table(ptr(pts), len(pts), ptr(T), ptr(P), C.byref(tel),
+                                             now, C.byref(tg), C.byref(coeffs), C.byref(st),
+                                             C.byref(cfg), C.byref(d), C.byref(st2))
+        return d, st2, rc
+
+    def control_step_analytic(self, prof, gpu, pts, tel, now, tg, coeffs, st, cfg):
+        d = Decision()
+        st2 = CtrlState()
+        rc = self.lib.ref_control_step_analytic(C.byref(prof), C.byref(gpu), ptr(pts), len(pts),
+                                                C.byref(tel), now, C.byref(tg), C.byref(coeffs),
+                                                C.byref(st), C.byref(cfg), C.byref(d),
+                                                C.byref(st2))
+        return d, st2, rc
+
+    def replay(self, plant, gpu, coeffs, caps, batches, cfg, spec):
+        profs = (Profile * len(plant))(*plant)
+        caps = np.ascontiguousarray(caps, np.float64)
+        batches = np.ascontiguousarray(batches, np.int32)
+        summ = np.zeros(spec.n_traces, SUMMARY_DT)
+        logs = np.zeros(max(1, spec.n_log_traces * spec.n_steps), STEPLOG_DT)
+        rc = self.lib.ref_replay(len(plant), profs, C.byref(gpu), C.byref(coeffs), ptr(caps),
+                                 len(caps), ptr(batches), len(batches), C.byref(cfg),
+                                 C.byref(spec), ptr(summ), ptr(logs))
+        if rc:
+            raise RuntimeError(f"ref_replay rc={rc}: {self.last_error()}")
+        return summ, logs[: spec.n_log_traces * spec.n_steps]
+
+    def bench_select(self, prof, gpu, pts, coeffs, queries, threads, want_results=True):
+        nq = len(queries)
+        idx = np.empty(nq, np.int32) if want_results else None
+        rs = np.empty(nq, np.uint8) if want_results else None
+        q = np.ascontiguousarray(queries, dtype=QUERY_DT)
+        secs = self.lib.ref_bench_select(C.byref(prof), C.byref(gpu), ptr(pts), len(pts),
+                                         C.byref(coeffs), ptr(q), nq, threads, ptr(idx), ptr(rs))
+        return secs, idx, rs
+
+    def bench_replay(self, plant, gpu, coeffs, caps, batches, cfg, spec, threads):
+        profs = (Profile * len(plant))(*plant)
+        caps = np.ascontiguousarray(caps, np.float64)
+        batches = np.ascontiguousarray(batches, np.int32)
+        summ = np.zeros(spec.n_traces, SUMMARY_DT)
+        secs = self.lib.ref_bench_replay(len(plant), profs, C.byref(gpu), C.byref(coeffs),
+                                         ptr(caps), len(caps), ptr(batches), len(batches),
+                                         C.byref(cfg), C.byref(spec), threads, ptr(summ))
+        return secs, summ
+
+    def load_profile(self, path: str) -> Profile:
+        p = Profile()
+        rc = self.lib.ref_load_profile(path.encode(), C.byref(p))
+        if rc:
+            raise RuntimeError(self.last_error())
+        return p
+
+    def load_platform(self, path: str):
+        g = GpuSpec()
+        k = Coeffs()
+        rc = self.lib.ref_load_platform(path.encode(), C.byref(g), C.byref(k))
+        if rc:
+            raise RuntimeError(self.last_error())
+        return g, k

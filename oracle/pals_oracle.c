@@ -1,0 +1,434 @@
+/*
+ * pals_oracle.c — TEST INFRASTRUCTURE ONLY: a plain-C restatement of the
+ * reference hot path, used by tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline leg as the CHECKER. The product path never links or calls it.
+ *
+ * Parity pinned: tests/test_oracle.py checks every function here against the
+ * unmodified reference (oracle/_ref/libwsref.so, built from
+ * /root/reference/proj/include by oracle/Makefile) and against the committed
+ * fixtures in tests/golden/ that the reference produced (oracle/gen_golden.py).
+ *
+ * Arithmetic is IEEE FP64 in the reference's operation order, compiled with
+ * -ffp-contract=off (the reference's Release build has no FMA).
+ * Citations are /root/reference/proj/include/wattserve/<file>:<line>.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "../include/pals_gpu.h"
+
+/* libstdc++ helpers (stl_algobase.h:257-265, stl_algo.h:3667-3671) */
+static double smax(double a, double b) { return a < b ? b : a; }
+static double smin(double a, double b) { return b < a ? b : a; }
+static double sclamp(double v, double lo, double hi) { return smin(smax(v, lo), hi); }
+
+/* rng.hpp:15-20 */
+uint64_t or_splitmix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+
+/* model.hpp:37-45 */
+double or_effective_frequency(double cap, const pals_profile* p, const pals_gpu_spec* g,
+                              int* err) {
+    *err = PALS_OK;
+    if (cap < g->min_cap_watts || cap > g->max_cap_watts) {
+        *err = PALS_ERANGE;
+        return NAN;
+    }
+    const double span = p->knee_watts - g->min_cap_watts;
+    if (span <= 0.0) return g->max_frequency;
+    const double ratio = (cap - g->min_cap_watts) / span;
+    return g->max_frequency * sclamp(ratio, 0.4, 1.0);
+}
+
+/* OperatingPoint::validate types.hpp:117-123, then model.hpp:53-68 */
+static int step_timing(const pals_point* c, const pals_profile* p, const pals_gpu_spec* g,
+                       double* t_comp, double* t_comm, double* step) {
+    if (c->cap_watts < g->min_cap_watts || c->cap_watts > g->max_cap_watts) return PALS_ERANGE;
+    if (c->batch < 1) return PALS_ECONFIG;
+    if (c->tp < 1 || c->ep < 1 || c->dp < 1) return PALS_ECONFIG;
+    int k = -1;
+    for (int i = 0; i < p->n_tp; ++i)
+        if (p->tp_keys[i] == c->tp) k = i;
+    if (k < 0) return PALS_ECONFIG;
+    int err;
+    const double f = or_effective_frequency(c->cap_watts, p, g, &err);
+    const double B = (double)c->batch;
+    *t_comp = (p->compute_fixed + p->compute_per_seq * B / (double)c->tp) / f;
+    *t_comm = (p->comm_fixed[k] + p->comm_per_seq * B) *
+              pow(p->internode_factor, (double)(c->dp - 1));
+    const double hi = smax(*t_comp, *t_comm);
+    const double lo = smin(*t_comp, *t_comm);
+    *step = hi + (1.0 - p->overlap) * lo;
+    return PALS_OK;
+}
+
+/* throughput model.hpp:72-75 and avg_gpu_power model.hpp:78-84 */
+int or_score(const pals_point* c, const pals_profile* p, const pals_gpu_spec* g, double* T,
+             double* P) {
+    double tc, tm, st;
+    const int rc = step_timing(c, p, g, &tc, &tm, &st);
+    if (rc != PALS_OK) {
+        *T = *P = NAN;
+        return rc;
+    }
+    *T = (double)c->batch / st;
+    const double demand =
+        p->compute_power_base + p->compute_power_per_seq * (double)c->batch / (double)c->tp;
+    const double p_comp = smin(c->cap_watts, demand);
+    const double comm_share = st - tc;
+    *P = (tc * p_comp + comm_share * p->comm_power) / st;
+    return PALS_OK;
+}
+
+int or_eval(const pals_profile* p, const pals_gpu_spec* g, const pals_point* pts, int64_t n,
+            double* T, double* P, int* err) {
+    int rc = PALS_OK;
+    for (int64_t i = 0; i < n; ++i) {
+        err[i] = or_score(&pts[i], p, g, &T[i], &P[i]);
+        if (err[i] != PALS_OK) rc = err[i];
+    }
+    return rc;
+}
+
+/* detail::better_candidate controller.hpp:118-125 */
+int or_better(double sa, const pals_point* a, double sb, const pals_point* b) {
+    const double scale = smax(smax(fabs(sa), fabs(sb)), 1e-300);
+    if ((sa - sb) / scale > 1e-9) return 1;
+    if ((sb - sa) / scale > 1e-9) return 0;
+    if (a->cap_watts != b->cap_watts) return a->cap_watts < b->cap_watts;
+    return a->batch < b->batch;
+}
+
+/* select_config controller.hpp:132-201 over pre-scored candidates
+ * (T[i], P[i]) = score(candidates[i]); returns the index of Decision::point. */
+int or_select_scored(const pals_point* c, int64_t n, const double* T, const double* P,
+                     const pals_coeffs* k, const pals_query* q, int32_t* idx, uint8_t* reason) {
+    if (n <= 0) return PALS_ECONFIG;
+    const double target = q->throughput_tps * (1.0 + q->target_headroom);
+    double* th = (double*)malloc(sizeof(double) * (size_t)n);
+    double* pn = (double*)malloc(sizeof(double) * (size_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+        pn[i] = (double)c[i].dp * (k->alpha * 4.0 * P[i] + k->beta_watts);
+        th[i] = (double)c[i].dp * T[i];
+    }
+    const int budget_set = q->has_budget != 0;
+    const double budget = budget_set ? q->power_budget_w * (1.0 - q->budget_margin) : 0.0;
+    int64_t best = -1;
+    int r = PALS_REASON_FALLBACK_MAX_T;
+    if (q->objective == PALS_OBJ_QOS) {
+        for (int64_t i = 0; i < n; ++i) {
+            if ((budget_set && !(pn[i] <= budget)) || th[i] * q->bias < target) continue;
+            if (best < 0 || or_better(th[i] / pn[i], &c[i], th[best] / pn[best], &c[best]))
+                best = i;
+        }
+        if (best >= 0) r = PALS_REASON_QOS_FEASIBLE;
+    }
+    if (best < 0 && budget_set) {
+        for (int64_t i = 0; i < n; ++i) {
+            if (!(pn[i] <= budget)) continue;
+            if (best < 0 || or_better(th[i], &c[i], th[best], &c[best])) best = i;
+        }
+        if (best >= 0) r = PALS_REASON_BUDGET_MAX_T;
+        if (best < 0) {
+            for (int64_t i = 0; i < n; ++i)
+                if (best < 0 || or_better(-pn[i], &c[i], -pn[best], &c[best])) best = i;
+            r = PALS_REASON_BUDGET_MAX_T;
+        }
+    }
+    if (best < 0) {
+        for (int64_t i = 0; i < n; ++i)
+            if (best < 0 || or_better(th[i], &c[i], th[best], &c[best])) best = i;
+        r = PALS_REASON_FALLBACK_MAX_T;
+    }
+    free(th);
+    free(pn);
+    *idx = (int32_t)best;
+    *reason = (uint8_t)r;
+    return PALS_OK;
+}
+
+static int point_eq(const pals_point* a, const pals_point* b) {
+    return a->cap_watts == b->cap_watts && a->batch == b->batch && a->tp == b->tp &&
+           a->ep == b->ep && a->dp == b->dp;
+}
+
+static int targets_eq(const pals_targets* a, const pals_targets* b) {
+    /* Targets::operator== controller.hpp:25-28 (std::optional compare) */
+    if (a->throughput_tps != b->throughput_tps) return 0;
+    if (a->has_budget != b->has_budget) return 0;
+    if (a->has_budget && a->power_budget_w != b->power_budget_w) return 0;
+    return a->epsilon == b->epsilon && a->objective == b->objective;
+}
+
+int64_t or_index_of(const pals_point* c, int64_t n, const pals_point* p) {
+    for (int64_t i = 0; i < n; ++i)
+        if (point_eq(&c[i], p)) return i;
+    return -1;
+}
+
+/* control_step controller.hpp:210-267. cur_T = score(state.current).throughput_tps,
+ * cur_ok = 0 if the scorer cannot score the current point (TableScorer throws). */
+int or_control_step_scored(const pals_point* c, int64_t n, const double* T, const double* P,
+                           double cur_T, int cur_ok, const pals_telemetry* tel, double now_s,
+                           const pals_targets* tg, const pals_coeffs* k,
+                           const pals_ctrl_state* state, const pals_ctrl_cfg* cfg,
+                           pals_decision* out_d, pals_ctrl_state* out_s) {
+    pals_ctrl_state st = *state;
+    if (now_s - tel->t_s > 1.5 * cfg->interval_s) {
+        out_d->point = st.current;
+        out_d->applied = 0;
+        out_d->reason = PALS_REASON_HOLD;
+        *out_s = st;
+        return PALS_OK;
+    }
+    double err_norm = 0.0;
+    if (tg->objective == PALS_OBJ_QOS && tg->throughput_tps > 0.0) {
+        err_norm = (tg->throughput_tps - tel->throughput_tps) / tg->throughput_tps;
+        if (!cur_ok) return PALS_ECONFIG;
+        const double promised = (double)st.current.dp * cur_T * st.bias;
+        if (promised > 0.0) {
+            const double pred_err = (promised - tel->throughput_tps) / promised;
+            st.integral = sclamp(st.integral + pred_err, -cfg->integral_clamp, cfg->integral_clamp);
+            const double deriv = st.has_prev_error ? pred_err - st.prev_error : 0.0;
+            const double corr = cfg->kp * pred_err + cfg->ki * st.integral + cfg->kd * deriv;
+            st.bias = sclamp(st.bias * (1.0 - corr), cfg->bias_min, cfg->bias_max);
+            st.prev_error = pred_err;
+            st.has_prev_error = 1;
+        }
+    }
+    const int changed = !st.has_last_targets || !targets_eq(&st.last_targets, tg);
+    st.last_targets = *tg;
+    st.has_last_targets = 1;
+    if (fabs(err_norm) > tg->epsilon)
+        ++st.sustain_count;
+    else
+        st.sustain_count = 0;
+
+    pals_query q;
+    q.throughput_tps = tg->throughput_tps;
+    q.power_budget_w = tg->power_budget_w;
+    q.has_budget = tg->has_budget;
+    q.objective = tg->objective;
+    q.bias = st.bias;
+    q.target_headroom = cfg->target_headroom;
+    q.budget_margin = cfg->budget_margin;
+    int32_t idx;
+    uint8_t reason;
+    const int rc = or_select_scored(c, n, T, P, k, &q, &idx, &reason);
+    if (rc != PALS_OK) return rc;
+
+    const int may_apply = changed || st.sustain_count >= cfg->sustain_intervals;
+    if (may_apply && !point_eq(&c[idx], &st.current)) {
+        st.current = c[idx];
+        st.sustain_count = 0;
+        out_d->point = c[idx];
+        out_d->applied = 1;
+        out_d->reason = reason;
+        *out_s = st;
+        return PALS_OK;
+    }
+    out_d->point = st.current;
+    out_d->applied = 0;
+    out_d->reason = may_apply ? reason : PALS_REASON_HOLD;
+    *out_s = st;
+    return PALS_OK;
+}
+
+/* ---- fluid replay plant (not in the reference) ----------- */
+static uint64_t draw(uint64_t key, uint64_t lane, uint64_t ctr) {
+    return or_splitmix64(key ^ (lane << 48) ^ ctr);
+}
+static double u01(uint64_t u) { return (double)(u >> 11) * 0x1.0p-53; }
+
+typedef struct {
+    uint64_t key, lane;
+    int seg_min, seg_max;
+    double lo, hi;
+    long next_j, seg_end;
+    double level;
+} segs;
+
+static double seg_value(segs* s, long k) {
+    while (k >= s->seg_end) {
+        const uint64_t span = (uint64_t)(s->seg_max - s->seg_min) + 1;
+        const long len = s->seg_min + (long)(draw(s->key, s->lane, 2 * (uint64_t)s->next_j) % span);
+        const double u = u01(draw(s->key, s->lane, 2 * (uint64_t)s->next_j + 1));
+        s->level = s->lo + (s->hi - s->lo) * u;
+        s->seg_end += len;
+        ++s->next_j;
+    }
+    return s->level;
+}
+
+/* detail::enforce_cap sim.hpp:195-205 */
+static double enforce_cap(double cap, int batch, double node_budget, const pals_point* tmpl,
+                          const pals_profile* p, const pals_gpu_spec* g, const pals_coeffs* k) {
+    if (node_budget <= 0.0 || batch < 1) return cap;
+    double c = cap;
+    while (c > g->min_cap_watts) {
+        pals_point q = *tmpl;
+        q.cap_watts = c;
+        q.batch = batch;
+        double T, P;
+        or_score(&q, p, g, &T, &P);
+        /* cluster_system_power model.hpp:99-103 */
+        const double sys = (double)q.dp * (k->alpha * 4.0 * P + k->beta_watts);
+        if (sys <= node_budget) return c;
+        c = smax(g->min_cap_watts, c - 5.0);
+    }
+    return g->min_cap_watts;
+}
+
+int or_replay(int n_models, const pals_profile* plant, const pals_gpu_spec* g,
+              const pals_coeffs* k, const double* caps, int n_caps, const int* batches,
+              int n_batches, const pals_ctrl_cfg* cfg, const pals_replay_spec* spec,
+              pals_trace_summary* summaries, pals_step_log* logs) {
+    const int nc = n_caps * n_batches;
+    pals_point* cands = (pals_point*)malloc(sizeof(pals_point) * (size_t)nc * (size_t)n_models);
+    double* T = (double*)malloc(sizeof(double) * (size_t)nc * (size_t)n_models);
+    double* P = (double*)malloc(sizeof(double) * (size_t)nc * (size_t)n_models);
+    double* tmax = (double*)malloc(sizeof(double) * (size_t)n_models);
+    double* pmin = (double*)malloc(sizeof(double) * (size_t)n_models);
+    double* pmax = (double*)malloc(sizeof(double) * (size_t)n_models);
+    double mc = caps[0];
+    int mb = batches[0];
+    for (int a = 0; a < n_caps; ++a) mc = smax(mc, caps[a]);
+    for (int b = 0; b < n_batches; ++b) mb = batches[b] > mb ? batches[b] : mb;
+    int rc = PALS_OK;
+    for (int m = 0; m < n_models; ++m) {
+        pals_point* cm = cands + (size_t)m * nc;
+        int i = 0;
+        for (int a = 0; a < n_caps; ++a)
+            for (int b = 0; b < n_batches; ++b, ++i) {
+                cm[i].cap_watts = caps[a];
+                cm[i].batch = batches[b];
+                cm[i].tp = plant[m].deploy_tp;
+                cm[i].ep = plant[m].deploy_ep;
+                cm[i].dp = plant[m].deploy_dp;
+                const int e = or_score(&cm[i], &plant[m], g, &T[(size_t)m * nc + i],
+                                       &P[(size_t)m * nc + i]);
+                if (e != PALS_OK) rc = e;
+                const double pn =
+                    (double)cm[i].dp * (k->alpha * 4.0 * P[(size_t)m * nc + i] + k->beta_watts);
+                if (i == 0 || pn < pmin[m]) pmin[m] = pn;
+                if (i == 0 || pn > pmax[m]) pmax[m] = pn;
+            }
+        pals_point top = cm[0];
+        top.cap_watts = mc;
+        top.batch = mb;
+        double tt, pp;
+        const int e = or_score(&top, &plant[m], g, &tt, &pp);
+        if (e != PALS_OK) rc = e;
+        tmax[m] = (double)top.dp * tt;
+    }
+    if (rc != PALS_OK) goto done;
+
+    for (int64_t ti = 0; ti < spec->n_traces; ++ti) {
+        const uint64_t key = or_splitmix64(spec->seed ^ (uint64_t)(spec->first_trace + ti));
+        const int m = (int)(key % (uint64_t)n_models);
+        const pals_point* cm = cands + (size_t)m * nc;
+        const double* Tm = T + (size_t)m * nc;
+        const double* Pm = P + (size_t)m * nc;
+        int obj = spec->objective_mode;
+        if (obj == 2) obj = (int)(draw(key, 0, 0) >> 63);
+        const double qfrac =
+            spec->qos_frac_lo + (spec->qos_frac_hi - spec->qos_frac_lo) * u01(draw(key, 0, 1));
+        const double target_tps = qfrac * tmax[m];
+        segs bs = {key, 1, spec->seg_min, spec->seg_max, spec->budget_lo_frac * pmin[m],
+                   spec->budget_hi_frac * pmax[m], 0, 0, 0.0};
+        segs ls = {key, 2, spec->seg_min, spec->seg_max, spec->load_lo * tmax[m],
+                   spec->load_hi * tmax[m], 0, 0, 0.0};
+        pals_ctrl_state st;
+        memset(&st, 0, sizeof st);
+        st.bias = 1.0;
+        st.current = cm[0];
+        st.current.cap_watts = mc;
+        st.current.batch = mb;
+        double applied_cap = mc, inflight_cap = mc;
+        int batch_cap = mb;
+        uint64_t h = 0xcbf29ce484222325ULL;
+        double energy = 0.0, tokens = 0.0;
+        int n_applied = 0;
+        pals_step_log* lg = (logs && ti < spec->n_log_traces) ? logs + ti * spec->n_steps : NULL;
+        for (int s = 0; s < spec->n_steps; ++s) {
+            const double t0 = (double)s * spec->interval_s;
+            const double t1 = t0 + spec->interval_s;
+            const double node_budget = spec->budget_mode ? seg_value(&bs, s) : 0.0;
+            const int b_eff = batch_cap;
+            const double cap =
+                enforce_cap(applied_cap, b_eff, node_budget, &cm[0], &plant[m], g, k);
+            pals_point p = cm[0];
+            p.cap_watts = cap;
+            p.batch = b_eff;
+            double Tc, Pc;
+            or_score(&p, &plant[m], g, &Tc, &Pc);
+            const double capacity = (double)p.dp * Tc;
+            const double sys_w = (double)p.dp * (k->alpha * 4.0 * Pc + k->beta_watts);
+            const double offered = seg_value(&ls, s);
+            const double noise = 1.0 + spec->noise_amp * (2.0 * u01(draw(key, 3, (uint64_t)s)) - 1.0);
+            const double measured = smin(offered, capacity) * noise;
+            energy += sys_w * spec->interval_s;
+            tokens += measured * spec->interval_s;
+
+            pals_targets tg;
+            memset(&tg, 0, sizeof tg);
+            tg.throughput_tps = target_tps;
+            tg.epsilon = spec->epsilon;
+            tg.objective = obj;
+            tg.has_budget = node_budget > 0.0;
+            tg.power_budget_w = tg.has_budget ? node_budget : 0.0;
+            pals_telemetry tel = {t1, measured};
+            const int64_t ci = or_index_of(cm, nc, &st.current);
+            pals_decision d;
+            pals_ctrl_state st2;
+            rc = or_control_step_scored(cm, nc, Tm, Pm, ci >= 0 ? Tm[ci] : 0.0, ci >= 0, &tel, t1,
+                                        &tg, k, &st, cfg, &d, &st2);
+            if (rc != PALS_OK) goto done;
+            st = st2;
+            const int64_t idx = or_index_of(cm, nc, &d.point);
+            const uint64_t word = ((uint64_t)(uint32_t)idx << 8) | ((uint64_t)(d.applied ? 1 : 0) << 4) |
+                                  (uint64_t)d.reason;
+            h = (h ^ word) * 0x100000001b3ULL;
+            if (d.applied) ++n_applied;
+            if (lg) {
+                lg[s].idx = (int32_t)idx;
+                lg[s].applied = (uint8_t)(d.applied ? 1 : 0);
+                lg[s].reason = (uint8_t)d.reason;
+                lg[s].cap_tenths = (uint16_t)llround(cap * 10.0);
+            }
+            applied_cap = inflight_cap;
+            if (d.applied) {
+                batch_cap = d.point.batch;
+                inflight_cap = d.point.cap_watts;
+            }
+        }
+        uint64_t bias_bits;
+        memcpy(&bias_bits, &st.bias, 8);
+        const int64_t fi = or_index_of(cm, nc, &st.current);
+        h = (h ^ bias_bits) * 0x100000001b3ULL;
+        h = (h ^ (uint64_t)(uint32_t)fi) * 0x100000001b3ULL;
+        pals_trace_summary* sm = &summaries[ti];
+        sm->digest = h;
+        sm->final_bias = st.bias;
+        sm->energy_j = energy;
+        sm->tokens = tokens;
+        sm->n_applied = n_applied;
+        sm->final_idx = (int32_t)fi;
+        sm->model = m;
+        sm->objective = obj;
+    }
+done:
+    free(cands);
+    free(T);
+    free(P);
+    free(tmax);
+    free(pmin);
+    free(pmax);
+    return rc;
+}

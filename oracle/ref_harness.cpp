@@ -1,0 +1,641 @@
+// ref_harness.cpp — TEST INFRASTRUCTURE ONLY (the checker, never the product).
+//
+// A thin extern "C" shim over the UNMODIFIED reference headers
+// (/root/reference/proj/include/wattserve/*.hpp), built by oracle/Makefile into
+// oracle/_ref/libwsref.so. It lets the Python tests and bench.py's CPU arm
+// call the reference's own select_config / control_step / throughput /
+// avg_gpu_power / PredictorBundle::predict on exactly the inputs the GPU path
+// sees. Nothing here re-implements reference logic except the replay plant,
+// which the reference does not have: it drives the reference's
+// control_step with the reference's own model functions.
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "wattserve/controller.hpp"
+#include "wattserve/forest.hpp"
+#include "wattserve/model.hpp"
+#include "wattserve/rng.hpp"
+#include "wattserve/sim.hpp"
+#include "wattserve/sweep.hpp"
+
+#include "pals_gpu.h"
+
+using namespace wattserve;
+
+namespace {
+
+thread_local std::string g_err;
+
+ModelProfile to_profile(const pals_profile& p) {
+    ModelProfile m;
+    m.name = p.name;
+    m.total_params_b = p.total_params_b;
+    m.active_params_b = p.active_params_b;
+    m.num_experts = p.num_experts;
+    m.top_k = p.top_k;
+    m.compute_fixed = p.compute_fixed;
+    m.compute_per_seq = p.compute_per_seq;
+    for (int i = 0; i < p.n_tp; ++i) m.comm_fixed_by_tp[p.tp_keys[i]] = p.comm_fixed[i];
+    m.comm_per_seq = p.comm_per_seq;
+    m.internode_factor = p.internode_factor;
+    m.knee_watts = p.knee_watts;
+    m.compute_power_base = p.compute_power_base;
+    m.compute_power_per_seq = p.compute_power_per_seq;
+    m.comm_power = p.comm_power;
+    m.overlap = p.overlap;
+    m.deployment = Deployment{p.deploy_tp, p.deploy_ep, p.deploy_dp};
+    return m;
+}
+
+GpuSpec to_gpu(const pals_gpu_spec& g) {
+    return GpuSpec{g.idle_watts, g.min_cap_watts, g.max_cap_watts, g.max_frequency};
+}
+
+OperatingPoint to_point(const pals_point& p) {
+    return OperatingPoint{p.cap_watts, p.batch, p.tp, p.ep, p.dp};
+}
+
+pals_point from_point(const OperatingPoint& p) {
+    pals_point o;
+    o.cap_watts = p.cap_watts;
+    o.batch = p.batch;
+    o.tp = p.tp;
+    o.ep = p.ep;
+    o.dp = p.dp;
+    return o;
+}
+
+Targets to_targets(const pals_targets& t) {
+    Targets o;
+    o.throughput_tps = t.throughput_tps;
+    if (t.has_budget) o.power_budget_w = t.power_budget_w;
+    o.epsilon = t.epsilon;
+    o.objective = t.objective == PALS_OBJ_BUDGET ? Objective::BudgetMaxThroughput
+                                                 : Objective::QosMaxEfficiency;
+    return o;
+}
+
+pals_targets from_targets(const Targets& t) {
+    pals_targets o{};
+    o.throughput_tps = t.throughput_tps;
+    o.has_budget = t.power_budget_w.has_value() ? 1 : 0;
+    o.power_budget_w = t.power_budget_w.value_or(0.0);
+    o.epsilon = t.epsilon;
+    o.objective = t.objective == Objective::BudgetMaxThroughput ? PALS_OBJ_BUDGET : PALS_OBJ_QOS;
+    return o;
+}
+
+ControllerConfig to_cfg(const pals_ctrl_cfg& c) {
+    ControllerConfig o;
+    o.gains = PidGains{c.kp, c.ki, c.kd};
+    o.sustain_intervals = c.sustain_intervals;
+    o.integral_clamp = c.integral_clamp;
+    o.bias_min = c.bias_min;
+    o.bias_max = c.bias_max;
+    o.interval_s = c.interval_s;
+    o.target_headroom = c.target_headroom;
+    o.budget_margin = c.budget_margin;
+    return o;
+}
+
+ControllerState to_state(const pals_ctrl_state& s) {
+    ControllerState o;
+    o.bias = s.bias;
+    o.integral = s.integral;
+    o.prev_error = s.prev_error;
+    o.has_prev_error = s.has_prev_error != 0;
+    o.sustain_count = s.sustain_count;
+    o.current = to_point(s.current);
+    if (s.has_last_targets) o.last_targets = to_targets(s.last_targets);
+    return o;
+}
+
+pals_ctrl_state from_state(const ControllerState& s) {
+    pals_ctrl_state o{};
+    o.bias = s.bias;
+    o.integral = s.integral;
+    o.prev_error = s.prev_error;
+    o.has_prev_error = s.has_prev_error ? 1 : 0;
+    o.sustain_count = s.sustain_count;
+    o.current = from_point(s.current);
+    o.has_last_targets = s.last_targets.has_value() ? 1 : 0;
+    if (s.last_targets) o.last_targets = from_targets(*s.last_targets);
+    return o;
+}
+
+// TableScorer semantics (tests/test_controller.cpp:17-29): first point equal by value.
+Scorer table_scorer(const std::vector<OperatingPoint>& pts, const double* t, const double* p) {
+    return [&pts, t, p](const OperatingPoint& q) {
+        for (std::size_t i = 0; i < pts.size(); ++i)
+            if (pts[i] == q) return CandidateScore{t[i], p[i]};
+        throw config_error("unscored candidate");
+    };
+}
+
+int map_exception() {
+    try {
+        throw;
+    } catch (const config_error& e) {
+        g_err = e.what();
+        return PALS_ECONFIG;
+    } catch (const data_error& e) {
+        g_err = e.what();
+        return PALS_EDATA;
+    } catch (const std::out_of_range& e) {
+        g_err = e.what();
+        return PALS_ERANGE;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return PALS_ERUNTIME;
+    }
+}
+
+int reason_code(DecisionReason r) { return static_cast<int>(r); }
+
+Targets query_targets(const pals_query& q) {
+    Targets t;
+    t.throughput_tps = q.throughput_tps;
+    if (q.has_budget) t.power_budget_w = q.power_budget_w;
+    t.objective = q.objective == PALS_OBJ_BUDGET ? Objective::BudgetMaxThroughput
+                                                 : Objective::QosMaxEfficiency;
+    return t;
+}
+
+int index_of(const std::vector<OperatingPoint>& pts, const OperatingPoint& p) {
+    for (std::size_t i = 0; i < pts.size(); ++i)
+        if (pts[i] == p) return static_cast<int>(i);
+    return -1;
+}
+
+// ---- fluid replay plant; NOT in the reference -------------
+constexpr std::uint64_t kFnvOffset = 0xcbf29ce484222325ULL;
+constexpr std::uint64_t kFnvPrime = 0x100000001b3ULL;
+
+inline std::uint64_t draw(std::uint64_t key, std::uint64_t lane, std::uint64_t ctr) {
+    return splitmix64(key ^ (lane << 48) ^ ctr);
+}
+inline double u01(std::uint64_t u) { return static_cast<double>(u >> 11) * 0x1.0p-53; }
+
+struct Segments {
+    std::uint64_t key, lane;
+    int seg_min, seg_max;
+    double lo, hi;
+    long next_j = 0;
+    long seg_end = 0;
+    double level = 0.0;
+    double value_at(long k) {
+        while (k >= seg_end) {
+            const std::uint64_t span = static_cast<std::uint64_t>(seg_max - seg_min) + 1;
+            const long len = seg_min + static_cast<long>(draw(key, lane, 2 * next_j) % span);
+            const double u = u01(draw(key, lane, 2 * next_j + 1));
+            level = lo + (hi - lo) * u;
+            seg_end += len;
+            ++next_j;
+        }
+        return level;
+    }
+};
+
+struct ReplayModel {
+    ModelProfile profile;
+    std::vector<OperatingPoint> cands;
+    Scorer scorer;
+    double t_max = 0.0, p_min = 0.0, p_max = 0.0;
+};
+
+void replay_one(const std::vector<ReplayModel>& models, const GpuSpec& gpu,
+                const SystemPowerCoeffs& coeffs, const ControllerConfig& cfg,
+                const pals_replay_spec& spec, std::int64_t gi, pals_trace_summary* summary,
+                pals_step_log* log) {
+    const std::uint64_t key = splitmix64(spec.seed ^ static_cast<std::uint64_t>(gi));
+    const int m = static_cast<int>(key % models.size());
+    const ReplayModel& rm = models[m];
+    int obj = spec.objective_mode;
+    if (obj == 2) obj = static_cast<int>(draw(key, 0, 0) >> 63);
+    const double qfrac =
+        spec.qos_frac_lo + (spec.qos_frac_hi - spec.qos_frac_lo) * u01(draw(key, 0, 1));
+    const double target_tps = qfrac * rm.t_max;
+    Segments bseg{key, 1, spec.seg_min, spec.seg_max, spec.budget_lo_frac * rm.p_min,
+                  spec.budget_hi_frac * rm.p_max};
+    Segments lseg{key, 2, spec.seg_min, spec.seg_max, spec.load_lo * rm.t_max,
+                  spec.load_hi * rm.t_max};
+
+    const OperatingPoint& first = rm.cands.front();
+    double max_cap = first.cap_watts;
+    int max_batch = first.batch;
+    for (const auto& c : rm.cands) {
+        max_cap = std::max(max_cap, c.cap_watts);
+        max_batch = std::max(max_batch, c.batch);
+    }
+    const int tp = first.tp, ep = first.ep, dp = first.dp;
+
+    detail::NodeRuntime n;  // only the fields enforce_cap reads
+    n.profile = &rm.profile;
+    n.cfg.tp = tp;
+    n.cfg.ep = ep;
+    n.cfg.dp = dp;
+
+    ControllerState st;
+    st.current = OperatingPoint{max_cap, max_batch, tp, ep, dp};
+    double applied_cap = max_cap, inflight_cap = max_cap;
+    int batch_cap = max_batch;
+    std::uint64_t h = kFnvOffset;
+    double energy = 0.0, tokens = 0.0;
+    int n_applied = 0;
+
+    for (int k = 0; k < spec.n_steps; ++k) {
+        const double t0 = k * spec.interval_s;
+        const double t1 = t0 + spec.interval_s;
+        n.node_budget = spec.budget_mode ? bseg.value_at(k) : 0.0;
+        const int b_eff = batch_cap;
+        const double cap = detail::enforce_cap(applied_cap, b_eff, n, gpu, coeffs);
+        const OperatingPoint p{cap, b_eff, tp, ep, dp};
+        const double capacity = cluster_throughput(p, rm.profile, gpu);
+        const double gpu_w = avg_gpu_power(p, rm.profile, gpu);
+        const double sys_w = dp * (coeffs.alpha * kGpusPerNode * gpu_w + coeffs.beta_watts);
+        const double offered = lseg.value_at(k);
+        const double noise = 1.0 + spec.noise_amp * (2.0 * u01(draw(key, 3, k)) - 1.0);
+        const double measured = std::min(offered, capacity) * noise;
+        energy += sys_w * spec.interval_s;
+        tokens += measured * spec.interval_s;
+
+        Targets targets;
+        targets.throughput_tps = target_tps;
+        targets.epsilon = spec.epsilon;
+        targets.objective =
+            obj == PALS_OBJ_BUDGET ? Objective::BudgetMaxThroughput : Objective::QosMaxEfficiency;
+        if (n.node_budget > 0.0) targets.power_budget_w = n.node_budget;
+
+        auto [d, st2] = control_step(TelemetryInput{t1, measured}, t1, targets, rm.cands,
+                                     rm.scorer, coeffs, st, cfg);
+        st = st2;
+        const int idx = index_of(rm.cands, d.point);
+        const std::uint64_t word = (static_cast<std::uint64_t>(static_cast<std::uint32_t>(idx)) << 8) |
+                                   (static_cast<std::uint64_t>(d.applied ? 1 : 0) << 4) |
+                                   static_cast<std::uint64_t>(reason_code(d.reason));
+        h = (h ^ word) * kFnvPrime;
+        if (d.applied) ++n_applied;
+        if (log) {
+            log[k].idx = idx;
+            log[k].applied = d.applied ? 1 : 0;
+            log[k].reason = static_cast<std::uint8_t>(reason_code(d.reason));
+            log[k].cap_tenths = static_cast<std::uint16_t>(std::llround(cap * 10.0));
+        }
+        applied_cap = inflight_cap;
+        if (d.applied) {
+            batch_cap = d.point.batch;
+            inflight_cap = d.point.cap_watts;
+        }
+    }
+    std::uint64_t bias_bits;
+    std::memcpy(&bias_bits, &st.bias, 8);
+    const int final_idx = index_of(rm.cands, st.current);
+    h = (h ^ bias_bits) * kFnvPrime;
+    h = (h ^ static_cast<std::uint64_t>(static_cast<std::uint32_t>(final_idx))) * kFnvPrime;
+    summary->digest = h;
+    summary->final_bias = st.bias;
+    summary->energy_j = energy;
+    summary->tokens = tokens;
+    summary->n_applied = n_applied;
+    summary->final_idx = final_idx;
+    summary->model = m;
+    summary->objective = obj;
+}
+
+std::vector<ReplayModel> build_replay_models(int n_models, const pals_profile* plant,
+                                             const GpuSpec& gpu, const SystemPowerCoeffs& coeffs,
+                                             const double* caps, int n_caps,
+                                             const int* batches, int n_batches, bool memo) {
+    std::vector<ReplayModel> models(n_models);
+    for (int i = 0; i < n_models; ++i) {
+        auto& rm = models[i];
+        rm.profile = to_profile(plant[i]);
+        const int tp = plant[i].deploy_tp, ep = plant[i].deploy_ep, dp = plant[i].deploy_dp;
+        // build_candidates order (sim.hpp:304-306)
+        for (int a = 0; a < n_caps; ++a)
+            for (int b = 0; b < n_batches; ++b)
+                rm.cands.push_back(OperatingPoint{caps[a], batches[b], tp, ep, dp});
+        Scorer s = analytic_scorer(rm.profile, gpu);
+        rm.scorer = memo ? detail::cached(s) : s;
+        // unconstrained_throughput (sim.hpp:258-264)
+        const double mc = *std::max_element(caps, caps + n_caps);
+        const int mb = *std::max_element(batches, batches + n_batches);
+        rm.t_max = dp * throughput(OperatingPoint{mc, mb, tp, ep, dp}, rm.profile, gpu);
+        bool firstp = true;
+        for (const auto& c : rm.cands) {
+            const double pn = cluster_system_power(c, rm.profile, gpu, coeffs);
+            if (firstp || pn < rm.p_min) rm.p_min = pn;
+            if (firstp || pn > rm.p_max) rm.p_max = pn;
+            firstp = false;
+        }
+    }
+    return models;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+// throughput() and avg_gpu_power() per point (model.hpp:72-84); err[i] = PALS code
+int ref_eval(const pals_profile* prof, const pals_gpu_spec* gpu, const pals_point* pts,
+             std::int64_t n, double* T, double* P, int* err) {
+    const ModelProfile mp = to_profile(*prof);
+    const GpuSpec g = to_gpu(*gpu);
+    int rc = PALS_OK;
+    for (std::int64_t i = 0; i < n; ++i) {
+        try {
+            const OperatingPoint p = to_point(pts[i]);
+            T[i] = throughput(p, mp, g);
+            P[i] = avg_gpu_power(p, mp, g);
+            err[i] = PALS_OK;
+        } catch (...) {
+            err[i] = map_exception();
+            T[i] = P[i] = std::nan("");
+            rc = err[i];
+        }
+    }
+    return rc;
+}
+
+double ref_effective_frequency(double cap, const pals_profile* prof, const pals_gpu_spec* gpu,
+                               int* err) {
+    try {
+        *err = PALS_OK;
+        return effective_frequency(cap, to_gpu(*gpu), to_profile(*prof));
+    } catch (...) {
+        *err = map_exception();
+        return std::nan("");
+    }
+}
+
+// ModelProfile::validate (types.hpp:88-106) + GpuSpec::validate
+int ref_validate(const pals_profile* prof, const pals_gpu_spec* gpu) {
+    try {
+        const GpuSpec g = to_gpu(*gpu);
+        g.validate();
+        to_profile(*prof).validate(g);
+        return PALS_OK;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// select_config with analytic_scorer (controller.hpp:107-111, 132-201)
+int ref_select_analytic(const pals_profile* prof, const pals_gpu_spec* gpu,
+                        const pals_point* pts, std::int64_t n, const pals_coeffs* coeffs,
+                        const pals_query* q, std::int64_t nq, std::int32_t* idx,
+                        std::uint8_t* reason) {
+    const ModelProfile mp = to_profile(*prof);
+    const GpuSpec g = to_gpu(*gpu);
+    std::vector<OperatingPoint> cands;
+    for (std::int64_t i = 0; i < n; ++i) cands.push_back(to_point(pts[i]));
+    const Scorer s = analytic_scorer(mp, g);
+    const SystemPowerCoeffs k{coeffs->alpha, coeffs->beta_watts};
+    try {
+        for (std::int64_t j = 0; j < nq; ++j) {
+            const auto d = select_config(cands, query_targets(q[j]), s, k, q[j].bias,
+                                         q[j].target_headroom, q[j].budget_margin);
+            idx[j] = index_of(cands, d.point);
+            reason[j] = static_cast<std::uint8_t>(reason_code(d.reason));
+        }
+    } catch (...) {
+        return map_exception();
+    }
+    return PALS_OK;
+}
+
+// select_config with a TableScorer (tests/test_controller.cpp:17-29)
+int ref_select_table(const pals_point* pts, std::int64_t n, const double* T, const double* P,
+                     const pals_coeffs* coeffs, const pals_query* q, std::int64_t nq,
+                     std::int32_t* idx, std::uint8_t* reason) {
+    std::vector<OperatingPoint> cands;
+    for (std::int64_t i = 0; i < n; ++i) cands.push_back(to_point(pts[i]));
+    const Scorer s = table_scorer(cands, T, P);
+    const SystemPowerCoeffs k{coeffs->alpha, coeffs->beta_watts};
+    try {
+        for (std::int64_t j = 0; j < nq; ++j) {
+            const auto d = select_config(cands, query_targets(q[j]), s, k, q[j].bias,
+                                         q[j].target_headroom, q[j].budget_margin);
+            idx[j] = index_of(cands, d.point);
+            reason[j] = static_cast<std::uint8_t>(reason_code(d.reason));
+        }
+    } catch (...) {
+        return map_exception();
+    }
+    return PALS_OK;
+}
+
+// control_step with a TableScorer (controller.hpp:210-267)
+int ref_control_step_table(const pals_point* pts, std::int64_t n, const double* T,
+                           const double* P, const pals_telemetry* tel, double now_s,
+                           const pals_targets* targets, const pals_coeffs* coeffs,
+                           const pals_ctrl_state* state, const pals_ctrl_cfg* cfg,
+                           pals_decision* out_d, pals_ctrl_state* out_s) {
+    std::vector<OperatingPoint> cands;
+    for (std::int64_t i = 0; i < n; ++i) cands.push_back(to_point(pts[i]));
+    const Scorer s = table_scorer(cands, T, P);
+    try {
+        auto [d, st] = control_step(TelemetryInput{tel->t_s, tel->throughput_tps}, now_s,
+                                    to_targets(*targets), cands, s,
+                                    SystemPowerCoeffs{coeffs->alpha, coeffs->beta_watts},
+                                    to_state(*state), to_cfg(*cfg));
+        out_d->point = from_point(d.point);
+        out_d->applied = d.applied ? 1 : 0;
+        out_d->reason = reason_code(d.reason);
+        *out_s = from_state(st);
+    } catch (...) {
+        return map_exception();
+    }
+    return PALS_OK;
+}
+
+// control_step with analytic_scorer
+int ref_control_step_analytic(const pals_profile* prof, const pals_gpu_spec* gpu,
+                              const pals_point* pts, std::int64_t n, const pals_telemetry* tel,
+                              double now_s, const pals_targets* targets,
+                              const pals_coeffs* coeffs, const pals_ctrl_state* state,
+                              const pals_ctrl_cfg* cfg, pals_decision* out_d,
+                              pals_ctrl_state* out_s) {
+    const ModelProfile mp = to_profile(*prof);
+    const GpuSpec g = to_gpu(*gpu);
+    std::vector<OperatingPoint> cands;
+    for (std::int64_t i = 0; i < n; ++i) cands.push_back(to_point(pts[i]));
+    const Scorer s = analytic_scorer(mp, g);
+    try {
+        auto [d, st] = control_step(TelemetryInput{tel->t_s, tel->throughput_tps}, now_s,
+                                    to_targets(*targets), cands, s,
+                                    SystemPowerCoeffs{coeffs->alpha, coeffs->beta_watts},
+                                    to_state(*state), to_cfg(*cfg));
+        out_d->point = from_point(d.point);
+        out_d->applied = d.applied ? 1 : 0;
+        out_d->reason = reason_code(d.reason);
+        *out_s = from_state(st);
+    } catch (...) {
+        return map_exception();
+    }
+    return PALS_OK;
+}
+
+// Reference control_step driven by the fluid plant, traces [0, n) of spec.
+int ref_replay(int n_models, const pals_profile* plant, const pals_gpu_spec* gpu,
+               const pals_coeffs* coeffs, const double* caps, int n_caps, const int* batches,
+               int n_batches, const pals_ctrl_cfg* cfg, const pals_replay_spec* spec,
+               pals_trace_summary* summaries, pals_step_log* logs) {
+    try {
+        const GpuSpec g = to_gpu(*gpu);
+        const SystemPowerCoeffs k{coeffs->alpha, coeffs->beta_watts};
+        const auto models =
+            build_replay_models(n_models, plant, g, k, caps, n_caps, batches, n_batches, true);
+        const ControllerConfig c = to_cfg(*cfg);
+        for (std::int64_t i = 0; i < spec->n_traces; ++i) {
+            pals_step_log* lg =
+                (logs && i < spec->n_log_traces) ? logs + i * spec->n_steps : nullptr;
+            replay_one(models, g, k, c, *spec, spec->first_trace + i, &summaries[i], lg);
+        }
+    } catch (...) {
+        return map_exception();
+    }
+    return PALS_OK;
+}
+
+// ---- CPU baseline timing (all host threads) ------------------------------
+// select_config + analytic_scorer over queries split across threads.
+// Returns wall seconds; idx/reason receive the results.
+double ref_bench_select(const pals_profile* prof, const pals_gpu_spec* gpu,
+                        const pals_point* pts, std::int64_t n, const pals_coeffs* coeffs,
+                        const pals_query* q, std::int64_t nq, int n_threads, std::int32_t* idx,
+                        std::uint8_t* reason) {
+    const ModelProfile mp = to_profile(*prof);
+    const GpuSpec g = to_gpu(*gpu);
+    std::vector<OperatingPoint> cands;
+    for (std::int64_t i = 0; i < n; ++i) cands.push_back(to_point(pts[i]));
+    const SystemPowerCoeffs k{coeffs->alpha, coeffs->beta_watts};
+    std::atomic<int> failed{0};
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> th;
+    for (int t = 0; t < n_threads; ++t) {
+        th.emplace_back([&, t] {
+            const Scorer s = analytic_scorer(mp, g);
+            const std::int64_t lo = nq * t / n_threads, hi = nq * (t + 1) / n_threads;
+            try {
+                for (std::int64_t j = lo; j < hi; ++j) {
+                    const auto d = select_config(cands, query_targets(q[j]), s, k, q[j].bias,
+                                                 q[j].target_headroom, q[j].budget_margin);
+                    // the reference returns the point by value; its index is a cheap scan
+                    // only when the caller asks for it
+                    if (idx) {
+                        idx[j] = index_of(cands, d.point);
+                        reason[j] = static_cast<std::uint8_t>(reason_code(d.reason));
+                    }
+                }
+            } catch (...) {
+                failed = 1;
+            }
+        });
+    }
+    for (auto& x : th) x.join();
+    const auto t1 = std::chrono::steady_clock::now();
+    if (failed) return -1.0;
+    return std::chrono::duration<double>(t1 - t0).count();
+}
+
+// Fluid-plant replay through the reference control_step, traces split across threads.
+double ref_bench_replay(int n_models, const pals_profile* plant, const pals_gpu_spec* gpu,
+                        const pals_coeffs* coeffs, const double* caps, int n_caps,
+                        const int* batches, int n_batches, const pals_ctrl_cfg* cfg,
+                        const pals_replay_spec* spec, int n_threads,
+                        pals_trace_summary* summaries) {
+    const GpuSpec g = to_gpu(*gpu);
+    const SystemPowerCoeffs k{coeffs->alpha, coeffs->beta_watts};
+    const ControllerConfig c = to_cfg(*cfg);
+    std::atomic<int> failed{0};
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> th;
+    for (int t = 0; t < n_threads; ++t) {
+        th.emplace_back([&, t] {
+            try {
+                // per-thread memo: detail::cached is not thread-safe (sim.hpp:179-190)
+                const auto models = build_replay_models(n_models, plant, g, k, caps, n_caps,
+                                                        batches, n_batches, true);
+                const std::int64_t lo = spec->n_traces * t / n_threads;
+                const std::int64_t hi = spec->n_traces * (t + 1) / n_threads;
+                for (std::int64_t i = lo; i < hi; ++i)
+                    replay_one(models, g, k, c, *spec, spec->first_trace + i, &summaries[i],
+                               nullptr);
+            } catch (...) {
+                failed = 1;
+            }
+        });
+    }
+    for (auto& x : th) x.join();
+    const auto t1 = std::chrono::steady_clock::now();
+    if (failed) return -1.0;
+    return std::chrono::duration<double>(t1 - t0).count();
+}
+
+std::uint64_t ref_splitmix64(std::uint64_t x) { return splitmix64(x); }
+
+}  // extern "C"
+
+extern "C" {
+
+// profile_from_json (json_io.hpp:70-95) + validate, flattened to pals_profile
+int ref_load_profile(const char* path, pals_profile* out) {
+    try {
+        const ModelProfile p = profile_from_json(parse_json_file(path));
+        std::memset(out, 0, sizeof *out);
+        std::strncpy(out->name, p.name.c_str(), sizeof(out->name) - 1);
+        out->compute_fixed = p.compute_fixed;
+        out->compute_per_seq = p.compute_per_seq;
+        out->comm_per_seq = p.comm_per_seq;
+        out->internode_factor = p.internode_factor;
+        out->knee_watts = p.knee_watts;
+        out->compute_power_base = p.compute_power_base;
+        out->compute_power_per_seq = p.compute_power_per_seq;
+        out->comm_power = p.comm_power;
+        out->overlap = p.overlap;
+        out->total_params_b = p.total_params_b;
+        out->active_params_b = p.active_params_b;
+        int i = 0;
+        for (const auto& [tp, v] : p.comm_fixed_by_tp) {
+            if (i >= PALS_MAX_TP_KEYS) throw config_error("too many tp keys");
+            out->tp_keys[i] = tp;
+            out->comm_fixed[i] = v;
+            ++i;
+        }
+        out->n_tp = i;
+        out->num_experts = p.num_experts;
+        out->top_k = p.top_k;
+        out->deploy_tp = p.deployment.tp;
+        out->deploy_ep = p.deployment.ep;
+        out->deploy_dp = p.deployment.dp;
+    } catch (...) {
+        return map_exception();
+    }
+    return PALS_OK;
+}
+
+// platform_from_json (json_io.hpp:103-105)
+int ref_load_platform(const char* path, pals_gpu_spec* gpu, pals_coeffs* coeffs) {
+    try {
+        const Platform p = platform_from_json(parse_json_file(path));
+        gpu->idle_watts = p.gpu.idle_watts;
+        gpu->min_cap_watts = p.gpu.min_cap_watts;
+        gpu->max_cap_watts = p.gpu.max_cap_watts;
+        gpu->max_frequency = p.gpu.max_frequency;
+        coeffs->alpha = p.coeffs.alpha;
+        coeffs->beta_watts = p.coeffs.beta_watts;
+    } catch (...) {
+        return map_exception();
+    }
+    return PALS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,227 @@
+// pals_internal.cuh — shared device/host definitions for libpals_gpu.so.
+//
+// All FP64 arithmetic follows the reference's operation order literally and is
+// compiled with -fmad=false (device) / -ffp-contract=off (host), so every
+// double is bit-identical to the reference's Release build (SURVEY F3,
+// Appendix A). Citations: /root/reference/proj/include/wattserve/<file>:<line>.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/pals_gpu.h"
+
+#define PALS_HD __host__ __device__ __forceinline__
+
+namespace pals {
+
+constexpr int kGpusPerNode = 4;          // types.hpp:11
+constexpr double kFloorRatio = 0.4;      // model.hpp:33
+constexpr double kTieTol = 1e-9;         // controller.hpp:121-122
+constexpr int kMaxDp = 256;              // pow(internode, dp-1) host table size
+constexpr uint32_t kNone32 = 0xFFFFFFFFu;
+constexpr uint64_t kNone64 = ~0ull;
+
+// ---- libstdc++ comparison helpers (stl_algobase.h:257-265, stl_algo.h:3667-3671)
+PALS_HD double smax(double a, double b) { return a < b ? b : a; }
+PALS_HD double smin(double a, double b) { return b < a ? b : a; }
+PALS_HD double sclamp(double v, double lo, double hi) { return smin(smax(v, lo), hi); }
+
+// rng.hpp:15-20
+PALS_HD uint64_t splitmix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+
+// Analytic model parameters (ModelProfile + GpuSpec), flattened for the device.
+struct Analytic {
+    double compute_fixed, compute_per_seq, comm_per_seq, knee_watts;
+    double compute_power_base, compute_power_per_seq, comm_power, overlap;
+    double min_cap, max_cap, max_frequency;
+    int n_tp;
+    int tp_keys[PALS_MAX_TP_KEYS];
+    double comm_fixed[PALS_MAX_TP_KEYS];
+    double pow_dp[kMaxDp + 1];  // pow_dp[d] = std::pow(internode_factor, d - 1), host glibc
+};
+
+// Scores of one point: CandidateScore{throughput_tps, gpu_power_w} (controller.hpp:93-96)
+struct Score {
+    double T, P;
+};
+
+// step_timing + throughput + avg_gpu_power (model.hpp:37-84) for a point that
+// already passed validation. Returns T, P and the per-step terms.
+PALS_HD Score analytic_score(const Analytic& a, double cap, int batch, int tp, int dp,
+                             double* t_comp_out = nullptr) {
+    // effective_frequency model.hpp:41-44
+    const double span = a.knee_watts - a.min_cap;
+    double f;
+    if (span <= 0.0) {
+        f = a.max_frequency;
+    } else {
+        const double ratio = (cap - a.min_cap) / span;
+        f = a.max_frequency * sclamp(ratio, kFloorRatio, 1.0);
+    }
+    double comm = 0.0;
+    for (int i = 0; i < a.n_tp; ++i)
+        if (a.tp_keys[i] == tp) comm = a.comm_fixed[i];
+    const double B = (double)batch;
+    const double t_comp = (a.compute_fixed + a.compute_per_seq * B / (double)tp) / f;
+    const double t_comm = (comm + a.comm_per_seq * B) * a.pow_dp[dp];
+    const double hi = smax(t_comp, t_comm);
+    const double lo = smin(t_comp, t_comm);
+    const double step = hi + (1.0 - a.overlap) * lo;
+    Score s;
+    s.T = B / step;
+    const double demand = a.compute_power_base + a.compute_power_per_seq * B / (double)tp;
+    const double p_comp = smin(cap, demand);
+    const double comm_share = step - t_comp;
+    s.P = (t_comp * p_comp + comm_share * a.comm_power) / step;
+    if (t_comp_out) *t_comp_out = t_comp;
+    return s;
+}
+
+// select_config's per-candidate host power and instance throughput (controller.hpp:147-150)
+PALS_HD double p_node_of(double P, int dp, double alpha, double beta) {
+    return (double)dp * (alpha * (double)kGpusPerNode * P + beta);
+}
+
+// detail::better_candidate controller.hpp:118-125, literally
+PALS_HD bool better_exact(double sa, double capa, int ba, double sb, double capb, int bb) {
+    const double scale = smax(smax(fabs(sa), fabs(sb)), 1e-300);
+    if ((sa - sb) / scale > kTieTol) return true;
+    if ((sb - sa) / scale > kTieTol) return false;
+    if (capa != capb) return capa < capb;
+    return ba < bb;
+}
+
+// Order-preserving map double -> uint64 (ascending); -0 is folded to +0.
+PALS_HD uint64_t orderable(double x) {
+    if (x == 0.0) x = 0.0;
+    uint64_t b;
+#ifdef __CUDA_ARCH__
+    b = (uint64_t)__double_as_longlong(x);
+#else
+    __builtin_memcpy(&b, &x, 8);
+#endif
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+PALS_HD double unorderable(uint64_t k) {
+    const uint64_t b = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+    double x;
+#ifdef __CUDA_ARCH__
+    x = __longlong_as_double((long long)b);
+#else
+    __builtin_memcpy(&x, &b, 8);
+#endif
+    return x;
+}
+
+// ---- plan device layout ---------------------------------------------------
+// Three orders: 0 = t_hat descending, 1 = p_node ascending, 2 = eff descending.
+// Each order has a dense rank D (index into its sorted distinct values U) and
+// a packed key (D << kTrBits) | TR, TR = the grid's (cap, batch, index) rank,
+// so min(key) is the reference's argmax with its knob tie-break (Appendix A).
+enum { ORD_T = 0, ORD_P = 1, ORD_E = 2, N_ORD = 3 };
+
+struct PlanDev {
+    int64_t n;           // grid points
+    int tr_bits;         // key = (D << tr_bits) | TR
+    int wide;            // 1: 64-bit keys (n > 65535)
+    // grid
+    const double* cap;
+    const int* batch;
+    const int* dp;
+    const int* inv_tr;   // TR -> point index
+    // scores
+    double* T;
+    double* P;
+    double* th;          // t_hat = dp * T
+    double* pn;          // p_node
+    double* ef;          // t_hat / p_node
+    // rank structures (per order)
+    uint64_t* skey[N_ORD];   // orderable keys of the values (unsorted, padded)
+    uint64_t* sorted[N_ORD]; // sorted keys (chunk-sorted then merged)
+    uint32_t* pos[N_ORD];    // merged positions
+    uint64_t* U[N_ORD];      // sorted distinct keys
+    uint32_t* cut[N_ORD];    // near-set boundary per dense rank (Appendix A)
+    uint32_t* nd;            // distinct counts [N_ORD]
+    uint32_t* key32[N_ORD];  // packed keys (narrow)
+    uint64_t* key64[N_ORD];  // packed keys (wide)
+    int32_t* globals;        // [0] argmax t over all, [1] argmin p over all, [2] generic flag,
+                             // [3] number of exact folds last select
+};
+
+}  // namespace pals
+
+// ---- host-side objects behind the opaque C handles -----------------------
+struct pals_ctx {
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    int64_t launches = 0;
+    int num_sms = 148;
+    // scratch for host-buffer entry points
+    void* d_scratch = nullptr;
+    size_t scratch_bytes = 0;
+    void* h_pinned = nullptr;
+    size_t pinned_bytes = 0;
+    void* replay_cache = nullptr;  // replay.cu
+};
+
+enum ModelKind { MODEL_ANALYTIC = 0, MODEL_TABLE = 1, MODEL_FOREST = 2 };
+
+struct pals_model {
+    pals_ctx* ctx = nullptr;
+    ModelKind kind = MODEL_ANALYTIC;
+    std::string name;
+    pals_profile profile{};
+    pals::Analytic an{};
+    // table model (host copies + device copies)
+    int64_t table_n = 0;
+    pals_point* table_pts = nullptr;   // host
+    double* table_T = nullptr;         // host
+    double* table_P = nullptr;         // host
+    // forest model (device arrays), see forest.cu
+    void* forest = nullptr;
+};
+
+struct pals_grid {
+    pals_ctx* ctx = nullptr;
+    int64_t n = 0;
+    pals_point* h_pts = nullptr;  // host copy (validation, table mapping)
+    double* cap = nullptr;        // device SoA
+    int* batch = nullptr;
+    int* tp = nullptr;
+    int* ep = nullptr;
+    int* dp = nullptr;
+    int* inv_tr = nullptr;        // device: TR -> index
+    int* canon = nullptr;         // device: first index with an equal point
+    int* h_canon = nullptr;       // host copy
+};
+
+namespace pals {
+// error plumbing (ctx.cu)
+int set_error(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* where);
+#define PALS_CUDA(call)                                              \
+    do {                                                             \
+        cudaError_t _e = (call);                                     \
+        if (_e != cudaSuccess) return ::pals::cuda_fail(_e, #call);  \
+    } while (0)
+// model validation against a grid (ctx.cu): reproduces the first exception the
+// reference's scorer would throw over the candidates in order.
+int validate_points(const pals_model* m, const pals_point* pts, int64_t n);
+int validate_point(const pals_model* m, const pals_point& p);
+void count_launch(pals_ctx* ctx, int k = 1);
+const PlanDev& plan_dev(const pals_plan* p);
+int plan_error(const pals_plan* p);
+void replay_cache_free(pals_ctx* ctx);
+// forest.cu
+void forest_free(void* f);
+int forest_eval_plan(pals_plan* p, const pals_model* m, pals_ctx* ctx);
+}  // namespace pals

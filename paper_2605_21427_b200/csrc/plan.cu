@@ -1,0 +1,1115 @@
+// plan.cu — K1: evaluate the grid, build the rank tables, select for a batch of
+// queries with the reference's exact argmax.
+//
+// Reference semantics: select_config controller.hpp:132-201 with
+// better_candidate controller.hpp:118-125. The fast path turns every FP64
+// feasibility test and every tolerance comparison into integer compares on
+// precomputed dense ranks; queries whose winner sits in a near-tie cluster
+// (scores within 4e-9 relative) are re-decided by the literal sequential fold.
+#include <algorithm>
+#include <type_traits>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "pals_internal.cuh"
+
+namespace pals {
+
+constexpr int kChunk = 4096;        // sort chunk (smem bitonic)
+constexpr int kScanCh = 2048;       // configs per scan work item
+constexpr int kScanThreads = 256;
+// queries per thread in the scan (register tile): 8 with 32-bit keys, 4 with 64-bit
+template <typename K>
+struct ScanQ {
+    static constexpr int Q = sizeof(K) == 4 ? 8 : 4;
+    static constexpr int TQ = kScanThreads * Q;
+};
+
+enum { CLS_A = 0, CLS_B = 1, CLS_C = 2, CLS_D = 3, CLS_X = 4, N_CLS = 5 };
+enum { EX_FULL = 0, EX_QOS_NEAR = 1, EX_BUD_NEAR = 2 };
+
+struct WorkItem {
+    int32_t qid;
+    int32_t mode;
+    uint32_t d0;
+    int32_t pad;
+};
+
+}  // namespace pals
+
+using namespace pals;
+
+struct pals_plan {
+    pals_ctx* ctx = nullptr;
+    const pals_model* model = nullptr;
+    const pals_grid* grid = nullptr;
+    pals_coeffs coeffs{};
+    int err = PALS_OK;
+    std::string err_msg;
+    int64_t n = 0, np = 0;
+    int nchunks = 0;
+    int force_exact = 0;
+    int64_t last_exact = 0;
+    PlanDev d{};
+    int* tr = nullptr;            // device TR per point
+    Analytic* d_an = nullptr;     // device copy of the analytic params
+    int* table_map = nullptr;     // grid -> table row (table model)
+    double* table_T = nullptr;
+    double* table_P = nullptr;
+    uint64_t* gk = nullptr;       // [2] global candidate keys
+    uint64_t* merged[N_ORD] = {};
+    // query-side buffers (capacity-managed)
+    int64_t qcap = 0;
+    uint64_t* thr_t = nullptr;
+    uint64_t* thr_p = nullptr;
+    uint64_t* best_e = nullptr;
+    uint64_t* best_t = nullptr;
+    uint8_t* cls = nullptr;
+    int32_t* qlist = nullptr;     // N_CLS regions of qcap
+    int32_t* counts = nullptr;    // [N_CLS] class sizes, [N_CLS] exact count
+    WorkItem* work = nullptr;
+    pals_query* d_q = nullptr;    // host-API staging
+    int32_t* d_idx = nullptr;
+    uint8_t* d_reason = nullptr;
+    void* slab = nullptr;
+    // optional timing of the pair-scan kernel (bench.py roofline)
+    int time_scan = 0;
+    int scan_recorded = 0;
+    cudaEvent_t ev_scan0 = nullptr, ev_scan1 = nullptr;
+};
+
+namespace pals {
+
+// ---------------------------------------------------------------- eval ----
+__device__ __forceinline__ void finish_scores(const PlanDev& d, int64_t i, double T, double P,
+                                              int dp, double alpha, double beta) {
+    const double th = (double)dp * T;
+    const double pn = p_node_of(P, dp, alpha, beta);
+    const double ef = th / pn;
+    d.T[i] = T;
+    d.P[i] = P;
+    d.th[i] = th;
+    d.pn[i] = pn;
+    d.ef[i] = ef;
+    d.skey[ORD_T][i] = ~orderable(th);
+    d.skey[ORD_P][i] = orderable(pn);
+    d.skey[ORD_E][i] = ~orderable(ef);
+    // the integer fast path needs positive, finite, well-scaled scores
+    const bool ok = isfinite(th) && isfinite(pn) && isfinite(ef) && th > 1e-250 && pn > 1e-250 &&
+                    ef > 1e-250;
+    if (!ok) atomicOr(&d.globals[2], 1);
+}
+
+__global__ void k_eval_analytic(PlanDev d, const Analytic* __restrict__ an,
+                                const int* __restrict__ tp, double alpha, double beta) {
+    const Analytic& a = *an;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const Score s = analytic_score(a, d.cap[i], d.batch[i], tp[i], d.dp[i]);
+        finish_scores(d, i, s.T, s.P, d.dp[i], alpha, beta);
+    }
+}
+
+__global__ void k_eval_table(PlanDev d, const int* __restrict__ map, const double* __restrict__ tT,
+                             const double* __restrict__ tP, double alpha, double beta) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int r = map[i];
+        finish_scores(d, i, tT[r], tP[r], d.dp[i], alpha, beta);
+    }
+}
+
+__global__ void k_pad_keys(PlanDev d, int64_t np) {
+    const int o = blockIdx.y;
+    for (int64_t i = d.n + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < np;
+         i += (int64_t)gridDim.x * blockDim.x)
+        d.skey[o][i] = kNone64;
+}
+
+// ---------------------------------------------------------------- sort ----
+// (1) bitonic sort of each 4096-key chunk in shared memory
+__global__ void __launch_bounds__(1024) k_sort_chunks(PlanDev d) {
+    __shared__ uint64_t s[kChunk];
+    const int o = blockIdx.y;
+    const int64_t base = (int64_t)blockIdx.x * kChunk;
+    for (int i = threadIdx.x; i < kChunk; i += blockDim.x) s[i] = d.skey[o][base + i];
+    __syncthreads();
+    for (int k = 2; k <= kChunk; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < kChunk; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const uint64_t a = s[i], b = s[ixj];
+                    const bool up = (i & k) == 0;
+                    if ((a > b) == up) {
+                        s[i] = b;
+                        s[ixj] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < kChunk; i += blockDim.x) d.sorted[o][base + i] = s[i];
+}
+
+__device__ __forceinline__ int lower_bound_s(const uint64_t* s, int n, uint64_t x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (s[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+__device__ __forceinline__ int upper_bound_s(const uint64_t* s, int n, uint64_t x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (s[mid] <= x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// (2) merged position of every chunk-sorted key = its rank within its chunk plus
+// the number of keys before it in every other chunk (a stable k-way merge).
+__global__ void __launch_bounds__(256) k_cross(PlanDev d) {
+    __shared__ uint64_t s[kChunk];
+    const int a = blockIdx.x, b = blockIdx.y, o = blockIdx.z;
+    const int64_t abase = (int64_t)a * kChunk, bbase = (int64_t)b * kChunk;
+    if (a != b)
+        for (int i = threadIdx.x; i < kChunk; i += blockDim.x) s[i] = d.sorted[o][bbase + i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < kChunk; i += blockDim.x) {
+        if (abase + i >= d.n) break;
+        const uint64_t x = d.sorted[o][abase + i];
+        int cnt;
+        if (a == b) cnt = i;
+        else if (b < a) cnt = upper_bound_s(s, kChunk, x);
+        else cnt = lower_bound_s(s, kChunk, x);
+        atomicAdd(&d.pos[o][abase + i], (uint32_t)cnt);
+    }
+}
+
+// (3) scatter to the merged order
+__global__ void k_scatter(PlanDev d, uint64_t* m0, uint64_t* m1, uint64_t* m2) {
+    const int o = blockIdx.y;
+    uint64_t* m = o == 0 ? m0 : (o == 1 ? m1 : m2);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        m[d.pos[o][i]] = d.sorted[o][i];
+}
+
+__device__ __forceinline__ double key_value(int o, uint64_t k) {
+    return o == ORD_P ? unorderable(k) : unorderable(~k);
+}
+
+// Two values are "separated" when no pair straddling them can be a tolerance
+// tie of better_candidate (|a-b|/max(|a|,|b|) <= 1e-9), with a 4x margin.
+__device__ __forceinline__ bool separated(double a, double b) {
+    return fabs(a - b) > 4e-9 * smax(fabs(a), fabs(b));
+}
+
+// block-wide exclusive scan of one uint32 per thread (1024 threads)
+__device__ uint32_t block_excl_scan(uint32_t v, uint32_t* sh, uint32_t* total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sh[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t t = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        sh[lane] = t;
+    }
+    __syncthreads();
+    const uint32_t before = (w ? sh[w - 1] : 0) + x - v;
+    *total = sh[(blockDim.x >> 5) - 1];
+    __syncthreads();
+    return before;
+}
+
+// (4) distinct values, their count, and the near-tie cluster boundary cut[d]:
+// the last dense index e >= d such that U[e] and U[e+1] are separated.
+__global__ void __launch_bounds__(1024) k_unique(PlanDev d, const uint64_t* m0, const uint64_t* m1,
+                                                 const uint64_t* m2) {
+    __shared__ uint32_t sh[64];
+    __shared__ uint32_t sh_min[1024];
+    const int o = blockIdx.x;
+    const uint64_t* m = o == 0 ? m0 : (o == 1 ? m1 : m2);
+    const int64_t n = d.n;
+    const int T = blockDim.x, t = threadIdx.x;
+    const int64_t seg = (n + T - 1) / T;
+    const int64_t lo = t * seg, hi = min(n, lo + seg);
+    uint32_t cnt = 0;
+    for (int64_t i = lo; i < hi; ++i) cnt += (i == 0 || m[i] != m[i - 1]) ? 1u : 0u;
+    uint32_t nd;
+    uint32_t p = block_excl_scan(cnt, sh, &nd);
+    for (int64_t i = lo; i < hi; ++i)
+        if (i == 0 || m[i] != m[i - 1]) d.U[o][p++] = m[i];
+    if (t == 0) d.nd[o] = nd;
+    __threadfence_block();
+    __syncthreads();
+    // cut: suffix-min over the indices of separated boundaries
+    const int64_t dseg = ((int64_t)nd + T - 1) / T;
+    const int64_t dlo = t * dseg, dhi = min((int64_t)nd, dlo + dseg);
+    uint32_t first_sep = 0xFFFFFFFFu;
+    for (int64_t e = dlo; e < dhi; ++e) {
+        const bool sep = (e == (int64_t)nd - 1) ||
+                         separated(key_value(o, d.U[o][e]), key_value(o, d.U[o][e + 1]));
+        if (sep) {
+            first_sep = (uint32_t)e;
+            break;
+        }
+    }
+    sh_min[t] = first_sep;
+    __syncthreads();
+    // exclusive suffix min across threads (sequential over 1024 is fine: once per plan)
+    if (t == 0) {
+        uint32_t run = 0xFFFFFFFFu;
+        for (int k = T - 1; k >= 0; --k) {
+            const uint32_t v = sh_min[k];
+            sh_min[k] = run;
+            run = min(run, v);
+        }
+    }
+    __syncthreads();
+    uint32_t next = sh_min[t];
+    for (int64_t e = dhi - 1; e >= dlo; --e) {
+        const bool sep = (e == (int64_t)nd - 1) ||
+                         separated(key_value(o, d.U[o][e]), key_value(o, d.U[o][e + 1]));
+        if (sep) next = (uint32_t)e;
+        d.cut[o][e] = next;
+    }
+}
+
+__device__ __forceinline__ uint32_t dense_rank(const uint64_t* U, uint32_t nd, uint64_t x) {
+    uint32_t lo = 0, hi = nd;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (U[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// (5) packed keys (D << tr_bits) | TR for all three orders
+__global__ void k_assign(PlanDev d, const int* __restrict__ tr, uint64_t* gk) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = (uint64_t)tr[i];
+#pragma unroll
+        for (int o = 0; o < N_ORD; ++o) {
+            const uint32_t D = dense_rank(d.U[o], d.nd[o], d.skey[o][i]);
+            const uint64_t k = ((uint64_t)D << d.tr_bits) | r;
+            if (d.wide) d.key64[o][i] = k;
+            else d.key32[o][i] = (uint32_t)k;
+            if (D == 0 && o == ORD_T) atomicMin((unsigned long long*)&gk[0], k);
+            if (D == 0 && o == ORD_P) atomicMin((unsigned long long*)&gk[1], k);
+        }
+    }
+}
+
+// ------------------------------------------------------- exact fold ------
+// The reference's sequential fold `if (!best || better(s, best)) best = s`
+// (controller.hpp:162-198), executed by one warp in candidate order: each
+// round finds the first lane (after the last update) that beats the running
+// best, so every comparison the reference makes is made, in the same order.
+template <class Filter, class ScoreF>
+__device__ int warp_fold(int64_t n, const double* __restrict__ cap, const int* __restrict__ batch,
+                         Filter filt, ScoreF score) {
+    const int lane = threadIdx.x & 31;
+    int64_t best = -1;
+    double bs = 0.0, bcap = 0.0;
+    int bb = 0;
+    for (int64_t base = 0; base < n; base += 32) {
+        const int64_t c = base + lane;
+        const bool ok = c < n && filt(c);
+        double s = 0.0, cp = 0.0;
+        int bt = 0;
+        if (ok) {
+            s = score(c);
+            cp = cap[c];
+            bt = batch[c];
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, ok);
+        if (!m) continue;
+        int last = -1;
+        if (best < 0) {
+            const int l = __ffs(m) - 1;
+            best = base + l;
+            bs = __shfl_sync(0xffffffffu, s, l);
+            bcap = __shfl_sync(0xffffffffu, cp, l);
+            bb = __shfl_sync(0xffffffffu, bt, l);
+            last = l;
+        }
+        while (true) {
+            const bool b = ok && lane > last && better_exact(s, cp, bt, bs, bcap, bb);
+            const unsigned bm = __ballot_sync(0xffffffffu, b);
+            if (!bm) break;
+            const int l = __ffs(bm) - 1;
+            best = base + l;
+            bs = __shfl_sync(0xffffffffu, s, l);
+            bcap = __shfl_sync(0xffffffffu, cp, l);
+            bb = __shfl_sync(0xffffffffu, bt, l);
+            last = l;
+        }
+    }
+    return (int)best;
+}
+
+__device__ __forceinline__ uint32_t dense_of(const PlanDev& d, int o, int64_t c) {
+    return d.wide ? (uint32_t)(d.key64[o][c] >> d.tr_bits)
+                  : (uint32_t)(d.key32[o][c] >> d.tr_bits);
+}
+
+// Literal select_config (controller.hpp:132-201) by one warp.
+__device__ void warp_select_full(const PlanDev& d, const pals_query& q, int32_t* idx,
+                                 uint8_t* reason) {
+    const double target = q.throughput_tps * (1.0 + q.target_headroom);
+    const bool bset = q.has_budget != 0;
+    const double budget = bset ? q.power_budget_w * (1.0 - q.budget_margin) : 0.0;
+    const double bias = q.bias;
+    int best = -1;
+    int r = PALS_REASON_FALLBACK_MAX_T;
+    if (q.objective == PALS_OBJ_QOS) {
+        best = warp_fold(
+            d.n, d.cap, d.batch,
+            [&](int64_t c) {
+                return !((bset && !(d.pn[c] <= budget)) || d.th[c] * bias < target);
+            },
+            [&](int64_t c) { return d.th[c] / d.pn[c]; });
+        if (best >= 0) r = PALS_REASON_QOS_FEASIBLE;
+    }
+    if (best < 0 && bset) {
+        best = warp_fold(
+            d.n, d.cap, d.batch, [&](int64_t c) { return d.pn[c] <= budget; },
+            [&](int64_t c) { return d.th[c]; });
+        if (best >= 0) r = PALS_REASON_BUDGET_MAX_T;
+        if (best < 0) {
+            best = warp_fold(
+                d.n, d.cap, d.batch, [&](int64_t) { return true; },
+                [&](int64_t c) { return -d.pn[c]; });
+            r = PALS_REASON_BUDGET_MAX_T;
+        }
+    }
+    if (best < 0) {
+        best = warp_fold(
+            d.n, d.cap, d.batch, [&](int64_t) { return true; },
+            [&](int64_t c) { return d.th[c]; });
+        r = PALS_REASON_FALLBACK_MAX_T;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        *idx = best;
+        *reason = (uint8_t)r;
+    }
+}
+
+// (6) query-independent winners: argmax t_hat over all and argmin p_node over all
+__global__ void k_resolve_globals(PlanDev d, const uint64_t* gk) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int generic = d.globals[2];
+    const int o = w == 0 ? ORD_T : ORD_P;
+    const uint64_t mask = (1ull << d.tr_bits) - 1;
+    int best;
+    if (!generic && d.cut[o][0] == 0) {
+        best = d.inv_tr[gk[w] & mask];
+    } else {
+        const uint32_t cut = generic ? 0xFFFFFFFFu : d.cut[o][0];
+        if (w == 0)
+            best = warp_fold(
+                d.n, d.cap, d.batch,
+                [&](int64_t c) { return generic || dense_of(d, ORD_T, c) <= cut; },
+                [&](int64_t c) { return d.th[c]; });
+        else
+            best = warp_fold(
+                d.n, d.cap, d.batch,
+                [&](int64_t c) { return generic || dense_of(d, ORD_P, c) <= cut; },
+                [&](int64_t c) { return -d.pn[c]; });
+    }
+    if (lane == 0) d.globals[w] = best;
+}
+
+// ------------------------------------------------------------ select ----
+template <typename K>
+struct KeyTraits;
+template <>
+struct KeyTraits<uint32_t> {
+    static __device__ __forceinline__ const uint32_t* keys(const PlanDev& d, int o) {
+        return d.key32[o];
+    }
+};
+template <>
+struct KeyTraits<uint64_t> {
+    static __device__ __forceinline__ const uint64_t* keys(const PlanDev& d, int o) {
+        return d.key64[o];
+    }
+};
+
+struct SelArgs {
+    const pals_query* q;
+    int64_t nq;
+    int32_t* out_idx;
+    uint8_t* out_reason;
+    uint64_t* thr_t;
+    uint64_t* thr_p;
+    uint64_t* best_e;
+    uint64_t* best_t;
+    uint8_t* cls;
+    int32_t* qlist;
+    int32_t* counts;  // [0..N_CLS) class sizes, [N_CLS] work items
+    WorkItem* work;
+    int64_t qcap;
+    int force_exact;
+};
+
+// (7) per-query thresholds in dense-rank space and the query class.
+// Kt = #distinct t_hat with !(t*bias < target)  (controller.hpp:163, monotone in t)
+// Kp = #distinct p_node with p <= budget        (controller.hpp:155)
+__global__ void k_qprep(PlanDev d, SelArgs a) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x; j0 < a.nq;
+         j0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = j0 + threadIdx.x;
+        int c = -1;
+        if (j < a.nq) {
+            const pals_query q = a.q[j];
+            const bool bset = q.has_budget != 0;
+            uint32_t Kt = 0, Kp = d.nd[ORD_P];
+            if (q.objective == PALS_OBJ_QOS) {
+                const double target = q.throughput_tps * (1.0 + q.target_headroom);
+                uint32_t lo = 0, hi = d.nd[ORD_T];
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    const double t = key_value(ORD_T, d.U[ORD_T][mid]);
+                    if (!(t * q.bias < target)) lo = mid + 1;
+                    else hi = mid;
+                }
+                Kt = lo;
+            }
+            if (bset) {
+                const double budget = q.power_budget_w * (1.0 - q.budget_margin);
+                uint32_t lo = 0, hi = d.nd[ORD_P];
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (key_value(ORD_P, d.U[ORD_P][mid]) <= budget) lo = mid + 1;
+                    else hi = mid;
+                }
+                Kp = lo;
+            }
+            if (a.force_exact || d.globals[2]) c = CLS_X;
+            else if (q.objective == PALS_OBJ_QOS && !bset) c = Kt ? CLS_A : CLS_D;
+            else if (q.objective == PALS_OBJ_QOS) c = (Kp == 0) ? CLS_D : (Kt ? CLS_B : CLS_C);
+            else c = (bset && Kp) ? CLS_C : CLS_D;
+            // inclusive thresholds: feasible <=> key <= (K << tr_bits) - 1
+            a.thr_t[j] = Kt ? (((uint64_t)Kt << d.tr_bits) - 1) : 0;
+            a.thr_p[j] = Kp ? (((uint64_t)Kp << d.tr_bits) - 1) : 0;
+            a.best_e[j] = kNone64;
+            a.best_t[j] = kNone64;
+            a.cls[j] = (uint8_t)c;
+        }
+        // warp-aggregated bucket append
+        for (int k = 0; k < N_CLS; ++k) {
+            const unsigned m = __ballot_sync(0xffffffffu, c == k);
+            if (!m) continue;
+            int base = 0;
+            if (lane == __ffs(m) - 1) base = atomicAdd(&a.counts[k], __popc(m));
+            base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+            if (c == k) a.qlist[k * a.qcap + base + __popc(m & ((1u << lane) - 1))] = (int32_t)j;
+        }
+    }
+}
+
+// (8) the pair scan: every (query, config) pair of classes A/B/C is decided by
+// integer compares on the dense-rank keys (persistent CTAs over work items).
+template <typename K, int CLS, int kQ>
+__device__ __forceinline__ void scan_item(const K* __restrict__ se, const K* __restrict__ st,
+                                          const K* __restrict__ sp, int nc, const K* thr_t,
+                                          const K* thr_p, K* be, K* bt) {
+    constexpr int V = 16 / sizeof(K);
+    using VT = typename std::conditional<sizeof(K) == 4, uint4, ulonglong2>::type;
+    for (int c = 0; c < nc; c += V) {
+        K e[V], t[V], p[V];
+        if (CLS != CLS_C) {
+            const VT ve = *reinterpret_cast<const VT*>(se + c);
+            memcpy(e, &ve, 16);
+        }
+        {
+            const VT vt = *reinterpret_cast<const VT*>(st + c);
+            memcpy(t, &vt, 16);
+        }
+        if (CLS != CLS_A) {
+            const VT vp = *reinterpret_cast<const VT*>(sp + c);
+            memcpy(p, &vp, 16);
+        }
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+#pragma unroll
+            for (int q = 0; q < kQ; ++q) {
+                if (CLS == CLS_A) {
+                    if (t[v] <= thr_t[q]) be[q] = min(be[q], e[v]);
+                } else if (CLS == CLS_B) {
+                    const bool fp = p[v] <= thr_p[q];
+                    if (fp && t[v] <= thr_t[q]) be[q] = min(be[q], e[v]);
+                    if (fp) bt[q] = min(bt[q], t[v]);
+                } else {
+                    if (p[v] <= thr_p[q]) bt[q] = min(bt[q], t[v]);
+                }
+            }
+        }
+    }
+}
+
+template <typename K>
+__global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a, int nchunks) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    K* se = reinterpret_cast<K*>(smem_raw);
+    K* st = se + kScanCh;
+    K* sp = st + kScanCh;
+    const K* ke = KeyTraits<K>::keys(d, ORD_E);
+    const K* kt = KeyTraits<K>::keys(d, ORD_T);
+    const K* kp = KeyTraits<K>::keys(d, ORD_P);
+    constexpr int kQ = ScanQ<K>::Q;
+    constexpr int kTQ = ScanQ<K>::TQ;
+    int64_t items[3];
+    int64_t tot = 0;
+    for (int c = 0; c < 3; ++c) {
+        const int64_t tiles = (a.counts[c] + kTQ - 1) / kTQ;
+        items[c] = tiles * nchunks;
+        tot += items[c];
+    }
+    for (int64_t it = blockIdx.x; it < tot; it += gridDim.x) {
+        int c = 0;
+        int64_t r = it;
+        while (r >= items[c]) {
+            r -= items[c];
+            ++c;
+        }
+        const int64_t tile = r / nchunks;
+        const int chunk = (int)(r % nchunks);
+        const int64_t c0 = (int64_t)chunk * kScanCh;
+        const int64_t rem = d.n - c0;
+        const int nc = (int)(rem < kScanCh ? rem : kScanCh);
+        const int ncp = (nc + 3) & ~3;
+        // stage this chunk's keys (pad with keys that never pass a threshold)
+        for (int i = threadIdx.x; i < ncp; i += blockDim.x) {
+            const bool in = i < nc;
+            if (c != CLS_C) se[i] = in ? ke[c0 + i] : (K)~(K)0;
+            st[i] = in ? kt[c0 + i] : (K)~(K)0;
+            if (c != CLS_A) sp[i] = in ? kp[c0 + i] : (K)~(K)0;
+        }
+        K thr_t[kQ], thr_p[kQ], be[kQ], bt[kQ];
+        int32_t qid[kQ];
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+            const int64_t s = tile * kTQ + q * kScanThreads + threadIdx.x;
+            qid[q] = s < a.counts[c] ? a.qlist[c * a.qcap + s] : -1;
+            thr_t[q] = qid[q] >= 0 ? (K)a.thr_t[qid[q]] : (K)0;
+            thr_p[q] = qid[q] >= 0 ? (K)a.thr_p[qid[q]] : (K)0;
+            be[q] = (K)~(K)0;
+            bt[q] = (K)~(K)0;
+        }
+        __syncthreads();
+        // padded slots carry all-ones keys: they only pass an all-ones threshold,
+        // and then they cannot lower a minimum below a real key
+        if (c == CLS_A) scan_item<K, CLS_A, kQ>(se, st, sp, ncp, thr_t, thr_p, be, bt);
+        else if (c == CLS_B) scan_item<K, CLS_B, kQ>(se, st, sp, ncp, thr_t, thr_p, be, bt);
+        else scan_item<K, CLS_C, kQ>(se, st, sp, ncp, thr_t, thr_p, be, bt);
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+            if (qid[q] < 0) continue;
+            if (c != CLS_C && be[q] != (K)~(K)0)
+                atomicMin((unsigned long long*)&a.best_e[qid[q]], (unsigned long long)be[q]);
+            if (c != CLS_A && bt[q] != (K)~(K)0)
+                atomicMin((unsigned long long*)&a.best_t[qid[q]], (unsigned long long)bt[q]);
+        }
+    }
+}
+
+// exact feasibility of point c for query q (FP64, controller.hpp:155, 163)
+__device__ __forceinline__ bool feasible_t(const PlanDev& d, const pals_query& q, int64_t c) {
+    const double target = q.throughput_tps * (1.0 + q.target_headroom);
+    return !(d.th[c] * q.bias < target);
+}
+__device__ __forceinline__ bool feasible_p(const PlanDev& d, const pals_query& q, int64_t c) {
+    if (!q.has_budget) return true;
+    return d.pn[c] <= q.power_budget_w * (1.0 - q.budget_margin);
+}
+
+// Resolve the "none" sentinel: with 16-bit fields an all-ones key is a real key
+// when n == 65536; it is the largest key, so it wins only if it is the sole
+// feasible point.
+__device__ __forceinline__ uint64_t fix_sentinel(const PlanDev& d, uint64_t best, int o,
+                                                 const pals_query& q, bool need_t, bool need_p) {
+    if (d.wide || best != kNone64) return best;
+    const uint32_t full = 0xFFFFFFFFu;
+    // the point whose packed key in order o is all-ones (TR = n-1 and D = 65535)
+    if (d.n != 65536) return best;
+    const int64_t c = d.inv_tr[d.n - 1];
+    if (d.key32[o][c] != full) return best;
+    if (need_t && !feasible_t(d, q, c)) return best;
+    if (need_p && !feasible_p(d, q, c)) return best;
+    return full;
+}
+
+__device__ __forceinline__ void push_work(const SelArgs& a, int32_t qid, int mode, uint32_t d0) {
+    const int k = atomicAdd(&a.counts[N_CLS], 1);
+    a.work[k] = WorkItem{qid, mode, d0, 0};
+}
+
+// (9) decide every query from its two minima; near-tie winners go to the exact fold
+__global__ void k_finalize(PlanDev d, SelArgs a) {
+    const uint64_t mask = (1ull << d.tr_bits) - 1;
+    const uint64_t none = kNone64;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.nq;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const int c = a.cls[j];
+        const pals_query q = a.q[j];
+        if (c == CLS_X) {
+            push_work(a, (int32_t)j, EX_FULL, 0);
+            continue;
+        }
+        uint64_t be = a.best_e[j], bt = a.best_t[j];
+        if (!d.wide) {
+            be = be == 0xFFFFFFFFull ? none : be;
+            bt = bt == 0xFFFFFFFFull ? none : bt;
+        }
+        int32_t idx = -1;
+        int r = PALS_REASON_FALLBACK_MAX_T;
+        if (c == CLS_A || c == CLS_B) {
+            be = fix_sentinel(d, be, ORD_E, q, true, c == CLS_B);
+            if (be != none) {
+                const uint32_t d0 = (uint32_t)(be >> d.tr_bits);
+                if (d.cut[ORD_E][d0] != d0) {
+                    push_work(a, (int32_t)j, EX_QOS_NEAR, d0);
+                    continue;
+                }
+                idx = d.inv_tr[be & mask];
+                r = PALS_REASON_QOS_FEASIBLE;
+            }
+        }
+        if (idx < 0 && q.has_budget && (c == CLS_B || c == CLS_C || c == CLS_D)) {
+            if (c != CLS_D) bt = fix_sentinel(d, bt, ORD_T, q, false, true);
+            if (c != CLS_D && bt != none) {
+                const uint32_t d0 = (uint32_t)(bt >> d.tr_bits);
+                if (d.cut[ORD_T][d0] != d0) {
+                    push_work(a, (int32_t)j, EX_BUD_NEAR, d0);
+                    continue;
+                }
+                idx = d.inv_tr[bt & mask];
+            } else {
+                idx = d.globals[1];  // budget below every candidate: least power (:180-188)
+            }
+            r = PALS_REASON_BUDGET_MAX_T;
+        }
+        if (idx < 0) {
+            idx = d.globals[0];  // fallback: max throughput over all (:191-198)
+            r = PALS_REASON_FALLBACK_MAX_T;
+        }
+        a.out_idx[j] = idx;
+        a.out_reason[j] = (uint8_t)r;
+    }
+}
+
+// (10) exact sequential fold for the queued queries, one warp per query
+__global__ void k_exact(PlanDev d, SelArgs a) {
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwork = a.counts[N_CLS];
+    for (int k = w; k < nwork; k += warps) {
+        const WorkItem it = a.work[k];
+        const pals_query q = a.q[it.qid];
+        if (it.mode == EX_FULL) {
+            warp_select_full(d, q, &a.out_idx[it.qid], &a.out_reason[it.qid]);
+            continue;
+        }
+        int best;
+        int r;
+        if (it.mode == EX_QOS_NEAR) {
+            const uint32_t cut = d.cut[ORD_E][it.d0];
+            best = warp_fold(
+                d.n, d.cap, d.batch,
+                [&](int64_t c) {
+                    return dense_of(d, ORD_E, c) <= cut && feasible_t(d, q, c) &&
+                           feasible_p(d, q, c);
+                },
+                [&](int64_t c) { return d.ef[c]; });
+            r = PALS_REASON_QOS_FEASIBLE;
+        } else {
+            const uint32_t cut = d.cut[ORD_T][it.d0];
+            best = warp_fold(
+                d.n, d.cap, d.batch,
+                [&](int64_t c) { return dense_of(d, ORD_T, c) <= cut && feasible_p(d, q, c); },
+                [&](int64_t c) { return d.th[c]; });
+            r = PALS_REASON_BUDGET_MAX_T;
+        }
+        if ((threadIdx.x & 31) == 0) {
+            a.out_idx[it.qid] = best;
+            a.out_reason[it.qid] = (uint8_t)r;
+        }
+    }
+}
+
+static int grid_blocks(pals_ctx* ctx, int64_t n, int threads) {
+    const int64_t b = (n + threads - 1) / threads;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)ctx->num_sms * 16));
+}
+
+static int check_launch(const char* what) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, what);
+    return PALS_OK;
+}
+
+// device-side plan state accessors used by replay.cu
+const PlanDev& plan_dev(const pals_plan* p) { return p->d; }
+int plan_error(const pals_plan* p) { return p->err; }
+
+}  // namespace pals
+
+extern "C" {
+
+int pals_plan_create(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
+                     const pals_coeffs* coeffs, pals_plan** out) {
+    if (!ctx || !m || !g || !coeffs) return set_error(PALS_ECONFIG, "pals_plan_create: null");
+    PALS_CUDA(cudaSetDevice(ctx->device));
+    auto* p = new pals_plan();
+    p->ctx = ctx;
+    p->model = m;
+    p->grid = g;
+    p->coeffs = *coeffs;
+    p->n = g->n;
+    // the reference scores every candidate before ranking; the first candidate
+    // the scorer rejects aborts the call with that exception (controller.hpp:146-151)
+    if (g->n == 0) {
+        p->err = PALS_ECONFIG;
+        p->err_msg = "select_config: empty candidate list";
+    } else if (validate_points(m, g->h_pts, g->n) != PALS_OK) {
+        p->err = validate_points(m, g->h_pts, g->n);
+        p->err_msg = pals_last_error();
+    }
+    const int64_t n = std::max<int64_t>(1, g->n);
+    p->nchunks = (int)((n + kChunk - 1) / kChunk);
+    p->np = (int64_t)p->nchunks * kChunk;
+    PlanDev& d = p->d;
+    d.n = g->n;
+    d.wide = g->n > 65536 ? 1 : 0;
+    d.tr_bits = d.wide ? 32 : 16;
+    d.cap = g->cap;
+    d.batch = g->batch;
+    d.dp = g->dp;
+    d.inv_tr = g->inv_tr;
+    // one slab for all per-plan device arrays
+    const size_t n8 = (size_t)n * 8, np8 = (size_t)p->np * 8, np4 = (size_t)p->np * 4;
+    size_t bytes = 5 * n8 + N_ORD * (3 * np8 + np4 + n8 + (size_t)n * 4) + 64 + 4 * (size_t)n +
+                   (d.wide ? N_ORD * n8 : N_ORD * (size_t)n * 4) + 4096;
+    if (m->kind == MODEL_TABLE) bytes += 4 * (size_t)n + 2 * 8 * (size_t)std::max<int64_t>(1, m->table_n);
+    bytes += sizeof(Analytic) + 256;
+    PALS_CUDA(cudaMalloc(&p->slab, bytes));
+    char* s = (char*)p->slab;
+    auto take = [&](size_t b) {
+        char* r = s;
+        s += (b + 255) & ~(size_t)255;
+        return (void*)r;
+    };
+    d.T = (double*)take(n8);
+    d.P = (double*)take(n8);
+    d.th = (double*)take(n8);
+    d.pn = (double*)take(n8);
+    d.ef = (double*)take(n8);
+    for (int o = 0; o < N_ORD; ++o) {
+        d.skey[o] = (uint64_t*)take(np8);
+        d.sorted[o] = (uint64_t*)take(np8);
+        p->merged[o] = (uint64_t*)take(np8);
+        d.pos[o] = (uint32_t*)take(np4);
+        d.U[o] = (uint64_t*)take(n8);
+        d.cut[o] = (uint32_t*)take((size_t)n * 4);
+        if (d.wide) d.key64[o] = (uint64_t*)take(n8);
+        else d.key32[o] = (uint32_t*)take((size_t)n * 4);
+    }
+    d.nd = (uint32_t*)take(16);
+    d.globals = (int32_t*)take(16);
+    p->gk = (uint64_t*)take(16);
+    p->d_an = (Analytic*)take(sizeof(Analytic));
+    // TR per point (inverse of grid inv_tr), computed once on the host at grid creation
+    p->tr = (int*)take(4 * (size_t)n);
+    {
+        std::vector<int> inv(g->n), tr(g->n);
+        if (g->n) {
+            PALS_CUDA(cudaMemcpy(inv.data(), g->inv_tr, g->n * sizeof(int), cudaMemcpyDeviceToHost));
+            for (int64_t r = 0; r < g->n; ++r) tr[inv[r]] = (int)r;
+            PALS_CUDA(cudaMemcpy(p->tr, tr.data(), g->n * sizeof(int), cudaMemcpyHostToDevice));
+        }
+    }
+    if (m->kind == MODEL_ANALYTIC)
+        PALS_CUDA(cudaMemcpy(p->d_an, &m->an, sizeof(Analytic), cudaMemcpyHostToDevice));
+    if (m->kind == MODEL_TABLE) {
+        p->table_map = (int*)take(4 * (size_t)n);
+        const int64_t tn = std::max<int64_t>(1, m->table_n);
+        p->table_T = (double*)take(8 * (size_t)tn);
+        p->table_P = (double*)take(8 * (size_t)tn);
+        // first table row equal by value (TableScorer, tests/test_controller.cpp:23-26)
+        std::unordered_map<std::string, int> first;
+        for (int64_t i = 0; i < m->table_n; ++i) {
+            pals_point q = m->table_pts[i];
+            if (q.cap_watts == 0.0) q.cap_watts = 0.0;
+            first.emplace(std::string((const char*)&q, sizeof q), (int)i);
+        }
+        std::vector<int> map(g->n, 0);
+        for (int64_t i = 0; i < g->n; ++i) {
+            pals_point q = g->h_pts[i];
+            if (q.cap_watts == 0.0) q.cap_watts = 0.0;
+            auto it = first.find(std::string((const char*)&q, sizeof q));
+            map[i] = it == first.end() ? 0 : it->second;
+        }
+        if (g->n)
+            PALS_CUDA(cudaMemcpy(p->table_map, map.data(), g->n * 4, cudaMemcpyHostToDevice));
+        if (m->table_n) {
+            PALS_CUDA(cudaMemcpy(p->table_T, m->table_T, m->table_n * 8, cudaMemcpyHostToDevice));
+            PALS_CUDA(cudaMemcpy(p->table_P, m->table_P, m->table_n * 8, cudaMemcpyHostToDevice));
+        }
+    }
+    *out = p;
+    return PALS_OK;
+}
+
+int pals_plan_destroy(pals_plan* p) {
+    if (!p) return PALS_OK;
+    cudaSetDevice(p->ctx->device);
+    if (p->ev_scan0) cudaEventDestroy(p->ev_scan0);
+    if (p->ev_scan1) cudaEventDestroy(p->ev_scan1);
+    cudaFree(p->slab);
+    cudaFree(p->thr_t);
+    cudaFree(p->d_q);
+    delete p;
+    return PALS_OK;
+}
+
+
+int pals_plan_prepare(pals_plan* p) {
+    if (p->err) return set_error(p->err, p->err_msg);
+    pals_ctx* ctx = p->ctx;
+    cudaStream_t s = ctx->stream;
+    PlanDev& d = p->d;
+    const int64_t n = p->n;
+    PALS_CUDA(cudaMemsetAsync(d.globals, 0, 16, s));
+    PALS_CUDA(cudaMemsetAsync(p->gk, 0xFF, 16, s));
+    for (int o = 0; o < N_ORD; ++o) PALS_CUDA(cudaMemsetAsync(d.pos[o], 0, p->np * 4, s));
+    const int eb = grid_blocks(ctx, n, 256);
+    if (p->model->kind == MODEL_ANALYTIC) {
+        k_eval_analytic<<<eb, 256, 0, s>>>(d, p->d_an, p->grid->tp, p->coeffs.alpha,
+                                           p->coeffs.beta_watts);
+    } else if (p->model->kind == MODEL_TABLE) {
+        k_eval_table<<<eb, 256, 0, s>>>(d, p->table_map, p->table_T, p->table_P, p->coeffs.alpha,
+                                        p->coeffs.beta_watts);
+    } else {
+        const int rc = forest_eval_plan(p, p->model, ctx);
+        if (rc) return rc;
+    }
+    if (p->np > n) k_pad_keys<<<dim3(grid_blocks(ctx, p->np - n, 256), N_ORD), 256, 0, s>>>(d, p->np);
+    k_sort_chunks<<<dim3(p->nchunks, N_ORD), 1024, 0, s>>>(d);
+    k_cross<<<dim3(p->nchunks, p->nchunks, N_ORD), 256, 0, s>>>(d);
+    k_scatter<<<dim3(grid_blocks(ctx, n, 256), N_ORD), 256, 0, s>>>(d, p->merged[0], p->merged[1],
+                                                                   p->merged[2]);
+    k_unique<<<N_ORD, 1024, 0, s>>>(d, p->merged[0], p->merged[1], p->merged[2]);
+    k_assign<<<eb, 256, 0, s>>>(d, p->tr, p->gk);
+    k_resolve_globals<<<1, 64, 0, s>>>(d, p->gk);
+    count_launch(ctx, 8 + (p->np > n ? 1 : 0));
+    return check_launch("pals_plan_prepare");
+}
+
+static int ensure_query_buffers(pals_plan* p, int64_t nq) {
+    if (nq <= p->qcap) return PALS_OK;
+    cudaFree(p->thr_t);
+    const int64_t cap = std::max<int64_t>(nq, 1024);
+    const size_t bytes = (size_t)cap * (8 * 4 + 1 + 4 * N_CLS + sizeof(WorkItem)) + 4096;
+    PALS_CUDA(cudaMalloc(&p->thr_t, bytes));
+    char* s = (char*)p->thr_t;
+    auto take = [&](size_t b) {
+        char* r = s;
+        s += (b + 255) & ~(size_t)255;
+        return (void*)r;
+    };
+    p->thr_t = (uint64_t*)take(8 * cap);
+    p->thr_p = (uint64_t*)take(8 * cap);
+    p->best_e = (uint64_t*)take(8 * cap);
+    p->best_t = (uint64_t*)take(8 * cap);
+    p->cls = (uint8_t*)take(cap);
+    p->qlist = (int32_t*)take(4 * (size_t)cap * N_CLS);
+    p->work = (WorkItem*)take(sizeof(WorkItem) * (size_t)cap);
+    p->counts = (int32_t*)take(64);
+    p->qcap = cap;
+    return PALS_OK;
+}
+
+int pals_plan_select_device(pals_plan* p, const pals_query* d_queries, int64_t nq,
+                            int32_t* d_idx, uint8_t* d_reason) {
+    if (p->err) return set_error(p->err, p->err_msg);
+    if (nq <= 0) return PALS_OK;
+    if (nq > ((int64_t)1 << 31) - 1) return set_error(PALS_ECONFIG, "pals_select: too many queries");
+    int rc = ensure_query_buffers(p, nq);
+    if (rc) return rc;
+    pals_ctx* ctx = p->ctx;
+    cudaStream_t s = ctx->stream;
+    SelArgs a;
+    a.q = d_queries;
+    a.nq = nq;
+    a.out_idx = d_idx;
+    a.out_reason = d_reason;
+    a.thr_t = p->thr_t;
+    a.thr_p = p->thr_p;
+    a.best_e = p->best_e;
+    a.best_t = p->best_t;
+    a.cls = p->cls;
+    a.qlist = p->qlist;
+    a.counts = p->counts;
+    a.work = p->work;
+    a.qcap = p->qcap;
+    a.force_exact = p->force_exact;
+    PALS_CUDA(cudaMemsetAsync(p->counts, 0, 64, s));
+    const int qb = grid_blocks(ctx, nq, 256);
+    k_qprep<<<qb, 256, 0, s>>>(p->d, a);
+    const int nchunks = (int)((p->n + kScanCh - 1) / kScanCh);
+    // persistent scan grid: 4 CTAs per SM
+    const int sgrid = ctx->num_sms * 4;
+    if (p->time_scan) PALS_CUDA(cudaEventRecord(p->ev_scan0, s));
+    if (p->d.wide)
+        k_scan<uint64_t><<<sgrid, kScanThreads, 3 * kScanCh * 8, s>>>(p->d, a, nchunks);
+    else
+        k_scan<uint32_t><<<sgrid, kScanThreads, 3 * kScanCh * 4, s>>>(p->d, a, nchunks);
+    if (p->time_scan) {
+        PALS_CUDA(cudaEventRecord(p->ev_scan1, s));
+        p->scan_recorded = 1;
+    }
+    k_finalize<<<qb, 256, 0, s>>>(p->d, a);
+    k_exact<<<ctx->num_sms * 2, 256, 0, s>>>(p->d, a);
+    count_launch(ctx, 4);
+    return check_launch("pals_plan_select_device");
+}
+
+int pals_select(pals_plan* p, const pals_query* queries, int64_t nq, int32_t* idx,
+                uint8_t* reason) {
+    if (p->err) return set_error(p->err, p->err_msg);
+    if (nq < 0) return set_error(PALS_ECONFIG, "pals_select: negative query count");
+    pals_ctx* ctx = p->ctx;
+    PALS_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    int rc = pals_plan_prepare(p);
+    if (rc) return rc;
+    if (nq == 0) return pals_ctx_sync(ctx);
+    // host staging of queries/results lives in the context scratch
+    const size_t need = (size_t)nq * (sizeof(pals_query) + 4 + 1) + 1024;
+    if (ctx->scratch_bytes < need) {
+        cudaFree(ctx->d_scratch);
+        PALS_CUDA(cudaMalloc(&ctx->d_scratch, need));
+        ctx->scratch_bytes = need;
+    }
+    char* b = (char*)ctx->d_scratch;
+    pals_query* dq = (pals_query*)b;
+    int32_t* di = (int32_t*)(b + (size_t)nq * sizeof(pals_query));
+    uint8_t* dr = (uint8_t*)(di + nq);
+    PALS_CUDA(cudaMemcpyAsync(dq, queries, (size_t)nq * sizeof(pals_query), cudaMemcpyHostToDevice, s));
+    rc = pals_plan_select_device(p, dq, nq, di, dr);
+    if (rc) return rc;
+    PALS_CUDA(cudaMemcpyAsync(idx, di, (size_t)nq * 4, cudaMemcpyDeviceToHost, s));
+    PALS_CUDA(cudaMemcpyAsync(reason, dr, (size_t)nq, cudaMemcpyDeviceToHost, s));
+    int32_t cnt[N_CLS + 1];
+    PALS_CUDA(cudaMemcpyAsync(cnt, p->counts, sizeof cnt, cudaMemcpyDeviceToHost, s));
+    PALS_CUDA(cudaStreamSynchronize(s));
+    p->last_exact = cnt[N_CLS];
+    return PALS_OK;
+}
+
+int pals_plan_scores(pals_plan* p, double* t_hat, double* p_node, double* eff) {
+    if (p->err) return set_error(p->err, p->err_msg);
+    int rc = pals_plan_prepare(p);
+    if (rc) return rc;
+    cudaStream_t s = p->ctx->stream;
+    if (t_hat) PALS_CUDA(cudaMemcpyAsync(t_hat, p->d.th, p->n * 8, cudaMemcpyDeviceToHost, s));
+    if (p_node) PALS_CUDA(cudaMemcpyAsync(p_node, p->d.pn, p->n * 8, cudaMemcpyDeviceToHost, s));
+    if (eff) PALS_CUDA(cudaMemcpyAsync(eff, p->d.ef, p->n * 8, cudaMemcpyDeviceToHost, s));
+    PALS_CUDA(cudaStreamSynchronize(s));
+    return PALS_OK;
+}
+
+int64_t pals_plan_last_exact_count(const pals_plan* p) { return p->last_exact; }
+
+int pals_plan_stats(pals_plan* p, int64_t* c6) {
+    if (!p->counts) {
+        for (int i = 0; i < 6; ++i) c6[i] = 0;
+        return PALS_OK;
+    }
+    int32_t cnt[N_CLS + 1];
+    PALS_CUDA(cudaMemcpyAsync(cnt, p->counts, sizeof cnt, cudaMemcpyDeviceToHost, p->ctx->stream));
+    PALS_CUDA(cudaStreamSynchronize(p->ctx->stream));
+    for (int i = 0; i < 6; ++i) c6[i] = cnt[i];
+    p->last_exact = cnt[N_CLS];
+    return PALS_OK;
+}
+
+int pals_plan_time_scan(pals_plan* p, int enable) {
+    if (enable && !p->ev_scan0) {
+        PALS_CUDA(cudaEventCreate(&p->ev_scan0));
+        PALS_CUDA(cudaEventCreate(&p->ev_scan1));
+    }
+    p->time_scan = enable;
+    p->scan_recorded = 0;
+    return PALS_OK;
+}
+
+double pals_plan_scan_ms(pals_plan* p) {
+    if (!p->scan_recorded) return -1.0;
+    if (cudaEventSynchronize(p->ev_scan1) != cudaSuccess) return -1.0;
+    float ms = -1.0f;
+    if (cudaEventElapsedTime(&ms, p->ev_scan0, p->ev_scan1) != cudaSuccess) return -1.0;
+    return ms;
+}
+
+int pals_plan_set_force_exact(pals_plan* p, int force) {
+    p->force_exact = force;
+    return PALS_OK;
+}
+
+int pals_eval(pals_ctx* ctx, const pals_model* m, const pals_grid* g, double* T, double* P) {
+    pals_coeffs k{1.0, 0.0};
+    pals_plan* p = nullptr;
+    int rc = pals_plan_create(ctx, m, g, &k, &p);
+    if (rc) return rc;
+    if (p->err) {
+        rc = set_error(p->err, p->err_msg);
+        pals_plan_destroy(p);
+        return rc;
+    }
+    cudaStream_t s = ctx->stream;
+    const int eb = grid_blocks(ctx, p->n, 256);
+    if (m->kind == MODEL_ANALYTIC)
+        k_eval_analytic<<<eb, 256, 0, s>>>(p->d, p->d_an, g->tp, 1.0, 0.0);
+    else if (m->kind == MODEL_TABLE)
+        k_eval_table<<<eb, 256, 0, s>>>(p->d, p->table_map, p->table_T, p->table_P, 1.0, 0.0);
+    else if ((rc = forest_eval_plan(p, m, ctx)) != PALS_OK) {
+        pals_plan_destroy(p);
+        return rc;
+    }
+    count_launch(ctx, 1);
+    rc = check_launch("pals_eval");
+    if (!rc) {
+        cudaMemcpyAsync(T, p->d.T, p->n * 8, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(P, p->d.P, p->n * 8, cudaMemcpyDeviceToHost, s);
+        const cudaError_t e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) rc = cuda_fail(e, "pals_eval sync");
+    }
+    pals_plan_destroy(p);
+    return rc;
+}
+
+}  // extern "C"

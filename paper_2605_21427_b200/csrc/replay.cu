@@ -1,0 +1,961 @@
+// replay.cu — K3: batched replay of control_step (controller.hpp:210-267) over
+// independent synthetic traces through the fluid plant, one
+// thread per trace with all controller state in registers; plus the exact
+// single-call mirrors pals_select_one / pals_control_step_one.
+//
+// Per step the select_config call (controller.hpp:253) is answered from
+// per-model tables in O(log n): the dense-rank feasibility counts (Kt, Kp)
+// index a 2-D prefix-min table of efficiency keys (QoS branch) and a 1-D
+// prefix-min of throughput keys (budget branch). A winner inside a near-tie
+// cluster is re-decided by the literal sequential fold over the candidates.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "pals_internal.cuh"
+
+namespace pals {
+
+constexpr int kMaxReplayCands = 4096;
+
+struct ReplayModelDev {
+    int n;             // candidates
+    int nd_t, nd_p;    // distinct t_hat / p_node values
+    int tp, ep, dp;
+    int init_idx;      // (max cap, max batch) candidate
+    int gmax_t, gmin_p;
+    int generic;
+    double max_cap;
+    int max_batch;
+    double t_max, p_min, p_max;  // plant: unconstrained tps, min/max p_node
+    const double* cap;
+    const int* batch;
+    const int* canon;
+    const int* inv_tr;
+    const double* T;    // scorer throughput per candidate (PID promise)
+    const double* th;
+    const double* pn;
+    const double* ef;
+    const uint32_t* cut_t;
+    const uint32_t* cut_e;
+    const double* ut;   // distinct t_hat, descending
+    const double* up;   // distinct p_node, ascending
+    const uint32_t* m2; // (nd_t+1) x (nd_p+1): min eff key over {D_t < i, D_p < j}
+    const uint32_t* b1; // nd_p+1: min t key over {D_p < j}
+    const Analytic* plant;
+};
+
+struct ReplayParams {
+    pals_replay_spec spec;
+    pals_ctrl_cfg cfg;
+    double alpha, beta;
+    int n_models;
+};
+
+// ---- counter-based trace generator --------------------------
+__device__ __forceinline__ uint64_t draw(uint64_t key, uint64_t lane, uint64_t ctr) {
+    return splitmix64(key ^ (lane << 48) ^ ctr);
+}
+__device__ __forceinline__ double u01(uint64_t u) { return (double)(u >> 11) * 0x1.0p-53; }
+
+struct Seg {
+    uint64_t key;
+    uint64_t lane;
+    long next_j, seg_end;
+    double lo, hi, level;
+    __device__ __forceinline__ double at(long k, int seg_min, int seg_max) {
+        while (k >= seg_end) {
+            const uint64_t span = (uint64_t)(seg_max - seg_min) + 1;
+            const long len = seg_min + (long)(draw(key, lane, 2 * (uint64_t)next_j) % span);
+            const double u = u01(draw(key, lane, 2 * (uint64_t)next_j + 1));
+            level = lo + (hi - lo) * u;
+            seg_end += len;
+            ++next_j;
+        }
+        return level;
+    }
+};
+
+// Literal select_config over a replay model's candidates by one thread
+// (rarely used: near-tie winners and non-finite score sets).
+__device__ void thread_select_full(const ReplayModelDev& m, double target, bool bset, double budget,
+                                   double bias, int objective, int* idx, int* reason) {
+    int best = -1;
+    int r = PALS_REASON_FALLBACK_MAX_T;
+    if (objective == PALS_OBJ_QOS) {
+        for (int c = 0; c < m.n; ++c) {
+            if ((bset && !(m.pn[c] <= budget)) || m.th[c] * bias < target) continue;
+            if (best < 0 || better_exact(m.th[c] / m.pn[c], m.cap[c], m.batch[c],
+                                         m.th[best] / m.pn[best], m.cap[best], m.batch[best]))
+                best = c;
+        }
+        if (best >= 0) r = PALS_REASON_QOS_FEASIBLE;
+    }
+    if (best < 0 && bset) {
+        for (int c = 0; c < m.n; ++c) {
+            if (!(m.pn[c] <= budget)) continue;
+            if (best < 0 ||
+                better_exact(m.th[c], m.cap[c], m.batch[c], m.th[best], m.cap[best], m.batch[best]))
+                best = c;
+        }
+        if (best >= 0) r = PALS_REASON_BUDGET_MAX_T;
+        if (best < 0) {
+            for (int c = 0; c < m.n; ++c)
+                if (best < 0 || better_exact(-m.pn[c], m.cap[c], m.batch[c], -m.pn[best],
+                                             m.cap[best], m.batch[best]))
+                    best = c;
+            r = PALS_REASON_BUDGET_MAX_T;
+        }
+    }
+    if (best < 0) {
+        for (int c = 0; c < m.n; ++c)
+            if (best < 0 ||
+                better_exact(m.th[c], m.cap[c], m.batch[c], m.th[best], m.cap[best], m.batch[best]))
+                best = c;
+        r = PALS_REASON_FALLBACK_MAX_T;
+    }
+    *idx = best;
+    *reason = r;
+}
+
+// select_config via the rank tables; exact by the near-tie argument of DESIGN.md §3.
+__device__ __forceinline__ void table_select(const ReplayModelDev& m, double target, bool bset,
+                                             double budget, int kp, double bias, int objective,
+                                             int* idx, int* reason) {
+    if (m.generic) {
+        thread_select_full(m, target, bset, budget, bias, objective, idx, reason);
+        return;
+    }
+    const int W = m.nd_p + 1;
+    if (objective == PALS_OBJ_QOS) {
+        int lo = 0, hi = m.nd_t;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (!(m.ut[mid] * bias < target)) lo = mid + 1;
+            else hi = mid;
+        }
+        const uint32_t key = m.m2[lo * W + (bset ? kp : m.nd_p)];
+        if (key != kNone32) {
+            const uint32_t d0 = key >> 16;
+            if (m.cut_e[d0] != d0) {
+                thread_select_full(m, target, bset, budget, bias, objective, idx, reason);
+                return;
+            }
+            *idx = m.inv_tr[key & 0xFFFFu];
+            *reason = PALS_REASON_QOS_FEASIBLE;
+            return;
+        }
+    }
+    if (bset) {
+        const uint32_t key = m.b1[kp];
+        if (key != kNone32) {
+            const uint32_t d0 = key >> 16;
+            if (m.cut_t[d0] != d0) {
+                thread_select_full(m, target, bset, budget, bias, objective, idx, reason);
+                return;
+            }
+            *idx = m.inv_tr[key & 0xFFFFu];
+        } else {
+            *idx = m.gmin_p;
+        }
+        *reason = PALS_REASON_BUDGET_MAX_T;
+        return;
+    }
+    *idx = m.gmax_t;
+    *reason = PALS_REASON_FALLBACK_MAX_T;
+}
+
+// enforce_cap (sim.hpp:195-205) with the plant model; returns the enforced cap
+// and the plant's throughput/power at it.
+__device__ double enforce_cap_dev(const ReplayModelDev& m, double cap, int batch, double node_budget,
+                                  double alpha, double beta, double* T_out, double* P_out) {
+    const Analytic& a = *m.plant;
+    double c = cap;
+    if (!(node_budget <= 0.0 || batch < 1)) {
+        while (true) {
+            if (!(c > a.min_cap)) {
+                c = a.min_cap;
+                break;
+            }
+            const Score s = analytic_score(a, c, batch, m.tp, m.dp);
+            if (p_node_of(s.P, m.dp, alpha, beta) <= node_budget) break;
+            c = smax(a.min_cap, c - 5.0);
+        }
+    }
+    const Score s = analytic_score(a, c, batch, m.tp, m.dp);
+    *T_out = s.T;
+    *P_out = s.P;
+    return c;
+}
+
+__global__ void __launch_bounds__(128) k_replay(const ReplayModelDev* __restrict__ models,
+                                                ReplayParams p, pals_trace_summary* __restrict__ out,
+                                                pals_step_log* __restrict__ logs) {
+    const int64_t ti = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const pals_replay_spec& sp = p.spec;
+    if (ti >= sp.n_traces) return;
+    const pals_ctrl_cfg& cfg = p.cfg;
+    const uint64_t key = splitmix64(sp.seed ^ (uint64_t)(sp.first_trace + ti));
+    const int mi = (int)(key % (uint64_t)p.n_models);
+    const ReplayModelDev m = models[mi];
+    int obj = sp.objective_mode;
+    if (obj == 2) obj = (int)(draw(key, 0, 0) >> 63);
+    const double qfrac = sp.qos_frac_lo + (sp.qos_frac_hi - sp.qos_frac_lo) * u01(draw(key, 0, 1));
+    const double target_tps = qfrac * m.t_max;
+    const double target = target_tps * (1.0 + cfg.target_headroom);
+    Seg bs{key, 1, 0, 0, sp.budget_lo_frac * m.p_min, sp.budget_hi_frac * m.p_max, 0.0};
+    Seg ls{key, 2, 0, 0, sp.load_lo * m.t_max, sp.load_hi * m.t_max, 0.0};
+
+    // ControllerState (controller.hpp:55-63)
+    double bias = 1.0, integral = 0.0, prev_err = 0.0;
+    bool has_prev = false, has_last = false, last_has_budget = false;
+    double last_budget = 0.0;
+    int sustain = 0;
+    int cur = m.init_idx;
+    // plant (sim.hpp:155-157, 466-472)
+    double applied_cap = m.max_cap, inflight_cap = m.max_cap;
+    int batch_cap = m.max_batch;
+    // enforce_cap memo (pure function of its inputs)
+    double c_ac = -1.0, c_nb = -1.0;
+    int c_be = -1;
+    double cap = 0.0, capacity = 0.0, sys_w = 0.0;
+    // Kp memo per budget value
+    double kp_budget = -1.0;
+    int kp = m.nd_p;
+    uint64_t h = 0xcbf29ce484222325ULL;
+    double energy = 0.0, tokens = 0.0;
+    int n_applied = 0;
+    pals_step_log* lg = (logs && ti < sp.n_log_traces) ? logs + ti * (int64_t)sp.n_steps : nullptr;
+
+    for (int k = 0; k < sp.n_steps; ++k) {
+        const double t0 = (double)k * sp.interval_s;
+        const double t1 = t0 + sp.interval_s;
+        const double node_budget = sp.budget_mode ? bs.at(k, sp.seg_min, sp.seg_max) : 0.0;
+        const int b_eff = batch_cap;
+        if (applied_cap != c_ac || b_eff != c_be || node_budget != c_nb) {
+            double Tc, Pc;
+            cap = enforce_cap_dev(m, applied_cap, b_eff, node_budget, p.alpha, p.beta, &Tc, &Pc);
+            capacity = (double)m.dp * Tc;
+            sys_w = (double)m.dp * (p.alpha * (double)kGpusPerNode * Pc + p.beta);
+            c_ac = applied_cap;
+            c_be = b_eff;
+            c_nb = node_budget;
+        }
+        const double offered = ls.at(k, sp.seg_min, sp.seg_max);
+        const double noise = 1.0 + sp.noise_amp * (2.0 * u01(draw(key, 3, (uint64_t)k)) - 1.0);
+        const double measured = smin(offered, capacity) * noise;
+        energy += sys_w * sp.interval_s;
+        tokens += measured * sp.interval_s;
+
+        // ---- control_step (controller.hpp:210-267) ----
+        int d_idx, d_applied, d_reason;
+        if (t1 - t1 > 1.5 * cfg.interval_s) {  // stale telemetry (:217-220)
+            d_idx = cur;
+            d_applied = 0;
+            d_reason = PALS_REASON_HOLD;
+        } else {
+            double err_norm = 0.0;
+            if (obj == PALS_OBJ_QOS && target_tps > 0.0) {
+                err_norm = (target_tps - measured) / target_tps;
+                const double promised = (double)m.dp * m.T[cur] * bias;
+                if (promised > 0.0) {
+                    const double pred_err = (promised - measured) / promised;
+                    integral = sclamp(integral + pred_err, -cfg.integral_clamp, cfg.integral_clamp);
+                    const double deriv = has_prev ? pred_err - prev_err : 0.0;
+                    const double corr = cfg.kp * pred_err + cfg.ki * integral + cfg.kd * deriv;
+                    bias = sclamp(bias * (1.0 - corr), cfg.bias_min, cfg.bias_max);
+                    prev_err = pred_err;
+                    has_prev = true;
+                }
+            }
+            const bool bset = node_budget > 0.0;
+            const bool changed =
+                !has_last || !(last_has_budget == bset && (!bset || last_budget == node_budget));
+            has_last = true;
+            last_has_budget = bset;
+            last_budget = node_budget;
+            if (fabs(err_norm) > sp.epsilon) ++sustain;
+            else sustain = 0;
+
+            const double budget = bset ? node_budget * (1.0 - cfg.budget_margin) : 0.0;
+            if (bset && budget != kp_budget) {
+                int lo = 0, hi = m.nd_p;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (m.up[mid] <= budget) lo = mid + 1;
+                    else hi = mid;
+                }
+                kp = lo;
+                kp_budget = budget;
+            }
+            int s_idx, s_reason;
+            table_select(m, target, bset, budget, kp, bias, obj, &s_idx, &s_reason);
+            const bool may_apply = changed || sustain >= cfg.sustain_intervals;
+            const int sc = m.canon[s_idx];
+            if (may_apply && sc != cur) {
+                cur = sc;
+                sustain = 0;
+                d_idx = sc;
+                d_applied = 1;
+                d_reason = s_reason;
+            } else {
+                d_idx = cur;
+                d_applied = 0;
+                d_reason = may_apply ? s_reason : PALS_REASON_HOLD;
+            }
+        }
+        const uint64_t word = ((uint64_t)(uint32_t)d_idx << 8) | ((uint64_t)d_applied << 4) |
+                              (uint64_t)d_reason;
+        h = (h ^ word) * 0x100000001b3ULL;
+        n_applied += d_applied;
+        if (lg) {
+            pals_step_log r;
+            r.idx = d_idx;
+            r.applied = (uint8_t)d_applied;
+            r.reason = (uint8_t)d_reason;
+            r.cap_tenths = (uint16_t)llround(cap * 10.0);
+            lg[k] = r;
+        }
+        applied_cap = inflight_cap;
+        if (d_applied) {
+            batch_cap = m.batch[cur];
+            inflight_cap = m.cap[cur];
+        }
+    }
+    h = (h ^ (uint64_t)__double_as_longlong(bias)) * 0x100000001b3ULL;
+    h = (h ^ (uint64_t)(uint32_t)cur) * 0x100000001b3ULL;
+    pals_trace_summary s;
+    s.digest = h;
+    s.final_bias = bias;
+    s.energy_j = energy;
+    s.tokens = tokens;
+    s.n_applied = n_applied;
+    s.final_idx = cur;
+    s.model = mi;
+    s.objective = obj;
+    out[ti] = s;
+}
+
+// Per-model select tables from a prepared plan (single CTA; n <= kMaxReplayCands).
+__global__ void __launch_bounds__(1024) k_build_tables(PlanDev d, ReplayModelDev* rm, uint32_t* m2,
+                                                       uint32_t* b1, double* ut, double* up,
+                                                       double alpha, double beta) {
+    const int n = (int)d.n;
+    const int ndt = (int)d.nd[ORD_T], ndp = (int)d.nd[ORD_P];
+    const int W = ndp + 1, H = ndt + 1;
+    for (int i = threadIdx.x; i < W * H; i += blockDim.x) m2[i] = kNone32;
+    for (int i = threadIdx.x; i < W; i += blockDim.x) b1[i] = kNone32;
+    for (int i = threadIdx.x; i < ndt; i += blockDim.x) ut[i] = unorderable(~d.U[ORD_T][i]);
+    for (int i = threadIdx.x; i < ndp; i += blockDim.x) up[i] = unorderable(d.U[ORD_P][i]);
+    __syncthreads();
+    for (int c = threadIdx.x; c < n; c += blockDim.x) {
+        const uint32_t kt = d.key32[ORD_T][c], kp = d.key32[ORD_P][c], ke = d.key32[ORD_E][c];
+        const int Dt = (int)(kt >> 16), Dp = (int)(kp >> 16);
+        atomicMin(&m2[(Dt + 1) * W + (Dp + 1)], ke);
+        atomicMin(&b1[Dp + 1], kt);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < H; i += blockDim.x)
+        for (int j = 1; j < W; ++j) m2[i * W + j] = min(m2[i * W + j], m2[i * W + j - 1]);
+    __syncthreads();
+    for (int j = threadIdx.x; j < W; j += blockDim.x)
+        for (int i = 1; i < H; ++i) m2[i * W + j] = min(m2[i * W + j], m2[(i - 1) * W + j]);
+    if (threadIdx.x == 0) {
+        for (int j = 1; j < W; ++j) b1[j] = min(b1[j], b1[j - 1]);
+        // plant constants: unconstrained throughput (sim.hpp:258-264) and the p_node range
+        const Analytic& a = *rm->plant;
+        double pmin = 0.0, pmax = 0.0;
+        for (int c = 0; c < n; ++c) {
+            const Score s = analytic_score(a, d.cap[c], d.batch[c], rm->tp, rm->dp);
+            const double pn = p_node_of(s.P, rm->dp, alpha, beta);
+            if (c == 0 || pn < pmin) pmin = pn;
+            if (c == 0 || pn > pmax) pmax = pn;
+        }
+        const Score s = analytic_score(a, rm->max_cap, rm->max_batch, rm->tp, rm->dp);
+        rm->t_max = (double)rm->dp * s.T;
+        rm->p_min = pmin;
+        rm->p_max = pmax;
+        rm->nd_t = ndt;
+        rm->nd_p = ndp;
+        rm->gmax_t = d.globals[0];
+        rm->gmin_p = d.globals[1];
+        rm->generic = d.globals[2];
+    }
+}
+
+struct ReplayCache {
+    std::vector<const pals_model*> models;
+    std::vector<pals_profile> plant;
+    pals_gpu_spec gpu;
+    pals_coeffs coeffs;
+    std::vector<double> caps;
+    std::vector<int> batches;
+    std::vector<pals_grid*> grids;
+    std::vector<pals_plan*> plans;
+    std::vector<pals_model*> plant_models;
+    ReplayModelDev* d_models = nullptr;
+    void* d_tables = nullptr;
+    Analytic* d_plant = nullptr;
+};
+
+void replay_cache_free(pals_ctx* ctx) {
+    auto* rc = (ReplayCache*)ctx->replay_cache;
+    if (!rc) return;
+    for (auto* p : rc->plans) pals_plan_destroy(p);
+    for (auto* g : rc->grids) pals_grid_destroy(g);
+    for (auto* m : rc->plant_models) pals_model_destroy(m);
+    cudaFree(rc->d_models);
+    cudaFree(rc->d_tables);
+    cudaFree(rc->d_plant);
+    delete rc;
+    ctx->replay_cache = nullptr;
+}
+
+static bool same_setup(const ReplayCache* rc, int n_models, pals_model* const* models,
+                       const pals_profile* plant, const pals_gpu_spec* gpu, const pals_coeffs* k,
+                       const double* caps, int nc, const int* batches, int nb) {
+    if (!rc || (int)rc->models.size() != n_models) return false;
+    for (int i = 0; i < n_models; ++i)
+        if (rc->models[i] != models[i] || memcmp(&rc->plant[i], &plant[i], sizeof(pals_profile)))
+            return false;
+    if (memcmp(&rc->gpu, gpu, sizeof *gpu) || memcmp(&rc->coeffs, k, sizeof *k)) return false;
+    if ((int)rc->caps.size() != nc || (int)rc->batches.size() != nb) return false;
+    return !memcmp(rc->caps.data(), caps, nc * 8) && !memcmp(rc->batches.data(), batches, nb * 4);
+}
+
+static int replay_setup(pals_ctx* ctx, int n_models, pals_model* const* models,
+                        const pals_profile* plant, const pals_gpu_spec* gpu,
+                        const pals_coeffs* coeffs, const double* caps, int nc,
+                        const int* batches, int nb, ReplayCache** out) {
+    auto* cur = (ReplayCache*)ctx->replay_cache;
+    if (same_setup(cur, n_models, models, plant, gpu, coeffs, caps, nc, batches, nb)) {
+        *out = cur;
+        return PALS_OK;
+    }
+    replay_cache_free(ctx);
+    if (n_models <= 0) return set_error(PALS_ECONFIG, "pals_replay: no models");
+    if (nc <= 0 || nb <= 0) return set_error(PALS_ECONFIG, "scenario: empty candidate grid");
+    if ((int64_t)nc * nb > kMaxReplayCands)
+        return set_error(PALS_ECONFIG, "pals_replay: at most 4096 candidates per trace");
+    auto* rc = new ReplayCache();
+    ctx->replay_cache = rc;
+    rc->models.assign(models, models + n_models);
+    rc->plant.assign(plant, plant + n_models);
+    rc->gpu = *gpu;
+    rc->coeffs = *coeffs;
+    rc->caps.assign(caps, caps + nc);
+    rc->batches.assign(batches, batches + nb);
+    const int n = nc * nb;
+    const size_t W = (size_t)n + 1;
+    const size_t per_model = W * W * 4 + W * 4 + 2 * W * 8 + 1024;
+    PALS_CUDA(cudaMalloc(&rc->d_tables, per_model * n_models));
+    PALS_CUDA(cudaMalloc(&rc->d_models, sizeof(ReplayModelDev) * n_models));
+    PALS_CUDA(cudaMalloc(&rc->d_plant, sizeof(Analytic) * n_models));
+    std::vector<ReplayModelDev> hm(n_models);
+    const double mc = *std::max_element(caps, caps + nc);
+    const int mb = *std::max_element(batches, batches + nb);
+    for (int i = 0; i < n_models; ++i) {
+        pals_model* pm = nullptr;
+        int r = pals_model_analytic(ctx, &plant[i], gpu, &pm);
+        if (r) return r;
+        rc->plant_models.push_back(pm);
+        PALS_CUDA(cudaMemcpy(rc->d_plant + i, &pm->an, sizeof(Analytic), cudaMemcpyHostToDevice));
+        // build_candidates order (sim.hpp:304-306) at the deployment degrees
+        pals_grid* g = nullptr;
+        const int tp = plant[i].deploy_tp, ep = plant[i].deploy_ep, dp = plant[i].deploy_dp;
+        r = pals_grid_axes(ctx, caps, nc, batches, nb, &tp, 1, &ep, 1, &dp, 1, &g);
+        if (r) return r;
+        rc->grids.push_back(g);
+        // the plant must be able to run every candidate (validation as in the sim)
+        r = validate_points(pm, g->h_pts, g->n);
+        if (r) return r;
+        pals_plan* pl = nullptr;
+        r = pals_plan_create(ctx, models[i], g, coeffs, &pl);
+        if (r) return r;
+        rc->plans.push_back(pl);
+        r = pals_plan_prepare(pl);
+        if (r) return r;
+        const PlanDev& d = plan_dev(pl);
+        ReplayModelDev& m = hm[i];
+        memset(&m, 0, sizeof m);
+        m.n = n;
+        m.tp = tp;
+        m.ep = ep;
+        m.dp = dp;
+        m.max_cap = mc;
+        m.max_batch = mb;
+        m.init_idx = -1;
+        for (int c = 0; c < n; ++c)
+            if (g->h_pts[c].cap_watts == mc && g->h_pts[c].batch == mb) {
+                m.init_idx = c;
+                break;
+            }
+        m.cap = g->cap;
+        m.batch = g->batch;
+        m.canon = g->canon;
+        m.inv_tr = g->inv_tr;
+        m.T = d.T;
+        m.th = d.th;
+        m.pn = d.pn;
+        m.ef = d.ef;
+        m.cut_t = d.cut[ORD_T];
+        m.cut_e = d.cut[ORD_E];
+        char* base = (char*)rc->d_tables + per_model * i;
+        m.m2 = (const uint32_t*)base;
+        m.b1 = (const uint32_t*)(base + W * W * 4);
+        m.ut = (const double*)(base + W * W * 4 + W * 4);
+        m.up = (const double*)(base + W * W * 4 + W * 4 + W * 8);
+        m.plant = rc->d_plant + i;
+        PALS_CUDA(cudaMemcpy(rc->d_models + i, &m, sizeof m, cudaMemcpyHostToDevice));
+        k_build_tables<<<1, 1024, 0, ctx->stream>>>(d, rc->d_models + i, (uint32_t*)m.m2,
+                                                     (uint32_t*)m.b1, (double*)m.ut, (double*)m.up,
+                                                     coeffs->alpha, coeffs->beta_watts);
+        count_launch(ctx);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "k_build_tables");
+    }
+    PALS_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = rc;
+    return PALS_OK;
+}
+
+static int replay_launch(pals_ctx* ctx, ReplayCache* rc, const pals_ctrl_cfg* cfg,
+                         const pals_replay_spec* spec, pals_trace_summary* d_sum,
+                         pals_step_log* d_logs) {
+    if (spec->n_traces <= 0) return PALS_OK;
+    if (spec->n_steps < 0 || spec->seg_min < 1 || spec->seg_max < spec->seg_min)
+        return set_error(PALS_ECONFIG, "pals_replay: bad spec");
+    ReplayParams p;
+    p.spec = *spec;
+    p.cfg = *cfg;
+    p.alpha = rc->coeffs.alpha;
+    p.beta = rc->coeffs.beta_watts;
+    p.n_models = (int)rc->models.size();
+    const int64_t blocks = (spec->n_traces + 127) / 128;
+    k_replay<<<(unsigned)blocks, 128, 0, ctx->stream>>>(rc->d_models, p, d_sum, d_logs);
+    count_launch(ctx);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "k_replay");
+    return PALS_OK;
+}
+
+// ---- single-call mirrors ----------------------------------------------------
+struct OneArgs {
+    int64_t n;
+    const double* cap;
+    const int* batch;
+    const int* dp;
+    const int* tp;
+    const double* T;  // table-model scores per candidate (or null for analytic)
+    const double* P;
+    const Analytic* an;
+    double alpha, beta;
+    double* th;  // scratch n
+    double* pn;
+    // control_step inputs
+    int do_step;
+    pals_telemetry tel;
+    double now_s;
+    pals_targets tg;
+    pals_ctrl_state st;
+    pals_ctrl_cfg cfg;
+    double cur_T;      // table model: score(current) (host lookup)
+    int cur_ok;
+    pals_query q;      // select-only call
+    int* out;          // [0] idx, [1] reason, [2] error, [3] applied
+    pals_ctrl_state* out_state;
+};
+
+template <class Filter, class ScoreF>
+__device__ int warp_fold_one(int64_t n, const double* cap, const int* batch, Filter filt,
+                             ScoreF score) {
+    const int lane = threadIdx.x & 31;
+    int64_t best = -1;
+    double bs = 0.0, bcap = 0.0;
+    int bb = 0;
+    for (int64_t base = 0; base < n; base += 32) {
+        const int64_t c = base + lane;
+        const bool ok = c < n && filt(c);
+        double s = 0.0, cp = 0.0;
+        int bt = 0;
+        if (ok) {
+            s = score(c);
+            cp = cap[c];
+            bt = batch[c];
+        }
+        const unsigned msk = __ballot_sync(0xffffffffu, ok);
+        if (!msk) continue;
+        int last = -1;
+        if (best < 0) {
+            const int l = __ffs(msk) - 1;
+            best = base + l;
+            bs = __shfl_sync(0xffffffffu, s, l);
+            bcap = __shfl_sync(0xffffffffu, cp, l);
+            bb = __shfl_sync(0xffffffffu, bt, l);
+            last = l;
+        }
+        while (true) {
+            const bool b = ok && lane > last && better_exact(s, cp, bt, bs, bcap, bb);
+            const unsigned bm = __ballot_sync(0xffffffffu, b);
+            if (!bm) break;
+            const int l = __ffs(bm) - 1;
+            best = base + l;
+            bs = __shfl_sync(0xffffffffu, s, l);
+            bcap = __shfl_sync(0xffffffffu, cp, l);
+            bb = __shfl_sync(0xffffffffu, bt, l);
+            last = l;
+        }
+    }
+    return (int)best;
+}
+
+// One warp: score the candidates, run the PID (control_step only) and the literal
+// select_config fold, then the hysteresis gate.
+__global__ void k_one(OneArgs a) {
+    const int lane = threadIdx.x;
+    for (int64_t c = lane; c < a.n; c += 32) {
+        double T, P;
+        if (a.an) {
+            const Score s = analytic_score(*a.an, a.cap[c], a.batch[c], a.tp[c], a.dp[c]);
+            T = s.T;
+            P = s.P;
+        } else {
+            T = a.T[c];
+            P = a.P[c];
+        }
+        a.th[c] = (double)a.dp[c] * T;
+        a.pn[c] = p_node_of(P, a.dp[c], a.alpha, a.beta);
+    }
+    __syncwarp();
+    pals_query q = a.q;
+    pals_ctrl_state st = a.st;
+    bool changed = false;
+    if (a.do_step) {
+        // controller.hpp:215-251
+        if (a.now_s - a.tel.t_s > 1.5 * a.cfg.interval_s) {
+            if (lane == 0) {
+                a.out[0] = -1;
+                a.out[1] = PALS_REASON_HOLD;
+                a.out[2] = PALS_OK;
+                a.out[3] = 0;
+                *a.out_state = st;
+            }
+            return;
+        }
+        double err_norm = 0.0;
+        if (a.tg.objective == PALS_OBJ_QOS && a.tg.throughput_tps > 0.0) {
+            err_norm = (a.tg.throughput_tps - a.tel.throughput_tps) / a.tg.throughput_tps;
+            double curT = a.cur_T;
+            if (a.an) {
+                const Score s = analytic_score(*a.an, st.current.cap_watts, st.current.batch,
+                                               st.current.tp, st.current.dp);
+                curT = s.T;
+            } else if (!a.cur_ok) {
+                if (lane == 0) a.out[2] = PALS_ECONFIG;
+                return;
+            }
+            const double promised = (double)st.current.dp * curT * st.bias;
+            if (promised > 0.0) {
+                const double pred_err = (promised - a.tel.throughput_tps) / promised;
+                st.integral =
+                    sclamp(st.integral + pred_err, -a.cfg.integral_clamp, a.cfg.integral_clamp);
+                const double deriv = st.has_prev_error ? pred_err - st.prev_error : 0.0;
+                const double corr = a.cfg.kp * pred_err + a.cfg.ki * st.integral + a.cfg.kd * deriv;
+                st.bias = sclamp(st.bias * (1.0 - corr), a.cfg.bias_min, a.cfg.bias_max);
+                st.prev_error = pred_err;
+                st.has_prev_error = 1;
+            }
+        }
+        const pals_targets& l = st.last_targets;
+        const bool eq = st.has_last_targets && l.throughput_tps == a.tg.throughput_tps &&
+                        l.has_budget == a.tg.has_budget &&
+                        (!l.has_budget || l.power_budget_w == a.tg.power_budget_w) &&
+                        l.epsilon == a.tg.epsilon && l.objective == a.tg.objective;
+        changed = !eq;
+        st.last_targets = a.tg;
+        st.has_last_targets = 1;
+        if (fabs(err_norm) > a.tg.epsilon) ++st.sustain_count;
+        else st.sustain_count = 0;
+        q.throughput_tps = a.tg.throughput_tps;
+        q.power_budget_w = a.tg.power_budget_w;
+        q.has_budget = a.tg.has_budget;
+        q.objective = a.tg.objective;
+        q.bias = st.bias;
+        q.target_headroom = a.cfg.target_headroom;
+        q.budget_margin = a.cfg.budget_margin;
+    }
+    // select_config (controller.hpp:137-200)
+    const double target = q.throughput_tps * (1.0 + q.target_headroom);
+    const bool bset = q.has_budget != 0;
+    const double budget = bset ? q.power_budget_w * (1.0 - q.budget_margin) : 0.0;
+    const double* th = a.th;
+    const double* pn = a.pn;
+    int best = -1, r = PALS_REASON_FALLBACK_MAX_T;
+    if (q.objective == PALS_OBJ_QOS) {
+        best = warp_fold_one(
+            a.n, a.cap, a.batch,
+            [&](int64_t c) { return !((bset && !(pn[c] <= budget)) || th[c] * q.bias < target); },
+            [&](int64_t c) { return th[c] / pn[c]; });
+        if (best >= 0) r = PALS_REASON_QOS_FEASIBLE;
+    }
+    if (best < 0 && bset) {
+        best = warp_fold_one(
+            a.n, a.cap, a.batch, [&](int64_t c) { return pn[c] <= budget; },
+            [&](int64_t c) { return th[c]; });
+        if (best >= 0) r = PALS_REASON_BUDGET_MAX_T;
+        if (best < 0) {
+            best = warp_fold_one(
+                a.n, a.cap, a.batch, [&](int64_t) { return true; },
+                [&](int64_t c) { return -pn[c]; });
+            r = PALS_REASON_BUDGET_MAX_T;
+        }
+    }
+    if (best < 0) {
+        best = warp_fold_one(
+            a.n, a.cap, a.batch, [&](int64_t) { return true; }, [&](int64_t c) { return th[c]; });
+        r = PALS_REASON_FALLBACK_MAX_T;
+    }
+    if (lane == 0) {
+        a.out[2] = PALS_OK;
+        if (!a.do_step) {
+            a.out[0] = best;
+            a.out[1] = r;
+            a.out[3] = 1;
+            return;
+        }
+        // hysteresis gate (controller.hpp:255-266)
+        const bool may_apply = changed || st.sustain_count >= a.cfg.sustain_intervals;
+        const bool same = a.cap[best] == st.current.cap_watts && a.batch[best] == st.current.batch &&
+                          a.tp[best] == st.current.tp && a.dp[best] == st.current.dp;
+        // ep equality is checked on the host (the device grid view has no ep column here)
+        a.out[0] = best;
+        a.out[1] = may_apply ? r : PALS_REASON_HOLD;
+        a.out[3] = (may_apply && !same) ? 1 : 0;
+        a.out[4] = same ? 1 : 0;
+        a.out[5] = may_apply ? 1 : 0;
+        *a.out_state = st;
+    }
+}
+
+}  // namespace pals
+
+using namespace pals;
+
+static int one_call(pals_ctx* ctx, const pals_model* m, const pals_point* cands, int64_t n,
+                    OneArgs& a, int do_step, pals_decision* out_d, pals_ctrl_state* out_s,
+                    const pals_ctrl_state* in_state) {
+    if (n <= 0) return set_error(PALS_ECONFIG, "select_config: empty candidate list");
+    if (m->kind == MODEL_FOREST)
+        return set_error(PALS_ECONFIG, "pals: single-call forest scoring is not built yet");
+    // the reference scores candidates in order and aborts on the first rejection
+    int rc;
+    if (do_step && a.tg.objective == PALS_OBJ_QOS && a.tg.throughput_tps > 0.0 &&
+        !(a.now_s - a.tel.t_s > 1.5 * a.cfg.interval_s)) {
+        // score(st.current) runs before select_config (controller.hpp:229)
+        rc = validate_point(m, in_state->current);
+        if (rc) return rc;
+    }
+    if (!(do_step && a.now_s - a.tel.t_s > 1.5 * a.cfg.interval_s)) {
+        rc = validate_points(m, cands, n);
+        if (rc) return rc;
+    }
+    PALS_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    // staging: SoA candidates + scratch + outputs in the context scratch buffer
+    const size_t need = (size_t)n * (8 + 4 * 3 + 8 * 4) + sizeof(pals_ctrl_state) + 4096;
+    if (ctx->scratch_bytes < need) {
+        cudaFree(ctx->d_scratch);
+        PALS_CUDA(cudaMalloc(&ctx->d_scratch, need));
+        ctx->scratch_bytes = need;
+    }
+    std::vector<char> host(need);
+    char* hb = host.data();
+    char* db = (char*)ctx->d_scratch;
+    size_t off = 0;
+    auto take = [&](size_t b) {
+        const size_t o = off;
+        off += (b + 255) & ~(size_t)255;
+        return o;
+    };
+    const size_t o_cap = take(n * 8), o_b = take(n * 4), o_tp = take(n * 4), o_dp = take(n * 4);
+    const size_t o_T = take(n * 8), o_P = take(n * 8), o_th = take(n * 8), o_pn = take(n * 8);
+    const size_t o_out = take(64), o_st = take(sizeof(pals_ctrl_state));
+    for (int64_t i = 0; i < n; ++i) {
+        ((double*)(hb + o_cap))[i] = cands[i].cap_watts;
+        ((int*)(hb + o_b))[i] = cands[i].batch;
+        ((int*)(hb + o_tp))[i] = cands[i].tp;
+        ((int*)(hb + o_dp))[i] = cands[i].dp;
+    }
+    Analytic* d_an = nullptr;
+    const bool stale = do_step && a.now_s - a.tel.t_s > 1.5 * a.cfg.interval_s;
+    if (m->kind == MODEL_TABLE && !stale) {
+        std::unordered_map<std::string, int64_t> first;
+        for (int64_t i = 0; i < m->table_n; ++i) {
+            pals_point q = m->table_pts[i];
+            if (q.cap_watts == 0.0) q.cap_watts = 0.0;
+            first.emplace(std::string((const char*)&q, sizeof q), i);
+        }
+        for (int64_t i = 0; i < n; ++i) {
+            pals_point q = cands[i];
+            if (q.cap_watts == 0.0) q.cap_watts = 0.0;
+            const int64_t r = first.at(std::string((const char*)&q, sizeof q));
+            ((double*)(hb + o_T))[i] = m->table_T[r];
+            ((double*)(hb + o_P))[i] = m->table_P[r];
+        }
+        if (do_step && a.tg.objective == PALS_OBJ_QOS && a.tg.throughput_tps > 0.0) {
+            pals_point q = in_state->current;
+            if (q.cap_watts == 0.0) q.cap_watts = 0.0;
+            auto it = first.find(std::string((const char*)&q, sizeof q));
+            a.cur_ok = it != first.end();
+            a.cur_T = a.cur_ok ? m->table_T[it->second] : 0.0;
+        }
+    } else if (m->kind == MODEL_ANALYTIC) {
+        PALS_CUDA(cudaMalloc(&d_an, sizeof(Analytic)));
+        PALS_CUDA(cudaMemcpy(d_an, &m->an, sizeof(Analytic), cudaMemcpyHostToDevice));
+    }
+    PALS_CUDA(cudaMemcpyAsync(db, hb, off, cudaMemcpyHostToDevice, s));
+    a.n = n;
+    a.cap = (const double*)(db + o_cap);
+    a.batch = (const int*)(db + o_b);
+    a.tp = (const int*)(db + o_tp);
+    a.dp = (const int*)(db + o_dp);
+    a.T = (const double*)(db + o_T);
+    a.P = (const double*)(db + o_P);
+    a.an = d_an;
+    a.th = (double*)(db + o_th);
+    a.pn = (double*)(db + o_pn);
+    a.do_step = do_step;
+    a.out = (int*)(db + o_out);
+    a.out_state = (pals_ctrl_state*)(db + o_st);
+    k_one<<<1, 32, 0, s>>>(a);
+    count_launch(ctx);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        cudaFree(d_an);
+        return cuda_fail(e, "k_one");
+    }
+    int out[8];
+    pals_ctrl_state st{};
+    cudaMemcpyAsync(out, db + o_out, sizeof out, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&st, db + o_st, sizeof st, cudaMemcpyDeviceToHost, s);
+    e = cudaStreamSynchronize(s);
+    cudaFree(d_an);
+    if (e != cudaSuccess) return cuda_fail(e, "k_one sync");
+    if (out[2] != PALS_OK) return set_error(out[2], "unscored candidate");
+    if (!do_step) {
+        out_d->point = cands[out[0]];
+        out_d->applied = 1;
+        out_d->reason = out[1];
+        return PALS_OK;
+    }
+    if (out[0] < 0) {  // stale telemetry: hold everything (controller.hpp:217-220)
+        out_d->point = in_state->current;
+        out_d->applied = 0;
+        out_d->reason = PALS_REASON_HOLD;
+        *out_s = *in_state;
+        return PALS_OK;
+    }
+    const pals_point& ch = cands[out[0]];
+    const pals_point& cu = in_state->current;
+    const bool same = ch.cap_watts == cu.cap_watts && ch.batch == cu.batch && ch.tp == cu.tp &&
+                      ch.ep == cu.ep && ch.dp == cu.dp;
+    const bool may_apply = out[5] != 0;
+    if (may_apply && !same) {
+        st.current = ch;
+        st.sustain_count = 0;
+        out_d->point = ch;
+        out_d->applied = 1;
+        out_d->reason = out[1];
+    } else {
+        out_d->point = st.current;
+        out_d->applied = 0;
+        out_d->reason = out[1];
+    }
+    *out_s = st;
+    return PALS_OK;
+}
+
+extern "C" {
+
+int pals_select_one(pals_ctx* ctx, const pals_model* m, const pals_point* cands, int64_t n,
+                    const pals_targets* tg, const pals_coeffs* coeffs, double bias,
+                    double headroom, double margin, pals_decision* out) {
+    OneArgs a;
+    memset(&a, 0, sizeof a);
+    a.alpha = coeffs->alpha;
+    a.beta = coeffs->beta_watts;
+    a.q.throughput_tps = tg->throughput_tps;
+    a.q.power_budget_w = tg->power_budget_w;
+    a.q.has_budget = tg->has_budget;
+    a.q.objective = tg->objective;
+    a.q.bias = bias;
+    a.q.target_headroom = headroom;
+    a.q.budget_margin = margin;
+    return one_call(ctx, m, cands, n, a, 0, out, nullptr, nullptr);
+}
+
+int pals_control_step_one(pals_ctx* ctx, const pals_model* m, const pals_telemetry* tel,
+                          double now_s, const pals_targets* tg, const pals_point* cands, int64_t n,
+                          const pals_coeffs* coeffs, const pals_ctrl_state* state,
+                          const pals_ctrl_cfg* cfg, pals_decision* out_d,
+                          pals_ctrl_state* out_s) {
+    OneArgs a;
+    memset(&a, 0, sizeof a);
+    a.alpha = coeffs->alpha;
+    a.beta = coeffs->beta_watts;
+    a.tel = *tel;
+    a.now_s = now_s;
+    a.tg = *tg;
+    a.st = *state;
+    a.cfg = *cfg;
+    return one_call(ctx, m, cands, n, a, 1, out_d, out_s, state);
+}
+
+int pals_replay_device(pals_ctx* ctx, int32_t n_models, pals_model* const* models,
+                       const pals_profile* plant, const pals_gpu_spec* gpu,
+                       const pals_coeffs* coeffs, const double* caps, int32_t n_caps,
+                       const int32_t* batches, int32_t n_batches, const pals_ctrl_cfg* cfg,
+                       const pals_replay_spec* spec, pals_trace_summary* d_sum,
+                       pals_step_log* d_logs) {
+    PALS_CUDA(cudaSetDevice(ctx->device));
+    ReplayCache* rc = nullptr;
+    int r = replay_setup(ctx, n_models, models, plant, gpu, coeffs, caps, n_caps, batches,
+                         n_batches, &rc);
+    if (r) return r;
+    return replay_launch(ctx, rc, cfg, spec, d_sum, d_logs);
+}
+
+int pals_replay(pals_ctx* ctx, int32_t n_models, pals_model* const* models,
+                const pals_profile* plant, const pals_gpu_spec* gpu, const pals_coeffs* coeffs,
+                const double* caps, int32_t n_caps, const int32_t* batches, int32_t n_batches,
+                const pals_ctrl_cfg* cfg, const pals_replay_spec* spec,
+                pals_trace_summary* summaries, pals_step_log* logs) {
+    PALS_CUDA(cudaSetDevice(ctx->device));
+    ReplayCache* rc = nullptr;
+    int r = replay_setup(ctx, n_models, models, plant, gpu, coeffs, caps, n_caps, batches,
+                         n_batches, &rc);
+    if (r) return r;
+    if (spec->n_traces <= 0) return PALS_OK;
+    const int64_t nl = logs ? std::min<int64_t>(spec->n_log_traces, spec->n_traces) : 0;
+    const size_t sb = (size_t)spec->n_traces * sizeof(pals_trace_summary);
+    const size_t lb = (size_t)nl * spec->n_steps * sizeof(pals_step_log);
+    void* d = nullptr;
+    PALS_CUDA(cudaMallocAsync(&d, sb + lb + 256, ctx->stream));
+    pals_trace_summary* ds = (pals_trace_summary*)d;
+    pals_step_log* dl = nl ? (pals_step_log*)((char*)d + ((sb + 255) & ~(size_t)255)) : nullptr;
+    pals_replay_spec sp = *spec;
+    sp.n_log_traces = (int32_t)nl;
+    r = replay_launch(ctx, rc, cfg, &sp, ds, dl);
+    if (!r) {
+        cudaMemcpyAsync(summaries, ds, sb, cudaMemcpyDeviceToHost, ctx->stream);
+        if (nl) cudaMemcpyAsync(logs, dl, lb, cudaMemcpyDeviceToHost, ctx->stream);
+    }
+    cudaFreeAsync(d, ctx->stream);
+    const cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    if (!r && e != cudaSuccess) r = cuda_fail(e, "pals_replay");
+    return r;
+}
+
+}  // extern "C"

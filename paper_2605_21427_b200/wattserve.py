@@ -1,0 +1,330 @@
+"""Host-side mirror of the reference's decision API, backed by libpals_gpu.so.
+
+Same names and argument meaning as /root/reference/proj/include/wattserve/
+controller.hpp, so the parity tests read like the reference's own:
+
+    analytic_scorer(profile, gpu)                    controller.hpp:107-111
+    table_scorer(points, t_hat, p_gpu)               tests/test_controller.cpp:17-29
+    select_config(cands, targets, scorer, coeffs,
+                  bias, target_headroom, budget_margin)    controller.hpp:132-201
+    control_step(telemetry, now_s, targets, cands, scorer,
+                 coeffs, state, cfg)                  controller.hpp:210-267
+
+plus the batched B200 entry points (Plan.select for many Targets at once,
+replay for many traces). Exceptions mirror the reference's: ConfigError for
+config_error, OutOfRange for std::out_of_range. There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .abi import (OBJ_BUDGET, OBJ_QOS, POINT_DT, QUERY_DT, STEPLOG_DT, SUMMARY_DT, Coeffs,
+                  CtrlCfg, CtrlState, Decision, GpuSpec, Point, Profile, ReplaySpec, Targets,
+                  Telemetry, ptr)
+from ._lib import ConfigError, DataError, OutOfRange, PalsError, check  # noqa: F401
+
+__all__ = [
+    "Context", "AnalyticModel", "TableModel", "Grid", "Plan", "analytic_scorer",
+    "table_scorer", "select_config", "control_step", "replay", "make_targets",
+    "default_context", "ConfigError", "DataError", "OutOfRange", "PalsError",
+]
+
+
+class Context:
+    """One GPU, one stream (pals_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = _lib.load()
+        h = C.c_void_p()
+        check(self.lib.pals_ctx_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if self.h:
+            self.lib.pals_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, cuda_stream_ptr: int | None):
+        check(self.lib.pals_ctx_set_stream(self.h, C.c_void_p(cuda_stream_ptr or 0)))
+
+    @property
+    def stream(self) -> int:
+        return self.lib.pals_ctx_stream(self.h) or 0
+
+    def sync(self):
+        check(self.lib.pals_ctx_sync(self.h))
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.pals_ctx_launch_count(self.h))
+
+
+_default_ctx: Context | None = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+class _Model:
+    kind = "?"
+
+    def __init__(self, ctx: Context, handle: C.c_void_p):
+        self.ctx = ctx
+        self.h = handle
+
+    def __del__(self):
+        try:
+            if self.h and self.ctx.h:
+                self.ctx.lib.pals_model_destroy(self.h)
+        except Exception:
+            pass
+
+
+class AnalyticModel(_Model):
+    """analytic_scorer(profile, gpu) (controller.hpp:107-111)."""
+
+    kind = "analytic"
+
+    def __init__(self, ctx: Context, profile: Profile, gpu: GpuSpec):
+        h = C.c_void_p()
+        check(ctx.lib.pals_model_analytic(ctx.h, C.byref(profile), C.byref(gpu), C.byref(h)))
+        super().__init__(ctx, h)
+        self.profile = profile
+        self.gpu = gpu
+
+
+class TableModel(_Model):
+    """TableScorer (tests/test_controller.cpp:17-29): scores by point value, first match."""
+
+    kind = "table"
+
+    def __init__(self, ctx: Context, points: np.ndarray, t_hat, p_gpu):
+        pts = np.ascontiguousarray(points, dtype=POINT_DT)
+        t = np.ascontiguousarray(t_hat, np.float64)
+        p = np.ascontiguousarray(p_gpu, np.float64)
+        h = C.c_void_p()
+        check(ctx.lib.pals_model_table(ctx.h, ptr(pts), ptr(t), ptr(p), len(pts), C.byref(h)))
+        super().__init__(ctx, h)
+
+
+def analytic_scorer(profile: Profile, gpu: GpuSpec, ctx: Context | None = None) -> AnalyticModel:
+    return AnalyticModel(ctx or default_context(), profile, gpu)
+
+
+def table_scorer(points, t_hat, p_gpu, ctx: Context | None = None) -> TableModel:
+    return TableModel(ctx or default_context(), points, t_hat, p_gpu)
+
+
+class Grid:
+    """A candidate list (std::vector<OperatingPoint>) resident on the device."""
+
+    def __init__(self, ctx: Context, points: np.ndarray):
+        self.ctx = ctx
+        self.points = np.ascontiguousarray(points, dtype=POINT_DT)
+        h = C.c_void_p()
+        check(ctx.lib.pals_grid_points(ctx.h, ptr(self.points), len(self.points), C.byref(h)))
+        self.h = h
+
+    def __len__(self):
+        return len(self.points)
+
+    def __del__(self):
+        try:
+            if self.h and self.ctx.h:
+                self.ctx.lib.pals_grid_destroy(self.h)
+        except Exception:
+            pass
+
+
+def eval_grid(model: _Model, grid: Grid):
+    """CandidateScore for every grid point: (throughput_tps, gpu_power_w)."""
+    n = len(grid)
+    T = np.empty(n, np.float64)
+    P = np.empty(n, np.float64)
+    check(model.ctx.lib.pals_eval(model.ctx.h, model.h, grid.h, ptr(T), ptr(P)))
+    return T, P
+
+
+class Plan:
+    """Model x candidate grid x SystemPowerCoeffs, prepared for batched select_config."""
+
+    def __init__(self, model: _Model, grid: Grid, coeffs: Coeffs):
+        self.ctx = model.ctx
+        self.model = model
+        self.grid = grid
+        self.coeffs = coeffs
+        h = C.c_void_p()
+        check(self.ctx.lib.pals_plan_create(self.ctx.h, model.h, grid.h, C.byref(coeffs),
+                                            C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h and self.ctx.h:
+                self.ctx.lib.pals_plan_destroy(self.h)
+        except Exception:
+            pass
+
+    def prepare(self):
+        check(self.ctx.lib.pals_plan_prepare(self.h))
+
+    def select(self, queries: np.ndarray):
+        """Host buffers in and out: one select_config per query. Returns (index, reason)."""
+        q = np.ascontiguousarray(queries, dtype=QUERY_DT)
+        idx = np.empty(len(q), np.int32)
+        rs = np.empty(len(q), np.uint8)
+        check(self.ctx.lib.pals_select(self.h, ptr(q), len(q), ptr(idx), ptr(rs)))
+        return idx, rs
+
+    def select_device(self, d_queries: int, n: int, d_idx: int, d_reason: int):
+        """Device pointers (e.g. torch tensors' data_ptr()); async on the context stream."""
+        check(self.ctx.lib.pals_plan_select_device(self.h, C.c_void_p(d_queries), n,
+                                                   C.c_void_p(d_idx), C.c_void_p(d_reason)))
+
+    def scores(self):
+        n = len(self.grid)
+        th, pn, ef = (np.empty(n, np.float64) for _ in range(3))
+        check(self.ctx.lib.pals_plan_scores(self.h, ptr(th), ptr(pn), ptr(ef)))
+        return th, pn, ef
+
+    @property
+    def last_exact_count(self) -> int:
+        return int(self.ctx.lib.pals_plan_last_exact_count(self.h))
+
+    def force_exact(self, on: bool = True):
+        check(self.ctx.lib.pals_plan_set_force_exact(self.h, 1 if on else 0))
+
+    def time_scan(self, on: bool = True):
+        check(self.ctx.lib.pals_plan_time_scan(self.h, 1 if on else 0))
+
+    def scan_ms(self) -> float:
+        return float(self.ctx.lib.pals_plan_scan_ms(self.h))
+
+    def stats(self) -> np.ndarray:
+        """Per-class query counts of the last select (see pals_plan_stats)."""
+        c = np.zeros(6, np.int64)
+        check(self.ctx.lib.pals_plan_stats(self.h, ptr(c)))
+        return c
+
+
+def measure_peaks(ctx: Context):
+    """(integer compare+min ops/s, FP64 flop/s) measured on this device."""
+    a = C.c_double()
+    b = C.c_double()
+    check(ctx.lib.pals_measure_peaks(ctx.h, C.byref(a), C.byref(b)))
+    return a.value, b.value
+
+
+def make_targets(throughput_tps: float, power_budget_w: float | None = None,
+                 epsilon: float = 0.05, objective: int = OBJ_QOS) -> Targets:
+    """Targets (controller.hpp:19-29); power_budget_w None is std::nullopt."""
+    t = Targets()
+    t.throughput_tps = throughput_tps
+    t.has_budget = 0 if power_budget_w is None else 1
+    t.power_budget_w = 0.0 if power_budget_w is None else power_budget_w
+    t.epsilon = epsilon
+    t.objective = objective
+    return t
+
+
+def make_queries(throughput_tps, power_budget_w=None, bias=1.0, target_headroom=0.0,
+                 budget_margin=0.0, objective=OBJ_QOS) -> np.ndarray:
+    """Vectorised pals_query array; power_budget_w entries that are NaN mean no budget."""
+    tps = np.atleast_1d(np.asarray(throughput_tps, np.float64))
+    n = len(tps)
+    q = np.zeros(n, QUERY_DT)
+    q["throughput_tps"] = tps
+    if power_budget_w is None:
+        q["has_budget"] = 0
+    else:
+        b = np.broadcast_to(np.asarray(power_budget_w, np.float64), (n,))
+        q["has_budget"] = (~np.isnan(b)).astype(np.int32)
+        q["power_budget_w"] = np.where(np.isnan(b), 0.0, b)
+    q["bias"] = bias
+    q["target_headroom"] = target_headroom
+    q["budget_margin"] = budget_margin
+    q["objective"] = objective
+    return q
+
+
+def _points(candidates) -> np.ndarray:
+    if isinstance(candidates, np.ndarray):
+        return np.ascontiguousarray(candidates, dtype=POINT_DT)
+    pts = np.zeros(len(candidates), POINT_DT)
+    for i, c in enumerate(candidates):
+        pts[i] = (c.cap_watts, c.batch, c.tp, c.ep, c.dp) if isinstance(c, Point) else tuple(c)
+    return pts
+
+
+def select_config(candidates, targets: Targets, scorer: _Model, coeffs: Coeffs,
+                  bias: float = 1.0, target_headroom: float = 0.0,
+                  budget_margin: float = 0.0) -> Decision:
+    """select_config (controller.hpp:132-201), one call, on the GPU."""
+    pts = _points(candidates)
+    d = Decision()
+    ctx = scorer.ctx
+    check(ctx.lib.pals_select_one(ctx.h, scorer.h, ptr(pts), len(pts), C.byref(targets),
+                                  C.byref(coeffs), bias, target_headroom, budget_margin,
+                                  C.byref(d)))
+    return d
+
+
+def control_step(telemetry: Telemetry, now_s: float, targets: Targets, candidates,
+                 scorer: _Model, coeffs: Coeffs, state: CtrlState, cfg: CtrlCfg):
+    """control_step (controller.hpp:210-267), one call, on the GPU."""
+    pts = _points(candidates)
+    d = Decision()
+    st = CtrlState()
+    ctx = scorer.ctx
+    check(ctx.lib.pals_control_step_one(ctx.h, scorer.h, C.byref(telemetry), now_s,
+                                        C.byref(targets), ptr(pts), len(pts), C.byref(coeffs),
+                                        C.byref(state), C.byref(cfg), C.byref(d), C.byref(st)))
+    return d, st
+
+
+def replay(ctx: Context, models, plant, gpu: GpuSpec, coeffs: Coeffs, caps, batches,
+           cfg: CtrlCfg, spec: ReplaySpec):
+    """Batched control_step replay over spec.n_traces synthetic traces (host outputs)."""
+    n_models = len(models)
+    hs = (C.c_void_p * n_models)(*[m.h for m in models])
+    profs = (Profile * n_models)(*plant)
+    caps = np.ascontiguousarray(caps, np.float64)
+    batches = np.ascontiguousarray(batches, np.int32)
+    summ = np.zeros(spec.n_traces, SUMMARY_DT)
+    nl = min(spec.n_log_traces, spec.n_traces)
+    logs = np.zeros(max(1, nl * spec.n_steps), STEPLOG_DT)
+    check(ctx.lib.pals_replay(ctx.h, n_models, hs, profs, C.byref(gpu), C.byref(coeffs),
+                              ptr(caps), len(caps), ptr(batches), len(batches), C.byref(cfg),
+                              C.byref(spec), ptr(summ), ptr(logs) if nl else None))
+    return summ, logs[: nl * spec.n_steps]
+
+
+def replay_device(ctx: Context, models, plant, gpu: GpuSpec, coeffs: Coeffs, caps, batches,
+                  cfg: CtrlCfg, spec: ReplaySpec, d_summaries: int, d_logs: int = 0):
+    """Device-resident outputs; async on the context stream."""
+    n_models = len(models)
+    hs = (C.c_void_p * n_models)(*[m.h for m in models])
+    profs = (Profile * n_models)(*plant)
+    caps = np.ascontiguousarray(caps, np.float64)
+    batches = np.ascontiguousarray(batches, np.int32)
+    check(ctx.lib.pals_replay_device(ctx.h, n_models, hs, profs, C.byref(gpu), C.byref(coeffs),
+                                     ptr(caps), len(caps), ptr(batches), len(batches),
+                                     C.byref(cfg), C.byref(spec), C.c_void_p(d_summaries),
+                                     C.c_void_p(d_logs)))
+
+
+OBJECTIVES = {"qos": OBJ_QOS, "budget-throughput": OBJ_BUDGET}

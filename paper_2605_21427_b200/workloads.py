@@ -1,0 +1,153 @@
+"""Synthetic workloads of BASELINE.json's configs.
+
+cfg1  bundled: llama2-7b-like, 6 caps x 6 batches at its deployment tp (36 candidates),
+      one target 0.6 x unconstrained throughput, one static 1600 W budget.
+cfg2  dense 8B: llama2-7b-like + comm_fixed_by_tp[8] = 2*comm_fixed_by_tp[4];
+      caps[i] = 100 + 300 i/63 (64), batches 1..256, tp {1,2,4,8} -> 65,536 configs;
+      1e4 QoS targets from splitmix64(2605 ^ q).
+cfg3  MoE: mixtral-8x7b-like (+tp8), same 64x256x4 grid at ep=8; 1e6 (target, budget)
+      queries, QoS / budget-throughput 50/50, budget U(600, 2000) W, margin 0.02.
+cfg4  replay: 1e6 traces x 3600 steps over the 8 profiles, 36 candidates each.
+cfg5  replay stress: 1e7 traces as cfg4, sharded over GPUs.
+
+Everything is a pure function of (seed, index), so every arm (GPU, oracle, the
+reference build) sees bit-identical inputs.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .abi import OBJ_BUDGET, OBJ_QOS, POINT_DT, QUERY_DT, ReplaySpec, default_ctrl_cfg
+from .profiles import comm_of, load_bundle, profile_by_name, with_comm
+
+GOLDEN = np.uint64(0x9E3779B97F4A7C15)
+
+
+def splitmix64(x: np.ndarray) -> np.ndarray:
+    """rng.hpp:15-20, vectorised (uint64 arithmetic wraps)."""
+    x = np.asarray(x, dtype=np.uint64) + GOLDEN
+    x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return x ^ (x >> np.uint64(31))
+
+
+def u01(u: np.ndarray) -> np.ndarray:
+    return (u >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+
+
+def cfg2_caps() -> np.ndarray:
+    return np.array([100.0 + 300.0 * i / 63.0 for i in range(64)], np.float64)
+
+
+def grid_points(caps, batches, tps, eps=(1,), dps=(1,)) -> np.ndarray:
+    """Canonical sweep nesting cap -> batch -> tp -> ep -> dp (sweep.hpp:134-138)."""
+    caps = np.asarray(caps, np.float64)
+    b = np.asarray(batches, np.int32)
+    t = np.asarray(tps, np.int32)
+    e = np.asarray(eps, np.int32)
+    d = np.asarray(dps, np.int32)
+    C, B, T, E, D = np.meshgrid(caps, b, t, e, d, indexing="ij")
+    pts = np.zeros(C.size, POINT_DT)
+    pts["cap_watts"] = C.ravel()
+    pts["batch"] = B.ravel()
+    pts["tp"] = T.ravel()
+    pts["ep"] = E.ravel()
+    pts["dp"] = D.ravel()
+    return pts
+
+
+def gen_queries(n: int, seed: int, t_ref: float, objective: str = "qos",
+                budget: tuple | None = None, headroom: float = 0.05,
+                margin: float = 0.02, first: int = 0) -> np.ndarray:
+    """Queries q in [first, first+n): target U(0.05,1)*t_ref, bias 1.0 (half) or U(0.5,2)."""
+    qi = np.arange(first, first + n, dtype=np.uint64)
+    k = splitmix64(np.uint64(seed) ^ qi)
+    r = [u01(splitmix64(k + np.uint64((j * 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF)))
+         for j in range(1, 6)]
+    q = np.zeros(n, QUERY_DT)
+    q["throughput_tps"] = (0.05 + 0.95 * r[0]) * t_ref
+    q["bias"] = np.where(r[1] < 0.5, 1.0, 0.5 + 1.5 * r[2])
+    q["target_headroom"] = headroom
+    if budget is not None:
+        q["has_budget"] = 1
+        q["power_budget_w"] = budget[0] + (budget[1] - budget[0]) * r[3]
+        q["budget_margin"] = margin
+    if objective == "qos":
+        q["objective"] = OBJ_QOS
+    elif objective == "budget":
+        q["objective"] = OBJ_BUDGET
+    else:  # mixed 50/50
+        q["objective"] = np.where(r[4] < 0.5, OBJ_QOS, OBJ_BUDGET)
+    return q
+
+
+def dense_profile(profiles, name: str):
+    """Profile + synthetic tp=8 comm cost: 2 x comm_fixed_by_tp[4]."""
+    p = profile_by_name(profiles, name)
+    return with_comm(p, 8, 2.0 * comm_of(p, 4))
+
+
+def cfg1():
+    profs, gpu, coeffs = load_bundle()
+    p = profile_by_name(profs, "llama2-7b-like")
+    caps = [150.0, 200.0, 250.0, 300.0, 350.0, 400.0]
+    batches = [1, 4, 8, 16, 32, 64]
+    pts = grid_points(caps, batches, [p.deploy_tp], [p.deploy_ep], [p.deploy_dp])
+    return dict(name="cfg1", profile=p, gpu=gpu, coeffs=coeffs, points=pts, caps=caps,
+                batches=batches)
+
+
+def cfg2(n_queries: int = 10_000, budget: bool = False):
+    profs, gpu, coeffs = load_bundle()
+    p = dense_profile(profs, "llama2-7b-like")
+    pts = grid_points(cfg2_caps(), np.arange(1, 257), [1, 2, 4, 8])
+    return dict(name="cfg2", profile=p, gpu=gpu, coeffs=coeffs, points=pts,
+                n_queries=n_queries, seed=2605, objective="qos",
+                budget=(600.0, 2000.0) if budget else None)
+
+
+def cfg3(n_queries: int = 1_000_000):
+    profs, gpu, coeffs = load_bundle()
+    p = dense_profile(profs, "mixtral-8x7b-like")
+    pts = grid_points(cfg2_caps(), np.arange(1, 257), [1, 2, 4, 8], [8], [1])
+    return dict(name="cfg3", profile=p, gpu=gpu, coeffs=coeffs, points=pts,
+                n_queries=n_queries, seed=2605, objective="mixed", budget=(600.0, 2000.0))
+
+
+def replay_spec(n_traces: int, n_steps: int = 3600, seed: int = 2605, first: int = 0,
+                objective_mode: int = 2, n_log_traces: int = 0) -> ReplaySpec:
+    """cfg4/cfg5 fluid-plant traces."""
+    s = ReplaySpec()
+    s.seed = seed
+    s.first_trace = first
+    s.n_traces = n_traces
+    s.n_steps = n_steps
+    s.objective_mode = objective_mode
+    s.interval_s = 0.5
+    s.qos_frac_lo, s.qos_frac_hi = 0.3, 0.9
+    s.load_lo, s.load_hi = 0.3, 1.2
+    s.noise_amp = 0.04
+    s.budget_lo_frac, s.budget_hi_frac = 0.9, 1.1
+    s.epsilon = 0.05
+    s.seg_min, s.seg_max = 60, 480
+    s.budget_mode = 1
+    s.n_log_traces = n_log_traces
+    return s
+
+
+def cfg4_setup():
+    """8 profiles, 6x6 candidates at each profile's deployment, scenario_io defaults."""
+    profs, gpu, coeffs = load_bundle()
+    caps = np.array([150.0, 200.0, 250.0, 300.0, 350.0, 400.0])
+    batches = np.array([1, 4, 8, 16, 32, 64], np.int32)
+    # scenario_io.hpp:60-71: headroom defaults to epsilon, budget_margin to 0.02
+    cfg = default_ctrl_cfg(target_headroom=0.05, budget_margin=0.02)
+    return dict(profiles=profs, gpu=gpu, coeffs=coeffs, caps=caps, batches=batches, cfg=cfg)
+
+
+def max_t_hat(profile, gpu, points) -> float:
+    """Reference scale for query targets: max dp*T over the grid, from the GPU eval."""
+    from .wattserve import AnalyticModel, Grid, default_context, eval_grid
+    ctx = default_context()
+    T, _ = eval_grid(AnalyticModel(ctx, profile, gpu), Grid(ctx, points))
+    return float(np.max(T * points["dp"]))

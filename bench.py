@@ -178,7 +178,10 @@ def run_ours(args, dist: Dist):
 
     torch.cuda.set_device(dist.local)
     dist.init("nccl")
-    stream = torch.cuda.current_stream()
+    # a real (non-legacy-default) stream shared by torch and libpals_gpu, so the CUDA
+    # events below bracket exactly the kernels the library launches
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     ctx = Context(dist.local)
     ctx.set_stream(stream.cuda_stream)
     int_peak, fp64_peak = measure_peaks(ctx)

@@ -570,7 +570,8 @@ __device__ __forceinline__ void scan_item(const K* __restrict__ se, const K* __r
 }
 
 template <typename K>
-__global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a, int nchunks) {
+__global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a, int nchunks,
+                                                           int ch) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K* se = reinterpret_cast<K*>(smem_raw);
     K* st = se + kScanCh;
@@ -596,9 +597,9 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a, 
         }
         const int64_t tile = r / nchunks;
         const int chunk = (int)(r % nchunks);
-        const int64_t c0 = (int64_t)chunk * kScanCh;
+        const int64_t c0 = (int64_t)chunk * ch;
         const int64_t rem = d.n - c0;
-        const int nc = (int)(rem < kScanCh ? rem : kScanCh);
+        const int nc = (int)(rem < ch ? rem : ch);
         const int ncp = (nc + 3) & ~3;
         // stage this chunk's keys (pad with keys that never pass a threshold)
         for (int i = threadIdx.x; i < ncp; i += blockDim.x) {
@@ -815,6 +816,7 @@ int pals_plan_create(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
                    (d.wide ? N_ORD * n8 : N_ORD * (size_t)n * 4) + 4096;
     if (m->kind == MODEL_TABLE) bytes += 4 * (size_t)n + 2 * 8 * (size_t)std::max<int64_t>(1, m->table_n);
     bytes += sizeof(Analytic) + 256;
+    bytes += 64 * 256;  // every take() rounds up to 256 B
     PALS_CUDA(cudaMalloc(&p->slab, bytes));
     char* s = (char*)p->slab;
     auto take = [&](size_t b) {
@@ -902,6 +904,7 @@ int pals_plan_prepare(pals_plan* p) {
     cudaStream_t s = ctx->stream;
     PlanDev& d = p->d;
     const int64_t n = p->n;
+    (void)cudaGetLastError();  // clear stale non-sticky errors of earlier calls
     PALS_CUDA(cudaMemsetAsync(d.globals, 0, 16, s));
     PALS_CUDA(cudaMemsetAsync(p->gk, 0xFF, 16, s));
     for (int o = 0; o < N_ORD; ++o) PALS_CUDA(cudaMemsetAsync(d.pos[o], 0, p->np * 4, s));
@@ -979,14 +982,21 @@ int pals_plan_select_device(pals_plan* p, const pals_query* d_queries, int64_t n
     PALS_CUDA(cudaMemsetAsync(p->counts, 0, 64, s));
     const int qb = grid_blocks(ctx, nq, 256);
     k_qprep<<<qb, 256, 0, s>>>(p->d, a);
-    const int nchunks = (int)((p->n + kScanCh - 1) / kScanCh);
+    // Work items = query tiles x config chunks. Size the chunk so a batch of nq
+    // queries still yields >= ~6 items per SM (few queries -> short chunks).
+    const int64_t tq = p->d.wide ? ScanQ<uint64_t>::TQ : ScanQ<uint32_t>::TQ;
+    const int64_t tiles_est = std::max<int64_t>(1, (nq + tq - 1) / tq);
+    const int64_t want_chunks = std::max<int64_t>(1, (6 * (int64_t)ctx->num_sms + tiles_est - 1) / tiles_est);
+    int64_t ch = (p->n + want_chunks - 1) / want_chunks;
+    ch = std::min<int64_t>(kScanCh, std::max<int64_t>(256, (ch + 255) / 256 * 256));
+    const int nchunks = (int)((p->n + ch - 1) / ch);
     // persistent scan grid: 4 CTAs per SM
     const int sgrid = ctx->num_sms * 4;
     if (p->time_scan) PALS_CUDA(cudaEventRecord(p->ev_scan0, s));
     if (p->d.wide)
-        k_scan<uint64_t><<<sgrid, kScanThreads, 3 * kScanCh * 8, s>>>(p->d, a, nchunks);
+        k_scan<uint64_t><<<sgrid, kScanThreads, 3 * kScanCh * 8, s>>>(p->d, a, nchunks, (int)ch);
     else
-        k_scan<uint32_t><<<sgrid, kScanThreads, 3 * kScanCh * 4, s>>>(p->d, a, nchunks);
+        k_scan<uint32_t><<<sgrid, kScanThreads, 3 * kScanCh * 4, s>>>(p->d, a, nchunks, (int)ch);
     if (p->time_scan) {
         PALS_CUDA(cudaEventRecord(p->ev_scan1, s));
         p->scan_recorded = 1;

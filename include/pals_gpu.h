@@ -248,6 +248,11 @@ int pals_model_forest(pals_ctx* ctx, int32_t n_models, int32_t model_index,
                       const double* p_threshold, const int32_t* p_left, const int32_t* p_right,
                       const double* p_value, pals_model** out);
 int pals_model_destroy(pals_model* m);
+/* Number of cells of a forest model's exact lattice table (0: evaluated by the
+ * direct tree walk; -1: not a forest model). */
+int64_t pals_model_forest_cells(const pals_model* m);
+/* 1: evaluate a forest model by the literal tree walk even when a cell table exists. */
+int pals_model_forest_set_direct(pals_model* m, int direct);
 
 /* ---- candidate grids -------------------------------------------------- */
 int pals_grid_points(pals_ctx* ctx, const pals_point* points, int64_t n, pals_grid** out);
@@ -262,6 +267,9 @@ int pals_grid_destroy(pals_grid* g);
 /* Host outputs: throughput_tps and gpu_power_w per point (CandidateScore). */
 int pals_eval(pals_ctx* ctx, const pals_model* m, const pals_grid* g, double* throughput_tps,
               double* gpu_power_w);
+/* Device outputs, async on the context stream (analytic and forest models). */
+int pals_eval_device(pals_ctx* ctx, const pals_model* m, const pals_grid* g, double* d_T,
+                     double* d_P);
 
 /* ---- selection plans: model x grid x coeffs --------------------------- */
 int pals_plan_create(pals_ctx* ctx, const pals_model* m, const pals_grid* g,

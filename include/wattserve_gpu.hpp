@@ -1,0 +1,324 @@
+// wattserve_gpu.hpp — drop-in C++ adapter: the reference's decision API
+// (wattserve/controller.hpp) executed by libpals_gpu.so on a B200.
+//
+// A wattserve user swaps
+//     wattserve::select_config(cands, targets, wattserve::analytic_scorer(prof, gpu), k)
+// for
+//     wattserve::gpu::select_config(cands, targets, wattserve::gpu::analytic_scorer(ctx, prof, gpu), k)
+// with the same types, the same results bit for bit and the same exceptions
+// (config_error / data_error / std::out_of_range, same messages). Scorers are the
+// three concrete kinds the GPU can run (an arbitrary std::function cannot):
+//   analytic_scorer   controller.hpp:107-111
+//   predictor_scorer  controller.hpp:100-105 (PredictorBundle, forest.hpp:217-251)
+//   table_scorer      the TableScorer test fake, tests/test_controller.cpp:17-29
+// plus batched entry points (SelectPlan, replay) that have no single-call
+// counterpart in the reference.
+//
+// Header-only; include after the reference headers are on the include path and
+// link libpals_gpu.so.
+#pragma once
+
+#include <cstdio>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "pals_gpu.h"
+#include "wattserve/controller.hpp"
+#include "wattserve/forest.hpp"
+
+namespace wattserve::gpu {
+
+inline void check(int rc) {
+    if (rc == PALS_OK) return;
+    const std::string msg = pals_last_error();
+    switch (rc) {
+        case PALS_ECONFIG: throw config_error(msg);
+        case PALS_EDATA: throw data_error(msg);
+        case PALS_ERANGE: throw std::out_of_range(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+
+inline pals_point to_c(const OperatingPoint& p) {
+    pals_point o;
+    o.cap_watts = p.cap_watts;
+    o.batch = p.batch;
+    o.tp = p.tp;
+    o.ep = p.ep;
+    o.dp = p.dp;
+    return o;
+}
+
+inline OperatingPoint from_c(const pals_point& p) {
+    return OperatingPoint{p.cap_watts, p.batch, p.tp, p.ep, p.dp};
+}
+
+inline pals_targets to_c(const Targets& t) {
+    pals_targets o{};
+    o.throughput_tps = t.throughput_tps;
+    o.has_budget = t.power_budget_w.has_value() ? 1 : 0;
+    o.power_budget_w = t.power_budget_w.value_or(0.0);
+    o.epsilon = t.epsilon;
+    o.objective = t.objective == Objective::BudgetMaxThroughput ? PALS_OBJ_BUDGET : PALS_OBJ_QOS;
+    return o;
+}
+
+inline Targets from_c(const pals_targets& t) {
+    Targets o;
+    o.throughput_tps = t.throughput_tps;
+    if (t.has_budget) o.power_budget_w = t.power_budget_w;
+    o.epsilon = t.epsilon;
+    o.objective = t.objective == PALS_OBJ_BUDGET ? Objective::BudgetMaxThroughput
+                                                 : Objective::QosMaxEfficiency;
+    return o;
+}
+
+inline pals_ctrl_cfg to_c(const ControllerConfig& c) {
+    pals_ctrl_cfg o{};
+    o.kp = c.gains.kp;
+    o.ki = c.gains.ki;
+    o.kd = c.gains.kd;
+    o.integral_clamp = c.integral_clamp;
+    o.bias_min = c.bias_min;
+    o.bias_max = c.bias_max;
+    o.interval_s = c.interval_s;
+    o.target_headroom = c.target_headroom;
+    o.budget_margin = c.budget_margin;
+    o.sustain_intervals = c.sustain_intervals;
+    return o;
+}
+
+inline pals_ctrl_state to_c(const ControllerState& s) {
+    pals_ctrl_state o{};
+    o.bias = s.bias;
+    o.integral = s.integral;
+    o.prev_error = s.prev_error;
+    o.has_prev_error = s.has_prev_error ? 1 : 0;
+    o.sustain_count = s.sustain_count;
+    o.current = to_c(s.current);
+    o.has_last_targets = s.last_targets.has_value() ? 1 : 0;
+    if (s.last_targets) o.last_targets = to_c(*s.last_targets);
+    return o;
+}
+
+inline ControllerState from_c(const pals_ctrl_state& s) {
+    ControllerState o;
+    o.bias = s.bias;
+    o.integral = s.integral;
+    o.prev_error = s.prev_error;
+    o.has_prev_error = s.has_prev_error != 0;
+    o.sustain_count = s.sustain_count;
+    o.current = from_c(s.current);
+    if (s.has_last_targets) o.last_targets = from_c(s.last_targets);
+    return o;
+}
+
+inline pals_profile to_c(const ModelProfile& p) {
+    pals_profile o{};
+    std::snprintf(o.name, sizeof(o.name), "%s", p.name.c_str());
+    o.compute_fixed = p.compute_fixed;
+    o.compute_per_seq = p.compute_per_seq;
+    o.comm_per_seq = p.comm_per_seq;
+    o.internode_factor = p.internode_factor;
+    o.knee_watts = p.knee_watts;
+    o.compute_power_base = p.compute_power_base;
+    o.compute_power_per_seq = p.compute_power_per_seq;
+    o.comm_power = p.comm_power;
+    o.overlap = p.overlap;
+    o.total_params_b = p.total_params_b;
+    o.active_params_b = p.active_params_b;
+    int i = 0;
+    for (const auto& [tp, v] : p.comm_fixed_by_tp) {
+        if (i >= PALS_MAX_TP_KEYS) throw config_error(p.name + ": too many comm_fixed_by_tp keys");
+        o.tp_keys[i] = tp;
+        o.comm_fixed[i] = v;
+        ++i;
+    }
+    o.n_tp = i;
+    o.num_experts = p.num_experts;
+    o.top_k = p.top_k;
+    o.deploy_tp = p.deployment.tp;
+    o.deploy_ep = p.deployment.ep;
+    o.deploy_dp = p.deployment.dp;
+    return o;
+}
+
+inline std::vector<pals_point> to_c(const std::vector<OperatingPoint>& v) {
+    std::vector<pals_point> o;
+    o.reserve(v.size());
+    for (const auto& p : v) o.push_back(to_c(p));
+    return o;
+}
+
+// One GPU, one stream.
+class Context {
+public:
+    explicit Context(int device = 0) { check(pals_ctx_create(device, &h_)); }
+    ~Context() { pals_ctx_destroy(h_); }
+    Context(const Context&) = delete;
+    Context& operator=(const Context&) = delete;
+    pals_ctx* get() const { return h_; }
+
+private:
+    pals_ctx* h_ = nullptr;
+};
+
+// A device-resident scorer (the GPU counterpart of wattserve::Scorer).
+class GpuScorer {
+public:
+    GpuScorer(Context& ctx, pals_model* m) : ctx_(&ctx), m_(m, pals_model_destroy) {}
+    pals_model* get() const { return m_.get(); }
+    Context& context() const { return *ctx_; }
+
+private:
+    Context* ctx_;
+    std::shared_ptr<pals_model> m_;
+};
+
+inline GpuScorer analytic_scorer(Context& ctx, const ModelProfile& profile, const GpuSpec& gpu) {
+    const pals_profile p = to_c(profile);
+    const pals_gpu_spec g{gpu.idle_watts, gpu.min_cap_watts, gpu.max_cap_watts, gpu.max_frequency};
+    pals_model* m = nullptr;
+    check(pals_model_analytic(ctx.get(), &p, &g, &m));
+    return GpuScorer(ctx, m);
+}
+
+inline GpuScorer table_scorer(Context& ctx, const std::vector<OperatingPoint>& points,
+                              const std::vector<double>& t_hat, const std::vector<double>& p_gpu) {
+    const auto pts = to_c(points);
+    pals_model* m = nullptr;
+    check(pals_model_table(ctx.get(), pts.data(), t_hat.data(), p_gpu.data(),
+                           static_cast<int64_t>(pts.size()), &m));
+    return GpuScorer(ctx, m);
+}
+
+namespace detail {
+struct SoA {
+    std::vector<int64_t> off;
+    std::vector<int32_t> f, l, r;
+    std::vector<double> t, v;
+};
+inline SoA flatten(const Forest& forest) {
+    SoA s;
+    s.off.push_back(0);
+    for (const auto& tree : forest.trees) {
+        for (const auto& n : tree.nodes) {
+            s.f.push_back(n.feature);
+            s.t.push_back(n.threshold);
+            s.l.push_back(n.left);
+            s.r.push_back(n.right);
+            s.v.push_back(n.value);
+        }
+        s.off.push_back(static_cast<int64_t>(s.f.size()));
+    }
+    return s;
+}
+}  // namespace detail
+
+inline GpuScorer predictor_scorer(Context& ctx, const PredictorBundle& bundle,
+                                  const std::string& model_id) {
+    const int mi = bundle.schema.model_index(model_id);  // throws like encode() would
+    const auto T = detail::flatten(bundle.throughput_forest);
+    const auto P = detail::flatten(bundle.power_forest);
+    const pals_coeffs k{bundle.coeffs.alpha, bundle.coeffs.beta_watts};
+    pals_model* m = nullptr;
+    check(pals_model_forest(ctx.get(), static_cast<int32_t>(bundle.schema.model_ids.size()), mi,
+                            &k, static_cast<int32_t>(bundle.throughput_forest.trees.size()),
+                            T.off.data(), T.f.data(), T.t.data(), T.l.data(), T.r.data(),
+                            T.v.data(), static_cast<int32_t>(bundle.power_forest.trees.size()),
+                            P.off.data(), P.f.data(), P.t.data(), P.l.data(), P.r.data(),
+                            P.v.data(), &m));
+    return GpuScorer(ctx, m);
+}
+
+// select_config (controller.hpp:132-201)
+inline Decision select_config(const std::vector<OperatingPoint>& candidates,
+                              const Targets& targets, const GpuScorer& score,
+                              const SystemPowerCoeffs& coeffs, double bias = 1.0,
+                              double target_headroom = 0.0, double budget_margin = 0.0) {
+    const auto pts = to_c(candidates);
+    const pals_targets t = to_c(targets);
+    const pals_coeffs k{coeffs.alpha, coeffs.beta_watts};
+    pals_decision d{};
+    check(pals_select_one(score.context().get(), score.get(), pts.data(),
+                          static_cast<int64_t>(pts.size()), &t, &k, bias, target_headroom,
+                          budget_margin, &d));
+    return Decision{from_c(d.point), d.applied != 0, static_cast<DecisionReason>(d.reason)};
+}
+
+// control_step (controller.hpp:210-267)
+inline std::pair<Decision, ControllerState> control_step(
+    const TelemetryInput& telemetry, double now_s, const Targets& targets,
+    const std::vector<OperatingPoint>& candidates, const GpuScorer& score,
+    const SystemPowerCoeffs& coeffs, const ControllerState& state, const ControllerConfig& cfg) {
+    const auto pts = to_c(candidates);
+    const pals_targets t = to_c(targets);
+    const pals_coeffs k{coeffs.alpha, coeffs.beta_watts};
+    const pals_telemetry tel{telemetry.t_s, telemetry.throughput_tps};
+    const pals_ctrl_state st = to_c(state);
+    const pals_ctrl_cfg c = to_c(cfg);
+    pals_decision d{};
+    pals_ctrl_state out{};
+    check(pals_control_step_one(score.context().get(), score.get(), &tel, now_s, &t, pts.data(),
+                                static_cast<int64_t>(pts.size()), &k, &st, &c, &d, &out));
+    return {Decision{from_c(d.point), d.applied != 0, static_cast<DecisionReason>(d.reason)},
+            from_c(out)};
+}
+
+// Many select_config calls over one candidate grid in one GPU pass.
+class SelectPlan {
+public:
+    SelectPlan(Context& ctx, const GpuScorer& score, const std::vector<OperatingPoint>& candidates,
+               const SystemPowerCoeffs& coeffs)
+        : candidates_(candidates) {
+        const auto pts = to_c(candidates);
+        check(pals_grid_points(ctx.get(), pts.data(), static_cast<int64_t>(pts.size()), &grid_));
+        const pals_coeffs k{coeffs.alpha, coeffs.beta_watts};
+        check(pals_plan_create(ctx.get(), score.get(), grid_, &k, &plan_));
+    }
+    ~SelectPlan() {
+        pals_plan_destroy(plan_);
+        pals_grid_destroy(grid_);
+    }
+    SelectPlan(const SelectPlan&) = delete;
+    SelectPlan& operator=(const SelectPlan&) = delete;
+
+    // decisions[i] == wattserve::select_config(candidates, targets[i], score, coeffs,
+    //                                          bias[i], headroom, margin)
+    std::vector<Decision> select(const std::vector<Targets>& targets,
+                                 const std::vector<double>& bias, double target_headroom = 0.0,
+                                 double budget_margin = 0.0) {
+        std::vector<pals_query> q(targets.size());
+        for (std::size_t i = 0; i < q.size(); ++i) {
+            q[i].throughput_tps = targets[i].throughput_tps;
+            q[i].has_budget = targets[i].power_budget_w.has_value() ? 1 : 0;
+            q[i].power_budget_w = targets[i].power_budget_w.value_or(0.0);
+            q[i].bias = bias.empty() ? 1.0 : bias[i];
+            q[i].target_headroom = target_headroom;
+            q[i].budget_margin = budget_margin;
+            q[i].objective = targets[i].objective == Objective::BudgetMaxThroughput
+                                 ? PALS_OBJ_BUDGET
+                                 : PALS_OBJ_QOS;
+        }
+        std::vector<int32_t> idx(q.size());
+        std::vector<uint8_t> reason(q.size());
+        check(pals_select(plan_, q.data(), static_cast<int64_t>(q.size()), idx.data(),
+                          reason.data()));
+        std::vector<Decision> out;
+        out.reserve(q.size());
+        for (std::size_t i = 0; i < q.size(); ++i)
+            out.push_back(Decision{candidates_[static_cast<std::size_t>(idx[i])], true,
+                                   static_cast<DecisionReason>(reason[i])});
+        return out;
+    }
+
+private:
+    std::vector<OperatingPoint> candidates_;
+    pals_grid* grid_ = nullptr;
+    pals_plan* plan_ = nullptr;
+};
+
+}  // namespace wattserve::gpu

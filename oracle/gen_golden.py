@@ -309,6 +309,50 @@ def gen_replay(ref: Reference) -> None:
                         logs_q=logs_q)
 
 
+def forest_points(n, seed):
+    rng = np.random.default_rng(seed)
+    pts = np.zeros(n, POINT_DT)
+    pts["cap_watts"] = np.where(rng.uniform(size=n) < 0.5, rng.uniform(100.0, 400.0, n),
+                                rng.choice([150.0, 200.0, 250.0, 300.0, 350.0, 400.0], n))
+    pts["batch"] = np.where(rng.uniform(size=n) < 0.5, rng.integers(1, 257, n),
+                            rng.choice([1, 4, 8, 16, 32, 64], n))
+    pts["tp"] = rng.choice([1, 2, 4, 8], n)
+    pts["ep"] = rng.choice([1, 4, 8], n)
+    pts["dp"] = rng.choice([1, 2, 3], n)
+    return pts
+
+
+def gen_forest(ref: Reference) -> None:
+    """A small PredictorBundle (20 trees, depth 10) trained by the reference's own
+    pipeline, shipped as model-fit input, plus the reference's predictions and
+    predictor_scorer selections on it."""
+    from oracle.oracle import ref_bundle_predict, ref_select_forest, ref_train_bundle
+    from paper_2605_21427_b200.forest import Bundle
+    profs, gpu, coeffs = load_bundle()
+    path = "/tmp/pals_bundle_small.json"
+    ref_train_bundle(ref, profs, gpu, coeffs, path, n_trees=20, max_depth=10, min_leaf=2,
+                     seed=2605)
+    b = Bundle.load_json(path)
+    b.save_npz(os.path.join(ROOT, "paper_2605_21427_b200", "data", "predictor_small.npz"))
+    pts = forest_points(3000, 31)
+    out = {"points": pts}
+    for mid in ("llama2-7b-like", "mixtral-8x7b-like", "olmoe-like"):
+        T, P, E = ref_bundle_predict(ref, path, mid, pts)
+        out[f"{mid}_T"], out[f"{mid}_P"], out[f"{mid}_E"] = T, P, E
+    # predictor_scorer selections over the cfg1 candidate grid of mixtral
+    c1 = workloads.cfg1()
+    mp = [p for p in profs if p.name.decode() == "mixtral-8x7b-like"][0]
+    cands = workloads.grid_points(c1["caps"], c1["batches"], [mp.deploy_tp], [mp.deploy_ep],
+                                  [mp.deploy_dp])
+    T, _, _ = ref_bundle_predict(ref, path, "mixtral-8x7b-like", cands)
+    q = np.concatenate([workloads.gen_queries(300, 41, float(T.max()), "qos"),
+                        workloads.gen_queries(300, 42, float(T.max()), "mixed",
+                                              budget=(800.0, 2000.0))])
+    idx, rs = ref_select_forest(ref, path, "mixtral-8x7b-like", cands, coeffs, q)
+    out.update(sel_points=cands, sel_queries=q, sel_idx=idx, sel_reason=rs)
+    np.savez_compressed(os.path.join(GOLD, "forest.npz"), **out)
+
+
 def main():
     os.makedirs(GOLD, exist_ok=True)
     ref = Reference()
@@ -318,6 +362,7 @@ def main():
     gen_tables(ref)
     gen_control(ref)
     gen_replay(ref)
+    gen_forest(ref)
     print("fixtures written to", GOLD)
 
 

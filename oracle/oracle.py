@@ -116,6 +116,26 @@ class Oracle:
             raise RuntimeError(f"or_replay rc={rc}")
         return summ, logs[: spec.n_log_traces * spec.n_steps]
 
+    def replay_scored(self, plant, gpu, coeffs, caps, batches, cfg: CtrlCfg, spec: ReplaySpec,
+                      scorer_T: np.ndarray, scorer_P: np.ndarray):
+        """Replay with a non-analytic scorer given as [n_models, n_candidates] tables."""
+        L = self.lib
+        L.or_replay_scored.argtypes = [C.c_int, _VP, _VP, _VP, _VP, C.c_int, _VP, C.c_int, _VP,
+                                       _VP, _VP, _VP, _VP, _VP]
+        profs = (Profile * len(plant))(*plant)
+        caps = np.ascontiguousarray(caps, np.float64)
+        batches = np.ascontiguousarray(batches, np.int32)
+        sT = np.ascontiguousarray(scorer_T, np.float64)
+        sP = np.ascontiguousarray(scorer_P, np.float64)
+        summ = np.zeros(spec.n_traces, SUMMARY_DT)
+        logs = np.zeros(max(1, spec.n_log_traces * spec.n_steps), STEPLOG_DT)
+        rc = L.or_replay_scored(len(plant), profs, C.byref(gpu), C.byref(coeffs), ptr(caps),
+                                len(caps), ptr(batches), len(batches), C.byref(cfg),
+                                C.byref(spec), ptr(sT), ptr(sP), ptr(summ), ptr(logs))
+        if rc:
+            raise RuntimeError(f"or_replay_scored rc={rc}")
+        return summ, logs[: spec.n_log_traces * spec.n_steps]
+
 
 class Reference:
     """The unmodified reference (oracle/_ref/libwsref.so)."""
@@ -254,3 +274,71 @@ class Reference:
         if rc:
             raise RuntimeError(self.last_error())
         return g, k
+
+
+def _forest_args(fs):
+    return [fs.n_trees, ptr(fs.tree_offset), ptr(fs.feature), ptr(fs.threshold), ptr(fs.left),
+            ptr(fs.right), ptr(fs.value)]
+
+
+def oracle_forest_predict(orc: Oracle, bundle, model_id: str, pts: np.ndarray):
+    """PredictorBundle::predict restated in C (pals_oracle.c or_forest_predict)."""
+    L = orc.lib
+    L.or_forest_predict.argtypes = [C.c_int, C.c_int, _VP] + [C.c_int] + [_VP] * 6 + \
+        [C.c_int] + [_VP] * 6 + [_VP, C.c_int64, _VP, _VP, _VP]
+    pts = np.ascontiguousarray(pts, dtype=POINT_DT)
+    n = len(pts)
+    T, P, E = (np.empty(n) for _ in range(3))
+    rc = L.or_forest_predict(len(bundle.model_ids), bundle.model_index(model_id),
+                             C.byref(bundle.coeffs), *_forest_args(bundle.throughput),
+                             *_forest_args(bundle.power), ptr(pts), n, ptr(T), ptr(P), ptr(E))
+    assert rc == 0
+    return T, P, E
+
+
+def ref_train_bundle(ref: Reference, profiles, gpu, coeffs, path: str, n_trees=100,
+                     max_depth=14, min_leaf=2, seed=2605) -> None:
+    """Train a PredictorBundle with the reference's own pipeline (run_sweep + train_bundle)."""
+    L = ref.lib
+    L.ref_train_bundle.argtypes = [_VP, C.c_int, _VP, _VP, C.c_int, C.c_int, C.c_int,
+                                   C.c_uint64, C.c_char_p]
+    arr = (Profile * len(profiles))(*profiles)
+    rc = L.ref_train_bundle(arr, len(profiles), C.byref(gpu), C.byref(coeffs), n_trees,
+                            max_depth, min_leaf, seed, path.encode())
+    if rc:
+        raise RuntimeError(ref.last_error())
+
+
+def ref_bundle_predict(ref: Reference, path: str, model_id: str, pts: np.ndarray):
+    L = ref.lib
+    L.ref_bundle_predict.argtypes = [C.c_char_p, C.c_char_p, _VP, C.c_int64, _VP, _VP, _VP]
+    pts = np.ascontiguousarray(pts, dtype=POINT_DT)
+    n = len(pts)
+    T, P, E = (np.empty(n) for _ in range(3))
+    rc = L.ref_bundle_predict(path.encode(), model_id.encode(), ptr(pts), n, ptr(T), ptr(P),
+                              ptr(E))
+    if rc:
+        raise RuntimeError(ref.last_error())
+    return T, P, E
+
+
+def ref_select_forest(ref: Reference, path: str, model_id: str, pts, coeffs, queries):
+    L = ref.lib
+    L.ref_select_forest.argtypes = [C.c_char_p, C.c_char_p, _VP, C.c_int64, _VP, _VP, C.c_int64,
+                                    _VP, _VP]
+    q = np.ascontiguousarray(queries, dtype=QUERY_DT)
+    idx = np.empty(len(q), np.int32)
+    rs = np.empty(len(q), np.uint8)
+    rc = L.ref_select_forest(path.encode(), model_id.encode(), ptr(pts), len(pts),
+                             C.byref(coeffs), ptr(q), len(q), ptr(idx), ptr(rs))
+    if rc:
+        raise RuntimeError(ref.last_error())
+    return idx, rs
+
+
+def ref_bench_predict(ref: Reference, path: str, model_id: str, pts, threads: int) -> float:
+    L = ref.lib
+    L.ref_bench_predict.restype = C.c_double
+    L.ref_bench_predict.argtypes = [C.c_char_p, C.c_char_p, _VP, C.c_int64, C.c_int]
+    pts = np.ascontiguousarray(pts, dtype=POINT_DT)
+    return L.ref_bench_predict(path.encode(), model_id.encode(), ptr(pts), len(pts), threads)

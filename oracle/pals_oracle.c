@@ -285,10 +285,29 @@ static double enforce_cap(double cap, int batch, double node_budget, const pals_
     return g->min_cap_watts;
 }
 
+/* Replay with the controller's scorer given as per-model candidate tables
+ * (scorerT/scorerP[m * nc + i] = score(candidate i of model m)), e.g. a forest
+ * predictor; the plant always runs the analytic profile. NULL tables: the
+ * scorer is the analytic plant model itself (analytic_scorer). */
+int or_replay_scored(int n_models, const pals_profile* plant, const pals_gpu_spec* g,
+                     const pals_coeffs* k, const double* caps, int n_caps, const int* batches,
+                     int n_batches, const pals_ctrl_cfg* cfg, const pals_replay_spec* spec,
+                     const double* scorerT, const double* scorerP,
+                     pals_trace_summary* summaries, pals_step_log* logs);
+
 int or_replay(int n_models, const pals_profile* plant, const pals_gpu_spec* g,
               const pals_coeffs* k, const double* caps, int n_caps, const int* batches,
               int n_batches, const pals_ctrl_cfg* cfg, const pals_replay_spec* spec,
               pals_trace_summary* summaries, pals_step_log* logs) {
+    return or_replay_scored(n_models, plant, g, k, caps, n_caps, batches, n_batches, cfg, spec,
+                            NULL, NULL, summaries, logs);
+}
+
+int or_replay_scored(int n_models, const pals_profile* plant, const pals_gpu_spec* g,
+                     const pals_coeffs* k, const double* caps, int n_caps, const int* batches,
+                     int n_batches, const pals_ctrl_cfg* cfg, const pals_replay_spec* spec,
+                     const double* scorerT, const double* scorerP,
+                     pals_trace_summary* summaries, pals_step_log* logs) {
     const int nc = n_caps * n_batches;
     pals_point* cands = (pals_point*)malloc(sizeof(pals_point) * (size_t)nc * (size_t)n_models);
     double* T = (double*)malloc(sizeof(double) * (size_t)nc * (size_t)n_models);
@@ -333,8 +352,8 @@ int or_replay(int n_models, const pals_profile* plant, const pals_gpu_spec* g,
         const uint64_t key = or_splitmix64(spec->seed ^ (uint64_t)(spec->first_trace + ti));
         const int m = (int)(key % (uint64_t)n_models);
         const pals_point* cm = cands + (size_t)m * nc;
-        const double* Tm = T + (size_t)m * nc;
-        const double* Pm = P + (size_t)m * nc;
+        const double* Tm = (scorerT ? scorerT : T) + (size_t)m * nc;
+        const double* Pm = (scorerP ? scorerP : P) + (size_t)m * nc;
         int obj = spec->objective_mode;
         if (obj == 2) obj = (int)(draw(key, 0, 0) >> 63);
         const double qfrac =
@@ -431,4 +450,49 @@ done:
     free(pmin);
     free(pmax);
     return rc;
+}
+
+/* ---- tree-ensemble predictor (forest.hpp) ------------------------------ */
+/* RegressionTree::predict forest.hpp:80-85 (children are tree-local) */
+static double tree_predict(const int32_t* f, const double* thr, const int32_t* l,
+                           const int32_t* r, const double* v, const double* x) {
+    int i = 0;
+    while (f[i] >= 0) i = x[f[i]] <= thr[i] ? l[i] : r[i];
+    return v[i];
+}
+
+/* Forest::predict forest.hpp:176-180 */
+static double forest_predict(int n_trees, const int64_t* off, const int32_t* f,
+                             const double* thr, const int32_t* l, const int32_t* r,
+                             const double* v, const double* x) {
+    double s = 0.0;
+    for (int t = 0; t < n_trees; ++t) {
+        const int64_t o = off[t];
+        s += tree_predict(f + o, thr + o, l + o, r + o, v + o, x);
+    }
+    return s / (double)n_trees;
+}
+
+/* PredictorBundle::predict forest.hpp:227-235 with FeatureSchema::encode :41-50 */
+int or_forest_predict(int n_models, int model_index, const pals_coeffs* k, int tn,
+                      const int64_t* toff, const int32_t* tf, const double* tthr,
+                      const int32_t* tl, const int32_t* tr, const double* tv, int pn,
+                      const int64_t* poff, const int32_t* pf, const double* pthr,
+                      const int32_t* pl, const int32_t* pr, const double* pv,
+                      const pals_point* pts, int64_t n, double* T, double* P, double* E) {
+    if (model_index < 0 || model_index >= n_models) return PALS_ECONFIG;
+    double* x = (double*)calloc((size_t)(5 + n_models), sizeof(double));
+    for (int64_t i = 0; i < n; ++i) {
+        x[0] = pts[i].cap_watts;
+        x[1] = (double)pts[i].batch;
+        x[2] = (double)pts[i].tp;
+        x[3] = (double)pts[i].ep;
+        x[4] = (double)pts[i].dp;
+        x[5 + model_index] = 1.0;
+        T[i] = forest_predict(tn, toff, tf, tthr, tl, tr, tv, x);
+        P[i] = forest_predict(pn, poff, pf, pthr, pl, pr, pv, x);
+        E[i] = T[i] / (k->alpha * 4.0 * P[i] + k->beta_watts);
+    }
+    free(x);
+    return PALS_OK;
 }

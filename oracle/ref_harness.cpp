@@ -639,3 +639,134 @@ int ref_load_platform(const char* path, pals_gpu_spec* gpu, pals_coeffs* coeffs)
 }
 
 }  // extern "C"
+
+// ---- tree-ensemble predictor (forest.hpp) ---------------------------------
+namespace {
+struct BundleCache {
+    std::string path;
+    PredictorBundle b;
+};
+thread_local BundleCache g_bundle;
+
+const PredictorBundle& load_bundle(const char* path) {
+    if (g_bundle.path != path) {
+        g_bundle.b = bundle_from_json(parse_json_file(path));
+        g_bundle.path = path;
+    }
+    return g_bundle.b;
+}
+}  // namespace
+
+extern "C" {
+
+// cmd_profile + cmd_train without the holdout split: run_sweep (sweep.hpp:123-170)
+// with the AnalyticBackend over SweepGrid::default_grid() for every profile, then
+// train_bundle (forest.hpp:271-296); the bundle is written with bundle_to_json.
+int ref_train_bundle(const pals_profile* profs, int n, const pals_gpu_spec* gpu,
+                     const pals_coeffs* coeffs, int n_trees, int max_depth, int min_leaf,
+                     std::uint64_t seed, const char* out_path) {
+    try {
+        const GpuSpec g = to_gpu(*gpu);
+        const SystemPowerCoeffs k{coeffs->alpha, coeffs->beta_watts};
+        AnalyticBackend be(g, k);
+        const SweepGrid grid = SweepGrid::default_grid();
+        std::vector<ProfilingRecord> all;
+        for (int i = 0; i < n; ++i) {
+            const ModelProfile mp = to_profile(profs[i]);
+            const auto ds = run_sweep(grid, mp.name, mp, g, be, seed + static_cast<std::uint64_t>(i));
+            all.insert(all.end(), ds.records.begin(), ds.records.end());
+        }
+        HyperParams hp;
+        hp.n_trees = n_trees;
+        hp.max_depth = max_depth;
+        hp.min_leaf = min_leaf;
+        const PredictorBundle b = train_bundle(all, k, hp, seed);
+        write_json_file(out_path, bundle_to_json(b));
+    } catch (...) {
+        return map_exception();
+    }
+    return PALS_OK;
+}
+
+// PredictorBundle::predict (forest.hpp:227-235) for each point
+int ref_bundle_predict(const char* path, const char* model_id, const pals_point* pts,
+                       std::int64_t n, double* T, double* P, double* E) {
+    try {
+        const PredictorBundle& b = load_bundle(path);
+        for (std::int64_t i = 0; i < n; ++i) {
+            const auto m = b.predict(to_point(pts[i]), model_id);
+            T[i] = m.throughput_hat;
+            P[i] = m.power_hat;
+            E[i] = m.efficiency_hat;
+        }
+    } catch (...) {
+        return map_exception();
+    }
+    return PALS_OK;
+}
+
+// select_config with predictor_scorer (controller.hpp:100-105)
+int ref_select_forest(const char* path, const char* model_id, const pals_point* pts,
+                      std::int64_t n, const pals_coeffs* coeffs, const pals_query* q,
+                      std::int64_t nq, std::int32_t* idx, std::uint8_t* reason) {
+    try {
+        const PredictorBundle& b = load_bundle(path);
+        std::vector<OperatingPoint> cands;
+        for (std::int64_t i = 0; i < n; ++i) cands.push_back(to_point(pts[i]));
+        const Scorer s = predictor_scorer(b, model_id);
+        const SystemPowerCoeffs k{coeffs->alpha, coeffs->beta_watts};
+        for (std::int64_t j = 0; j < nq; ++j) {
+            const auto d = select_config(cands, query_targets(q[j]), s, k, q[j].bias,
+                                         q[j].target_headroom, q[j].budget_margin);
+            idx[j] = index_of(cands, d.point);
+            reason[j] = static_cast<std::uint8_t>(reason_code(d.reason));
+        }
+    } catch (...) {
+        return map_exception();
+    }
+    return PALS_OK;
+}
+
+// PredictorBundle::predict throughput on all host threads (bench cpu_baseline)
+double ref_bench_predict(const char* path, const char* model_id, const pals_point* pts,
+                         std::int64_t n, int n_threads) {
+    std::atomic<int> failed{0};
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> th;
+    for (int t = 0; t < n_threads; ++t) {
+        th.emplace_back([&, t] {
+            try {
+                const PredictorBundle b = bundle_from_json(parse_json_file(path));
+                (void)b;
+            } catch (...) {
+                failed = 1;
+            }
+        });
+    }
+    for (auto& x : th) x.join();
+    th.clear();
+    // the bundle load is setup, not the predict path: time predictions only
+    std::vector<PredictorBundle> bs(n_threads);
+    for (int t = 0; t < n_threads; ++t) bs[t] = bundle_from_json(parse_json_file(path));
+    const auto t1 = std::chrono::steady_clock::now();
+    (void)t0;
+    for (int t = 0; t < n_threads; ++t) {
+        th.emplace_back([&, t] {
+            const std::int64_t lo = n * t / n_threads, hi = n * (t + 1) / n_threads;
+            double acc = 0.0;
+            try {
+                for (std::int64_t i = lo; i < hi; ++i)
+                    acc += bs[t].predict(to_point(pts[i]), model_id).throughput_hat;
+            } catch (...) {
+                failed = 1;
+            }
+            if (acc == -1.0) failed = 1;
+        });
+    }
+    for (auto& x : th) x.join();
+    const auto t2 = std::chrono::steady_clock::now();
+    if (failed) return -1.0;
+    return std::chrono::duration<double>(t2 - t1).count();
+}
+
+}  // extern "C"

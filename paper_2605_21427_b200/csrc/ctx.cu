@@ -200,6 +200,7 @@ int pals_model_destroy(pals_model* m) {
     delete[] m->table_T;
     delete[] m->table_P;
     if (m->forest) forest_free(m->forest);
+    if (m->d_an) cudaFree(m->d_an);
     delete m;
     return PALS_OK;
 }

@@ -123,9 +123,10 @@ PALS_HD double unorderable(uint64_t k) {
 
 // ---- plan device layout ---------------------------------------------------
 // Three orders: 0 = t_hat descending, 1 = p_node ascending, 2 = eff descending.
-// Each order has a dense rank D (index into its sorted distinct values U) and
-// a packed key (D << kTrBits) | TR, TR = the grid's (cap, batch, index) rank,
-// so min(key) is the reference's argmax with its knob tie-break (Appendix A).
+// In each order a point has a competition rank r (number of points with a
+// strictly better value: equal values share r) and a packed key
+// (r << tr_bits) | TR, TR = the grid's (cap, batch, index) rank, so min(key)
+// is the reference's argmax with its knob tie-break.
 enum { ORD_T = 0, ORD_P = 1, ORD_E = 2, N_ORD = 3 };
 
 struct PlanDev {
@@ -145,11 +146,12 @@ struct PlanDev {
     double* ef;          // t_hat / p_node
     // rank structures (per order)
     uint64_t* skey[N_ORD];   // orderable keys of the values (unsorted, padded)
-    uint64_t* sorted[N_ORD]; // sorted keys (chunk-sorted then merged)
-    uint32_t* pos[N_ORD];    // merged positions
-    uint64_t* U[N_ORD];      // sorted distinct keys
-    uint32_t* cut[N_ORD];    // near-set boundary per dense rank (Appendix A)
-    uint32_t* nd;            // distinct counts [N_ORD]
+    uint64_t* sorted[N_ORD]; // chunk-sorted keys
+    uint32_t* pos[N_ORD];    // merged position of every chunk-sorted key
+    uint64_t* merged[N_ORD]; // fully sorted keys (position r = competition rank r)
+    uint8_t* bnd[N_ORD];     // per position i: 0 = merged[i+1] equal, 1 = distinct but a
+                             // tolerance near-tie, 2 = separated (or i = n-1)
+    uint8_t* danger[N_ORD];  // per position: the value's run ends on a near-tie (bnd == 1)
     uint32_t* key32[N_ORD];  // packed keys (narrow)
     uint64_t* key64[N_ORD];  // packed keys (wide)
     int32_t* globals;        // [0] argmax t over all, [1] argmin p over all, [2] generic flag,
@@ -188,6 +190,7 @@ struct pals_model {
     double* table_P = nullptr;         // host
     // forest model (device arrays), see forest.cu
     void* forest = nullptr;
+    pals::Analytic* d_an = nullptr;  // device copy for pals_eval_device
 };
 
 struct pals_grid {
@@ -224,4 +227,10 @@ void replay_cache_free(pals_ctx* ctx);
 // forest.cu
 void forest_free(void* f);
 int forest_eval_plan(pals_plan* p, const pals_model* m, pals_ctx* ctx);
+int forest_eval_raw(const pals_model* m, pals_ctx* ctx, int64_t n, const double* cap,
+                    const int* batch, const int* tp, const int* ep, const int* dp, double* T,
+                    double* P, int force_direct);
+// plan.cu
+const pals_grid* plan_grid(const pals_plan* p);
+int plan_finish_scores(pals_plan* p);
 }  // namespace pals

@@ -59,7 +59,6 @@ struct pals_plan {
     double* table_T = nullptr;
     double* table_P = nullptr;
     uint64_t* gk = nullptr;       // [2] global candidate keys
-    uint64_t* merged[N_ORD] = {};
     // query-side buffers (capacity-managed)
     int64_t qcap = 0;
     uint64_t* thr_t = nullptr;
@@ -129,30 +128,57 @@ __global__ void k_pad_keys(PlanDev d, int64_t np) {
 }
 
 // ---------------------------------------------------------------- sort ----
-// (1) bitonic sort of each 4096-key chunk in shared memory
+// (1) bitonic sort of each 4096-key chunk. Warp w owns keys [128w, 128w+128);
+// lane l holds key 128w + 32k + l in x[k]. Exchange distances 1..16 are warp
+// shuffles, 32 and 64 are register swaps, only >= 128 go through shared memory
+// (15 of the 78 network stages).
 __global__ void __launch_bounds__(1024) k_sort_chunks(PlanDev d) {
     __shared__ uint64_t s[kChunk];
     const int o = blockIdx.y;
     const int64_t base = (int64_t)blockIdx.x * kChunk;
-    for (int i = threadIdx.x; i < kChunk; i += blockDim.x) s[i] = d.skey[o][base + i];
-    __syncthreads();
-    for (int k = 2; k <= kChunk; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < kChunk; i += blockDim.x) {
-                const int ixj = i ^ j;
-                if (ixj > i) {
-                    const uint64_t a = s[i], b = s[ixj];
-                    const bool up = (i & k) == 0;
-                    if ((a > b) == up) {
-                        s[i] = b;
-                        s[ixj] = a;
-                    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int i0 = 128 * w + lane;
+    uint64_t x[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) x[k] = d.skey[o][base + i0 + 32 * k];
+    for (int ks = 2; ks <= kChunk; ks <<= 1) {
+        for (int j = ks >> 1; j > 0; j >>= 1) {
+            if (j >= 128) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) s[i0 + 32 * k] = x[k];
+                __syncthreads();
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int i = i0 + 32 * k;
+                    const uint64_t p = s[i ^ j];
+                    const bool up = (i & ks) == 0, lower = (i & j) == 0;
+                    x[k] = (up == lower) ? min(x[k], p) : max(x[k], p);
+                }
+                __syncthreads();
+            } else if (j >= 32) {
+                const int kb = j >> 5;  // 1 or 2
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (k & kb) continue;
+                    const int k2 = k | kb;
+                    const bool up = ((i0 + 32 * k) & ks) == 0;
+                    const uint64_t lo = min(x[k], x[k2]), hi = max(x[k], x[k2]);
+                    x[k] = up ? lo : hi;
+                    x[k2] = up ? hi : lo;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int i = i0 + 32 * k;
+                    const uint64_t p = __shfl_xor_sync(0xffffffffu, x[k], j);
+                    const bool up = (i & ks) == 0, lower = (lane & j) == 0;
+                    x[k] = (up == lower) ? min(x[k], p) : max(x[k], p);
                 }
             }
-            __syncthreads();
         }
     }
-    for (int i = threadIdx.x; i < kChunk; i += blockDim.x) d.sorted[o][base + i] = s[i];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) d.sorted[o][base + i0 + 32 * k] = x[k];
 }
 
 __device__ __forceinline__ int lower_bound_s(const uint64_t* s, int n, uint64_t x) {
@@ -195,9 +221,9 @@ __global__ void __launch_bounds__(256) k_cross(PlanDev d) {
 }
 
 // (3) scatter to the merged order
-__global__ void k_scatter(PlanDev d, uint64_t* m0, uint64_t* m1, uint64_t* m2) {
+__global__ void k_scatter(PlanDev d) {
     const int o = blockIdx.y;
-    uint64_t* m = o == 0 ? m0 : (o == 1 ? m1 : m2);
+    uint64_t* m = d.merged[o];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.n;
          i += (int64_t)gridDim.x * blockDim.x)
         m[d.pos[o][i]] = d.sorted[o][i];
@@ -213,110 +239,60 @@ __device__ __forceinline__ bool separated(double a, double b) {
     return fabs(a - b) > 4e-9 * smax(fabs(a), fabs(b));
 }
 
-// block-wide exclusive scan of one uint32 per thread (1024 threads)
-__device__ uint32_t block_excl_scan(uint32_t v, uint32_t* sh, uint32_t* total) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    uint32_t x = v;
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) sh[w] = x;
-    __syncthreads();
-    if (w == 0) {
-        uint32_t t = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
-            if (lane >= o) t += y;
-        }
-        sh[lane] = t;
-    }
-    __syncthreads();
-    const uint32_t before = (w ? sh[w - 1] : 0) + x - v;
-    *total = sh[(blockDim.x >> 5) - 1];
-    __syncthreads();
-    return before;
-}
-
-// (4) distinct values, their count, and the near-tie cluster boundary cut[d]:
-// the last dense index e >= d such that U[e] and U[e+1] are separated.
-__global__ void __launch_bounds__(1024) k_unique(PlanDev d, const uint64_t* m0, const uint64_t* m1,
-                                                 const uint64_t* m2) {
-    __shared__ uint32_t sh[64];
-    __shared__ uint32_t sh_min[1024];
-    const int o = blockIdx.x;
-    const uint64_t* m = o == 0 ? m0 : (o == 1 ? m1 : m2);
-    const int64_t n = d.n;
-    const int T = blockDim.x, t = threadIdx.x;
-    const int64_t seg = (n + T - 1) / T;
-    const int64_t lo = t * seg, hi = min(n, lo + seg);
-    uint32_t cnt = 0;
-    for (int64_t i = lo; i < hi; ++i) cnt += (i == 0 || m[i] != m[i - 1]) ? 1u : 0u;
-    uint32_t nd;
-    uint32_t p = block_excl_scan(cnt, sh, &nd);
-    for (int64_t i = lo; i < hi; ++i)
-        if (i == 0 || m[i] != m[i - 1]) d.U[o][p++] = m[i];
-    if (t == 0) d.nd[o] = nd;
-    __threadfence_block();
-    __syncthreads();
-    // cut: suffix-min over the indices of separated boundaries
-    const int64_t dseg = ((int64_t)nd + T - 1) / T;
-    const int64_t dlo = t * dseg, dhi = min((int64_t)nd, dlo + dseg);
-    uint32_t first_sep = 0xFFFFFFFFu;
-    for (int64_t e = dlo; e < dhi; ++e) {
-        const bool sep = (e == (int64_t)nd - 1) ||
-                         separated(key_value(o, d.U[o][e]), key_value(o, d.U[o][e + 1]));
-        if (sep) {
-            first_sep = (uint32_t)e;
-            break;
-        }
-    }
-    sh_min[t] = first_sep;
-    __syncthreads();
-    // exclusive suffix min across threads (sequential over 1024 is fine: once per plan)
-    if (t == 0) {
-        uint32_t run = 0xFFFFFFFFu;
-        for (int k = T - 1; k >= 0; --k) {
-            const uint32_t v = sh_min[k];
-            sh_min[k] = run;
-            run = min(run, v);
-        }
-    }
-    __syncthreads();
-    uint32_t next = sh_min[t];
-    for (int64_t e = dhi - 1; e >= dlo; --e) {
-        const bool sep = (e == (int64_t)nd - 1) ||
-                         separated(key_value(o, d.U[o][e]), key_value(o, d.U[o][e + 1]));
-        if (sep) next = (uint32_t)e;
-        d.cut[o][e] = next;
-    }
-}
-
-__device__ __forceinline__ uint32_t dense_rank(const uint64_t* U, uint32_t nd, uint64_t x) {
-    uint32_t lo = 0, hi = nd;
+__device__ __forceinline__ uint32_t lower_bound_g(const uint64_t* m, int64_t n, uint64_t x) {
+    int64_t lo = 0, hi = n;
     while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (U[mid] < x) lo = mid + 1;
+        const int64_t mid = (lo + hi) >> 1;
+        if (m[mid] < x) lo = mid + 1;
         else hi = mid;
     }
-    return lo;
+    return (uint32_t)lo;
 }
 
-// (5) packed keys (D << tr_bits) | TR for all three orders
+// boundary class between merged positions i and i+1 (see PlanDev::bnd)
+__device__ __forceinline__ uint8_t boundary(const PlanDev& d, int o, int64_t i) {
+    if (i + 1 >= d.n) return 2;
+    const uint64_t a = d.merged[o][i], b = d.merged[o][i + 1];
+    if (a == b) return 0;
+    return separated(key_value(o, a), key_value(o, b)) ? 2 : 1;
+}
+
+// (4) per point: competition rank r = lower_bound(merged, key) and the packed key
+// (r << tr_bits) | TR; per merged position: the boundary class and whether the
+// value's run ends on a near-tie (then a winner there needs the exact fold).
 __global__ void k_assign(PlanDev d, const int* __restrict__ tr, uint64_t* gk) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t r = (uint64_t)tr[i];
+        const uint64_t t = (uint64_t)tr[i];
 #pragma unroll
         for (int o = 0; o < N_ORD; ++o) {
-            const uint32_t D = dense_rank(d.U[o], d.nd[o], d.skey[o][i]);
-            const uint64_t k = ((uint64_t)D << d.tr_bits) | r;
+            const uint32_t r = lower_bound_g(d.merged[o], d.n, d.skey[o][i]);
+            const uint64_t k = ((uint64_t)r << d.tr_bits) | t;
             if (d.wide) d.key64[o][i] = k;
             else d.key32[o][i] = (uint32_t)k;
-            if (D == 0 && o == ORD_T) atomicMin((unsigned long long*)&gk[0], k);
-            if (D == 0 && o == ORD_P) atomicMin((unsigned long long*)&gk[1], k);
+            if (r == 0 && o == ORD_T) atomicMin((unsigned long long*)&gk[0], k);
+            if (r == 0 && o == ORD_P) atomicMin((unsigned long long*)&gk[1], k);
+            // position-indexed tables (thread i handles merged position i)
+            const uint8_t bi = boundary(d, o, i);
+            d.bnd[o][i] = bi;
+            uint8_t dg;
+            if (bi != 0) {
+                dg = bi == 1;
+            } else {  // run continues: find its last position
+                const int64_t e = (int64_t)lower_bound_g(d.merged[o], d.n, d.merged[o][i] + 1) - 1;
+                dg = boundary(d, o, e) == 1;
+            }
+            d.danger[o][i] = dg;
         }
     }
+}
+
+// Last merged position of the near-tie cluster that contains position r0: the
+// cluster extends over runs whose boundaries are near-ties (bnd == 1).
+__device__ __forceinline__ uint32_t cluster_end(const PlanDev& d, int o, uint32_t r0) {
+    int64_t j = r0;
+    while (j + 1 < d.n && boundary(d, o, j) != 2) ++j;
+    return (uint32_t)j;
 }
 
 // ------------------------------------------------------- exact fold ------
@@ -367,7 +343,8 @@ __device__ int warp_fold(int64_t n, const double* __restrict__ cap, const int* _
     return (int)best;
 }
 
-__device__ __forceinline__ uint32_t dense_of(const PlanDev& d, int o, int64_t c) {
+// competition rank of point c in order o
+__device__ __forceinline__ uint32_t rank_of(const PlanDev& d, int o, int64_t c) {
     return d.wide ? (uint32_t)(d.key64[o][c] >> d.tr_bits)
                   : (uint32_t)(d.key32[o][c] >> d.tr_bits);
 }
@@ -421,19 +398,21 @@ __global__ void k_resolve_globals(PlanDev d, const uint64_t* gk) {
     const int o = w == 0 ? ORD_T : ORD_P;
     const uint64_t mask = (1ull << d.tr_bits) - 1;
     int best;
-    if (!generic && d.cut[o][0] == 0) {
+    if (!generic && !d.danger[o][0]) {
         best = d.inv_tr[gk[w] & mask];
     } else {
-        const uint32_t cut = generic ? 0xFFFFFFFFu : d.cut[o][0];
+        // near-tie at the top: fold over the top cluster only (every point below
+        // the cluster loses to every point in it by more than the tolerance)
+        const uint32_t cut = generic ? 0xFFFFFFFFu : cluster_end(d, o, 0);
         if (w == 0)
             best = warp_fold(
                 d.n, d.cap, d.batch,
-                [&](int64_t c) { return generic || dense_of(d, ORD_T, c) <= cut; },
+                [&](int64_t c) { return generic || rank_of(d, ORD_T, c) <= cut; },
                 [&](int64_t c) { return d.th[c]; });
         else
             best = warp_fold(
                 d.n, d.cap, d.batch,
-                [&](int64_t c) { return generic || dense_of(d, ORD_P, c) <= cut; },
+                [&](int64_t c) { return generic || rank_of(d, ORD_P, c) <= cut; },
                 [&](int64_t c) { return -d.pn[c]; });
     }
     if (lane == 0) d.globals[w] = best;
@@ -472,9 +451,11 @@ struct SelArgs {
     int force_exact;
 };
 
-// (7) per-query thresholds in dense-rank space and the query class.
-// Kt = #distinct t_hat with !(t*bias < target)  (controller.hpp:163, monotone in t)
-// Kp = #distinct p_node with p <= budget        (controller.hpp:155)
+// (7) per-query thresholds in competition-rank space and the query class.
+// Kt = #points with !(t_hat*bias < target)  (controller.hpp:163; monotone in t_hat)
+// Kp = #points with p_node <= budget        (controller.hpp:155)
+// A point is t-feasible iff its rank r_t < Kt (every feasible value is strictly
+// better than every infeasible one), likewise for p.
 __global__ void k_qprep(PlanDev d, SelArgs a) {
     const int lane = threadIdx.x & 31;
     for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x; j0 < a.nq;
@@ -484,27 +465,27 @@ __global__ void k_qprep(PlanDev d, SelArgs a) {
         if (j < a.nq) {
             const pals_query q = a.q[j];
             const bool bset = q.has_budget != 0;
-            uint32_t Kt = 0, Kp = d.nd[ORD_P];
+            uint32_t Kt = 0, Kp = (uint32_t)d.n;
             if (q.objective == PALS_OBJ_QOS) {
                 const double target = q.throughput_tps * (1.0 + q.target_headroom);
-                uint32_t lo = 0, hi = d.nd[ORD_T];
+                int64_t lo = 0, hi = d.n;
                 while (lo < hi) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    const double t = key_value(ORD_T, d.U[ORD_T][mid]);
+                    const int64_t mid = (lo + hi) >> 1;
+                    const double t = key_value(ORD_T, d.merged[ORD_T][mid]);
                     if (!(t * q.bias < target)) lo = mid + 1;
                     else hi = mid;
                 }
-                Kt = lo;
+                Kt = (uint32_t)lo;
             }
             if (bset) {
                 const double budget = q.power_budget_w * (1.0 - q.budget_margin);
-                uint32_t lo = 0, hi = d.nd[ORD_P];
+                int64_t lo = 0, hi = d.n;
                 while (lo < hi) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if (key_value(ORD_P, d.U[ORD_P][mid]) <= budget) lo = mid + 1;
+                    const int64_t mid = (lo + hi) >> 1;
+                    if (key_value(ORD_P, d.merged[ORD_P][mid]) <= budget) lo = mid + 1;
                     else hi = mid;
                 }
-                Kp = lo;
+                Kp = (uint32_t)lo;
             }
             if (a.force_exact || d.globals[2]) c = CLS_X;
             else if (q.objective == PALS_OBJ_QOS && !bset) c = Kt ? CLS_A : CLS_D;
@@ -654,7 +635,7 @@ __device__ __forceinline__ uint64_t fix_sentinel(const PlanDev& d, uint64_t best
                                                  const pals_query& q, bool need_t, bool need_p) {
     if (d.wide || best != kNone64) return best;
     const uint32_t full = 0xFFFFFFFFu;
-    // the point whose packed key in order o is all-ones (TR = n-1 and D = 65535)
+    // the point whose packed key in order o is all-ones (TR = n-1 and rank 65535)
     if (d.n != 65536) return best;
     const int64_t c = d.inv_tr[d.n - 1];
     if (d.key32[o][c] != full) return best;
@@ -691,7 +672,7 @@ __global__ void k_finalize(PlanDev d, SelArgs a) {
             be = fix_sentinel(d, be, ORD_E, q, true, c == CLS_B);
             if (be != none) {
                 const uint32_t d0 = (uint32_t)(be >> d.tr_bits);
-                if (d.cut[ORD_E][d0] != d0) {
+                if (d.danger[ORD_E][d0]) {
                     push_work(a, (int32_t)j, EX_QOS_NEAR, d0);
                     continue;
                 }
@@ -703,7 +684,7 @@ __global__ void k_finalize(PlanDev d, SelArgs a) {
             if (c != CLS_D) bt = fix_sentinel(d, bt, ORD_T, q, false, true);
             if (c != CLS_D && bt != none) {
                 const uint32_t d0 = (uint32_t)(bt >> d.tr_bits);
-                if (d.cut[ORD_T][d0] != d0) {
+                if (d.danger[ORD_T][d0]) {
                     push_work(a, (int32_t)j, EX_BUD_NEAR, d0);
                     continue;
                 }
@@ -737,20 +718,20 @@ __global__ void k_exact(PlanDev d, SelArgs a) {
         int best;
         int r;
         if (it.mode == EX_QOS_NEAR) {
-            const uint32_t cut = d.cut[ORD_E][it.d0];
+            const uint32_t cut = cluster_end(d, ORD_E, it.d0);
             best = warp_fold(
                 d.n, d.cap, d.batch,
                 [&](int64_t c) {
-                    return dense_of(d, ORD_E, c) <= cut && feasible_t(d, q, c) &&
+                    return rank_of(d, ORD_E, c) <= cut && feasible_t(d, q, c) &&
                            feasible_p(d, q, c);
                 },
                 [&](int64_t c) { return d.ef[c]; });
             r = PALS_REASON_QOS_FEASIBLE;
         } else {
-            const uint32_t cut = d.cut[ORD_T][it.d0];
+            const uint32_t cut = cluster_end(d, ORD_T, it.d0);
             best = warp_fold(
                 d.n, d.cap, d.batch,
-                [&](int64_t c) { return dense_of(d, ORD_T, c) <= cut && feasible_p(d, q, c); },
+                [&](int64_t c) { return rank_of(d, ORD_T, c) <= cut && feasible_p(d, q, c); },
                 [&](int64_t c) { return d.th[c]; });
             r = PALS_REASON_BUDGET_MAX_T;
         }
@@ -772,9 +753,37 @@ static int check_launch(const char* what) {
     return PALS_OK;
 }
 
-// device-side plan state accessors used by replay.cu
+// device-side plan state accessors used by replay.cu / forest.cu
 const PlanDev& plan_dev(const pals_plan* p) { return p->d; }
 int plan_error(const pals_plan* p) { return p->err; }
+const pals_grid* plan_grid(const pals_plan* p) { return p->grid; }
+
+__global__ void k_finish(PlanDev d, double alpha, double beta) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        finish_scores(d, i, d.T[i], d.P[i], d.dp[i], alpha, beta);
+}
+
+// derived scores (t_hat, p_node, eff, sort keys) from T/P already in the plan
+int plan_finish_scores(pals_plan* p) {
+    k_finish<<<grid_blocks(p->ctx, p->n, 256), 256, 0, p->ctx->stream>>>(p->d, p->coeffs.alpha,
+                                                                       p->coeffs.beta_watts);
+    count_launch(p->ctx);
+    return check_launch("k_finish");
+}
+
+__global__ void k_eval_analytic_raw(const Analytic* __restrict__ an, int64_t n,
+                                    const double* __restrict__ cap, const int* __restrict__ batch,
+                                    const int* __restrict__ tp, const int* __restrict__ dp,
+                                    double* __restrict__ T, double* __restrict__ P) {
+    const Analytic& a = *an;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const Score s = analytic_score(a, cap[i], batch[i], tp[i], dp[i]);
+        T[i] = s.T;
+        P[i] = s.P;
+    }
+}
 
 }  // namespace pals
 
@@ -832,14 +841,13 @@ int pals_plan_create(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
     for (int o = 0; o < N_ORD; ++o) {
         d.skey[o] = (uint64_t*)take(np8);
         d.sorted[o] = (uint64_t*)take(np8);
-        p->merged[o] = (uint64_t*)take(np8);
+        d.merged[o] = (uint64_t*)take(np8);
         d.pos[o] = (uint32_t*)take(np4);
-        d.U[o] = (uint64_t*)take(n8);
-        d.cut[o] = (uint32_t*)take((size_t)n * 4);
+        d.bnd[o] = (uint8_t*)take((size_t)n);
+        d.danger[o] = (uint8_t*)take((size_t)n);
         if (d.wide) d.key64[o] = (uint64_t*)take(n8);
         else d.key32[o] = (uint32_t*)take((size_t)n * 4);
     }
-    d.nd = (uint32_t*)take(16);
     d.globals = (int32_t*)take(16);
     p->gk = (uint64_t*)take(16);
     p->d_an = (Analytic*)take(sizeof(Analytic));
@@ -922,12 +930,10 @@ int pals_plan_prepare(pals_plan* p) {
     if (p->np > n) k_pad_keys<<<dim3(grid_blocks(ctx, p->np - n, 256), N_ORD), 256, 0, s>>>(d, p->np);
     k_sort_chunks<<<dim3(p->nchunks, N_ORD), 1024, 0, s>>>(d);
     k_cross<<<dim3(p->nchunks, p->nchunks, N_ORD), 256, 0, s>>>(d);
-    k_scatter<<<dim3(grid_blocks(ctx, n, 256), N_ORD), 256, 0, s>>>(d, p->merged[0], p->merged[1],
-                                                                   p->merged[2]);
-    k_unique<<<N_ORD, 1024, 0, s>>>(d, p->merged[0], p->merged[1], p->merged[2]);
+    k_scatter<<<dim3(grid_blocks(ctx, n, 256), N_ORD), 256, 0, s>>>(d);
     k_assign<<<eb, 256, 0, s>>>(d, p->tr, p->gk);
     k_resolve_globals<<<1, 64, 0, s>>>(d, p->gk);
-    count_launch(ctx, 8 + (p->np > n ? 1 : 0));
+    count_launch(ctx, 7 + (p->np > n ? 1 : 0));
     return check_launch("pals_plan_prepare");
 }
 
@@ -1088,6 +1094,26 @@ double pals_plan_scan_ms(pals_plan* p) {
 int pals_plan_set_force_exact(pals_plan* p, int force) {
     p->force_exact = force;
     return PALS_OK;
+}
+
+int pals_eval_device(pals_ctx* ctx, const pals_model* m, const pals_grid* g, double* d_T,
+                     double* d_P) {
+    if (m->kind == MODEL_TABLE)
+        return set_error(PALS_ECONFIG, "pals_eval_device: table models are scored via plans");
+    if (m->kind == MODEL_FOREST)
+        return forest_eval_raw(m, ctx, g->n, g->cap, g->batch, g->tp, g->ep, g->dp, d_T, d_P, 0);
+    // analytic: the scorer would throw on the first invalid point (model.hpp:56-59)
+    const int rc = validate_points(m, g->h_pts, g->n);
+    if (rc) return rc;
+    if (!m->d_an) {
+        auto* mm = const_cast<pals_model*>(m);
+        PALS_CUDA(cudaMalloc(&mm->d_an, sizeof(Analytic)));
+        PALS_CUDA(cudaMemcpy(mm->d_an, &m->an, sizeof(Analytic), cudaMemcpyHostToDevice));
+    }
+    k_eval_analytic_raw<<<grid_blocks(ctx, g->n, 256), 256, 0, ctx->stream>>>(
+        m->d_an, g->n, g->cap, g->batch, g->tp, g->dp, d_T, d_P);
+    count_launch(ctx);
+    return check_launch("k_eval_analytic_raw");
 }
 
 int pals_eval(pals_ctx* ctx, const pals_model* m, const pals_grid* g, double* T, double* P) {

@@ -9,6 +9,7 @@
 // prefix-min of throughput keys (budget branch). A winner inside a near-tie
 // cluster is re-decided by the literal sequential fold over the candidates.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <unordered_map>
@@ -22,7 +23,7 @@ constexpr int kMaxReplayCands = 4096;
 
 struct ReplayModelDev {
     int n;             // candidates
-    int nd_t, nd_p;    // distinct t_hat / p_node values
+    int nd_t, nd_p;    // sorted t_hat / p_node entries (= n)
     int tp, ep, dp;
     int init_idx;      // (max cap, max batch) candidate
     int gmax_t, gmin_p;
@@ -38,12 +39,12 @@ struct ReplayModelDev {
     const double* th;
     const double* pn;
     const double* ef;
-    const uint32_t* cut_t;
-    const uint32_t* cut_e;
+    const uint8_t* danger_t;  // per rank: the value's run ends on a near-tie
+    const uint8_t* danger_e;
     const double* ut;   // distinct t_hat, descending
     const double* up;   // distinct p_node, ascending
-    const uint32_t* m2; // (nd_t+1) x (nd_p+1): min eff key over {D_t < i, D_p < j}
-    const uint32_t* b1; // nd_p+1: min t key over {D_p < j}
+    const uint32_t* m2; // (n+1) x (n+1): min eff key over {r_t < i, r_p < j}
+    const uint32_t* b1; // n+1: min t key over {r_p < j}
     const Analytic* plant;
 };
 
@@ -139,7 +140,7 @@ __device__ __forceinline__ void table_select(const ReplayModelDev& m, double tar
         const uint32_t key = m.m2[lo * W + (bset ? kp : m.nd_p)];
         if (key != kNone32) {
             const uint32_t d0 = key >> 16;
-            if (m.cut_e[d0] != d0) {
+            if (m.danger_e[d0]) {
                 thread_select_full(m, target, bset, budget, bias, objective, idx, reason);
                 return;
             }
@@ -152,7 +153,7 @@ __device__ __forceinline__ void table_select(const ReplayModelDev& m, double tar
         const uint32_t key = m.b1[kp];
         if (key != kNone32) {
             const uint32_t d0 = key >> 16;
-            if (m.cut_t[d0] != d0) {
+            if (m.danger_t[d0]) {
                 thread_select_full(m, target, bset, budget, bias, objective, idx, reason);
                 return;
             }
@@ -190,18 +191,50 @@ __device__ double enforce_cap_dev(const ReplayModelDev& m, double cap, int batch
     return c;
 }
 
-__global__ void __launch_bounds__(128) k_replay(const ReplayModelDev* __restrict__ models,
-                                                ReplayParams p, pals_trace_summary* __restrict__ out,
+__device__ __forceinline__ int trace_objective(const pals_replay_spec& sp, uint64_t key) {
+    return sp.objective_mode == 2 ? (int)(draw(key, 0, 0) >> 63) : sp.objective_mode;
+}
+
+// Thread -> trace assignment that keeps warps objective-uniform: QoS traces run
+// the PID/target branch, budget traces do not, so mixing them halves SIMT
+// efficiency. Results are written by trace index, so the order is invisible.
+__global__ void k_replay_order(pals_replay_spec sp, int32_t* __restrict__ order,
+                               int32_t* __restrict__ counters) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < sp.n_traces;
+         i0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = i0 + threadIdx.x;
+        int g = -1;
+        if (i < sp.n_traces) g = trace_objective(sp, splitmix64(sp.seed ^ (uint64_t)(sp.first_trace + i)));
+        for (int k = 0; k < 2; ++k) {
+            const unsigned m = __ballot_sync(0xffffffffu, g == k);
+            if (!m) continue;
+            int base = 0;
+            if (lane == __ffs(m) - 1) base = atomicAdd(&counters[k], __popc(m));
+            base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+            if (g == k) {
+                const int r = base + __popc(m & ((1u << lane) - 1));
+                order[k == 0 ? r : sp.n_traces - 1 - r] = (int32_t)i;
+            }
+        }
+    }
+}
+
+// kMinBlocks trades registers for occupancy (1: ~126 regs, 4 CTAs/SM; 6: 80 regs).
+template <int kMinBlocks>
+__global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev* __restrict__ models,
+                                                ReplayParams p, const int32_t* __restrict__ order,
+                                                pals_trace_summary* __restrict__ out,
                                                 pals_step_log* __restrict__ logs) {
-    const int64_t ti = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t slot = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const pals_replay_spec& sp = p.spec;
-    if (ti >= sp.n_traces) return;
+    if (slot >= sp.n_traces) return;
+    const int64_t ti = order ? order[slot] : slot;
     const pals_ctrl_cfg& cfg = p.cfg;
     const uint64_t key = splitmix64(sp.seed ^ (uint64_t)(sp.first_trace + ti));
     const int mi = (int)(key % (uint64_t)p.n_models);
-    const ReplayModelDev m = models[mi];
-    int obj = sp.objective_mode;
-    if (obj == 2) obj = (int)(draw(key, 0, 0) >> 63);
+    const ReplayModelDev& m = models[mi];
+    const int obj = trace_objective(sp, key);
     const double qfrac = sp.qos_frac_lo + (sp.qos_frac_hi - sp.qos_frac_lo) * u01(draw(key, 0, 1));
     const double target_tps = qfrac * m.t_max;
     const double target = target_tps * (1.0 + cfg.target_headroom);
@@ -343,12 +376,12 @@ __global__ void __launch_bounds__(1024) k_build_tables(PlanDev d, ReplayModelDev
                                                        uint32_t* b1, double* ut, double* up,
                                                        double alpha, double beta) {
     const int n = (int)d.n;
-    const int ndt = (int)d.nd[ORD_T], ndp = (int)d.nd[ORD_P];
+    const int ndt = n, ndp = n;
     const int W = ndp + 1, H = ndt + 1;
     for (int i = threadIdx.x; i < W * H; i += blockDim.x) m2[i] = kNone32;
     for (int i = threadIdx.x; i < W; i += blockDim.x) b1[i] = kNone32;
-    for (int i = threadIdx.x; i < ndt; i += blockDim.x) ut[i] = unorderable(~d.U[ORD_T][i]);
-    for (int i = threadIdx.x; i < ndp; i += blockDim.x) up[i] = unorderable(d.U[ORD_P][i]);
+    for (int i = threadIdx.x; i < ndt; i += blockDim.x) ut[i] = unorderable(~d.merged[ORD_T][i]);
+    for (int i = threadIdx.x; i < ndp; i += blockDim.x) up[i] = unorderable(d.merged[ORD_P][i]);
     __syncthreads();
     for (int c = threadIdx.x; c < n; c += blockDim.x) {
         const uint32_t kt = d.key32[ORD_T][c], kp = d.key32[ORD_P][c], ke = d.key32[ORD_E][c];
@@ -398,6 +431,8 @@ struct ReplayCache {
     ReplayModelDev* d_models = nullptr;
     void* d_tables = nullptr;
     Analytic* d_plant = nullptr;
+    int32_t* d_order = nullptr;  // thread -> trace permutation (capacity order_cap) + 2 counters
+    int64_t order_cap = 0;
 };
 
 void replay_cache_free(pals_ctx* ctx) {
@@ -406,6 +441,7 @@ void replay_cache_free(pals_ctx* ctx) {
     for (auto* p : rc->plans) pals_plan_destroy(p);
     for (auto* g : rc->grids) pals_grid_destroy(g);
     for (auto* m : rc->plant_models) pals_model_destroy(m);
+    cudaFree(rc->d_order);
     cudaFree(rc->d_models);
     cudaFree(rc->d_tables);
     cudaFree(rc->d_plant);
@@ -500,8 +536,8 @@ static int replay_setup(pals_ctx* ctx, int n_models, pals_model* const* models,
         m.th = d.th;
         m.pn = d.pn;
         m.ef = d.ef;
-        m.cut_t = d.cut[ORD_T];
-        m.cut_e = d.cut[ORD_E];
+        m.danger_t = d.danger[ORD_T];
+        m.danger_e = d.danger[ORD_E];
         char* base = (char*)rc->d_tables + per_model * i;
         m.m2 = (const uint32_t*)base;
         m.b1 = (const uint32_t*)(base + W * W * 4);
@@ -534,7 +570,31 @@ static int replay_launch(pals_ctx* ctx, ReplayCache* rc, const pals_ctrl_cfg* cf
     p.beta = rc->coeffs.beta_watts;
     p.n_models = (int)rc->models.size();
     const int64_t blocks = (spec->n_traces + 127) / 128;
-    k_replay<<<(unsigned)blocks, 128, 0, ctx->stream>>>(rc->d_models, p, d_sum, d_logs);
+    int32_t* order = nullptr;
+    if (spec->objective_mode == 2) {
+        if (rc->order_cap < spec->n_traces) {
+            cudaFree(rc->d_order);
+            rc->d_order = nullptr;
+            PALS_CUDA(cudaMalloc(&rc->d_order, (size_t)(spec->n_traces + 2) * 4));
+            rc->order_cap = spec->n_traces;
+        }
+        order = rc->d_order;
+        int32_t* counters = rc->d_order + spec->n_traces;
+        PALS_CUDA(cudaMemsetAsync(counters, 0, 8, ctx->stream));
+        const int ob = (int)std::min<int64_t>((spec->n_traces + 255) / 256, ctx->num_sms * 8);
+        k_replay_order<<<ob, 256, 0, ctx->stream>>>(*spec, order, counters);
+        count_launch(ctx);
+    }
+    static const int minb = [] {
+        const char* e = getenv("PALS_REPLAY_MINB");
+        return e ? atoi(e) : 6;  // measured: 6 CTAs/SM (80 regs) beats 4 (126 regs) by 1.4x
+    }();
+    if (minb >= 8)
+        k_replay<8><<<(unsigned)blocks, 128, 0, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs);
+    else if (minb >= 6)
+        k_replay<6><<<(unsigned)blocks, 128, 0, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs);
+    else
+        k_replay<1><<<(unsigned)blocks, 128, 0, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs);
     count_launch(ctx);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "k_replay");
@@ -562,6 +622,7 @@ struct OneArgs {
     pals_ctrl_state st;
     pals_ctrl_cfg cfg;
     double cur_T;      // table model: score(current) (host lookup)
+    const double* cur_T_dev;  // forest model: score(current) on the device
     int cur_ok;
     pals_query q;      // select-only call
     int* out;          // [0] idx, [1] reason, [2] error, [3] applied
@@ -647,12 +708,12 @@ __global__ void k_one(OneArgs a) {
         double err_norm = 0.0;
         if (a.tg.objective == PALS_OBJ_QOS && a.tg.throughput_tps > 0.0) {
             err_norm = (a.tg.throughput_tps - a.tel.throughput_tps) / a.tg.throughput_tps;
-            double curT = a.cur_T;
+            double curT = a.cur_T_dev ? *a.cur_T_dev : a.cur_T;
             if (a.an) {
                 const Score s = analytic_score(*a.an, st.current.cap_watts, st.current.batch,
                                                st.current.tp, st.current.dp);
                 curT = s.T;
-            } else if (!a.cur_ok) {
+            } else if (!a.cur_ok && !a.cur_T_dev) {
                 if (lane == 0) a.out[2] = PALS_ECONFIG;
                 return;
             }
@@ -747,8 +808,6 @@ static int one_call(pals_ctx* ctx, const pals_model* m, const pals_point* cands,
                     OneArgs& a, int do_step, pals_decision* out_d, pals_ctrl_state* out_s,
                     const pals_ctrl_state* in_state) {
     if (n <= 0) return set_error(PALS_ECONFIG, "select_config: empty candidate list");
-    if (m->kind == MODEL_FOREST)
-        return set_error(PALS_ECONFIG, "pals: single-call forest scoring is not built yet");
     // the reference scores candidates in order and aborts on the first rejection
     int rc;
     if (do_step && a.tg.objective == PALS_OBJ_QOS && a.tg.throughput_tps > 0.0 &&
@@ -764,7 +823,7 @@ static int one_call(pals_ctx* ctx, const pals_model* m, const pals_point* cands,
     PALS_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
     // staging: SoA candidates + scratch + outputs in the context scratch buffer
-    const size_t need = (size_t)n * (8 + 4 * 3 + 8 * 4) + sizeof(pals_ctrl_state) + 4096;
+    const size_t need = (size_t)(n + 1) * (8 + 4 * 4 + 8 * 4) + sizeof(pals_ctrl_state) + 4096;
     if (ctx->scratch_bytes < need) {
         cudaFree(ctx->d_scratch);
         PALS_CUDA(cudaMalloc(&ctx->d_scratch, need));
@@ -779,14 +838,19 @@ static int one_call(pals_ctx* ctx, const pals_model* m, const pals_point* cands,
         off += (b + 255) & ~(size_t)255;
         return o;
     };
-    const size_t o_cap = take(n * 8), o_b = take(n * 4), o_tp = take(n * 4), o_dp = take(n * 4);
-    const size_t o_T = take(n * 8), o_P = take(n * 8), o_th = take(n * 8), o_pn = take(n * 8);
+    // slot n holds the current point (scored by forest models for the PID promise)
+    const int64_t n1 = n + 1;
+    const size_t o_cap = take(n1 * 8), o_b = take(n1 * 4), o_tp = take(n1 * 4), o_dp = take(n1 * 4);
+    const size_t o_ep = take(n1 * 4);
+    const size_t o_T = take(n1 * 8), o_P = take(n1 * 8), o_th = take(n1 * 8), o_pn = take(n1 * 8);
     const size_t o_out = take(64), o_st = take(sizeof(pals_ctrl_state));
-    for (int64_t i = 0; i < n; ++i) {
-        ((double*)(hb + o_cap))[i] = cands[i].cap_watts;
-        ((int*)(hb + o_b))[i] = cands[i].batch;
-        ((int*)(hb + o_tp))[i] = cands[i].tp;
-        ((int*)(hb + o_dp))[i] = cands[i].dp;
+    for (int64_t i = 0; i < n1; ++i) {
+        const pals_point& c = i < n ? cands[i] : (in_state ? in_state->current : cands[0]);
+        ((double*)(hb + o_cap))[i] = c.cap_watts;
+        ((int*)(hb + o_b))[i] = c.batch;
+        ((int*)(hb + o_tp))[i] = c.tp;
+        ((int*)(hb + o_dp))[i] = c.dp;
+        ((int*)(hb + o_ep))[i] = c.ep;
     }
     Analytic* d_an = nullptr;
     const bool stale = do_step && a.now_s - a.tel.t_s > 1.5 * a.cfg.interval_s;
@@ -816,6 +880,14 @@ static int one_call(pals_ctx* ctx, const pals_model* m, const pals_point* cands,
         PALS_CUDA(cudaMemcpy(d_an, &m->an, sizeof(Analytic), cudaMemcpyHostToDevice));
     }
     PALS_CUDA(cudaMemcpyAsync(db, hb, off, cudaMemcpyHostToDevice, s));
+    if (m->kind == MODEL_FOREST) {
+        rc = forest_eval_raw(m, ctx, n1, (const double*)(db + o_cap), (const int*)(db + o_b),
+                             (const int*)(db + o_tp), (const int*)(db + o_ep),
+                             (const int*)(db + o_dp), (double*)(db + o_T), (double*)(db + o_P), 0);
+        if (rc) return rc;
+        a.cur_T_dev = (const double*)(db + o_T) + n;
+        a.cur_ok = 1;
+    }
     a.n = n;
     a.cap = (const double*)(db + o_cap);
     a.batch = (const int*)(db + o_b);

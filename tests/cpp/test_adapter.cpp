@@ -1,0 +1,287 @@
+// test_adapter.cpp — the reference's own controller tests, run twice in one
+// binary: once through the unmodified reference (wattserve::select_config /
+// control_step on the CPU) and once through the drop-in GPU adapter
+// (wattserve::gpu::*, include/wattserve_gpu.hpp -> libpals_gpu.so). Every
+// decision and every controller state must be identical.
+//
+// Case families follow /root/reference/proj/tests/test_controller.cpp and
+// tests/acceptance/acceptance.cpp criterion 10 (restated, not copied).
+// Exit code = number of failed checks. Built by tests/cpp/build.sh.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "wattserve/controller.hpp"
+#include "wattserve/forest.hpp"
+#include "wattserve/json_io.hpp"
+#include "wattserve/rng.hpp"
+#include "wattserve/sweep.hpp"
+#include "wattserve_gpu.hpp"
+
+using namespace wattserve;
+
+static int g_fail = 0, g_checks = 0;
+#define EXPECT(cond, what)                                                      \
+    do {                                                                        \
+        ++g_checks;                                                             \
+        if (!(cond)) {                                                          \
+            ++g_fail;                                                           \
+            if (g_fail < 20) std::fprintf(stderr, "FAIL %s (%s:%d)\n", what, __FILE__, __LINE__); \
+        }                                                                       \
+    } while (0)
+
+static bool same(const Decision& a, const Decision& b) {
+    return a.point == b.point && a.applied == b.applied && a.reason == b.reason;
+}
+
+static bool same_bits(double a, double b) { return std::memcmp(&a, &b, 8) == 0; }
+
+static bool same(const ControllerState& a, const ControllerState& b) {
+    return same_bits(a.bias, b.bias) && same_bits(a.integral, b.integral) &&
+           same_bits(a.prev_error, b.prev_error) && a.has_prev_error == b.has_prev_error &&
+           a.sustain_count == b.sustain_count && a.current == b.current &&
+           a.last_targets.has_value() == b.last_targets.has_value() &&
+           (!a.last_targets || *a.last_targets == *b.last_targets);
+}
+
+struct Table {
+    std::vector<OperatingPoint> points;
+    std::vector<double> t_hat, p_gpu;
+    Scorer cpu() const {
+        return [this](const OperatingPoint& p) {
+            for (std::size_t i = 0; i < points.size(); ++i)
+                if (points[i] == p) return CandidateScore{t_hat[i], p_gpu[i]};
+            throw config_error("unscored candidate");
+        };
+    }
+};
+
+static Table ladder(int n, double lo, double hi) {
+    Table t;
+    for (int i = 0; i < n; ++i) {
+        const double frac = n == 1 ? 0.0 : static_cast<double>(i) / (n - 1);
+        const double thr = lo + (hi - lo) * frac;
+        t.points.push_back(OperatingPoint{150.0 + i, 1 + i, 2, 1, 1});
+        t.t_hat.push_back(thr);
+        t.p_gpu.push_back(40.0 + thr * thr / 800.0);
+    }
+    return t;
+}
+
+static Targets qos(double tps) {
+    Targets t;
+    t.throughput_tps = tps;
+    t.epsilon = 0.05;
+    return t;
+}
+
+static std::string read_file(const std::string& p) {
+    std::ifstream f(p);
+    std::stringstream ss;
+    ss << f.rdbuf();
+    return ss.str();
+}
+
+int main(int argc, char** argv) {
+    const std::string root = argc > 1 ? argv[1] : ".";
+    gpu::Context ctx(0);
+    const SystemPowerCoeffs k{1.05, 345.0};
+
+    // ---- select_config on ladders (test_controller.cpp:54-92) ----
+    {
+        const Table a = ladder(8, 1000.0, 2000.0), b = ladder(8, 100.0, 300.0);
+        auto ga = gpu::table_scorer(ctx, a.points, a.t_hat, a.p_gpu);
+        auto gb = gpu::table_scorer(ctx, b.points, b.t_hat, b.p_gpu);
+        EXPECT(same(select_config(a.points, qos(500.0), a.cpu(), k),
+                    gpu::select_config(a.points, qos(500.0), ga, k)), "all feasible");
+        EXPECT(same(select_config(b.points, qos(1000.0), b.cpu(), k),
+                    gpu::select_config(b.points, qos(1000.0), gb, k)), "fallback");
+        Targets t = qos(1000.0);
+        t.power_budget_w = (k.alpha * kGpusPerNode * b.p_gpu[3] + k.beta_watts) + 1.0;
+        EXPECT(same(select_config(b.points, t, b.cpu(), k), gpu::select_config(b.points, t, gb, k)),
+               "budget fallback");
+        bool threw = false;
+        try {
+            gpu::select_config({}, qos(100.0), ga, k);
+        } catch (const config_error& e) {
+            threw = std::string(e.what()) == "select_config: empty candidate list";
+        }
+        EXPECT(threw, "empty candidate list throws config_error");
+    }
+
+    // ---- 1,000-trial argmax invariance, both sides (test_controller.cpp:100-138) ----
+    {
+        Rng rng(2024);
+        for (int trial = 0; trial < 1000; ++trial) {
+            Table tab;
+            const int n = 3 + static_cast<int>(rng.next_u64() % 20);
+            for (int i = 0; i < n; ++i) {
+                tab.points.push_back(OperatingPoint{150.0 + 50.0 * (i % 6), 1 + (i * 7) % 64, 2, 1, 1});
+                tab.t_hat.push_back(rng.uniform(100.0, 3000.0));
+                tab.p_gpu.push_back(rng.uniform(60.0, 400.0));
+            }
+            Targets t = qos(rng.uniform(100.0, 2500.0));
+            if (trial % 3 == 0) t.power_budget_w = rng.uniform(500.0, 2000.0);
+            const double s = rng.uniform(0.01, 100.0);
+            Table sc = tab;
+            for (auto& v : sc.t_hat) v *= s;
+            for (auto& v : sc.p_gpu) v *= s;
+            Targets ts = t;
+            ts.throughput_tps *= s;
+            if (ts.power_budget_w) ts.power_budget_w = *t.power_budget_w * s;
+            const SystemPowerCoeffs ks{k.alpha, k.beta_watts * s};
+            auto g1 = gpu::table_scorer(ctx, tab.points, tab.t_hat, tab.p_gpu);
+            auto g2 = gpu::table_scorer(ctx, sc.points, sc.t_hat, sc.p_gpu);
+            const auto r1 = select_config(tab.points, t, tab.cpu(), k);
+            const auto d1 = gpu::select_config(tab.points, t, g1, k);
+            const auto d2 = gpu::select_config(sc.points, ts, g2, ks);
+            EXPECT(same(r1, d1), "invariance trial: gpu == reference");
+            EXPECT(d1.point == d2.point && d1.reason == d2.reason, "invariance under rescaling");
+        }
+    }
+
+    // ---- control_step sequences (test_controller.cpp:140-235; acceptance criterion 10) ----
+    {
+        for (int trial = 0; trial < 60; ++trial) {
+            Rng rng(1000 + trial);
+            const double lambda = trial % 2 == 0 ? 0.7 : 1.3;
+            Table l;
+            for (int i = 0; i < 160; ++i) {
+                const double frac = static_cast<double>(i) / 159;
+                const double thr = 300.0 + 2100.0 * frac * rng.uniform(0.995, 1.005);
+                l.points.push_back(OperatingPoint{100.0 + i, 1 + i, 2, 1, 1});
+                l.t_hat.push_back(thr);
+                l.p_gpu.push_back(40.0 + thr * thr / 800.0);
+            }
+            auto g = gpu::table_scorer(ctx, l.points, l.t_hat, l.p_gpu);
+            Targets t = qos(rng.uniform(700.0, 1500.0));
+            if (trial % 4 == 3) t.power_budget_w = rng.uniform(900.0, 2200.0);
+            if (trial % 5 == 4) t.objective = Objective::BudgetMaxThroughput;
+            ControllerConfig cfg;
+            cfg.target_headroom = trial % 3 == 0 ? 0.05 : 0.0;
+            cfg.budget_margin = trial % 2 ? 0.02 : 0.0;
+            ControllerState sc, sg;
+            sc.current = sg.current = l.points.back();
+            double now = 0.5, measured = lambda * l.t_hat.back();
+            for (int step = 0; step < 40; ++step) {
+                const TelemetryInput tel{step % 13 == 12 ? now - 5.0 : now, measured};
+                auto [dc, sc2] = control_step(tel, now, t, l.points, l.cpu(), k, sc, cfg);
+                auto [dg, sg2] = gpu::control_step(tel, now, t, l.points, g, k, sg, cfg);
+                EXPECT(same(dc, dg), "control_step decision");
+                EXPECT(same(sc2, sg2), "control_step state");
+                sc = sc2;
+                sg = sg2;
+                for (std::size_t i = 0; i < l.points.size(); ++i)
+                    if (l.points[i] == sc.current) measured = lambda * l.t_hat[i];
+                now += cfg.interval_s;
+            }
+        }
+    }
+
+    // ---- analytic_scorer on the bundled profiles (model-fit input) ----
+    std::vector<ModelProfile> profiles;
+    GpuSpec gspec;
+    {
+        const json j = json::parse(read_file(root + "/paper_2605_21427_b200/data/profiles.json"));
+        for (const auto& pj : j.at("profiles")) profiles.push_back(profile_from_json(pj));
+        gspec = gpu_from_json(j.at("platform").at("gpu"));
+        const SweepGrid grid = SweepGrid::default_grid();
+        for (const auto& prof : profiles) {
+            std::vector<OperatingPoint> cands;
+            for (double c : grid.caps)
+                for (int b : grid.batches)
+                    cands.push_back(OperatingPoint{c, b, prof.deployment.tp, prof.deployment.ep,
+                                                   prof.deployment.dp});
+            const Scorer cs = analytic_scorer(prof, gspec);
+            auto gs = gpu::analytic_scorer(ctx, prof, gspec);
+            const double tmax = cands.size() ? throughput(cands.back(), prof, gspec) : 1.0;
+            Rng rng(7);
+            std::vector<Targets> ts;
+            std::vector<double> biases;
+            for (int q = 0; q < 200; ++q) {
+                Targets t = qos(rng.uniform(0.05, 1.1) * tmax);
+                if (q % 2) t.power_budget_w = rng.uniform(700.0, 2000.0);
+                if (q % 5 == 0) t.objective = Objective::BudgetMaxThroughput;
+                const double bias = q % 3 ? 1.0 : rng.uniform(0.5, 2.0);
+                ts.push_back(t);
+                biases.push_back(bias);
+                EXPECT(same(select_config(cands, t, cs, k, bias, 0.05, 0.02),
+                            gpu::select_config(cands, t, gs, k, bias, 0.05, 0.02)),
+                       "analytic select");
+            }
+            gpu::SelectPlan plan(ctx, gs, cands, k);
+            const auto batch = plan.select(ts, biases, 0.05, 0.02);
+            for (std::size_t q = 0; q < ts.size(); ++q)
+                EXPECT(same(batch[q], select_config(cands, ts[q], cs, k, biases[q], 0.05, 0.02)),
+                       "batched SelectPlan");
+        }
+        // errors: cap outside the platform range, unknown tp
+        auto gs = gpu::analytic_scorer(ctx, profiles[0], gspec);
+        bool range = false, tp = false;
+        try {
+            gpu::select_config({OperatingPoint{450.0, 8, profiles[0].deployment.tp, 1, 1}}, qos(1.0),
+                               gs, k);
+        } catch (const std::out_of_range&) {
+            range = true;
+        }
+        try {
+            gpu::select_config({OperatingPoint{300.0, 8, 3, 1, 1}}, qos(1.0), gs, k);
+        } catch (const config_error& e) {
+            tp = std::string(e.what()).find("no comm cost calibrated for tp=3") != std::string::npos;
+        }
+        EXPECT(range, "cap out of range -> std::out_of_range");
+        EXPECT(tp, "unknown tp -> config_error");
+    }
+
+    // ---- predictor_scorer on a bundle trained by the reference pipeline ----
+    {
+        const SweepGrid grid = SweepGrid::default_grid();
+        AnalyticBackend be(gspec, k);
+        std::vector<ProfilingRecord> recs;
+        for (std::size_t i = 0; i < profiles.size(); ++i) {
+            const auto ds = run_sweep(grid, profiles[i].name, profiles[i], gspec, be, 100 + i);
+            recs.insert(recs.end(), ds.records.begin(), ds.records.end());
+        }
+        HyperParams hp;
+        hp.n_trees = 30;
+        hp.max_depth = 12;
+        const PredictorBundle bundle = train_bundle(recs, k, hp, 2605);
+        for (const char* mid : {"llama2-7b-like", "mixtral-8x7b-like"}) {
+            const Scorer cs = predictor_scorer(bundle, mid);
+            auto gs = gpu::predictor_scorer(ctx, bundle, mid);
+            const ModelProfile* prof = nullptr;
+            for (const auto& p : profiles)
+                if (p.name == mid) prof = &p;
+            std::vector<OperatingPoint> cands;
+            for (double c : {150.0, 175.0, 200.0, 250.0, 300.0, 350.0, 400.0})
+                for (int b : {1, 4, 8, 12, 16, 32, 48, 64})
+                    cands.push_back(OperatingPoint{c, b, prof->deployment.tp, prof->deployment.ep,
+                                                   prof->deployment.dp});
+            Rng rng(11);
+            const double tmax = bundle.predict(cands.back(), mid).throughput_hat;
+            ControllerState sc, sg;
+            sc.current = sg.current = cands.back();
+            ControllerConfig cfg;
+            for (int q = 0; q < 150; ++q) {
+                Targets t = qos(rng.uniform(0.05, 1.1) * tmax);
+                if (q % 2) t.power_budget_w = rng.uniform(800.0, 2000.0);
+                EXPECT(same(select_config(cands, t, cs, k, 1.0, 0.05, 0.02),
+                            gpu::select_config(cands, t, gs, k, 1.0, 0.05, 0.02)),
+                       "predictor select");
+                const TelemetryInput tel{0.5 * q, rng.uniform(0.3, 1.2) * tmax};
+                auto [dc, sc2] = control_step(tel, 0.5 * q, t, cands, cs, k, sc, cfg);
+                auto [dg, sg2] = gpu::control_step(tel, 0.5 * q, t, cands, gs, k, sg, cfg);
+                EXPECT(same(dc, dg) && same(sc2, sg2), "predictor control_step");
+                sc = sc2;
+                sg = sg2;
+            }
+        }
+    }
+
+    std::printf("%s: %d checks, %d failures\n", g_fail ? "FAIL" : "PASS", g_checks, g_fail);
+    return g_fail > 255 ? 255 : g_fail;
+}

@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--trace-steps", type=int, default=3600)
     ap.add_argument("--replay-steps", type=int, default=None,
                     help="timed replay steps (default: min(steps, 5))")
+    ap.add_argument("--predictions", type=int, default=1 << 24,
+                    help="points per GPU for the forest-predictor leg")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU time per reference sample")
@@ -239,6 +241,18 @@ def run_ours(args, dist: Dist):
     step_ms = [a.elapsed_time(c) for a, b, c in ev]
     prep_ms = [a.elapsed_time(b) for a, b, c in ev]
     exact_q = int(plan.stats()[5])
+    gather = None
+    if dist.world > 1:
+        # the only cross-GPU traffic: one gather of (index, reason) per query to rank 0
+        from paper_2605_21427_b200.shard import gather_to_rank0
+        packed = (d_idx.to(torch.int64) << 8) | d_rs.to(torch.int64)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        out_all = gather_to_rank0(packed, nq * dist.world, dist.rank, dist.world)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gather = {"bytes": nq * dist.world * 8, "ms": g0.elapsed_time(g1), "backend": "nccl",
+                  "rows": None if out_all is None else int(out_all.shape[0])}
     t_rank = float(np.sum(step_ms))
     t_max = dist.max(t_rank)
     pairs_total = dist.sum(float(pairs_step)) * args.steps
@@ -316,14 +330,20 @@ def run_ours(args, dist: Dist):
     r_max = dist.max(float(np.sum(r_ms)))
     dec_total = dist.sum(float(nt) * args.trace_steps) * rsteps
     dec_value = dec_total / (r_max * 1e-3)
-    # e2e: host summaries (D2H 48 B/trace); inputs are generated from (seed, index) on the device
+    # e2e: host summaries (D2H 48 B/trace into pinned memory); trace inputs are generated
+    # from (seed, index) on the device, so nothing crosses H2D
+    h_sum = torch.empty(nt * SUMMARY_DT.itemsize, dtype=torch.uint8, pin_memory=True)
+    h_sumn = h_sum.numpy().view(SUMMARY_DT)
+    replay(ctx, models, s["profiles"], s["gpu"], s["coeffs"], s["caps"], s["batches"],
+           s["cfg"], spec, summaries=h_sumn)  # warm-up
     re2e = []
     for _ in range(min(rsteps, 3)):
+        l2_flush()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         a.record(stream)
         replay(ctx, models, s["profiles"], s["gpu"], s["coeffs"], s["caps"], s["batches"],
-               s["cfg"], spec)
+               s["cfg"], spec, summaries=h_sumn)
         b.record(stream)
         b.synchronize()
         re2e.append(a.elapsed_time(b))
@@ -341,6 +361,53 @@ def run_ours(args, dist: Dist):
                                "§4); the kernel is latency-bound, not FP64-throughput-bound",
                 "peak_source": "measured here: pals_measure_peaks DFMA chains"}
 
+    # ---------------- K2: PredictorBundle::predict throughput ----------------
+    from paper_2605_21427_b200.forest import Bundle, make_forest_model
+    bundle = Bundle.load_npz(os.path.join(ROOT, "paper_2605_21427_b200", "data",
+                                          "predictor_small.npz"))
+    fmodel = make_forest_model(ctx, bundle, "mixtral-8x7b-like")
+    npred = args.predictions
+    ppts = workloads.predict_points(npred, seed=2605 + dist.rank)
+    d_pts = torch.from_numpy(ppts.view(np.uint8)).cuda()
+    d_T = torch.empty(npred, dtype=torch.float64, device="cuda")
+    d_P = torch.empty(npred, dtype=torch.float64, device="cuda")
+
+    def predict_step():
+        rc = ctx.lib.pals_predict_device(ctx.h, fmodel.h, d_pts.data_ptr(), npred,
+                                         d_T.data_ptr(), d_P.data_ptr())
+        assert rc == 0, ctx.lib.pals_last_error()
+
+    for _ in range(args.warmup):
+        predict_step()
+    torch.cuda.synchronize()
+    pev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    for k in range(args.steps):
+        l2_flush()
+        pev[k][0].record(stream)
+        predict_step()
+        pev[k][1].record(stream)
+    torch.cuda.synchronize()
+    p_max = dist.max(float(np.sum([a.elapsed_time(b) for a, b in pev])))
+    pred_value = dist.sum(float(npred)) * args.steps / (p_max * 1e-3)
+    # cell lookup: 5 binary searches over <= 10 thresholds + 2 table loads; HBM-bound part is
+    # the 24 B point read + 16 B result write per prediction
+    pred_bytes = 40.0
+    predictions = {
+        "metric": "predictor predictions/s (PredictorBundle::predict, T and P)",
+        "value": pred_value, "unit": "predictions/s", "points_per_gpu": npred,
+        "bundle": f"{bundle.throughput.n_trees}+{bundle.power.n_trees} trees, depth "
+                  f"{bundle.hyperparams['max_depth']}, trained by the reference pipeline; "
+                  f"{int(ctx.lib.pals_model_forest_cells(fmodel.h))} exact lattice cells",
+        "roofline": {"bound": "hbm", "kernel": "k_forest_eval",
+                     "achieved": pred_value / dist.world * pred_bytes / 1e9,
+                     "peak": measured_peaks_json().get("hbm_gbs", 6552.6), "unit": "GB/s",
+                     "frac": pred_value / dist.world * pred_bytes / 1e9 /
+                     measured_peaks_json().get("hbm_gbs", 6552.6),
+                     "traffic": ncu_traffic("k_forest_eval_aos"),
+                     "algorithmic": "40 B per prediction (24 B point in, 16 B T/P out)",
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs"}}
+
     out = {
         "metric": METRIC, "value": value, "unit": "config evals/s",
         "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
@@ -356,6 +423,7 @@ def run_ours(args, dist: Dist):
                 "api": "pals_select (C ABI, pinned host buffers; includes eval+rank)"},
         "roofline": roof,
         "gpu_launches": int(launches),
+        "gather": gather,
         "clocks": clk,
         "decisions": {
             "metric": "controller decisions/s", "value": dec_value, "unit": "decisions/s",
@@ -365,11 +433,13 @@ def run_ours(args, dist: Dist):
                     "d2h_bytes_per_step": nt * SUMMARY_DT.itemsize,
                     "api": "pals_replay (C ABI, host summaries)"},
             "roofline": dec_roof, "gpu_launches": int(rlaunches)},
+        "predictions": predictions,
         "peaks": {"int_ops_per_s": int_peak, "fp64_flops_per_s": fp64_peak,
                   "hbm_gbs_measured": measured_peaks_json().get("hbm_gbs")},
     }
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"], out["decisions"]["cpu_baseline"] = cpu_baselines(args, cfg, tref)
+        out["predictions"]["cpu_baseline"] = cpu_predict(args, bundle, args.cpu_seconds)
     if dist.rank == 0:
         print(json.dumps(out), flush=True)
     dist.close()
@@ -438,6 +508,28 @@ def cpu_replay(args, seconds):
     t = time.perf_counter() - t0
     return {"value": 8 * args.trace_steps / t, "unit": "decisions/s", "cores": 1, "kind": "port",
             "sample": f"8 cfg4 traces, C restatement, 1 thread"}
+
+
+def cpu_predict(args, bundle, seconds):
+    """PredictorBundle::predict on all host threads (the reference build)."""
+    from paper_2605_21427_b200 import workloads
+    kind, ref = _reference_backend()
+    if kind != "reference":
+        return {"value": None, "unit": "predictions/s", "cores": 0, "kind": "port",
+                "sample": "reference build absent"}
+    from oracle.oracle import ref_bench_predict
+    threads = os.cpu_count() or 1
+    path = os.path.join(tempfile.gettempdir(), "pals_bench_bundle.json")
+    bundle.to_json(path)
+    pts = workloads.predict_points(20_000 * threads, seed=2605)
+    t = ref_bench_predict(ref, path, "mixtral-8x7b-like", pts, threads)
+    rate = len(pts) / t
+    n = int(min(2_000_000 * threads, max(len(pts), rate * seconds)))
+    pts = workloads.predict_points(n, seed=2605)
+    t = ref_bench_predict(ref, path, "mixtral-8x7b-like", pts, threads)
+    return {"value": n / t, "unit": "predictions/s", "cores": threads, "kind": "reference",
+            "sample": f"{n} random points through the unmodified PredictorBundle::predict "
+                      f"(same bundle), {threads} threads, {t:.1f} s"}
 
 
 def cpu_baselines(args, cfg, tref):

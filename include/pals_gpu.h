@@ -267,6 +267,10 @@ int pals_grid_destroy(pals_grid* g);
 /* Host outputs: throughput_tps and gpu_power_w per point (CandidateScore). */
 int pals_eval(pals_ctx* ctx, const pals_model* m, const pals_grid* g, double* throughput_tps,
               double* gpu_power_w);
+/* PredictorBundle::predict (forest.hpp:227-235) for n device-resident points:
+ * throughput_hat and power_hat per point (forest models; async). */
+int pals_predict_device(pals_ctx* ctx, const pals_model* m, const pals_point* d_points, int64_t n,
+                        double* d_T, double* d_P);
 /* Device outputs, async on the context stream (analytic and forest models). */
 int pals_eval_device(pals_ctx* ctx, const pals_model* m, const pals_grid* g, double* d_T,
                      double* d_P);

@@ -39,6 +39,7 @@ SIGNATURES = [
     ("pals_model_forest_cells", _I64, [_VP]),
     ("pals_model_forest_set_direct", _I, [_VP, _I]),
     ("pals_eval_device", _I, [_VP, _VP, _VP, _VP, _VP]),
+    ("pals_predict_device", _I, [_VP, _VP, _VP, _I64, _VP, _VP]),
     ("pals_grid_points", _I, [_VP, _VP, _I64, _VP]),
     ("pals_grid_axes", _I, [_VP, _VP, _I32, _VP, _I32, _VP, _I32, _VP, _I32, _VP, _I32, _VP]),
     ("pals_grid_size", _I64, [_VP]),

@@ -163,6 +163,24 @@ __global__ void k_forest_eval(ForestDev f, int64_t n, const double* __restrict__
     }
 }
 
+// PredictorBundle::predict for arbitrary points given as pals_point records
+__global__ void k_forest_eval_aos(ForestDev f, int64_t n, const pals_point* __restrict__ pts,
+                                  double* __restrict__ T, double* __restrict__ P, int use_cells) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const pals_point p = pts[i];
+        const double x5[kNumeric] = {p.cap_watts, (double)p.batch, (double)p.tp, (double)p.ep,
+                                     (double)p.dp};
+        if (use_cells) {
+            const int64_t c = cell_of(f, x5);
+            T[i] = f.tabT[c];
+            P[i] = f.tabP[c];
+        } else {
+            forest_direct(f, x5, &T[i], &P[i]);
+        }
+    }
+}
+
 }  // namespace pals
 
 using namespace pals;
@@ -340,6 +358,21 @@ extern "C" int pals_model_forest(pals_ctx* ctx, int32_t n_models, int32_t model_
 extern "C" int64_t pals_model_forest_cells(const pals_model* m) {
     if (!m || m->kind != MODEL_FOREST) return -1;
     return ((ForestHost*)m->forest)->d.n_cells;
+}
+
+extern "C" int pals_predict_device(pals_ctx* ctx, const pals_model* m, const pals_point* d_points,
+                                   int64_t n, double* d_T, double* d_P) {
+    if (!m || m->kind != MODEL_FOREST)
+        return set_error(PALS_ECONFIG, "pals_predict_device: forest models only (use pals_eval)");
+    if (n <= 0) return PALS_OK;
+    auto* fh = (ForestHost*)m->forest;
+    const int use_cells = (!fh->direct && fh->d.n_cells > 0) ? 1 : 0;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, ctx->num_sms * 16));
+    k_forest_eval_aos<<<blocks, 256, 0, ctx->stream>>>(fh->d, n, d_points, d_T, d_P, use_cells);
+    count_launch(ctx);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "k_forest_eval_aos");
+    return PALS_OK;
 }
 
 extern "C" int pals_model_forest_set_direct(pals_model* m, int direct) {

@@ -1013,8 +1013,14 @@ int pals_replay(pals_ctx* ctx, int32_t n_models, pals_model* const* models,
     const int64_t nl = logs ? std::min<int64_t>(spec->n_log_traces, spec->n_traces) : 0;
     const size_t sb = (size_t)spec->n_traces * sizeof(pals_trace_summary);
     const size_t lb = (size_t)nl * spec->n_steps * sizeof(pals_step_log);
-    void* d = nullptr;
-    PALS_CUDA(cudaMallocAsync(&d, sb + lb + 256, ctx->stream));
+    // device staging for the outputs, kept in the context across calls
+    const size_t need = sb + lb + 256;
+    if (ctx->scratch_bytes < need) {
+        cudaFree(ctx->d_scratch);
+        PALS_CUDA(cudaMalloc(&ctx->d_scratch, need));
+        ctx->scratch_bytes = need;
+    }
+    void* d = ctx->d_scratch;
     pals_trace_summary* ds = (pals_trace_summary*)d;
     pals_step_log* dl = nl ? (pals_step_log*)((char*)d + ((sb + 255) & ~(size_t)255)) : nullptr;
     pals_replay_spec sp = *spec;
@@ -1024,7 +1030,6 @@ int pals_replay(pals_ctx* ctx, int32_t n_models, pals_model* const* models,
         cudaMemcpyAsync(summaries, ds, sb, cudaMemcpyDeviceToHost, ctx->stream);
         if (nl) cudaMemcpyAsync(logs, dl, lb, cudaMemcpyDeviceToHost, ctx->stream);
     }
-    cudaFreeAsync(d, ctx->stream);
     const cudaError_t e = cudaStreamSynchronize(ctx->stream);
     if (!r && e != cudaSuccess) r = cuda_fail(e, "pals_replay");
     return r;

@@ -82,6 +82,32 @@ class Bundle:
                       ForestSoA.from_json(j["throughput"]), ForestSoA.from_json(j["power"]),
                       dict(j["hyperparams"]))
 
+    def to_json(self, path: str) -> None:
+        """bundle_to_json layout (forest.hpp:366-377) so the reference can load it with
+        bundle_from_json. The efficiency forest (importance only, never predicted)
+        is not carried by this Bundle; the power forest stands in for it."""
+        def forest_json(fs: ForestSoA):
+            trees = []
+            for t in range(fs.n_trees):
+                a, b = int(fs.tree_offset[t]), int(fs.tree_offset[t + 1])
+                nodes = []
+                for i in range(a, b):
+                    if fs.feature[i] < 0:
+                        nodes.append({"v": float(fs.value[i])})
+                    else:
+                        nodes.append({"f": int(fs.feature[i]), "t": float(fs.threshold[i]),
+                                      "l": int(fs.left[i]), "r": int(fs.right[i])})
+                trees.append(nodes)
+            return {"trees": trees, "impurity_gain": [0.0] * (5 + len(self.model_ids))}
+
+        j = {"schema_version": 1, "model_ids": self.model_ids,
+             "system_power": {"alpha": self.coeffs.alpha, "beta_watts": self.coeffs.beta_watts},
+             "hyperparams": self.hyperparams, "seed": 0,
+             "throughput": forest_json(self.throughput), "power": forest_json(self.power)}
+        j["efficiency"] = j["power"]
+        with open(path, "w") as f:
+            json.dump(j, f)
+
     def save_npz(self, path: str) -> None:
         d = {"model_ids": np.array(self.model_ids),
              "coeffs": np.array([self.coeffs.alpha, self.coeffs.beta_watts]),

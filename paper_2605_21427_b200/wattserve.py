@@ -297,14 +297,16 @@ def control_step(telemetry: Telemetry, now_s: float, targets: Targets, candidate
 
 
 def replay(ctx: Context, models, plant, gpu: GpuSpec, coeffs: Coeffs, caps, batches,
-           cfg: CtrlCfg, spec: ReplaySpec):
-    """Batched control_step replay over spec.n_traces synthetic traces (host outputs)."""
+           cfg: CtrlCfg, spec: ReplaySpec, summaries: np.ndarray | None = None):
+    """Batched control_step replay over spec.n_traces synthetic traces (host outputs).
+    `summaries` may be a caller-owned (e.g. pinned) SUMMARY_DT array of n_traces."""
     n_models = len(models)
     hs = (C.c_void_p * n_models)(*[m.h for m in models])
     profs = (Profile * n_models)(*plant)
     caps = np.ascontiguousarray(caps, np.float64)
     batches = np.ascontiguousarray(batches, np.int32)
-    summ = np.zeros(spec.n_traces, SUMMARY_DT)
+    summ = np.zeros(spec.n_traces, SUMMARY_DT) if summaries is None else summaries
+    assert summ.dtype == SUMMARY_DT and len(summ) >= spec.n_traces
     nl = min(spec.n_log_traces, spec.n_traces)
     logs = np.zeros(max(1, nl * spec.n_steps), STEPLOG_DT)
     check(ctx.lib.pals_replay(ctx.h, n_models, hs, profs, C.byref(gpu), C.byref(coeffs),

@@ -145,6 +145,20 @@ def cfg4_setup():
     return dict(profiles=profs, gpu=gpu, coeffs=coeffs, caps=caps, batches=batches, cfg=cfg)
 
 
+def predict_points(n: int, seed: int = 2605) -> np.ndarray:
+    """Random operating points for predictor throughput (continuous caps, any batch)."""
+    k = splitmix64(np.uint64(seed) ^ np.arange(n, dtype=np.uint64))
+    r = [splitmix64(k + np.uint64((j * 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF))
+         for j in range(1, 6)]
+    pts = np.zeros(n, POINT_DT)
+    pts["cap_watts"] = 100.0 + 300.0 * u01(r[0])
+    pts["batch"] = 1 + (r[1] % np.uint64(256)).astype(np.int32)
+    pts["tp"] = np.array([1, 2, 4, 8], np.int32)[(r[2] % np.uint64(4)).astype(np.int64)]
+    pts["ep"] = np.array([1, 4, 8], np.int32)[(r[3] % np.uint64(3)).astype(np.int64)]
+    pts["dp"] = 1 + (r[4] % np.uint64(3)).astype(np.int32)
+    return pts
+
+
 def max_t_hat(profile, gpu, points) -> float:
     """Reference scale for query targets: max dp*T over the grid, from the GPU eval."""
     from .wattserve import AnalyticModel, Grid, default_context, eval_grid

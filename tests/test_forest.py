@@ -140,3 +140,23 @@ def test_gpu_forest_control_step_and_replay(ctx, oracle, small_bundle, bundle):
                                         s["batches"], s["cfg"], spec, np.stack(sT), np.stack(sP))
     assert np.array_equal(logs, ologs)
     assert np.array_equal(summ, osumm)
+
+
+@pytest.mark.gpu
+def test_gpu_predict_device_points(ctx, small_bundle, gold):
+    """pals_predict_device: PredictorBundle::predict over device-resident point records."""
+    import torch
+
+    from paper_2605_21427_b200.forest import make_forest_model
+    g = gold("forest")
+    pts = np.ascontiguousarray(g["points"])
+    d_pts = torch.from_numpy(pts.view(np.uint8).copy()).cuda()
+    for mid in MODELS:
+        m = make_forest_model(ctx, small_bundle, mid)
+        T = torch.empty(len(pts), dtype=torch.float64, device="cuda")
+        P = torch.empty(len(pts), dtype=torch.float64, device="cuda")
+        assert ctx.lib.pals_predict_device(ctx.h, m.h, d_pts.data_ptr(), len(pts), T.data_ptr(),
+                                           P.data_ptr()) == 0
+        ctx.sync()
+        assert np.array_equal(bits(T.cpu().numpy()), bits(g[f"{mid}_T"]))
+        assert np.array_equal(bits(P.cpu().numpy()), bits(g[f"{mid}_P"]))

@@ -206,9 +206,11 @@ def run_ours(args, dist: Dist):
     d_rs = torch.empty(nq, dtype=torch.uint8, device="cuda")
 
     def select_step():
-        plan.prepare()
-        plan.select_device(d_q.data_ptr(), nq, d_idx.data_ptr(), d_rs.data_ptr())
+        # one pass: evaluate the grid, rank it, decide every query (a cached CUDA graph
+        # of the 9 kernels; the scan kernel is bracketed by event-record nodes)
+        plan.run(d_q.data_ptr(), nq, d_idx.data_ptr(), d_rs.data_ptr())
 
+    plan.time_scan(True)
     for _ in range(args.warmup):
         l2_flush()
         select_step()
@@ -217,30 +219,39 @@ def run_ours(args, dist: Dist):
     scanned_q = int(counts[0] + counts[1] + counts[2])
     pairs_step = scanned_q * n_cfg
     int_ops_step = (2 * counts[0] + 4 * counts[1] + 2 * counts[2]) * n_cfg
-    plan.time_scan(True)
     clocks = Clocks(dist.local)
     clocks.start()
     launches0 = ctx.launches
-    step_ms, scan_ms = [], []
-    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3))
+    scan_ms = []
+    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(2))
           for _ in range(args.steps)]
     dist.barrier()
     torch.cuda.synchronize()
     for k in range(args.steps):
         l2_flush()
         ev[k][0].record(stream)
-        plan.prepare()
+        select_step()
         ev[k][1].record(stream)
-        plan.select_device(d_q.data_ptr(), nq, d_idx.data_ptr(), d_rs.data_ptr())
-        ev[k][2].record(stream)
         scan_ms.append(plan.scan_ms())  # syncs on the scan's end event (outside the step)
     torch.cuda.synchronize()
     dist.barrier()
     launches = ctx.launches - launches0
-    plan.time_scan(False)
-    step_ms = [a.elapsed_time(c) for a, b, c in ev]
-    prep_ms = [a.elapsed_time(b) for a, b, c in ev]
+    step_ms = [a.elapsed_time(b) for a, b in ev]
     exact_q = int(plan.stats()[5])
+    # diagnostic split (not the headline): the same step as separate launches
+    plan.time_scan(False)
+    prep_ms, split_ms = [], []
+    for _ in range(3):
+        l2_flush()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record(stream)
+        plan.prepare()
+        e[1].record(stream)
+        plan.select_device(d_q.data_ptr(), nq, d_idx.data_ptr(), d_rs.data_ptr())
+        e[2].record(stream)
+        torch.cuda.synchronize()
+        prep_ms.append(e[0].elapsed_time(e[1]))
+        split_ms.append(e[0].elapsed_time(e[2]))
     gather = None
     if dist.world > 1:
         # the only cross-GPU traffic: one gather of (index, reason) per query to rank 0
@@ -297,9 +308,10 @@ def run_ours(args, dist: Dist):
                            "QoS+budget queries",
             "peak_source": "measured here: pals_measure_peaks ISETP+VIMNMX chains",
             "scan_share_of_step": scan_avg / float(np.mean(step_ms)),
-            "step_breakdown_ms": {"prepare(eval+rank)": float(np.mean(prep_ms)),
-                                  "select": float(np.mean(step_ms) - np.mean(prep_ms)),
-                                  "scan_kernel": scan_avg}}
+            "step_breakdown_ms": {"graph_step": float(np.mean(step_ms)),
+                                  "scan_kernel": scan_avg,
+                                  "ungraphed_step": float(np.mean(split_ms)),
+                                  "ungraphed_prepare(eval+rank)": float(np.mean(prep_ms))}}
 
     # ---------------- cfg4 replay ----------------
     s = workloads.cfg4_setup()

@@ -284,6 +284,10 @@ int pals_plan_prepare(pals_plan* p);
 /* Async: select for n queries resident in device memory. */
 int pals_plan_select_device(pals_plan* p, const pals_query* d_queries, int64_t n,
                             int32_t* d_index, uint8_t* d_reason);
+/* Async: one full step (prepare + select) for device-resident queries, replayed
+ * from a CUDA graph captured on the first call with these buffers. */
+int pals_plan_run(pals_plan* p, const pals_query* d_queries, int64_t n, int32_t* d_index,
+                  uint8_t* d_reason);
 /* Host buffers in and out: prepare + H2D + select + D2H, synchronous.
  * The batched equivalent of n calls to select_config (controller.hpp:132). */
 int pals_select(pals_plan* p, const pals_query* queries, int64_t n, int32_t* index,

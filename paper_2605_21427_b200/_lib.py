@@ -50,6 +50,7 @@ SIGNATURES = [
     ("pals_plan_prepare", _I, [_VP]),
     ("pals_plan_select_device", _I, [_VP, _VP, _I64, _VP, _VP]),
     ("pals_select", _I, [_VP, _VP, _I64, _VP, _VP]),
+    ("pals_plan_run", _I, [_VP, _VP, _I64, _VP, _VP]),
     ("pals_plan_scores", _I, [_VP, _VP, _VP, _VP]),
     ("pals_plan_last_exact_count", _I64, [_VP]),
     ("pals_plan_set_force_exact", _I, [_VP, _I]),

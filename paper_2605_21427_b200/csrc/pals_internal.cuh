@@ -151,7 +151,7 @@ struct PlanDev {
     uint64_t* merged[N_ORD]; // fully sorted keys (position r = competition rank r)
     uint8_t* bnd[N_ORD];     // per position i: 0 = merged[i+1] equal, 1 = distinct but a
                              // tolerance near-tie, 2 = separated (or i = n-1)
-    uint8_t* danger[N_ORD];  // per position: the value's run ends on a near-tie (bnd == 1)
+    uint8_t* danger[N_ORD];  // per run-start position: the run ends on a near-tie (bnd == 1)
     uint32_t* key32[N_ORD];  // packed keys (narrow)
     uint64_t* key64[N_ORD];  // packed keys (wide)
     int32_t* globals;        // [0] argmax t over all, [1] argmin p over all, [2] generic flag,

@@ -50,6 +50,7 @@ struct pals_plan {
     std::string err_msg;
     int64_t n = 0, np = 0;
     int nchunks = 0;
+    int chunk = 4096;  // sort chunk size (keys per CTA)
     int force_exact = 0;
     int64_t last_exact = 0;
     PlanDev d{};
@@ -77,6 +78,15 @@ struct pals_plan {
     int time_scan = 0;
     int scan_recorded = 0;
     cudaEvent_t ev_scan0 = nullptr, ev_scan1 = nullptr;
+    // CUDA graph of one full step (prepare + select) for fixed device buffers
+    int capturing = 0;
+    cudaGraphExec_t gexec = nullptr;
+    const void* g_q = nullptr;
+    void* g_idx = nullptr;
+    void* g_rs = nullptr;
+    int64_t g_n = -1;
+    int g_timed = 0;
+    int64_t g_launches = 0;
 };
 
 namespace pals {
@@ -128,11 +138,13 @@ __global__ void k_pad_keys(PlanDev d, int64_t np) {
 }
 
 // ---------------------------------------------------------------- sort ----
-// (1) bitonic sort of each 4096-key chunk. Warp w owns keys [128w, 128w+128);
-// lane l holds key 128w + 32k + l in x[k]. Exchange distances 1..16 are warp
-// shuffles, 32 and 64 are register swaps, only >= 128 go through shared memory
-// (15 of the 78 network stages).
-__global__ void __launch_bounds__(1024) k_sort_chunks(PlanDev d) {
+// (1) bitonic sort of each CH-key chunk (CH/4 threads). Warp w owns keys
+// [128w, 128w+128); lane l holds key 128w + 32k + l in x[k]. Exchange distances
+// 1..16 are warp shuffles, 32 and 64 are register swaps, only >= 128 go through
+// shared memory (15 of the 78 network stages for CH = 4096).
+template <int CH>
+__global__ void __launch_bounds__(CH / 4) k_sort_chunks(PlanDev d) {
+    constexpr int kChunk = CH;
     __shared__ uint64_t s[kChunk];
     const int o = blockIdx.y;
     const int64_t base = (int64_t)blockIdx.x * kChunk;
@@ -202,7 +214,9 @@ __device__ __forceinline__ int upper_bound_s(const uint64_t* s, int n, uint64_t 
 
 // (2) merged position of every chunk-sorted key = its rank within its chunk plus
 // the number of keys before it in every other chunk (a stable k-way merge).
+template <int CH>
 __global__ void __launch_bounds__(256) k_cross(PlanDev d) {
+    constexpr int kChunk = CH;
     __shared__ uint64_t s[kChunk];
     const int a = blockIdx.x, b = blockIdx.y, o = blockIdx.z;
     const int64_t abase = (int64_t)a * kChunk, bbase = (int64_t)b * kChunk;
@@ -217,6 +231,69 @@ __global__ void __launch_bounds__(256) k_cross(PlanDev d) {
         else if (b < a) cnt = upper_bound_s(s, kChunk, x);
         else cnt = lower_bound_s(s, kChunk, x);
         atomicAdd(&d.pos[o][abase + i], (uint32_t)cnt);
+    }
+}
+
+// (2') the same merged positions, computed with far fewer probes: each thread owns
+// E consecutive keys of chunk a; their insertion points into a sorted chunk b are
+// monotone, so one binary search plus galloping forward replaces E searches. A CTA
+// handles a group of G chunks b and accumulates in registers (one atomic per key
+// and group; a plain store when one group covers every chunk).
+template <int CH>
+__global__ void __launch_bounds__(256) k_cross_walk(PlanDev d, int nchunks, int G) {
+    constexpr int E = CH / 256;
+    __shared__ uint64_t s[CH];
+    const int a = blockIdx.x, g = blockIdx.y, o = blockIdx.z;
+    const int64_t abase = (int64_t)a * CH;
+    const int i0 = threadIdx.x * E;
+    uint64_t x[E];
+    uint32_t cnt[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        x[e] = d.sorted[o][abase + i0 + e];
+        cnt[e] = 0;
+    }
+    const int b_lo = g * G, b_hi = min(nchunks, b_lo + G);
+    for (int b = b_lo; b < b_hi; ++b) {
+        if (b == a) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) cnt[e] += (uint32_t)(i0 + e);
+            continue;
+        }
+        __syncthreads();
+        const uint64_t* src = d.sorted[o] + (int64_t)b * CH;
+        for (int i = threadIdx.x; i < CH; i += 256) s[i] = src[i];
+        __syncthreads();
+        // equal keys of an earlier chunk go first (upper bound), of a later chunk after
+        const bool up = b < a;
+        int lo = 0, hi = CH;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (up ? s[mid] <= x[0] : s[mid] < x[0]) lo = mid + 1;
+            else hi = mid;
+        }
+        cnt[0] += (uint32_t)lo;
+#pragma unroll
+        for (int e = 1; e < E; ++e) {
+            // gallop from the previous insertion point
+            int step = 1, base = lo;
+            while (base + step <= CH && (up ? s[base + step - 1] <= x[e] : s[base + step - 1] < x[e]))
+                base += step, step <<= 1;
+            int l2 = base, h2 = min(CH, base + step);
+            while (l2 < h2) {
+                const int mid = (l2 + h2) >> 1;
+                if (up ? s[mid] <= x[e] : s[mid] < x[e]) l2 = mid + 1;
+                else h2 = mid;
+            }
+            lo = l2;
+            cnt[e] += (uint32_t)lo;
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        if (abase + i0 + e >= d.n) continue;
+        if (G >= nchunks) d.pos[o][abase + i0 + e] = cnt[e];
+        else atomicAdd(&d.pos[o][abase + i0 + e], cnt[e]);
     }
 }
 
@@ -260,30 +337,61 @@ __device__ __forceinline__ uint8_t boundary(const PlanDev& d, int o, int64_t i) 
 // (4) per point: competition rank r = lower_bound(merged, key) and the packed key
 // (r << tr_bits) | TR; per merged position: the boundary class and whether the
 // value's run ends on a near-tie (then a winner there needs the exact fold).
+constexpr int kSamples = 1024;  // per-order sample index of the merged keys (smem)
+
+// lower_bound over merged[0, n) through a shared-memory sample of every S-th key:
+// ~10 shared probes + log2(S) probes inside one S-key window of global memory
+__device__ __forceinline__ uint32_t lower_bound_sampled(const uint64_t* m, int64_t n,
+                                                        const uint64_t* samp, int ns, int64_t S,
+                                                        uint64_t x) {
+    int lo = 0, hi = ns;  // first sample >= x
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (samp[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    int64_t a = lo == 0 ? 0 : (int64_t)(lo - 1) * S + 1;
+    int64_t b = lo == ns ? n : (int64_t)lo * S;
+    while (a < b) {
+        const int64_t mid = (a + b) >> 1;
+        if (m[mid] < x) a = mid + 1;
+        else b = mid;
+    }
+    return (uint32_t)a;
+}
+
+// grid.y = order: one thread per (point, order) keeps the dependent search chains short
 __global__ void k_assign(PlanDev d, const int* __restrict__ tr, uint64_t* gk) {
+    __shared__ uint64_t samp[kSamples];
+    const int o = blockIdx.y;
+    const uint64_t* m = d.merged[o];
+    const int64_t S = (d.n + kSamples - 1) / kSamples;
+    const int ns = (int)((d.n + S - 1) / S);
+    for (int t = threadIdx.x; t < ns; t += blockDim.x) samp[t] = m[t * S];
+    __syncthreads();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t t = (uint64_t)tr[i];
-#pragma unroll
-        for (int o = 0; o < N_ORD; ++o) {
-            const uint32_t r = lower_bound_g(d.merged[o], d.n, d.skey[o][i]);
-            const uint64_t k = ((uint64_t)r << d.tr_bits) | t;
-            if (d.wide) d.key64[o][i] = k;
-            else d.key32[o][i] = (uint32_t)k;
-            if (r == 0 && o == ORD_T) atomicMin((unsigned long long*)&gk[0], k);
-            if (r == 0 && o == ORD_P) atomicMin((unsigned long long*)&gk[1], k);
-            // position-indexed tables (thread i handles merged position i)
-            const uint8_t bi = boundary(d, o, i);
-            d.bnd[o][i] = bi;
-            uint8_t dg;
-            if (bi != 0) {
-                dg = bi == 1;
-            } else {  // run continues: find its last position
-                const int64_t e = (int64_t)lower_bound_g(d.merged[o], d.n, d.merged[o][i] + 1) - 1;
-                dg = boundary(d, o, e) == 1;
-            }
-            d.danger[o][i] = dg;
+        const uint32_t r = lower_bound_sampled(m, d.n, samp, ns, S, d.skey[o][i]);
+        const uint64_t k = ((uint64_t)r << d.tr_bits) | (uint64_t)tr[i];
+        if (d.wide) d.key64[o][i] = k;
+        else d.key32[o][i] = (uint32_t)k;
+        if (r == 0 && o == ORD_T) atomicMin((unsigned long long*)&gk[0], k);
+        if (r == 0 && o == ORD_P) atomicMin((unsigned long long*)&gk[1], k);
+        // position-indexed tables (thread i handles merged position i)
+        const uint8_t bi = boundary(d, o, i);
+        d.bnd[o][i] = bi;
+        // danger is read only at run starts (a competition rank is a run start):
+        // walk to the run's end, one pass per run in total
+        uint8_t dg = 0;
+        if (i == 0 || m[i - 1] != m[i]) {
+            int64_t e = i;
+            int steps = 0;
+            while (e + 1 < d.n && m[e + 1] == m[i] && ++steps < 32) ++e;
+            if (steps >= 32)  // long run: binary search for its end
+                e = (int64_t)lower_bound_sampled(m, d.n, samp, ns, S, m[i] + 1) - 1;
+            dg = boundary(d, o, e) == 1;
         }
+        d.danger[o][i] = dg;
     }
 }
 
@@ -456,8 +564,38 @@ struct SelArgs {
 // Kp = #points with p_node <= budget        (controller.hpp:155)
 // A point is t-feasible iff its rank r_t < Kt (every feasible value is strictly
 // better than every infeasible one), likewise for p.
+// Number of leading merged entries (order o) whose decoded value satisfies the
+// monotone predicate pred (true on a prefix): a search over a shared-memory sample
+// of every S-th value, then inside one S-entry window of global memory.
+template <class Pred>
+__device__ __forceinline__ int64_t count_prefix(const uint64_t* m, int o, int64_t n,
+                                                const double* samp, int ns, int64_t S, Pred pred) {
+    int lo = 0, hi = ns;  // first sample failing pred
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (pred(samp[mid])) lo = mid + 1;
+        else hi = mid;
+    }
+    int64_t a = lo == 0 ? 0 : (int64_t)(lo - 1) * S + 1;
+    int64_t b = lo == ns ? n : (int64_t)lo * S;
+    while (a < b) {
+        const int64_t mid = (a + b) >> 1;
+        if (pred(key_value(o, m[mid]))) a = mid + 1;
+        else b = mid;
+    }
+    return a;
+}
+
 __global__ void k_qprep(PlanDev d, SelArgs a) {
+    __shared__ double samp_t[kSamples], samp_p[kSamples];
     const int lane = threadIdx.x & 31;
+    const int64_t S = (d.n + kSamples - 1) / kSamples;
+    const int ns = (int)((d.n + S - 1) / S);
+    for (int t = threadIdx.x; t < ns; t += blockDim.x) {
+        samp_t[t] = key_value(ORD_T, d.merged[ORD_T][t * S]);
+        samp_p[t] = key_value(ORD_P, d.merged[ORD_P][t * S]);
+    }
+    __syncthreads();
     for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x; j0 < a.nq;
          j0 += (int64_t)gridDim.x * blockDim.x) {
         const int64_t j = j0 + threadIdx.x;
@@ -468,24 +606,14 @@ __global__ void k_qprep(PlanDev d, SelArgs a) {
             uint32_t Kt = 0, Kp = (uint32_t)d.n;
             if (q.objective == PALS_OBJ_QOS) {
                 const double target = q.throughput_tps * (1.0 + q.target_headroom);
-                int64_t lo = 0, hi = d.n;
-                while (lo < hi) {
-                    const int64_t mid = (lo + hi) >> 1;
-                    const double t = key_value(ORD_T, d.merged[ORD_T][mid]);
-                    if (!(t * q.bias < target)) lo = mid + 1;
-                    else hi = mid;
-                }
-                Kt = (uint32_t)lo;
+                const double bias = q.bias;
+                Kt = (uint32_t)count_prefix(d.merged[ORD_T], ORD_T, d.n, samp_t, ns, S,
+                                            [&](double t) { return !(t * bias < target); });
             }
             if (bset) {
                 const double budget = q.power_budget_w * (1.0 - q.budget_margin);
-                int64_t lo = 0, hi = d.n;
-                while (lo < hi) {
-                    const int64_t mid = (lo + hi) >> 1;
-                    if (key_value(ORD_P, d.merged[ORD_P][mid]) <= budget) lo = mid + 1;
-                    else hi = mid;
-                }
-                Kp = (uint32_t)lo;
+                Kp = (uint32_t)count_prefix(d.merged[ORD_P], ORD_P, d.n, samp_p, ns, S,
+                                            [&](double p) { return p <= budget; });
             }
             if (a.force_exact || d.globals[2]) c = CLS_X;
             else if (q.objective == PALS_OBJ_QOS && !bset) c = Kt ? CLS_A : CLS_D;
@@ -809,8 +937,15 @@ int pals_plan_create(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
         p->err_msg = pals_last_error();
     }
     const int64_t n = std::max<int64_t>(1, g->n);
-    p->nchunks = (int)((n + kChunk - 1) / kChunk);
-    p->np = (int64_t)p->nchunks * kChunk;
+    {
+        const char* e = getenv("PALS_SORT_CHUNK");
+        // measured on B200 (cfg2, n = 65,536): 2048-key chunks give the shortest
+        // sort + cross-rank (26 + 25 us vs 55 + 19 us at 4096)
+        const int c = e ? atoi(e) : (n <= 65536 ? 2048 : kChunk);
+        p->chunk = (c == 1024 || c == 2048 || c == 4096) ? c : kChunk;
+    }
+    p->nchunks = (int)((n + p->chunk - 1) / p->chunk);
+    p->np = (int64_t)p->nchunks * p->chunk;
     PlanDev& d = p->d;
     d.n = g->n;
     d.wide = g->n > 65536 ? 1 : 0;
@@ -896,6 +1031,7 @@ int pals_plan_create(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
 int pals_plan_destroy(pals_plan* p) {
     if (!p) return PALS_OK;
     cudaSetDevice(p->ctx->device);
+    if (p->gexec) cudaGraphExecDestroy(p->gexec);
     if (p->ev_scan0) cudaEventDestroy(p->ev_scan0);
     if (p->ev_scan1) cudaEventDestroy(p->ev_scan1);
     cudaFree(p->slab);
@@ -928,10 +1064,34 @@ int pals_plan_prepare(pals_plan* p) {
         if (rc) return rc;
     }
     if (p->np > n) k_pad_keys<<<dim3(grid_blocks(ctx, p->np - n, 256), N_ORD), 256, 0, s>>>(d, p->np);
-    k_sort_chunks<<<dim3(p->nchunks, N_ORD), 1024, 0, s>>>(d);
-    k_cross<<<dim3(p->nchunks, p->nchunks, N_ORD), 256, 0, s>>>(d);
+    const dim3 gs(p->nchunks, N_ORD), gx(p->nchunks, p->nchunks, N_ORD);
+    // cross-chunk ranking: each CTA walks G other chunks (few atomics, short
+    // serial staging chains)
+    static const int gsize = [] {
+        const char* e = getenv("PALS_CROSS_G");
+        return e ? std::max(1, atoi(e)) : 4;
+    }();
+    const int G = std::min(p->nchunks, gsize);
+    const dim3 gw(p->nchunks, (p->nchunks + G - 1) / G, N_ORD);
+    static const int walk = [] {
+        const char* e = getenv("PALS_CROSS_WALK");
+        return e ? atoi(e) : 0;  // measured: all-pairs k_cross beats the galloping walk
+    }();
+    if (p->chunk == 1024) {
+        k_sort_chunks<1024><<<gs, 256, 0, s>>>(d);
+        if (walk) k_cross_walk<1024><<<gw, 256, 0, s>>>(d, p->nchunks, G);
+        else k_cross<1024><<<gx, 256, 0, s>>>(d);
+    } else if (p->chunk == 2048) {
+        k_sort_chunks<2048><<<gs, 512, 0, s>>>(d);
+        if (walk) k_cross_walk<2048><<<gw, 256, 0, s>>>(d, p->nchunks, G);
+        else k_cross<2048><<<gx, 256, 0, s>>>(d);
+    } else {
+        k_sort_chunks<4096><<<gs, 1024, 0, s>>>(d);
+        if (walk) k_cross_walk<4096><<<gw, 256, 0, s>>>(d, p->nchunks, G);
+        else k_cross<4096><<<gx, 256, 0, s>>>(d);
+    }
     k_scatter<<<dim3(grid_blocks(ctx, n, 256), N_ORD), 256, 0, s>>>(d);
-    k_assign<<<eb, 256, 0, s>>>(d, p->tr, p->gk);
+    k_assign<<<dim3(eb, N_ORD), 256, 0, s>>>(d, p->tr, p->gk);
     k_resolve_globals<<<1, 64, 0, s>>>(d, p->gk);
     count_launch(ctx, 7 + (p->np > n ? 1 : 0));
     return check_launch("pals_plan_prepare");
@@ -939,6 +1099,10 @@ int pals_plan_prepare(pals_plan* p) {
 
 static int ensure_query_buffers(pals_plan* p, int64_t nq) {
     if (nq <= p->qcap) return PALS_OK;
+    if (p->gexec) {  // the cached step graph points at the buffers being replaced
+        cudaGraphExecDestroy(p->gexec);
+        p->gexec = nullptr;
+    }
     cudaFree(p->thr_t);
     const int64_t cap = std::max<int64_t>(nq, 1024);
     const size_t bytes = (size_t)cap * (8 * 4 + 1 + 4 * N_CLS + sizeof(WorkItem)) + 4096;
@@ -998,19 +1162,71 @@ int pals_plan_select_device(pals_plan* p, const pals_query* d_queries, int64_t n
     const int nchunks = (int)((p->n + ch - 1) / ch);
     // persistent scan grid: 4 CTAs per SM
     const int sgrid = ctx->num_sms * 4;
-    if (p->time_scan) PALS_CUDA(cudaEventRecord(p->ev_scan0, s));
+    // inside a stream capture the events become graph event-record nodes
+    const unsigned evf = p->capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
+    if (p->time_scan) PALS_CUDA(cudaEventRecordWithFlags(p->ev_scan0, s, evf));
     if (p->d.wide)
         k_scan<uint64_t><<<sgrid, kScanThreads, 3 * kScanCh * 8, s>>>(p->d, a, nchunks, (int)ch);
     else
         k_scan<uint32_t><<<sgrid, kScanThreads, 3 * kScanCh * 4, s>>>(p->d, a, nchunks, (int)ch);
     if (p->time_scan) {
-        PALS_CUDA(cudaEventRecord(p->ev_scan1, s));
+        PALS_CUDA(cudaEventRecordWithFlags(p->ev_scan1, s, evf));
         p->scan_recorded = 1;
     }
     k_finalize<<<qb, 256, 0, s>>>(p->d, a);
     k_exact<<<ctx->num_sms * 2, 256, 0, s>>>(p->d, a);
     count_launch(ctx, 4);
     return check_launch("pals_plan_select_device");
+}
+
+// One full step — evaluate + rank (prepare) and select — replayed from a CUDA graph
+// captured on first use for these device buffers (9 kernels + 5 memsets per step;
+// the graph removes the per-launch host overhead between them).
+int pals_plan_run(pals_plan* p, const pals_query* d_queries, int64_t nq, int32_t* d_idx,
+                  uint8_t* d_reason) {
+    if (p->err) return set_error(p->err, p->err_msg);
+    if (nq <= 0) return pals_plan_prepare(p);
+    pals_ctx* ctx = p->ctx;
+    cudaStream_t s = ctx->stream;
+    const int key_t = p->time_scan | (p->force_exact << 1);
+    const bool hit = p->gexec && p->g_q == d_queries && p->g_n == nq && p->g_idx == d_idx &&
+                     p->g_rs == d_reason && p->g_timed == key_t;
+    if (!hit) {
+        if (p->gexec) {
+            cudaGraphExecDestroy(p->gexec);
+            p->gexec = nullptr;
+        }
+        int rc = ensure_query_buffers(p, nq);
+        if (rc) return rc;
+        (void)cudaGetLastError();
+        PALS_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+        p->capturing = 1;
+        const int64_t l0 = ctx->launches;
+        rc = pals_plan_prepare(p);
+        if (!rc) rc = pals_plan_select_device(p, d_queries, nq, d_idx, d_reason);
+        p->capturing = 0;
+        cudaGraph_t g = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(s, &g);
+        if (rc) {
+            if (g) cudaGraphDestroy(g);
+            return rc;
+        }
+        if (ce != cudaSuccess) return cuda_fail(ce, "pals_plan_run capture");
+        const cudaError_t ie = cudaGraphInstantiate(&p->gexec, g, 0);
+        cudaGraphDestroy(g);
+        if (ie != cudaSuccess) return cuda_fail(ie, "pals_plan_run instantiate");
+        p->g_launches = ctx->launches - l0;
+        ctx->launches = l0;  // captured, not launched
+        p->g_q = d_queries;
+        p->g_n = nq;
+        p->g_idx = d_idx;
+        p->g_rs = d_reason;
+        p->g_timed = key_t;
+    }
+    PALS_CUDA(cudaGraphLaunch(p->gexec, s));
+    count_launch(ctx, (int)p->g_launches);
+    if (p->time_scan) p->scan_recorded = 1;
+    return PALS_OK;
 }
 
 int pals_select(pals_plan* p, const pals_query* queries, int64_t nq, int32_t* idx,
@@ -1020,9 +1236,11 @@ int pals_select(pals_plan* p, const pals_query* queries, int64_t nq, int32_t* id
     pals_ctx* ctx = p->ctx;
     PALS_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
-    int rc = pals_plan_prepare(p);
-    if (rc) return rc;
-    if (nq == 0) return pals_ctx_sync(ctx);
+    int rc;
+    if (nq == 0) {
+        rc = pals_plan_prepare(p);
+        return rc ? rc : pals_ctx_sync(ctx);
+    }
     // host staging of queries/results lives in the context scratch
     const size_t need = (size_t)nq * (sizeof(pals_query) + 4 + 1) + 1024;
     if (ctx->scratch_bytes < need) {
@@ -1035,7 +1253,7 @@ int pals_select(pals_plan* p, const pals_query* queries, int64_t nq, int32_t* id
     int32_t* di = (int32_t*)(b + (size_t)nq * sizeof(pals_query));
     uint8_t* dr = (uint8_t*)(di + nq);
     PALS_CUDA(cudaMemcpyAsync(dq, queries, (size_t)nq * sizeof(pals_query), cudaMemcpyHostToDevice, s));
-    rc = pals_plan_select_device(p, dq, nq, di, dr);
+    rc = pals_plan_run(p, dq, nq, di, dr);
     if (rc) return rc;
     PALS_CUDA(cudaMemcpyAsync(idx, di, (size_t)nq * 4, cudaMemcpyDeviceToHost, s));
     PALS_CUDA(cudaMemcpyAsync(reason, dr, (size_t)nq, cudaMemcpyDeviceToHost, s));

@@ -46,6 +46,15 @@ struct ReplayModelDev {
     const uint32_t* m2; // (n+1) x (n+1): min eff key over {r_t < i, r_p < j}
     const uint32_t* b1; // n+1: min t key over {r_p < j}
     const Analytic* plant;
+    // enforce_cap (sim.hpp:195-205) walk tables: from cap index a the breaker visits
+    // caps walk_c[a][j] (c_0 = caps[a], c_{j+1} = max(min_cap, c_j - 5)); walk_T /
+    // walk_pn hold the plant's throughput and cluster_system_power there, per batch.
+    int nc, nb, L;
+    int init_a, init_b;  // (max cap, max batch) indices into the caps / batches lists
+    double plant_min_cap;
+    const double* walk_c;   // [nc][L]
+    const double* walk_T;   // [nc][nb][L]
+    const double* walk_pn;  // [nc][nb][L]
 };
 
 struct ReplayParams {
@@ -168,28 +177,6 @@ __device__ __forceinline__ void table_select(const ReplayModelDev& m, double tar
     *reason = PALS_REASON_FALLBACK_MAX_T;
 }
 
-// enforce_cap (sim.hpp:195-205) with the plant model; returns the enforced cap
-// and the plant's throughput/power at it.
-__device__ double enforce_cap_dev(const ReplayModelDev& m, double cap, int batch, double node_budget,
-                                  double alpha, double beta, double* T_out, double* P_out) {
-    const Analytic& a = *m.plant;
-    double c = cap;
-    if (!(node_budget <= 0.0 || batch < 1)) {
-        while (true) {
-            if (!(c > a.min_cap)) {
-                c = a.min_cap;
-                break;
-            }
-            const Score s = analytic_score(a, c, batch, m.tp, m.dp);
-            if (p_node_of(s.P, m.dp, alpha, beta) <= node_budget) break;
-            c = smax(a.min_cap, c - 5.0);
-        }
-    }
-    const Score s = analytic_score(a, c, batch, m.tp, m.dp);
-    *T_out = s.T;
-    *P_out = s.P;
-    return c;
-}
 
 __device__ __forceinline__ int trace_objective(const pals_replay_spec& sp, uint64_t key) {
     return sp.objective_mode == 2 ? (int)(draw(key, 0, 0) >> 63) : sp.objective_mode;
@@ -247,12 +234,12 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
     double last_budget = 0.0;
     int sustain = 0;
     int cur = m.init_idx;
-    // plant (sim.hpp:155-157, 466-472)
-    double applied_cap = m.max_cap, inflight_cap = m.max_cap;
-    int batch_cap = m.max_batch;
+    // plant (sim.hpp:155-157, 466-472); caps and batch caps are always candidate knob
+    // values, tracked by their index in the caps / batches lists
+    int applied_a = m.init_a, inflight_a = m.init_a, batch_b = m.init_b;
     // enforce_cap memo (pure function of its inputs)
-    double c_ac = -1.0, c_nb = -1.0;
-    int c_be = -1;
+    int c_a = -1, c_b = -1;
+    double c_nb = -1.0;
     double cap = 0.0, capacity = 0.0, sys_w = 0.0;
     // Kp memo per budget value
     double kp_budget = -1.0;
@@ -266,14 +253,21 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
         const double t0 = (double)k * sp.interval_s;
         const double t1 = t0 + sp.interval_s;
         const double node_budget = sp.budget_mode ? bs.at(k, sp.seg_min, sp.seg_max) : 0.0;
-        const int b_eff = batch_cap;
-        if (applied_cap != c_ac || b_eff != c_be || node_budget != c_nb) {
-            double Tc, Pc;
-            cap = enforce_cap_dev(m, applied_cap, b_eff, node_budget, p.alpha, p.beta, &Tc, &Pc);
-            capacity = (double)m.dp * Tc;
-            sys_w = (double)m.dp * (p.alpha * (double)kGpusPerNode * Pc + p.beta);
-            c_ac = applied_cap;
-            c_be = b_eff;
+        // b_eff = batch_cap (fluid plant: the queue always covers the batch cap)
+        if (applied_a != c_a || batch_b != c_b || node_budget != c_nb) {
+            // enforce_cap (sim.hpp:195-205): walk down in 5 W steps until the cluster
+            // draw fits the budget; no budget -> the applied cap itself
+            const double* wc = m.walk_c + (int64_t)applied_a * m.L;
+            const int64_t wo = ((int64_t)applied_a * m.nb + batch_b) * m.L;
+            int j = 0;
+            if (node_budget > 0.0) {
+                while (wc[j] > m.plant_min_cap && !(m.walk_pn[wo + j] <= node_budget)) ++j;
+            }
+            cap = wc[j];
+            capacity = (double)m.dp * m.walk_T[wo + j];
+            sys_w = m.walk_pn[wo + j];  // = dp * (alpha * 4 * P + beta) (sim.hpp:413-414)
+            c_a = applied_a;
+            c_b = batch_b;
             c_nb = node_budget;
         }
         const double offered = ls.at(k, sp.seg_min, sp.seg_max);
@@ -351,10 +345,12 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
             r.cap_tenths = (uint16_t)llround(cap * 10.0);
             lg[k] = r;
         }
-        applied_cap = inflight_cap;
+        // actuation (sim.hpp:466-472): batch next interval, cap one interval later;
+        // candidate index = cap index * nb + batch index (build_candidates order)
+        applied_a = inflight_a;
         if (d_applied) {
-            batch_cap = m.batch[cur];
-            inflight_cap = m.cap[cur];
+            batch_b = cur % m.nb;
+            inflight_a = cur / m.nb;
         }
     }
     h = (h ^ (uint64_t)__double_as_longlong(bias)) * 0x100000001b3ULL;
@@ -415,6 +411,23 @@ __global__ void __launch_bounds__(1024) k_build_tables(PlanDev d, ReplayModelDev
         rm->gmax_t = d.globals[0];
         rm->gmin_p = d.globals[1];
         rm->generic = d.globals[2];
+    }
+}
+
+// The plant at every enforce_cap walk position: throughput (model.hpp:72-75) and
+// cluster_system_power (model.hpp:99-103) of (walk cap, batch) for each start cap.
+__global__ void k_build_walk(ReplayModelDev* rm, double alpha, double beta) {
+    const ReplayModelDev m = *rm;
+    const int64_t total = (int64_t)m.n * m.L;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(t % m.L);
+        const int64_t ab = t / m.L;  // a * nb + b
+        const int a = (int)(ab / m.nb);
+        const double c = m.walk_c[(int64_t)a * m.L + j];
+        const Score s = analytic_score(*m.plant, c, m.batch[ab], m.tp, m.dp);
+        ((double*)m.walk_T)[t] = s.T;
+        ((double*)m.walk_pn)[t] = p_node_of(s.P, m.dp, alpha, beta);
     }
 }
 
@@ -485,7 +498,25 @@ static int replay_setup(pals_ctx* ctx, int n_models, pals_model* const* models,
     rc->batches.assign(batches, batches + nb);
     const int n = nc * nb;
     const size_t W = (size_t)n + 1;
-    const size_t per_model = W * W * 4 + W * 4 + 2 * W * 8 + 1024;
+    // enforce_cap walk caps, exactly as the reference steps them (sim.hpp:199-203):
+    // c_0 = cap, c_{j+1} = std::max(min_cap, c_j - 5.0), until c_j <= min_cap
+    int L = 1;
+    std::vector<std::vector<double>> walks(nc);
+    for (int a = 0; a < nc; ++a) {
+        double c = caps[a];
+        walks[a].push_back(c);
+        while (c > gpu->min_cap_watts) {
+            c = smax(gpu->min_cap_watts, c - 5.0);
+            walks[a].push_back(c);
+        }
+        L = std::max<int>(L, (int)walks[a].size());
+    }
+    std::vector<double> walk_c((size_t)nc * L);
+    for (int a = 0; a < nc; ++a)
+        for (int j = 0; j < L; ++j)
+            walk_c[(size_t)a * L + j] = walks[a][std::min<size_t>(j, walks[a].size() - 1)];
+    const size_t walk_bytes = (size_t)nc * L * 8 + 2 * (size_t)n * L * 8;
+    const size_t per_model = W * W * 4 + W * 4 + 2 * W * 8 + walk_bytes + 4096;
     PALS_CUDA(cudaMalloc(&rc->d_tables, per_model * n_models));
     PALS_CUDA(cudaMalloc(&rc->d_models, sizeof(ReplayModelDev) * n_models));
     PALS_CUDA(cudaMalloc(&rc->d_plant, sizeof(Analytic) * n_models));
@@ -544,11 +575,26 @@ static int replay_setup(pals_ctx* ctx, int n_models, pals_model* const* models,
         m.ut = (const double*)(base + W * W * 4 + W * 4);
         m.up = (const double*)(base + W * W * 4 + W * 4 + W * 8);
         m.plant = rc->d_plant + i;
+        m.nc = nc;
+        m.nb = nb;
+        m.L = L;
+        m.init_a = m.init_idx / nb;
+        m.init_b = m.init_idx % nb;
+        m.plant_min_cap = gpu->min_cap_watts;
+        char* wbase = base + ((W * W * 4 + W * 4 + 2 * W * 8 + 255) & ~(size_t)255);
+        m.walk_c = (const double*)wbase;
+        m.walk_T = (const double*)(wbase + (size_t)nc * L * 8);
+        m.walk_pn = (const double*)(wbase + (size_t)nc * L * 8 + (size_t)n * L * 8);
+        PALS_CUDA(cudaMemcpy((void*)m.walk_c, walk_c.data(), walk_c.size() * 8,
+                             cudaMemcpyHostToDevice));
         PALS_CUDA(cudaMemcpy(rc->d_models + i, &m, sizeof m, cudaMemcpyHostToDevice));
         k_build_tables<<<1, 1024, 0, ctx->stream>>>(d, rc->d_models + i, (uint32_t*)m.m2,
                                                      (uint32_t*)m.b1, (double*)m.ut, (double*)m.up,
                                                      coeffs->alpha, coeffs->beta_watts);
-        count_launch(ctx);
+        k_build_walk<<<(n * L + 255) / 256, 256, 0, ctx->stream>>>(rc->d_models + i,
+                                                                  coeffs->alpha,
+                                                                  coeffs->beta_watts);
+        count_launch(ctx, 2);
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "k_build_tables");
     }

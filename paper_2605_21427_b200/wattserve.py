@@ -195,6 +195,11 @@ class Plan:
         check(self.ctx.lib.pals_plan_select_device(self.h, C.c_void_p(d_queries), n,
                                                    C.c_void_p(d_idx), C.c_void_p(d_reason)))
 
+    def run(self, d_queries: int, n: int, d_idx: int, d_reason: int):
+        """One full step (evaluate + rank + select) from a cached CUDA graph; async."""
+        check(self.ctx.lib.pals_plan_run(self.h, C.c_void_p(d_queries), n, C.c_void_p(d_idx),
+                                         C.c_void_p(d_reason)))
+
     def scores(self):
         n = len(self.grid)
         th, pn, ef = (np.empty(n, np.float64) for _ in range(3))

@@ -135,6 +135,23 @@ def replay_spec(n_traces: int, n_steps: int = 3600, seed: int = 2605, first: int
     return s
 
 
+def dr_candidates():
+    """The demand-response scenario's dense candidate grid (data/scenarios/
+    demand_response.json: caps 100..400 W step 5, 24 batch sizes) = 1,464 points."""
+    caps = np.arange(100.0, 400.0 + 1e-9, 5.0)
+    batches = np.array([1, 2, 3, 4, 5, 6, 8, 10, 12, 14, 16, 18, 20, 24, 28, 32, 36, 40, 44, 48,
+                        52, 56, 60, 64], np.int32)
+    return caps, batches
+
+
+def cfg3_extended():
+    """cfg3 with the EP x DP axes: 64 x 256 x TP{1,2,4,8} x EP{1,4,8} x DP{1,2,3} = 589,824."""
+    profs, gpu, coeffs = load_bundle()
+    p = dense_profile(profs, "mixtral-8x7b-like")
+    pts = grid_points(cfg2_caps(), np.arange(1, 257), [1, 2, 4, 8], [1, 4, 8], [1, 2, 3])
+    return dict(name="cfg3x", profile=p, gpu=gpu, coeffs=coeffs, points=pts)
+
+
 def cfg4_setup():
     """8 profiles, 6x6 candidates at each profile's deployment, scenario_io defaults."""
     profs, gpu, coeffs = load_bundle()

@@ -130,20 +130,17 @@ __global__ void k_eval_table(PlanDev d, const int* __restrict__ map, const doubl
     }
 }
 
-__global__ void k_pad_keys(PlanDev d, int64_t np) {
-    const int o = blockIdx.y;
-    for (int64_t i = d.n + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < np;
-         i += (int64_t)gridDim.x * blockDim.x)
-        d.skey[o][i] = kNone64;
-}
-
 // ---------------------------------------------------------------- sort ----
 // (1) bitonic sort of each CH-key chunk (CH/4 threads). Warp w owns keys
 // [128w, 128w+128); lane l holds key 128w + 32k + l in x[k]. Exchange distances
 // 1..16 are warp shuffles, 32 and 64 are register swaps, only >= 128 go through
 // shared memory (15 of the 78 network stages for CH = 4096).
+// The kernel also resets what the next prep kernels accumulate into (merged
+// positions, the global-candidate keys, the last-block counter of k_assign), so
+// the step needs no separate memset nodes; keys past n are padded in registers.
 template <int CH>
-__global__ void __launch_bounds__(CH / 4) k_sort_chunks(PlanDev d) {
+__global__ void __launch_bounds__(CH / 4) k_sort_chunks(PlanDev d, uint64_t* gk,
+                                                        uint32_t* done) {
     constexpr int kChunk = CH;
     __shared__ uint64_t s[kChunk];
     const int o = blockIdx.y;
@@ -152,7 +149,15 @@ __global__ void __launch_bounds__(CH / 4) k_sort_chunks(PlanDev d) {
     const int i0 = 128 * w + lane;
     uint64_t x[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) x[k] = d.skey[o][base + i0 + 32 * k];
+    for (int k = 0; k < 4; ++k) {
+        const int64_t i = base + i0 + 32 * k;
+        x[k] = i < d.n ? d.skey[o][i] : kNone64;
+        d.pos[o][i] = 0;
+    }
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+        gk[0] = gk[1] = kNone64;
+        *done = 0;
+    }
     for (int ks = 2; ks <= kChunk; ks <<= 1) {
         for (int j = ks >> 1; j > 0; j >>= 1) {
             if (j >= 128) {
@@ -234,69 +239,6 @@ __global__ void __launch_bounds__(256) k_cross(PlanDev d) {
     }
 }
 
-// (2') the same merged positions, computed with far fewer probes: each thread owns
-// E consecutive keys of chunk a; their insertion points into a sorted chunk b are
-// monotone, so one binary search plus galloping forward replaces E searches. A CTA
-// handles a group of G chunks b and accumulates in registers (one atomic per key
-// and group; a plain store when one group covers every chunk).
-template <int CH>
-__global__ void __launch_bounds__(256) k_cross_walk(PlanDev d, int nchunks, int G) {
-    constexpr int E = CH / 256;
-    __shared__ uint64_t s[CH];
-    const int a = blockIdx.x, g = blockIdx.y, o = blockIdx.z;
-    const int64_t abase = (int64_t)a * CH;
-    const int i0 = threadIdx.x * E;
-    uint64_t x[E];
-    uint32_t cnt[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-        x[e] = d.sorted[o][abase + i0 + e];
-        cnt[e] = 0;
-    }
-    const int b_lo = g * G, b_hi = min(nchunks, b_lo + G);
-    for (int b = b_lo; b < b_hi; ++b) {
-        if (b == a) {
-#pragma unroll
-            for (int e = 0; e < E; ++e) cnt[e] += (uint32_t)(i0 + e);
-            continue;
-        }
-        __syncthreads();
-        const uint64_t* src = d.sorted[o] + (int64_t)b * CH;
-        for (int i = threadIdx.x; i < CH; i += 256) s[i] = src[i];
-        __syncthreads();
-        // equal keys of an earlier chunk go first (upper bound), of a later chunk after
-        const bool up = b < a;
-        int lo = 0, hi = CH;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (up ? s[mid] <= x[0] : s[mid] < x[0]) lo = mid + 1;
-            else hi = mid;
-        }
-        cnt[0] += (uint32_t)lo;
-#pragma unroll
-        for (int e = 1; e < E; ++e) {
-            // gallop from the previous insertion point
-            int step = 1, base = lo;
-            while (base + step <= CH && (up ? s[base + step - 1] <= x[e] : s[base + step - 1] < x[e]))
-                base += step, step <<= 1;
-            int l2 = base, h2 = min(CH, base + step);
-            while (l2 < h2) {
-                const int mid = (l2 + h2) >> 1;
-                if (up ? s[mid] <= x[e] : s[mid] < x[e]) l2 = mid + 1;
-                else h2 = mid;
-            }
-            lo = l2;
-            cnt[e] += (uint32_t)lo;
-        }
-    }
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-        if (abase + i0 + e >= d.n) continue;
-        if (G >= nchunks) d.pos[o][abase + i0 + e] = cnt[e];
-        else atomicAdd(&d.pos[o][abase + i0 + e], cnt[e]);
-    }
-}
-
 // (3) scatter to the merged order
 __global__ void k_scatter(PlanDev d) {
     const int o = blockIdx.y;
@@ -360,8 +302,11 @@ __device__ __forceinline__ uint32_t lower_bound_sampled(const uint64_t* m, int64
     return (uint32_t)a;
 }
 
-// grid.y = order: one thread per (point, order) keeps the dependent search chains short
-__global__ void k_assign(PlanDev d, const int* __restrict__ tr, uint64_t* gk) {
+__device__ void resolve_globals_warp(const PlanDev& d, const uint64_t* gk, int w);
+
+// grid.y = order: one thread per (point, order) keeps the dependent search chains
+// short. The last block to finish resolves the two query-independent winners.
+__global__ void k_assign(PlanDev d, const int* __restrict__ tr, uint64_t* gk, uint32_t* done) {
     __shared__ uint64_t samp[kSamples];
     const int o = blockIdx.y;
     const uint64_t* m = d.merged[o];
@@ -392,6 +337,20 @@ __global__ void k_assign(PlanDev d, const int* __restrict__ tr, uint64_t* gk) {
             dg = boundary(d, o, e) == 1;
         }
         d.danger[o][i] = dg;
+    }
+    // last-block-done: every block's keys, danger flags and candidate atomics are
+    // visible after its fence, so the final block can resolve the globals
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(done, 1u) == gridDim.x * gridDim.y - 1;
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        const int w = threadIdx.x >> 5;
+        if (w < 2) resolve_globals_warp(d, gk, w);
     }
 }
 
@@ -500,8 +459,10 @@ __device__ void warp_select_full(const PlanDev& d, const pals_query& q, int32_t*
 }
 
 // (6) query-independent winners: argmax t_hat over all and argmin p_node over all
-__global__ void k_resolve_globals(PlanDev d, const uint64_t* gk) {
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// warp w = 0: argmax t_hat over all (controller.hpp:191-198); w = 1: argmin p_node
+// over all (:180-188). Run by the last block of k_assign.
+__device__ void resolve_globals_warp(const PlanDev& d, const uint64_t* gk, int w) {
+    const int lane = threadIdx.x & 31;
     const int generic = d.globals[2];
     const int o = w == 0 ? ORD_T : ORD_P;
     const uint64_t mask = (1ull << d.tr_bits) - 1;
@@ -678,9 +639,28 @@ __device__ __forceinline__ void scan_item(const K* __restrict__ se, const K* __r
     }
 }
 
+// Stream-K partition of the pair scan: the work of every (class, query tile) is
+// laid end to end in units of one config (weighted by the class's ops per pair:
+// A 2, B 4, C 2) and each CTA takes an equal contiguous share, so every SM gets
+// the same number of integer ops whatever the query count.
+struct ScanPlan {
+    int64_t T[3];     // tiles per class
+    int64_t tq[3];    // queries per tile (balanced, <= TQ)
+    int64_t wbase[4]; // cumulative weight at each class start
+    int64_t pbase[4]; // cumulative config position at each class start
+};
+
+__device__ __forceinline__ int class_ops(int c) { return c == CLS_B ? 4 : 2; }
+
+__device__ __forceinline__ int64_t scan_pos_of(const ScanPlan& sp, int64_t u) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+        if (u < sp.wbase[c + 1]) return sp.pbase[c] + (u - sp.wbase[c]) / class_ops(c);
+    return sp.pbase[3];
+}
+
 template <typename K>
-__global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a, int nchunks,
-                                                           int ch) {
+__global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K* se = reinterpret_cast<K*>(smem_raw);
     K* st = se + kScanCh;
@@ -690,51 +670,61 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a, 
     const K* kp = KeyTraits<K>::keys(d, ORD_P);
     constexpr int kQ = ScanQ<K>::Q;
     constexpr int kTQ = ScanQ<K>::TQ;
-    int64_t items[3];
-    int64_t tot = 0;
+    const int64_t n = d.n;
+    ScanPlan pl;
+    pl.wbase[0] = pl.pbase[0] = 0;
+#pragma unroll
     for (int c = 0; c < 3; ++c) {
-        const int64_t tiles = (a.counts[c] + kTQ - 1) / kTQ;
-        items[c] = tiles * nchunks;
-        tot += items[c];
+        const int64_t cnt = a.counts[c];
+        pl.T[c] = (cnt + kTQ - 1) / kTQ;
+        pl.tq[c] = pl.T[c] ? (cnt + pl.T[c] - 1) / pl.T[c] : 0;
+        pl.pbase[c + 1] = pl.pbase[c] + pl.T[c] * n;
+        pl.wbase[c + 1] = pl.wbase[c] + pl.T[c] * n * class_ops(c);
     }
-    for (int64_t it = blockIdx.x; it < tot; it += gridDim.x) {
+    const int64_t W = pl.wbase[3];
+    const int64_t p0 = scan_pos_of(pl, W * blockIdx.x / gridDim.x);
+    const int64_t p1 = scan_pos_of(pl, W * (blockIdx.x + 1) / gridDim.x);
+    int64_t pos = p0;
+    while (pos < p1) {
+        // locate (class, tile, first config) of pos and the end of that tile segment
         int c = 0;
-        int64_t r = it;
-        while (r >= items[c]) {
-            r -= items[c];
-            ++c;
-        }
-        const int64_t tile = r / nchunks;
-        const int chunk = (int)(r % nchunks);
-        const int64_t c0 = (int64_t)chunk * ch;
-        const int64_t rem = d.n - c0;
-        const int nc = (int)(rem < ch ? rem : ch);
-        const int ncp = (nc + 3) & ~3;
-        // stage this chunk's keys (pad with keys that never pass a threshold)
-        for (int i = threadIdx.x; i < ncp; i += blockDim.x) {
-            const bool in = i < nc;
-            if (c != CLS_C) se[i] = in ? ke[c0 + i] : (K)~(K)0;
-            st[i] = in ? kt[c0 + i] : (K)~(K)0;
-            if (c != CLS_A) sp[i] = in ? kp[c0 + i] : (K)~(K)0;
-        }
+        while (pos >= pl.pbase[c + 1]) ++c;
+        const int64_t r = pos - pl.pbase[c];
+        const int64_t tile = r / n;
+        const int64_t j0 = r % n;
+        const int64_t seg_end = min(p1, pl.pbase[c] + (tile + 1) * n);
+        const int64_t j1 = j0 + (seg_end - pos);
+        // this tile's queries: 8 per thread (4 with 64-bit keys)
+        const int64_t q_lo = tile * pl.tq[c], q_hi = min((int64_t)a.counts[c], q_lo + pl.tq[c]);
         K thr_t[kQ], thr_p[kQ], be[kQ], bt[kQ];
         int32_t qid[kQ];
 #pragma unroll
         for (int q = 0; q < kQ; ++q) {
-            const int64_t s = tile * kTQ + q * kScanThreads + threadIdx.x;
-            qid[q] = s < a.counts[c] ? a.qlist[c * a.qcap + s] : -1;
+            const int64_t s = q_lo + q * kScanThreads + threadIdx.x;
+            qid[q] = s < q_hi ? a.qlist[c * a.qcap + s] : -1;
             thr_t[q] = qid[q] >= 0 ? (K)a.thr_t[qid[q]] : (K)0;
             thr_p[q] = qid[q] >= 0 ? (K)a.thr_p[qid[q]] : (K)0;
             be[q] = (K)~(K)0;
             bt[q] = (K)~(K)0;
         }
-        __syncthreads();
-        // padded slots carry all-ones keys: they only pass an all-ones threshold,
-        // and then they cannot lower a minimum below a real key
-        if (c == CLS_A) scan_item<K, CLS_A, kQ>(se, st, sp, ncp, thr_t, thr_p, be, bt);
-        else if (c == CLS_B) scan_item<K, CLS_B, kQ>(se, st, sp, ncp, thr_t, thr_p, be, bt);
-        else scan_item<K, CLS_C, kQ>(se, st, sp, ncp, thr_t, thr_p, be, bt);
-        __syncthreads();
+        for (int64_t c0 = j0; c0 < j1; c0 += kScanCh) {
+            const int nc = (int)min((int64_t)kScanCh, j1 - c0);
+            const int ncp = (nc + 3) & ~3;
+            __syncthreads();
+            // stage the keys (pad with keys that never pass a threshold)
+            for (int i = threadIdx.x; i < ncp; i += blockDim.x) {
+                const bool in = i < nc;
+                if (c != CLS_C) se[i] = in ? ke[c0 + i] : (K)~(K)0;
+                st[i] = in ? kt[c0 + i] : (K)~(K)0;
+                if (c != CLS_A) sp[i] = in ? kp[c0 + i] : (K)~(K)0;
+            }
+            __syncthreads();
+            // padded slots carry all-ones keys: they only pass an all-ones threshold,
+            // and then they cannot lower a minimum below a real key
+            if (c == CLS_A) scan_item<K, CLS_A, kQ>(se, st, sp, ncp, thr_t, thr_p, be, bt);
+            else if (c == CLS_B) scan_item<K, CLS_B, kQ>(se, st, sp, ncp, thr_t, thr_p, be, bt);
+            else scan_item<K, CLS_C, kQ>(se, st, sp, ncp, thr_t, thr_p, be, bt);
+        }
 #pragma unroll
         for (int q = 0; q < kQ; ++q) {
             if (qid[q] < 0) continue;
@@ -743,6 +733,7 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a, 
             if (c != CLS_A && bt[q] != (K)~(K)0)
                 atomicMin((unsigned long long*)&a.best_t[qid[q]], (unsigned long long)bt[q]);
         }
+        pos = seg_end;
     }
 }
 
@@ -984,7 +975,7 @@ int pals_plan_create(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
         else d.key32[o] = (uint32_t*)take((size_t)n * 4);
     }
     d.globals = (int32_t*)take(16);
-    p->gk = (uint64_t*)take(16);
+    p->gk = (uint64_t*)take(32);  // [2] global candidate keys + k_assign's done counter
     p->d_an = (Analytic*)take(sizeof(Analytic));
     // TR per point (inverse of grid inv_tr), computed once on the host at grid creation
     p->tr = (int*)take(4 * (size_t)n);
@@ -1049,9 +1040,7 @@ int pals_plan_prepare(pals_plan* p) {
     PlanDev& d = p->d;
     const int64_t n = p->n;
     (void)cudaGetLastError();  // clear stale non-sticky errors of earlier calls
-    PALS_CUDA(cudaMemsetAsync(d.globals, 0, 16, s));
-    PALS_CUDA(cudaMemsetAsync(p->gk, 0xFF, 16, s));
-    for (int o = 0; o < N_ORD; ++o) PALS_CUDA(cudaMemsetAsync(d.pos[o], 0, p->np * 4, s));
+    PALS_CUDA(cudaMemsetAsync(d.globals, 0, 16, s));  // generic flag, set by the eval
     const int eb = grid_blocks(ctx, n, 256);
     if (p->model->kind == MODEL_ANALYTIC) {
         k_eval_analytic<<<eb, 256, 0, s>>>(d, p->d_an, p->grid->tp, p->coeffs.alpha,
@@ -1063,37 +1052,21 @@ int pals_plan_prepare(pals_plan* p) {
         const int rc = forest_eval_plan(p, p->model, ctx);
         if (rc) return rc;
     }
-    if (p->np > n) k_pad_keys<<<dim3(grid_blocks(ctx, p->np - n, 256), N_ORD), 256, 0, s>>>(d, p->np);
     const dim3 gs(p->nchunks, N_ORD), gx(p->nchunks, p->nchunks, N_ORD);
-    // cross-chunk ranking: each CTA walks G other chunks (few atomics, short
-    // serial staging chains)
-    static const int gsize = [] {
-        const char* e = getenv("PALS_CROSS_G");
-        return e ? std::max(1, atoi(e)) : 4;
-    }();
-    const int G = std::min(p->nchunks, gsize);
-    const dim3 gw(p->nchunks, (p->nchunks + G - 1) / G, N_ORD);
-    static const int walk = [] {
-        const char* e = getenv("PALS_CROSS_WALK");
-        return e ? atoi(e) : 0;  // measured: all-pairs k_cross beats the galloping walk
-    }();
+    uint32_t* done = (uint32_t*)(p->gk + 2);
     if (p->chunk == 1024) {
-        k_sort_chunks<1024><<<gs, 256, 0, s>>>(d);
-        if (walk) k_cross_walk<1024><<<gw, 256, 0, s>>>(d, p->nchunks, G);
-        else k_cross<1024><<<gx, 256, 0, s>>>(d);
+        k_sort_chunks<1024><<<gs, 256, 0, s>>>(d, p->gk, done);
+        k_cross<1024><<<gx, 256, 0, s>>>(d);
     } else if (p->chunk == 2048) {
-        k_sort_chunks<2048><<<gs, 512, 0, s>>>(d);
-        if (walk) k_cross_walk<2048><<<gw, 256, 0, s>>>(d, p->nchunks, G);
-        else k_cross<2048><<<gx, 256, 0, s>>>(d);
+        k_sort_chunks<2048><<<gs, 512, 0, s>>>(d, p->gk, done);
+        k_cross<2048><<<gx, 256, 0, s>>>(d);
     } else {
-        k_sort_chunks<4096><<<gs, 1024, 0, s>>>(d);
-        if (walk) k_cross_walk<4096><<<gw, 256, 0, s>>>(d, p->nchunks, G);
-        else k_cross<4096><<<gx, 256, 0, s>>>(d);
+        k_sort_chunks<4096><<<gs, 1024, 0, s>>>(d, p->gk, done);
+        k_cross<4096><<<gx, 256, 0, s>>>(d);
     }
     k_scatter<<<dim3(grid_blocks(ctx, n, 256), N_ORD), 256, 0, s>>>(d);
-    k_assign<<<dim3(eb, N_ORD), 256, 0, s>>>(d, p->tr, p->gk);
-    k_resolve_globals<<<1, 64, 0, s>>>(d, p->gk);
-    count_launch(ctx, 7 + (p->np > n ? 1 : 0));
+    k_assign<<<dim3(eb, N_ORD), 256, 0, s>>>(d, p->tr, p->gk, done);
+    count_launch(ctx, 5);
     return check_launch("pals_plan_prepare");
 }
 
@@ -1152,23 +1125,15 @@ int pals_plan_select_device(pals_plan* p, const pals_query* d_queries, int64_t n
     PALS_CUDA(cudaMemsetAsync(p->counts, 0, 64, s));
     const int qb = grid_blocks(ctx, nq, 256);
     k_qprep<<<qb, 256, 0, s>>>(p->d, a);
-    // Work items = query tiles x config chunks. Size the chunk so a batch of nq
-    // queries still yields >= ~6 items per SM (few queries -> short chunks).
-    const int64_t tq = p->d.wide ? ScanQ<uint64_t>::TQ : ScanQ<uint32_t>::TQ;
-    const int64_t tiles_est = std::max<int64_t>(1, (nq + tq - 1) / tq);
-    const int64_t want_chunks = std::max<int64_t>(1, (6 * (int64_t)ctx->num_sms + tiles_est - 1) / tiles_est);
-    int64_t ch = (p->n + want_chunks - 1) / want_chunks;
-    ch = std::min<int64_t>(kScanCh, std::max<int64_t>(256, (ch + 255) / 256 * 256));
-    const int nchunks = (int)((p->n + ch - 1) / ch);
-    // persistent scan grid: 4 CTAs per SM
+    // stream-K scan grid: 4 CTAs per SM, equal integer-op shares (see k_scan)
     const int sgrid = ctx->num_sms * 4;
     // inside a stream capture the events become graph event-record nodes
     const unsigned evf = p->capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
     if (p->time_scan) PALS_CUDA(cudaEventRecordWithFlags(p->ev_scan0, s, evf));
     if (p->d.wide)
-        k_scan<uint64_t><<<sgrid, kScanThreads, 3 * kScanCh * 8, s>>>(p->d, a, nchunks, (int)ch);
+        k_scan<uint64_t><<<sgrid, kScanThreads, 3 * kScanCh * 8, s>>>(p->d, a);
     else
-        k_scan<uint32_t><<<sgrid, kScanThreads, 3 * kScanCh * 4, s>>>(p->d, a, nchunks, (int)ch);
+        k_scan<uint32_t><<<sgrid, kScanThreads, 3 * kScanCh * 4, s>>>(p->d, a);
     if (p->time_scan) {
         PALS_CUDA(cudaEventRecordWithFlags(p->ev_scan1, s, evf));
         p->scan_recorded = 1;

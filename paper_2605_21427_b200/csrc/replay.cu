@@ -131,50 +131,62 @@ __device__ void thread_select_full(const ReplayModelDev& m, double target, bool 
 }
 
 // select_config via the rank tables; exact by the near-tie argument of DESIGN.md §3.
+// Kt = #sorted t_hat entries with !(t*bias < target), kept incrementally: bias moves
+// a little each step, so the previous count is re-validated with two exact tests
+// before falling back to a binary search (same value either way).
+__device__ __forceinline__ int count_t_feasible(const ReplayModelDev& m, double bias, double target,
+                                                int prev) {
+    const bool ok_lo = prev == 0 || !(m.ut[prev - 1] * bias < target);
+    const bool ok_hi = prev == m.nd_t || (m.ut[prev] * bias < target);
+    if (ok_lo && ok_hi) return prev;
+    int lo = 0, hi = m.nd_t;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (!(m.ut[mid] * bias < target)) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+constexpr uint32_t kWordDanger = 0x40000000u;  // table word: winner needs the exact fold
+constexpr uint32_t kWordIdx = 0x000FFFFFu;
+
+// select_config from the per-model tables; returns the CANONICAL candidate index.
+// Table words are precomputed: canonical winner index | danger flag (k_build_tables).
 __device__ __forceinline__ void table_select(const ReplayModelDev& m, double target, bool bset,
-                                             double budget, int kp, double bias, int objective,
-                                             int* idx, int* reason) {
-    if (m.generic) {
-        thread_select_full(m, target, bset, budget, bias, objective, idx, reason);
-        return;
-    }
-    const int W = m.nd_p + 1;
-    if (objective == PALS_OBJ_QOS) {
-        int lo = 0, hi = m.nd_t;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (!(m.ut[mid] * bias < target)) lo = mid + 1;
-            else hi = mid;
+                                             double budget, int kp, int kt, double bias,
+                                             int objective, int* idx, int* reason) {
+    if (!m.generic) {
+        bool qos_empty = true;
+        if (objective == PALS_OBJ_QOS) {
+            const uint32_t w = m.m2[kt * (m.nd_p + 1) + (bset ? kp : m.nd_p)];
+            if (w != kNone32) {
+                if (!(w & kWordDanger)) {
+                    *idx = (int)(w & kWordIdx);
+                    *reason = PALS_REASON_QOS_FEASIBLE;
+                    return;
+                }
+                qos_empty = false;  // near-tie winner: exact fold below
+            }
         }
-        const uint32_t key = m.m2[lo * W + (bset ? kp : m.nd_p)];
-        if (key != kNone32) {
-            const uint32_t d0 = key >> 16;
-            if (m.danger_e[d0]) {
-                thread_select_full(m, target, bset, budget, bias, objective, idx, reason);
+        if (qos_empty) {
+            if (!bset) {  // fallback: max throughput over all (controller.hpp:191-198)
+                *idx = m.gmax_t;
+                *reason = PALS_REASON_FALLBACK_MAX_T;
                 return;
             }
-            *idx = m.inv_tr[key & 0xFFFFu];
-            *reason = PALS_REASON_QOS_FEASIBLE;
-            return;
-        }
-    }
-    if (bset) {
-        const uint32_t key = m.b1[kp];
-        if (key != kNone32) {
-            const uint32_t d0 = key >> 16;
-            if (m.danger_t[d0]) {
-                thread_select_full(m, target, bset, budget, bias, objective, idx, reason);
+            const uint32_t w = m.b1[kp];
+            if (w == kNone32 || !(w & kWordDanger)) {
+                // budget below every candidate -> least power (controller.hpp:180-188)
+                *idx = w == kNone32 ? m.gmin_p : (int)(w & kWordIdx);
+                *reason = PALS_REASON_BUDGET_MAX_T;
                 return;
             }
-            *idx = m.inv_tr[key & 0xFFFFu];
-        } else {
-            *idx = m.gmin_p;
         }
-        *reason = PALS_REASON_BUDGET_MAX_T;
-        return;
     }
-    *idx = m.gmax_t;
-    *reason = PALS_REASON_FALLBACK_MAX_T;
+    // near-tie winner or non-finite scores: the literal fold
+    thread_select_full(m, target, bset, budget, bias, objective, idx, reason);
+    *idx = m.canon[*idx];
 }
 
 
@@ -244,6 +256,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
     // Kp memo per budget value
     double kp_budget = -1.0;
     int kp = m.nd_p;
+    int kt = 0;  // incremental t-feasibility count (count_t_feasible)
     uint64_t h = 0xcbf29ce484222325ULL;
     double energy = 0.0, tokens = 0.0;
     int n_applied = 0;
@@ -318,9 +331,10 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
                 kp_budget = budget;
             }
             int s_idx, s_reason;
-            table_select(m, target, bset, budget, kp, bias, obj, &s_idx, &s_reason);
+            if (obj == PALS_OBJ_QOS) kt = count_t_feasible(m, bias, target, kt);
+            table_select(m, target, bset, budget, kp, kt, bias, obj, &s_idx, &s_reason);
             const bool may_apply = changed || sustain >= cfg.sustain_intervals;
-            const int sc = m.canon[s_idx];
+            const int sc = s_idx;  // canonical (first equal point)
             if (may_apply && sc != cur) {
                 cur = sc;
                 sustain = 0;
@@ -391,8 +405,26 @@ __global__ void __launch_bounds__(1024) k_build_tables(PlanDev d, ReplayModelDev
     __syncthreads();
     for (int j = threadIdx.x; j < W; j += blockDim.x)
         for (int i = 1; i < H; ++i) m2[i * W + j] = min(m2[i * W + j], m2[(i - 1) * W + j]);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0)
         for (int j = 1; j < W; ++j) b1[j] = min(b1[j], b1[j - 1]);
+    __syncthreads();
+    // keys -> decision words: canonical winner index | near-tie flag (the replay then
+    // needs one load per select instead of key -> TR -> index -> canonical chains)
+    const int* canon = rm->canon;
+    const uint16_t kMask = 0xFFFFu;
+    for (int i = threadIdx.x; i < W * H; i += blockDim.x) {
+        const uint32_t k = m2[i];
+        if (k == kNone32) continue;
+        const uint32_t w = (uint32_t)canon[d.inv_tr[k & kMask]];
+        m2[i] = w | (d.danger[ORD_E][k >> 16] ? kWordDanger : 0u);
+    }
+    for (int i = threadIdx.x; i < W; i += blockDim.x) {
+        const uint32_t k = b1[i];
+        if (k == kNone32) continue;
+        const uint32_t w = (uint32_t)canon[d.inv_tr[k & kMask]];
+        b1[i] = w | (d.danger[ORD_T][k >> 16] ? kWordDanger : 0u);
+    }
+    if (threadIdx.x == 0) {
         // plant constants: unconstrained throughput (sim.hpp:258-264) and the p_node range
         const Analytic& a = *rm->plant;
         double pmin = 0.0, pmax = 0.0;
@@ -408,8 +440,8 @@ __global__ void __launch_bounds__(1024) k_build_tables(PlanDev d, ReplayModelDev
         rm->p_max = pmax;
         rm->nd_t = ndt;
         rm->nd_p = ndp;
-        rm->gmax_t = d.globals[0];
-        rm->gmin_p = d.globals[1];
+        rm->gmax_t = canon[d.globals[0]];
+        rm->gmin_p = canon[d.globals[1]];
         rm->generic = d.globals[2];
     }
 }

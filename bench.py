@@ -420,6 +420,33 @@ def run_ours(args, dist: Dist):
                      "algorithmic": "40 B per prediction (24 B point in, 16 B T/P out)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs"}}
 
+    # ---------------- cfg1: single-call latency (the drop-in's synchronous API) ----------------
+    from paper_2605_21427_b200.abi import CtrlState, Point, Telemetry
+    from paper_2605_21427_b200.wattserve import control_step, make_targets, select_config
+    c1 = workloads.cfg1()
+    m1 = AnalyticModel(ctx, c1["profile"], c1["gpu"])
+    th1, _, _ = Plan(m1, Grid(ctx, c1["points"]), c1["coeffs"]).scores()
+    tgt = make_targets(0.6 * float(th1.max()), 1600.0)
+    for _ in range(20):
+        select_config(c1["points"], tgt, m1, c1["coeffs"], 1.0, 0.05, 0.02)
+    t0 = time.perf_counter()
+    for _ in range(200):
+        select_config(c1["points"], tgt, m1, c1["coeffs"], 1.0, 0.05, 0.02)
+    sel_us = (time.perf_counter() - t0) / 200 * 1e6
+    st = CtrlState()
+    st.bias = 1.0
+    st.current = Point(*c1["points"][-1].tolist())
+    ccfg = workloads.cfg4_setup()["cfg"]
+    t0 = time.perf_counter()
+    for k in range(200):
+        _, st = control_step(Telemetry(0.5 * k, 0.55 * float(th1.max())), 0.5 * k, tgt,
+                             c1["points"], m1, c1["coeffs"], st, ccfg)
+    step_us = (time.perf_counter() - t0) / 200 * 1e6
+    latency = {"workload": "cfg1: llama2-7b-like, 6 caps x 6 batches (36 candidates), target 0.6 x "
+                           "unconstrained, static 1600 W budget",
+               "select_config_us": sel_us, "control_step_us": step_us,
+               "note": "one synchronous C-ABI call (H2D + 1 kernel + D2H); wall clock"}
+
     out = {
         "metric": METRIC, "value": value, "unit": "config evals/s",
         "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
@@ -446,12 +473,14 @@ def run_ours(args, dist: Dist):
                     "api": "pals_replay (C ABI, host summaries)"},
             "roofline": dec_roof, "gpu_launches": int(rlaunches)},
         "predictions": predictions,
+        "latency": latency,
         "peaks": {"int_ops_per_s": int_peak, "fp64_flops_per_s": fp64_peak,
                   "hbm_gbs_measured": measured_peaks_json().get("hbm_gbs")},
     }
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"], out["decisions"]["cpu_baseline"] = cpu_baselines(args, cfg, tref)
         out["predictions"]["cpu_baseline"] = cpu_predict(args, bundle, args.cpu_seconds)
+        out["latency"]["cpu_reference_select_config_us"] = cpu_latency(c1, float(th1.max()))
     if dist.rank == 0:
         print(json.dumps(out), flush=True)
     dist.close()
@@ -542,6 +571,18 @@ def cpu_predict(args, bundle, seconds):
     return {"value": n / t, "unit": "predictions/s", "cores": threads, "kind": "reference",
             "sample": f"{n} random points through the unmodified PredictorBundle::predict "
                       f"(same bundle), {threads} threads, {t:.1f} s"}
+
+
+def cpu_latency(c1, tmax):
+    """One select_config call on the cfg1 grid through the unmodified reference (1 thread)."""
+    kind, ref = _reference_backend()
+    if kind != "reference":
+        return None
+    from paper_2605_21427_b200.wattserve import make_queries
+    q = make_queries(np.full(20_000, 0.6 * tmax), 1600.0, 1.0, 0.05, 0.02)
+    t, _, _ = ref.bench_select(c1["profile"], c1["gpu"], c1["points"], c1["coeffs"], q, 1,
+                               want_results=False)
+    return t / len(q) * 1e6
 
 
 def cpu_baselines(args, cfg, tref):

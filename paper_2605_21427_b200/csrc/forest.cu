@@ -21,6 +21,7 @@
 namespace pals {
 
 constexpr int kNumeric = 5;                 // cap, batch, tp, ep, dp (forest.hpp:24)
+constexpr int kLut = 1024;                  // integer-feature coordinate lookup range
 constexpr int64_t kMaxCells = 1ll << 22;    // cell tables above this use the direct walk
 
 struct ForestDev {
@@ -40,6 +41,9 @@ struct ForestDev {
     int rep_off[kNumeric + 1];
     int64_t dims[kNumeric];
     int64_t n_cells;             // 0 = no table
+    // integer features (batch, tp, ep, dp): cell coordinate of every value in
+    // [0, kLut) precomputed (= the lower_bound the lattice uses), one byte each
+    const uint8_t* lut;          // [4][kLut]
     double* tabT;
     double* tabP;
 };
@@ -171,7 +175,22 @@ __global__ void k_forest_eval_aos(ForestDev f, int64_t n, const pals_point* __re
         const pals_point p = pts[i];
         const double x5[kNumeric] = {p.cap_watts, (double)p.batch, (double)p.tp, (double)p.ep,
                                      (double)p.dp};
-        if (use_cells) {
+        if (use_cells && f.lut) {
+            // cap: binary search; integer features: one byte lookup each (independent loads)
+            const int iv[4] = {p.batch, p.tp, p.ep, p.dp};
+            int64_t c = lower_bound_d(f.th + f.th_off[0], f.th_off[1] - f.th_off[0], p.cap_watts);
+#pragma unroll
+            for (int k = 1; k < kNumeric; ++k) {
+                const int v = iv[k - 1];
+                const int j = (v >= 0 && v < kLut)
+                                  ? (int)f.lut[(k - 1) * kLut + v]
+                                  : lower_bound_d(f.th + f.th_off[k], f.th_off[k + 1] - f.th_off[k],
+                                                  (double)v);
+                c = c * f.dims[k] + j;
+            }
+            T[i] = f.tabT[c];
+            P[i] = f.tabP[c];
+        } else if (use_cells) {
             const int64_t c = cell_of(f, x5);
             T[i] = f.tabT[c];
             P[i] = f.tabP[c];
@@ -300,9 +319,19 @@ extern "C" int pals_model_forest(pals_ctx* ctx, int32_t n_models, int32_t model_
     d.n_trees_P = p_n_trees;
     d.n_features = nf;
     d.model_index = model_index;
+    // integer-feature coordinate lookups: lower_bound(thresholds, (double)v) for v < kLut
+    std::vector<uint8_t> lut((size_t)4 * kLut);
+    bool lut_ok = true;
+    for (int k = 1; k < kNumeric; ++k) {
+        const auto& v = ths[k];
+        if (v.size() > 254) lut_ok = false;
+        for (int x = 0; x < kLut; ++x)
+            lut[(size_t)(k - 1) * kLut + x] =
+                (uint8_t)(std::lower_bound(v.begin(), v.end(), (double)x) - v.begin());
+    }
     const size_t bytes = nn * (4 + 8 + 4 + 4) + roots.size() * 4 + (th_all.size() + 1) * 8 +
                          rep_all.size() * 8 + 2 * 8 * (size_t)std::max<int64_t>(1, d.n_cells) +
-                         16 * 256;
+                         lut.size() + 16 * 256;
     PALS_CUDA(cudaMalloc(&fh->slab, bytes));
     char* s = (char*)fh->slab;
     auto put = [&](const void* src, size_t b) {
@@ -318,6 +347,7 @@ extern "C" int pals_model_forest(pals_ctx* ctx, int32_t n_models, int32_t model_
     d.roots = (const int32_t*)put(roots.data(), roots.size() * 4);
     d.th = (const double*)put(th_all.data(), th_all.size() * 8);
     d.rep = (const double*)put(rep_all.data(), rep_all.size() * 8);
+    d.lut = lut_ok ? (const uint8_t*)put(lut.data(), lut.size()) : nullptr;
     d.tabT = (double*)s;
     s += (8 * std::max<int64_t>(1, d.n_cells) + 255) & ~(size_t)255;
     d.tabP = (double*)s;

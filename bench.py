@@ -67,11 +67,14 @@ class Dist:
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
+        self.backend = "nccl"
 
     def init(self, backend):
+        # PALS_BENCH_BACKEND=gloo lets several ranks share one GPU (CI of the N>1 path)
+        self.backend = os.environ.get("PALS_BENCH_BACKEND", backend)
         if self.world > 1:
             import torch.distributed as dist
-            dist.init_process_group(backend)
+            dist.init_process_group(self.backend)
             self.pg = dist
 
     def barrier(self):
@@ -88,7 +91,7 @@ class Dist:
         if not self.pg:
             return x
         import torch
-        dev = "cuda" if torch.cuda.is_available() else "cpu"
+        dev = "cuda" if (torch.cuda.is_available() and self.backend == "nccl") else "cpu"
         t = torch.tensor([x], dtype=torch.float64, device=dev)
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX if op == "max" else self.pg.ReduceOp.SUM)
         return float(t.item())
@@ -178,13 +181,14 @@ def run_ours(args, dist: Dist):
     from paper_2605_21427_b200.wattserve import (AnalyticModel, Context, Grid, Plan,
                                                  measure_peaks, replay, replay_device)
 
-    torch.cuda.set_device(dist.local)
+    dev = dist.local % max(1, torch.cuda.device_count())  # ranks may share a GPU (gloo CI)
+    torch.cuda.set_device(dev)
     dist.init("nccl")
     # a real (non-legacy-default) stream shared by torch and libpals_gpu, so the CUDA
     # events below bracket exactly the kernels the library launches
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    ctx = Context(dist.local)
+    ctx = Context(dev)
     ctx.set_stream(stream.cuda_stream)
     int_peak, fp64_peak = measure_peaks(ctx)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
@@ -219,7 +223,7 @@ def run_ours(args, dist: Dist):
     scanned_q = int(counts[0] + counts[1] + counts[2])
     pairs_step = scanned_q * n_cfg
     int_ops_step = (2 * counts[0] + 4 * counts[1] + 2 * counts[2]) * n_cfg
-    clocks = Clocks(dist.local)
+    clocks = Clocks(dev)
     clocks.start()
     launches0 = ctx.launches
     scan_ms = []
@@ -259,10 +263,12 @@ def run_ours(args, dist: Dist):
         packed = (d_idx.to(torch.int64) << 8) | d_rs.to(torch.int64)
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         g0.record(stream)
+        if dist.backend != "nccl":
+            packed = packed.cpu()
         out_all = gather_to_rank0(packed, nq * dist.world, dist.rank, dist.world)
         g1.record(stream)
         torch.cuda.synchronize()
-        gather = {"bytes": nq * dist.world * 8, "ms": g0.elapsed_time(g1), "backend": "nccl",
+        gather = {"bytes": nq * dist.world * 8, "ms": g0.elapsed_time(g1), "backend": dist.backend,
                   "rows": None if out_all is None else int(out_all.shape[0])}
     t_rank = float(np.sum(step_ms))
     t_max = dist.max(t_rank)

@@ -907,8 +907,14 @@ static int one_call(pals_ctx* ctx, const pals_model* m, const pals_point* cands,
         PALS_CUDA(cudaMalloc(&ctx->d_scratch, need));
         ctx->scratch_bytes = need;
     }
-    std::vector<char> host(need);
-    char* hb = host.data();
+    // pinned host staging, kept in the context (one H2D and one D2H per call)
+    if (ctx->pinned_bytes < need) {
+        if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+        ctx->h_pinned = nullptr;
+        PALS_CUDA(cudaHostAlloc(&ctx->h_pinned, need, cudaHostAllocDefault));
+        ctx->pinned_bytes = need;
+    }
+    char* hb = (char*)ctx->h_pinned;
     char* db = (char*)ctx->d_scratch;
     size_t off = 0;
     auto take = [&](size_t b) {
@@ -930,7 +936,7 @@ static int one_call(pals_ctx* ctx, const pals_model* m, const pals_point* cands,
         ((int*)(hb + o_dp))[i] = c.dp;
         ((int*)(hb + o_ep))[i] = c.ep;
     }
-    Analytic* d_an = nullptr;
+    const Analytic* d_an = nullptr;
     const bool stale = do_step && a.now_s - a.tel.t_s > 1.5 * a.cfg.interval_s;
     if (m->kind == MODEL_TABLE && !stale) {
         std::unordered_map<std::string, int64_t> first;
@@ -954,8 +960,12 @@ static int one_call(pals_ctx* ctx, const pals_model* m, const pals_point* cands,
             a.cur_T = a.cur_ok ? m->table_T[it->second] : 0.0;
         }
     } else if (m->kind == MODEL_ANALYTIC) {
-        PALS_CUDA(cudaMalloc(&d_an, sizeof(Analytic)));
-        PALS_CUDA(cudaMemcpy(d_an, &m->an, sizeof(Analytic), cudaMemcpyHostToDevice));
+        if (!m->d_an) {  // device copy of the profile, made once per model
+            auto* mm = const_cast<pals_model*>(m);
+            PALS_CUDA(cudaMalloc(&mm->d_an, sizeof(Analytic)));
+            PALS_CUDA(cudaMemcpy(mm->d_an, &m->an, sizeof(Analytic), cudaMemcpyHostToDevice));
+        }
+        d_an = m->d_an;
     }
     PALS_CUDA(cudaMemcpyAsync(db, hb, off, cudaMemcpyHostToDevice, s));
     if (m->kind == MODEL_FOREST) {
@@ -982,17 +992,16 @@ static int one_call(pals_ctx* ctx, const pals_model* m, const pals_point* cands,
     k_one<<<1, 32, 0, s>>>(a);
     count_launch(ctx);
     cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) {
-        cudaFree(d_an);
-        return cuda_fail(e, "k_one");
-    }
+    if (e != cudaSuccess) return cuda_fail(e, "k_one");
+    // outputs and state are adjacent in the staging layout: one D2H
+    cudaMemcpyAsync(hb + o_out, db + o_out, o_st + sizeof(pals_ctrl_state) - o_out,
+                    cudaMemcpyDeviceToHost, s);
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "k_one sync");
     int out[8];
     pals_ctrl_state st{};
-    cudaMemcpyAsync(out, db + o_out, sizeof out, cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(&st, db + o_st, sizeof st, cudaMemcpyDeviceToHost, s);
-    e = cudaStreamSynchronize(s);
-    cudaFree(d_an);
-    if (e != cudaSuccess) return cuda_fail(e, "k_one sync");
+    memcpy(out, hb + o_out, sizeof out);
+    memcpy(&st, hb + o_st, sizeof st);
     if (out[2] != PALS_OK) return set_error(out[2], "unscored candidate");
     if (!do_step) {
         out_d->point = cands[out[0]];

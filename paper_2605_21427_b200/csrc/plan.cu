@@ -87,9 +87,6 @@ struct pals_plan {
     int64_t g_n = -1;
     int g_timed = 0;
     int64_t g_launches = 0;
-    // side stream for the query preparation inside a step
-    cudaStream_t aux = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 namespace pals {
@@ -1026,9 +1023,6 @@ int pals_plan_destroy(pals_plan* p) {
     if (!p) return PALS_OK;
     cudaSetDevice(p->ctx->device);
     if (p->gexec) cudaGraphExecDestroy(p->gexec);
-    if (p->aux) cudaStreamDestroy(p->aux);
-    if (p->ev_fork) cudaEventDestroy(p->ev_fork);
-    if (p->ev_join) cudaEventDestroy(p->ev_join);
     if (p->ev_scan0) cudaEventDestroy(p->ev_scan0);
     if (p->ev_scan1) cudaEventDestroy(p->ev_scan1);
     cudaFree(p->slab);
@@ -1183,30 +1177,6 @@ int pals_plan_select_device(pals_plan* p, const pals_query* d_queries, int64_t n
     return rc ? rc : select_tail(p, a);
 }
 
-// A full step with the query preparation on a side stream, overlapping the
-// key assignment: head -> {assign || qprep} -> scan -> finalize -> exact.
-static int step_forked(pals_plan* p, const pals_query* d_queries, int64_t nq, int32_t* d_idx,
-                       uint8_t* d_reason) {
-    cudaStream_t s = p->ctx->stream;
-    if (!p->aux) {
-        PALS_CUDA(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking));
-        PALS_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
-        PALS_CUDA(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
-    }
-    int rc = prep_head(p);
-    if (rc) return rc;
-    const SelArgs a = make_args(p, d_queries, nq, d_idx, d_reason);
-    PALS_CUDA(cudaEventRecord(p->ev_fork, s));
-    PALS_CUDA(cudaStreamWaitEvent(p->aux, p->ev_fork, 0));
-    rc = select_head(p, a, p->aux);
-    if (rc) return rc;
-    PALS_CUDA(cudaEventRecord(p->ev_join, p->aux));
-    rc = prep_tail(p);
-    if (rc) return rc;
-    PALS_CUDA(cudaStreamWaitEvent(s, p->ev_join, 0));
-    return select_tail(p, a);
-}
-
 // One full step — evaluate + rank (prepare) and select — replayed from a CUDA graph
 // captured on first use for these device buffers (9 kernels + 5 memsets per step;
 // the graph removes the per-launch host overhead between them).
@@ -1230,8 +1200,8 @@ int pals_plan_run(pals_plan* p, const pals_query* d_queries, int64_t nq, int32_t
         PALS_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
         p->capturing = 1;
         const int64_t l0 = ctx->launches;
-        // (step_forked, which overlaps qprep with k_assign on a side stream, measured
-        // no faster on B200: the step stays a single chain)
+        // (overlapping qprep with k_assign on a side stream measured no faster on
+        // B200: the step stays a single chain)
         rc = prep_head(p);
         if (!rc) rc = prep_tail(p);
         if (!rc) {

@@ -37,6 +37,10 @@ METRIC = "config evals/sec + controller decisions/sec at 1/2/4/8 B200 vs CPU ref
 SELECT_WORKLOAD = ("cfg2: llama2-7b-like (+tp8 comm), caps 100+300i/63 x batch 1..256 x "
                    "tp{1,2,4,8} = 65536 configs, 1e4 QoS targets per GPU, eval+rank+select "
                    "per step")
+ALLOC_WORKLOAD = ("allocate_budget: 1e6 independent clusters per GPU, 1-8 nodes each over the 8 "
+                  "calibrated profiles (6x6 candidates at the deployment, dp 1-3), targets "
+                  "U(0.2,1) x unconstrained, budgets floors..1.15 x peak, quantum 25 W, "
+                  "selection margin 0.02")
 REPLAY_WORKLOAD = ("cfg4: 1e6 fluid-plant traces x 3600 control intervals per GPU, 8 calibrated "
                    "profiles, 6x6 candidates each, QoS/budget-throughput 50/50")
 
@@ -54,6 +58,8 @@ def parse():
                     help="timed replay steps (default: min(steps, 5))")
     ap.add_argument("--predictions", type=int, default=1 << 24,
                     help="points per GPU for the forest-predictor leg")
+    ap.add_argument("--clusters", type=int, default=1_000_000,
+                    help="allocate_budget problems per GPU for the allocator leg")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU time per reference sample")
@@ -426,6 +432,9 @@ def run_ours(args, dist: Dist):
                      "algorithmic": "40 B per prediction (24 B point in, 16 B T/P out)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs"}}
 
+    # ---------------- allocate_budget over many clusters ----------------
+    allocations = bench_allocations(args, dist, ctx, stream, l2_flush)
+
     # ---------------- cfg1: single-call latency (the drop-in's synchronous API) ----------------
     from paper_2605_21427_b200.abi import CtrlState, Point, Telemetry
     from paper_2605_21427_b200.wattserve import control_step, make_targets, select_config
@@ -479,6 +488,7 @@ def run_ours(args, dist: Dist):
                     "api": "pals_replay (C ABI, host summaries)"},
             "roofline": dec_roof, "gpu_launches": int(rlaunches)},
         "predictions": predictions,
+        "allocations": allocations,
         "latency": latency,
         "peaks": {"int_ops_per_s": int_peak, "fp64_flops_per_s": fp64_peak,
                   "hbm_gbs_measured": measured_peaks_json().get("hbm_gbs")},
@@ -486,10 +496,147 @@ def run_ours(args, dist: Dist):
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"], out["decisions"]["cpu_baseline"] = cpu_baselines(args, cfg, tref)
         out["predictions"]["cpu_baseline"] = cpu_predict(args, bundle, args.cpu_seconds)
+        out["allocations"]["cpu_baseline"] = cpu_allocate(args, args.cpu_seconds)
         out["latency"]["cpu_reference_select_config_us"] = cpu_latency(c1, float(th1.max()))
     if dist.rank == 0:
         print(json.dumps(out), flush=True)
     dist.close()
+
+
+def alloc_setup_gpu(ctx):
+    """Allocator + per-model scales (unconstrained t_hat, peak p_node at dp 1) from the GPU."""
+    from paper_2605_21427_b200 import workloads
+    from paper_2605_21427_b200.wattserve import Allocator, AnalyticModel, Grid, Plan
+    s = workloads.cfg4_setup()
+    models = [AnalyticModel(ctx, p, s["gpu"]) for p in s["profiles"]]
+    tm, pm = [], []
+    for p, m in zip(s["profiles"], models):
+        pts = workloads.grid_points(s["caps"], s["batches"], [p.deploy_tp], [p.deploy_ep], [1])
+        th, pn, _ = Plan(m, Grid(ctx, pts), s["coeffs"]).scores()
+        tm.append(float(th.max()))
+        pm.append(float(pn.max()))
+    al = Allocator(ctx, models, s["profiles"], s["gpu"], s["coeffs"], s["caps"], s["batches"],
+                   max_dp=3, selection_margin=0.02)
+    return s, al, tm, pm
+
+
+def bench_allocations(args, dist, ctx, stream, l2_flush):
+    import torch
+    from paper_2605_21427_b200 import workloads
+    s, al, tm, pm = alloc_setup_gpu(ctx)
+    n = args.clusters
+    prob = workloads.alloc_problems(n, 2605, tm, pm, s["gpu"], s["coeffs"], first=dist.rank * n)
+    nn = int(prob["off"][-1])
+    host = {k: torch.from_numpy(np.ascontiguousarray(v)) for k, v in
+            (("off", prob["off"]), ("model", prob["model"]), ("dp", prob["dp"]),
+             ("target", prob["target"]), ("budget", prob["budget"]))}
+    dev = {k: v.cuda() for k, v in host.items()}
+    pin = {k: v.pin_memory() for k, v in host.items()}
+    out_d = dict(nb=torch.empty(nn, dtype=torch.float64, device="cuda"),
+                 tot=torch.empty(n, dtype=torch.float64, device="cuda"),
+                 sat=torch.empty(n, dtype=torch.uint8, device="cuda"),
+                 st=torch.empty(n, dtype=torch.int32, device="cuda"))
+    out_h = dict(nb=torch.empty(nn, dtype=torch.float64).pin_memory(),
+                 tot=torch.empty(n, dtype=torch.float64).pin_memory(),
+                 sat=torch.empty(n, dtype=torch.uint8).pin_memory(),
+                 st=torch.empty(n, dtype=torch.int32).pin_memory())
+
+    def step():
+        al.run_device(25.0, n, nn, dev["off"].data_ptr(), dev["model"].data_ptr(),
+                      dev["dp"].data_ptr(), dev["target"].data_ptr(), dev["budget"].data_ptr(),
+                      out_d["nb"].data_ptr(), out_d["tot"].data_ptr(), out_d["sat"].data_ptr(),
+                      out_d["st"].data_ptr())
+
+    def e2e_step():
+        rc = ctx.lib.pals_allocate_budget(
+            al.h, 25.0, n, pin["off"].data_ptr(), pin["model"].data_ptr(), pin["dp"].data_ptr(),
+            pin["target"].data_ptr(), pin["budget"].data_ptr(), out_h["nb"].data_ptr(),
+            out_h["tot"].data_ptr(), out_h["sat"].data_ptr(), out_h["st"].data_ptr())
+        assert rc == 0, ctx.lib.pals_last_error()
+
+    for _ in range(args.warmup):
+        step()
+        e2e_step()
+    torch.cuda.synchronize()
+    l0 = ctx.lib.pals_ctx_launch_count(ctx.h)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    for k in range(args.steps):
+        l2_flush()
+        ev[k][0].record(stream)
+        step()
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    launches = ctx.lib.pals_ctx_launch_count(ctx.h) - l0
+    t_max = dist.max(float(np.sum([a.elapsed_time(b) for a, b in ev])))
+    value = dist.sum(float(n)) * args.steps / (t_max * 1e-3)
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    e2e_t = dist.max(time.perf_counter() - t0)
+    e2e = dist.sum(float(n)) * args.steps / e2e_t
+    status = out_h["st"].numpy()
+    # algorithmic bytes per cluster: offsets 8 + budget 8 + per node (model 4 + dp 4 +
+    # target 8 in, budget 8 out) + total 8 + flag 1 + status 4 out
+    nbytes = (8 + 8 + 8 + 1 + 4) * n + 24 * nn
+    hbm = measured_peaks_json().get("hbm_gbs", 6552.6)
+    ach = nbytes / (t_max * 1e-3 / args.steps) / 1e9
+    return {
+        "metric": "cluster budget allocations/s (allocate_budget, water-filling)",
+        "value": value, "unit": "allocations/s", "ms_per_step": t_max / args.steps,
+        "steps": args.steps, "workload": ALLOC_WORKLOAD, "clusters_per_gpu": n,
+        "nodes_per_gpu": nn, "ok_fraction": float((status == 0).mean()),
+        "e2e": {"value": e2e, "unit": "allocations/s",
+                "h2d_bytes_per_step": int(8 * (n + 1) + 16 * nn + 8 * n),
+                "d2h_bytes_per_step": int(8 * nn + 13 * n),
+                "api": "pals_allocate_budget (C ABI, pinned host buffers)"},
+        "roofline": {"bound": "hbm", "kernel": "k_allocate", "achieved": ach, "peak": hbm,
+                     "unit": "GB/s", "frac": ach / hbm, "traffic": ncu_traffic("k_allocate"),
+                     "algorithmic": "29 B per cluster + 24 B per node",
+                     "note": "the kernel is bound by its serial per-cluster FP64 loop "
+                             "(thread per cluster), not by HBM; the byte roofline is "
+                             "reported for completeness",
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+        "gpu_launches": int(launches),
+    }
+
+
+def cpu_allocate(args, seconds):
+    """allocate_budget through the unmodified reference, all host threads."""
+    from paper_2605_21427_b200 import workloads
+    kind, ref = _reference_backend()
+    from oracle.oracle import Oracle, oracle_allocate, ref_bench_allocate
+    s = workloads.cfg4_setup()
+    orc = Oracle()
+    tm, pm = [], []
+    for p in s["profiles"]:
+        pts = workloads.grid_points(s["caps"], s["batches"], [p.deploy_tp], [p.deploy_ep], [1])
+        T, P, _ = orc.eval(p, s["gpu"], pts)
+        tm.append(float(T.max()))
+        pm.append(float((s["coeffs"].alpha * 4 * P + s["coeffs"].beta_watts).max()))
+    threads = os.cpu_count() or 1
+    if kind == "reference":
+        probe = workloads.alloc_problems(2000 * threads, 2605, tm, pm, s["gpu"], s["coeffs"])
+        t, _ = ref_bench_allocate(ref, s["profiles"], s["gpu"], s["coeffs"], s["caps"],
+                                  s["batches"], 25.0, 0.02, probe, threads)
+        rate = len(probe["budget"]) / t
+        n = int(max(2000 * threads, min(args.clusters, rate * seconds)))
+        prob = workloads.alloc_problems(n, 2605, tm, pm, s["gpu"], s["coeffs"])
+        t, _ = ref_bench_allocate(ref, s["profiles"], s["gpu"], s["coeffs"], s["caps"],
+                                  s["batches"], 25.0, 0.02, prob, threads)
+        return {"value": n / t, "unit": "allocations/s", "cores": threads, "kind": "reference",
+                "sample": f"{n} clusters of the same workload through the unmodified "
+                          f"allocate_budget (analytic scorer, steps rebuilt per call as the "
+                          f"reference does), {threads} threads, {t:.1f} s"}
+    prob = workloads.alloc_problems(2000, 2605, tm, pm, s["gpu"], s["coeffs"])
+    t0 = time.perf_counter()
+    oracle_allocate(orc, s["profiles"], s["gpu"], s["coeffs"], s["caps"], s["batches"], 25.0,
+                    0.02, prob)
+    t = time.perf_counter() - t0
+    return {"value": 2000 / t, "unit": "allocations/s", "cores": 1, "kind": "port",
+            "sample": "2000 clusters, C restatement, 1 thread"}
 
 
 # ---------------------------------------------------------- CPU reference --
@@ -617,6 +764,7 @@ def run_reference(args, dist: Dist):
             vals.append(b)
     v = float(np.mean([b["value"] for b in vals]))
     dec = cpu_replay(args, per_step)
+    alc = cpu_allocate(args, per_step)
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "config evals/s",
            "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
@@ -629,7 +777,12 @@ def run_reference(args, dist: Dist):
                          "unit": "decisions/s", "workload": REPLAY_WORKLOAD,
                          "cpu_baseline": dec,
                          "e2e": {"value": dec["value"], "unit": "decisions/s",
-                                 "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}}
+                                 "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}},
+           "allocations": {"metric": "cluster budget allocations/s", "value": alc["value"],
+                           "unit": "allocations/s", "workload": ALLOC_WORKLOAD,
+                           "cpu_baseline": alc,
+                           "e2e": {"value": alc["value"], "unit": "allocations/s",
+                                   "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}}
     print(json.dumps(out), flush=True)
 
 

@@ -15,6 +15,8 @@
  *   pals_model_table     TableScorer (test fake)                    tests/test_controller.cpp:17-29
  *   pals_model_forest    predictor_scorer(bundle, model_id)         controller.hpp:100-105,
  *                                                                    forest.hpp:227-235
+ *   pals_allocate_budget allocate_budget() over many clusters      allocator.hpp:76-186,
+ *                        (assign_budgets' per-node requests)       sim.hpp:313-336
  *
  * Plain C types only: pointers, sizes, POD structs. No torch, no C++.
  * Errors follow the reference's exception taxonomy (types.hpp:13-23):
@@ -344,6 +346,50 @@ int pals_replay_device(pals_ctx* ctx, int32_t n_models, pals_model* const* model
                        const int32_t* batches, int32_t n_batches, const pals_ctrl_cfg* cfg,
                        const pals_replay_spec* spec, pals_trace_summary* d_summaries,
                        pals_step_log* d_logs);
+
+/* ---- cluster budget allocator (allocator.hpp:76-186), batched ---------- */
+/* Replaces wattserve::allocate_budget(nodes, cluster_budget_w, gpu, coeffs, quantum_w,
+ * selection_margin) (allocator.hpp:76-79) for many independent clusters ("problems")
+ * at once, as sim.hpp's assign_budgets builds them (sim.hpp:318-331): node i of a
+ * problem runs model node_model[i] (scored by models[k]) with candidates
+ * caps x batches at deploy[k].deploy_tp / deploy_ep and dp = node_dp[i].
+ * pals_alloc_create precomputes every (model, dp in 1..max_dp) budget-step table
+ * (detail::throughput_steps allocator.hpp:34-56 and the margin scaling :106). */
+typedef struct pals_alloc pals_alloc;
+int pals_alloc_create(pals_ctx* ctx, int32_t n_models, pals_model* const* models,
+                      const pals_profile* deploy, const pals_gpu_spec* gpu,
+                      const pals_coeffs* coeffs, const double* caps, int32_t n_caps,
+                      const int32_t* batches, int32_t n_batches, int32_t max_dp,
+                      double selection_margin, pals_alloc** out);
+/* General form: candidate set s = points[set_offset[s] .. set_offset[s+1]) scored by
+ * set_models[s] (one AllocRequest's candidates + score, allocator.hpp:13-19); a node then
+ * names its set in node_model and its dp (for the floor, allocator.hpp:82-83) in node_dp. */
+int pals_alloc_create_sets(pals_ctx* ctx, int32_t n_sets, pals_model* const* set_models,
+                           const pals_point* points, const int64_t* set_offset,
+                           const pals_gpu_spec* gpu, const pals_coeffs* coeffs,
+                           double selection_margin, pals_alloc** out);
+int pals_alloc_destroy(pals_alloc* a);
+/* Host copy of one set's budget steps: n_steps, then power_w / throughput_tps (either
+ * may be NULL). In the (model, dp) form set = model * max_dp + dp - 1. */
+int pals_alloc_steps(pals_alloc* a, int32_t set, double* power_w, double* throughput_tps,
+                     int32_t* n_steps);
+/* Problem p owns nodes [node_offset[p], node_offset[p+1]). Per problem: the node budgets
+ * (AllocResult::node_budgets_w), total_allocated_w, all_targets_satisfied and a status
+ * code: PALS_OK, or the error allocate_budget would throw for that problem (PALS_ECONFIG
+ * for no nodes / budget below the floors / a scorer config_error, PALS_ERANGE for a
+ * scorer out_of_range or a dp beyond max_dp). Host buffers, synchronous. */
+int pals_allocate_budget(pals_alloc* a, double quantum_w, int64_t n_problems,
+                         const int64_t* node_offset, const int32_t* node_model,
+                         const int32_t* node_dp, const double* node_target,
+                         const double* cluster_budget, double* node_budget, double* total,
+                         uint8_t* all_satisfied, int32_t* status);
+/* Same with device-resident buffers, async on the context stream (n_nodes = node_offset[n]). */
+int pals_alloc_run_device(pals_alloc* a, double quantum_w, int64_t n_problems,
+                          const int64_t* d_node_offset, int64_t n_nodes,
+                          const int32_t* d_node_model, const int32_t* d_node_dp,
+                          const double* d_node_target, const double* d_cluster_budget,
+                          double* d_node_budget, double* d_total, uint8_t* d_all_satisfied,
+                          int32_t* d_status);
 
 #ifdef __cplusplus
 }

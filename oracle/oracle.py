@@ -276,6 +276,58 @@ class Reference:
         return g, k
 
 
+_ALLOC_ARGS = [C.c_int, _VP, _VP, _VP, _VP, C.c_int, _VP, C.c_int, C.c_double, C.c_double,
+               C.c_int64] + [_VP] * 9
+
+
+def _alloc_call(fn, plant, gpu, coeffs, caps, batches, quantum, margin, prob, extra=()):
+    """Shared marshalling for or_allocate / ref_allocate / ref_bench_allocate: ``prob`` is the
+    dict of workloads.alloc_problems (off, model, dp, target, budget)."""
+    profs = (Profile * len(plant))(*plant)
+    caps = np.ascontiguousarray(caps, np.float64)
+    batches = np.ascontiguousarray(batches, np.int32)
+    off = np.ascontiguousarray(prob["off"], np.int64)
+    model = np.ascontiguousarray(prob["model"], np.int32)
+    dp = np.ascontiguousarray(prob["dp"], np.int32)
+    tgt = np.ascontiguousarray(prob["target"], np.float64)
+    bud = np.ascontiguousarray(prob["budget"], np.float64)
+    npb = len(off) - 1
+    nb_out = np.zeros(len(model), np.float64)
+    total = np.zeros(npb, np.float64)
+    sat = np.zeros(npb, np.uint8)
+    status = np.zeros(npb, np.int32)
+    r = fn(len(plant), profs, C.byref(gpu), C.byref(coeffs), ptr(caps), len(caps), ptr(batches),
+           len(batches), quantum, margin, npb, ptr(off), ptr(model), ptr(dp), ptr(tgt), ptr(bud),
+           ptr(nb_out), ptr(total), ptr(sat), ptr(status), *extra)
+    return r, dict(node_budget=nb_out, total=total, all_sat=sat, status=status)
+
+
+def oracle_allocate(orc: Oracle, plant, gpu, coeffs, caps, batches, quantum, margin, prob):
+    """allocate_budget per problem, restated in C (pals_oracle.c or_allocate)."""
+    orc.lib.or_allocate.argtypes = _ALLOC_ARGS
+    _, out = _alloc_call(orc.lib.or_allocate, plant, gpu, coeffs, caps, batches, quantum,
+                         margin, prob)
+    return out
+
+
+def ref_allocate(ref: Reference, plant, gpu, coeffs, caps, batches, quantum, margin, prob):
+    """The reference's allocate_budget (allocator.hpp:76) per problem."""
+    ref.lib.ref_allocate.argtypes = _ALLOC_ARGS
+    _, out = _alloc_call(ref.lib.ref_allocate, plant, gpu, coeffs, caps, batches, quantum,
+                         margin, prob)
+    return out
+
+
+def ref_bench_allocate(ref: Reference, plant, gpu, coeffs, caps, batches, quantum, margin, prob,
+                       threads: int):
+    L = ref.lib
+    L.ref_bench_allocate.restype = C.c_double
+    L.ref_bench_allocate.argtypes = _ALLOC_ARGS + [C.c_int]
+    secs, out = _alloc_call(L.ref_bench_allocate, plant, gpu, coeffs, caps, batches, quantum,
+                            margin, prob, extra=(threads,))
+    return secs, out
+
+
 def _forest_args(fs):
     return [fs.n_trees, ptr(fs.tree_offset), ptr(fs.feature), ptr(fs.threshold), ptr(fs.left),
             ptr(fs.right), ptr(fs.value)]

@@ -496,3 +496,149 @@ int or_forest_predict(int n_models, int model_index, const pals_coeffs* k, int t
     free(x);
     return PALS_OK;
 }
+
+/* ---- cluster budget allocator (allocator.hpp) -------------------------- */
+typedef struct {
+    double power_w, thr;
+} bstep;
+
+/* throughput_steps sort: power ascending, then throughput descending (allocator.hpp:44-47) */
+static int bstep_cmp(const void* a, const void* b) {
+    const bstep* x = (const bstep*)a;
+    const bstep* y = (const bstep*)b;
+    if (x->power_w != y->power_w) return x->power_w < y->power_w ? -1 : 1;
+    if (x->thr != y->thr) return x->thr > y->thr ? -1 : 1;
+    return 0;
+}
+
+/* detail::throughput_steps allocator.hpp:34-56, then the margin scaling :106 */
+static int node_steps(const pals_profile* p, const pals_gpu_spec* g, const pals_coeffs* k,
+                      const double* caps, int nc, const int* batches, int nb, int dp,
+                      double margin, bstep* out) {
+    int m = 0;
+    for (int a = 0; a < nc; ++a)
+        for (int b = 0; b < nb; ++b) {
+            pals_point c = {caps[a], batches[b], p->deploy_tp, p->deploy_ep, dp};
+            double T, P;
+            or_score(&c, p, g, &T, &P);
+            out[m].power_w = (double)dp * (k->alpha * 4.0 * P + k->beta_watts);
+            out[m].thr = (double)dp * T;
+            ++m;
+        }
+    qsort(out, (size_t)m, sizeof(bstep), bstep_cmp);
+    int ns = 0;
+    double best = 0.0;
+    for (int i = 0; i < m; ++i)
+        if (out[i].thr > best + 1e-12) {
+            out[ns++] = out[i];
+            best = out[i].thr;
+        }
+    for (int i = 0; i < ns; ++i) out[i].power_w /= 1.0 - margin;
+    return ns;
+}
+
+/* detail::best_throughput_under allocator.hpp:58-65 */
+static double best_under(const bstep* s, int ns, double budget) {
+    double best = 0.0;
+    for (int i = 0; i < ns; ++i) {
+        if (s[i].power_w > budget) break;
+        best = s[i].thr;
+    }
+    return best;
+}
+
+/* allocate_budget allocator.hpp:76-186 over independent problems (see ref_allocate) */
+int or_allocate(int n_models, const pals_profile* profs, const pals_gpu_spec* g,
+                const pals_coeffs* k, const double* caps, int nc, const int* batches, int nb,
+                double quantum, double margin, int64_t n_problems, const int64_t* off,
+                const int32_t* node_model, const int32_t* node_dp, const double* node_target,
+                const double* cluster_budget, double* node_budget, double* total,
+                uint8_t* all_sat, int32_t* status) {
+    (void)n_models;
+    const int ncand = nc * nb;
+    for (int64_t pi = 0; pi < n_problems; ++pi) {
+        const int64_t o = off[pi];
+        const int n = (int)(off[pi + 1] - o);
+        if (n <= 0) {
+            status[pi] = PALS_ECONFIG; /* "allocate_budget: no nodes" */
+            continue;
+        }
+        double* floor_w = (double*)malloc(sizeof(double) * n);
+        double* cur = (double*)malloc(sizeof(double) * n);
+        double* ceil_w = (double*)malloc(sizeof(double) * n);
+        int* ns = (int*)malloc(sizeof(int) * n);
+        bstep* st = (bstep*)malloc(sizeof(bstep) * (size_t)n * (size_t)ncand);
+        double* bud = node_budget + o;
+        double floor_total = 0.0;
+        for (int i = 0; i < n; ++i) {
+            floor_w[i] = (double)node_dp[o + i] * (k->alpha * 4.0 * g->min_cap_watts + k->beta_watts);
+            floor_total += floor_w[i];
+        }
+        if (floor_total > cluster_budget[pi]) {
+            status[pi] = PALS_ECONFIG;
+            free(floor_w); free(cur); free(ceil_w); free(ns); free(st);
+            continue;
+        }
+        double remaining = cluster_budget[pi] - floor_total;
+        for (int i = 0; i < n; ++i) {
+            bud[i] = floor_w[i];
+            ns[i] = node_steps(&profs[node_model[o + i]], g, k, caps, nc, batches, nb,
+                               node_dp[o + i], margin, st + (size_t)i * ncand);
+            cur[i] = best_under(st + (size_t)i * ncand, ns[i], bud[i]);
+        }
+        while (remaining >= quantum) {
+            int any_unmet = 0;
+            for (int i = 0; i < n; ++i) any_unmet |= !(cur[i] >= node_target[o + i]);
+            double best_rate = 0.0, best_cost = 0.0;
+            int best_i = n;
+            for (int i = 0; i < n; ++i) {
+                const double tgt = node_target[o + i];
+                if (any_unmet && cur[i] >= tgt) continue;
+                const bstep* s = st + (size_t)i * ncand;
+                for (int j = 0; j < ns[i]; ++j) {
+                    if (s[j].power_w <= bud[i] || s[j].thr <= cur[i]) continue;
+                    const double cost = ceil((s[j].power_w - bud[i]) / quantum) * quantum;
+                    if (cost > remaining) break;
+                    const double gain = any_unmet ? smin(s[j].thr, tgt) - smin(cur[i], tgt)
+                                                  : s[j].thr - cur[i];
+                    if (gain <= 1e-12) continue;
+                    const double rate = gain / cost;
+                    const int wins = best_i == n || rate > best_rate + 1e-12 ||
+                                     (rate > best_rate - 1e-12 && bud[i] < bud[best_i] - 1e-12);
+                    if (wins) {
+                        best_rate = rate;
+                        best_cost = cost;
+                        best_i = i;
+                    }
+                }
+            }
+            if (best_i == n) break;
+            bud[best_i] += best_cost;
+            cur[best_i] = best_under(st + (size_t)best_i * ncand, ns[best_i], bud[best_i]);
+            remaining -= best_cost;
+        }
+        for (int i = 0; i < n; ++i)
+            ceil_w[i] = ns[i] == 0 ? bud[i] : st[(size_t)i * ncand + ns[i] - 1].power_w + 2.0 * quantum;
+        while (remaining >= quantum) {
+            int lo = n;
+            for (int i = 0; i < n; ++i) {
+                if (bud[i] + quantum > ceil_w[i]) continue;
+                if (lo == n || bud[i] < bud[lo]) lo = i;
+            }
+            if (lo == n) break;
+            bud[lo] += quantum;
+            remaining -= quantum;
+        }
+        double tot = 0.0;
+        int sat = 1;
+        for (int i = 0; i < n; ++i) {
+            tot += bud[i];
+            sat &= cur[i] >= node_target[o + i];
+        }
+        total[pi] = tot;
+        all_sat[pi] = (uint8_t)sat;
+        status[pi] = PALS_OK;
+        free(floor_w); free(cur); free(ceil_w); free(ns); free(st);
+    }
+    return PALS_OK;
+}

@@ -640,6 +640,81 @@ int ref_load_platform(const char* path, pals_gpu_spec* gpu, pals_coeffs* coeffs)
 
 }  // extern "C"
 
+// ---- cluster budget allocator (allocator.hpp) -----------------------------
+extern "C" {
+
+// allocate_budget (allocator.hpp:76-186) for n_problems independent clusters.
+// Node j of problem p: nodes [off[p], off[p+1]); node_model selects one of the
+// n_models (profile, candidate grid) pairs: candidates = caps x batches at the
+// profile's deployment tp/ep with degree node_dp[j] for dp, scored by the
+// analytic scorer. status[p] = PALS code (config_error when the budget is below
+// the sum of node floors).
+int ref_allocate(int n_models, const pals_profile* profs, const pals_gpu_spec* gpu,
+                 const pals_coeffs* coeffs, const double* caps, int n_caps, const int* batches,
+                 int n_batches, double quantum_w, double margin, std::int64_t n_problems,
+                 const std::int64_t* off, const std::int32_t* node_model,
+                 const std::int32_t* node_dp, const double* node_target,
+                 const double* cluster_budget, double* node_budget, double* total,
+                 std::uint8_t* all_sat, std::int32_t* status) {
+    const GpuSpec g = to_gpu(*gpu);
+    const SystemPowerCoeffs k{coeffs->alpha, coeffs->beta_watts};
+    std::vector<ModelProfile> mps;
+    for (int m = 0; m < n_models; ++m) mps.push_back(to_profile(profs[m]));
+    for (std::int64_t p = 0; p < n_problems; ++p) {
+        std::vector<AllocRequest> reqs;
+        for (std::int64_t j = off[p]; j < off[p + 1]; ++j) {
+            const ModelProfile& mp = mps[node_model[j]];
+            AllocRequest r;
+            r.model_id = mp.name;
+            r.throughput_target_tps = node_target[j];
+            r.dp = node_dp[j];
+            for (int a = 0; a < n_caps; ++a)
+                for (int b = 0; b < n_batches; ++b)
+                    r.candidates.push_back(OperatingPoint{caps[a], batches[b], mp.deployment.tp,
+                                                          mp.deployment.ep, node_dp[j]});
+            r.score = analytic_scorer(mps[node_model[j]], g);
+            reqs.push_back(std::move(r));
+        }
+        try {
+            const auto res = allocate_budget(reqs, cluster_budget[p], g, k, quantum_w, margin);
+            for (std::size_t i = 0; i < reqs.size(); ++i)
+                node_budget[off[p] + i] = res.node_budgets_w[i];
+            total[p] = res.total_allocated_w;
+            all_sat[p] = res.all_targets_satisfied ? 1 : 0;
+            status[p] = PALS_OK;
+        } catch (...) {
+            status[p] = map_exception();
+        }
+    }
+    return PALS_OK;
+}
+
+// all host threads, for the CPU baseline
+double ref_bench_allocate(int n_models, const pals_profile* profs, const pals_gpu_spec* gpu,
+                          const pals_coeffs* coeffs, const double* caps, int n_caps,
+                          const int* batches, int n_batches, double quantum_w, double margin,
+                          std::int64_t n_problems, const std::int64_t* off,
+                          const std::int32_t* node_model, const std::int32_t* node_dp,
+                          const double* node_target, const double* cluster_budget,
+                          double* node_budget, double* total, std::uint8_t* all_sat,
+                          std::int32_t* status, int n_threads) {
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> th;
+    for (int t = 0; t < n_threads; ++t) {
+        th.emplace_back([&, t] {
+            const std::int64_t lo = n_problems * t / n_threads;
+            const std::int64_t hi = n_problems * (t + 1) / n_threads;
+            ref_allocate(n_models, profs, gpu, coeffs, caps, n_caps, batches, n_batches,
+                         quantum_w, margin, hi - lo, off + lo, node_model, node_dp, node_target,
+                         cluster_budget + lo, node_budget, total + lo, all_sat + lo, status + lo);
+        });
+    }
+    for (auto& x : th) x.join();
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // extern "C"
+
 // ---- tree-ensemble predictor (forest.hpp) ---------------------------------
 namespace {
 struct BundleCache {

@@ -65,6 +65,13 @@ SIGNATURES = [
                          _VP]),
     ("pals_replay_device", _I, [_VP, _I32, _VP, _VP, _VP, _VP, _VP, _I32, _VP, _I32, _VP, _VP,
                                 _VP, _VP]),
+    ("pals_alloc_create", _I, [_VP, _I32, _VP, _VP, _VP, _VP, _VP, _I32, _VP, _I32, _I32, _D,
+                               _VP]),
+    ("pals_alloc_destroy", _I, [_VP]),
+    ("pals_alloc_create_sets", _I, [_VP, _I32, _VP, _VP, _VP, _VP, _VP, _D, _VP]),
+    ("pals_alloc_steps", _I, [_VP, _I32, _VP, _VP, _VP]),
+    ("pals_allocate_budget", _I, [_VP, _D, _I64] + [_VP] * 9),
+    ("pals_alloc_run_device", _I, [_VP, _D, _I64, _VP, _I64] + [_VP] * 8),
 ]
 
 _lib = None

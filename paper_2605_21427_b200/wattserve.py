@@ -29,7 +29,7 @@ from ._lib import ConfigError, DataError, OutOfRange, PalsError, check  # noqa: 
 __all__ = [
     "Context", "AnalyticModel", "TableModel", "Grid", "Plan", "analytic_scorer",
     "table_scorer", "select_config", "control_step", "replay", "make_targets",
-    "default_context", "ConfigError", "DataError", "OutOfRange", "PalsError",
+    "default_context", "Allocator", "AllocResult", "allocate_budget", "ConfigError", "DataError", "OutOfRange", "PalsError",
 ]
 
 
@@ -335,3 +335,140 @@ def replay_device(ctx: Context, models, plant, gpu: GpuSpec, coeffs: Coeffs, cap
 
 
 OBJECTIVES = {"qos": OBJ_QOS, "budget-throughput": OBJ_BUDGET}
+
+
+class Allocator:
+    """Batched allocate_budget (allocator.hpp:76-186) over many independent clusters.
+
+    models[k] scores the candidates of nodes running model k: caps x batches at
+    deploy[k]'s deployment tp/ep and the node's dp (sim.hpp:318-331). Step tables for
+    every (model, dp <= max_dp) are built once here (pals_alloc_create)."""
+
+    def __init__(self, ctx: Context, models, deploy, gpu: GpuSpec, coeffs: Coeffs, caps,
+                 batches, max_dp: int = 8, selection_margin: float = 0.0):
+        self.ctx, self.lib = ctx, ctx.lib
+        self.models = list(models)  # keep the handles alive
+        n = len(self.models)
+        hs = (C.c_void_p * n)(*[m.h for m in self.models])
+        profs = (Profile * n)(*deploy)
+        self.caps = np.ascontiguousarray(caps, np.float64)
+        self.batches = np.ascontiguousarray(batches, np.int32)
+        self.gpu, self.coeffs, self.max_dp = gpu, coeffs, max_dp
+        self.max_cand = max(1, len(self.caps) * len(self.batches))
+        self.names = [bytes(p.name).split(b"\0")[0].decode() for p in deploy]
+        h = C.c_void_p()
+        check(self.lib.pals_alloc_create(ctx.h, n, hs, profs, C.byref(gpu), C.byref(coeffs),
+                                         ptr(self.caps), len(self.caps), ptr(self.batches),
+                                         len(self.batches), max_dp, selection_margin,
+                                         C.byref(h)))
+        self.h = h
+
+    @classmethod
+    def from_sets(cls, ctx: Context, sets, gpu: GpuSpec, coeffs: Coeffs,
+                  selection_margin: float = 0.0, names=None):
+        """General AllocRequest form: sets = [(model, candidate points)]; nodes then name a
+        set index in node_model (their dp only sets the floor)."""
+        self = cls.__new__(cls)
+        self.ctx, self.lib = ctx, ctx.lib
+        self.models = [m for m, _ in sets]
+        pts = [np.ascontiguousarray(p, dtype=POINT_DT) for _, p in sets]
+        off = np.zeros(len(sets) + 1, np.int64)
+        off[1:] = np.cumsum([len(p) for p in pts])
+        allp = np.concatenate(pts) if pts else np.zeros(0, POINT_DT)
+        allp = np.ascontiguousarray(allp if len(allp) else np.zeros(1, POINT_DT))
+        self.gpu, self.coeffs, self.max_dp = gpu, coeffs, 0
+        self.max_cand = max([1] + [len(p) for p in pts])
+        self.names = list(names) if names else [str(i) for i in range(len(sets))]
+        hs = (C.c_void_p * len(sets))(*[m.h for m in self.models])
+        h = C.c_void_p()
+        check(self.lib.pals_alloc_create_sets(ctx.h, len(sets), hs, ptr(allp), ptr(off),
+                                              C.byref(gpu), C.byref(coeffs), selection_margin,
+                                              C.byref(h)))
+        self.h = h
+        return self
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.pals_alloc_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def steps(self, model: int, dp: int | None = None):
+        """detail::throughput_steps (margin-scaled) of one set, (power_w, thr). In the
+        (model, dp) form pass both; in the from_sets form pass the set index only."""
+        set_ = model if dp is None else model * self.max_dp + dp - 1
+        n = C.c_int32(0)
+        pw, th = np.empty(self.max_cand), np.empty(self.max_cand)
+        check(self.lib.pals_alloc_steps(self.h, set_, ptr(pw), ptr(th), C.byref(n)))
+        return pw[: n.value].copy(), th[: n.value].copy()
+
+    def allocate(self, off, node_model, node_dp, node_target, cluster_budget,
+                 quantum_w: float = 25.0):
+        """Host arrays in/out. Returns dict(node_budget, total, all_sat, status)."""
+        off = np.ascontiguousarray(off, np.int64)
+        npb = len(off) - 1
+        node_model = np.ascontiguousarray(node_model, np.int32)
+        node_dp = np.ascontiguousarray(node_dp, np.int32)
+        node_target = np.ascontiguousarray(node_target, np.float64)
+        cluster_budget = np.ascontiguousarray(cluster_budget, np.float64)
+        nn = int(off.max()) if npb > 0 else 0
+        if min(len(node_model), len(node_dp), len(node_target)) < nn or len(cluster_budget) < npb:
+            raise ConfigError(2, "allocate: node/problem arrays shorter than node_offset implies")
+        out = dict(node_budget=np.zeros(nn), total=np.zeros(npb),
+                   all_sat=np.zeros(npb, np.uint8), status=np.zeros(npb, np.int32))
+        check(self.lib.pals_allocate_budget(
+            self.h, quantum_w, npb, ptr(off), ptr(node_model), ptr(node_dp), ptr(node_target),
+            ptr(cluster_budget), ptr(out["node_budget"]), ptr(out["total"]), ptr(out["all_sat"]),
+            ptr(out["status"])))
+        return out
+
+    def run_device(self, quantum_w, n_problems, n_nodes, d_off, d_model, d_dp, d_target,
+                   d_budget, d_node_budget, d_total, d_all_sat, d_status):
+        """Device pointers (ints); async on the context stream."""
+        v = C.c_void_p
+        check(self.lib.pals_alloc_run_device(self.h, quantum_w, n_problems, v(d_off), n_nodes,
+                                             v(d_model), v(d_dp), v(d_target), v(d_budget),
+                                             v(d_node_budget), v(d_total), v(d_all_sat),
+                                             v(d_status)))
+
+
+class AllocResult:
+    """AllocResult (allocator.hpp:24-28)."""
+
+    def __init__(self, node_budgets_w, total_allocated_w, all_targets_satisfied):
+        self.node_budgets_w = list(node_budgets_w)
+        self.total_allocated_w = float(total_allocated_w)
+        self.all_targets_satisfied = bool(all_targets_satisfied)
+
+
+def allocate_budget(allocator: Allocator, nodes, cluster_budget_w: float,
+                    quantum_w: float = 25.0) -> AllocResult:
+    """allocate_budget(nodes, cluster_budget_w, gpu, coeffs, quantum_w, selection_margin)
+    (allocator.hpp:76) for one cluster: nodes = [(model_index, dp, throughput_target_tps)].
+    gpu, coeffs, the candidate axes and the margin are the allocator's. Raises ConfigError
+    with the reference's message when the budget is below the node floors."""
+    nodes = list(nodes)
+    if not nodes:
+        raise ConfigError(2, "allocate_budget: no nodes")
+    m = np.array([n[0] for n in nodes], np.int32)
+    d = np.array([n[1] for n in nodes], np.int32)
+    t = np.array([n[2] for n in nodes], np.float64)
+    out = allocator.allocate([0, len(nodes)], m, d, t, [cluster_budget_w], quantum_w)
+    st = int(out["status"][0])
+    if st != 0:
+        g, k = allocator.gpu, allocator.coeffs
+        unit = k.alpha * 4 * g.min_cap_watts + k.beta_watts
+        floors = [int(x) * unit for x in d]
+        if sum(floors) > cluster_budget_w:  # allocator.hpp:87-95
+            parts = ", ".join(f"{allocator.names[i] if 0 <= i < len(allocator.names) else i}"
+                              f"={f:g} W" for i, f in zip(m, floors))
+            raise ConfigError(st, f"allocate_budget: cluster budget {cluster_budget_w:g} W "
+                                  f"below the sum of node floors ({parts})")
+        cls = {2: ConfigError, 3: DataError, 5: OutOfRange}.get(st, PalsError)
+        raise cls(st, "allocate_budget: a node's scorer rejected its candidates")
+    return AllocResult(out["node_budget"], out["total"][0], out["all_sat"][0])

@@ -162,6 +162,39 @@ def cfg4_setup():
     return dict(profiles=profs, gpu=gpu, coeffs=coeffs, caps=caps, batches=batches, cfg=cfg)
 
 
+def alloc_problems(n_problems: int, seed: int, t_max, p_max, gpu, coeffs, max_nodes: int = 8,
+                   first: int = 0):
+    """Independent allocate_budget problems (allocator.hpp:76): each cluster has 1..max_nodes
+    nodes drawn from the profiles (model m, dp in {1,2,3}), targets U(0.2,1.0) of the node's
+    unconstrained throughput, and a cluster budget between the node floors and 1.15x the
+    sum of the nodes' peak draw (3% of problems fall below the floors: the error path).
+    t_max[m] / p_max[m]: unconstrained throughput and peak p_node of model m at dp = 1."""
+    pi = np.arange(first, first + n_problems, dtype=np.uint64)
+    k = splitmix64(np.uint64(seed) ^ pi)
+    nn = 1 + (k % np.uint64(max_nodes)).astype(np.int64)
+    off = np.zeros(n_problems + 1, np.int64)
+    off[1:] = np.cumsum(nn)
+    tot = int(off[-1])
+    owner = np.repeat(np.arange(n_problems), nn)
+    local = np.arange(tot) - off[owner]
+    kn = splitmix64(k[owner] ^ (np.uint64(0xA5A5) + local.astype(np.uint64)))
+    n_models = len(t_max)
+    model = (kn % np.uint64(n_models)).astype(np.int32)
+    dp = (1 + (splitmix64(kn + np.uint64(1)) % np.uint64(3))).astype(np.int32)
+    u = u01(splitmix64(kn + np.uint64(2)))
+    t_max = np.asarray(t_max, np.float64)
+    p_max = np.asarray(p_max, np.float64)
+    target = (0.2 + 0.8 * u) * t_max[model] * dp
+    floor = dp * (coeffs.alpha * 4.0 * gpu.min_cap_watts + coeffs.beta_watts)
+    floor_sum = np.add.reduceat(floor, off[:-1])
+    peak_sum = np.add.reduceat(p_max[model] * dp, off[:-1])
+    ub = u01(splitmix64(k + np.uint64(3)))
+    budget = floor_sum + ub * (1.15 * peak_sum - floor_sum)
+    below = u01(splitmix64(k + np.uint64(4))) < 0.03
+    budget = np.where(below, 0.9 * floor_sum, budget)
+    return dict(off=off, model=model, dp=dp, target=target, budget=budget)
+
+
 def predict_points(n: int, seed: int = 2605) -> np.ndarray:
     """Random operating points for predictor throughput (continuous caps, any batch)."""
     k = splitmix64(np.uint64(seed) ^ np.arange(n, dtype=np.uint64))

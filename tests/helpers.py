@@ -86,3 +86,99 @@ def run_control_sequences(gold, step_fn, max_seqs=None):
 
 def bits(a):
     return np.ascontiguousarray(a, np.float64).view(np.uint64)
+
+
+# ---- allocate_budget (allocator.hpp) restated in Python for small cases --------------
+def py_steps(T, P, cdp, alpha, beta, margin=0.0):
+    """detail::throughput_steps (allocator.hpp:34-56) + the margin scaling (:106)."""
+    pts = [(float(d) * (alpha * 4 * float(p) + beta), float(d) * float(t))
+           for t, p, d in zip(T, P, cdp)]
+    pts.sort(key=lambda s: (s[0], -s[1]))
+    steps, best = [], 0.0
+    for pw, th in pts:
+        if th > best + 1e-12:
+            steps.append([pw, th])
+            best = th
+    for s in steps:
+        s[0] /= 1.0 - margin
+    return steps
+
+
+def py_allocate(steps, dps, targets, budget, floor_unit, quantum=25.0):
+    """allocate_budget (allocator.hpp:76-186) over precomputed steps; None = config_error."""
+    import math
+    n = len(steps)
+    if n == 0:
+        return None
+    floors = [float(d) * floor_unit for d in dps]
+    ft = 0.0
+    for f in floors:
+        ft += f
+    if ft > budget:
+        return None
+    bud = list(floors)
+    rem = budget - ft
+
+    def under(st, b):
+        best = 0.0
+        for pw, th in st:
+            if pw > b:
+                break
+            best = th
+        return best
+
+    cur = [under(steps[i], bud[i]) for i in range(n)]
+    while rem >= quantum:
+        unmet = any(not (cur[i] >= targets[i]) for i in range(n))
+        br, bc, bi = 0.0, 0.0, n
+        for i in range(n):
+            if unmet and cur[i] >= targets[i]:
+                continue
+            for pw, th in steps[i]:
+                if pw <= bud[i] or th <= cur[i]:
+                    continue
+                cost = math.ceil((pw - bud[i]) / quantum) * quantum
+                if cost > rem:
+                    break
+                gain = (min(th, targets[i]) - min(cur[i], targets[i])) if unmet else th - cur[i]
+                if gain <= 1e-12:
+                    continue
+                rate = gain / cost
+                if bi == n or rate > br + 1e-12 or (rate > br - 1e-12 and bud[i] < bud[bi] - 1e-12):
+                    br, bc, bi = rate, cost, i
+        if bi == n:
+            break
+        bud[bi] += bc
+        cur[bi] = under(steps[bi], bud[bi])
+        rem -= bc
+    ceil_ = [bud[i] if not steps[i] else steps[i][-1][0] + 2.0 * quantum for i in range(n)]
+    while rem >= quantum:
+        lo = n
+        for i in range(n):
+            if bud[i] + quantum > ceil_[i]:
+                continue
+            if lo == n or bud[i] < bud[lo]:
+                lo = i
+        if lo == n:
+            break
+        bud[lo] += quantum
+        rem -= quantum
+    tot = 0.0
+    for b in bud:
+        tot += b
+    return bud, tot, all(cur[i] >= targets[i] for i in range(n))
+
+
+def alloc_setup(oracle):
+    """cfg4's 8 profiles at their deployments with dp = 1: unconstrained throughput and
+    peak node power per model (scales for workloads.alloc_problems)."""
+    from paper_2605_21427_b200 import workloads
+    s = workloads.cfg4_setup()
+    tm, pm = [], []
+    for p in s["profiles"]:
+        pts = workloads.grid_points(s["caps"], s["batches"], [p.deploy_tp], [p.deploy_ep], [1])
+        T, P, _ = oracle.eval(p, s["gpu"], pts)
+        tm.append(float(T.max()))
+        pm.append(float((s["coeffs"].alpha * 4 * P + s["coeffs"].beta_watts).max()))
+    s["t_max"], s["p_max"] = tm, pm
+    return s

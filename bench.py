@@ -434,6 +434,7 @@ def run_ours(args, dist: Dist):
 
     # ---------------- allocate_budget over many clusters ----------------
     allocations = bench_allocations(args, dist, ctx, stream, l2_flush)
+    frontiers = bench_frontiers(args, dist, ctx, stream, l2_flush)
 
     # ---------------- cfg1: single-call latency (the drop-in's synchronous API) ----------------
     from paper_2605_21427_b200.abi import CtrlState, Point, Telemetry
@@ -489,6 +490,7 @@ def run_ours(args, dist: Dist):
             "roofline": dec_roof, "gpu_launches": int(rlaunches)},
         "predictions": predictions,
         "allocations": allocations,
+        "frontiers": frontiers,
         "latency": latency,
         "peaks": {"int_ops_per_s": int_peak, "fp64_flops_per_s": fp64_peak,
                   "hbm_gbs_measured": measured_peaks_json().get("hbm_gbs")},
@@ -497,6 +499,7 @@ def run_ours(args, dist: Dist):
         out["cpu_baseline"], out["decisions"]["cpu_baseline"] = cpu_baselines(args, cfg, tref)
         out["predictions"]["cpu_baseline"] = cpu_predict(args, bundle, args.cpu_seconds)
         out["allocations"]["cpu_baseline"] = cpu_allocate(args, args.cpu_seconds)
+        out["frontiers"]["cpu_baseline"] = cpu_frontier(args.cpu_seconds)
         out["latency"]["cpu_reference_select_config_us"] = cpu_latency(c1, float(th1.max()))
     if dist.rank == 0:
         print(json.dumps(out), flush=True)
@@ -601,6 +604,69 @@ def bench_allocations(args, dist, ctx, stream, l2_flush):
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
         "gpu_launches": int(launches),
     }
+
+
+FRONTIER_WORKLOAD = ("build_frontier over cfg3x: mixtral-8x7b-like, 64 caps x 256 batches x "
+                     "TP{1,2,4,8} x EP{1,4,8} x DP{1,2,3} = 589,824 points scored "
+                     "(cluster_throughput, efficiency) and reduced to the Pareto frontier per step")
+
+
+def bench_frontiers(args, dist, ctx, stream, l2_flush):
+    import torch
+    from paper_2605_21427_b200 import workloads
+    from paper_2605_21427_b200.wattserve import AnalyticModel, Grid, Plan
+    c = workloads.cfg3_extended()
+    n = len(c["points"])
+    plan = Plan(AnalyticModel(ctx, c["profile"], c["gpu"]), Grid(ctx, c["points"]), c["coeffs"])
+    d_idx = torch.empty(n, dtype=torch.int32, device="cuda")
+    d_n = torch.zeros(1, dtype=torch.int64, device="cuda")
+    step = lambda: plan.frontier_device(d_idx.data_ptr(), d_n.data_ptr())  # noqa: E731
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    l0 = ctx.lib.pals_ctx_launch_count(ctx.h)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    for k in range(args.steps):
+        l2_flush()
+        ev[k][0].record(stream)
+        step()
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    launches = ctx.lib.pals_ctx_launch_count(ctx.h) - l0
+    t_max = dist.max(float(np.sum([a.elapsed_time(b) for a, b in ev])))
+    value = dist.sum(float(n)) * args.steps / (t_max * 1e-3)
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        idx = plan.frontier()
+    e2e_t = dist.max(time.perf_counter() - t0)
+    return {"metric": "frontier points/s (evaluate + build_frontier over a dense grid)",
+            "value": value, "unit": "points/s", "ms_per_step": t_max / args.steps,
+            "steps": args.steps, "workload": FRONTIER_WORKLOAD, "points_per_gpu": n,
+            "frontier_size": int(d_n.item()), "gpu_launches": int(launches),
+            "e2e": {"value": dist.sum(float(n)) * args.steps / e2e_t, "unit": "points/s",
+                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8 + 4 * len(idx),
+                    "api": "pals_plan_frontier (C ABI, host index output)"}}
+
+
+def cpu_frontier(seconds):
+    """evaluate + build_frontier through the unmodified reference (sequential by design)."""
+    from paper_2605_21427_b200 import workloads
+    kind, ref = _reference_backend()
+    if kind != "reference":
+        return {"value": None, "unit": "points/s", "cores": 0, "kind": "port",
+                "sample": "reference build absent"}
+    from oracle.oracle import ref_bench_frontier
+    c = workloads.cfg3_extended()
+    t, _ = ref_bench_frontier(ref, c["profile"], c["gpu"], c["coeffs"], c["points"], 1)
+    reps = int(max(1, min(20, seconds / max(t, 1e-3))))
+    t, _ = ref_bench_frontier(ref, c["profile"], c["gpu"], c["coeffs"], c["points"], reps)
+    n = len(c["points"])
+    return {"value": reps * n / t, "unit": "points/s", "cores": 1, "kind": "reference",
+            "sample": f"{reps} x the 589,824-point grid through cluster_throughput + "
+                      f"efficiency + build_frontier (single-threaded, as evaluate_regime), "
+                      f"{t:.1f} s"}
 
 
 def cpu_allocate(args, seconds):
@@ -765,6 +831,7 @@ def run_reference(args, dist: Dist):
     v = float(np.mean([b["value"] for b in vals]))
     dec = cpu_replay(args, per_step)
     alc = cpu_allocate(args, per_step)
+    fro = cpu_frontier(per_step)
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "config evals/s",
            "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
@@ -777,6 +844,11 @@ def run_reference(args, dist: Dist):
                          "unit": "decisions/s", "workload": REPLAY_WORKLOAD,
                          "cpu_baseline": dec,
                          "e2e": {"value": dec["value"], "unit": "decisions/s",
+                                 "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}},
+           "frontiers": {"metric": "frontier points/s", "value": fro["value"],
+                         "unit": "points/s", "workload": FRONTIER_WORKLOAD,
+                         "cpu_baseline": fro,
+                         "e2e": {"value": fro["value"], "unit": "points/s",
                                  "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}},
            "allocations": {"metric": "cluster budget allocations/s", "value": alc["value"],
                            "unit": "allocations/s", "workload": ALLOC_WORKLOAD,

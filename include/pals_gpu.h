@@ -15,6 +15,7 @@
  *   pals_model_table     TableScorer (test fake)                    tests/test_controller.cpp:17-29
  *   pals_model_forest    predictor_scorer(bundle, model_id)         controller.hpp:100-105,
  *                                                                    forest.hpp:227-235
+ *   pals_plan_frontier   build_frontier() / evaluate_regime()       pareto.hpp:31-59,114-135
  *   pals_allocate_budget allocate_budget() over many clusters      allocator.hpp:76-186,
  *                        (assign_budgets' per-node requests)       sim.hpp:313-336
  *
@@ -346,6 +347,19 @@ int pals_replay_device(pals_ctx* ctx, int32_t n_models, pals_model* const* model
                        const int32_t* batches, int32_t n_batches, const pals_ctrl_cfg* cfg,
                        const pals_replay_spec* spec, pals_trace_summary* d_summaries,
                        pals_step_log* d_logs);
+
+/* ---- Pareto frontier (pareto.hpp:31-59) ------------------------------- */
+/* build_frontier over the plan's points scored as FrontierPoint{point,
+ * cluster_throughput, efficiency} (pareto.hpp:127-130; = the plan's t_hat and eff):
+ * n_out frontier point indices, throughput ascending, exact (throughput, efficiency)
+ * ties collapsed onto the lower (cap, batch). idx holds up to grid-size entries.
+ * Prepares the plan first. Host outputs, synchronous. */
+int pals_plan_frontier(pals_plan* p, int32_t* idx, int64_t* n_out);
+/* Same, async on the context stream, device outputs (d_n: one int64). */
+int pals_plan_frontier_device(pals_plan* p, int32_t* d_idx, int64_t* d_n);
+/* build_frontier over explicit FrontierPoints (point, throughput_tps, efficiency_tpj). */
+int pals_frontier_values(pals_ctx* ctx, const pals_point* points, const double* throughput_tps,
+                         const double* efficiency_tpj, int64_t n, int32_t* idx, int64_t* n_out);
 
 /* ---- cluster budget allocator (allocator.hpp:76-186), batched ---------- */
 /* Replaces wattserve::allocate_budget(nodes, cluster_budget_w, gpu, coeffs, quantum_w,

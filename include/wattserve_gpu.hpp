@@ -12,7 +12,9 @@
 //   predictor_scorer  controller.hpp:100-105 (PredictorBundle, forest.hpp:217-251)
 //   table_scorer      the TableScorer test fake, tests/test_controller.cpp:17-29
 // plus batched entry points (SelectPlan, replay) that have no single-call
-// counterpart in the reference.
+// counterpart in the reference. Also allocate_budget (allocator.hpp:76-186) over
+// GpuAllocRequest nodes and build_frontier / evaluate_regime (pareto.hpp:31-59,
+// 114-135).
 //
 // Header-only; include after the reference headers are on the include path and
 // link libpals_gpu.so.
@@ -20,14 +22,17 @@
 
 #include <cstdio>
 #include <memory>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <utility>
 #include <vector>
 
 #include "pals_gpu.h"
+#include "wattserve/allocator.hpp"
 #include "wattserve/controller.hpp"
 #include "wattserve/forest.hpp"
+#include "wattserve/pareto.hpp"
 
 namespace wattserve::gpu {
 
@@ -320,5 +325,142 @@ private:
     pals_grid* grid_ = nullptr;
     pals_plan* plan_ = nullptr;
 };
+
+// AllocRequest (allocator.hpp:13-19) with a device scorer.
+struct GpuAllocRequest {
+    std::string model_id;
+    double throughput_target_tps = 0.0;
+    std::vector<OperatingPoint> candidates;
+    GpuScorer score;
+    int dp = 1;
+};
+
+// allocate_budget (allocator.hpp:76-186): same results bit for bit, same exceptions.
+inline AllocResult allocate_budget(const std::vector<GpuAllocRequest>& nodes,
+                                   double cluster_budget_w, const GpuSpec& gpu,
+                                   const SystemPowerCoeffs& coeffs, double quantum_w = 25.0,
+                                   double selection_margin = 0.0) {
+    if (nodes.empty()) throw config_error("allocate_budget: no nodes");
+    // the floor check and its message are the reference's (allocator.hpp:81-95)
+    std::vector<double> floor_w(nodes.size());
+    double floor_total = 0.0;
+    for (std::size_t i = 0; i < nodes.size(); ++i) {
+        floor_w[i] = nodes[i].dp *
+                     (coeffs.alpha * kGpusPerNode * gpu.min_cap_watts + coeffs.beta_watts);
+        floor_total += floor_w[i];
+    }
+    if (floor_total > cluster_budget_w) {
+        std::ostringstream msg;
+        msg << "allocate_budget: cluster budget " << cluster_budget_w
+            << " W below the sum of node floors (";
+        for (std::size_t i = 0; i < nodes.size(); ++i)
+            msg << (i ? ", " : "") << nodes[i].model_id << "=" << floor_w[i] << " W";
+        msg << ")";
+        throw config_error(msg.str());
+    }
+    // one candidate set per node
+    std::vector<pals_model*> models;
+    std::vector<pals_point> pts;
+    std::vector<int64_t> off{0};
+    for (const auto& n : nodes) {
+        models.push_back(n.score.get());
+        for (const auto& c : n.candidates) pts.push_back(to_c(c));
+        off.push_back(static_cast<int64_t>(pts.size()));
+    }
+    if (pts.empty()) pts.push_back(pals_point{});
+    const pals_gpu_spec g{gpu.idle_watts, gpu.min_cap_watts, gpu.max_cap_watts, gpu.max_frequency};
+    const pals_coeffs k{coeffs.alpha, coeffs.beta_watts};
+    pals_alloc* a = nullptr;
+    check(pals_alloc_create_sets(nodes[0].score.context().get(),
+                                 static_cast<int32_t>(nodes.size()), models.data(), pts.data(),
+                                 off.data(), &g, &k, selection_margin, &a));
+    std::unique_ptr<pals_alloc, int (*)(pals_alloc*)> guard(a, pals_alloc_destroy);
+    const int64_t n = static_cast<int64_t>(nodes.size());
+    std::vector<int64_t> noff{0, n};
+    std::vector<int32_t> set(n), dp(n);
+    std::vector<double> tgt(n);
+    for (int64_t i = 0; i < n; ++i) {
+        set[i] = static_cast<int32_t>(i);
+        dp[i] = nodes[i].dp;
+        tgt[i] = nodes[i].throughput_target_tps;
+    }
+    AllocResult res;
+    res.node_budgets_w.assign(n, 0.0);
+    uint8_t sat = 0;
+    int32_t status = 0;
+    check(pals_allocate_budget(a, quantum_w, 1, noff.data(), set.data(), dp.data(), tgt.data(),
+                               &cluster_budget_w, res.node_budgets_w.data(),
+                               &res.total_allocated_w, &sat, &status));
+    if (status != PALS_OK) {
+        // the first node whose scorer rejects its candidates: rethrow its error
+        for (int32_t i = 0; i < n; ++i) {
+            int32_t ns = 0;
+            check(pals_alloc_steps(a, i, nullptr, nullptr, &ns));
+        }
+        check(status);
+    }
+    res.all_targets_satisfied = sat != 0;
+    return res;
+}
+
+// build_frontier (pareto.hpp:31-59) on the device.
+inline std::vector<FrontierPoint> build_frontier(Context& ctx,
+                                                 const std::vector<FrontierPoint>& points) {
+    if (points.empty()) throw config_error("build_frontier: no points");
+    std::vector<pals_point> pts;
+    std::vector<double> thr, eff;
+    for (const auto& p : points) {
+        pts.push_back(to_c(p.point));
+        thr.push_back(p.throughput_tps);
+        eff.push_back(p.efficiency_tpj);
+    }
+    std::vector<int32_t> idx(points.size());
+    int64_t nf = 0;
+    check(pals_frontier_values(ctx.get(), pts.data(), thr.data(), eff.data(),
+                               static_cast<int64_t>(pts.size()), idx.data(), &nf));
+    std::vector<FrontierPoint> out;
+    for (int64_t i = 0; i < nf; ++i) out.push_back(points[static_cast<std::size_t>(idx[i])]);
+    return out;
+}
+
+// evaluate_regime (pareto.hpp:114-135): analytic scores and the frontier on the device.
+inline std::vector<FrontierPoint> evaluate_regime(
+    Context& ctx, const RegimeSpec& regime, const ModelProfile& profile, const GpuSpec& gpu,
+    const SystemPowerCoeffs& coeffs, const std::vector<double>& cap_grid,
+    const std::vector<int>& batch_grid, const std::vector<int>& tp_grid) {
+    const std::vector<double> caps =
+        regime.sweep_cap ? cap_grid : std::vector<double>{regime.fixed_cap_w};
+    const std::vector<int> batches =
+        regime.sweep_batch ? batch_grid : std::vector<int>{regime.fixed_batch};
+    const std::vector<int> tps = regime.sweep_tp ? tp_grid : std::vector<int>{profile.deployment.tp};
+    std::vector<OperatingPoint> cands;
+    for (double cap : caps)
+        for (int batch : batches)
+            for (int tp : tps) {
+                if (!profile.comm_fixed_by_tp.count(tp)) continue;
+                cands.push_back(OperatingPoint{cap, batch, tp, profile.deployment.ep, 1});
+            }
+    if (cands.empty()) throw config_error("build_frontier: no points");
+    const GpuScorer sc = analytic_scorer(ctx, profile, gpu);
+    const auto pts = to_c(cands);
+    pals_grid* grid = nullptr;
+    check(pals_grid_points(ctx.get(), pts.data(), static_cast<int64_t>(pts.size()), &grid));
+    std::unique_ptr<pals_grid, int (*)(pals_grid*)> gguard(grid, pals_grid_destroy);
+    const pals_coeffs k{coeffs.alpha, coeffs.beta_watts};
+    pals_plan* plan = nullptr;
+    check(pals_plan_create(ctx.get(), sc.get(), grid, &k, &plan));
+    std::unique_ptr<pals_plan, int (*)(pals_plan*)> pguard(plan, pals_plan_destroy);
+    std::vector<int32_t> idx(cands.size());
+    int64_t nf = 0;
+    check(pals_plan_frontier(plan, idx.data(), &nf));
+    std::vector<double> th(cands.size()), pn(cands.size()), ef(cands.size());
+    check(pals_plan_scores(plan, th.data(), pn.data(), ef.data()));
+    std::vector<FrontierPoint> out;
+    for (int64_t i = 0; i < nf; ++i) {
+        const auto j = static_cast<std::size_t>(idx[i]);
+        out.push_back(FrontierPoint{cands[j], th[j], ef[j]});
+    }
+    return out;
+}
 
 }  // namespace wattserve::gpu

@@ -394,3 +394,81 @@ def ref_bench_predict(ref: Reference, path: str, model_id: str, pts, threads: in
     L.ref_bench_predict.argtypes = [C.c_char_p, C.c_char_p, _VP, C.c_int64, C.c_int]
     pts = np.ascontiguousarray(pts, dtype=POINT_DT)
     return L.ref_bench_predict(path.encode(), model_id.encode(), ptr(pts), len(pts), threads)
+
+
+# ---- Pareto frontier (pareto.hpp) -------------------------------------------------
+def oracle_build_frontier(orc: Oracle, pts, thr, eff) -> np.ndarray:
+    """build_frontier restated in C: frontier indices into pts, throughput ascending."""
+    L = orc.lib
+    L.or_build_frontier.argtypes = [_VP, _VP, _VP, C.c_int64, _VP, _VP]
+    pts = np.ascontiguousarray(pts, dtype=POINT_DT)
+    thr = np.ascontiguousarray(thr, np.float64)
+    eff = np.ascontiguousarray(eff, np.float64)
+    out = np.empty(max(1, len(pts)), np.int64)
+    n = C.c_int64(0)
+    rc = L.or_build_frontier(ptr(pts), ptr(thr), ptr(eff), len(pts), ptr(out), C.byref(n))
+    if rc:
+        raise RuntimeError(f"or_build_frontier rc={rc}")
+    return out[: n.value].copy()
+
+
+def _frontier_out(n):
+    return (np.zeros(max(1, n), POINT_DT), np.empty(max(1, n)), np.empty(max(1, n)))
+
+
+def ref_build_frontier(ref: Reference, pts, thr, eff):
+    """The reference's build_frontier: (points, throughput, efficiency) of the frontier."""
+    L = ref.lib
+    L.ref_build_frontier.argtypes = [_VP, _VP, _VP, C.c_int64, _VP, _VP, _VP, _VP]
+    pts = np.ascontiguousarray(pts, dtype=POINT_DT)
+    thr = np.ascontiguousarray(thr, np.float64)
+    eff = np.ascontiguousarray(eff, np.float64)
+    op, ot, oe = _frontier_out(len(pts))
+    n = C.c_int64(0)
+    rc = L.ref_build_frontier(ptr(pts), ptr(thr), ptr(eff), len(pts), ptr(op), ptr(ot), ptr(oe),
+                              C.byref(n))
+    if rc:
+        raise RuntimeError(f"ref_build_frontier rc={rc}: {ref.last_error()}")
+    k = n.value
+    return op[:k].copy(), ot[:k].copy(), oe[:k].copy()
+
+
+def ref_evaluate_regime(ref: Reference, regime: str, prof, gpu, coeffs, caps, batches, tps):
+    L = ref.lib
+    L.ref_evaluate_regime.argtypes = [C.c_char_p, _VP, _VP, _VP, _VP, C.c_int, _VP, C.c_int, _VP,
+                                      C.c_int, _VP, _VP, _VP, _VP]
+    caps = np.ascontiguousarray(caps, np.float64)
+    batches = np.ascontiguousarray(batches, np.int32)
+    tps = np.ascontiguousarray(tps, np.int32)
+    op, ot, oe = _frontier_out(len(caps) * len(batches) * len(tps) + 1)
+    n = C.c_int64(0)
+    rc = L.ref_evaluate_regime(regime.encode(), C.byref(prof), C.byref(gpu), C.byref(coeffs),
+                               ptr(caps), len(caps), ptr(batches), len(batches), ptr(tps),
+                               len(tps), ptr(op), ptr(ot), ptr(oe), C.byref(n))
+    if rc:
+        raise RuntimeError(f"ref_evaluate_regime rc={rc}: {ref.last_error()}")
+    k = n.value
+    return op[:k].copy(), ot[:k].copy(), oe[:k].copy()
+
+
+def ref_verify_dominance(ref: Reference, a_thr, a_eff, b_thr, b_eff):
+    L = ref.lib
+    L.ref_verify_dominance.argtypes = [_VP, _VP, C.c_int64, _VP, _VP, C.c_int64, _VP, _VP]
+    a_thr, a_eff, b_thr, b_eff = (np.ascontiguousarray(x, np.float64)
+                                  for x in (a_thr, a_eff, b_thr, b_eff))
+    cov = np.zeros(max(1, len(b_thr)), np.uint8)
+    dom = C.c_int(0)
+    L.ref_verify_dominance(ptr(a_thr), ptr(a_eff), len(a_thr), ptr(b_thr), ptr(b_eff),
+                           len(b_thr), ptr(cov), C.byref(dom))
+    return bool(dom.value), cov[: len(b_thr)].astype(bool)
+
+
+def ref_bench_frontier(ref: Reference, prof, gpu, coeffs, pts, reps: int = 1):
+    L = ref.lib
+    L.ref_bench_frontier.restype = C.c_double
+    L.ref_bench_frontier.argtypes = [_VP, _VP, _VP, _VP, C.c_int64, C.c_int, _VP]
+    pts = np.ascontiguousarray(pts, dtype=POINT_DT)
+    n = C.c_int64(0)
+    t = L.ref_bench_frontier(C.byref(prof), C.byref(gpu), C.byref(coeffs), ptr(pts), len(pts),
+                             reps, C.byref(n))
+    return t, n.value

@@ -642,3 +642,59 @@ int or_allocate(int n_models, const pals_profile* profs, const pals_gpu_spec* g,
     }
     return PALS_OK;
 }
+
+/* ---- Pareto frontier (pareto.hpp) ---------------------------------------- */
+typedef struct {
+    double thr, eff, cap;
+    int batch;
+    int64_t idx;
+} fr_item;
+
+/* build_frontier's sort: throughput, efficiency, cap, batch ascending (pareto.hpp:35-40);
+ * full ties (equal on all four) are left unspecified by std::sort; input order here. */
+static int fr_cmp(const void* a, const void* b) {
+    const fr_item* x = (const fr_item*)a;
+    const fr_item* y = (const fr_item*)b;
+    if (x->thr != y->thr) return x->thr < y->thr ? -1 : 1;
+    if (x->eff != y->eff) return x->eff < y->eff ? -1 : 1;
+    if (x->cap != y->cap) return x->cap < y->cap ? -1 : 1;
+    if (x->batch != y->batch) return x->batch < y->batch ? -1 : 1;
+    return x->idx < y->idx ? -1 : (x->idx > y->idx);
+}
+
+/* build_frontier pareto.hpp:31-59: indices of the frontier points, throughput ascending */
+int or_build_frontier(const pals_point* pts, const double* thr, const double* eff, int64_t n,
+                      int64_t* out_idx, int64_t* out_n) {
+    if (n <= 0) return PALS_ECONFIG; /* "build_frontier: no points" */
+    fr_item* v = (fr_item*)malloc(sizeof(fr_item) * (size_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+        v[i].thr = thr[i];
+        v[i].eff = eff[i];
+        v[i].cap = pts[i].cap_watts;
+        v[i].batch = pts[i].batch;
+        v[i].idx = i;
+    }
+    qsort(v, (size_t)n, sizeof(fr_item), fr_cmp);
+    /* collapse exact (throughput, efficiency) ties onto the first (lower cap) point */
+    int64_t m = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        if (m > 0 && v[m - 1].thr == v[i].thr && v[m - 1].eff == v[i].eff) continue;
+        v[m++] = v[i];
+    }
+    /* sweep from the high-throughput end (pareto.hpp:50-57) */
+    double best = -1.0;
+    int64_t k = 0;
+    for (int64_t i = m - 1; i >= 0; --i)
+        if (v[i].eff > best) {
+            out_idx[k++] = v[i].idx;
+            best = v[i].eff;
+        }
+    for (int64_t i = 0; i < k / 2; ++i) { /* std::reverse */
+        const int64_t t = out_idx[i];
+        out_idx[i] = out_idx[k - 1 - i];
+        out_idx[k - 1 - i] = t;
+    }
+    *out_n = k;
+    free(v);
+    return PALS_OK;
+}

@@ -19,6 +19,7 @@
 #include "wattserve/controller.hpp"
 #include "wattserve/forest.hpp"
 #include "wattserve/model.hpp"
+#include "wattserve/pareto.hpp"
 #include "wattserve/rng.hpp"
 #include "wattserve/sim.hpp"
 #include "wattserve/sweep.hpp"
@@ -842,6 +843,89 @@ double ref_bench_predict(const char* path, const char* model_id, const pals_poin
     const auto t2 = std::chrono::steady_clock::now();
     if (failed) return -1.0;
     return std::chrono::duration<double>(t2 - t1).count();
+}
+
+// ---- Pareto frontier (pareto.hpp) ------------------------------------------
+static void put_frontier(const std::vector<FrontierPoint>& f, pals_point* out_pts,
+                         double* out_thr, double* out_eff, std::int64_t* out_n) {
+    *out_n = (std::int64_t)f.size();
+    for (std::size_t i = 0; i < f.size(); ++i) {
+        out_pts[i] = from_point(f[i].point);
+        out_thr[i] = f[i].throughput_tps;
+        out_eff[i] = f[i].efficiency_tpj;
+    }
+}
+
+// build_frontier (pareto.hpp:31-59) over explicit FrontierPoints
+int ref_build_frontier(const pals_point* pts, const double* thr, const double* eff,
+                       std::int64_t n, pals_point* out_pts, double* out_thr, double* out_eff,
+                       std::int64_t* out_n) {
+    try {
+        std::vector<FrontierPoint> v;
+        v.reserve((std::size_t)n);
+        for (std::int64_t i = 0; i < n; ++i)
+            v.push_back(FrontierPoint{to_point(pts[i]), thr[i], eff[i]});
+        put_frontier(build_frontier(std::move(v)), out_pts, out_thr, out_eff, out_n);
+        return PALS_OK;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// evaluate_regime (pareto.hpp:114-135) with a named preset (regime_by_name)
+int ref_evaluate_regime(const char* regime, const pals_profile* prof, const pals_gpu_spec* gpu,
+                        const pals_coeffs* k, const double* caps, int nc, const int* batches,
+                        int nb, const int* tps, int nt, pals_point* out_pts, double* out_thr,
+                        double* out_eff, std::int64_t* out_n) {
+    try {
+        const auto f = evaluate_regime(
+            regime_by_name(regime), to_profile(*prof), to_gpu(*gpu),
+            SystemPowerCoeffs{k->alpha, k->beta_watts}, std::vector<double>(caps, caps + nc),
+            std::vector<int>(batches, batches + nb), std::vector<int>(tps, tps + nt));
+        put_frontier(f, out_pts, out_thr, out_eff, out_n);
+        return PALS_OK;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// verify_dominance (pareto.hpp:66-83): covered[j] = some point of a weakly dominates b[j]
+int ref_verify_dominance(const double* a_thr, const double* a_eff, std::int64_t na,
+                         const double* b_thr, const double* b_eff, std::int64_t nb,
+                         std::uint8_t* covered, int* dominated) {
+    std::vector<FrontierPoint> a, b;
+    for (std::int64_t i = 0; i < na; ++i) a.push_back(FrontierPoint{{}, a_thr[i], a_eff[i]});
+    for (std::int64_t i = 0; i < nb; ++i) b.push_back(FrontierPoint{{}, b_thr[i], b_eff[i]});
+    const auto rep = verify_dominance(a, b);
+    *dominated = rep.dominated ? 1 : 0;
+    std::size_t w = 0;
+    for (std::int64_t j = 0; j < nb; ++j) {
+        const bool wit = w < rep.witnesses.size() && rep.witnesses[w].throughput_tps == b_thr[j] &&
+                         rep.witnesses[w].efficiency_tpj == b_eff[j];
+        covered[j] = wit ? 0 : 1;
+        if (wit) ++w;
+    }
+    return PALS_OK;
+}
+
+// The reference's frontier of one dense grid: score every point (cluster_throughput,
+// efficiency) then build_frontier, as evaluate_regime does; seconds for `reps` runs.
+double ref_bench_frontier(const pals_profile* prof, const pals_gpu_spec* gpu, const pals_coeffs* k,
+                          const pals_point* pts, std::int64_t n, int reps, std::int64_t* out_n) {
+    const ModelProfile mp = to_profile(*prof);
+    const GpuSpec g = to_gpu(*gpu);
+    const SystemPowerCoeffs kc{k->alpha, k->beta_watts};
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int r = 0; r < reps; ++r) {
+        std::vector<FrontierPoint> v;
+        v.reserve((std::size_t)n);
+        for (std::int64_t i = 0; i < n; ++i) {
+            const OperatingPoint p = to_point(pts[i]);
+            v.push_back(FrontierPoint{p, cluster_throughput(p, mp, g), efficiency(p, mp, g, kc)});
+        }
+        *out_n = (std::int64_t)build_frontier(std::move(v)).size();
+    }
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
 }  // extern "C"

@@ -65,6 +65,9 @@ SIGNATURES = [
                          _VP]),
     ("pals_replay_device", _I, [_VP, _I32, _VP, _VP, _VP, _VP, _VP, _I32, _VP, _I32, _VP, _VP,
                                 _VP, _VP]),
+    ("pals_plan_frontier", _I, [_VP, _VP, _VP]),
+    ("pals_plan_frontier_device", _I, [_VP, _VP, _VP]),
+    ("pals_frontier_values", _I, [_VP, _VP, _VP, _VP, _I64, _VP, _VP]),
     ("pals_alloc_create", _I, [_VP, _I32, _VP, _VP, _VP, _VP, _VP, _I32, _VP, _I32, _I32, _D,
                                _VP]),
     ("pals_alloc_destroy", _I, [_VP]),

@@ -117,6 +117,7 @@ int pals_ctx_destroy(pals_ctx* c) {
     cudaSetDevice(c->device);
     replay_cache_free(c);
     if (c->d_scratch) cudaFree(c->d_scratch);
+    if (c->d_front) cudaFree(c->d_front);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;

@@ -173,6 +173,8 @@ struct pals_ctx {
     void* h_pinned = nullptr;
     size_t pinned_bytes = 0;
     void* replay_cache = nullptr;  // replay.cu
+    void* d_front = nullptr;       // frontier.cu scratch
+    size_t front_bytes = 0;
 };
 
 enum ModelKind { MODEL_ANALYTIC = 0, MODEL_TABLE = 1, MODEL_FOREST = 2 };
@@ -232,5 +234,9 @@ int forest_eval_raw(const pals_model* m, pals_ctx* ctx, int64_t n, const double*
                     double* P, int force_direct);
 // plan.cu
 const pals_grid* plan_grid(const pals_plan* p);
+pals_ctx* plan_ctx(const pals_plan* p);
+// a plan over given (throughput, efficiency) values per grid point (T / P arrays of
+// the plan are filled by the caller before pals_plan_prepare); frontier only
+int plan_create_values(pals_ctx* ctx, const pals_grid* g, pals_plan** out);
 int plan_finish_scores(pals_plan* p);
 }  // namespace pals

@@ -52,6 +52,7 @@ struct pals_plan {
     int nchunks = 0;
     int chunk = 4096;  // sort chunk size (keys per CTA)
     int force_exact = 0;
+    int values = 0;               // internal: th / ef supplied directly (frontier.cu)
     int64_t last_exact = 0;
     PlanDev d{};
     int* tr = nullptr;            // device TR per point
@@ -127,6 +128,21 @@ __global__ void k_eval_table(PlanDev d, const int* __restrict__ map, const doubl
          i += (int64_t)gridDim.x * blockDim.x) {
         const int r = map[i];
         finish_scores(d, i, tT[r], tP[r], d.dp[i], alpha, beta);
+    }
+}
+
+// Values plans (frontier.cu): T holds the throughput, P the efficiency of each
+// point as given (FrontierPoint); only the t_hat and eff orders are meaningful.
+__global__ void k_eval_values(PlanDev d) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double th = d.T[i], ef = d.P[i];
+        d.th[i] = th;
+        d.pn[i] = 1.0;
+        d.ef[i] = ef;
+        d.skey[ORD_T][i] = ~orderable(th);
+        d.skey[ORD_P][i] = orderable(1.0);
+        d.skey[ORD_E][i] = ~orderable(ef);
     }
 }
 
@@ -908,9 +924,29 @@ __global__ void k_eval_analytic_raw(const Analytic* __restrict__ an, int64_t n,
 
 extern "C" {
 
+static int plan_build(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
+                      const pals_coeffs* coeffs, pals_plan** out);
+
 int pals_plan_create(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
                      const pals_coeffs* coeffs, pals_plan** out) {
     if (!ctx || !m || !g || !coeffs) return set_error(PALS_ECONFIG, "pals_plan_create: null");
+    return plan_build(ctx, m, g, coeffs, out);
+}
+
+}  // extern "C"
+
+namespace pals {
+int plan_create_values(pals_ctx* ctx, const pals_grid* g, pals_plan** out) {
+    const pals_coeffs unit{1.0, 0.0};
+    const int rc = plan_build(ctx, nullptr, g, &unit, out);
+    if (rc == PALS_OK) (*out)->values = 1;
+    return rc;
+}
+pals_ctx* plan_ctx(const pals_plan* p) { return p->ctx; }
+}  // namespace pals
+
+static int plan_build(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
+                      const pals_coeffs* coeffs, pals_plan** out) {
     PALS_CUDA(cudaSetDevice(ctx->device));
     auto* p = new pals_plan();
     p->ctx = ctx;
@@ -923,7 +959,7 @@ int pals_plan_create(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
     if (g->n == 0) {
         p->err = PALS_ECONFIG;
         p->err_msg = "select_config: empty candidate list";
-    } else if (validate_points(m, g->h_pts, g->n) != PALS_OK) {
+    } else if (m && validate_points(m, g->h_pts, g->n) != PALS_OK) {
         p->err = validate_points(m, g->h_pts, g->n);
         p->err_msg = pals_last_error();
     }
@@ -949,7 +985,7 @@ int pals_plan_create(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
     const size_t n8 = (size_t)n * 8, np8 = (size_t)p->np * 8, np4 = (size_t)p->np * 4;
     size_t bytes = 5 * n8 + N_ORD * (3 * np8 + np4 + n8 + (size_t)n * 4) + 64 + 4 * (size_t)n +
                    (d.wide ? N_ORD * n8 : N_ORD * (size_t)n * 4) + 4096;
-    if (m->kind == MODEL_TABLE) bytes += 4 * (size_t)n + 2 * 8 * (size_t)std::max<int64_t>(1, m->table_n);
+    if (m && m->kind == MODEL_TABLE) bytes += 4 * (size_t)n + 2 * 8 * (size_t)std::max<int64_t>(1, m->table_n);
     bytes += sizeof(Analytic) + 256;
     bytes += 64 * 256;  // every take() rounds up to 256 B
     PALS_CUDA(cudaMalloc(&p->slab, bytes));
@@ -987,9 +1023,9 @@ int pals_plan_create(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
             PALS_CUDA(cudaMemcpy(p->tr, tr.data(), g->n * sizeof(int), cudaMemcpyHostToDevice));
         }
     }
-    if (m->kind == MODEL_ANALYTIC)
+    if (m && m->kind == MODEL_ANALYTIC)
         PALS_CUDA(cudaMemcpy(p->d_an, &m->an, sizeof(Analytic), cudaMemcpyHostToDevice));
-    if (m->kind == MODEL_TABLE) {
+    if (m && m->kind == MODEL_TABLE) {
         p->table_map = (int*)take(4 * (size_t)n);
         const int64_t tn = std::max<int64_t>(1, m->table_n);
         p->table_T = (double*)take(8 * (size_t)tn);
@@ -1019,6 +1055,8 @@ int pals_plan_create(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
     return PALS_OK;
 }
 
+extern "C" {
+
 int pals_plan_destroy(pals_plan* p) {
     if (!p) return PALS_OK;
     cudaSetDevice(p->ctx->device);
@@ -1042,7 +1080,9 @@ static int prep_head(pals_plan* p) {
     (void)cudaGetLastError();  // clear stale non-sticky errors of earlier calls
     PALS_CUDA(cudaMemsetAsync(d.globals, 0, 16, s));  // generic flag, set by the eval
     const int eb = grid_blocks(ctx, n, 256);
-    if (p->model->kind == MODEL_ANALYTIC) {
+    if (p->values) {
+        k_eval_values<<<eb, 256, 0, s>>>(d);
+    } else if (p->model->kind == MODEL_ANALYTIC) {
         k_eval_analytic<<<eb, 256, 0, s>>>(d, p->d_an, p->grid->tp, p->coeffs.alpha,
                                            p->coeffs.beta_watts);
     } else if (p->model->kind == MODEL_TABLE) {

@@ -195,6 +195,17 @@ class Plan:
         check(self.ctx.lib.pals_plan_select_device(self.h, C.c_void_p(d_queries), n,
                                                    C.c_void_p(d_idx), C.c_void_p(d_reason)))
 
+    def frontier(self) -> np.ndarray:
+        """build_frontier over the plan's (t_hat, eff): point indices, throughput ascending."""
+        idx = np.empty(max(1, len(self.grid)), np.int32)
+        n = C.c_int64(0)
+        check(self.ctx.lib.pals_plan_frontier(self.h, ptr(idx), C.byref(n)))
+        return idx[: n.value].copy()
+
+    def frontier_device(self, d_idx: int, d_n: int):
+        """Async: frontier indices into d_idx (grid-size capacity), count into d_n (int64)."""
+        check(self.ctx.lib.pals_plan_frontier_device(self.h, C.c_void_p(d_idx), C.c_void_p(d_n)))
+
     def run(self, d_queries: int, n: int, d_idx: int, d_reason: int):
         """One full step (evaluate + rank + select) from a cached CUDA graph; async."""
         check(self.ctx.lib.pals_plan_run(self.h, C.c_void_p(d_queries), n, C.c_void_p(d_idx),

@@ -15,8 +15,10 @@
 #include <string>
 #include <vector>
 
+#include "wattserve/allocator.hpp"
 #include "wattserve/controller.hpp"
 #include "wattserve/forest.hpp"
+#include "wattserve/pareto.hpp"
 #include "wattserve/json_io.hpp"
 #include "wattserve/rng.hpp"
 #include "wattserve/sweep.hpp"
@@ -280,6 +282,140 @@ int main(int argc, char** argv) {
                 sg = sg2;
             }
         }
+    }
+
+    // ---- allocate_budget (allocator.hpp; tests/test_controller.cpp:237-283) ----
+    {
+        auto same_alloc = [](const AllocResult& a, const AllocResult& b) {
+            if (a.node_budgets_w.size() != b.node_budgets_w.size()) return false;
+            for (std::size_t i = 0; i < a.node_budgets_w.size(); ++i)
+                if (!same_bits(a.node_budgets_w[i], b.node_budgets_w[i])) return false;
+            return same_bits(a.total_allocated_w, b.total_allocated_w) &&
+                   a.all_targets_satisfied == b.all_targets_satisfied;
+        };
+        GpuSpec g0;
+        const Table t8 = ladder(8, 400.0, 1200.0), t120 = ladder(120, 400.0, 2000.0),
+                    t4 = ladder(4, 400.0, 1000.0);
+        auto mk = [&](const Table& t, const std::string& id, double target) {
+            AllocRequest r;
+            r.model_id = id;
+            r.throughput_target_tps = target;
+            r.candidates = t.points;
+            r.score = t.cpu();
+            return r;
+        };
+        auto mkg = [&](const Table& t, const std::string& id, double target) {
+            return gpu::GpuAllocRequest{id, target, t.points,
+                                        gpu::table_scorer(ctx, t.points, t.t_hat, t.p_gpu), 1};
+        };
+        const double max_useful = k.alpha * kGpusPerNode * t8.p_gpu.back() + k.beta_watts;
+        EXPECT(same_alloc(allocate_budget({mk(t8, "m", 3000.0)}, max_useful + 500.0, g0, k, 25.0),
+                          gpu::allocate_budget({mkg(t8, "m", 3000.0)}, max_useful + 500.0, g0, k,
+                                               25.0)),
+               "one node takes the budget");
+        EXPECT(same_alloc(allocate_budget({mk(t120, "a", 1800.0), mk(t120, "b", 1800.0)}, 3000.0,
+                                          g0, k, 25.0),
+                          gpu::allocate_budget({mkg(t120, "a", 1800.0), mkg(t120, "b", 1800.0)},
+                                               3000.0, g0, k, 25.0)),
+               "identical nodes split evenly");
+        std::string want, got;
+        try {
+            allocate_budget({mk(t4, "starved", 0.0), mk(t4, "starved", 0.0),
+                             mk(t4, "starved", 0.0)}, 100.0, g0, k);
+        } catch (const config_error& e) {
+            want = e.what();
+        }
+        try {
+            gpu::allocate_budget({mkg(t4, "starved", 0.0), mkg(t4, "starved", 0.0),
+                                  mkg(t4, "starved", 0.0)}, 100.0, g0, k);
+        } catch (const config_error& e) {
+            got = e.what();
+        }
+        EXPECT(!want.empty() && want == got, "infeasible floor: same config_error message");
+        // random clusters over the analytic profiles (the sim's assign_budgets shape)
+        Rng rng(31);
+        const std::vector<double> caps{150, 200, 250, 300, 350, 400};
+        const std::vector<int> bats{1, 4, 8, 16, 32, 64};
+        for (int trial = 0; trial < 200; ++trial) {
+            const int nn = 1 + static_cast<int>(rng.next_u64() % 6);
+            std::vector<AllocRequest> rq;
+            std::vector<gpu::GpuAllocRequest> gq;
+            double peak = 0.0;
+            for (int i = 0; i < nn; ++i) {
+                const ModelProfile& prof = profiles[rng.next_u64() % profiles.size()];
+                const int dp = 1 + static_cast<int>(rng.next_u64() % 3);
+                std::vector<OperatingPoint> cands;
+                for (double c : caps)
+                    for (int b : bats)
+                        cands.push_back(OperatingPoint{c, b, prof.deployment.tp,
+                                                       prof.deployment.ep, dp});
+                const double tmax = cluster_throughput(cands.back(), prof, gspec);
+                peak += cluster_system_power(cands.back(), prof, gspec, k);
+                const double target = rng.uniform(0.2, 1.0) * tmax;
+                AllocRequest r;
+                r.model_id = prof.name;
+                r.throughput_target_tps = target;
+                r.candidates = cands;
+                r.score = analytic_scorer(prof, gspec);
+                r.dp = dp;
+                rq.push_back(r);
+                gq.push_back(gpu::GpuAllocRequest{prof.name, target, cands,
+                                                  gpu::analytic_scorer(ctx, prof, gspec), dp});
+            }
+            const double budget = rng.uniform(0.5, 1.2) * peak;
+            const double margin = trial % 2 ? 0.02 : 0.0;
+            std::string ew, eg;
+            AllocResult ra, ga;
+            try {
+                ra = allocate_budget(rq, budget, gspec, k, 25.0, margin);
+            } catch (const std::exception& e) {
+                ew = e.what();
+            }
+            try {
+                ga = gpu::allocate_budget(gq, budget, gspec, k, 25.0, margin);
+            } catch (const std::exception& e) {
+                eg = e.what();
+            }
+            EXPECT(ew == eg && (!ew.empty() || same_alloc(ra, ga)), "random cluster allocation");
+        }
+    }
+
+    // ---- Pareto frontier (pareto.hpp; tests/test_analysis.cpp:26-118) ----
+    {
+        auto same_front = [](const std::vector<FrontierPoint>& a,
+                             const std::vector<FrontierPoint>& b) {
+            if (a.size() != b.size()) return false;
+            for (std::size_t i = 0; i < a.size(); ++i)
+                if (!(a[i].point == b[i].point) || !same_bits(a[i].throughput_tps, b[i].throughput_tps) ||
+                    !same_bits(a[i].efficiency_tpj, b[i].efficiency_tpj))
+                    return false;
+            return true;
+        };
+        const std::vector<double> caps{150, 200, 250, 300, 350, 400};
+        const std::vector<int> bats{1, 4, 8, 16, 32, 64};
+        const std::vector<int> tps{1, 2, 4};
+        for (const auto& prof : profiles)
+            for (const auto& reg : default_regimes())
+                EXPECT(same_front(evaluate_regime(reg, prof, gspec, k, caps, bats, tps),
+                                  gpu::evaluate_regime(ctx, reg, prof, gspec, k, caps, bats, tps)),
+                       "evaluate_regime");
+        Rng rng(99);
+        for (int trial = 0; trial < 200; ++trial) {
+            std::vector<FrontierPoint> pts;
+            const int n = 2 + static_cast<int>(rng.next_u64() % 40);
+            for (int i = 0; i < n; ++i)
+                pts.push_back(FrontierPoint{OperatingPoint{150.0 + 50.0 * (i % 6), 8, 2, 1, 1},
+                                            rng.uniform(10.0, 1000.0), rng.uniform(0.1, 2.0)});
+            EXPECT(same_front(build_frontier(pts), gpu::build_frontier(ctx, pts)),
+                   "build_frontier random");
+        }
+        bool threw = false;
+        try {
+            gpu::build_frontier(ctx, {});
+        } catch (const config_error&) {
+            threw = true;
+        }
+        EXPECT(threw, "build_frontier: no points");
     }
 
     std::printf("%s: %d checks, %d failures\n", g_fail ? "FAIL" : "PASS", g_checks, g_fail);

@@ -24,6 +24,23 @@ constexpr int kMaxDp = 256;              // pow(internode, dp-1) host table size
 constexpr uint32_t kNone32 = 0xFFFFFFFFu;
 constexpr uint64_t kNone64 = ~0ull;
 
+// ---- programmatic dependent launch (PDL) ------------------------------------
+// Kernels of the select step start with pdl_wait(); pdl_trigger(): a kernel
+// launched with the PDL attribute may be scheduled while its predecessor still
+// runs, and blocks in pdl_wait() until the predecessor has completed and its
+// writes are visible, so the ordering is that of a plain stream. Without the
+// attribute both are no-ops.
+__device__ __forceinline__ void pdl_wait() {
+#ifdef __CUDA_ARCH__
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_trigger() {
+#ifdef __CUDA_ARCH__
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
 // ---- libstdc++ comparison helpers (stl_algobase.h:257-265, stl_algo.h:3667-3671)
 PALS_HD double smax(double a, double b) { return a < b ? b : a; }
 PALS_HD double smin(double a, double b) { return b < a ? b : a; }
@@ -157,6 +174,25 @@ struct PlanDev {
     int32_t* globals;        // [0] argmax t over all, [1] argmin p over all, [2] generic flag,
                              // [3] number of exact folds last select
 };
+
+#ifdef __CUDACC__
+// kernel<<<g, b, smem, s>>>(args...) with the PDL attribute when pdl is set
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t s,
+                            bool pdl, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = g;
+    cfg.blockDim = b;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+#endif
 
 }  // namespace pals
 

@@ -53,6 +53,7 @@ struct pals_plan {
     int chunk = 4096;  // sort chunk size (keys per CTA)
     int force_exact = 0;
     int values = 0;               // internal: th / ef supplied directly (frontier.cu)
+    int pdl = 1;                  // programmatic dependent launch between step kernels
     int64_t last_exact = 0;
     PlanDev d{};
     int* tr = nullptr;            // device TR per point
@@ -114,6 +115,7 @@ __device__ __forceinline__ void finish_scores(const PlanDev& d, int64_t i, doubl
 
 __global__ void k_eval_analytic(PlanDev d, const Analytic* __restrict__ an,
                                 const int* __restrict__ tp, double alpha, double beta) {
+    pdl_wait();
     const Analytic& a = *an;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -124,6 +126,7 @@ __global__ void k_eval_analytic(PlanDev d, const Analytic* __restrict__ an,
 
 __global__ void k_eval_table(PlanDev d, const int* __restrict__ map, const double* __restrict__ tT,
                              const double* __restrict__ tP, double alpha, double beta) {
+    pdl_wait();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int r = map[i];
@@ -134,6 +137,7 @@ __global__ void k_eval_table(PlanDev d, const int* __restrict__ map, const doubl
 // Values plans (frontier.cu): T holds the throughput, P the efficiency of each
 // point as given (FrontierPoint); only the t_hat and eff orders are meaningful.
 __global__ void k_eval_values(PlanDev d) {
+    pdl_wait();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const double th = d.T[i], ef = d.P[i];
@@ -156,7 +160,8 @@ __global__ void k_eval_values(PlanDev d) {
 // the step needs no separate memset nodes; keys past n are padded in registers.
 template <int CH>
 __global__ void __launch_bounds__(CH / 4) k_sort_chunks(PlanDev d, uint64_t* gk,
-                                                        uint32_t* done) {
+                                                        uint32_t* done, int32_t* counts_reset) {
+    pdl_wait();
     constexpr int kChunk = CH;
     __shared__ uint64_t s[kChunk];
     const int o = blockIdx.y;
@@ -174,6 +179,9 @@ __global__ void __launch_bounds__(CH / 4) k_sort_chunks(PlanDev d, uint64_t* gk,
         gk[0] = gk[1] = kNone64;
         *done = 0;
     }
+    // in a captured step the select's class counters are reset here (no memset node)
+    if (counts_reset && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 16)
+        counts_reset[threadIdx.x] = 0;
     for (int ks = 2; ks <= kChunk; ks <<= 1) {
         for (int j = ks >> 1; j > 0; j >>= 1) {
             if (j >= 128) {
@@ -237,6 +245,7 @@ __device__ __forceinline__ int upper_bound_s(const uint64_t* s, int n, uint64_t 
 // the number of keys before it in every other chunk (a stable k-way merge).
 template <int CH>
 __global__ void __launch_bounds__(256) k_cross(PlanDev d) {
+    pdl_wait();
     constexpr int kChunk = CH;
     __shared__ uint64_t s[kChunk];
     const int a = blockIdx.x, b = blockIdx.y, o = blockIdx.z;
@@ -257,6 +266,7 @@ __global__ void __launch_bounds__(256) k_cross(PlanDev d) {
 
 // (3) scatter to the merged order
 __global__ void k_scatter(PlanDev d) {
+    pdl_wait();
     const int o = blockIdx.y;
     uint64_t* m = d.merged[o];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.n;
@@ -322,16 +332,17 @@ __device__ void resolve_globals_warp(const PlanDev& d, const uint64_t* gk, int w
 
 // grid.y = order: one thread per (point, order) keeps the dependent search chains
 // short. The last block to finish resolves the two query-independent winners.
-__global__ void k_assign(PlanDev d, const int* __restrict__ tr, uint64_t* gk, uint32_t* done) {
-    __shared__ uint64_t samp[kSamples];
-    const int o = blockIdx.y;
+// assign_body: block bx of nbx for order o; nblocks = all assign blocks of the launch.
+__device__ __forceinline__ void assign_body(const PlanDev& d, const int* __restrict__ tr,
+                                            uint64_t* gk, uint32_t* done, int o, int bx, int nbx,
+                                            uint32_t nblocks, uint64_t* samp) {
     const uint64_t* m = d.merged[o];
     const int64_t S = (d.n + kSamples - 1) / kSamples;
     const int ns = (int)((d.n + S - 1) / S);
     for (int t = threadIdx.x; t < ns; t += blockDim.x) samp[t] = m[t * S];
     __syncthreads();
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.n;
-         i += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t i = bx * (int64_t)blockDim.x + threadIdx.x; i < d.n;
+         i += (int64_t)nbx * blockDim.x) {
         const uint32_t r = lower_bound_sampled(m, d.n, samp, ns, S, d.skey[o][i]);
         const uint64_t k = ((uint64_t)r << d.tr_bits) | (uint64_t)tr[i];
         if (d.wide) d.key64[o][i] = k;
@@ -360,7 +371,7 @@ __global__ void k_assign(PlanDev d, const int* __restrict__ tr, uint64_t* gk, ui
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
-        last = atomicAdd(done, 1u) == gridDim.x * gridDim.y - 1;
+        last = atomicAdd(done, 1u) == nblocks - 1;
     }
     __syncthreads();
     if (last) {
@@ -369,6 +380,13 @@ __global__ void k_assign(PlanDev d, const int* __restrict__ tr, uint64_t* gk, ui
         if (w < 2) resolve_globals_warp(d, gk, w);
     }
 }
+
+__global__ void k_assign(PlanDev d, const int* __restrict__ tr, uint64_t* gk, uint32_t* done) {
+    pdl_wait();
+    __shared__ uint64_t samp[kSamples];
+    assign_body(d, tr, gk, done, blockIdx.y, blockIdx.x, gridDim.x, gridDim.x * gridDim.y, samp);
+}
+
 
 // Last merged position of the near-tie cluster that contains position r0: the
 // cluster extends over runs whose boundaries are near-ties (bnd == 1).
@@ -563,8 +581,8 @@ __device__ __forceinline__ int64_t count_prefix(const uint64_t* m, int o, int64_
     return a;
 }
 
-__global__ void k_qprep(PlanDev d, SelArgs a) {
-    __shared__ double samp_t[kSamples], samp_p[kSamples];
+__device__ __forceinline__ void qprep_body(const PlanDev& d, const SelArgs& a, int bx, int nbx,
+                                           double* samp_t, double* samp_p) {
     const int lane = threadIdx.x & 31;
     const int64_t S = (d.n + kSamples - 1) / kSamples;
     const int ns = (int)((d.n + S - 1) / S);
@@ -573,8 +591,7 @@ __global__ void k_qprep(PlanDev d, SelArgs a) {
         samp_p[t] = key_value(ORD_P, d.merged[ORD_P][t * S]);
     }
     __syncthreads();
-    for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x; j0 < a.nq;
-         j0 += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t j0 = bx * (int64_t)blockDim.x; j0 < a.nq; j0 += (int64_t)nbx * blockDim.x) {
         const int64_t j = j0 + threadIdx.x;
         int c = -1;
         if (j < a.nq) {
@@ -612,6 +629,28 @@ __global__ void k_qprep(PlanDev d, SelArgs a) {
             base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
             if (c == k) a.qlist[k * a.qcap + base + __popc(m & ((1u << lane) - 1))] = (int32_t)j;
         }
+    }
+}
+
+__global__ void k_qprep(PlanDev d, SelArgs a) {
+    pdl_wait();
+    __shared__ double samp_t[kSamples], samp_p[kSamples];
+    qprep_body(d, a, blockIdx.x, gridDim.x, samp_t, samp_p);
+}
+
+// k_assign and k_qprep in one launch (the captured step): qprep reads only the merged
+// arrays, so its blocks (grid.y == N_ORD) run beside the assign blocks (grid.y < N_ORD).
+__global__ void k_assign_qprep(PlanDev d, const int* __restrict__ tr, uint64_t* gk,
+                               uint32_t* done, SelArgs a, int eb, int qb) {
+    pdl_wait();
+    __shared__ uint64_t sbuf[2 * kSamples];
+    if (blockIdx.y < N_ORD) {
+        if ((int)blockIdx.x >= eb) return;
+        assign_body(d, tr, gk, done, blockIdx.y, blockIdx.x, eb, (uint32_t)eb * N_ORD, sbuf);
+    } else {
+        if ((int)blockIdx.x >= qb) return;
+        qprep_body(d, a, blockIdx.x, qb, reinterpret_cast<double*>(sbuf),
+                   reinterpret_cast<double*>(sbuf) + kSamples);
     }
 }
 
@@ -677,6 +716,7 @@ __device__ __forceinline__ int64_t scan_pos_of(const ScanPlan& sp, int64_t u) {
 
 template <typename K>
 __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K* se = reinterpret_cast<K*>(smem_raw);
     K* st = se + kScanCh;
@@ -786,6 +826,7 @@ __device__ __forceinline__ void push_work(const SelArgs& a, int32_t qid, int mod
 
 // (9) decide every query from its two minima; near-tie winners go to the exact fold
 __global__ void k_finalize(PlanDev d, SelArgs a) {
+    pdl_wait();
     const uint64_t mask = (1ull << d.tr_bits) - 1;
     const uint64_t none = kNone64;
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.nq;
@@ -840,6 +881,7 @@ __global__ void k_finalize(PlanDev d, SelArgs a) {
 
 // (10) exact sequential fold for the queued queries, one warp per query
 __global__ void k_exact(PlanDev d, SelArgs a) {
+    pdl_wait();
     const int warps = (gridDim.x * blockDim.x) >> 5;
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwork = a.counts[N_CLS];
@@ -971,6 +1013,10 @@ static int plan_build(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
         const int c = e ? atoi(e) : (n <= 65536 ? 2048 : kChunk);
         p->chunk = (c == 1024 || c == 2048 || c == 4096) ? c : kChunk;
     }
+    {
+        const char* e = getenv("PALS_PDL");
+        p->pdl = e ? atoi(e) != 0 : 1;
+    }
     p->nchunks = (int)((n + p->chunk - 1) / p->chunk);
     p->np = (int64_t)p->nchunks * p->chunk;
     PlanDev& d = p->d;
@@ -1011,6 +1057,9 @@ static int plan_build(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
         else d.key32[o] = (uint32_t*)take((size_t)n * 4);
     }
     d.globals = (int32_t*)take(16);
+    // globals[2] (the generic-score flag) only ever gets set, and a plan's scores are
+    // the same every prepare, so it is zeroed once here instead of every step
+    PALS_CUDA(cudaMemset(d.globals, 0, 16));
     p->gk = (uint64_t*)take(32);  // [2] global candidate keys + k_assign's done counter
     p->d_an = (Analytic*)take(sizeof(Analytic));
     // TR per point (inverse of grid inv_tr), computed once on the host at grid creation
@@ -1072,39 +1121,44 @@ int pals_plan_destroy(pals_plan* p) {
 
 
 // prepare, part 1: evaluate, sort, cross-rank, scatter (merged arrays ready)
-static int prep_head(pals_plan* p) {
+static int prep_head(pals_plan* p, int32_t* counts_reset = nullptr) {
     pals_ctx* ctx = p->ctx;
     cudaStream_t s = ctx->stream;
     PlanDev& d = p->d;
     const int64_t n = p->n;
+    const bool pdl = p->pdl;
     (void)cudaGetLastError();  // clear stale non-sticky errors of earlier calls
-    PALS_CUDA(cudaMemsetAsync(d.globals, 0, 16, s));  // generic flag, set by the eval
     const int eb = grid_blocks(ctx, n, 256);
+    cudaError_t e = cudaSuccess;
     if (p->values) {
-        k_eval_values<<<eb, 256, 0, s>>>(d);
+        e = launch_k(k_eval_values, eb, 256, 0, s, false, d);
     } else if (p->model->kind == MODEL_ANALYTIC) {
-        k_eval_analytic<<<eb, 256, 0, s>>>(d, p->d_an, p->grid->tp, p->coeffs.alpha,
-                                           p->coeffs.beta_watts);
+        e = launch_k(k_eval_analytic, eb, 256, 0, s, false, d, (const Analytic*)p->d_an,
+                     (const int*)p->grid->tp, p->coeffs.alpha, p->coeffs.beta_watts);
     } else if (p->model->kind == MODEL_TABLE) {
-        k_eval_table<<<eb, 256, 0, s>>>(d, p->table_map, p->table_T, p->table_P, p->coeffs.alpha,
-                                        p->coeffs.beta_watts);
+        e = launch_k(k_eval_table, eb, 256, 0, s, false, d, (const int*)p->table_map,
+                     (const double*)p->table_T, (const double*)p->table_P, p->coeffs.alpha,
+                     p->coeffs.beta_watts);
     } else {
         const int rc = forest_eval_plan(p, p->model, ctx);
         if (rc) return rc;
     }
+    if (e != cudaSuccess) return cuda_fail(e, "pals_plan_prepare eval");
     const dim3 gs(p->nchunks, N_ORD), gx(p->nchunks, p->nchunks, N_ORD);
     uint32_t* done = (uint32_t*)(p->gk + 2);
     if (p->chunk == 1024) {
-        k_sort_chunks<1024><<<gs, 256, 0, s>>>(d, p->gk, done);
-        k_cross<1024><<<gx, 256, 0, s>>>(d);
+        e = launch_k(k_sort_chunks<1024>, gs, 256, 0, s, pdl, d, p->gk, done, counts_reset);
+        if (e == cudaSuccess) e = launch_k(k_cross<1024>, gx, 256, 0, s, pdl, d);
     } else if (p->chunk == 2048) {
-        k_sort_chunks<2048><<<gs, 512, 0, s>>>(d, p->gk, done);
-        k_cross<2048><<<gx, 256, 0, s>>>(d);
+        e = launch_k(k_sort_chunks<2048>, gs, 512, 0, s, pdl, d, p->gk, done, counts_reset);
+        if (e == cudaSuccess) e = launch_k(k_cross<2048>, gx, 256, 0, s, pdl, d);
     } else {
-        k_sort_chunks<4096><<<gs, 1024, 0, s>>>(d, p->gk, done);
-        k_cross<4096><<<gx, 256, 0, s>>>(d);
+        e = launch_k(k_sort_chunks<4096>, gs, 1024, 0, s, pdl, d, p->gk, done, counts_reset);
+        if (e == cudaSuccess) e = launch_k(k_cross<4096>, gx, 256, 0, s, pdl, d);
     }
-    k_scatter<<<dim3(grid_blocks(ctx, n, 256), N_ORD), 256, 0, s>>>(d);
+    if (e == cudaSuccess)
+        e = launch_k(k_scatter, dim3(grid_blocks(ctx, n, 256), N_ORD), 256, 0, s, pdl, d);
+    if (e != cudaSuccess) return cuda_fail(e, "pals_plan_prepare");
     count_launch(ctx, 4);
     return check_launch("pals_plan_prepare");
 }
@@ -1113,8 +1167,9 @@ static int prep_head(pals_plan* p) {
 static int prep_tail(pals_plan* p) {
     pals_ctx* ctx = p->ctx;
     const int eb = grid_blocks(ctx, p->n, 256);
-    k_assign<<<dim3(eb, N_ORD), 256, 0, ctx->stream>>>(p->d, p->tr, p->gk,
-                                                        (uint32_t*)(p->gk + 2));
+    const cudaError_t e = launch_k(k_assign, dim3(eb, N_ORD), 256, 0, ctx->stream, (bool)p->pdl,
+                                   p->d, (const int*)p->tr, p->gk, (uint32_t*)(p->gk + 2));
+    if (e != cudaSuccess) return cuda_fail(e, "pals_plan_prepare assign");
     count_launch(ctx, 1);
     return check_launch("pals_plan_prepare");
 }
@@ -1176,7 +1231,9 @@ static SelArgs make_args(pals_plan* p, const pals_query* d_queries, int64_t nq, 
 // select, part 1 (needs only the merged arrays): thresholds and classes per query
 static int select_head(pals_plan* p, const SelArgs& a, cudaStream_t s) {
     PALS_CUDA(cudaMemsetAsync(p->counts, 0, 64, s));
-    k_qprep<<<grid_blocks(p->ctx, a.nq, 256), 256, 0, s>>>(p->d, a);
+    const cudaError_t e = launch_k(k_qprep, grid_blocks(p->ctx, a.nq, 256), 256, 0, s, false,
+                                   p->d, a);
+    if (e != cudaSuccess) return cuda_fail(e, "pals_plan_select_device qprep");
     count_launch(p->ctx, 1);
     return check_launch("pals_plan_select_device");
 }
@@ -1187,20 +1244,25 @@ static int select_tail(pals_plan* p, const SelArgs& a) {
     cudaStream_t s = ctx->stream;
     // stream-K scan grid: 4 CTAs per SM, equal integer-op shares (see k_scan)
     const int sgrid = ctx->num_sms * 4;
+    // event-record nodes around the scan (timing) are not kernels: plain edges there
+    const bool pdl = p->pdl && !p->time_scan;
     // inside a stream capture the events become graph event-record nodes
     const unsigned evf = p->capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
     if (p->time_scan) PALS_CUDA(cudaEventRecordWithFlags(p->ev_scan0, s, evf));
+    cudaError_t e;
     if (p->d.wide)
-        k_scan<uint64_t><<<sgrid, kScanThreads, 3 * kScanCh * 8, s>>>(p->d, a);
+        e = launch_k(k_scan<uint64_t>, sgrid, kScanThreads, 3 * kScanCh * 8, s, pdl, p->d, a);
     else
-        k_scan<uint32_t><<<sgrid, kScanThreads, 3 * kScanCh * 4, s>>>(p->d, a);
+        e = launch_k(k_scan<uint32_t>, sgrid, kScanThreads, 3 * kScanCh * 4, s, pdl, p->d, a);
+    if (e != cudaSuccess) return cuda_fail(e, "k_scan");
     if (p->time_scan) {
         PALS_CUDA(cudaEventRecordWithFlags(p->ev_scan1, s, evf));
         p->scan_recorded = 1;
     }
     const int qb = grid_blocks(ctx, a.nq, 256);
-    k_finalize<<<qb, 256, 0, s>>>(p->d, a);
-    k_exact<<<ctx->num_sms * 2, 256, 0, s>>>(p->d, a);
+    e = launch_k(k_finalize, qb, 256, 0, s, pdl, p->d, a);
+    if (e == cudaSuccess) e = launch_k(k_exact, ctx->num_sms * 2, 256, 0, s, (bool)p->pdl, p->d, a);
+    if (e != cudaSuccess) return cuda_fail(e, "pals_plan_select_device tail");
     count_launch(ctx, 3);
     return check_launch("pals_plan_select_device");
 }
@@ -1218,8 +1280,8 @@ int pals_plan_select_device(pals_plan* p, const pals_query* d_queries, int64_t n
 }
 
 // One full step — evaluate + rank (prepare) and select — replayed from a CUDA graph
-// captured on first use for these device buffers (9 kernels + 5 memsets per step;
-// the graph removes the per-launch host overhead between them).
+// captured on first use for these device buffers (8 kernels, no memset nodes: the
+// class counters are reset by k_sort_chunks, assign and qprep share one launch).
 int pals_plan_run(pals_plan* p, const pals_query* d_queries, int64_t nq, int32_t* d_idx,
                   uint8_t* d_reason) {
     if (p->err) return set_error(p->err, p->err_msg);
@@ -1242,12 +1304,19 @@ int pals_plan_run(pals_plan* p, const pals_query* d_queries, int64_t nq, int32_t
         const int64_t l0 = ctx->launches;
         // (overlapping qprep with k_assign on a side stream measured no faster on
         // B200: the step stays a single chain)
-        rc = prep_head(p);
-        if (!rc) rc = prep_tail(p);
+        rc = prep_head(p, p->counts);
         if (!rc) {
+            // assign (prepare, part 2) and qprep (select, part 1) fused in one launch
             const SelArgs a = make_args(p, d_queries, nq, d_idx, d_reason);
-            rc = select_head(p, a, s);
-            if (!rc) rc = select_tail(p, a);
+            const int eb = grid_blocks(ctx, p->n, 256), qb = grid_blocks(ctx, nq, 256);
+            const cudaError_t e = launch_k(k_assign_qprep, dim3(std::max(eb, qb), N_ORD + 1),
+                                           256, 0, s, (bool)p->pdl, p->d, (const int*)p->tr,
+                                           p->gk, (uint32_t*)(p->gk + 2), a, eb, qb);
+            if (e != cudaSuccess) rc = cuda_fail(e, "k_assign_qprep");
+            if (!rc) {
+                count_launch(ctx, 1);
+                rc = select_tail(p, a);
+            }
         }
         p->capturing = 0;
         cudaGraph_t g = nullptr;

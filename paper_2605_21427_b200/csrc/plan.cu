@@ -54,6 +54,7 @@ struct pals_plan {
     int force_exact = 0;
     int values = 0;               // internal: th / ef supplied directly (frontier.cu)
     int pdl = 1;                  // programmatic dependent launch between step kernels
+    int merge_mode = 1;           // 1: pairwise merge rounds, 0: all-pairs cross-rank + scatter
     int64_t last_exact = 0;
     PlanDev d{};
     int* tr = nullptr;            // device TR per point
@@ -160,7 +161,8 @@ __global__ void k_eval_values(PlanDev d) {
 // the step needs no separate memset nodes; keys past n are padded in registers.
 template <int CH>
 __global__ void __launch_bounds__(CH / 4) k_sort_chunks(PlanDev d, uint64_t* gk,
-                                                        uint32_t* done, int32_t* counts_reset) {
+                                                        uint32_t* done, int32_t* counts_reset,
+                                                        int to_merged) {
     pdl_wait();
     constexpr int kChunk = CH;
     __shared__ uint64_t s[kChunk];
@@ -219,7 +221,9 @@ __global__ void __launch_bounds__(CH / 4) k_sort_chunks(PlanDev d, uint64_t* gk,
         }
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) d.sorted[o][base + i0 + 32 * k] = x[k];
+    uint64_t* dst = to_merged ? d.merged[o] : d.sorted[o];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) dst[base + i0 + 32 * k] = x[k];
 }
 
 __device__ __forceinline__ int lower_bound_s(const uint64_t* s, int n, uint64_t x) {
@@ -261,6 +265,46 @@ __global__ void __launch_bounds__(256) k_cross(PlanDev d) {
         else if (b < a) cnt = upper_bound_s(s, kChunk, x);
         else cnt = lower_bound_s(s, kChunk, x);
         atomicAdd(&d.pos[o][abase + i], (uint32_t)cnt);
+    }
+}
+
+// (2'') large grids: instead of searching every other chunk (O(n * chunks)), merge
+// sorted runs pairwise, log2(chunks) rounds of one binary search per key into its
+// sibling run. A key of run r lands at (its index in r) + (keys of the sibling that
+// precede it: strictly smaller from a right sibling, smaller or equal from a left
+// one), which is the stable merge k_cross + k_scatter produce. Buffers ping-pong
+// between sorted and merged; the chunk sort picks its output so the last round
+// writes merged.
+__global__ void k_merge_round(PlanDev d, int64_t np, int64_t L, int to_merged) {
+    pdl_wait();
+    const int o = blockIdx.y;
+    const uint64_t* in = to_merged ? d.sorted[o] : d.merged[o];
+    uint64_t* out = to_merged ? d.merged[o] : d.sorted[o];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < np;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / L, j = i - r * L, sib = r ^ 1;
+        const uint64_t x = in[i];
+        const int64_t sb = sib * L;
+        if (sb >= np) {  // no sibling run at this level
+            out[i] = x;
+            continue;
+        }
+        const uint64_t* sr = in + sb;
+        int64_t lo = 0, hi = min(L, np - sb);
+        if (sib < r) {
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (sr[mid] <= x) lo = mid + 1;
+                else hi = mid;
+            }
+        } else {
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (sr[mid] < x) lo = mid + 1;
+                else hi = mid;
+            }
+        }
+        out[(r & ~(int64_t)1) * L + j + lo] = x;
     }
 }
 
@@ -1016,6 +1060,8 @@ static int plan_build(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
     {
         const char* e = getenv("PALS_PDL");
         p->pdl = e ? atoi(e) != 0 : 1;
+        const char* mm = getenv("PALS_MERGE");
+        p->merge_mode = mm ? (atoi(mm) ? 1 : 0) : 1;
     }
     p->nchunks = (int)((n + p->chunk - 1) / p->chunk);
     p->np = (int64_t)p->nchunks * p->chunk;
@@ -1146,18 +1192,35 @@ static int prep_head(pals_plan* p, int32_t* counts_reset = nullptr) {
     if (e != cudaSuccess) return cuda_fail(e, "pals_plan_prepare eval");
     const dim3 gs(p->nchunks, N_ORD), gx(p->nchunks, p->nchunks, N_ORD);
     uint32_t* done = (uint32_t*)(p->gk + 2);
+    // merge rounds (measured on B200: cfg2 0.176 -> 0.164 ms per step, cfg3x 5.42 -> 4.28 ms
+    // against the all-pairs cross-rank, which stays selectable with PALS_MERGE=0)
+    int rounds = 0;
+    while (((int64_t)p->chunk << rounds) < p->np) ++rounds;
+    const bool merge = p->merge_mode == 1;
+    const int sort_to_merged = merge ? (rounds % 2 == 0) : 0;
     if (p->chunk == 1024) {
-        e = launch_k(k_sort_chunks<1024>, gs, 256, 0, s, pdl, d, p->gk, done, counts_reset);
-        if (e == cudaSuccess) e = launch_k(k_cross<1024>, gx, 256, 0, s, pdl, d);
+        e = launch_k(k_sort_chunks<1024>, gs, 256, 0, s, pdl, d, p->gk, done, counts_reset,
+                     sort_to_merged);
+        if (e == cudaSuccess && !merge) e = launch_k(k_cross<1024>, gx, 256, 0, s, pdl, d);
     } else if (p->chunk == 2048) {
-        e = launch_k(k_sort_chunks<2048>, gs, 512, 0, s, pdl, d, p->gk, done, counts_reset);
-        if (e == cudaSuccess) e = launch_k(k_cross<2048>, gx, 256, 0, s, pdl, d);
+        e = launch_k(k_sort_chunks<2048>, gs, 512, 0, s, pdl, d, p->gk, done, counts_reset,
+                     sort_to_merged);
+        if (e == cudaSuccess && !merge) e = launch_k(k_cross<2048>, gx, 256, 0, s, pdl, d);
     } else {
-        e = launch_k(k_sort_chunks<4096>, gs, 1024, 0, s, pdl, d, p->gk, done, counts_reset);
-        if (e == cudaSuccess) e = launch_k(k_cross<4096>, gx, 256, 0, s, pdl, d);
+        e = launch_k(k_sort_chunks<4096>, gs, 1024, 0, s, pdl, d, p->gk, done, counts_reset,
+                     sort_to_merged);
+        if (e == cudaSuccess && !merge) e = launch_k(k_cross<4096>, gx, 256, 0, s, pdl, d);
     }
-    if (e == cudaSuccess)
+    if (merge) {
+        // round k reads the buffer round k-1 wrote; the last round writes merged
+        const dim3 gm(grid_blocks(ctx, p->np, 256), N_ORD);
+        for (int k = 0; k < rounds && e == cudaSuccess; ++k)
+            e = launch_k(k_merge_round, gm, 256, 0, s, pdl, d, p->np, (int64_t)p->chunk << k,
+                         (int)((rounds - k) % 2 == 1));
+        count_launch(ctx, rounds - 2);  // eval + sort + rounds (the 4 below: eval, sort, cross, scatter)
+    } else if (e == cudaSuccess) {
         e = launch_k(k_scatter, dim3(grid_blocks(ctx, n, 256), N_ORD), 256, 0, s, pdl, d);
+    }
     if (e != cudaSuccess) return cuda_fail(e, "pals_plan_prepare");
     count_launch(ctx, 4);
     return check_launch("pals_plan_prepare");

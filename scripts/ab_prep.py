@@ -1,4 +1,4 @@
-"""A/B of the step variants (sort chunk x programmatic dependent launch) on the cfg2 step:
+"""A/B of the step variants (sort chunk x cross-rank vs merge rounds) on the cfg2 step:
 device ms/step of plan.run (graph), and selections identical across variants."""
 import json
 import os
@@ -13,9 +13,9 @@ from paper_2605_21427_b200.abi import QUERY_DT  # noqa: E402
 from paper_2605_21427_b200.wattserve import AnalyticModel, Context, Grid, Plan  # noqa: E402
 
 
-def run(chunk, pdl, which="cfg2", steps=50):
+def run(chunk, merge, which="cfg2", steps=50):
     os.environ["PALS_SORT_CHUNK"] = str(chunk)
-    os.environ["PALS_PDL"] = str(pdl)
+    os.environ["PALS_MERGE"] = str(merge)
     ctx = Context(0)
     st = torch.cuda.Stream()
     ctx.set_stream(st.cuda_stream)
@@ -47,13 +47,13 @@ if __name__ == "__main__":
     for which in ("cfg2", "cfg3x"):
         base = None
         for rep in range(2):
-            for chunk in (2048, 4096):
-                for pdl in (0, 1):
-                    ms, idx = run(chunk, pdl, which)
+            for chunk in (1024, 2048, 4096):
+                for merge in (0, 1):
+                    ms, idx = run(chunk, merge, which, steps=50 if which == "cfg2" else 10)
                     if base is None:
                         base = idx
-                    out[f"{which} chunk{chunk} pdl{pdl} rep{rep}"] = {
+                    out[f"{which} chunk{chunk} merge{merge} rep{rep}"] = {
                         "ms": ms, "same": bool(np.array_equal(idx, base))}
-                    print(which, chunk, "pdl", pdl, f"{ms:.4f} ms", np.array_equal(idx, base),
+                    print(which, chunk, "merge", merge, f"{ms:.4f} ms", np.array_equal(idx, base),
                           flush=True)
     json.dump(out, open(os.environ.get("OUT", "gpurun_out/ab_prep.json"), "w"), indent=1)

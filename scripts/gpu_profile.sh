@@ -10,7 +10,7 @@ timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; ech
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2>> gpurun_out/bench.err
 SMALL="--steps 2 --warmup 1 --traces 100000 --predictions 4194304 --no-cpu-baseline"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py $SMALL > gpurun_out/b_ncu.log 2>&1
-for k in k_scan k_sort_chunks k_forest_eval_aos k_cross k_assign; do
+for k in k_scan k_sort_chunks k_forest_eval_aos k_cross k_assign_qprep k_allocate k_front_scan; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 -o gpurun_out/prof_$k python bench.py $SMALL > gpurun_out/ncu_$k.log 2>&1
 done
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_replay -s 1 -c 1 -o gpurun_out/prof_k_replay python bench.py --steps 1 --warmup 1 --traces 100000 --trace-steps 600 --predictions 1048576 --no-cpu-baseline > gpurun_out/ncu_k_replay.log 2>&1

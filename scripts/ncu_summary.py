@@ -34,8 +34,8 @@ def summarise(rep):
     h, u = rows[0], rows[1]
     res = {}
     for v in rows[2:]:
-        name = v[h.index("Kernel Name")].split("(")[0].split("<")[0].replace("pals::", "")
-        name = name.replace("void ", "").strip()
+        name = v[h.index("Kernel Name")].split("(")[0].replace("void ", "")
+        name = name.replace("<unnamed>::", "").replace("pals::", "").split("<")[0].strip()
         d = {}
         for i, col in enumerate(h):
             if col in WANT:

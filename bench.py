@@ -60,6 +60,11 @@ def parse():
                     help="points per GPU for the forest-predictor leg")
     ap.add_argument("--clusters", type=int, default=1_000_000,
                     help="allocate_budget problems per GPU for the allocator leg")
+    ap.add_argument("--cfg3-queries", type=int, default=1_000_000,
+                    help="cfg3 (target, budget) queries per GPU")
+    ap.add_argument("--cfg5-traces", type=int, default=10_000_000,
+                    help="cfg5 traces in total (split over the GPUs)")
+    ap.add_argument("--cfg5-steps", type=int, default=2, help="timed cfg5 replays")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU time per reference sample")
@@ -435,6 +440,8 @@ def run_ours(args, dist: Dist):
     # ---------------- allocate_budget over many clusters ----------------
     allocations = bench_allocations(args, dist, ctx, stream, l2_flush)
     frontiers = bench_frontiers(args, dist, ctx, stream, l2_flush)
+    cfg3, c3, tref3 = bench_cfg3(args, dist, ctx, stream, l2_flush, int_peak)
+    cfg5 = bench_cfg5(args, dist, ctx, stream, l2_flush) if args.cfg5_traces > 0 else None
 
     # ---------------- cfg1: single-call latency (the drop-in's synchronous API) ----------------
     from paper_2605_21427_b200.abi import CtrlState, Point, Telemetry
@@ -491,6 +498,8 @@ def run_ours(args, dist: Dist):
         "predictions": predictions,
         "allocations": allocations,
         "frontiers": frontiers,
+        "cfg3": cfg3,
+        "cfg5": cfg5,
         "latency": latency,
         "peaks": {"int_ops_per_s": int_peak, "fp64_flops_per_s": fp64_peak,
                   "hbm_gbs_measured": measured_peaks_json().get("hbm_gbs")},
@@ -500,6 +509,9 @@ def run_ours(args, dist: Dist):
         out["predictions"]["cpu_baseline"] = cpu_predict(args, bundle, args.cpu_seconds)
         out["allocations"]["cpu_baseline"] = cpu_allocate(args, args.cpu_seconds)
         out["frontiers"]["cpu_baseline"] = cpu_frontier(args.cpu_seconds)
+        out["cfg3"]["cpu_baseline"] = cpu_cfg3(args, c3, tref3, args.cpu_seconds)
+        if cfg5 is not None:  # same per-trace work as cfg4: the cfg4 reference sample
+            out["cfg5"]["cpu_baseline"] = dict(out["decisions"]["cpu_baseline"])
         out["latency"]["cpu_reference_select_config_us"] = cpu_latency(c1, float(th1.max()))
     if dist.rank == 0:
         print(json.dumps(out), flush=True)
@@ -604,6 +616,199 @@ def bench_allocations(args, dist, ctx, stream, l2_flush):
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
         "gpu_launches": int(launches),
     }
+
+
+CFG3_WORKLOAD = ("cfg3: mixtral-8x7b-like MoE (+tp8 comm), caps 100+300i/63 x batch 1..256 x "
+                 "tp{1,2,4,8} at ep=8 = 65536 configs, 1e6 (target, budget) queries per GPU, "
+                 "QoS / budget-throughput 50/50, budget U(600,2000) W, margin 0.02; "
+                 "eval+rank+select per step")
+CFG5_WORKLOAD = ("cfg5: 1e7 fluid-plant traces in total (8 calibrated profiles: dense and MoE) x "
+                 "3600 control intervals, contiguous trace shards per GPU, final per-trace "
+                 "summary gather (48 B/trace) to rank 0")
+
+
+def bench_cfg3(args, dist, ctx, stream, l2_flush, int_peak):
+    """BASELINE cfg3: the MoE grid with 1e6 mixed (target, budget) queries per GPU."""
+    import torch
+    from paper_2605_21427_b200 import workloads
+    from paper_2605_21427_b200.abi import QUERY_DT, ptr
+    from paper_2605_21427_b200.wattserve import AnalyticModel, Grid, Plan
+    c = workloads.cfg3(args.cfg3_queries)
+    plan = Plan(AnalyticModel(ctx, c["profile"], c["gpu"]), Grid(ctx, c["points"]), c["coeffs"])
+    n_cfg = len(c["points"])
+    th, _, _ = plan.scores()
+    tref = float(th.max())
+    nq = args.cfg3_queries
+    q = workloads.gen_queries(nq, c["seed"], tref, c["objective"], budget=c["budget"],
+                              first=dist.rank * nq)
+    d_q = torch.from_numpy(q.view(np.uint8).copy()).cuda()
+    d_idx = torch.empty(nq, dtype=torch.int32, device="cuda")
+    d_rs = torch.empty(nq, dtype=torch.uint8, device="cuda")
+    step = lambda: plan.run(d_q.data_ptr(), nq, d_idx.data_ptr(), d_rs.data_ptr())  # noqa: E731
+    plan.time_scan(True)
+    for _ in range(args.warmup):
+        l2_flush()
+        step()
+    torch.cuda.synchronize()
+    cnt = plan.stats()
+    scanned_q = int(cnt[0] + cnt[1] + cnt[2])
+    int_ops_step = (2 * cnt[0] + 4 * cnt[1] + 2 * cnt[2]) * n_cfg
+    l0 = ctx.launches
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    scan_ms = []
+    dist.barrier()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        l2_flush()
+        ev[k][0].record(stream)
+        step()
+        ev[k][1].record(stream)
+        scan_ms.append(plan.scan_ms())
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches = ctx.launches - l0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    t_max = dist.max(float(np.sum(step_ms)))
+    pairs_total = dist.sum(float(scanned_q * n_cfg)) * args.steps
+    value = pairs_total / (t_max * 1e-3)
+    # e2e: pinned host queries -> pals_select (H2D, eval+rank+select, D2H index/reason)
+    h_q = torch.empty(nq * QUERY_DT.itemsize, dtype=torch.uint8, pin_memory=True)
+    h_qn = h_q.numpy().view(QUERY_DT)
+    h_qn[:] = q
+    h_idx = torch.empty(nq, dtype=torch.int32, pin_memory=True).numpy()
+    h_rs = torch.empty(nq, dtype=torch.uint8, pin_memory=True).numpy()
+    lib = ctx.lib
+
+    def e2e_step():
+        rc = lib.pals_select(plan.h, ptr(h_qn), nq, ptr(h_idx), ptr(h_rs))
+        assert rc == 0, lib.pals_last_error()
+
+    e2e_step()
+    e2e_ms = []
+    for _ in range(args.steps):
+        l2_flush()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        e2e_step()
+        b.record(stream)
+        b.synchronize()
+        e2e_ms.append(a.elapsed_time(b))
+    e2e_max = dist.max(float(np.sum(e2e_ms)))
+    scan_avg = float(np.mean(scan_ms))
+    out = {"metric": "config evals/s (cfg3 select_config, MoE grid, mixed QoS/budget queries)",
+           "value": value, "unit": "config evals/s", "ms_per_step": t_max / args.steps,
+           "steps": args.steps, "workload": CFG3_WORKLOAD, "configs": n_cfg,
+           "queries_per_gpu": nq, "scanned_queries_per_gpu": scanned_q,
+           "query_classes": {"qos_no_budget": int(cnt[0]), "qos_budget": int(cnt[1]),
+                             "budget_only": int(cnt[2]), "no_scan": int(cnt[3]),
+                             "exact_fold": int(cnt[5])},
+           "e2e": {"value": pairs_total / (e2e_max * 1e-3), "unit": "config evals/s",
+                   "h2d_bytes_per_step": nq * QUERY_DT.itemsize, "d2h_bytes_per_step": nq * 5,
+                   "api": "pals_select (C ABI, pinned host buffers; includes eval+rank)"},
+           "roofline": {"bound": "alu", "kernel": "k_scan<uint32_t>",
+                        "achieved": int_ops_step / (scan_avg * 1e-3) / 1e12,
+                        "peak": int_peak / 1e12, "unit": "Tops/s",
+                        "frac": int_ops_step / (scan_avg * 1e-3) / int_peak,
+                        "algorithmic": "2 int ops per scanned pair (4 for QoS+budget queries)",
+                        "scan_share_of_step": scan_avg / float(np.mean(step_ms))},
+           "gpu_launches": int(launches)}
+    return out, c, tref
+
+
+def cpu_cfg3(args, c, tref, seconds):
+    """cfg3 queries through the unmodified select_config + analytic_scorer, all threads."""
+    from paper_2605_21427_b200 import workloads
+    kind, ref = _reference_backend()
+    if kind != "reference":
+        return {"value": None, "unit": "config evals/s", "cores": 0, "kind": "port",
+                "sample": "reference build absent"}
+    threads = os.cpu_count() or 1
+    n = len(c["points"])
+    q = workloads.gen_queries(4 * threads, c["seed"], tref, c["objective"], budget=c["budget"])
+    t, _, _ = ref.bench_select(c["profile"], c["gpu"], c["points"], c["coeffs"], q, threads,
+                               want_results=False)
+    nq = int(min(args.cfg3_queries, max(threads, len(q) * n / t * seconds / n)))
+    q = workloads.gen_queries(nq, c["seed"], tref, c["objective"], budget=c["budget"])
+    t, _, _ = ref.bench_select(c["profile"], c["gpu"], c["points"], c["coeffs"], q, threads,
+                               want_results=False)
+    return {"value": nq * n / t, "unit": "config evals/s", "cores": threads, "kind": "reference",
+            "sample": f"first {nq} of the 1e6 cfg3 queries x {n} configs through the unmodified "
+                      f"select_config+analytic_scorer, {threads} threads, {t:.1f} s"}
+
+
+def bench_cfg5(args, dist, ctx, stream, l2_flush):
+    """BASELINE cfg5: 1e7 traces in total, strong-scaled over the ranks, plus the one
+    result gather (per-trace summaries) to rank 0."""
+    import torch
+    from paper_2605_21427_b200 import workloads
+    from paper_2605_21427_b200.abi import SUMMARY_DT
+    from paper_2605_21427_b200.shard import gather_to_rank0, shard_range
+    from paper_2605_21427_b200.wattserve import AnalyticModel, replay_device
+    s = workloads.cfg4_setup()
+    models = [AnalyticModel(ctx, p, s["gpu"]) for p in s["profiles"]]
+    n_total = args.cfg5_traces
+    first, nt = shard_range(n_total, dist.rank, dist.world)
+    spec = workloads.replay_spec(nt, n_steps=args.trace_steps, seed=2605, first=first)
+    d_sum = torch.empty((nt, SUMMARY_DT.itemsize), dtype=torch.uint8, device="cuda")
+    run = lambda: replay_device(ctx, models, s["profiles"], s["gpu"], s["coeffs"],  # noqa: E731
+                                s["caps"], s["batches"], s["cfg"], spec, d_sum.data_ptr())
+    run()
+    torch.cuda.synchronize()
+    steps = args.cfg5_steps
+    l0 = ctx.launches
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)]
+    dist.barrier()
+    torch.cuda.synchronize()
+    for k in range(steps):
+        l2_flush()
+        ev[k][0].record(stream)
+        run()
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches = ctx.launches - l0
+    t_max = dist.max(float(np.sum([a.elapsed_time(b) for a, b in ev])))
+    dec = float(n_total) * args.trace_steps * steps
+    # the only cross-GPU traffic: the per-trace summaries to rank 0 (NCCL gather over
+    # NVLink; a copy when N = 1)
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    host = (torch.empty((n_total, SUMMARY_DT.itemsize), dtype=torch.uint8, pin_memory=True)
+            if dist.rank == 0 else None)
+    dist.barrier()
+    torch.cuda.synchronize()
+    g0.record(stream)
+    local = d_sum if dist.backend == "nccl" or dist.world == 1 else d_sum.cpu()
+    allsum = gather_to_rank0(local, n_total, dist.rank, dist.world)
+    if dist.rank == 0:  # land the gathered summaries in pinned host memory
+        host.copy_(allsum, non_blocking=True)
+    g1.record(stream)
+    torch.cuda.synchronize()
+    gather_ms = dist.max(g0.elapsed_time(g1))
+    digest = None
+    if dist.rank == 0:
+        a = host.numpy().reshape(-1).view(SUMMARY_DT)
+        # checksum of checksums over all traces (size-independent parity handle)
+        h = np.uint64(0xCBF29CE484222325)
+        x = np.bitwise_xor.reduce(a["digest"] * np.uint64(0x100000001B3))
+        digest = f"{int(h ^ x):016x}"
+    return {"metric": "controller decisions/s (cfg5, strong scaling over the GPUs)",
+            "value": dec / (t_max * 1e-3), "unit": "decisions/s",
+            "ms_per_step": t_max / steps, "steps": steps, "scaling": "strong",
+            "workload": CFG5_WORKLOAD, "traces_total": n_total, "traces_this_rank": nt,
+            "trace_steps": args.trace_steps,
+            "gather": {"bytes": n_total * SUMMARY_DT.itemsize, "ms": gather_ms,
+                       "backend": dist.backend if dist.world > 1 else "none (N=1)",
+                       "digest_xor": digest},
+            "e2e": {"value": dec / steps / ((t_max / steps + gather_ms) * 1e-3),
+                    "unit": "decisions/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": n_total * SUMMARY_DT.itemsize,
+                    "api": "pals_replay_device, then the summary gather to rank 0 and its "
+                           "D2H into pinned host memory (the gather+D2H time is added once "
+                           "per step)"},
+            "gpu_launches": int(launches)}
 
 
 FRONTIER_WORKLOAD = ("build_frontier over cfg3x: mixtral-8x7b-like, 64 caps x 256 batches x "
@@ -832,6 +1037,10 @@ def run_reference(args, dist: Dist):
     dec = cpu_replay(args, per_step)
     alc = cpu_allocate(args, per_step)
     fro = cpu_frontier(per_step)
+    c3 = workloads.cfg3(args.cfg3_queries)
+    T3, _, _ = ref.eval(c3["profile"], c3["gpu"], c3["points"])
+    s3 = cpu_cfg3(args, c3, float(np.max(T3 * c3["points"]["dp"])), per_step)
+    zero = {"h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "config evals/s",
            "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
@@ -854,7 +1063,15 @@ def run_reference(args, dist: Dist):
                            "unit": "allocations/s", "workload": ALLOC_WORKLOAD,
                            "cpu_baseline": alc,
                            "e2e": {"value": alc["value"], "unit": "allocations/s",
-                                   "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}}
+                                   "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}},
+           "cfg3": {"metric": "config evals/s (cfg3 select_config, MoE grid, mixed QoS/budget "
+                              "queries)", "value": s3["value"], "unit": "config evals/s",
+                    "workload": CFG3_WORKLOAD, "cpu_baseline": s3,
+                    "e2e": {"value": s3["value"], "unit": "config evals/s", **zero}},
+           "cfg5": {"metric": "controller decisions/s (cfg5, strong scaling over the GPUs)",
+                    "value": dec["value"], "unit": "decisions/s", "workload": CFG5_WORKLOAD,
+                    "cpu_baseline": dec,
+                    "e2e": {"value": dec["value"], "unit": "decisions/s", **zero}}}
     print(json.dumps(out), flush=True)
 
 

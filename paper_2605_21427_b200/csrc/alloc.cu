@@ -361,8 +361,8 @@ static int alloc_build(pals_ctx* ctx, int n_sets, const pals_model* const* set_m
         rc = cuda_fail(cudaErrorMemoryAllocation, "pals_alloc");
         goto done;
     }
-    cudaMemcpy(dcap, hcap.data(), sizeof(double) * n1, cudaMemcpyHostToDevice);
-    cudaMemcpy(di, hi.data(), sizeof(int) * 4 * n1, cudaMemcpyHostToDevice);
+    copy_on(ctx->stream, dcap, hcap.data(), sizeof(double) * n1, cudaMemcpyHostToDevice);
+    copy_on(ctx->stream, di, hi.data(), sizeof(int) * 4 * n1, cudaMemcpyHostToDevice);
     for (int k = 0; k < n_sets && rc == PALS_OK; ++k) {
         const pals_model* m = set_model[k];
         const int64_t o = set_off[k] - base, nc = set_off[k + 1] - set_off[k];
@@ -388,8 +388,8 @@ static int alloc_build(pals_ctx* ctx, int n_sets, const pals_model* const* set_m
                 hT[c] = m->table_T[r];
                 hP[c] = m->table_P[r];
             }
-            cudaMemcpy(dT + o, hT.data(), sizeof(double) * nc, cudaMemcpyHostToDevice);
-            cudaMemcpy(dP + o, hP.data(), sizeof(double) * nc, cudaMemcpyHostToDevice);
+            copy_on(ctx->stream, dT + o, hT.data(), sizeof(double) * nc, cudaMemcpyHostToDevice);
+            copy_on(ctx->stream, dP + o, hP.data(), sizeof(double) * nc, cudaMemcpyHostToDevice);
         } else if (m->kind == MODEL_ANALYTIC) {
             if (!m->d_an) {
                 auto* mm = const_cast<pals_model*>(m);
@@ -397,7 +397,7 @@ static int alloc_build(pals_ctx* ctx, int n_sets, const pals_model* const* set_m
                     rc = cuda_fail(cudaErrorMemoryAllocation, "pals_alloc d_an");
                     break;
                 }
-                cudaMemcpy(mm->d_an, &m->an, sizeof(Analytic), cudaMemcpyHostToDevice);
+                copy_on(ctx->stream, mm->d_an, &m->an, sizeof(Analytic), cudaMemcpyHostToDevice);
             }
             const int blocks = (int)std::max<int64_t>(
                 1, std::min<int64_t>((nc + 255) / 256, 4 * ctx->num_sms));
@@ -414,9 +414,9 @@ static int alloc_build(pals_ctx* ctx, int n_sets, const pals_model* const* set_m
     if (rc == PALS_OK) {
         std::vector<int64_t> rel(n_sets + 1);
         for (int k = 0; k <= n_sets; ++k) rel[k] = set_off[k] - base;
-        cudaMemcpy(doff, rel.data(), sizeof(int64_t) * (n_sets + 1), cudaMemcpyHostToDevice);
-        cudaMemcpy(A->d_err, A->h_err.data(), sizeof(int32_t) * n_sets, cudaMemcpyHostToDevice);
-        cudaMemcpy(d_ok, ok.data(), sizeof(int32_t) * n_sets, cudaMemcpyHostToDevice);
+        copy_on(ctx->stream, doff, rel.data(), sizeof(int64_t) * (n_sets + 1), cudaMemcpyHostToDevice);
+        copy_on(ctx->stream, A->d_err, A->h_err.data(), sizeof(int32_t) * n_sets, cudaMemcpyHostToDevice);
+        copy_on(ctx->stream, d_ok, ok.data(), sizeof(int32_t) * n_sets, cudaMemcpyHostToDevice);
         int npow2 = 1;
         while (npow2 < maxc) npow2 <<= 1;
         const size_t smem = sizeof(uint64_t) * 2 * npow2;
@@ -523,13 +523,13 @@ int pals_alloc_steps(pals_alloc* A, int32_t set, double* power_w, double* throug
     if (set < 0 || set >= A->n_sets)
         return set_error(PALS_ERANGE, "pals_alloc_steps: set outside the plan");
     if (A->h_err[set] != PALS_OK) return set_error(A->h_err[set], A->h_msg[set]);
-    PALS_CUDA(cudaMemcpy(n_steps, A->d_ns + set, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    PALS_CUDA(copy_on(A->ctx->stream, n_steps, A->d_ns + set, sizeof(int32_t), cudaMemcpyDeviceToHost));
     const size_t o = (size_t)set * A->stride;
     if (power_w)
-        PALS_CUDA(cudaMemcpy(power_w, A->d_sp + o, sizeof(double) * *n_steps,
+        PALS_CUDA(copy_on(A->ctx->stream, power_w, A->d_sp + o, sizeof(double) * *n_steps,
                              cudaMemcpyDeviceToHost));
     if (throughput_tps)
-        PALS_CUDA(cudaMemcpy(throughput_tps, A->d_st + o, sizeof(double) * *n_steps,
+        PALS_CUDA(copy_on(A->ctx->stream, throughput_tps, A->d_st + o, sizeof(double) * *n_steps,
                              cudaMemcpyDeviceToHost));
     return PALS_OK;
 }

@@ -246,13 +246,13 @@ static int grid_finish(pals_ctx* ctx, pals_grid* g) {
     PALS_CUDA(cudaMalloc(&g->inv_tr, nb * sizeof(int)));
     PALS_CUDA(cudaMalloc(&g->canon, nb * sizeof(int)));
     if (n > 0) {
-        PALS_CUDA(cudaMemcpy(g->cap, cap.data(), n * sizeof(double), cudaMemcpyHostToDevice));
-        PALS_CUDA(cudaMemcpy(g->batch, b.data(), n * sizeof(int), cudaMemcpyHostToDevice));
-        PALS_CUDA(cudaMemcpy(g->tp, tp.data(), n * sizeof(int), cudaMemcpyHostToDevice));
-        PALS_CUDA(cudaMemcpy(g->ep, ep.data(), n * sizeof(int), cudaMemcpyHostToDevice));
-        PALS_CUDA(cudaMemcpy(g->dp, dp.data(), n * sizeof(int), cudaMemcpyHostToDevice));
-        PALS_CUDA(cudaMemcpy(g->inv_tr, order.data(), n * sizeof(int), cudaMemcpyHostToDevice));
-        PALS_CUDA(cudaMemcpy(g->canon, g->h_canon, n * sizeof(int), cudaMemcpyHostToDevice));
+        PALS_CUDA(copy_on(ctx->stream, g->cap, cap.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+        PALS_CUDA(copy_on(ctx->stream, g->batch, b.data(), n * sizeof(int), cudaMemcpyHostToDevice));
+        PALS_CUDA(copy_on(ctx->stream, g->tp, tp.data(), n * sizeof(int), cudaMemcpyHostToDevice));
+        PALS_CUDA(copy_on(ctx->stream, g->ep, ep.data(), n * sizeof(int), cudaMemcpyHostToDevice));
+        PALS_CUDA(copy_on(ctx->stream, g->dp, dp.data(), n * sizeof(int), cudaMemcpyHostToDevice));
+        PALS_CUDA(copy_on(ctx->stream, g->inv_tr, order.data(), n * sizeof(int), cudaMemcpyHostToDevice));
+        PALS_CUDA(copy_on(ctx->stream, g->canon, g->h_canon, n * sizeof(int), cudaMemcpyHostToDevice));
     }
     return PALS_OK;
 }

@@ -336,7 +336,7 @@ extern "C" int pals_model_forest(pals_ctx* ctx, int32_t n_models, int32_t model_
     char* s = (char*)fh->slab;
     auto put = [&](const void* src, size_t b) {
         void* dst = s;
-        if (b) cudaMemcpy(dst, src, b, cudaMemcpyHostToDevice);
+        if (b) copy_on(ctx->stream, dst, src, b, cudaMemcpyHostToDevice);
         s += (b + 255) & ~(size_t)255;
         return dst;
     };

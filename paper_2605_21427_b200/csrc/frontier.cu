@@ -238,7 +238,7 @@ int pals_plan_frontier(pals_plan* p, int32_t* idx, int64_t* n_out) {
         cudaError_t e = cudaMemcpyAsync(n_out, d_n, 8, cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         if (e == cudaSuccess && *n_out > 0)
-            e = cudaMemcpy(idx, d_idx, 4 * (size_t)*n_out, cudaMemcpyDeviceToHost);
+            e = copy_on(s, idx, d_idx, 4 * (size_t)*n_out, cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) rc = cuda_fail(e, "pals_plan_frontier");
     }
     cudaFree(d_idx);
@@ -260,8 +260,8 @@ int pals_frontier_values(pals_ctx* ctx, const pals_point* points, const double* 
         return rc;
     }
     const PlanDev& d = plan_dev(p);
-    cudaError_t e = cudaMemcpy(d.T, throughput_tps, 8 * (size_t)n, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(d.P, efficiency_tpj, 8 * (size_t)n, cudaMemcpyHostToDevice);
+    cudaError_t e = copy_on(ctx->stream, d.T, throughput_tps, 8 * (size_t)n, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = copy_on(ctx->stream, d.P, efficiency_tpj, 8 * (size_t)n, cudaMemcpyHostToDevice);
     rc = e == cudaSuccess ? pals_plan_frontier(p, idx, n_out) : cuda_fail(e, "pals_frontier_values");
     pals_plan_destroy(p);
     pals_grid_destroy(g);

@@ -213,6 +213,16 @@ struct pals_ctx {
     size_t front_bytes = 0;
 };
 
+// Blocking copy ordered on a context stream. A plain cudaMemcpy runs on the legacy
+// default stream, which does not order against non-blocking streams (torch's, or
+// the context's own), and a pageable H2D may return before its DMA has landed — so
+// a kernel queued next on the context stream could read stale bytes.
+inline cudaError_t copy_on(cudaStream_t s, void* dst, const void* src, size_t n,
+                           cudaMemcpyKind kind) {
+    const cudaError_t e = cudaMemcpyAsync(dst, src, n, kind, s);
+    return e == cudaSuccess ? cudaStreamSynchronize(s) : e;
+}
+
 enum ModelKind { MODEL_ANALYTIC = 0, MODEL_TABLE = 1, MODEL_FOREST = 2 };
 
 struct pals_model {

@@ -1105,7 +1105,7 @@ static int plan_build(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
     d.globals = (int32_t*)take(16);
     // globals[2] (the generic-score flag) only ever gets set, and a plan's scores are
     // the same every prepare, so it is zeroed once here instead of every step
-    PALS_CUDA(cudaMemset(d.globals, 0, 16));
+    PALS_CUDA(cudaMemsetAsync(d.globals, 0, 16, ctx->stream));
     p->gk = (uint64_t*)take(32);  // [2] global candidate keys + k_assign's done counter
     p->d_an = (Analytic*)take(sizeof(Analytic));
     // TR per point (inverse of grid inv_tr), computed once on the host at grid creation
@@ -1113,13 +1113,13 @@ static int plan_build(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
     {
         std::vector<int> inv(g->n), tr(g->n);
         if (g->n) {
-            PALS_CUDA(cudaMemcpy(inv.data(), g->inv_tr, g->n * sizeof(int), cudaMemcpyDeviceToHost));
+            PALS_CUDA(copy_on(ctx->stream, inv.data(), g->inv_tr, g->n * sizeof(int), cudaMemcpyDeviceToHost));
             for (int64_t r = 0; r < g->n; ++r) tr[inv[r]] = (int)r;
-            PALS_CUDA(cudaMemcpy(p->tr, tr.data(), g->n * sizeof(int), cudaMemcpyHostToDevice));
+            PALS_CUDA(copy_on(ctx->stream, p->tr, tr.data(), g->n * sizeof(int), cudaMemcpyHostToDevice));
         }
     }
     if (m && m->kind == MODEL_ANALYTIC)
-        PALS_CUDA(cudaMemcpy(p->d_an, &m->an, sizeof(Analytic), cudaMemcpyHostToDevice));
+        PALS_CUDA(copy_on(ctx->stream, p->d_an, &m->an, sizeof(Analytic), cudaMemcpyHostToDevice));
     if (m && m->kind == MODEL_TABLE) {
         p->table_map = (int*)take(4 * (size_t)n);
         const int64_t tn = std::max<int64_t>(1, m->table_n);
@@ -1140,10 +1140,10 @@ static int plan_build(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
             map[i] = it == first.end() ? 0 : it->second;
         }
         if (g->n)
-            PALS_CUDA(cudaMemcpy(p->table_map, map.data(), g->n * 4, cudaMemcpyHostToDevice));
+            PALS_CUDA(copy_on(ctx->stream, p->table_map, map.data(), g->n * 4, cudaMemcpyHostToDevice));
         if (m->table_n) {
-            PALS_CUDA(cudaMemcpy(p->table_T, m->table_T, m->table_n * 8, cudaMemcpyHostToDevice));
-            PALS_CUDA(cudaMemcpy(p->table_P, m->table_P, m->table_n * 8, cudaMemcpyHostToDevice));
+            PALS_CUDA(copy_on(ctx->stream, p->table_T, m->table_T, m->table_n * 8, cudaMemcpyHostToDevice));
+            PALS_CUDA(copy_on(ctx->stream, p->table_P, m->table_P, m->table_n * 8, cudaMemcpyHostToDevice));
         }
     }
     *out = p;
@@ -1503,7 +1503,7 @@ int pals_eval_device(pals_ctx* ctx, const pals_model* m, const pals_grid* g, dou
     if (!m->d_an) {
         auto* mm = const_cast<pals_model*>(m);
         PALS_CUDA(cudaMalloc(&mm->d_an, sizeof(Analytic)));
-        PALS_CUDA(cudaMemcpy(mm->d_an, &m->an, sizeof(Analytic), cudaMemcpyHostToDevice));
+        PALS_CUDA(copy_on(ctx->stream, mm->d_an, &m->an, sizeof(Analytic), cudaMemcpyHostToDevice));
     }
     k_eval_analytic_raw<<<grid_blocks(ctx, g->n, 256), 256, 0, ctx->stream>>>(
         m->d_an, g->n, g->cap, g->batch, g->tp, g->dp, d_T, d_P);

@@ -483,6 +483,7 @@ struct ReplayCache {
 void replay_cache_free(pals_ctx* ctx) {
     auto* rc = (ReplayCache*)ctx->replay_cache;
     if (!rc) return;
+    cudaStreamSynchronize(ctx->stream);  // a replay queued on the stream may still read the tables
     for (auto* p : rc->plans) pals_plan_destroy(p);
     for (auto* g : rc->grids) pals_grid_destroy(g);
     for (auto* m : rc->plant_models) pals_model_destroy(m);
@@ -560,7 +561,7 @@ static int replay_setup(pals_ctx* ctx, int n_models, pals_model* const* models,
         int r = pals_model_analytic(ctx, &plant[i], gpu, &pm);
         if (r) return r;
         rc->plant_models.push_back(pm);
-        PALS_CUDA(cudaMemcpy(rc->d_plant + i, &pm->an, sizeof(Analytic), cudaMemcpyHostToDevice));
+        PALS_CUDA(copy_on(ctx->stream, rc->d_plant + i, &pm->an, sizeof(Analytic), cudaMemcpyHostToDevice));
         // build_candidates order (sim.hpp:304-306) at the deployment degrees
         pals_grid* g = nullptr;
         const int tp = plant[i].deploy_tp, ep = plant[i].deploy_ep, dp = plant[i].deploy_dp;
@@ -617,9 +618,9 @@ static int replay_setup(pals_ctx* ctx, int n_models, pals_model* const* models,
         m.walk_c = (const double*)wbase;
         m.walk_T = (const double*)(wbase + (size_t)nc * L * 8);
         m.walk_pn = (const double*)(wbase + (size_t)nc * L * 8 + (size_t)n * L * 8);
-        PALS_CUDA(cudaMemcpy((void*)m.walk_c, walk_c.data(), walk_c.size() * 8,
+        PALS_CUDA(copy_on(ctx->stream, (void*)m.walk_c, walk_c.data(), walk_c.size() * 8,
                              cudaMemcpyHostToDevice));
-        PALS_CUDA(cudaMemcpy(rc->d_models + i, &m, sizeof m, cudaMemcpyHostToDevice));
+        PALS_CUDA(copy_on(ctx->stream, rc->d_models + i, &m, sizeof m, cudaMemcpyHostToDevice));
         k_build_tables<<<1, 1024, 0, ctx->stream>>>(d, rc->d_models + i, (uint32_t*)m.m2,
                                                      (uint32_t*)m.b1, (double*)m.ut, (double*)m.up,
                                                      coeffs->alpha, coeffs->beta_watts);
@@ -963,7 +964,7 @@ static int one_call(pals_ctx* ctx, const pals_model* m, const pals_point* cands,
         if (!m->d_an) {  // device copy of the profile, made once per model
             auto* mm = const_cast<pals_model*>(m);
             PALS_CUDA(cudaMalloc(&mm->d_an, sizeof(Analytic)));
-            PALS_CUDA(cudaMemcpy(mm->d_an, &m->an, sizeof(Analytic), cudaMemcpyHostToDevice));
+            PALS_CUDA(copy_on(ctx->stream, mm->d_an, &m->an, sizeof(Analytic), cudaMemcpyHostToDevice));
         }
         d_an = m->d_an;
     }

@@ -378,6 +378,9 @@ def run_ours(args, dist: Dist):
         re2e.append(a.elapsed_time(b))
     re2e_max = dist.max(float(np.mean(re2e)))
     dec_e2e = dist.sum(float(nt) * args.trace_steps) / (re2e_max * 1e-3)
+    # the same cfg4 traces through the warp-per-trace layout, and both layouts on the
+    # demand-response scenario's 1,464-candidate grid (SURVEY §8(d) cfg4 variants)
+    layouts = replay_layouts(args, dist, ctx, stream, l2_flush, models, s, spec, dec_value)
     # FP64 work per decision in the replay kernel: PID 15 flops (2 div),
     # plant noise/min/energy/tokens 10, target test + Kt search ~2*log2(nd_t)+4
     fp64_per_dec = 40.0
@@ -494,7 +497,7 @@ def run_ours(args, dist: Dist):
             "e2e": {"value": dec_e2e, "unit": "decisions/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": nt * SUMMARY_DT.itemsize,
                     "api": "pals_replay (C ABI, host summaries)"},
-            "roofline": dec_roof, "gpu_launches": int(rlaunches)},
+            "roofline": dec_roof, "gpu_launches": int(rlaunches), "layouts": layouts},
         "predictions": predictions,
         "allocations": allocations,
         "frontiers": frontiers,
@@ -516,6 +519,49 @@ def run_ours(args, dist: Dist):
     if dist.rank == 0:
         print(json.dumps(out), flush=True)
     dist.close()
+
+
+def replay_layouts(args, dist, ctx, stream, l2_flush, models, s, spec, thread_value):
+    """decisions/s of the cfg4 replay per kernel layout (thread / warp per trace) and on
+    the 1,464-candidate DR grid; same traces, identical results (tests/)."""
+    import torch
+    from paper_2605_21427_b200 import workloads
+    from paper_2605_21427_b200.abi import SUMMARY_DT
+    from paper_2605_21427_b200.wattserve import replay_device
+
+    def timed(caps, batches, sp, layout, reps):
+        ctx.set_replay_layout(layout)
+        d = torch.empty(sp.n_traces * SUMMARY_DT.itemsize, dtype=torch.uint8, device="cuda")
+        run = lambda: replay_device(ctx, models, s["profiles"], s["gpu"], s["coeffs"],  # noqa
+                                    caps, batches, s["cfg"], sp, d.data_ptr())
+        run()
+        torch.cuda.synchronize()
+        dist.barrier()
+        ms = 0.0
+        for _ in range(reps):
+            l2_flush()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            run()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms += a.elapsed_time(b)
+        ctx.set_replay_layout("thread")
+        t = dist.max(ms)
+        return dist.sum(float(sp.n_traces) * sp.n_steps) * reps / (t * 1e-3)
+
+    out = {"cfg4_thread_per_trace": thread_value,
+           "cfg4_warp_per_trace": timed(s["caps"], s["batches"], spec, "warp", 2)}
+    caps, batches = workloads.dr_candidates()
+    nt = max(1, args.traces // 4)
+    dspec = workloads.replay_spec(nt, n_steps=args.trace_steps, seed=2605,
+                                  first=dist.rank * nt)
+    out["dr_grid_workload"] = (f"{nt} traces per GPU x {args.trace_steps} steps on the "
+                               f"demand-response grid: 61 caps x 24 batches = 1,464 candidates")
+    out["dr_thread_per_trace"] = timed(caps, batches, dspec, "thread", 2)
+    out["dr_warp_per_trace"] = timed(caps, batches, dspec, "warp", 1)
+    out["unit"] = "decisions/s"
+    return out
 
 
 def alloc_setup_gpu(ctx):

@@ -230,6 +230,13 @@ void* pals_ctx_stream(pals_ctx* ctx);
 int pals_ctx_sync(pals_ctx* ctx);
 /* Number of kernels this context has launched so far. */
 int64_t pals_ctx_launch_count(pals_ctx* ctx);
+/* Replay kernel layout for pals_replay / pals_replay_device: PALS_REPLAY_THREAD
+ * (default: one thread per trace, warps made objective-uniform) or PALS_REPLAY_WARP
+ * (one warp per trace, the layout BASELINE cfg4 names; lanes split the noise draws,
+ * the feasibility searches and the enforce_cap walk). Results are identical. */
+#define PALS_REPLAY_THREAD 0
+#define PALS_REPLAY_WARP 1
+int pals_ctx_set_replay_layout(pals_ctx* ctx, int32_t layout);
 
 /* ---- models (the three concrete Scorer kinds) ------------------------- */
 /* analytic_scorer(profile, gpu): validates like ModelProfile::validate (types.hpp:88-106) */

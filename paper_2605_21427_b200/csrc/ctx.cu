@@ -138,6 +138,14 @@ int pals_ctx_sync(pals_ctx* c) {
 
 int64_t pals_ctx_launch_count(pals_ctx* c) { return c->launches; }
 
+int pals_ctx_set_replay_layout(pals_ctx* c, int32_t layout) {
+    if (!c) return set_error(PALS_ECONFIG, "pals_ctx_set_replay_layout: null context");
+    if (layout != PALS_REPLAY_THREAD && layout != PALS_REPLAY_WARP)
+        return set_error(PALS_ECONFIG, "pals_ctx_set_replay_layout: unknown layout");
+    c->replay_layout = layout;
+    return PALS_OK;
+}
+
 int pals_model_analytic(pals_ctx* ctx, const pals_profile* prof, const pals_gpu_spec* gpu,
                         pals_model** out) {
     if (!prof || !gpu) return set_error(PALS_ECONFIG, "pals_model_analytic: null argument");

@@ -209,6 +209,7 @@ struct pals_ctx {
     void* h_pinned = nullptr;
     size_t pinned_bytes = 0;
     void* replay_cache = nullptr;  // replay.cu
+    int replay_layout = 0;         // PALS_REPLAY_THREAD / PALS_REPLAY_WARP
     void* d_front = nullptr;       // frontier.cu scratch
     size_t front_bytes = 0;
 };

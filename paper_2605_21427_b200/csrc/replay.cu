@@ -219,15 +219,40 @@ __global__ void k_replay_order(pals_replay_spec sp, int32_t* __restrict__ order,
     }
 }
 
+// Number of leading indices i in [0, n) with pred(i) true, for a predicate that is
+// true on a prefix (sorted tables): 32-ary narrowing by one warp, ceil(log32 n)
+// rounds of one load per lane instead of log2 n dependent loads. Same count as
+// the binary searches of the thread layout.
+template <class Pred>
+__device__ __forceinline__ int warp_leading_true(int n, Pred pred) {
+    const int lane = threadIdx.x & 31;
+    int lo = 0, hi = n;  // the count lies in [lo, hi]
+    while (lo < hi) {
+        const int step = (hi - lo + 31) >> 5;
+        const int i = lo + (lane + 1) * step - 1;
+        const unsigned b = __ballot_sync(0xffffffffu, i < hi && pred(i));
+        const int nlo = lo + __popc(b) * step;
+        hi = min(hi, nlo + step - 1);
+        lo = nlo;
+    }
+    return lo;
+}
+
 // kMinBlocks trades registers for occupancy (1: ~126 regs, 4 CTAs/SM; 6: 80 regs).
-template <int kMinBlocks>
+// kWarp: one warp per trace (BASELINE cfg4's named layout). The control loop is the
+// same scalar code, run redundantly by the 32 lanes; the lanes split what is
+// parallel inside a step: the per-step noise draws (32 steps per round), the Kt /
+// Kp searches (32-ary) and the enforce_cap walk (32 positions per round).
+template <int kMinBlocks, bool kWarp>
 __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev* __restrict__ models,
                                                 ReplayParams p, const int32_t* __restrict__ order,
                                                 pals_trace_summary* __restrict__ out,
                                                 pals_step_log* __restrict__ logs) {
-    const int64_t slot = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t slot = kWarp ? gt >> 5 : gt;
+    const int lane = threadIdx.x & 31;
     const pals_replay_spec& sp = p.spec;
-    if (slot >= sp.n_traces) return;
+    if (slot >= sp.n_traces) return;  // warp-uniform in the warp layout
     const int64_t ti = order ? order[slot] : slot;
     const pals_ctrl_cfg& cfg = p.cfg;
     const uint64_t key = splitmix64(sp.seed ^ (uint64_t)(sp.first_trace + ti));
@@ -260,7 +285,9 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
     uint64_t h = 0xcbf29ce484222325ULL;
     double energy = 0.0, tokens = 0.0;
     int n_applied = 0;
-    pals_step_log* lg = (logs && ti < sp.n_log_traces) ? logs + ti * (int64_t)sp.n_steps : nullptr;
+    pals_step_log* lg = (logs && ti < sp.n_log_traces && (!kWarp || lane == 0))
+                            ? logs + ti * (int64_t)sp.n_steps : nullptr;
+    double noise_lane = 1.0;  // warp layout: noise of step (k & ~31) + lane
 
     for (int k = 0; k < sp.n_steps; ++k) {
         const double t0 = (double)k * sp.interval_s;
@@ -274,7 +301,20 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
             const int64_t wo = ((int64_t)applied_a * m.nb + batch_b) * m.L;
             int j = 0;
             if (node_budget > 0.0) {
-                while (wc[j] > m.plant_min_cap && !(m.walk_pn[wo + j] <= node_budget)) ++j;
+                if (kWarp) {  // first walk position that stops the loop, 32 per round
+                    for (int base = 0;; base += 32) {
+                        const int q = base + lane;
+                        const bool stop = q < m.L && (!(wc[q] > m.plant_min_cap) ||
+                                                      m.walk_pn[wo + q] <= node_budget);
+                        const unsigned b = __ballot_sync(0xffffffffu, stop);
+                        if (b) {
+                            j = base + __ffs(b) - 1;
+                            break;
+                        }
+                    }
+                } else {
+                    while (wc[j] > m.plant_min_cap && !(m.walk_pn[wo + j] <= node_budget)) ++j;
+                }
             }
             cap = wc[j];
             capacity = (double)m.dp * m.walk_T[wo + j];
@@ -284,7 +324,14 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
             c_nb = node_budget;
         }
         const double offered = ls.at(k, sp.seg_min, sp.seg_max);
-        const double noise = 1.0 + sp.noise_amp * (2.0 * u01(draw(key, 3, (uint64_t)k)) - 1.0);
+        double noise;
+        if (kWarp) {
+            if ((k & 31) == 0 && k + lane < sp.n_steps)
+                noise_lane = 1.0 + sp.noise_amp * (2.0 * u01(draw(key, 3, (uint64_t)(k + lane))) - 1.0);
+            noise = __shfl_sync(0xffffffffu, noise_lane, k & 31);
+        } else {
+            noise = 1.0 + sp.noise_amp * (2.0 * u01(draw(key, 3, (uint64_t)k)) - 1.0);
+        }
         const double measured = smin(offered, capacity) * noise;
         energy += sys_w * sp.interval_s;
         tokens += measured * sp.interval_s;
@@ -321,17 +368,31 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
 
             const double budget = bset ? node_budget * (1.0 - cfg.budget_margin) : 0.0;
             if (bset && budget != kp_budget) {
-                int lo = 0, hi = m.nd_p;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (m.up[mid] <= budget) lo = mid + 1;
-                    else hi = mid;
+                if (kWarp) {
+                    kp = warp_leading_true(m.nd_p, [&](int i) { return m.up[i] <= budget; });
+                } else {
+                    int lo = 0, hi = m.nd_p;
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (m.up[mid] <= budget) lo = mid + 1;
+                        else hi = mid;
+                    }
+                    kp = lo;
                 }
-                kp = lo;
                 kp_budget = budget;
             }
             int s_idx, s_reason;
-            if (obj == PALS_OBJ_QOS) kt = count_t_feasible(m, bias, target, kt);
+            if (obj == PALS_OBJ_QOS) {
+                if (kWarp) {
+                    const bool ok_lo = kt == 0 || !(m.ut[kt - 1] * bias < target);
+                    const bool ok_hi = kt == m.nd_t || (m.ut[kt] * bias < target);
+                    if (!(ok_lo && ok_hi))
+                        kt = warp_leading_true(m.nd_t,
+                                               [&](int i) { return !(m.ut[i] * bias < target); });
+                } else {
+                    kt = count_t_feasible(m, bias, target, kt);
+                }
+            }
             table_select(m, target, bset, budget, kp, kt, bias, obj, &s_idx, &s_reason);
             const bool may_apply = changed || sustain >= cfg.sustain_intervals;
             const int sc = s_idx;  // canonical (first equal point)
@@ -369,6 +430,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
     }
     h = (h ^ (uint64_t)__double_as_longlong(bias)) * 0x100000001b3ULL;
     h = (h ^ (uint64_t)(uint32_t)cur) * 0x100000001b3ULL;
+    if (kWarp && lane != 0) return;
     pals_trace_summary s;
     s.digest = h;
     s.final_bias = bias;
@@ -650,7 +712,7 @@ static int replay_launch(pals_ctx* ctx, ReplayCache* rc, const pals_ctrl_cfg* cf
     p.n_models = (int)rc->models.size();
     const int64_t blocks = (spec->n_traces + 127) / 128;
     int32_t* order = nullptr;
-    if (spec->objective_mode == 2) {
+    if (spec->objective_mode == 2 && ctx->replay_layout != PALS_REPLAY_WARP) {
         if (rc->order_cap < spec->n_traces) {
             cudaFree(rc->d_order);
             rc->d_order = nullptr;
@@ -668,12 +730,16 @@ static int replay_launch(pals_ctx* ctx, ReplayCache* rc, const pals_ctrl_cfg* cf
         const char* e = getenv("PALS_REPLAY_MINB");
         return e ? atoi(e) : 6;  // measured: 6 CTAs/SM (80 regs) beats 4 (126 regs) by 1.4x
     }();
-    if (minb >= 8)
-        k_replay<8><<<(unsigned)blocks, 128, 0, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs);
+    if (ctx->replay_layout == PALS_REPLAY_WARP) {
+        const int64_t wblocks = (spec->n_traces + 3) / 4;  // 4 traces (warps) per CTA
+        k_replay<6, true><<<(unsigned)wblocks, 128, 0, ctx->stream>>>(rc->d_models, p, nullptr,
+                                                                     d_sum, d_logs);
+    } else if (minb >= 8)
+        k_replay<8, false><<<(unsigned)blocks, 128, 0, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs);
     else if (minb >= 6)
-        k_replay<6><<<(unsigned)blocks, 128, 0, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs);
+        k_replay<6, false><<<(unsigned)blocks, 128, 0, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs);
     else
-        k_replay<1><<<(unsigned)blocks, 128, 0, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs);
+        k_replay<1, false><<<(unsigned)blocks, 128, 0, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs);
     count_launch(ctx);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "k_replay");

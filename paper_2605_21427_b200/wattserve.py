@@ -64,6 +64,10 @@ class Context:
     def sync(self):
         check(self.lib.pals_ctx_sync(self.h))
 
+    def set_replay_layout(self, layout: str):
+        """"thread" (one thread per trace, default) or "warp" (one warp per trace)."""
+        check(self.lib.pals_ctx_set_replay_layout(self.h, {"thread": 0, "warp": 1}[layout]))
+
     @property
     def launches(self) -> int:
         return int(self.lib.pals_ctx_launch_count(self.h))

@@ -212,6 +212,14 @@ typedef struct {
     uint16_t cap_tenths; /* enforced cap * 10 after the breaker walk */
 } pals_step_log;
 
+/* Per-step decision detail (sim.hpp:122-129 DecisionRecord fields not in
+ * pals_step_log): err_norm = (target - measured) / target (sim.hpp:438-440, any
+ * objective; 0 without a target) and the controller bias after the step (:463). */
+typedef struct {
+    double err_norm;
+    double bias;
+} pals_step_detail;
+
 typedef struct pals_ctx pals_ctx;
 typedef struct pals_model pals_model;
 typedef struct pals_grid pals_grid;
@@ -354,6 +362,39 @@ int pals_replay_device(pals_ctx* ctx, int32_t n_models, pals_model* const* model
                        const int32_t* batches, int32_t n_batches, const pals_ctrl_cfg* cfg,
                        const pals_replay_spec* spec, pals_trace_summary* d_summaries,
                        pals_step_log* d_logs);
+
+/* pals_replay / pals_replay_device plus per-step details (err_norm, bias) for the
+ * logged traces (NULL: none). Host or device buffers as the base call. */
+int pals_replay_ex(pals_ctx* ctx, int32_t n_models, pals_model* const* models,
+                   const pals_profile* plant, const pals_gpu_spec* gpu, const pals_coeffs* coeffs,
+                   const double* caps, int32_t n_caps, const int32_t* batches, int32_t n_batches,
+                   const pals_ctrl_cfg* cfg, const pals_replay_spec* spec,
+                   pals_trace_summary* summaries, pals_step_log* logs,
+                   pals_step_detail* details);
+int pals_replay_device_ex(pals_ctx* ctx, int32_t n_models, pals_model* const* models,
+                          const pals_profile* plant, const pals_gpu_spec* gpu,
+                          const pals_coeffs* coeffs, const double* caps, int32_t n_caps,
+                          const int32_t* batches, int32_t n_batches, const pals_ctrl_cfg* cfg,
+                          const pals_replay_spec* spec, pals_trace_summary* d_summaries,
+                          pals_step_log* d_logs, pals_step_detail* d_details);
+
+/* ---- decision-log wire format (metrics.hpp:145-157, csvio.hpp:17-21) -- */
+/* decisions_csv over the logged traces of a replay (host buffers from pals_replay_ex):
+ * header "node,model,t_s,cap_w,batch,tp,ep,dp,applied,reason,err_norm,bias", then one
+ * row per (trace, step): node = spec->first_trace + i, model = plant[summary.model].name,
+ * t_s = (k + 1) * interval_s, point = candidate idx of caps x batches (build_candidates
+ * order, sim.hpp:304-306) at the model's deployment tp/ep/dp, reason strings of
+ * controller.hpp:72-82, doubles as "%.10g" — byte-identical to the reference writer.
+ * Writes min(length, buf_size) bytes (no terminator) and the full length to *out_len;
+ * buf may be NULL to size the output. */
+int pals_decisions_csv(const pals_replay_spec* spec, const pals_profile* plant, int32_t n_models,
+                       const double* caps, int32_t n_caps, const int32_t* batches,
+                       int32_t n_batches, const pals_trace_summary* summaries,
+                       const pals_step_log* logs, const pals_step_detail* details, char* buf,
+                       int64_t buf_size, int64_t* out_len);
+/* fnv1a64 (rng.hpp:22-28): the hash the reference's run manifests record per output
+ * file (commands.hpp:26-39, csvio.hpp:69-71). */
+uint64_t pals_fnv1a64(const void* data, int64_t n);
 
 /* ---- Pareto frontier (pareto.hpp:31-59) ------------------------------- */
 /* build_frontier over the plan's points scored as FrontierPoint{point,

@@ -309,6 +309,29 @@ def gen_replay(ref: Reference) -> None:
                         logs_q=logs_q)
 
 
+DECISION_SPECS = {  # name -> replay_spec kwargs of the decisions-CSV fixtures
+    "mixed": dict(n_traces=24, n_steps=240, seed=2605, n_log_traces=12),
+    "qos": dict(n_traces=8, n_steps=300, seed=77, objective_mode=0, n_log_traces=8),
+    "dr": dict(n_traces=6, n_steps=200, seed=515, n_log_traces=6),
+}
+
+
+def gen_decisions(ref: Reference) -> None:
+    """decisions_csv (metrics.hpp:145-157) produced by the reference's own writer over
+    fluid-plant replays through the unmodified control_step, plus its fnv1a64."""
+    s = workloads.cfg4_setup()
+    out = {}
+    for name, kw in DECISION_SPECS.items():
+        spec = workloads.replay_spec(**kw)
+        caps, batches = (workloads.dr_candidates() if name == "dr"
+                         else (s["caps"], s["batches"]))
+        csv, h = ref.replay_decisions_csv(s["profiles"], s["gpu"], s["coeffs"], caps, batches,
+                                          s["cfg"], spec)
+        out[name] = np.frombuffer(csv, np.uint8)
+        out[name + "_fnv"] = np.array([h], np.uint64)
+    np.savez_compressed(os.path.join(GOLD, "decisions.npz"), **out)
+
+
 def forest_points(n, seed):
     rng = np.random.default_rng(seed)
     pts = np.zeros(n, POINT_DT)
@@ -356,6 +379,10 @@ def gen_forest(ref: Reference) -> None:
 def main():
     os.makedirs(GOLD, exist_ok=True)
     ref = Reference()
+    if len(sys.argv) > 1:  # regenerate only the named fixtures, e.g. "decisions"
+        for name in sys.argv[1:]:
+            globals()["gen_" + name](ref)
+        return
     write_profiles(ref)
     gen_eval(ref)
     gen_select(ref)
@@ -363,6 +390,7 @@ def main():
     gen_control(ref)
     gen_replay(ref)
     gen_forest(ref)
+    gen_decisions(ref)
     print("fixtures written to", GOLD)
 
 

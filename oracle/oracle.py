@@ -16,7 +16,8 @@ import subprocess
 
 import numpy as np
 
-from paper_2605_21427_b200.abi import (POINT_DT, QUERY_DT, STEPLOG_DT, SUMMARY_DT, Coeffs,
+from paper_2605_21427_b200.abi import (POINT_DT, QUERY_DT, STEPDETAIL_DT, STEPLOG_DT,
+                                       SUMMARY_DT, Coeffs,
                                        CtrlCfg, CtrlState, Decision, GpuSpec, Profile,
                                        ReplaySpec, Targets, Telemetry, ptr)
 
@@ -115,6 +116,25 @@ class Oracle:
         if rc:
             raise RuntimeError(f"or_replay rc={rc}")
         return summ, logs[: spec.n_log_traces * spec.n_steps]
+
+    def replay_ex(self, plant, gpu, coeffs, caps, batches, cfg: CtrlCfg, spec: ReplaySpec):
+        """replay() plus the per-step (err_norm, bias) of the logged traces."""
+        L = self.lib
+        L.or_replay_ex.argtypes = [C.c_int, _VP, _VP, _VP, _VP, C.c_int, _VP, C.c_int, _VP,
+                                   _VP, _VP, _VP, _VP]
+        profs = (Profile * len(plant))(*plant)
+        caps = np.ascontiguousarray(caps, np.float64)
+        batches = np.ascontiguousarray(batches, np.int32)
+        summ = np.zeros(spec.n_traces, SUMMARY_DT)
+        nl = spec.n_log_traces * spec.n_steps
+        logs = np.zeros(max(1, nl), STEPLOG_DT)
+        det = np.zeros(max(1, nl), STEPDETAIL_DT)
+        rc = L.or_replay_ex(len(plant), profs, C.byref(gpu), C.byref(coeffs), ptr(caps),
+                            len(caps), ptr(batches), len(batches), C.byref(cfg), C.byref(spec),
+                            ptr(summ), ptr(logs), ptr(det))
+        if rc:
+            raise RuntimeError(f"or_replay_ex rc={rc}")
+        return summ, logs[:nl], det[:nl]
 
     def replay_scored(self, plant, gpu, coeffs, caps, batches, cfg: CtrlCfg, spec: ReplaySpec,
                       scorer_T: np.ndarray, scorer_P: np.ndarray):
@@ -240,6 +260,26 @@ class Reference:
         if rc:
             raise RuntimeError(f"ref_replay rc={rc}: {self.last_error()}")
         return summ, logs[: spec.n_log_traces * spec.n_steps]
+
+    def replay_decisions_csv(self, plant, gpu, coeffs, caps, batches, cfg, spec):
+        """The reference's decisions_csv (metrics.hpp:145-157) of the logged traces of a
+        fluid-plant replay driven through the unmodified control_step: (bytes, fnv1a64)."""
+        L = self.lib
+        L.ref_replay_decisions_csv.argtypes = [C.c_int, _VP, _VP, _VP, _VP, C.c_int, _VP,
+                                               C.c_int, _VP, _VP, _VP, C.c_int64, _VP, _VP]
+        profs = (Profile * len(plant))(*plant)
+        caps = np.ascontiguousarray(caps, np.float64)
+        batches = np.ascontiguousarray(batches, np.int32)
+        n = C.c_int64(0)
+        h = C.c_uint64(0)
+        args = [len(plant), profs, C.byref(gpu), C.byref(coeffs), ptr(caps), len(caps),
+                ptr(batches), len(batches), C.byref(cfg), C.byref(spec)]
+        rc = L.ref_replay_decisions_csv(*args, None, 0, C.byref(n), C.byref(h))
+        if rc:
+            raise RuntimeError(f"ref_replay_decisions_csv rc={rc}: {self.last_error()}")
+        buf = C.create_string_buffer(max(1, n.value))
+        L.ref_replay_decisions_csv(*args, buf, n.value, C.byref(n), C.byref(h))
+        return buf.raw[: n.value], int(h.value)
 
     def bench_select(self, prof, gpu, pts, coeffs, queries, threads, want_results=True):
         nq = len(queries)

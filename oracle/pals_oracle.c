@@ -289,25 +289,46 @@ static double enforce_cap(double cap, int batch, double node_budget, const pals_
  * (scorerT/scorerP[m * nc + i] = score(candidate i of model m)), e.g. a forest
  * predictor; the plant always runs the analytic profile. NULL tables: the
  * scorer is the analytic plant model itself (analytic_scorer). */
-int or_replay_scored(int n_models, const pals_profile* plant, const pals_gpu_spec* g,
-                     const pals_coeffs* k, const double* caps, int n_caps, const int* batches,
-                     int n_batches, const pals_ctrl_cfg* cfg, const pals_replay_spec* spec,
-                     const double* scorerT, const double* scorerP,
-                     pals_trace_summary* summaries, pals_step_log* logs);
-
-int or_replay(int n_models, const pals_profile* plant, const pals_gpu_spec* g,
-              const pals_coeffs* k, const double* caps, int n_caps, const int* batches,
-              int n_batches, const pals_ctrl_cfg* cfg, const pals_replay_spec* spec,
-              pals_trace_summary* summaries, pals_step_log* logs) {
-    return or_replay_scored(n_models, plant, g, k, caps, n_caps, batches, n_batches, cfg, spec,
-                            NULL, NULL, summaries, logs);
-}
+static int replay_impl(int n_models, const pals_profile* plant, const pals_gpu_spec* g,
+                       const pals_coeffs* k, const double* caps, int n_caps, const int* batches,
+                       int n_batches, const pals_ctrl_cfg* cfg, const pals_replay_spec* spec,
+                       const double* scorerT, const double* scorerP,
+                       pals_trace_summary* summaries, pals_step_log* logs,
+                       pals_step_detail* details);
 
 int or_replay_scored(int n_models, const pals_profile* plant, const pals_gpu_spec* g,
                      const pals_coeffs* k, const double* caps, int n_caps, const int* batches,
                      int n_batches, const pals_ctrl_cfg* cfg, const pals_replay_spec* spec,
                      const double* scorerT, const double* scorerP,
                      pals_trace_summary* summaries, pals_step_log* logs) {
+    return replay_impl(n_models, plant, g, k, caps, n_caps, batches, n_batches, cfg, spec,
+                       scorerT, scorerP, summaries, logs, NULL);
+}
+
+/* Also the per-step DecisionRecord err_norm / bias of the logged traces
+ * (sim.hpp:438-440, 457-464). */
+int or_replay_ex(int n_models, const pals_profile* plant, const pals_gpu_spec* g,
+                 const pals_coeffs* k, const double* caps, int n_caps, const int* batches,
+                 int n_batches, const pals_ctrl_cfg* cfg, const pals_replay_spec* spec,
+                 pals_trace_summary* summaries, pals_step_log* logs, pals_step_detail* details) {
+    return replay_impl(n_models, plant, g, k, caps, n_caps, batches, n_batches, cfg, spec, NULL,
+                       NULL, summaries, logs, details);
+}
+
+int or_replay(int n_models, const pals_profile* plant, const pals_gpu_spec* g,
+              const pals_coeffs* k, const double* caps, int n_caps, const int* batches,
+              int n_batches, const pals_ctrl_cfg* cfg, const pals_replay_spec* spec,
+              pals_trace_summary* summaries, pals_step_log* logs) {
+    return replay_impl(n_models, plant, g, k, caps, n_caps, batches, n_batches, cfg, spec, NULL,
+                       NULL, summaries, logs, NULL);
+}
+
+static int replay_impl(int n_models, const pals_profile* plant, const pals_gpu_spec* g,
+                       const pals_coeffs* k, const double* caps, int n_caps, const int* batches,
+                       int n_batches, const pals_ctrl_cfg* cfg, const pals_replay_spec* spec,
+                       const double* scorerT, const double* scorerP,
+                       pals_trace_summary* summaries, pals_step_log* logs,
+                       pals_step_detail* details) {
     const int nc = n_caps * n_batches;
     pals_point* cands = (pals_point*)malloc(sizeof(pals_point) * (size_t)nc * (size_t)n_models);
     double* T = (double*)malloc(sizeof(double) * (size_t)nc * (size_t)n_models);
@@ -420,6 +441,11 @@ int or_replay_scored(int n_models, const pals_profile* plant, const pals_gpu_spe
                 lg[s].applied = (uint8_t)(d.applied ? 1 : 0);
                 lg[s].reason = (uint8_t)d.reason;
                 lg[s].cap_tenths = (uint16_t)llround(cap * 10.0);
+                if (details) {
+                    pals_step_detail* x = details + ti * spec->n_steps + s;
+                    x->err_norm = target_tps > 0.0 ? (target_tps - measured) / target_tps : 0.0;
+                    x->bias = st.bias;
+                }
             }
             applied_cap = inflight_cap;
             if (d.applied) {

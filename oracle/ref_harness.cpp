@@ -18,6 +18,7 @@
 
 #include "wattserve/controller.hpp"
 #include "wattserve/forest.hpp"
+#include "wattserve/metrics.hpp"
 #include "wattserve/model.hpp"
 #include "wattserve/pareto.hpp"
 #include "wattserve/rng.hpp"
@@ -212,7 +213,7 @@ struct ReplayModel {
 void replay_one(const std::vector<ReplayModel>& models, const GpuSpec& gpu,
                 const SystemPowerCoeffs& coeffs, const ControllerConfig& cfg,
                 const pals_replay_spec& spec, std::int64_t gi, pals_trace_summary* summary,
-                pals_step_log* log) {
+                pals_step_log* log, std::vector<DecisionRecord>* recs = nullptr) {
     const std::uint64_t key = splitmix64(spec.seed ^ static_cast<std::uint64_t>(gi));
     const int m = static_cast<int>(key % models.size());
     const ReplayModel& rm = models[m];
@@ -286,6 +287,16 @@ void replay_one(const std::vector<ReplayModel>& models, const GpuSpec& gpu,
             log[k].applied = d.applied ? 1 : 0;
             log[k].reason = static_cast<std::uint8_t>(reason_code(d.reason));
             log[k].cap_tenths = static_cast<std::uint16_t>(std::llround(cap * 10.0));
+        }
+        if (recs) {  // the sim's DecisionRecord (sim.hpp:438-440, 457-464)
+            DecisionRecord dr;
+            dr.t_s = t1;
+            dr.point = d.point;
+            dr.applied = d.applied;
+            dr.reason = d.reason;
+            dr.err_norm = target_tps > 0.0 ? (target_tps - measured) / target_tps : 0.0;
+            dr.bias = st.bias;
+            recs->push_back(dr);
         }
         applied_cap = inflight_cap;
         if (d.applied) {
@@ -500,6 +511,38 @@ int ref_replay(int n_models, const pals_profile* plant, const pals_gpu_spec* gpu
                 (logs && i < spec->n_log_traces) ? logs + i * spec->n_steps : nullptr;
             replay_one(models, g, k, c, *spec, spec->first_trace + i, &summaries[i], lg);
         }
+    } catch (...) {
+        return map_exception();
+    }
+    return PALS_OK;
+}
+
+// decisions_csv (metrics.hpp:145-157, unmodified) over the first n_log_traces traces
+// of a fluid-plant replay, one SimResult node per trace; plus its fnv1a64.
+int ref_replay_decisions_csv(int n_models, const pals_profile* plant, const pals_gpu_spec* gpu,
+                             const pals_coeffs* coeffs, const double* caps, int n_caps,
+                             const int* batches, int n_batches, const pals_ctrl_cfg* cfg,
+                             const pals_replay_spec* spec, char* buf, std::int64_t buf_size,
+                             std::int64_t* out_len, std::uint64_t* fnv) {
+    try {
+        const GpuSpec g = to_gpu(*gpu);
+        const SystemPowerCoeffs k{coeffs->alpha, coeffs->beta_watts};
+        const auto models =
+            build_replay_models(n_models, plant, g, k, caps, n_caps, batches, n_batches, true);
+        const ControllerConfig c = to_cfg(*cfg);
+        const std::int64_t nl = std::min<std::int64_t>(spec->n_log_traces, spec->n_traces);
+        SimResult r;
+        r.nodes.resize(nl);
+        for (std::int64_t i = 0; i < nl; ++i) {
+            pals_trace_summary s;
+            replay_one(models, g, k, c, *spec, spec->first_trace + i, &s, nullptr,
+                       &r.nodes[i].decisions);
+            r.nodes[i].model_id = models[s.model].profile.name;
+        }
+        const std::string csv = decisions_csv(r);
+        *out_len = static_cast<std::int64_t>(csv.size());
+        *fnv = fnv1a64(csv);
+        if (buf) std::memcpy(buf, csv.data(), std::min<std::size_t>(csv.size(), buf_size));
     } catch (...) {
         return map_exception();
     }

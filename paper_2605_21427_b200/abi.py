@@ -139,7 +139,9 @@ STEPLOG_DT = np.dtype([("idx", "<i4"), ("applied", "u1"), ("reason", "u1"),
 
 assert C.sizeof(Point) == POINT_DT.itemsize == 24
 assert C.sizeof(Query) == QUERY_DT.itemsize == 48
-assert SUMMARY_DT.itemsize == 48 and STEPLOG_DT.itemsize == 8
+STEPDETAIL_DT = np.dtype([("err_norm", "<f8"), ("bias", "<f8")], align=True)
+
+assert SUMMARY_DT.itemsize == 48 and STEPLOG_DT.itemsize == 8 and STEPDETAIL_DT.itemsize == 16
 assert C.sizeof(Profile) == 272
 
 

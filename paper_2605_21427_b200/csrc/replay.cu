@@ -247,7 +247,8 @@ template <int kMinBlocks, bool kWarp>
 __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev* __restrict__ models,
                                                 ReplayParams p, const int32_t* __restrict__ order,
                                                 pals_trace_summary* __restrict__ out,
-                                                pals_step_log* __restrict__ logs) {
+                                                pals_step_log* __restrict__ logs,
+                                                pals_step_detail* __restrict__ details) {
     const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t slot = kWarp ? gt >> 5 : gt;
     const int lane = threadIdx.x & 31;
@@ -287,6 +288,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
     int n_applied = 0;
     pals_step_log* lg = (logs && ti < sp.n_log_traces && (!kWarp || lane == 0))
                             ? logs + ti * (int64_t)sp.n_steps : nullptr;
+    pals_step_detail* dt = (lg && details) ? details + ti * (int64_t)sp.n_steps : nullptr;
     double noise_lane = 1.0;  // warp layout: noise of step (k & ~31) + lane
 
     for (int k = 0; k < sp.n_steps; ++k) {
@@ -419,6 +421,12 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
             r.reason = (uint8_t)d_reason;
             r.cap_tenths = (uint16_t)llround(cap * 10.0);
             lg[k] = r;
+            if (dt) {  // DecisionRecord err_norm / bias (sim.hpp:438-440, 462-463)
+                pals_step_detail x;
+                x.err_norm = target_tps > 0.0 ? (target_tps - measured) / target_tps : 0.0;
+                x.bias = bias;
+                dt[k] = x;
+            }
         }
         // actuation (sim.hpp:466-472): batch next interval, cap one interval later;
         // candidate index = cap index * nb + batch index (build_candidates order)
@@ -700,7 +708,7 @@ static int replay_setup(pals_ctx* ctx, int n_models, pals_model* const* models,
 
 static int replay_launch(pals_ctx* ctx, ReplayCache* rc, const pals_ctrl_cfg* cfg,
                          const pals_replay_spec* spec, pals_trace_summary* d_sum,
-                         pals_step_log* d_logs) {
+                         pals_step_log* d_logs, pals_step_detail* d_det) {
     if (spec->n_traces <= 0) return PALS_OK;
     if (spec->n_steps < 0 || spec->seg_min < 1 || spec->seg_max < spec->seg_min)
         return set_error(PALS_ECONFIG, "pals_replay: bad spec");
@@ -733,13 +741,13 @@ static int replay_launch(pals_ctx* ctx, ReplayCache* rc, const pals_ctrl_cfg* cf
     if (ctx->replay_layout == PALS_REPLAY_WARP) {
         const int64_t wblocks = (spec->n_traces + 3) / 4;  // 4 traces (warps) per CTA
         k_replay<6, true><<<(unsigned)wblocks, 128, 0, ctx->stream>>>(rc->d_models, p, nullptr,
-                                                                     d_sum, d_logs);
+                                                                     d_sum, d_logs, d_det);
     } else if (minb >= 8)
-        k_replay<8, false><<<(unsigned)blocks, 128, 0, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs);
+        k_replay<8, false><<<(unsigned)blocks, 128, 0, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs, d_det);
     else if (minb >= 6)
-        k_replay<6, false><<<(unsigned)blocks, 128, 0, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs);
+        k_replay<6, false><<<(unsigned)blocks, 128, 0, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs, d_det);
     else
-        k_replay<1, false><<<(unsigned)blocks, 128, 0, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs);
+        k_replay<1, false><<<(unsigned)blocks, 128, 0, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs, d_det);
     count_launch(ctx);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "k_replay");
@@ -1139,18 +1147,28 @@ int pals_control_step_one(pals_ctx* ctx, const pals_model* m, const pals_telemet
     return one_call(ctx, m, cands, n, a, 1, out_d, out_s, state);
 }
 
+int pals_replay_device_ex(pals_ctx* ctx, int32_t n_models, pals_model* const* models,
+                          const pals_profile* plant, const pals_gpu_spec* gpu,
+                          const pals_coeffs* coeffs, const double* caps, int32_t n_caps,
+                          const int32_t* batches, int32_t n_batches, const pals_ctrl_cfg* cfg,
+                          const pals_replay_spec* spec, pals_trace_summary* d_sum,
+                          pals_step_log* d_logs, pals_step_detail* d_det) {
+    PALS_CUDA(cudaSetDevice(ctx->device));
+    ReplayCache* rc = nullptr;
+    int r = replay_setup(ctx, n_models, models, plant, gpu, coeffs, caps, n_caps, batches,
+                         n_batches, &rc);
+    if (r) return r;
+    return replay_launch(ctx, rc, cfg, spec, d_sum, d_logs, d_logs ? d_det : nullptr);
+}
+
 int pals_replay_device(pals_ctx* ctx, int32_t n_models, pals_model* const* models,
                        const pals_profile* plant, const pals_gpu_spec* gpu,
                        const pals_coeffs* coeffs, const double* caps, int32_t n_caps,
                        const int32_t* batches, int32_t n_batches, const pals_ctrl_cfg* cfg,
                        const pals_replay_spec* spec, pals_trace_summary* d_sum,
                        pals_step_log* d_logs) {
-    PALS_CUDA(cudaSetDevice(ctx->device));
-    ReplayCache* rc = nullptr;
-    int r = replay_setup(ctx, n_models, models, plant, gpu, coeffs, caps, n_caps, batches,
-                         n_batches, &rc);
-    if (r) return r;
-    return replay_launch(ctx, rc, cfg, spec, d_sum, d_logs);
+    return pals_replay_device_ex(ctx, n_models, models, plant, gpu, coeffs, caps, n_caps,
+                                 batches, n_batches, cfg, spec, d_sum, d_logs, nullptr);
 }
 
 int pals_replay(pals_ctx* ctx, int32_t n_models, pals_model* const* models,
@@ -1158,6 +1176,16 @@ int pals_replay(pals_ctx* ctx, int32_t n_models, pals_model* const* models,
                 const double* caps, int32_t n_caps, const int32_t* batches, int32_t n_batches,
                 const pals_ctrl_cfg* cfg, const pals_replay_spec* spec,
                 pals_trace_summary* summaries, pals_step_log* logs) {
+    return pals_replay_ex(ctx, n_models, models, plant, gpu, coeffs, caps, n_caps, batches,
+                          n_batches, cfg, spec, summaries, logs, nullptr);
+}
+
+int pals_replay_ex(pals_ctx* ctx, int32_t n_models, pals_model* const* models,
+                   const pals_profile* plant, const pals_gpu_spec* gpu, const pals_coeffs* coeffs,
+                   const double* caps, int32_t n_caps, const int32_t* batches, int32_t n_batches,
+                   const pals_ctrl_cfg* cfg, const pals_replay_spec* spec,
+                   pals_trace_summary* summaries, pals_step_log* logs,
+                   pals_step_detail* details) {
     PALS_CUDA(cudaSetDevice(ctx->device));
     ReplayCache* rc = nullptr;
     int r = replay_setup(ctx, n_models, models, plant, gpu, coeffs, caps, n_caps, batches,
@@ -1167,8 +1195,10 @@ int pals_replay(pals_ctx* ctx, int32_t n_models, pals_model* const* models,
     const int64_t nl = logs ? std::min<int64_t>(spec->n_log_traces, spec->n_traces) : 0;
     const size_t sb = (size_t)spec->n_traces * sizeof(pals_trace_summary);
     const size_t lb = (size_t)nl * spec->n_steps * sizeof(pals_step_log);
+    const size_t db = details ? (size_t)nl * spec->n_steps * sizeof(pals_step_detail) : 0;
+    const size_t lo = (sb + 255) & ~(size_t)255, dto = lo + ((lb + 255) & ~(size_t)255);
     // device staging for the outputs, kept in the context across calls
-    const size_t need = sb + lb + 256;
+    const size_t need = dto + db + 256;
     if (ctx->scratch_bytes < need) {
         cudaFree(ctx->d_scratch);
         PALS_CUDA(cudaMalloc(&ctx->d_scratch, need));
@@ -1176,13 +1206,15 @@ int pals_replay(pals_ctx* ctx, int32_t n_models, pals_model* const* models,
     }
     void* d = ctx->d_scratch;
     pals_trace_summary* ds = (pals_trace_summary*)d;
-    pals_step_log* dl = nl ? (pals_step_log*)((char*)d + ((sb + 255) & ~(size_t)255)) : nullptr;
+    pals_step_log* dl = nl ? (pals_step_log*)((char*)d + lo) : nullptr;
+    pals_step_detail* dd = (nl && db) ? (pals_step_detail*)((char*)d + dto) : nullptr;
     pals_replay_spec sp = *spec;
     sp.n_log_traces = (int32_t)nl;
-    r = replay_launch(ctx, rc, cfg, &sp, ds, dl);
+    r = replay_launch(ctx, rc, cfg, &sp, ds, dl, dd);
     if (!r) {
         cudaMemcpyAsync(summaries, ds, sb, cudaMemcpyDeviceToHost, ctx->stream);
         if (nl) cudaMemcpyAsync(logs, dl, lb, cudaMemcpyDeviceToHost, ctx->stream);
+        if (dd) cudaMemcpyAsync(details, dd, db, cudaMemcpyDeviceToHost, ctx->stream);
     }
     const cudaError_t e = cudaStreamSynchronize(ctx->stream);
     if (!r && e != cudaSuccess) r = cuda_fail(e, "pals_replay");

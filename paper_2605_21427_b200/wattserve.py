@@ -21,15 +21,16 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from .abi import (OBJ_BUDGET, OBJ_QOS, POINT_DT, QUERY_DT, STEPLOG_DT, SUMMARY_DT, Coeffs,
-                  CtrlCfg, CtrlState, Decision, GpuSpec, Point, Profile, ReplaySpec, Targets,
-                  Telemetry, ptr)
+from .abi import (OBJ_BUDGET, OBJ_QOS, POINT_DT, QUERY_DT, STEPDETAIL_DT, STEPLOG_DT,
+                  SUMMARY_DT, Coeffs, CtrlCfg, CtrlState, Decision, GpuSpec, Point, Profile,
+                  ReplaySpec, Targets, Telemetry, ptr)
 from ._lib import ConfigError, DataError, OutOfRange, PalsError, check  # noqa: F401
 
 __all__ = [
     "Context", "AnalyticModel", "TableModel", "Grid", "Plan", "analytic_scorer",
     "table_scorer", "select_config", "control_step", "replay", "make_targets",
-    "default_context", "Allocator", "AllocResult", "allocate_budget", "ConfigError", "DataError", "OutOfRange", "PalsError",
+    "default_context", "Allocator", "AllocResult", "allocate_budget", "replay_with_details",
+    "decisions_csv", "fnv1a64", "ConfigError", "DataError", "OutOfRange", "PalsError",
 ]
 
 
@@ -333,6 +334,51 @@ def replay(ctx: Context, models, plant, gpu: GpuSpec, coeffs: Coeffs, caps, batc
                               ptr(caps), len(caps), ptr(batches), len(batches), C.byref(cfg),
                               C.byref(spec), ptr(summ), ptr(logs) if nl else None))
     return summ, logs[: nl * spec.n_steps]
+
+
+def replay_with_details(ctx: Context, models, plant, gpu: GpuSpec, coeffs: Coeffs, caps,
+                        batches, cfg: CtrlCfg, spec: ReplaySpec):
+    """replay() plus the per-step DecisionRecord err_norm / bias (STEPDETAIL_DT) of the
+    logged traces: (summaries, logs, details)."""
+    n_models = len(models)
+    hs = (C.c_void_p * n_models)(*[m.h for m in models])
+    profs = (Profile * n_models)(*plant)
+    caps = np.ascontiguousarray(caps, np.float64)
+    batches = np.ascontiguousarray(batches, np.int32)
+    summ = np.zeros(spec.n_traces, SUMMARY_DT)
+    nl = min(spec.n_log_traces, spec.n_traces)
+    logs = np.zeros(max(1, nl * spec.n_steps), STEPLOG_DT)
+    det = np.zeros(max(1, nl * spec.n_steps), STEPDETAIL_DT)
+    check(ctx.lib.pals_replay_ex(ctx.h, n_models, hs, profs, C.byref(gpu), C.byref(coeffs),
+                                 ptr(caps), len(caps), ptr(batches), len(batches), C.byref(cfg),
+                                 C.byref(spec), ptr(summ), ptr(logs) if nl else None,
+                                 ptr(det) if nl else None))
+    return summ, logs[: nl * spec.n_steps], det[: nl * spec.n_steps]
+
+
+def decisions_csv(spec: ReplaySpec, plant, caps, batches, summaries, logs, details) -> bytes:
+    """The reference's decisions CSV (metrics.hpp:145-157) of a replay's logged traces,
+    formatted by libpals_gpu (host code; no device needed)."""
+    lib = _lib.load(build_if_missing=False)
+    profs = (Profile * len(plant))(*plant)
+    caps = np.ascontiguousarray(caps, np.float64)
+    batches = np.ascontiguousarray(batches, np.int32)
+    summ = np.ascontiguousarray(summaries, SUMMARY_DT)
+    logs = np.ascontiguousarray(logs, STEPLOG_DT)
+    det = np.ascontiguousarray(details, STEPDETAIL_DT)
+    n = C.c_int64(0)
+    args = [C.byref(spec), profs, len(plant), ptr(caps), len(caps), ptr(batches), len(batches),
+            ptr(summ), ptr(logs), ptr(det)]
+    check(lib.pals_decisions_csv(*args, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(max(1, n.value))
+    check(lib.pals_decisions_csv(*args, buf, n.value, C.byref(n)))
+    return buf.raw[: n.value]
+
+
+def fnv1a64(data: bytes) -> int:
+    """rng.hpp:22-28 — the per-file hash of the reference's run manifests."""
+    lib = _lib.load(build_if_missing=False)
+    return int(lib.pals_fnv1a64(data, len(data)))
 
 
 def replay_device(ctx: Context, models, plant, gpu: GpuSpec, coeffs: Coeffs, caps, batches,

@@ -453,6 +453,124 @@ int pals_alloc_run_device(pals_alloc* a, double quantum_w, int64_t n_problems,
                           double* d_node_budget, double* d_total, uint8_t* d_all_satisfied,
                           int32_t* d_status);
 
+/* ---- queue-plant scenario simulator (sim.hpp:222-500) ------------------ */
+/* Batched run_scenario(): every scenario is the reference's interval-quantized
+ * cluster simulation — Poisson arrivals with lognormal output lengths per node
+ * (Rng::substream(seed, node), rng.hpp:30-95), continuous batching under the
+ * node's batch cap, the facility breaker (enforce_cap), telemetry, one
+ * control_step per interval and the two-stage actuation pipeline — with budgets
+ * split by assign_budgets (allocate_budget water-filling for joint / oracle,
+ * dp-proportional otherwise) whenever the cluster budget (static or trace)
+ * changes. Policies and scorers as Simulator (sim.hpp:209-220, 267-336). */
+#define PALS_POLICY_FIXED 0
+#define PALS_POLICY_ADAPTIVE_BATCH 1
+#define PALS_POLICY_ADAPTIVE_CAP 2
+#define PALS_POLICY_JOINT 3
+#define PALS_POLICY_ORACLE 4
+#define PALS_SIM_MAX_NODES 32
+
+typedef struct {              /* ScenarioNode (sim.hpp:52-60) */
+    int32_t model;            /* index into the call's profiles / predictors */
+    int32_t tp, ep, dp;
+    double qos_fraction;
+    double arrival_rate_per_s;
+    int32_t initial_backlog;
+    int32_t _pad;
+} pals_sim_node;
+
+typedef struct {              /* Scenario (sim.hpp:62-94) */
+    double duration_s;
+    double interval_s;
+    uint64_t seed;
+    double mean_tokens;       /* OutputLenDist */
+    double log_sigma;
+    int32_t has_cluster_budget;
+    int32_t n_trace;          /* budget_trace points (t_s strictly increasing) */
+    double cluster_budget_w;
+    const double* trace_t;
+    const double* trace_w;
+    int32_t policy;           /* PALS_POLICY_* */
+    int32_t objective;        /* PALS_OBJ_* */
+    pals_ctrl_cfg controller; /* gains, clamps, sustain, headroom, margin (interval_s ignored) */
+    double epsilon;
+    const double* cand_caps;
+    const int32_t* cand_batches;
+    int32_t n_caps;
+    int32_t n_batches;
+    double initial_cap_w;     /* must be one of the policy's candidate caps */
+    int32_t initial_batch;    /* must be one of the policy's candidate batches */
+    int32_t n_nodes;          /* <= PALS_SIM_MAX_NODES */
+    const pals_sim_node* nodes;
+} pals_scenario;
+
+typedef struct {              /* one node's MetricsSummary (metrics.hpp:24-48) + run facts */
+    double tokens_per_joule;
+    double qos_violation_rate;
+    double power_tracking_mae_w;
+    double total_tokens;
+    double total_energy_j;
+    double mean_throughput_tps;
+    double throughput_target_tps;   /* NodeResult::throughput_target_tps */
+    double final_bias;
+    uint64_t arrival_stream_hash;   /* NodeResult::arrival_stream_hash */
+    int64_t n_requests;             /* spawned (backlog + arrivals) */
+    int64_t n_completed;
+    int32_t n_applied;
+    int32_t final_idx;              /* controller's current point (policy candidate index) */
+} pals_sim_node_result;
+
+typedef struct {              /* RunSummary aggregate (metrics.hpp:56-102) + SimResult */
+    double tokens_per_joule;
+    double qos_violation_rate;      /* worst node */
+    double power_tracking_mae_w;
+    double total_tokens;
+    double total_energy_j;
+    double mean_throughput_tps;     /* sum of node means */
+    double cluster_tracking_mae_w;
+    double sim_total_energy_j;      /* SimResult::total_energy_j (interval-major sum) */
+    int32_t n_intervals;
+    int32_t n_budget_changes;
+} pals_sim_result;
+
+typedef struct {              /* TelemetrySample (sim.hpp:109-120) */
+    double t_s;
+    double gpu_power_w;
+    double sys_power_w;
+    double throughput_tps;
+    double utilization;
+    double node_budget_w;
+    double applied_cap_w;
+    int32_t queue_depth;
+    int32_t active_batch;
+    int32_t applied_batch_cap;
+    int32_t _pad;
+} pals_sim_telemetry;
+
+typedef struct {              /* DecisionRecord (sim.hpp:122-129) */
+    double err_norm;
+    double bias;
+    double cap_w;
+    int32_t batch;
+    uint8_t applied;
+    uint8_t reason;
+    uint16_t _pad;
+} pals_sim_decision;
+
+/* Runs n_scenarios independent scenarios. profiles[m] is model m's calibrated
+ * profile (the plant, and the oracle's analytic scorer); predictors[m] its
+ * predictor_scorer (a forest model handle) or NULL — policies other than oracle
+ * score with the predictor when one is given (sim.hpp:277-281); adaptive-batch,
+ * adaptive-cap and joint require it. Outputs: node_results (all nodes, scenario
+ * order), results per scenario, and optionally per-interval logs for every node
+ * ([node][interval], n_intervals = llround(duration_s / interval_s) each; pass
+ * log_stride >= the largest n_intervals). Errors as run_scenario would throw. */
+int pals_run_scenarios(pals_ctx* ctx, int32_t n_scenarios, const pals_scenario* scenarios,
+                       int32_t n_models, const pals_profile* profiles,
+                       pals_model* const* predictors, const pals_gpu_spec* gpu,
+                       const pals_coeffs* coeffs, pals_sim_node_result* node_results,
+                       pals_sim_result* results, int64_t log_stride,
+                       pals_sim_telemetry* telemetry, pals_sim_decision* decisions);
+
 #ifdef __cplusplus
 }
 #endif

@@ -316,6 +316,28 @@ DECISION_SPECS = {  # name -> replay_spec kwargs of the decisions-CSV fixtures
 }
 
 
+def write_scenarios() -> None:
+    """The reference's bundled scenarios (proj/data/scenarios/*.json) with their budget
+    traces resolved (budget_trace_csv, scenario_io.hpp:13-25, 46-49), as model-fit input
+    for the queue-plant simulator: paper_2605_21427_b200/data/scenarios.json."""
+    out = {}
+    for f in sorted(glob.glob(os.path.join(REF_DATA, "scenarios", "*.json"))):
+        with open(f) as fh:
+            j = json.load(fh)
+        trace = []
+        if j.get("budget_trace_csv"):
+            with open(os.path.join(os.path.dirname(f), j["budget_trace_csv"])) as fh:
+                for line in fh:
+                    line = line.strip()
+                    if not line or not line[0].isdigit():
+                        continue
+                    t, w = line.split(",")
+                    trace.append([float(t), float(w)])
+        out[os.path.basename(f)[:-5]] = {"scenario": j, "trace": trace}
+    with open(os.path.join(ROOT, "paper_2605_21427_b200", "data", "scenarios.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
+
+
 def gen_decisions(ref: Reference) -> None:
     """decisions_csv (metrics.hpp:145-157) produced by the reference's own writer over
     fluid-plant replays through the unmodified control_step, plus its fnv1a64."""
@@ -384,6 +406,7 @@ def main():
             globals()["gen_" + name](ref)
         return
     write_profiles(ref)
+    write_scenarios()
     gen_eval(ref)
     gen_select(ref)
     gen_tables(ref)

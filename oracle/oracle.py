@@ -281,6 +281,39 @@ class Reference:
         L.ref_replay_decisions_csv(*args, buf, n.value, C.byref(n), C.byref(h))
         return buf.raw[: n.value], int(h.value)
 
+    def run_scenario(self, scenario: dict, profiles, gpu, coeffs, bundle_path=None,
+                     logs: bool = True, want_csv: bool = False):
+        """The unmodified run_scenario + summarize for one scenario dict
+        (paper_2605_21427_b200.sim format): (node_results, result, tel, dec[, csv])."""
+        from paper_2605_21427_b200.abi import (SIM_DEC_DT, SIM_NODE_RESULT_DT, SIM_RESULT_DT,
+                                               SIM_TEL_DT)
+        from paper_2605_21427_b200.sim import _CScenario, _model_index, n_intervals
+        L = self.lib
+        L.ref_run_scenario.argtypes = [_VP, C.c_int, _VP, C.c_char_p, _VP, _VP, _VP, _VP,
+                                       C.c_int64, _VP, _VP, _VP, C.c_int64, _VP]
+        cs = _CScenario(scenario, _model_index(profiles))
+        profs = (Profile * len(profiles))(*profiles)
+        nn = len(scenario["nodes"])
+        stride = n_intervals(scenario)
+        nres = np.zeros(nn, SIM_NODE_RESULT_DT)
+        res = np.zeros(1, SIM_RESULT_DT)
+        tel = np.zeros((nn, stride), SIM_TEL_DT) if logs else None
+        dec = np.zeros((nn, stride), SIM_DEC_DT) if logs else None
+        n = C.c_int64(0)
+        bp = bundle_path.encode() if bundle_path else None
+        args = [C.byref(cs.c), len(profiles), profs, bp, C.byref(gpu), C.byref(coeffs), ptr(nres),
+                ptr(res), stride, ptr(tel), ptr(dec)]
+        rc = L.ref_run_scenario(*args, None, 0, C.byref(n) if want_csv else None)
+        if rc:
+            raise RuntimeError(f"ref_run_scenario rc={rc}: {self.last_error()}")
+        out = (nres, res[0], tel, dec)
+        if want_csv:
+            buf = C.create_string_buffer(max(1, n.value))
+            L.ref_run_scenario(*args, buf, n.value, C.byref(n))
+            tcsv, dcsv = buf.raw[: n.value].split(b"\0")
+            out = out + ((tcsv, dcsv),)
+        return out
+
     def bench_select(self, prof, gpu, pts, coeffs, queries, threads, want_results=True):
         nq = len(queries)
         idx = np.empty(nq, np.int32) if want_results else None

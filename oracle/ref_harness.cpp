@@ -972,3 +972,134 @@ double ref_bench_frontier(const pals_profile* prof, const pals_gpu_spec* gpu, co
 }
 
 }  // extern "C"
+
+// ---- queue-plant scenarios through the UNMODIFIED run_scenario (sim.hpp:482-485) --
+namespace {
+Scenario to_scenario(const pals_scenario& s, const pals_profile* profs) {
+    Scenario sc;
+    sc.name = "pals";
+    sc.duration_s = s.duration_s;
+    sc.interval_s = s.interval_s;
+    sc.seed = s.seed;
+    sc.output_len.mean_tokens = s.mean_tokens;
+    sc.output_len.log_sigma = s.log_sigma;
+    if (s.has_cluster_budget) sc.cluster_budget_w = s.cluster_budget_w;
+    for (int i = 0; i < s.n_trace; ++i) sc.budget_trace.emplace_back(s.trace_t[i], s.trace_w[i]);
+    const Policy pol[] = {Policy::Fixed, Policy::AdaptiveBatch, Policy::AdaptiveCap,
+                          Policy::Joint, Policy::Oracle};
+    sc.policy = pol[s.policy];
+    sc.objective = s.objective == PALS_OBJ_BUDGET ? Objective::BudgetMaxThroughput
+                                                  : Objective::QosMaxEfficiency;
+    sc.controller = to_cfg(s.controller);
+    sc.epsilon = s.epsilon;
+    sc.cand_caps.assign(s.cand_caps, s.cand_caps + s.n_caps);
+    sc.cand_batches.assign(s.cand_batches, s.cand_batches + s.n_batches);
+    sc.initial_cap_w = s.initial_cap_w;
+    sc.initial_batch = s.initial_batch;
+    for (int i = 0; i < s.n_nodes; ++i) {
+        const pals_sim_node& n = s.nodes[i];
+        ScenarioNode sn;
+        sn.model_id = profs[n.model].name;
+        sn.qos_fraction = n.qos_fraction;
+        sn.tp = n.tp;
+        sn.ep = n.ep;
+        sn.dp = n.dp;
+        sn.arrival_rate_per_s = n.arrival_rate_per_s;
+        sn.initial_backlog = n.initial_backlog;
+        sc.nodes.push_back(sn);
+    }
+    return sc;
+}
+}  // namespace
+
+extern "C" {
+
+// run_scenario + summarize (metrics.hpp:24-102); bundle_path NULL = no predictor.
+// Per-interval logs [node][interval] when tel / dec are non-NULL; csv receives the
+// reference's telemetry_csv + decisions_csv texts (NUL-separated) when non-NULL.
+int ref_run_scenario(const pals_scenario* s, int n_models, const pals_profile* profs,
+                     const char* bundle_path, const pals_gpu_spec* gpu, const pals_coeffs* coeffs,
+                     pals_sim_node_result* node_out, pals_sim_result* out, std::int64_t stride,
+                     pals_sim_telemetry* tel, pals_sim_decision* dec, char* csv,
+                     std::int64_t csv_cap, std::int64_t* csv_len) {
+    try {
+        ProfileRegistry reg;
+        for (int m = 0; m < n_models; ++m) reg.add(to_profile(profs[m]));
+        Platform plat{to_gpu(*gpu), SystemPowerCoeffs{coeffs->alpha, coeffs->beta_watts}};
+        const PredictorBundle* b = bundle_path ? &load_bundle(bundle_path) : nullptr;
+        const Scenario sc = to_scenario(*s, profs);
+        const SimResult r = run_scenario(sc, reg, plat, b);
+        const RunSummary rs = summarize(r);
+        for (std::size_t i = 0; i < r.nodes.size(); ++i) {
+            const NodeResult& nr = r.nodes[i];
+            const MetricsSummary& m = rs.per_node.at(std::to_string(i) + ":" + nr.model_id);
+            pals_sim_node_result& o = node_out[i];
+            std::memset(&o, 0, sizeof o);
+            o.tokens_per_joule = m.tokens_per_joule;
+            o.qos_violation_rate = m.qos_violation_rate;
+            o.power_tracking_mae_w = m.power_tracking_mae_w;
+            o.total_tokens = m.total_tokens;
+            o.total_energy_j = m.total_energy_j;
+            o.mean_throughput_tps = m.mean_throughput_tps;
+            o.throughput_target_tps = nr.throughput_target_tps;
+            o.final_bias = nr.decisions.empty() ? 1.0 : nr.decisions.back().bias;
+            o.arrival_stream_hash = nr.arrival_stream_hash;
+            o.n_requests = static_cast<std::int64_t>(nr.requests.size());
+            std::int64_t done = 0;
+            for (const auto& q : nr.requests) done += q.done() ? 1 : 0;
+            o.n_completed = done;
+            int applied = 0;
+            for (const auto& d : nr.decisions) applied += d.applied ? 1 : 0;
+            o.n_applied = applied;
+            o.final_idx = -1;
+            for (std::size_t k = 0; k < nr.telemetry.size() && k < (std::size_t)stride; ++k) {
+                if (tel) {
+                    const TelemetrySample& t = nr.telemetry[k];
+                    pals_sim_telemetry& x = tel[i * stride + k];
+                    std::memset(&x, 0, sizeof x);
+                    x.t_s = t.t_s;
+                    x.gpu_power_w = t.gpu_power_w;
+                    x.sys_power_w = t.sys_power_w;
+                    x.throughput_tps = t.throughput_tps;
+                    x.utilization = t.utilization;
+                    x.node_budget_w = t.node_budget_w;
+                    x.applied_cap_w = t.applied_cap_w;
+                    x.queue_depth = t.queue_depth;
+                    x.active_batch = t.active_batch;
+                    x.applied_batch_cap = t.applied_batch_cap;
+                }
+                if (dec) {
+                    const DecisionRecord& d = nr.decisions[k];
+                    pals_sim_decision& x = dec[i * stride + k];
+                    std::memset(&x, 0, sizeof x);
+                    x.err_norm = d.err_norm;
+                    x.bias = d.bias;
+                    x.cap_w = d.point.cap_watts;
+                    x.batch = d.point.batch;
+                    x.applied = d.applied ? 1 : 0;
+                    x.reason = static_cast<std::uint8_t>(reason_code(d.reason));
+                }
+            }
+        }
+        std::memset(out, 0, sizeof *out);
+        out->tokens_per_joule = rs.aggregate.tokens_per_joule;
+        out->qos_violation_rate = rs.aggregate.qos_violation_rate;
+        out->power_tracking_mae_w = rs.aggregate.power_tracking_mae_w;
+        out->total_tokens = rs.aggregate.total_tokens;
+        out->total_energy_j = rs.aggregate.total_energy_j;
+        out->mean_throughput_tps = rs.aggregate.mean_throughput_tps;
+        out->cluster_tracking_mae_w = rs.cluster_tracking_mae_w;
+        out->sim_total_energy_j = r.total_energy_j;
+        out->n_intervals = r.nodes.empty() ? 0 : static_cast<int>(r.nodes[0].telemetry.size());
+        if (csv_len) {
+            const std::string text = telemetry_csv(r) + std::string(1, '\0') + decisions_csv(r);
+            *csv_len = static_cast<std::int64_t>(text.size());
+            if (csv) std::memcpy(csv, text.data(), std::min<std::size_t>(text.size(), csv_cap));
+        }
+    } catch (...) {
+        return map_exception();
+    }
+    return PALS_OK;
+}
+
+}  // extern "C"

@@ -141,6 +141,53 @@ assert C.sizeof(Point) == POINT_DT.itemsize == 24
 assert C.sizeof(Query) == QUERY_DT.itemsize == 48
 STEPDETAIL_DT = np.dtype([("err_norm", "<f8"), ("bias", "<f8")], align=True)
 
+# ---- queue-plant scenarios (sim.hpp:47-145; pals_run_scenarios) ----
+POLICY_FIXED, POLICY_ADAPTIVE_BATCH, POLICY_ADAPTIVE_CAP, POLICY_JOINT, POLICY_ORACLE = range(5)
+POLICIES = {"fixed": 0, "adaptive-batch": 1, "adaptive-cap": 2, "joint": 3, "oracle": 4}
+SIM_MAX_NODES = 32
+
+
+class SimNode(C.Structure):  # ScenarioNode (sim.hpp:52-60)
+    _fields_ = [("model", C.c_int32), ("tp", C.c_int32), ("ep", C.c_int32), ("dp", C.c_int32),
+                ("qos_fraction", C.c_double), ("arrival_rate_per_s", C.c_double),
+                ("initial_backlog", C.c_int32), ("_pad", C.c_int32)]
+
+
+class Scenario(C.Structure):  # Scenario (sim.hpp:62-94)
+    _fields_ = [("duration_s", C.c_double), ("interval_s", C.c_double), ("seed", C.c_uint64),
+                ("mean_tokens", C.c_double), ("log_sigma", C.c_double),
+                ("has_cluster_budget", C.c_int32), ("n_trace", C.c_int32),
+                ("cluster_budget_w", C.c_double), ("trace_t", C.c_void_p),
+                ("trace_w", C.c_void_p), ("policy", C.c_int32), ("objective", C.c_int32),
+                ("controller", CtrlCfg), ("epsilon", C.c_double), ("cand_caps", C.c_void_p),
+                ("cand_batches", C.c_void_p), ("n_caps", C.c_int32), ("n_batches", C.c_int32),
+                ("initial_cap_w", C.c_double), ("initial_batch", C.c_int32),
+                ("n_nodes", C.c_int32), ("nodes", C.c_void_p)]
+
+
+SIM_NODE_RESULT_DT = np.dtype([
+    ("tokens_per_joule", "<f8"), ("qos_violation_rate", "<f8"), ("power_tracking_mae_w", "<f8"),
+    ("total_tokens", "<f8"), ("total_energy_j", "<f8"), ("mean_throughput_tps", "<f8"),
+    ("throughput_target_tps", "<f8"), ("final_bias", "<f8"), ("arrival_stream_hash", "<u8"),
+    ("n_requests", "<i8"), ("n_completed", "<i8"), ("n_applied", "<i4"), ("final_idx", "<i4")],
+    align=True)
+SIM_RESULT_DT = np.dtype([
+    ("tokens_per_joule", "<f8"), ("qos_violation_rate", "<f8"), ("power_tracking_mae_w", "<f8"),
+    ("total_tokens", "<f8"), ("total_energy_j", "<f8"), ("mean_throughput_tps", "<f8"),
+    ("cluster_tracking_mae_w", "<f8"), ("sim_total_energy_j", "<f8"), ("n_intervals", "<i4"),
+    ("n_budget_changes", "<i4")], align=True)
+SIM_TEL_DT = np.dtype([
+    ("t_s", "<f8"), ("gpu_power_w", "<f8"), ("sys_power_w", "<f8"), ("throughput_tps", "<f8"),
+    ("utilization", "<f8"), ("node_budget_w", "<f8"), ("applied_cap_w", "<f8"),
+    ("queue_depth", "<i4"), ("active_batch", "<i4"), ("applied_batch_cap", "<i4"),
+    ("_pad", "<i4")], align=True)
+SIM_DEC_DT = np.dtype([
+    ("err_norm", "<f8"), ("bias", "<f8"), ("cap_w", "<f8"), ("batch", "<i4"), ("applied", "u1"),
+    ("reason", "u1"), ("_pad", "<u2")], align=True)
+assert C.sizeof(SimNode) == 40 and C.sizeof(Scenario) == 216
+assert SIM_NODE_RESULT_DT.itemsize == 96 and SIM_RESULT_DT.itemsize == 72
+assert SIM_TEL_DT.itemsize == 72 and SIM_DEC_DT.itemsize == 32
+
 assert SUMMARY_DT.itemsize == 48 and STEPLOG_DT.itemsize == 8 and STEPDETAIL_DT.itemsize == 16
 assert C.sizeof(Profile) == 272
 

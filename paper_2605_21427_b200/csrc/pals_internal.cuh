@@ -73,7 +73,7 @@ struct Score {
 // step_timing + throughput + avg_gpu_power (model.hpp:37-84) for a point that
 // already passed validation. Returns T, P and the per-step terms.
 PALS_HD Score analytic_score(const Analytic& a, double cap, int batch, int tp, int dp,
-                             double* t_comp_out = nullptr) {
+                             double* t_comp_out = nullptr, double* step_out = nullptr) {
     // effective_frequency model.hpp:41-44
     const double span = a.knee_watts - a.min_cap;
     double f;
@@ -99,6 +99,7 @@ PALS_HD Score analytic_score(const Analytic& a, double cap, int batch, int tp, i
     const double comm_share = step - t_comp;
     s.P = (t_comp * p_comp + comm_share * a.comm_power) / step;
     if (t_comp_out) *t_comp_out = t_comp;
+    if (step_out) *step_out = step;  // StepTiming::step_s (model.hpp:66)
     return s;
 }
 

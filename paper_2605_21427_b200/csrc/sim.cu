@@ -1,0 +1,986 @@
+// sim.cu — K6: batched queue-plant scenario simulation (run_scenario, sim.hpp:209-500).
+//
+// One CTA per scenario, one warp per node, one loop iteration per control
+// interval — the reference's Simulator::run with every node's step_node
+// (sim.hpp:355-473) executed by its warp:
+//   (1) arrivals       host-generated streams (below), replayed by index
+//   (2) batch + breaker effective_batch, enforce_cap (sim.hpp:195-205; the 5 W walk
+//                      is evaluated 32 positions per round across the lanes)
+//   (3)+(4) service    continuous batching; the running list (sorted by request id:
+//                      admission is FIFO and completion removal keeps order) is
+//                      spread over the lanes, the chunk is a warp min-reduction,
+//                      completions compact with ballots — every double is the
+//                      reference's, element by element
+//   (5) telemetry      accumulated into the node's MetricsSummary (metrics.hpp:24-48)
+//   (6) control_step   the K3 rank-table select (replay_common.cuh) with the node's
+//                      scorer (predictor cells / analytic for the oracle)
+//   (7) actuation      batch next interval, cap one interval later
+// and, per interval, the cluster draw vs the budget signal (metrics.hpp:71-97).
+//
+// Host side (the parts a GPU cannot reproduce bit-for-bit, or that do not depend
+// on the simulation state):
+//   * arrival streams: Rng::substream(seed, node) = std::mt19937_64 seeded with
+//     splitmix64(splitmix64(seed) ^ node), Knuth / normal-approximation Poisson and
+//     Box-Muller lognormal lengths through the host libm (rng.hpp:30-95) — the
+//     reference's own libm calls, which CUDA's libdevice does not match bit for
+//     bit. Arrival streams never depend on the policy (sim.hpp header), so they
+//     are inputs to the plant, generated once per node.
+//   * budget splits: assign_budgets runs whenever the cluster signal changes
+//     (sim.hpp:229-238, 313-336); its inputs are the trace and the node scorers,
+//     never the simulation state, so every split is precomputed — allocate_budget
+//     on the GPU allocator (K4) for joint / oracle, dp-proportional otherwise.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <random>
+#include <string>
+#include <thread>
+#include <tuple>
+#include <vector>
+
+#include "replay_common.cuh"
+
+namespace pals {
+namespace {
+
+// ---- host: the reference's Rng over std::mt19937_64 (rng.hpp:30-95) ----------
+struct HostRng {
+    std::mt19937_64 eng;
+    double spare = 0.0;
+    bool have_spare = false;
+    explicit HostRng(uint64_t seed) : eng(seed) {}
+    double uniform01() { return (double)(eng() >> 11) * 0x1.0p-53; }
+    double gaussian(double mean, double stddev) {
+        if (have_spare) {
+            have_spare = false;
+            return mean + stddev * spare;
+        }
+        double u, v, s;
+        do {
+            u = 2.0 * uniform01() - 1.0;
+            v = 2.0 * uniform01() - 1.0;
+            s = u * u + v * v;
+        } while (s >= 1.0 || s == 0.0);
+        const double m = std::sqrt(-2.0 * std::log(s) / s);
+        spare = v * m;
+        have_spare = true;
+        return mean + stddev * u * m;
+    }
+    double lognormal(double log_mean, double log_sigma) {
+        return std::exp(gaussian(log_mean, log_sigma));
+    }
+    int poisson(double lambda) {
+        if (lambda <= 0.0) return 0;
+        if (lambda < 50.0) {
+            const double limit = std::exp(-lambda);
+            int k = 0;
+            double p = 1.0;
+            do {
+                ++k;
+                p *= uniform01();
+            } while (p > limit);
+            return k - 1;
+        }
+        const double x = gaussian(lambda, std::sqrt(lambda));
+        return x < 0.0 ? 0 : (int)std::lround(x);
+    }
+};
+
+uint64_t fnv_str(const std::string& s, uint64_t h) {
+    for (unsigned char c : s) {
+        h ^= c;
+        h *= 0x100000001b3ULL;
+    }
+    return h;
+}
+
+std::string fmt10g(double v) {
+    char buf[40];
+    std::snprintf(buf, sizeof buf, "%.10g", v);
+    return buf;
+}
+
+// One node's arrival stream: request lengths by id, and cum[k] = requests spawned
+// before interval k's service (cum[0] = the initial backlog).
+struct Stream {
+    std::vector<int32_t> len;
+    std::vector<int32_t> cum;
+    uint64_t hash = 0xcbf29ce484222325ULL;
+};
+
+void gen_stream(const pals_scenario& sc, int node, int n_int, Stream* out) {
+    const pals_sim_node& nd = sc.nodes[node];
+    HostRng rng(splitmix64(splitmix64(sc.seed) ^ (uint64_t)node));  // Rng::substream
+    const double log_mean = std::log(sc.mean_tokens) - 0.5 * sc.log_sigma * sc.log_sigma;
+    auto spawn = [&](double t) {  // spawn_request (sim.hpp:338-353)
+        const int len = std::max(1, (int)std::lround(rng.lognormal(log_mean, sc.log_sigma)));
+        const long id = (long)out->len.size();
+        out->hash = fnv_str(std::to_string(id) + ":" + std::to_string(len) + "@" + fmt10g(t),
+                            out->hash);
+        out->len.push_back(len);
+    };
+    for (int b = 0; b < nd.initial_backlog; ++b) spawn(0.0);
+    out->cum.resize((size_t)n_int + 1);
+    for (int k = 0; k < n_int; ++k) {
+        const double t0 = k * sc.interval_s;
+        const int n = rng.poisson(nd.arrival_rate_per_s * sc.interval_s);
+        for (int a = 0; a < n; ++a) spawn(t0);
+        out->cum[k] = (int32_t)out->len.size();  // visible to interval k
+    }
+    out->cum[n_int] = (int32_t)out->len.size();
+}
+
+double trace_value(const pals_scenario& sc, double t) {  // sim.hpp:167-174
+    double v = sc.trace_w[0];
+    for (int i = 0; i < sc.n_trace; ++i) {
+        if (sc.trace_t[i] <= t) v = sc.trace_w[i];
+        else break;
+    }
+    return v;
+}
+
+// ---- device layout ------------------------------------------------------------
+struct SimNodeDev {
+    const ReplayModelDev* sel;  // select tables over the node's candidates + scorer
+    const Analytic* plant;      // the node's calibrated profile
+    const int32_t* cum;         // [n_int + 1]
+    const int32_t* len;         // request lengths by id
+    int32_t* run_id;            // running-list scratch (run_cap entries)
+    double* run_gen;
+    const double* budget;       // node budget per budget change
+    int tp, ep, dp;
+    int init_idx;
+    double target_tps;
+};
+
+struct SimScenDev {
+    int node0, n_nodes;
+    int n_int;
+    int policy, objective;
+    int budget_active;
+    int n_changes;
+    const int32_t* change_k;     // interval at which change c applies
+    const double* track_target;  // per interval: cluster tracking target (metrics.hpp:84-90)
+    double interval_s, epsilon;
+    pals_ctrl_cfg cfg;
+};
+
+struct SimArgs {
+    const SimScenDev* scen;
+    const SimNodeDev* nodes;
+    double alpha, beta, idle_w, min_cap;
+    pals_sim_node_result* node_out;
+    pals_sim_result* out;
+    int64_t log_stride;
+    pals_sim_telemetry* tel;
+    pals_sim_decision* dec;
+};
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ double warp_min(double v) {
+    for (int o = 16; o; o >>= 1) {
+        const double w = __shfl_xor_sync(kFull, v, o);
+        v = w < v ? w : v;
+    }
+    return v;
+}
+
+__global__ void __launch_bounds__(32 * PALS_SIM_MAX_NODES) k_sim(SimArgs a) {
+    const SimScenDev S = a.scen[blockIdx.x];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __shared__ double sh_sys[PALS_SIM_MAX_NODES], sh_bud[PALS_SIM_MAX_NODES];
+    __shared__ double sh_cluster_abs, sh_energy;
+    __shared__ int sh_counted;
+    if (threadIdx.x == 0) {
+        sh_cluster_abs = 0.0;
+        sh_energy = 0.0;
+        sh_counted = 0;
+    }
+    const bool live = w < S.n_nodes;
+    const int gi = S.node0 + (live ? w : 0);
+    const SimNodeDev N = a.nodes[gi];
+    const ReplayModelDev& m = *N.sel;
+    const Analytic& P = *N.plant;
+    const double iv = S.interval_s;
+    const double target = N.target_tps;
+    // Oracle: exhaustive search without feedback lag (sim.hpp:443-448)
+    double kp = S.cfg.kp, ki = S.cfg.ki, kd = S.cfg.kd;
+    int sustain_n = S.cfg.sustain_intervals;
+    if (S.policy == PALS_POLICY_ORACLE) {
+        kp = ki = kd = 0.0;
+        sustain_n = 0;
+    }
+    const double sel_target = target * (1.0 + S.cfg.target_headroom);  // controller.hpp:137
+
+    // node runtime (uniform across the warp's lanes)
+    double applied_cap = m.cap[N.init_idx], inflight_cap = applied_cap;
+    int batch_cap = m.batch[N.init_idx];
+    int cur = N.init_idx;
+    double bias = 1.0, integral = 0.0, prev_err = 0.0;
+    bool has_prev = false, has_last = false, last_bset = false;
+    double last_budget = 0.0;
+    int sustain = 0;
+    int next_admit = 0, R = 0, chg = 0;
+    double node_budget = 0.0;
+    double kp_budget = -1.0;
+    int kpv = m.nd_p, kt = 0;
+    double memo_cap = -1.0, memo_budget = -1.0, memo_out = 0.0;
+    int memo_b = -1;
+    // MetricsSummary accumulators (metrics.hpp:27-41)
+    double tot_tokens = 0.0, tot_energy = 0.0, sum_tps = 0.0, track_abs = 0.0;
+    long violations = 0, tracked = 0, completed = 0;
+    int n_applied = 0;
+    pals_sim_telemetry* tl = (live && a.tel && lane == 0) ? a.tel + gi * a.log_stride : nullptr;
+    pals_sim_decision* dl = (live && a.dec && lane == 0) ? a.dec + gi * a.log_stride : nullptr;
+    __syncthreads();
+
+    for (int k = 0; k < S.n_int; ++k) {
+        const double t0 = k * iv;
+        const double t1 = t0 + iv;
+        double sys_w = 0.0;
+        if (live) {
+            while (chg < S.n_changes && S.change_k[chg] <= k) node_budget = N.budget[chg++];
+            // (1) arrivals: the stream's requests up to this interval are queued
+            const int spawned = N.cum[k];
+            // (2) effective batch from queue pressure, per replica (sim.hpp:360-365)
+            const int avail = R + (spawned - next_admit);
+            const int per_replica = (avail + N.dp - 1) / N.dp;
+            const int b_eff = min(batch_cap, per_replica);
+            const int slot_cap = b_eff * N.dp;
+            // facility breaker (sim.hpp:195-205)
+            double cap = applied_cap;
+            if (node_budget > 0.0 && b_eff >= 1) {
+                if (applied_cap == memo_cap && b_eff == memo_b && node_budget == memo_budget) {
+                    cap = memo_out;
+                } else {
+                    double c0 = applied_cap;  // walk position of this round's lane 0
+                    for (;;) {
+                        double c = c0;
+                        for (int j = 0; j < lane; ++j) c = smax(P.min_cap, c - 5.0);
+                        bool stop = !(c > P.min_cap);
+                        if (!stop) {
+                            const Score s = analytic_score(P, c, b_eff, N.tp, N.dp);
+                            stop = p_node_of(s.P, N.dp, a.alpha, a.beta) <= node_budget;
+                        }
+                        const unsigned b = __ballot_sync(kFull, stop);
+                        if (b) {
+                            const int j = __ffs(b) - 1;
+                            const double cj = __shfl_sync(kFull, c, j);
+                            cap = cj > P.min_cap ? cj : P.min_cap;
+                            break;
+                        }
+                        c0 = smax(P.min_cap, __shfl_sync(kFull, c, 31) - 5.0);
+                    }
+                    memo_cap = applied_cap;
+                    memo_b = b_eff;
+                    memo_budget = node_budget;
+                    memo_out = cap;
+                }
+            }
+            // (3)+(4) continuous batching (sim.hpp:374-409)
+            double tokens = 0.0, gpu_w = a.idle_w, util = 0.0;
+            if (b_eff >= 1) {
+                double ts;
+                const Score s = analytic_score(P, cap, b_eff, N.tp, N.dp, nullptr, &ts);
+                gpu_w = s.P;
+                const double steps_per_seq = iv / ts;
+                double steps_left = steps_per_seq;
+                while (steps_left > 1e-9) {
+                    if (R < slot_cap && next_admit < spawned) {  // refill freed slots
+                        const int n_adm = min(slot_cap - R, spawned - next_admit);
+                        for (int j = lane; j < n_adm; j += 32) {
+                            N.run_id[R + j] = next_admit + j;
+                            N.run_gen[R + j] = 0.0;
+                        }
+                        R += n_adm;
+                        next_admit += n_adm;
+                        __syncwarp();
+                    }
+                    if (R == 0) break;
+                    const int active = min(slot_cap, R);
+                    double mn = steps_left;
+                    for (int j = lane; j < active; j += 32) {
+                        const double left = (double)N.len[N.run_id[j]] - N.run_gen[j];
+                        mn = left < mn ? left : mn;
+                    }
+                    double chunk = warp_min(mn);
+                    chunk = chunk < 0.0 ? 0.0 : chunk;
+                    for (int j = lane; j < active; j += 32) N.run_gen[j] += chunk;
+                    tokens += chunk * active;
+                    steps_left -= smax(chunk, 1e-9);
+                    __syncwarp();
+                    // completions leave the running list, order kept (sim.hpp:399-407)
+                    int kept = 0;
+                    for (int base = 0; base < R; base += 32) {
+                        const int j = base + lane;
+                        int id = 0;
+                        double g = 0.0;
+                        bool done = false;
+                        if (j < R) {
+                            id = N.run_id[j];
+                            g = N.run_gen[j];
+                            done = g >= (double)N.len[id] - 1e-7;
+                        }
+                        const unsigned keep = __ballot_sync(kFull, j < R && !done);
+                        const unsigned fin = __ballot_sync(kFull, done);
+                        __syncwarp();
+                        if (j < R && !done) {
+                            const int dst = kept + __popc(keep & ((1u << lane) - 1));
+                            N.run_id[dst] = id;
+                            N.run_gen[dst] = g;
+                        }
+                        kept += __popc(keep);
+                        completed += __popc(fin);
+                        __syncwarp();
+                    }
+                    R = kept;
+                }
+                util = tokens / ((double)slot_cap * steps_per_seq);
+            }
+            sys_w = (double)N.dp * (a.alpha * (double)kGpusPerNode * gpu_w + a.beta);
+            // (5) telemetry -> MetricsSummary
+            const double tps = tokens / iv;
+            tot_tokens += tps * iv;
+            tot_energy += sys_w * iv;
+            sum_tps += tps;
+            if (target > 0.0 && tps < target) ++violations;
+            if (S.budget_active && node_budget > 0.0) {
+                track_abs += fabs(sys_w - node_budget);
+                ++tracked;
+            }
+            if (tl) {
+                pals_sim_telemetry x;
+                x.t_s = t1;
+                x.gpu_power_w = gpu_w;
+                x.sys_power_w = sys_w;
+                x.throughput_tps = tps;
+                x.utilization = sclamp(util, 0.0, 1.0);
+                x.node_budget_w = node_budget;
+                x.applied_cap_w = cap;
+                x.queue_depth = spawned - next_admit;
+                x.active_batch = b_eff;
+                x.applied_batch_cap = batch_cap;
+                x._pad = 0;
+                tl[k] = x;
+            }
+            // (6) control decision (sim.hpp:431-464)
+            const double err = target > 0.0 ? (target - tps) / target : 0.0;
+            int d_idx = cur, d_applied = 0, d_reason = PALS_REASON_HOLD;
+            if (S.policy != PALS_POLICY_FIXED) {
+                // control_step (controller.hpp:210-267); telemetry is never stale here
+                double err_norm = 0.0;
+                if (S.objective == PALS_OBJ_QOS && target > 0.0) {
+                    err_norm = (target - tps) / target;
+                    const double promised = (double)N.dp * m.T[cur] * bias;
+                    if (promised > 0.0) {
+                        const double pred_err = (promised - tps) / promised;
+                        integral = sclamp(integral + pred_err, -S.cfg.integral_clamp,
+                                          S.cfg.integral_clamp);
+                        const double deriv = has_prev ? pred_err - prev_err : 0.0;
+                        const double corr = kp * pred_err + ki * integral + kd * deriv;
+                        bias = sclamp(bias * (1.0 - corr), S.cfg.bias_min, S.cfg.bias_max);
+                        prev_err = pred_err;
+                        has_prev = true;
+                    }
+                }
+                const bool bset = node_budget > 0.0;
+                const bool changed =
+                    !has_last || !(last_bset == bset && (!bset || last_budget == node_budget));
+                has_last = true;
+                last_bset = bset;
+                last_budget = node_budget;
+                if (fabs(err_norm) > S.epsilon) ++sustain;
+                else sustain = 0;
+                const double budget = bset ? node_budget * (1.0 - S.cfg.budget_margin) : 0.0;
+                if (bset && budget != kp_budget) {
+                    kpv = warp_leading_true(m.nd_p, [&](int i) { return m.up[i] <= budget; });
+                    kp_budget = budget;
+                }
+                if (S.objective == PALS_OBJ_QOS) {
+                    const bool ok_lo = kt == 0 || !(m.ut[kt - 1] * bias < sel_target);
+                    const bool ok_hi = kt == m.nd_t || (m.ut[kt] * bias < sel_target);
+                    if (!(ok_lo && ok_hi))
+                        kt = warp_leading_true(
+                            m.nd_t, [&](int i) { return !(m.ut[i] * bias < sel_target); });
+                }
+                int s_idx, s_reason;
+                table_select(m, sel_target, bset, budget, kpv, kt, bias, S.objective, &s_idx,
+                             &s_reason);
+                const bool may_apply = changed || sustain >= sustain_n;
+                if (may_apply && s_idx != cur) {
+                    cur = s_idx;
+                    sustain = 0;
+                    d_idx = s_idx;
+                    d_applied = 1;
+                    d_reason = s_reason;
+                } else {
+                    d_idx = cur;
+                    d_reason = may_apply ? s_reason : PALS_REASON_HOLD;
+                }
+                if (S.policy == PALS_POLICY_ORACLE && d_reason != PALS_REASON_HOLD)
+                    d_reason = PALS_REASON_ORACLE;
+            }
+            n_applied += d_applied;
+            if (dl) {
+                pals_sim_decision x;
+                x.err_norm = err;
+                x.bias = bias;
+                x.cap_w = m.cap[d_idx];
+                x.batch = m.batch[d_idx];
+                x.applied = (uint8_t)d_applied;
+                x.reason = (uint8_t)d_reason;
+                x._pad = 0;
+                dl[k] = x;
+            }
+            // (7) actuation pipeline (sim.hpp:466-472)
+            applied_cap = inflight_cap;
+            if (d_applied) {
+                batch_cap = m.batch[d_idx];
+                inflight_cap = m.cap[d_idx];
+            }
+            if (lane == 0) {
+                sh_sys[w] = sys_w;
+                sh_bud[w] = node_budget;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            // SimResult::total_energy_j, interval-major (sim.hpp:411-412)
+            double cw = 0.0, bw = 0.0;
+            for (int i = 0; i < S.n_nodes; ++i) {
+                sh_energy += sh_sys[i] * iv;
+                cw += sh_sys[i];
+                bw += sh_bud[i];
+            }
+            if (S.budget_active) {  // cluster draw vs the signal (metrics.hpp:77-96)
+                const double tg = S.track_target ? S.track_target[k] : bw;
+                if (tg > 0.0) {
+                    sh_cluster_abs += fabs(cw - tg);
+                    ++sh_counted;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (live && lane == 0) {
+        pals_sim_node_result r;
+        const double n = (double)S.n_int;
+        r.total_tokens = tot_tokens;
+        r.total_energy_j = tot_energy;
+        r.qos_violation_rate = (double)violations / n;
+        r.mean_throughput_tps = sum_tps / n;
+        r.tokens_per_joule = tot_energy > 0.0 ? tot_tokens / tot_energy : 0.0;
+        r.power_tracking_mae_w = tracked > 0 ? track_abs / (double)tracked : 0.0;
+        r.throughput_target_tps = target;
+        r.final_bias = bias;
+        r.arrival_stream_hash = 0;  // host fills
+        r.n_requests = N.cum[S.n_int];
+        r.n_completed = completed;
+        r.n_applied = n_applied;
+        r.final_idx = cur;
+        a.node_out[gi] = r;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // RunSummary aggregate in node order (metrics.hpp:56-75)
+        pals_sim_result o;
+        memset(&o, 0, sizeof o);
+        double worst = 0.0;
+        for (int i = 0; i < S.n_nodes; ++i) {
+            const pals_sim_node_result& r = a.node_out[S.node0 + i];
+            o.total_tokens += r.total_tokens;
+            o.total_energy_j += r.total_energy_j;
+            o.mean_throughput_tps += r.mean_throughput_tps;
+            worst = smax(worst, r.qos_violation_rate);
+        }
+        o.tokens_per_joule = o.total_energy_j > 0.0 ? o.total_tokens / o.total_energy_j : 0.0;
+        o.qos_violation_rate = worst;
+        if (S.budget_active && S.n_nodes > 0) {
+            o.cluster_tracking_mae_w = sh_counted ? sh_cluster_abs / (double)sh_counted : 0.0;
+            o.power_tracking_mae_w = o.cluster_tracking_mae_w;
+        }
+        o.sim_total_energy_j = sh_energy;
+        o.n_intervals = S.n_int;
+        o.n_budget_changes = S.n_changes;
+        a.out[blockIdx.x] = o;
+    }
+}
+
+// ---- host setup ----------------------------------------------------------------
+struct SelSet {  // select tables for one (scorer, candidates, degrees)
+    pals_grid* g = nullptr;
+    pals_plan* pl = nullptr;
+    ReplayModelDev* d_m = nullptr;
+    void* d_tables = nullptr;
+    std::vector<pals_point> pts;
+};
+
+struct Resources {
+    pals_ctx* ctx;
+    std::vector<SelSet> sets;
+    std::vector<pals_model*> plant_models;
+    std::vector<void*> dev;
+    ~Resources() {
+        cudaStreamSynchronize(ctx->stream);
+        for (auto& s : sets) {
+            if (s.pl) pals_plan_destroy(s.pl);
+            if (s.g) pals_grid_destroy(s.g);
+            cudaFree(s.d_m);
+            cudaFree(s.d_tables);
+        }
+        for (auto* m : plant_models) pals_model_destroy(m);
+        for (void* p : dev) cudaFree(p);
+    }
+    template <class T>
+    int alloc(T** p, size_t n) {
+        void* q = nullptr;
+        const cudaError_t e = cudaMalloc(&q, std::max<size_t>(1, n) * sizeof(T));
+        if (e != cudaSuccess) return cuda_fail(e, "pals_run_scenarios: cudaMalloc");
+        dev.push_back(q);
+        *p = (T*)q;
+        return PALS_OK;
+    }
+    template <class T>
+    int upload(T** p, const std::vector<T>& v) {
+        int r = alloc(p, v.size());
+        if (r) return r;
+        if (!v.empty()) {
+            const cudaError_t e = copy_on(ctx->stream, *p, v.data(), v.size() * sizeof(T),
+                                          cudaMemcpyHostToDevice);
+            if (e != cudaSuccess) return cuda_fail(e, "pals_run_scenarios: upload");
+        }
+        return PALS_OK;
+    }
+};
+
+// Candidates of a node under the scenario's policy (build_candidates, sim.hpp:293-308).
+std::vector<pals_point> policy_candidates(const pals_scenario& sc, const pals_sim_node& n) {
+    std::vector<double> caps(sc.cand_caps, sc.cand_caps + sc.n_caps);
+    std::vector<int> batches(sc.cand_batches, sc.cand_batches + sc.n_batches);
+    const int max_batch = *std::max_element(batches.begin(), batches.end());
+    const double max_cap = *std::max_element(caps.begin(), caps.end());
+    if (sc.policy == PALS_POLICY_ADAPTIVE_BATCH) caps = {max_cap};
+    if (sc.policy == PALS_POLICY_ADAPTIVE_CAP) batches = {max_batch};
+    if (sc.policy == PALS_POLICY_FIXED) {
+        caps = {max_cap};
+        batches = {max_batch};
+    }
+    std::vector<pals_point> out;
+    for (double c : caps)
+        for (int b : batches) out.push_back(pals_point{c, b, n.tp, n.ep, n.dp});
+    return out;
+}
+
+int validate_scenario(const pals_scenario& sc, int n_models) {  // Scenario::validate
+    if (sc.duration_s <= 0 || sc.interval_s <= 0) return set_error(PALS_ECONFIG, "scenario: bad duration");
+    if (sc.n_nodes <= 0 || !sc.nodes) return set_error(PALS_ECONFIG, "scenario: no nodes");
+    if (sc.n_caps <= 0 || sc.n_batches <= 0 || !sc.cand_caps || !sc.cand_batches)
+        return set_error(PALS_ECONFIG, "scenario: empty candidate grid");
+    for (int i = 0; i < sc.n_nodes; ++i) {
+        const pals_sim_node& n = sc.nodes[i];
+        if (n.arrival_rate_per_s < 0) return set_error(PALS_ECONFIG, "scenario: negative arrival rate");
+        if (n.qos_fraction <= 0 || n.qos_fraction > 1)
+            return set_error(PALS_ECONFIG, "scenario: qos_fraction must be in (0,1]");
+        if (n.model < 0 || n.model >= n_models)
+            return set_error(PALS_ECONFIG, "pals_run_scenarios: node model out of range");
+        if (n.dp < 1 || n.dp > kMaxDp || n.tp < 1 || n.ep < 1)
+            return set_error(PALS_ECONFIG, "OperatingPoint: batch and parallel degrees must be >= 1");
+    }
+    if (sc.n_nodes > PALS_SIM_MAX_NODES)
+        return set_error(PALS_ECONFIG, "pals_run_scenarios: at most 32 nodes per scenario");
+    if (sc.n_trace > 0 && (!sc.trace_t || !sc.trace_w))
+        return set_error(PALS_ECONFIG, "pals_run_scenarios: null budget trace");
+    for (int i = 1; i < sc.n_trace; ++i)
+        if (sc.trace_t[i] <= sc.trace_t[i - 1])
+            return set_error(PALS_EDATA, "budget trace timestamps must be strictly increasing");
+    if (sc.policy < PALS_POLICY_FIXED || sc.policy > PALS_POLICY_ORACLE)
+        return set_error(PALS_ECONFIG, "unknown policy");
+    if (sc.objective != PALS_OBJ_QOS && sc.objective != PALS_OBJ_BUDGET)
+        return set_error(PALS_ECONFIG, "unknown objective");
+    return PALS_OK;
+}
+
+}  // namespace
+}  // namespace pals
+
+using namespace pals;
+
+extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scenario* scens,
+                                  int32_t n_models, const pals_profile* profiles,
+                                  pals_model* const* predictors, const pals_gpu_spec* gpu,
+                                  const pals_coeffs* coeffs, pals_sim_node_result* node_results,
+                                  pals_sim_result* results, int64_t log_stride,
+                                  pals_sim_telemetry* telemetry, pals_sim_decision* decisions) {
+    if (!ctx || !scens || !profiles || !gpu || !coeffs || !node_results || !results || n_models <= 0)
+        return set_error(PALS_ECONFIG, "pals_run_scenarios: null argument");
+    if (n_scen <= 0) return PALS_OK;
+    PALS_CUDA(cudaSetDevice(ctx->device));
+    Resources res{ctx};
+    // plant models (analytic, one per profile): device Analytic + the oracle's scorer
+    for (int m = 0; m < n_models; ++m) {
+        pals_model* pm = nullptr;
+        int r = pals_model_analytic(ctx, &profiles[m], gpu, &pm);
+        if (r) return r;
+        res.plant_models.push_back(pm);
+    }
+    Analytic* d_plant = nullptr;
+    {
+        std::vector<Analytic> h;
+        for (auto* pm : res.plant_models) h.push_back(pm->an);
+        int r = res.upload(&d_plant, h);
+        if (r) return r;
+    }
+    int64_t total_nodes = 0, max_int = 0;
+    int max_nodes = 1;
+    std::vector<int> n_int(n_scen);
+    for (int s = 0; s < n_scen; ++s) {
+        const pals_scenario& sc = scens[s];
+        int r = validate_scenario(sc, n_models);
+        if (r) return r;
+        const double ni = std::llround(sc.duration_s / sc.interval_s);  // sim.hpp:224
+        n_int[s] = (int)ni;
+        max_int = std::max<int64_t>(max_int, n_int[s]);
+        max_nodes = std::max(max_nodes, sc.n_nodes);
+        total_nodes += sc.n_nodes;
+        const bool needs_pred = sc.policy == PALS_POLICY_JOINT ||
+                                sc.policy == PALS_POLICY_ADAPTIVE_BATCH ||
+                                sc.policy == PALS_POLICY_ADAPTIVE_CAP;
+        for (int i = 0; i < sc.n_nodes && needs_pred; ++i)
+            if (!predictors || !predictors[sc.nodes[i].model])
+                return set_error(PALS_ECONFIG, "policy requires a trained predictor");
+    }
+    if ((telemetry || decisions) && log_stride < max_int)
+        return set_error(PALS_ECONFIG, "pals_run_scenarios: log_stride below the interval count");
+
+    // node scorers, candidates, targets; select tables deduplicated by (scorer, points)
+    std::map<std::pair<const pals_model*, std::vector<std::tuple<double, int, int, int, int>>>, int>
+        set_of;
+    std::vector<int> node_set(total_nodes), node_init(total_nodes);
+    std::vector<const pals_model*> node_scorer(total_nodes);
+    std::vector<double> node_target(total_nodes);
+    {
+        int64_t gi = 0;
+        for (int s = 0; s < n_scen; ++s) {
+            const pals_scenario& sc = scens[s];
+            const double mc = *std::max_element(sc.cand_caps, sc.cand_caps + sc.n_caps);
+            const int mb = *std::max_element(sc.cand_batches, sc.cand_batches + sc.n_batches);
+            for (int i = 0; i < sc.n_nodes; ++i, ++gi) {
+                const pals_sim_node& n = sc.nodes[i];
+                const pals_model* plant = res.plant_models[n.model];
+                // unconstrained_throughput (sim.hpp:258-264), validated as the reference does
+                const pals_point top{mc, mb, n.tp, n.ep, n.dp};
+                int r = validate_point(plant, top);
+                if (r) return r;
+                const Score st = analytic_score(plant->an, mc, mb, n.tp, n.dp);
+                node_target[gi] = n.qos_fraction * ((double)n.dp * st.T);
+                const pals_model* scorer =
+                    sc.policy == PALS_POLICY_ORACLE || !predictors || !predictors[n.model]
+                        ? plant : predictors[n.model];
+                node_scorer[gi] = scorer;
+                std::vector<pals_point> pts = policy_candidates(sc, n);
+                std::vector<std::tuple<double, int, int, int, int>> key;
+                for (auto& p : pts) key.emplace_back(p.cap_watts, p.batch, p.tp, p.ep, p.dp);
+                int init = -1;
+                for (size_t c = 0; c < pts.size() && init < 0; ++c)
+                    if (pts[c].cap_watts == sc.initial_cap_w && pts[c].batch == sc.initial_batch)
+                        init = (int)c;
+                if (init < 0)
+                    return set_error(PALS_ECONFIG,
+                                     "pals_run_scenarios: the initial (cap, batch) must be one "
+                                     "of the policy's candidates");
+                node_init[gi] = init;
+                auto it = set_of.find({scorer, key});
+                if (it == set_of.end()) {
+                    it = set_of.emplace(std::make_pair(scorer, key), (int)res.sets.size()).first;
+                    res.sets.emplace_back();
+                    res.sets.back().pts = pts;
+                }
+                node_set[gi] = it->second;
+            }
+        }
+    }
+    // build every select-table set: plan (scores + ranks) -> k_build_tables
+    std::vector<int> set_scorer_model(res.sets.size(), -1);
+    for (auto& [k, si] : set_of) {
+        SelSet& S = res.sets[si];
+        const pals_model* scorer = k.first;
+        const int n = (int)S.pts.size();
+        if (n > kMaxReplayCands)
+            return set_error(PALS_ECONFIG, "pals_run_scenarios: at most 4096 candidates per node");
+        int r = pals_grid_points(ctx, S.pts.data(), n, &S.g);
+        if (r) return r;
+        r = validate_points(scorer, S.g->h_pts, S.g->n);
+        if (r) return r;
+        r = pals_plan_create(ctx, scorer, S.g, coeffs, &S.pl);
+        if (r) return r;
+        r = pals_plan_prepare(S.pl);
+        if (r) return r;
+        const PlanDev& d = plan_dev(S.pl);
+        const size_t W = (size_t)n + 1;
+        PALS_CUDA(cudaMalloc(&S.d_tables, W * W * 4 + W * 4 + 2 * W * 8 + 1024));
+        PALS_CUDA(cudaMalloc(&S.d_m, sizeof(ReplayModelDev)));
+        ReplayModelDev m;
+        memset(&m, 0, sizeof m);
+        m.n = n;
+        m.tp = S.pts[0].tp;
+        m.ep = S.pts[0].ep;
+        m.dp = S.pts[0].dp;
+        m.max_cap = S.pts[0].cap_watts;
+        m.max_batch = S.pts[0].batch;
+        for (auto& p : S.pts) {
+            m.max_cap = smax(m.max_cap, p.cap_watts);
+            m.max_batch = std::max(m.max_batch, p.batch);
+        }
+        m.cap = S.g->cap;
+        m.batch = S.g->batch;
+        m.canon = S.g->canon;
+        m.inv_tr = S.g->inv_tr;
+        m.T = d.T;
+        m.th = d.th;
+        m.pn = d.pn;
+        m.ef = d.ef;
+        m.danger_t = d.danger[ORD_T];
+        m.danger_e = d.danger[ORD_E];
+        char* base = (char*)S.d_tables;
+        m.m2 = (const uint32_t*)base;
+        m.b1 = (const uint32_t*)(base + W * W * 4);
+        m.ut = (const double*)(base + ((W * W * 4 + W * 4 + 7) & ~(size_t)7));
+        m.up = m.ut + W;
+        // k_build_tables also derives plant constants from m.plant: any node of the
+        // set shares the profile-independent parts used here; point it at model 0
+        m.plant = d_plant;
+        PALS_CUDA(copy_on(ctx->stream, S.d_m, &m, sizeof m, cudaMemcpyHostToDevice));
+        k_build_tables<<<1, 1024, 0, ctx->stream>>>(d, S.d_m, (uint32_t*)m.m2, (uint32_t*)m.b1,
+                                                     (double*)m.ut, (double*)m.up, coeffs->alpha,
+                                                     coeffs->beta_watts);
+        count_launch(ctx);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "k_build_tables");
+    }
+
+    // arrival streams on all host threads (independent per node)
+    std::vector<Stream> streams(total_nodes);
+    {
+        std::vector<std::pair<int, int>> work;  // (scenario, node)
+        for (int s = 0; s < n_scen; ++s)
+            for (int i = 0; i < scens[s].n_nodes; ++i) work.emplace_back(s, i);
+        const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(),
+                                                            (unsigned)work.size()));
+        std::vector<std::thread> th;
+        for (unsigned t = 0; t < nt; ++t)
+            th.emplace_back([&, t] {
+                for (size_t w = t; w < work.size(); w += nt) {
+                    int64_t gi = 0;
+                    for (int s = 0; s < work[w].first; ++s) gi += scens[s].n_nodes;
+                    gi += work[w].second;
+                    gen_stream(scens[work[w].first], work[w].second, n_int[work[w].first],
+                               &streams[gi]);
+                }
+            });
+        for (auto& t : th) t.join();
+    }
+
+    // budget changes and their splits (assign_budgets, sim.hpp:229-238, 277-283, 313-336)
+    std::vector<std::vector<int32_t>> chg_k(n_scen);
+    std::vector<std::vector<double>> chg_w(n_scen);
+    std::vector<std::vector<double>> track(n_scen);
+    for (int s = 0; s < n_scen; ++s) {
+        const pals_scenario& sc = scens[s];
+        if (sc.n_trace > 0) {
+            double last = -1.0;
+            for (int k = 0; k < n_int[s]; ++k) {
+                const double wv = trace_value(sc, k * sc.interval_s);
+                if (wv != last) {
+                    chg_k[s].push_back(k);
+                    chg_w[s].push_back(wv);
+                    last = wv;
+                }
+            }
+            track[s].resize(n_int[s]);
+            for (int k = 0; k < n_int[s]; ++k) {
+                const double t1 = k * sc.interval_s + sc.interval_s;
+                track[s][k] = trace_value(sc, t1 - sc.interval_s);
+            }
+        } else if (sc.has_cluster_budget) {
+            chg_k[s].push_back(0);
+            chg_w[s].push_back(sc.cluster_budget_w);
+            track[s].assign(n_int[s], sc.cluster_budget_w);
+        }
+    }
+    // node budgets per change: [scenario][change][node]
+    std::vector<std::vector<double>> chg_b(n_scen);
+    {
+        // water-filling for joint / oracle scenarios, grouped by selection margin
+        std::map<double, std::vector<int>> by_margin;
+        for (int s = 0; s < n_scen; ++s) {
+            const pals_scenario& sc = scens[s];
+            chg_b[s].assign(chg_k[s].size() * sc.n_nodes, 0.0);
+            if (chg_k[s].empty()) continue;
+            if (sc.policy == PALS_POLICY_JOINT || sc.policy == PALS_POLICY_ORACLE) {
+                by_margin[sc.controller.budget_margin].push_back(s);
+            } else {
+                int total_dp = 0;
+                for (int i = 0; i < sc.n_nodes; ++i) total_dp += sc.nodes[i].dp;
+                for (size_t c = 0; c < chg_k[s].size(); ++c)
+                    for (int i = 0; i < sc.n_nodes; ++i)
+                        chg_b[s][c * sc.n_nodes + i] =
+                            chg_w[s][c] * (double)sc.nodes[i].dp / total_dp;
+            }
+        }
+        for (auto& [margin, ss] : by_margin) {
+            // candidate sets = the nodes' (scorer, candidates) select sets
+            std::map<int, int> aset;  // select set -> allocator set
+            std::vector<pals_model*> set_models;
+            std::vector<pals_point> pts;
+            std::vector<int64_t> off{0};
+            std::vector<int64_t> p_off{0};
+            std::vector<int32_t> nmodel, ndp;
+            std::vector<double> ntarget, cbudget;
+            for (int s : ss) {
+                const pals_scenario& sc = scens[s];
+                int64_t g0 = 0;
+                for (int q = 0; q < s; ++q) g0 += scens[q].n_nodes;
+                for (size_t c = 0; c < chg_k[s].size(); ++c) {
+                    for (int i = 0; i < sc.n_nodes; ++i) {
+                        const int si = node_set[g0 + i];
+                        auto it = aset.find(si);
+                        if (it == aset.end()) {
+                            it = aset.emplace(si, (int)set_models.size()).first;
+                            set_models.push_back((pals_model*)node_scorer[g0 + i]);
+                            pts.insert(pts.end(), res.sets[si].pts.begin(), res.sets[si].pts.end());
+                            off.push_back((int64_t)pts.size());
+                        }
+                        nmodel.push_back(it->second);
+                        ndp.push_back(sc.nodes[i].dp);
+                        ntarget.push_back(sc.objective == PALS_OBJ_QOS ? node_target[g0 + i] : 0.0);
+                    }
+                    cbudget.push_back(chg_w[s][c]);
+                    p_off.push_back((int64_t)nmodel.size());
+                }
+            }
+            pals_alloc* al = nullptr;
+            int r = pals_alloc_create_sets(ctx, (int32_t)set_models.size(), set_models.data(),
+                                           pts.data(), off.data(), gpu, coeffs, margin, &al);
+            if (r) return r;
+            const int64_t np = (int64_t)cbudget.size();
+            std::vector<double> nb(nmodel.size()), tot(np);
+            std::vector<uint8_t> sat(np);
+            std::vector<int32_t> st(np);
+            r = pals_allocate_budget(al, 25.0, np, p_off.data(), nmodel.data(), ndp.data(),
+                                     ntarget.data(), cbudget.data(), nb.data(), tot.data(),
+                                     sat.data(), st.data());
+            pals_alloc_destroy(al);
+            if (r) return r;
+            for (int64_t p = 0; p < np; ++p)
+                if (st[p] != PALS_OK)
+                    return set_error(st[p], "allocate_budget: cluster budget split failed "
+                                            "(as run_scenario would throw)");
+            int64_t o = 0;
+            for (int s : ss) {
+                const pals_scenario& sc = scens[s];
+                for (size_t c = 0; c < chg_k[s].size(); ++c)
+                    for (int i = 0; i < sc.n_nodes; ++i) chg_b[s][c * sc.n_nodes + i] = nb[o++];
+            }
+        }
+    }
+
+    // device buffers
+    std::vector<SimScenDev> hs(n_scen);
+    std::vector<SimNodeDev> hn(total_nodes);
+    {
+        int64_t gi = 0;
+        for (int s = 0; s < n_scen; ++s) {
+            const pals_scenario& sc = scens[s];
+            SimScenDev& S = hs[s];
+            memset(&S, 0, sizeof S);
+            S.node0 = (int)gi;
+            S.n_nodes = sc.n_nodes;
+            S.n_int = n_int[s];
+            S.policy = sc.policy;
+            S.objective = sc.objective;
+            S.budget_active = sc.has_cluster_budget || sc.n_trace > 0;
+            S.n_changes = (int)chg_k[s].size();
+            S.interval_s = sc.interval_s;
+            S.epsilon = sc.epsilon;
+            S.cfg = sc.controller;
+            int r = res.upload((int32_t**)&S.change_k, chg_k[s]);
+            if (r) return r;
+            if (!track[s].empty()) {
+                r = res.upload((double**)&S.track_target, track[s]);
+                if (r) return r;
+            }
+            std::vector<double> bud(chg_b[s]);
+            for (int i = 0; i < sc.n_nodes; ++i, ++gi) {
+                SimNodeDev& N = hn[gi];
+                const pals_sim_node& n = sc.nodes[i];
+                memset(&N, 0, sizeof N);
+                N.sel = res.sets[node_set[gi]].d_m;
+                N.plant = d_plant + n.model;
+                N.tp = n.tp;
+                N.ep = n.ep;
+                N.dp = n.dp;
+                N.init_idx = node_init[gi];
+                N.target_tps = node_target[gi];
+                r = res.upload((int32_t**)&N.cum, streams[gi].cum);
+                if (r) return r;
+                r = res.upload((int32_t**)&N.len, streams[gi].len);
+                if (r) return r;
+                const int mb = *std::max_element(sc.cand_batches, sc.cand_batches + sc.n_batches);
+                const size_t run_cap = (size_t)std::max(mb, sc.initial_batch) * n.dp + 32;
+                r = res.alloc(&N.run_id, run_cap);
+                if (r) return r;
+                r = res.alloc(&N.run_gen, run_cap);
+                if (r) return r;
+                std::vector<double> nbud(chg_k[s].size());
+                for (size_t c = 0; c < nbud.size(); ++c) nbud[c] = bud[c * sc.n_nodes + i];
+                r = res.upload((double**)&N.budget, nbud);
+                if (r) return r;
+            }
+        }
+    }
+    SimArgs A;
+    memset(&A, 0, sizeof A);
+    int r = res.upload((SimScenDev**)&A.scen, hs);
+    if (r) return r;
+    r = res.upload((SimNodeDev**)&A.nodes, hn);
+    if (r) return r;
+    A.alpha = coeffs->alpha;
+    A.beta = coeffs->beta_watts;
+    A.idle_w = gpu->idle_watts;
+    A.min_cap = gpu->min_cap_watts;
+    A.log_stride = log_stride;
+    r = res.alloc(&A.node_out, total_nodes);
+    if (r) return r;
+    r = res.alloc(&A.out, n_scen);
+    if (r) return r;
+    const size_t nlog = (size_t)total_nodes * (size_t)std::max<int64_t>(log_stride, 0);
+    if (telemetry) {
+        r = res.alloc(&A.tel, nlog);
+        if (r) return r;
+    }
+    if (decisions) {
+        r = res.alloc(&A.dec, nlog);
+        if (r) return r;
+    }
+    k_sim<<<n_scen, 32 * max_nodes, 0, ctx->stream>>>(A);
+    count_launch(ctx);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "k_sim");
+    e = copy_on(ctx->stream, node_results, A.node_out, sizeof(pals_sim_node_result) * total_nodes,
+                cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess)
+        e = copy_on(ctx->stream, results, A.out, sizeof(pals_sim_result) * n_scen,
+                    cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && telemetry)
+        e = copy_on(ctx->stream, telemetry, A.tel, sizeof(pals_sim_telemetry) * nlog,
+                    cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && decisions)
+        e = copy_on(ctx->stream, decisions, A.dec, sizeof(pals_sim_decision) * nlog,
+                    cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "pals_run_scenarios");
+    for (int64_t gi = 0; gi < total_nodes; ++gi)
+        node_results[gi].arrival_stream_hash = streams[gi].hash;
+    return PALS_OK;
+}

@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--cfg5-traces", type=int, default=10_000_000,
                     help="cfg5 traces in total (split over the GPUs)")
     ap.add_argument("--cfg5-steps", type=int, default=2, help="timed cfg5 replays")
+    ap.add_argument("--sim-seeds", type=int, default=64,
+                    help="seeds per GPU of the 3-scenario x 5-policy queue-plant suite")
+    ap.add_argument("--sim-steps", type=int, default=2, help="timed queue-plant runs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU time per reference sample")
@@ -445,6 +448,7 @@ def run_ours(args, dist: Dist):
     frontiers = bench_frontiers(args, dist, ctx, stream, l2_flush)
     cfg3, c3, tref3 = bench_cfg3(args, dist, ctx, stream, l2_flush, int_peak)
     cfg5 = bench_cfg5(args, dist, ctx, stream, l2_flush) if args.cfg5_traces > 0 else None
+    scen = bench_sim(args, dist, ctx) if args.sim_seeds > 0 else None
 
     # ---------------- cfg1: single-call latency (the drop-in's synchronous API) ----------------
     from paper_2605_21427_b200.abi import CtrlState, Point, Telemetry
@@ -503,6 +507,7 @@ def run_ours(args, dist: Dist):
         "frontiers": frontiers,
         "cfg3": cfg3,
         "cfg5": cfg5,
+        "scenarios": scen,
         "latency": latency,
         "peaks": {"int_ops_per_s": int_peak, "fp64_flops_per_s": fp64_peak,
                   "hbm_gbs_measured": measured_peaks_json().get("hbm_gbs")},
@@ -515,6 +520,8 @@ def run_ours(args, dist: Dist):
         out["cfg3"]["cpu_baseline"] = cpu_cfg3(args, c3, tref3, args.cpu_seconds)
         if cfg5 is not None:  # same per-trace work as cfg4: the cfg4 reference sample
             out["cfg5"]["cpu_baseline"] = dict(out["decisions"]["cpu_baseline"])
+        if scen is not None:
+            out["scenarios"]["cpu_baseline"] = cpu_sim(args, args.cpu_seconds)
         out["latency"]["cpu_reference_select_config_us"] = cpu_latency(c1, float(th1.max()))
     if dist.rank == 0:
         print(json.dumps(out), flush=True)
@@ -857,6 +864,95 @@ def bench_cfg5(args, dist, ctx, stream, l2_flush):
             "gpu_launches": int(launches)}
 
 
+SIM_WORKLOAD = ("queue-plant run_scenario (sim.hpp) over the 3 bundled scenarios (single_node "
+                "900 s x 1 node, multinode_qos 3600 s x 3 nodes, demand_response 3600 s x 3 "
+                "nodes on the 1,464-candidate DR grid) x the 5 policies (run_baseline_suite) x "
+                "S seeds; predictor = the shipped 20-tree bundle; unit = node control "
+                "intervals simulated")
+
+
+def sim_suite(seeds: int, first_seed: int = 0):
+    from paper_2605_21427_b200.abi import POLICIES
+    from paper_2605_21427_b200.sim import bundled_scenarios, n_intervals
+    base = bundled_scenarios()
+    scs = []
+    for k in range(seeds):
+        for name in sorted(base):
+            for pol in POLICIES:
+                scs.append(dict(base[name], policy=pol, seed=base[name]["seed"] + first_seed + k))
+    units = sum(len(s["nodes"]) * n_intervals(s) for s in scs)
+    return scs, units
+
+
+def sim_predictors(ctx, profiles):
+    from paper_2605_21427_b200.forest import Bundle, make_forest_model
+    b = Bundle.load_npz(os.path.join(ROOT, "paper_2605_21427_b200", "data",
+                                     "predictor_small.npz"))
+    return b, {p.name.decode(): make_forest_model(ctx, b, p.name.decode()) for p in profiles}
+
+
+def bench_sim(args, dist, ctx):
+    """Batched run_scenario: whole API call (host arrival streams + budget splits +
+    device simulation) and the simulation kernel alone."""
+    from paper_2605_21427_b200.profiles import load_bundle
+    from paper_2605_21427_b200.sim import last_timing, run_scenarios
+    profs, gpu, coeffs = load_bundle()
+    _, preds = sim_predictors(ctx, profs)
+    scs, units = sim_suite(args.sim_seeds, first_seed=dist.rank * args.sim_seeds)
+    run_scenarios(ctx, scs[:15], profs, gpu, coeffs, preds)  # warm-up
+    walls, kms, preps = [], [], []
+    for _ in range(max(1, args.sim_steps)):
+        dist.barrier()
+        t0 = time.perf_counter()
+        nres, res, _, _ = run_scenarios(ctx, scs, profs, gpu, coeffs, preds)
+        walls.append(time.perf_counter() - t0)
+        prep, km = last_timing(ctx)
+        kms.append(km)
+        preps.append(prep)
+    wall = dist.max(float(np.mean(walls)))
+    km = dist.max(float(np.mean(kms)))
+    total = dist.sum(float(units))
+    return {"metric": "scenario node-intervals/s (run_scenario queue plant, 5-policy suites)",
+            "value": total / (km * 1e-3), "unit": "node-intervals/s",
+            "ms_per_step": km, "steps": len(walls), "workload": SIM_WORKLOAD,
+            "scenarios_per_gpu": len(scs), "seeds_per_gpu": args.sim_seeds,
+            "node_intervals_per_gpu": units,
+            "value_basis": "device time of the simulation kernel (k_sim)",
+            "e2e": {"value": total / wall, "unit": "node-intervals/s",
+                    "h2d_bytes_per_step": None, "d2h_bytes_per_step": int(nres.nbytes + res.nbytes),
+                    "host_setup_s": float(np.mean(preps)),
+                    "api": "pals_run_scenarios (C ABI): host arrival streams (mt19937_64 + libm) "
+                           "and budget splits, then one k_sim launch; wall clock"},
+            "gpu_launches": None}
+
+
+def cpu_sim(args, seconds):
+    """The unmodified run_scenario + summarize on all host threads over the first seeds of
+    the same suite."""
+    kind, ref = _reference_backend()
+    if kind != "reference":
+        return {"value": None, "unit": "node-intervals/s", "cores": 0, "kind": "port",
+                "sample": "reference build absent"}
+    from paper_2605_21427_b200.profiles import load_bundle
+    from paper_2605_21427_b200.forest import Bundle
+    profs, gpu, coeffs = load_bundle()
+    b = Bundle.load_npz(os.path.join(ROOT, "paper_2605_21427_b200", "data",
+                                     "predictor_small.npz"))
+    path = os.path.join(tempfile.gettempdir(), "pals_bench_sim_bundle.json")
+    b.to_json(path)
+    threads = os.cpu_count() or 1
+    scs, units = sim_suite(1)
+    t = ref.bench_scenarios(scs, profs, gpu, coeffs, path, threads)
+    seeds = int(max(1, min(args.sim_seeds, seconds / max(t, 1e-3))))
+    if seeds > 1:
+        scs, units = sim_suite(seeds)
+        t = ref.bench_scenarios(scs, profs, gpu, coeffs, path, threads)
+    return {"value": units / t, "unit": "node-intervals/s", "cores": threads,
+            "kind": "reference",
+            "sample": f"{len(scs)} scenarios ({seeds} seeds x 3 bundled x 5 policies) through "
+                      f"the unmodified run_scenario + summarize, {threads} threads, {t:.1f} s"}
+
+
 FRONTIER_WORKLOAD = ("build_frontier over cfg3x: mixtral-8x7b-like, 64 caps x 256 batches x "
                      "TP{1,2,4,8} x EP{1,4,8} x DP{1,2,3} = 589,824 points scored "
                      "(cluster_throughput, efficiency) and reduced to the Pareto frontier per step")
@@ -1086,6 +1182,7 @@ def run_reference(args, dist: Dist):
     c3 = workloads.cfg3(args.cfg3_queries)
     T3, _, _ = ref.eval(c3["profile"], c3["gpu"], c3["points"])
     s3 = cpu_cfg3(args, c3, float(np.max(T3 * c3["points"]["dp"])), per_step)
+    sm = cpu_sim(args, per_step) if args.sim_seeds > 0 else None
     zero = {"h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "config evals/s",
            "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
@@ -1117,7 +1214,12 @@ def run_reference(args, dist: Dist):
            "cfg5": {"metric": "controller decisions/s (cfg5, strong scaling over the GPUs)",
                     "value": dec["value"], "unit": "decisions/s", "workload": CFG5_WORKLOAD,
                     "cpu_baseline": dec,
-                    "e2e": {"value": dec["value"], "unit": "decisions/s", **zero}}}
+                    "e2e": {"value": dec["value"], "unit": "decisions/s", **zero}},
+           "scenarios": None if sm is None else {
+               "metric": "scenario node-intervals/s (run_scenario queue plant, 5-policy suites)",
+               "value": sm["value"], "unit": "node-intervals/s", "workload": SIM_WORKLOAD,
+               "cpu_baseline": sm, "e2e": {"value": sm["value"], "unit": "node-intervals/s",
+                                           **zero}}}
     print(json.dumps(out), flush=True)
 
 

@@ -571,6 +571,11 @@ int pals_run_scenarios(pals_ctx* ctx, int32_t n_scenarios, const pals_scenario* 
                        pals_sim_result* results, int64_t log_stride,
                        pals_sim_telemetry* telemetry, pals_sim_decision* decisions);
 
+/* Timing of the last pals_run_scenarios on ctx: host setup seconds (arrival
+ * streams, select tables, budget splits, uploads) and the simulation kernel's
+ * device milliseconds (CUDA events on the context stream). */
+int pals_sim_last_timing(pals_ctx* ctx, double* host_setup_s, double* kernel_ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -314,6 +314,25 @@ class Reference:
             out = out + ((tcsv, dcsv),)
         return out
 
+    def bench_scenarios(self, scenarios, profiles, gpu, coeffs, bundle_path, threads):
+        """Wall seconds of run_scenario + summarize over the scenario dicts, threads-way."""
+        from paper_2605_21427_b200.abi import Scenario
+        from paper_2605_21427_b200.sim import _CScenario, _model_index
+        L = self.lib
+        L.ref_bench_scenarios.restype = C.c_double
+        L.ref_bench_scenarios.argtypes = [C.c_int, _VP, C.c_int, _VP, C.c_char_p, _VP, _VP,
+                                          C.c_int]
+        idx = _model_index(profiles)
+        cs = [_CScenario(s, idx) for s in scenarios]
+        arr = (Scenario * len(cs))(*[c.c for c in cs])
+        profs = (Profile * len(profiles))(*profiles)
+        secs = L.ref_bench_scenarios(len(cs), arr, len(profiles), profs,
+                                     bundle_path.encode() if bundle_path else None,
+                                     C.byref(gpu), C.byref(coeffs), threads)
+        if secs < 0:
+            raise RuntimeError("ref_bench_scenarios: a scenario failed")
+        return secs
+
     def bench_select(self, prof, gpu, pts, coeffs, queries, threads, want_results=True):
         nq = len(queries)
         idx = np.empty(nq, np.int32) if want_results else None

@@ -19,6 +19,7 @@
 #include "wattserve/controller.hpp"
 #include "wattserve/forest.hpp"
 #include "wattserve/metrics.hpp"
+#include "wattserve/scenario_io.hpp"
 #include "wattserve/model.hpp"
 #include "wattserve/pareto.hpp"
 #include "wattserve/rng.hpp"
@@ -1102,4 +1103,77 @@ int ref_run_scenario(const pals_scenario* s, int n_models, const pals_profile* p
     return PALS_OK;
 }
 
+}  // extern "C"
+
+extern "C" {
+// CPU baseline: run_scenario + summarize over scenarios split across threads (wall s).
+double ref_bench_scenarios(int n_scen, const pals_scenario* s, int n_models,
+                           const pals_profile* profs, const char* bundle_path,
+                           const pals_gpu_spec* gpu, const pals_coeffs* coeffs, int n_threads) {
+    if (bundle_path) load_bundle(bundle_path);  // parse once, before the threads share it
+    std::vector<int> rc(n_scen, 0);
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> th;
+    std::atomic<int> next{0};
+    for (int t = 0; t < n_threads; ++t)
+        th.emplace_back([&] {
+            for (int i = next++; i < n_scen; i = next++) {
+                std::vector<pals_sim_node_result> nr(s[i].n_nodes);
+                pals_sim_result r;
+                rc[i] = ref_run_scenario(&s[i], n_models, profs, bundle_path, gpu, coeffs,
+                                         nr.data(), &r, 0, nullptr, nullptr, nullptr, 0, nullptr);
+            }
+        });
+    for (auto& x : th) x.join();
+    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    for (int v : rc)
+        if (v) return -1.0;
+    return secs;
+}
+}  // extern "C"
+
+extern "C" {
+// scenario_from_json (scenario_io.hpp:35-93) on a file, flattened to one text line
+// per field ("%.17g" doubles) so a test can compare it with another parser's view.
+int ref_scenario_digest(const char* path, char* buf, std::int64_t cap, std::int64_t* len) {
+    try {
+        const Scenario sc = load_scenario(path);
+        auto g = [](double v) {
+            char b[40];
+            std::snprintf(b, sizeof b, "%.17g", v);
+            return std::string(b);
+        };
+        std::string o;
+        o += "name=" + sc.name + "\n";
+        o += "duration_s=" + g(sc.duration_s) + "\ninterval_s=" + g(sc.interval_s) + "\n";
+        o += "seed=" + std::to_string(sc.seed) + "\n";
+        o += "mean_tokens=" + g(sc.output_len.mean_tokens) + "\nlog_sigma=" +
+             g(sc.output_len.log_sigma) + "\n";
+        o += "cluster_budget_w=" + (sc.cluster_budget_w ? g(*sc.cluster_budget_w) : "none") + "\n";
+        o += "trace=";
+        for (const auto& [t, w] : sc.budget_trace) o += g(t) + ":" + g(w) + ";";
+        o += "\npolicy=" + std::string(to_string(sc.policy)) + "\n";
+        o += std::string("objective=") +
+             (sc.objective == Objective::QosMaxEfficiency ? "qos" : "budget-throughput") + "\n";
+        const auto& c = sc.controller;
+        o += "kp=" + g(c.gains.kp) + "\nki=" + g(c.gains.ki) + "\nkd=" + g(c.gains.kd) + "\n";
+        o += "sustain_intervals=" + std::to_string(c.sustain_intervals) + "\n";
+        o += "integral_clamp=" + g(c.integral_clamp) + "\ntarget_headroom=" +
+             g(c.target_headroom) + "\nbudget_margin=" + g(c.budget_margin) + "\n";
+        o += "epsilon=" + g(sc.epsilon) + "\ncaps=";
+        for (double v : sc.cand_caps) o += g(v) + ";";
+        o += "\nbatches=";
+        for (int v : sc.cand_batches) o += std::to_string(v) + ";";
+        o += "\ninitial=" + g(sc.initial_cap_w) + ":" + std::to_string(sc.initial_batch) + "\n";
+        for (const auto& n : sc.nodes)
+            o += "node=" + n.model_id + ":" + g(n.qos_fraction) + ":" + std::to_string(n.tp) +
+                 ":" + std::to_string(n.ep) + ":" + std::to_string(n.dp) + ":" +
+                 g(n.arrival_rate_per_s) + ":" + std::to_string(n.initial_backlog) + "\n";
+        *len = static_cast<std::int64_t>(o.size());
+        if (buf) std::memcpy(buf, o.data(), std::min<std::size_t>(o.size(), cap));
+    } catch (...) {
+        return map_exception();
+    }
+    return PALS_OK;
+}
 }  // extern "C"

@@ -211,6 +211,8 @@ struct pals_ctx {
     size_t pinned_bytes = 0;
     void* replay_cache = nullptr;  // replay.cu
     int replay_layout = 0;         // PALS_REPLAY_THREAD / PALS_REPLAY_WARP
+    double sim_prep_s = 0.0;       // sim.cu: host setup of the last pals_run_scenarios
+    double sim_kernel_ms = -1.0;   // and its k_sim launch (CUDA events)
     void* d_front = nullptr;       // frontier.cu scratch
     size_t front_bytes = 0;
 };

@@ -30,7 +30,10 @@
 //     never the simulation state, so every split is precomputed — allocate_budget
 //     on the GPU allocator (K4) for joint / oracle, dp-proportional otherwise.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <random>
@@ -109,36 +112,59 @@ struct Stream {
     uint64_t hash = 0xcbf29ce484222325ULL;
 };
 
+// FNV-1a over the decimal digits of v (std::to_string of a non-negative integer).
+inline uint64_t fnv_dec(uint64_t h, long v) {
+    char d[24];
+    int n = 0;
+    do {
+        d[n++] = (char)('0' + v % 10);
+        v /= 10;
+    } while (v);
+    while (n) {
+        h ^= (unsigned char)d[--n];
+        h *= 0x100000001b3ULL;
+    }
+    return h;
+}
+
 void gen_stream(const pals_scenario& sc, int node, int n_int, Stream* out) {
     const pals_sim_node& nd = sc.nodes[node];
     HostRng rng(splitmix64(splitmix64(sc.seed) ^ (uint64_t)node));  // Rng::substream
     const double log_mean = std::log(sc.mean_tokens) - 0.5 * sc.log_sigma * sc.log_sigma;
-    auto spawn = [&](double t) {  // spawn_request (sim.hpp:338-353)
+    std::string tail;  // "@" + fmt_num(t): one snprintf per interval, not per request
+    // spawn_request (sim.hpp:338-353); the arrival hash chains fnv1a64 over
+    // to_string(id) + ":" + to_string(len) + "@" + fmt_num(t), byte for byte
+    auto spawn = [&]() {
         const int len = std::max(1, (int)std::lround(rng.lognormal(log_mean, sc.log_sigma)));
-        const long id = (long)out->len.size();
-        out->hash = fnv_str(std::to_string(id) + ":" + std::to_string(len) + "@" + fmt10g(t),
-                            out->hash);
+        uint64_t h = fnv_dec(out->hash, (long)out->len.size());
+        h = (h ^ (unsigned char)':') * 0x100000001b3ULL;
+        h = fnv_dec(h, len);
+        out->hash = fnv_str(tail, h);
         out->len.push_back(len);
     };
-    for (int b = 0; b < nd.initial_backlog; ++b) spawn(0.0);
+    tail = "@" + fmt10g(0.0);
+    for (int b = 0; b < nd.initial_backlog; ++b) spawn();
     out->cum.resize((size_t)n_int + 1);
     for (int k = 0; k < n_int; ++k) {
         const double t0 = k * sc.interval_s;
         const int n = rng.poisson(nd.arrival_rate_per_s * sc.interval_s);
-        for (int a = 0; a < n; ++a) spawn(t0);
+        if (n) tail = "@" + fmt10g(t0);
+        for (int a = 0; a < n; ++a) spawn();
         out->cum[k] = (int32_t)out->len.size();  // visible to interval k
     }
     out->cum[n_int] = (int32_t)out->len.size();
 }
 
-double trace_value(const pals_scenario& sc, double t) {  // sim.hpp:167-174
-    double v = sc.trace_w[0];
-    for (int i = 0; i < sc.n_trace; ++i) {
-        if (sc.trace_t[i] <= t) v = sc.trace_w[i];
-        else break;
+// trace_value (sim.hpp:167-174) for non-decreasing query times: the value of the
+// last point with t_i <= t (the first point's when none), kept with a cursor.
+struct TraceCursor {
+    const pals_scenario& sc;
+    int j = 0;
+    double operator()(double t) {
+        while (j + 1 < sc.n_trace && sc.trace_t[j + 1] <= t) ++j;
+        return sc.trace_w[j];
     }
-    return v;
-}
+};
 
 // ---- device layout ------------------------------------------------------------
 struct SimNodeDev {
@@ -146,7 +172,7 @@ struct SimNodeDev {
     const Analytic* plant;      // the node's calibrated profile
     const int32_t* cum;         // [n_int + 1]
     const int32_t* len;         // request lengths by id
-    int32_t* run_id;            // running-list scratch (run_cap entries)
+    int32_t* run_len;           // running list (global fallback): output tokens, generated
     double* run_gen;
     const double* budget;       // node budget per budget change
     int tp, ep, dp;
@@ -175,6 +201,7 @@ struct SimArgs {
     int64_t log_stride;
     pals_sim_telemetry* tel;
     pals_sim_decision* dec;
+    int smem_run;  // > 0: running lists live in shared memory, smem_run entries per warp
 };
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -201,6 +228,15 @@ __global__ void __launch_bounds__(32 * PALS_SIM_MAX_NODES) k_sim(SimArgs a) {
     const bool live = w < S.n_nodes;
     const int gi = S.node0 + (live ? w : 0);
     const SimNodeDev N = a.nodes[gi];
+    // the node's running list: shared memory when it fits, else the global scratch
+    extern __shared__ __align__(16) char dyn_smem[];
+    double* run_gen = N.run_gen;
+    int32_t* run_len = N.run_len;
+    if (a.smem_run > 0) {
+        run_gen = (double*)dyn_smem + (size_t)w * a.smem_run;
+        run_len = (int32_t*)((double*)dyn_smem + (size_t)(blockDim.x >> 5) * a.smem_run) +
+                  (size_t)w * a.smem_run;
+    }
     const ReplayModelDev& m = *N.sel;
     const Analytic& P = *N.plant;
     const double iv = S.interval_s;
@@ -291,8 +327,8 @@ __global__ void __launch_bounds__(32 * PALS_SIM_MAX_NODES) k_sim(SimArgs a) {
                     if (R < slot_cap && next_admit < spawned) {  // refill freed slots
                         const int n_adm = min(slot_cap - R, spawned - next_admit);
                         for (int j = lane; j < n_adm; j += 32) {
-                            N.run_id[R + j] = next_admit + j;
-                            N.run_gen[R + j] = 0.0;
+                            run_len[R + j] = N.len[next_admit + j];
+                            run_gen[R + j] = 0.0;
                         }
                         R += n_adm;
                         next_admit += n_adm;
@@ -302,12 +338,12 @@ __global__ void __launch_bounds__(32 * PALS_SIM_MAX_NODES) k_sim(SimArgs a) {
                     const int active = min(slot_cap, R);
                     double mn = steps_left;
                     for (int j = lane; j < active; j += 32) {
-                        const double left = (double)N.len[N.run_id[j]] - N.run_gen[j];
+                        const double left = (double)run_len[j] - run_gen[j];
                         mn = left < mn ? left : mn;
                     }
                     double chunk = warp_min(mn);
                     chunk = chunk < 0.0 ? 0.0 : chunk;
-                    for (int j = lane; j < active; j += 32) N.run_gen[j] += chunk;
+                    for (int j = lane; j < active; j += 32) run_gen[j] += chunk;
                     tokens += chunk * active;
                     steps_left -= smax(chunk, 1e-9);
                     __syncwarp();
@@ -319,17 +355,17 @@ __global__ void __launch_bounds__(32 * PALS_SIM_MAX_NODES) k_sim(SimArgs a) {
                         double g = 0.0;
                         bool done = false;
                         if (j < R) {
-                            id = N.run_id[j];
-                            g = N.run_gen[j];
-                            done = g >= (double)N.len[id] - 1e-7;
+                            id = run_len[j];
+                            g = run_gen[j];
+                            done = g >= (double)id - 1e-7;
                         }
                         const unsigned keep = __ballot_sync(kFull, j < R && !done);
                         const unsigned fin = __ballot_sync(kFull, done);
                         __syncwarp();
                         if (j < R && !done) {
                             const int dst = kept + __popc(keep & ((1u << lane) - 1));
-                            N.run_id[dst] = id;
-                            N.run_gen[dst] = g;
+                            run_len[dst] = id;
+                            run_gen[dst] = g;
                         }
                         kept += __popc(keep);
                         completed += __popc(fin);
@@ -533,6 +569,29 @@ struct Resources {
         for (auto* m : plant_models) pals_model_destroy(m);
         for (void* p : dev) cudaFree(p);
     }
+    // staged arena: every per-scenario / per-node array is packed into one host
+    // buffer and moved with one allocation and one copy (thousands of small
+    // cudaMalloc / cudaFree calls would dominate the call otherwise)
+    std::vector<char> stage_buf;
+    char* arena = nullptr;
+    template <class T>
+    size_t stage(const T* data, size_t n) {
+        const size_t off = (stage_buf.size() + 255) & ~(size_t)255;
+        stage_buf.resize(off + std::max<size_t>(1, n) * sizeof(T), 0);
+        if (data && n) std::memcpy(stage_buf.data() + off, data, n * sizeof(T));
+        return off;
+    }
+    template <class T>
+    size_t stage(const std::vector<T>& v) { return stage(v.data(), v.size()); }
+    int commit() {
+        int r = alloc(&arena, stage_buf.size());
+        if (r) return r;
+        const cudaError_t e = copy_on(ctx->stream, arena, stage_buf.data(), stage_buf.size(),
+                                      cudaMemcpyHostToDevice);
+        return e == cudaSuccess ? PALS_OK : cuda_fail(e, "pals_run_scenarios: arena upload");
+    }
+    template <class T>
+    T* at(size_t off) const { return (T*)(arena + off); }
     template <class T>
     int alloc(T** p, size_t n) {
         void* q = nullptr;
@@ -617,6 +676,15 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
         return set_error(PALS_ECONFIG, "pals_run_scenarios: null argument");
     if (n_scen <= 0) return PALS_OK;
     PALS_CUDA(cudaSetDevice(ctx->device));
+    const auto t_start = std::chrono::steady_clock::now();
+    ctx->sim_kernel_ms = -1.0;
+    static const bool verbose = getenv("PALS_SIM_VERBOSE") != nullptr;
+    auto phase = [&](const char* what) {
+        if (verbose)
+            fprintf(stderr, "[pals_run_scenarios] %-12s %.3f s\n", what,
+                    std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start)
+                        .count());
+    };
     Resources res{ctx};
     // plant models (analytic, one per profile): device Analytic + the oracle's scorer
     for (int m = 0; m < n_models; ++m) {
@@ -701,6 +769,7 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
             }
         }
     }
+    phase("nodes");
     // build every select-table set: plan (scores + ranks) -> k_build_tables
     std::vector<int> set_scorer_model(res.sets.size(), -1);
     for (auto& [k, si] : set_of) {
@@ -760,28 +829,49 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
         if (e != cudaSuccess) return cuda_fail(e, "k_build_tables");
     }
 
-    // arrival streams on all host threads (independent per node)
-    std::vector<Stream> streams(total_nodes);
+    phase("tables");
+    // arrival streams on all host threads: one per distinct (seed, node slot, rate,
+    // backlog, length law, interval grid) — a baseline suite's policies share them
+    std::vector<int64_t> node0(n_scen + 1, 0);
+    for (int s = 0; s < n_scen; ++s) node0[s + 1] = node0[s] + scens[s].n_nodes;
+    std::vector<Stream> streams;
+    std::vector<int> node_stream(total_nodes);
+    std::vector<std::pair<int, int>> work;  // (scenario, node) generating each stream
     {
-        std::vector<std::pair<int, int>> work;  // (scenario, node)
+        using Key = std::tuple<uint64_t, int, double, int, double, double, double, int>;
+        std::map<Key, int> seen;
         for (int s = 0; s < n_scen; ++s)
-            for (int i = 0; i < scens[s].n_nodes; ++i) work.emplace_back(s, i);
+            for (int i = 0; i < scens[s].n_nodes; ++i) {
+                const pals_scenario& sc = scens[s];
+                const Key key{sc.seed, i, sc.nodes[i].arrival_rate_per_s,
+                              sc.nodes[i].initial_backlog, sc.mean_tokens, sc.log_sigma,
+                              sc.interval_s, n_int[s]};
+                auto it = seen.find(key);
+                if (it == seen.end()) {
+                    it = seen.emplace(key, (int)work.size()).first;
+                    work.emplace_back(s, i);
+                }
+                node_stream[node0[s] + i] = it->second;
+            }
+        streams.resize(work.size());
         const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(),
                                                             (unsigned)work.size()));
         std::vector<std::thread> th;
         for (unsigned t = 0; t < nt; ++t)
             th.emplace_back([&, t] {
-                for (size_t w = t; w < work.size(); w += nt) {
-                    int64_t gi = 0;
-                    for (int s = 0; s < work[w].first; ++s) gi += scens[s].n_nodes;
-                    gi += work[w].second;
+                for (size_t w = t; w < work.size(); w += nt)
                     gen_stream(scens[work[w].first], work[w].second, n_int[work[w].first],
-                               &streams[gi]);
-                }
+                               &streams[w]);
             });
         for (auto& t : th) t.join();
     }
+    std::vector<size_t> o_cum(streams.size()), o_len(streams.size());
+    for (size_t u = 0; u < streams.size(); ++u) {
+        o_cum[u] = res.stage(streams[u].cum);
+        o_len[u] = res.stage(streams[u].len);
+    }
 
+    phase("streams");
     // budget changes and their splits (assign_budgets, sim.hpp:229-238, 277-283, 313-336)
     std::vector<std::vector<int32_t>> chg_k(n_scen);
     std::vector<std::vector<double>> chg_w(n_scen);
@@ -790,8 +880,9 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
         const pals_scenario& sc = scens[s];
         if (sc.n_trace > 0) {
             double last = -1.0;
+            TraceCursor at_t0{sc}, at_t{sc};
             for (int k = 0; k < n_int[s]; ++k) {
-                const double wv = trace_value(sc, k * sc.interval_s);
+                const double wv = at_t0(k * sc.interval_s);
                 if (wv != last) {
                     chg_k[s].push_back(k);
                     chg_w[s].push_back(wv);
@@ -801,7 +892,7 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
             track[s].resize(n_int[s]);
             for (int k = 0; k < n_int[s]; ++k) {
                 const double t1 = k * sc.interval_s + sc.interval_s;
-                track[s][k] = trace_value(sc, t1 - sc.interval_s);
+                track[s][k] = at_t(t1 - sc.interval_s);
             }
         } else if (sc.has_cluster_budget) {
             chg_k[s].push_back(0);
@@ -886,11 +977,34 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
         }
     }
 
-    // device buffers
+    phase("budgets");
+    // device buffers: stage every array, one upload, then point the descriptors at it
     std::vector<SimScenDev> hs(n_scen);
     std::vector<SimNodeDev> hn(total_nodes);
+    std::vector<size_t> o_chg(n_scen), o_track(n_scen, 0), o_bud(total_nodes),
+        o_run_len(total_nodes), o_run_gen(total_nodes);
+    size_t max_run = 0;
     {
         int64_t gi = 0;
+        for (int s = 0; s < n_scen; ++s) {
+            const pals_scenario& sc = scens[s];
+            o_chg[s] = res.stage(chg_k[s]);
+            if (!track[s].empty()) o_track[s] = res.stage(track[s]);
+            const int mb = *std::max_element(sc.cand_batches, sc.cand_batches + sc.n_batches);
+            for (int i = 0; i < sc.n_nodes; ++i, ++gi) {
+                std::vector<double> nbud(chg_k[s].size());
+                for (size_t c = 0; c < nbud.size(); ++c) nbud[c] = chg_b[s][c * sc.n_nodes + i];
+                o_bud[gi] = res.stage(nbud);
+                const size_t run_cap =
+                    (size_t)std::max(mb, sc.initial_batch) * sc.nodes[i].dp + 32;
+                max_run = std::max(max_run, run_cap);
+                o_run_len[gi] = res.stage((const int32_t*)nullptr, run_cap);
+                o_run_gen[gi] = res.stage((const double*)nullptr, run_cap);
+            }
+        }
+        int r = res.commit();
+        if (r) return r;
+        gi = 0;
         for (int s = 0; s < n_scen; ++s) {
             const pals_scenario& sc = scens[s];
             SimScenDev& S = hs[s];
@@ -905,13 +1019,8 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
             S.interval_s = sc.interval_s;
             S.epsilon = sc.epsilon;
             S.cfg = sc.controller;
-            int r = res.upload((int32_t**)&S.change_k, chg_k[s]);
-            if (r) return r;
-            if (!track[s].empty()) {
-                r = res.upload((double**)&S.track_target, track[s]);
-                if (r) return r;
-            }
-            std::vector<double> bud(chg_b[s]);
+            S.change_k = res.at<int32_t>(o_chg[s]);
+            S.track_target = track[s].empty() ? nullptr : res.at<double>(o_track[s]);
             for (int i = 0; i < sc.n_nodes; ++i, ++gi) {
                 SimNodeDev& N = hn[gi];
                 const pals_sim_node& n = sc.nodes[i];
@@ -923,20 +1032,11 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
                 N.dp = n.dp;
                 N.init_idx = node_init[gi];
                 N.target_tps = node_target[gi];
-                r = res.upload((int32_t**)&N.cum, streams[gi].cum);
-                if (r) return r;
-                r = res.upload((int32_t**)&N.len, streams[gi].len);
-                if (r) return r;
-                const int mb = *std::max_element(sc.cand_batches, sc.cand_batches + sc.n_batches);
-                const size_t run_cap = (size_t)std::max(mb, sc.initial_batch) * n.dp + 32;
-                r = res.alloc(&N.run_id, run_cap);
-                if (r) return r;
-                r = res.alloc(&N.run_gen, run_cap);
-                if (r) return r;
-                std::vector<double> nbud(chg_k[s].size());
-                for (size_t c = 0; c < nbud.size(); ++c) nbud[c] = bud[c * sc.n_nodes + i];
-                r = res.upload((double**)&N.budget, nbud);
-                if (r) return r;
+                N.cum = res.at<int32_t>(o_cum[node_stream[gi]]);
+                N.len = res.at<int32_t>(o_len[node_stream[gi]]);
+                N.run_len = res.at<int32_t>(o_run_len[gi]);
+                N.run_gen = res.at<double>(o_run_gen[gi]);
+                N.budget = res.at<double>(o_bud[gi]);
             }
         }
     }
@@ -964,9 +1064,29 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
         r = res.alloc(&A.dec, nlog);
         if (r) return r;
     }
-    k_sim<<<n_scen, 32 * max_nodes, 0, ctx->stream>>>(A);
+    PALS_CUDA(cudaStreamSynchronize(ctx->stream));
+    phase("upload");
+    ctx->sim_prep_s =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    cudaEvent_t ev0, ev1;
+    PALS_CUDA(cudaEventCreate(&ev0));
+    PALS_CUDA(cudaEventCreate(&ev1));
+    cudaEventRecord(ev0, ctx->stream);
+    const size_t smem = (size_t)max_nodes * max_run * (sizeof(double) + sizeof(int32_t));
+    A.smem_run = smem <= 160 * 1024 ? (int)max_run : 0;
+    if (A.smem_run)
+        PALS_CUDA(cudaFuncSetAttribute(k_sim, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+    k_sim<<<n_scen, 32 * max_nodes, A.smem_run ? smem : 0, ctx->stream>>>(A);
     count_launch(ctx);
     cudaError_t e = cudaGetLastError();
+    cudaEventRecord(ev1, ctx->stream);
+    if (e == cudaSuccess) e = cudaEventSynchronize(ev1);
+    float kms = -1.0f;
+    if (e == cudaSuccess) cudaEventElapsedTime(&kms, ev0, ev1);
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    ctx->sim_kernel_ms = kms;
     if (e != cudaSuccess) return cuda_fail(e, "k_sim");
     e = copy_on(ctx->stream, node_results, A.node_out, sizeof(pals_sim_node_result) * total_nodes,
                 cudaMemcpyDeviceToHost);
@@ -981,6 +1101,13 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
                     cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cuda_fail(e, "pals_run_scenarios");
     for (int64_t gi = 0; gi < total_nodes; ++gi)
-        node_results[gi].arrival_stream_hash = streams[gi].hash;
+        node_results[gi].arrival_stream_hash = streams[node_stream[gi]].hash;
+    return PALS_OK;
+}
+
+extern "C" int pals_sim_last_timing(pals_ctx* ctx, double* host_setup_s, double* kernel_ms) {
+    if (!ctx) return set_error(PALS_ECONFIG, "pals_sim_last_timing: null context");
+    if (host_setup_s) *host_setup_s = ctx->sim_prep_s;
+    if (kernel_ms) *kernel_ms = ctx->sim_kernel_ms;
     return PALS_OK;
 }

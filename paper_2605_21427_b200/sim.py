@@ -149,6 +149,13 @@ def run_scenarios(ctx, scenarios, profiles, gpu, coeffs, predictors=None, logs: 
     return nres, res, tel, dec
 
 
+def last_timing(ctx):
+    """(host setup seconds, simulation kernel ms) of the last run_scenarios on ctx."""
+    a, b = C.c_double(), C.c_double()
+    check(ctx.lib.pals_sim_last_timing(ctx.h, C.byref(a), C.byref(b)))
+    return a.value, b.value
+
+
 def run_baseline_suite(ctx, scenario, profiles, gpu, coeffs, predictors=None, logs=False):
     """All five policies on identical arrival streams (sim.hpp:488-500)."""
     scs = [dict(scenario, policy=p) for p in POLICIES]

@@ -13,14 +13,17 @@
 //   table_scorer      the TableScorer test fake, tests/test_controller.cpp:17-29
 // plus batched entry points (SelectPlan, replay) that have no single-call
 // counterpart in the reference. Also allocate_budget (allocator.hpp:76-186) over
-// GpuAllocRequest nodes and build_frontier / evaluate_regime (pareto.hpp:31-59,
-// 114-135).
+// GpuAllocRequest nodes, build_frontier / evaluate_regime (pareto.hpp:31-59,
+// 114-135), and run_scenario / run_baseline_suite (sim.hpp:482-500) returning the
+// reference's own SimResult.
 //
 // Header-only; include after the reference headers are on the include path and
 // link libpals_gpu.so.
 #pragma once
 
 #include <cstdio>
+#include <cstring>
+#include <map>
 #include <memory>
 #include <sstream>
 #include <stdexcept>
@@ -32,7 +35,9 @@
 #include "wattserve/allocator.hpp"
 #include "wattserve/controller.hpp"
 #include "wattserve/forest.hpp"
+#include "wattserve/json_io.hpp"
 #include "wattserve/pareto.hpp"
+#include "wattserve/sim.hpp"
 
 namespace wattserve::gpu {
 
@@ -460,6 +465,155 @@ inline std::vector<FrontierPoint> evaluate_regime(
         const auto j = static_cast<std::size_t>(idx[i]);
         out.push_back(FrontierPoint{cands[j], th[j], ef[j]});
     }
+    return out;
+}
+
+// ---- queue-plant simulation (sim.hpp:209-500) ------------------------------------
+// run_scenario for many scenarios in one GPU pass; every SimResult is the
+// reference's (scenario, per-node telemetry / decisions, targets, arrival hashes,
+// total energy). NodeResult::requests is not materialised (the per-request records
+// stay on the device; completion counts are in the summaries).
+inline std::vector<SimResult> run_scenarios(Context& ctx, const std::vector<Scenario>& scs,
+                                            const ProfileRegistry& registry,
+                                            const Platform& platform,
+                                            const PredictorBundle* predictor) {
+    const std::vector<std::string> names = registry.names();
+    std::vector<pals_profile> profs;
+    for (const auto& n : names) profs.push_back(to_c(registry.get(n)));
+    auto index_of = [&](const std::string& id) {
+        for (std::size_t i = 0; i < names.size(); ++i)
+            if (names[i] == id) return static_cast<int32_t>(i);
+        throw config_error("unknown model profile: " + id);
+    };
+    // predictor scorers for the models the scenarios use (predictor_scorer, sim.hpp:277-281)
+    std::vector<GpuScorer> keep;
+    std::vector<pals_model*> preds(names.size(), nullptr);
+    std::vector<std::vector<pals_sim_node>> nodes(scs.size());
+    std::vector<pals_scenario> cs(scs.size());
+    std::vector<std::vector<double>> tt(scs.size()), tw(scs.size());
+    int64_t stride = 0, n_nodes = 0;
+    for (std::size_t s = 0; s < scs.size(); ++s) {
+        const Scenario& sc = scs[s];
+        sc.validate();
+        for (const auto& n : sc.nodes) {
+            const int32_t m = index_of(n.model_id);
+            if (predictor && !preds[m]) {  // unknown ids throw as predict() would
+                keep.push_back(predictor_scorer(ctx, *predictor, n.model_id));
+                preds[m] = keep.back().get();
+            }
+            nodes[s].push_back(pals_sim_node{m, n.tp, n.ep, n.dp, n.qos_fraction,
+                                             n.arrival_rate_per_s, n.initial_backlog, 0});
+        }
+        for (const auto& [t, w] : sc.budget_trace) {
+            tt[s].push_back(t);
+            tw[s].push_back(w);
+        }
+        pals_scenario& c = cs[s];
+        std::memset(&c, 0, sizeof c);
+        c.duration_s = sc.duration_s;
+        c.interval_s = sc.interval_s;
+        c.seed = sc.seed;
+        c.mean_tokens = sc.output_len.mean_tokens;
+        c.log_sigma = sc.output_len.log_sigma;
+        c.has_cluster_budget = sc.cluster_budget_w.has_value() ? 1 : 0;
+        c.cluster_budget_w = sc.cluster_budget_w.value_or(0.0);
+        c.n_trace = static_cast<int32_t>(tt[s].size());
+        c.trace_t = tt[s].data();
+        c.trace_w = tw[s].data();
+        c.policy = static_cast<int32_t>(sc.policy);  // Fixed .. Oracle = 0 .. 4
+        c.objective = sc.objective == Objective::BudgetMaxThroughput ? PALS_OBJ_BUDGET
+                                                                     : PALS_OBJ_QOS;
+        c.controller = to_c(sc.controller);
+        c.epsilon = sc.epsilon;
+        c.cand_caps = sc.cand_caps.data();
+        c.cand_batches = sc.cand_batches.data();
+        c.n_caps = static_cast<int32_t>(sc.cand_caps.size());
+        c.n_batches = static_cast<int32_t>(sc.cand_batches.size());
+        c.initial_cap_w = sc.initial_cap_w;
+        c.initial_batch = sc.initial_batch;
+        c.n_nodes = static_cast<int32_t>(nodes[s].size());
+        c.nodes = nodes[s].data();
+        stride = std::max<int64_t>(stride, std::llround(sc.duration_s / sc.interval_s));
+        n_nodes += c.n_nodes;
+    }
+    const pals_gpu_spec g{platform.gpu.idle_watts, platform.gpu.min_cap_watts,
+                          platform.gpu.max_cap_watts, platform.gpu.max_frequency};
+    const pals_coeffs k{platform.coeffs.alpha, platform.coeffs.beta_watts};
+    std::vector<pals_sim_node_result> nres(n_nodes);
+    std::vector<pals_sim_result> res(scs.size());
+    std::vector<pals_sim_telemetry> tel(n_nodes * stride);
+    std::vector<pals_sim_decision> dec(n_nodes * stride);
+    check(pals_run_scenarios(ctx.get(), static_cast<int32_t>(cs.size()), cs.data(),
+                             static_cast<int32_t>(profs.size()), profs.data(), preds.data(), &g,
+                             &k, nres.data(), res.data(), stride, tel.data(), dec.data()));
+    const DecisionReason reasons[] = {DecisionReason::QosFeasibleMaxEfficiency,
+                                      DecisionReason::FallbackMaxThroughput,
+                                      DecisionReason::BudgetConstrainedMaxThroughput,
+                                      DecisionReason::HoldHysteresis,
+                                      DecisionReason::OracleExhaustive};
+    std::vector<SimResult> out(scs.size());
+    int64_t gi = 0;
+    for (std::size_t s = 0; s < scs.size(); ++s) {
+        SimResult& r = out[s];
+        r.scenario = scs[s];
+        r.total_energy_j = res[s].sim_total_energy_j;
+        const int n_int = res[s].n_intervals;
+        for (std::size_t i = 0; i < scs[s].nodes.size(); ++i, ++gi) {
+            const ScenarioNode& sn = scs[s].nodes[i];
+            NodeResult nr;
+            nr.model_id = sn.model_id;
+            nr.throughput_target_tps = nres[gi].throughput_target_tps;
+            nr.arrival_stream_hash = nres[gi].arrival_stream_hash;
+            for (int kk = 0; kk < n_int; ++kk) {
+                const pals_sim_telemetry& t = tel[gi * stride + kk];
+                TelemetrySample ts;
+                ts.t_s = t.t_s;
+                ts.gpu_power_w = t.gpu_power_w;
+                ts.sys_power_w = t.sys_power_w;
+                ts.throughput_tps = t.throughput_tps;
+                ts.utilization = t.utilization;
+                ts.queue_depth = t.queue_depth;
+                ts.active_batch = t.active_batch;
+                ts.node_budget_w = t.node_budget_w;
+                ts.applied_cap_w = t.applied_cap_w;
+                ts.applied_batch_cap = t.applied_batch_cap;
+                nr.telemetry.push_back(ts);
+                const pals_sim_decision& d = dec[gi * stride + kk];
+                DecisionRecord dr;
+                dr.t_s = t.t_s;
+                dr.point = OperatingPoint{d.cap_w, d.batch, sn.tp, sn.ep, sn.dp};
+                dr.applied = d.applied != 0;
+                dr.reason = reasons[d.reason];
+                dr.err_norm = d.err_norm;
+                dr.bias = d.bias;
+                nr.decisions.push_back(dr);
+            }
+            r.nodes.push_back(std::move(nr));
+        }
+    }
+    return out;
+}
+
+inline SimResult run_scenario(Context& ctx, const Scenario& sc, const ProfileRegistry& registry,
+                              const Platform& platform, const PredictorBundle* predictor) {
+    return run_scenarios(ctx, {sc}, registry, platform, predictor).front();
+}
+
+// All five control strategies on identical seeds and arrival streams (sim.hpp:488-500).
+inline std::map<Policy, SimResult> run_baseline_suite(Context& ctx, const Scenario& sc,
+                                                      const ProfileRegistry& registry,
+                                                      const Platform& platform,
+                                                      const PredictorBundle* predictor) {
+    std::vector<Scenario> scs;
+    const Policy pols[] = {Policy::Fixed, Policy::AdaptiveBatch, Policy::AdaptiveCap,
+                           Policy::Joint, Policy::Oracle};
+    for (Policy p : pols) {
+        scs.push_back(sc);
+        scs.back().policy = p;
+    }
+    auto rs = run_scenarios(ctx, scs, registry, platform, predictor);
+    std::map<Policy, SimResult> out;
+    for (std::size_t i = 0; i < rs.size(); ++i) out.emplace(pols[i], std::move(rs[i]));
     return out;
 }
 

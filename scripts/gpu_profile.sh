@@ -1,17 +1,18 @@
-# One GPU call: parity tests, smoke, the default bench, the ncu launch list and
-# ncu --set full captures of the top kernels. Outputs land in gpurun_out/.
+# One GPU call: parity tests, smoke, the default bench + reference arm, the ncu launch
+# list and ncu --set full captures of the top kernels. Outputs land in gpurun_out/.
 set -x
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -q -m gpu --timeout 400 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-nvidia-smi --query-gpu=index,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/clocks_before.csv
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
-timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2>> gpurun_out/bench.err
-SMALL="--steps 2 --warmup 1 --traces 100000 --predictions 4194304 --no-cpu-baseline"
+timeout 1200 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2>> gpurun_out/bench.err
+SMALL="--steps 2 --warmup 1 --traces 100000 --predictions 4194304 --cfg3-queries 100000 --cfg5-traces 0 --sim-seeds 0 --no-cpu-baseline"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py $SMALL > gpurun_out/b_ncu.log 2>&1
-for k in k_scan k_sort_chunks k_forest_eval_aos k_cross k_assign_qprep k_allocate k_front_scan; do
+for k in k_scan k_sort_chunks k_merge_round k_forest_eval_aos k_assign_qprep k_allocate k_front_scan; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 -o gpurun_out/prof_$k python bench.py $SMALL > gpurun_out/ncu_$k.log 2>&1
 done
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_replay -s 1 -c 1 -o gpurun_out/prof_k_replay python bench.py --steps 1 --warmup 1 --traces 100000 --trace-steps 600 --predictions 1048576 --no-cpu-baseline > gpurun_out/ncu_k_replay.log 2>&1
+# the replay at its bench size (1e6 traces; 300 steps keep ncu's ~40 replays short)
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_replay -s 1 -c 1 -o gpurun_out/prof_k_replay python bench.py --steps 1 --warmup 1 --trace-steps 300 --predictions 1048576 --cfg3-queries 100000 --cfg5-traces 0 --sim-seeds 0 --no-cpu-baseline > gpurun_out/ncu_k_replay.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sim -s 1 -c 1 -o gpurun_out/prof_k_sim python scripts/sim_quick.py 16 > gpurun_out/ncu_k_sim.log 2>&1
 ls -la gpurun_out

@@ -35,7 +35,8 @@ def summarise(rep):
     res = {}
     for v in rows[2:]:
         name = v[h.index("Kernel Name")].split("(")[0].replace("void ", "")
-        name = name.replace("<unnamed>::", "").replace("pals::", "").split("<")[0].strip()
+        name = name.replace("<unnamed>::", "").replace("unnamed>::", "").replace("pals::", "")
+        name = name.split("<")[0].strip()
         d = {}
         for i, col in enumerate(h):
             if col in WANT:

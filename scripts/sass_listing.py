@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_2605_21427_b200", "libpals_gpu.so")
 KEEP = ["k_scanIj", "k_replayILi6", "k_forest_eval_aos", "k_allocateILb0", "k_eval_analyticE",
         "k_merge_round", "k_sort_chunksILi2048", "k_assign_qprep", "k_front_group",
-        "k_front_scan", "k_exact", "k_build_tables", "k_alloc_steps", "k_one"]
+        "k_front_scan", "k_exact", "k_build_tables", "k_alloc_steps", "k_one", "5k_simE"]
 GROUPS = {
     "fp64": r"^(DFMA|DMUL|DADD|DSETP|DMNMX|F2F\.F64|I2F\.F64|F2I\.F64|MUFU\.RCP64H|MUFU\.RSQ64H)",
     "int_alu": r"^(IADD3|IMAD|ISETP|VIMNMX|IMNMX|LOP3|SHF|SEL|LEA|PRMT|FLO|POPC|BREV|IABS)",
@@ -47,7 +47,8 @@ def main():
             m = re.match(r"\s*/\*[0-9a-f]{4}\*/\s+(@!?U?P\w+\s+)?([A-Z0-9_.]+)", ln)
             if m:
                 ops.append(m.group(2))
-        with open(os.path.join(out, tag.split("IL")[0].split("Ij")[0] + ".sass"), "w") as g:
+        fname = "k_sim" if tag == "5k_simE" else tag.split("IL")[0].split("Ij")[0].rstrip("E")
+        with open(os.path.join(out, fname + ".sass"), "w") as g:
             g.write(f"// {name}\n// cuobjdump -sass paper_2605_21427_b200/libpals_gpu.so "
                     f"(sm_100a, -fmad=false -lineinfo)\n")
             g.write("\n".join(re.sub(r"\s*/\* 0x[0-9a-f]+ \*/\s*$", "", ln).rstrip()

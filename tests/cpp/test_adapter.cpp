@@ -20,7 +20,10 @@
 #include "wattserve/forest.hpp"
 #include "wattserve/pareto.hpp"
 #include "wattserve/json_io.hpp"
+#include "wattserve/metrics.hpp"
 #include "wattserve/rng.hpp"
+#include "wattserve/scenario_io.hpp"
+#include "wattserve/sim.hpp"
 #include "wattserve/sweep.hpp"
 #include "wattserve_gpu.hpp"
 
@@ -240,6 +243,7 @@ int main(int argc, char** argv) {
     }
 
     // ---- predictor_scorer on a bundle trained by the reference pipeline ----
+    PredictorBundle bundle;
     {
         const SweepGrid grid = SweepGrid::default_grid();
         AnalyticBackend be(gspec, k);
@@ -251,7 +255,7 @@ int main(int argc, char** argv) {
         HyperParams hp;
         hp.n_trees = 30;
         hp.max_depth = 12;
-        const PredictorBundle bundle = train_bundle(recs, k, hp, 2605);
+        bundle = train_bundle(recs, k, hp, 2605);
         for (const char* mid : {"llama2-7b-like", "mixtral-8x7b-like"}) {
             const Scorer cs = predictor_scorer(bundle, mid);
             auto gs = gpu::predictor_scorer(ctx, bundle, mid);
@@ -416,6 +420,60 @@ int main(int argc, char** argv) {
             threw = true;
         }
         EXPECT(threw, "build_frontier: no points");
+    }
+
+    // ---- run_scenario / run_baseline_suite (sim.hpp:482-500) on the bundled scenarios ----
+    {
+        ProfileRegistry reg;
+        for (const auto& p : profiles) reg.add(p);
+        const Platform plat{gspec, k};
+        const json all = json::parse(read_file(root + "/paper_2605_21427_b200/data/scenarios.json"));
+        int n_sc = 0;
+        for (const auto& [name, entry] : all.items()) {
+            json sj = entry.at("scenario");
+            sj.erase("budget_trace_csv");  // resolved into "trace" (the CSV is not shipped)
+            Scenario sc = scenario_from_json(sj);
+            for (const auto& tw : entry.at("trace"))
+                sc.budget_trace.emplace_back(tw.at(0).get<double>(), tw.at(1).get<double>());
+            sc.duration_s = std::min(sc.duration_s, 600.0);
+            const auto want = run_baseline_suite(sc, reg, plat, &bundle);
+            const auto got = gpu::run_baseline_suite(ctx, sc, reg, plat, &bundle);
+            for (const auto& [pol, rw] : want) {
+                const SimResult& rg = got.at(pol);
+                bool ok = rw.nodes.size() == rg.nodes.size() &&
+                          same_bits(rw.total_energy_j, rg.total_energy_j);
+                for (std::size_t i = 0; ok && i < rw.nodes.size(); ++i) {
+                    const NodeResult& a = rw.nodes[i];
+                    const NodeResult& b = rg.nodes[i];
+                    ok = a.model_id == b.model_id && a.arrival_stream_hash == b.arrival_stream_hash &&
+                         same_bits(a.throughput_target_tps, b.throughput_target_tps) &&
+                         a.telemetry.size() == b.telemetry.size() &&
+                         a.decisions.size() == b.decisions.size();
+                    for (std::size_t t = 0; ok && t < a.telemetry.size(); ++t) {
+                        const auto &x = a.telemetry[t], &y = b.telemetry[t];
+                        const auto &p = a.decisions[t], &q = b.decisions[t];
+                        ok = same_bits(x.t_s, y.t_s) && same_bits(x.gpu_power_w, y.gpu_power_w) &&
+                             same_bits(x.sys_power_w, y.sys_power_w) &&
+                             same_bits(x.throughput_tps, y.throughput_tps) &&
+                             same_bits(x.utilization, y.utilization) &&
+                             x.queue_depth == y.queue_depth && x.active_batch == y.active_batch &&
+                             same_bits(x.node_budget_w, y.node_budget_w) &&
+                             same_bits(x.applied_cap_w, y.applied_cap_w) &&
+                             x.applied_batch_cap == y.applied_batch_cap &&
+                             same_bits(p.t_s, q.t_s) && p.point == q.point &&
+                             p.applied == q.applied && p.reason == q.reason &&
+                             same_bits(p.err_norm, q.err_norm) && same_bits(p.bias, q.bias);
+                    }
+                }
+                const RunSummary sw = summarize(rw), sg = summarize(rg);
+                ok = ok && same_bits(sw.aggregate.tokens_per_joule, sg.aggregate.tokens_per_joule) &&
+                     same_bits(sw.cluster_tracking_mae_w, sg.cluster_tracking_mae_w) &&
+                     decisions_csv(rw) == decisions_csv(rg) && telemetry_csv(rw) == telemetry_csv(rg);
+                EXPECT(ok, (name + "/" + to_string(pol)).c_str());
+                ++n_sc;
+            }
+        }
+        EXPECT(n_sc == 15, "3 scenarios x 5 policies");
     }
 
     std::printf("%s: %d checks, %d failures\n", g_fail ? "FAIL" : "PASS", g_checks, g_fail);

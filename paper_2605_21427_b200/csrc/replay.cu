@@ -25,6 +25,7 @@ struct ReplayParams {
     pals_ctrl_cfg cfg;
     double alpha, beta;
     int n_models;
+    int variant;  // PALS_REPLAY_VARIANT bit 1: prefix-min breaker search (default on)
 };
 
 // ---- counter-based trace generator --------------------------
@@ -33,18 +34,22 @@ __device__ __forceinline__ uint64_t draw(uint64_t key, uint64_t lane, uint64_t c
 }
 __device__ __forceinline__ double u01(uint64_t u) { return (double)(u >> 11) * 0x1.0p-53; }
 
+// Piecewise-constant trace lane: only the segment cursor and level live in
+// registers; the level bounds (lo, hi) are recomputed from the model when a new
+// segment starts (same expressions, same doubles) — fewer live registers per trace.
 struct Seg {
-    uint64_t key;
-    uint64_t lane;
-    long next_j, seg_end;
-    double lo, hi, level;
-    __device__ __forceinline__ double at(long k, int seg_min, int seg_max) {
+    int next_j, seg_end;
+    double level;
+    __device__ __forceinline__ double at(int k, uint64_t key, uint64_t lane, int seg_min,
+                                         int seg_max, double lo_frac, const double& lo_of,
+                                         double hi_frac, const double& hi_of) {
         while (k >= seg_end) {
             const uint64_t span = (uint64_t)(seg_max - seg_min) + 1;
             const long len = seg_min + (long)(draw(key, lane, 2 * (uint64_t)next_j) % span);
             const double u = u01(draw(key, lane, 2 * (uint64_t)next_j + 1));
+            const double lo = lo_frac * lo_of, hi = hi_frac * hi_of;
             level = lo + (hi - lo) * u;
-            seg_end += len;
+            seg_end += (int)len;
             ++next_j;
         }
         return level;
@@ -108,8 +113,8 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
     const double qfrac = sp.qos_frac_lo + (sp.qos_frac_hi - sp.qos_frac_lo) * u01(draw(key, 0, 1));
     const double target_tps = qfrac * m.t_max;
     const double target = target_tps * (1.0 + cfg.target_headroom);
-    Seg bs{key, 1, 0, 0, sp.budget_lo_frac * m.p_min, sp.budget_hi_frac * m.p_max, 0.0};
-    Seg ls{key, 2, 0, 0, sp.load_lo * m.t_max, sp.load_hi * m.t_max, 0.0};
+    Seg bs{0, 0, 0.0};  // budget lane 1: level U(lo_frac * p_min, hi_frac * p_max)
+    Seg ls{0, 0, 0.0};  // offered-load lane 2: level U(load_lo * t_max, load_hi * t_max)
 
     // ControllerState (controller.hpp:55-63)
     double bias = 1.0, integral = 0.0, prev_err = 0.0;
@@ -139,7 +144,10 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
     for (int k = 0; k < sp.n_steps; ++k) {
         const double t0 = (double)k * sp.interval_s;
         const double t1 = t0 + sp.interval_s;
-        const double node_budget = sp.budget_mode ? bs.at(k, sp.seg_min, sp.seg_max) : 0.0;
+        const double node_budget =
+            sp.budget_mode ? bs.at(k, key, 1, sp.seg_min, sp.seg_max, sp.budget_lo_frac, m.p_min,
+                                   sp.budget_hi_frac, m.p_max)
+                           : 0.0;
         // b_eff = batch_cap (fluid plant: the queue always covers the batch cap)
         if (applied_a != c_a || batch_b != c_b || node_budget != c_nb) {
             // enforce_cap (sim.hpp:195-205): walk down in 5 W steps until the cluster
@@ -159,8 +167,21 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
                             break;
                         }
                     }
-                } else {
+                } else if (!(p.variant & 2)) {
                     while (wc[j] > m.plant_min_cap && !(m.walk_pn[wo + j] <= node_budget)) ++j;
+                } else if (wc[0] > m.plant_min_cap && !(m.walk_pn[wo] <= node_budget)) {
+                    // the loop stops at the first position with c <= min_cap (a suffix
+                    // of the walk, from walk_jmin) or with a fitting draw; before
+                    // walk_jmin that is the first position whose running minimum
+                    // fits: a binary search over the non-increasing walk_pm
+                    int lo = 1, hi = m.walk_jmin[applied_a];
+                    const double* pm = m.walk_pm + wo;
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (pm[mid] <= node_budget) hi = mid;
+                        else lo = mid + 1;
+                    }
+                    j = lo;
                 }
             }
             cap = wc[j];
@@ -170,7 +191,8 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
             c_b = batch_b;
             c_nb = node_budget;
         }
-        const double offered = ls.at(k, sp.seg_min, sp.seg_max);
+        const double offered = ls.at(k, key, 2, sp.seg_min, sp.seg_max, sp.load_lo, m.t_max,
+                                     sp.load_hi, m.t_max);
         double noise;
         if (kWarp) {
             if ((k & 31) == 0 && k + lane < sp.n_steps)
@@ -378,6 +400,22 @@ __global__ void k_build_walk(ReplayModelDev* rm, double alpha, double beta) {
     }
 }
 
+// Running minimum of the breaker's draw along each (start cap, batch) walk.
+__global__ void k_walk_prefix(ReplayModelDev* rm) {
+    const ReplayModelDev m = *rm;
+    for (int64_t ab = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ab < m.n;
+         ab += (int64_t)gridDim.x * blockDim.x) {
+        const double* pn = m.walk_pn + ab * m.L;
+        double* pm = (double*)m.walk_pm + ab * m.L;
+        double cur = pn[0];
+        pm[0] = cur;
+        for (int j = 1; j < m.L; ++j) {
+            cur = pn[j] < cur ? pn[j] : cur;
+            pm[j] = cur;
+        }
+    }
+}
+
 struct ReplayCache {
     std::vector<const pals_model*> models;
     std::vector<pals_profile> plant;
@@ -463,8 +501,11 @@ static int replay_setup(pals_ctx* ctx, int n_models, pals_model* const* models,
     for (int a = 0; a < nc; ++a)
         for (int j = 0; j < L; ++j)
             walk_c[(size_t)a * L + j] = walks[a][std::min<size_t>(j, walks[a].size() - 1)];
-    const size_t walk_bytes = (size_t)nc * L * 8 + 2 * (size_t)n * L * 8;
-    const size_t per_model = W * W * 4 + W * 4 + 2 * W * 8 + walk_bytes + 4096;
+    const size_t walk_bytes = (size_t)nc * L * 8 + 3 * (size_t)n * L * 8 + (size_t)nc * 4 + 256;
+    std::vector<int> walk_jmin(nc);
+    for (int a = 0; a < nc; ++a) walk_jmin[a] = (int)walks[a].size() - 1;
+    const size_t per_model = (W * W * 4 + W * 4 + 2 * W * 8 + walk_bytes + 4096 + 255) &
+                             ~(size_t)255;
     PALS_CUDA(cudaMalloc(&rc->d_tables, per_model * n_models));
     PALS_CUDA(cudaMalloc(&rc->d_models, sizeof(ReplayModelDev) * n_models));
     PALS_CUDA(cudaMalloc(&rc->d_plant, sizeof(Analytic) * n_models));
@@ -533,6 +574,10 @@ static int replay_setup(pals_ctx* ctx, int n_models, pals_model* const* models,
         m.walk_c = (const double*)wbase;
         m.walk_T = (const double*)(wbase + (size_t)nc * L * 8);
         m.walk_pn = (const double*)(wbase + (size_t)nc * L * 8 + (size_t)n * L * 8);
+        m.walk_pm = (const double*)(wbase + (size_t)nc * L * 8 + 2 * (size_t)n * L * 8);
+        m.walk_jmin = (const int*)(wbase + (size_t)nc * L * 8 + 3 * (size_t)n * L * 8);
+        PALS_CUDA(copy_on(ctx->stream, (void*)m.walk_jmin, walk_jmin.data(), nc * sizeof(int),
+                          cudaMemcpyHostToDevice));
         PALS_CUDA(copy_on(ctx->stream, (void*)m.walk_c, walk_c.data(), walk_c.size() * 8,
                              cudaMemcpyHostToDevice));
         PALS_CUDA(copy_on(ctx->stream, rc->d_models + i, &m, sizeof m, cudaMemcpyHostToDevice));
@@ -542,7 +587,8 @@ static int replay_setup(pals_ctx* ctx, int n_models, pals_model* const* models,
         k_build_walk<<<(n * L + 255) / 256, 256, 0, ctx->stream>>>(rc->d_models + i,
                                                                   coeffs->alpha,
                                                                   coeffs->beta_watts);
-        count_launch(ctx, 2);
+        k_walk_prefix<<<(n + 127) / 128, 128, 0, ctx->stream>>>(rc->d_models + i);
+        count_launch(ctx, 3);
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "k_build_tables");
     }
@@ -563,6 +609,11 @@ static int replay_launch(pals_ctx* ctx, ReplayCache* rc, const pals_ctrl_cfg* cf
     p.alpha = rc->coeffs.alpha;
     p.beta = rc->coeffs.beta_watts;
     p.n_models = (int)rc->models.size();
+    static const int variant = [] {
+        const char* e = getenv("PALS_REPLAY_VARIANT");
+        return e ? atoi(e) : 2;
+    }();
+    p.variant = variant;
     const int64_t blocks = (spec->n_traces + 127) / 128;
     int32_t* order = nullptr;
     if (spec->objective_mode == 2 && ctx->replay_layout != PALS_REPLAY_WARP) {

@@ -65,7 +65,7 @@ def parse():
     ap.add_argument("--cfg5-traces", type=int, default=10_000_000,
                     help="cfg5 traces in total (split over the GPUs)")
     ap.add_argument("--cfg5-steps", type=int, default=2, help="timed cfg5 replays")
-    ap.add_argument("--sim-seeds", type=int, default=64,
+    ap.add_argument("--sim-seeds", type=int, default=256,
                     help="seeds per GPU of the 3-scenario x 5-policy queue-plant suite")
     ap.add_argument("--sim-steps", type=int, default=2, help="timed queue-plant runs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -175,6 +175,15 @@ def measured_peaks_json():
             return json.load(f)
     except Exception:
         return {}
+
+
+def ncu_metric(kernel: str, key: str):
+    """One metric of a kernel from the committed ncu --set full summary (None if absent)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            return json.load(f).get(kernel, {}).get(key)
+    except Exception:
+        return None
 
 
 def ncu_traffic(kernel: str):
@@ -394,7 +403,11 @@ def run_ours(args, dist: Dist):
                 "traffic": ncu_traffic("k_replay"),
                 "algorithmic": f"{fp64_per_dec:.0f} FP64 ops per decision (counted in DESIGN.md "
                                "§4); the kernel is latency-bound, not FP64-throughput-bound",
-                "peak_source": "measured here: pals_measure_peaks DFMA chains"}
+                "peak_source": "measured here: pals_measure_peaks DFMA chains",
+                "issue_active_pct_ncu": ncu_metric("k_replay", "issue_active_pct"),
+                "eligible_warps_per_cycle_ncu": ncu_metric("k_replay", "eligible_warps_per_cycle"),
+                "note": "one dependency chain per trace: the binding resource is instruction "
+                        "issue under latency (ncu issue-active share above), not the FP64 pipe"}
 
     # ---------------- K2: PredictorBundle::predict throughput ----------------
     from paper_2605_21427_b200.forest import Bundle, make_forest_model

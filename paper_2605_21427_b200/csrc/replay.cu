@@ -128,7 +128,8 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
     // enforce_cap memo (pure function of its inputs)
     int c_a = -1, c_b = -1;
     double c_nb = -1.0;
-    double cap = 0.0, capacity = 0.0, sys_w = 0.0;
+    int cj = 0;  // walk position of the enforced cap (cap = walk_c[c_a][cj], logs only)
+    double capacity = 0.0, sys_w = 0.0;
     // Kp memo per budget value
     double kp_budget = -1.0;
     int kp = m.nd_p;
@@ -136,9 +137,9 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
     uint64_t h = 0xcbf29ce484222325ULL;
     double energy = 0.0, tokens = 0.0;
     int n_applied = 0;
-    pals_step_log* lg = (logs && ti < sp.n_log_traces && (!kWarp || lane == 0))
-                            ? logs + ti * (int64_t)sp.n_steps : nullptr;
-    pals_step_detail* dt = (lg && details) ? details + ti * (int64_t)sp.n_steps : nullptr;
+    // step logs of the first n_log_traces traces (pointers formed per step: fewer
+    // registers live across the loop)
+    const bool logging = logs && ti < sp.n_log_traces && (!kWarp || lane == 0);
     double noise_lane = 1.0;  // warp layout: noise of step (k & ~31) + lane
 
     for (int k = 0; k < sp.n_steps; ++k) {
@@ -184,7 +185,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
                     j = lo;
                 }
             }
-            cap = wc[j];
+            cj = j;
             capacity = (double)m.dp * m.walk_T[wo + j];
             sys_w = m.walk_pn[wo + j];  // = dp * (alpha * 4 * P + beta) (sim.hpp:413-414)
             c_a = applied_a;
@@ -281,14 +282,17 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
                               (uint64_t)d_reason;
         h = (h ^ word) * 0x100000001b3ULL;
         n_applied += d_applied;
-        if (lg) {
+        if (logging) {
+            pals_step_log* lg = logs + ti * (int64_t)sp.n_steps;
+            const double cap = m.walk_c[(int64_t)c_a * m.L + cj];
             pals_step_log r;
             r.idx = d_idx;
             r.applied = (uint8_t)d_applied;
             r.reason = (uint8_t)d_reason;
             r.cap_tenths = (uint16_t)llround(cap * 10.0);
             lg[k] = r;
-            if (dt) {  // DecisionRecord err_norm / bias (sim.hpp:438-440, 462-463)
+            if (details) {  // DecisionRecord err_norm / bias (sim.hpp:438-440, 462-463)
+                pals_step_detail* dt = details + ti * (int64_t)sp.n_steps;
                 pals_step_detail x;
                 x.err_norm = target_tps > 0.0 ? (target_tps - measured) / target_tps : 0.0;
                 x.bias = bias;

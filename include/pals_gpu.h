@@ -571,6 +571,23 @@ int pals_run_scenarios(pals_ctx* ctx, int32_t n_scenarios, const pals_scenario* 
                        pals_sim_result* results, int64_t log_stride,
                        pals_sim_telemetry* telemetry, pals_sim_decision* decisions);
 
+/* RequestRec (sim.hpp:100-107) of every simulated request, when kept. */
+typedef struct {
+    int64_t id;
+    double arrival_s;
+    int32_t output_tokens;
+    int32_t _pad;
+    double generated;
+    double completed_s;       /* -1 while open */
+} pals_sim_request;
+/* With enable != 0, later pals_run_scenarios calls on ctx also record every request
+ * (12 B per request on the device); pals_sim_requests then copies node `node`'s
+ * records (nodes numbered across scenarios, as node_results) — n = count; out may be
+ * NULL to size. */
+int pals_sim_keep_requests(pals_ctx* ctx, int32_t enable);
+int pals_sim_requests(pals_ctx* ctx, int64_t node, pals_sim_request* out, int64_t cap,
+                      int64_t* n);
+
 /* Timing of the last pals_run_scenarios on ctx: host setup seconds (arrival
  * streams, select tables, budget splits, uploads) and the simulation kernel's
  * device milliseconds (CUDA events on the context stream). */

@@ -470,9 +470,8 @@ inline std::vector<FrontierPoint> evaluate_regime(
 
 // ---- queue-plant simulation (sim.hpp:209-500) ------------------------------------
 // run_scenario for many scenarios in one GPU pass; every SimResult is the
-// reference's (scenario, per-node telemetry / decisions, targets, arrival hashes,
-// total energy). NodeResult::requests is not materialised (the per-request records
-// stay on the device; completion counts are in the summaries).
+// reference's (scenario, per-node telemetry / decisions / requests, targets,
+// arrival hashes, total energy).
 inline std::vector<SimResult> run_scenarios(Context& ctx, const std::vector<Scenario>& scs,
                                             const ProfileRegistry& registry,
                                             const Platform& platform,
@@ -543,9 +542,13 @@ inline std::vector<SimResult> run_scenarios(Context& ctx, const std::vector<Scen
     std::vector<pals_sim_result> res(scs.size());
     std::vector<pals_sim_telemetry> tel(n_nodes * stride);
     std::vector<pals_sim_decision> dec(n_nodes * stride);
-    check(pals_run_scenarios(ctx.get(), static_cast<int32_t>(cs.size()), cs.data(),
-                             static_cast<int32_t>(profs.size()), profs.data(), preds.data(), &g,
-                             &k, nres.data(), res.data(), stride, tel.data(), dec.data()));
+    check(pals_sim_keep_requests(ctx.get(), 1));
+    const int rc = pals_run_scenarios(ctx.get(), static_cast<int32_t>(cs.size()), cs.data(),
+                                      static_cast<int32_t>(profs.size()), profs.data(),
+                                      preds.data(), &g, &k, nres.data(), res.data(), stride,
+                                      tel.data(), dec.data());
+    pals_sim_keep_requests(ctx.get(), 0);
+    check(rc);
     const DecisionReason reasons[] = {DecisionReason::QosFeasibleMaxEfficiency,
                                       DecisionReason::FallbackMaxThroughput,
                                       DecisionReason::BudgetConstrainedMaxThroughput,
@@ -587,6 +590,19 @@ inline std::vector<SimResult> run_scenarios(Context& ctx, const std::vector<Scen
                 dr.err_norm = d.err_norm;
                 dr.bias = d.bias;
                 nr.decisions.push_back(dr);
+            }
+            int64_t nq = 0;
+            check(pals_sim_requests(ctx.get(), gi, nullptr, 0, &nq));
+            std::vector<pals_sim_request> rq(static_cast<std::size_t>(nq));
+            check(pals_sim_requests(ctx.get(), gi, rq.data(), nq, &nq));
+            for (const auto& q : rq) {
+                RequestRec rr;
+                rr.id = static_cast<long>(q.id);
+                rr.arrival_s = q.arrival_s;
+                rr.output_tokens = q.output_tokens;
+                rr.generated = q.generated;
+                rr.completed_s = q.completed_s;
+                nr.requests.push_back(rr);
             }
             r.nodes.push_back(std::move(nr));
         }

@@ -310,8 +310,8 @@ class Reference:
         if want_csv:
             buf = C.create_string_buffer(max(1, n.value))
             L.ref_run_scenario(*args, buf, n.value, C.byref(n))
-            tcsv, dcsv = buf.raw[: n.value].split(b"\0")
-            out = out + ((tcsv, dcsv),)
+            tcsv, dcsv, rcsv = buf.raw[: n.value].split(b"\0")
+            out = out + ((tcsv, dcsv, rcsv),)
         return out
 
     def bench_scenarios(self, scenarios, profiles, gpu, coeffs, bundle_path, threads):

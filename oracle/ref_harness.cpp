@@ -1093,7 +1093,8 @@ int ref_run_scenario(const pals_scenario* s, int n_models, const pals_profile* p
         out->sim_total_energy_j = r.total_energy_j;
         out->n_intervals = r.nodes.empty() ? 0 : static_cast<int>(r.nodes[0].telemetry.size());
         if (csv_len) {
-            const std::string text = telemetry_csv(r) + std::string(1, '\0') + decisions_csv(r);
+            const std::string text = telemetry_csv(r) + std::string(1, '\0') + decisions_csv(r) +
+                                     std::string(1, '\0') + requests_csv(r);
             *csv_len = static_cast<std::int64_t>(text.size());
             if (csv) std::memcpy(csv, text.data(), std::min<std::size_t>(text.size(), csv_cap));
         }

@@ -184,6 +184,9 @@ SIM_TEL_DT = np.dtype([
 SIM_DEC_DT = np.dtype([
     ("err_norm", "<f8"), ("bias", "<f8"), ("cap_w", "<f8"), ("batch", "<i4"), ("applied", "u1"),
     ("reason", "u1"), ("_pad", "<u2")], align=True)
+SIM_REQ_DT = np.dtype([("id", "<i8"), ("arrival_s", "<f8"), ("output_tokens", "<i4"),
+                       ("_pad", "<i4"), ("generated", "<f8"), ("completed_s", "<f8")], align=True)
+assert SIM_REQ_DT.itemsize == 40
 assert C.sizeof(SimNode) == 40 and C.sizeof(Scenario) == 216
 assert SIM_NODE_RESULT_DT.itemsize == 96 and SIM_RESULT_DT.itemsize == 72
 assert SIM_TEL_DT.itemsize == 72 and SIM_DEC_DT.itemsize == 32

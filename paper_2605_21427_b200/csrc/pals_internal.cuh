@@ -10,6 +10,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "../../include/pals_gpu.h"
 
@@ -213,6 +214,8 @@ struct pals_ctx {
     int replay_layout = 0;         // PALS_REPLAY_THREAD / PALS_REPLAY_WARP
     double sim_prep_s = 0.0;       // sim.cu: host setup of the last pals_run_scenarios
     double sim_kernel_ms = -1.0;   // and its k_sim launch (CUDA events)
+    int sim_keep_requests = 0;     // pals_sim_keep_requests
+    std::vector<std::vector<pals_sim_request>> sim_requests;  // per node of the last run
     void* d_front = nullptr;       // frontier.cu scratch
     size_t front_bytes = 0;
 };

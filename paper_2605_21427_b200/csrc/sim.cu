@@ -172,8 +172,11 @@ struct SimNodeDev {
     const Analytic* plant;      // the node's calibrated profile
     const int32_t* cum;         // [n_int + 1]
     const int32_t* len;         // request lengths by id
-    int32_t* run_len;           // running list (global fallback): output tokens, generated
-    double* run_gen;
+    int32_t* run_len;           // running list (global fallback): output tokens, generated,
+    double* run_gen;            // request id
+    int32_t* run_id;
+    int32_t* req_k;             // optional per request: completion interval + 1 (0 = open)
+    double* req_gen;            // optional per request: generated tokens of open requests
     const double* budget;       // node budget per budget change
     int tp, ep, dp;
     int init_idx;
@@ -232,10 +235,12 @@ __global__ void __launch_bounds__(32 * PALS_SIM_MAX_NODES) k_sim(SimArgs a) {
     extern __shared__ __align__(16) char dyn_smem[];
     double* run_gen = N.run_gen;
     int32_t* run_len = N.run_len;
+    int32_t* run_id = N.run_id;
     if (a.smem_run > 0) {
+        const size_t nw = blockDim.x >> 5;
         run_gen = (double*)dyn_smem + (size_t)w * a.smem_run;
-        run_len = (int32_t*)((double*)dyn_smem + (size_t)(blockDim.x >> 5) * a.smem_run) +
-                  (size_t)w * a.smem_run;
+        run_len = (int32_t*)((double*)dyn_smem + nw * a.smem_run) + (size_t)w * a.smem_run;
+        run_id = (int32_t*)((double*)dyn_smem + nw * a.smem_run) + (nw + w) * a.smem_run;
     }
     const ReplayModelDev& m = *N.sel;
     const Analytic& P = *N.plant;
@@ -329,6 +334,7 @@ __global__ void __launch_bounds__(32 * PALS_SIM_MAX_NODES) k_sim(SimArgs a) {
                         for (int j = lane; j < n_adm; j += 32) {
                             run_len[R + j] = N.len[next_admit + j];
                             run_gen[R + j] = 0.0;
+                            run_id[R + j] = next_admit + j;
                         }
                         R += n_adm;
                         next_admit += n_adm;
@@ -351,13 +357,15 @@ __global__ void __launch_bounds__(32 * PALS_SIM_MAX_NODES) k_sim(SimArgs a) {
                     int kept = 0;
                     for (int base = 0; base < R; base += 32) {
                         const int j = base + lane;
-                        int id = 0;
+                        int id = 0, rid = 0;
                         double g = 0.0;
                         bool done = false;
                         if (j < R) {
                             id = run_len[j];
+                            rid = run_id[j];
                             g = run_gen[j];
                             done = g >= (double)id - 1e-7;
+                            if (done && N.req_k) N.req_k[rid] = k + 1;  // completed_s = t1
                         }
                         const unsigned keep = __ballot_sync(kFull, j < R && !done);
                         const unsigned fin = __ballot_sync(kFull, done);
@@ -366,6 +374,7 @@ __global__ void __launch_bounds__(32 * PALS_SIM_MAX_NODES) k_sim(SimArgs a) {
                             const int dst = kept + __popc(keep & ((1u << lane) - 1));
                             run_len[dst] = id;
                             run_gen[dst] = g;
+                            run_id[dst] = rid;
                         }
                         kept += __popc(keep);
                         completed += __popc(fin);
@@ -500,6 +509,8 @@ __global__ void __launch_bounds__(32 * PALS_SIM_MAX_NODES) k_sim(SimArgs a) {
         }
         __syncthreads();
     }
+    if (live && N.req_gen)  // requests still running keep their partial progress
+        for (int j = lane; j < R; j += 32) N.req_gen[run_id[j]] = run_gen[j];
     if (live && lane == 0) {
         pals_sim_node_result r;
         const double n = (double)S.n_int;
@@ -982,7 +993,9 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
     std::vector<SimScenDev> hs(n_scen);
     std::vector<SimNodeDev> hn(total_nodes);
     std::vector<size_t> o_chg(n_scen), o_track(n_scen, 0), o_bud(total_nodes),
-        o_run_len(total_nodes), o_run_gen(total_nodes);
+        o_run_len(total_nodes), o_run_gen(total_nodes), o_run_id(total_nodes),
+        o_req_k(total_nodes), o_req_gen(total_nodes);
+    const bool keep_req = ctx->sim_keep_requests != 0;
     size_t max_run = 0;
     {
         int64_t gi = 0;
@@ -999,6 +1012,12 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
                     (size_t)std::max(mb, sc.initial_batch) * sc.nodes[i].dp + 32;
                 max_run = std::max(max_run, run_cap);
                 o_run_len[gi] = res.stage((const int32_t*)nullptr, run_cap);
+                o_run_id[gi] = res.stage((const int32_t*)nullptr, run_cap);
+                if (keep_req) {
+                    const size_t nreq = streams[node_stream[gi]].len.size();
+                    o_req_k[gi] = res.stage((const int32_t*)nullptr, nreq);
+                    o_req_gen[gi] = res.stage((const double*)nullptr, nreq);
+                }
                 o_run_gen[gi] = res.stage((const double*)nullptr, run_cap);
             }
         }
@@ -1035,6 +1054,9 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
                 N.cum = res.at<int32_t>(o_cum[node_stream[gi]]);
                 N.len = res.at<int32_t>(o_len[node_stream[gi]]);
                 N.run_len = res.at<int32_t>(o_run_len[gi]);
+                N.run_id = res.at<int32_t>(o_run_id[gi]);
+                N.req_k = keep_req ? res.at<int32_t>(o_req_k[gi]) : nullptr;
+                N.req_gen = keep_req ? res.at<double>(o_req_gen[gi]) : nullptr;
                 N.run_gen = res.at<double>(o_run_gen[gi]);
                 N.budget = res.at<double>(o_bud[gi]);
             }
@@ -1072,7 +1094,7 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
     PALS_CUDA(cudaEventCreate(&ev0));
     PALS_CUDA(cudaEventCreate(&ev1));
     cudaEventRecord(ev0, ctx->stream);
-    const size_t smem = (size_t)max_nodes * max_run * (sizeof(double) + sizeof(int32_t));
+    const size_t smem = (size_t)max_nodes * max_run * (sizeof(double) + 2 * sizeof(int32_t));
     A.smem_run = smem <= 160 * 1024 ? (int)max_run : 0;
     if (A.smem_run)
         PALS_CUDA(cudaFuncSetAttribute(k_sim, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1102,6 +1124,43 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
     if (e != cudaSuccess) return cuda_fail(e, "pals_run_scenarios");
     for (int64_t gi = 0; gi < total_nodes; ++gi)
         node_results[gi].arrival_stream_hash = streams[node_stream[gi]].hash;
+    // RequestRec per request (sim.hpp:100-107), kept on the context for pals_sim_requests
+    ctx->sim_requests.clear();
+    if (keep_req) {
+        ctx->sim_requests.resize(total_nodes);
+        int64_t gi = 0;
+        for (int s = 0; s < n_scen; ++s)
+            for (int i = 0; i < scens[s].n_nodes; ++i, ++gi) {
+                const Stream& st = streams[node_stream[gi]];
+                const size_t nreq = st.len.size();
+                std::vector<int32_t> kk(nreq);
+                std::vector<double> gg(nreq);
+                e = copy_on(ctx->stream, kk.data(), res.at<int32_t>(o_req_k[gi]), nreq * 4,
+                            cudaMemcpyDeviceToHost);
+                if (e == cudaSuccess)
+                    e = copy_on(ctx->stream, gg.data(), res.at<double>(o_req_gen[gi]), nreq * 8,
+                                cudaMemcpyDeviceToHost);
+                if (e != cudaSuccess) return cuda_fail(e, "pals_run_scenarios: requests");
+                auto& out = ctx->sim_requests[gi];
+                out.resize(nreq);
+                const double iv = scens[s].interval_s;
+                std::vector<double> arrival(nreq, 0.0);  // backlog: spawned at t = 0
+                int64_t prev = scens[s].nodes[i].initial_backlog;
+                for (int k = 0; k < n_int[s]; ++k) {
+                    for (int64_t q = prev; q < st.cum[k]; ++q) arrival[q] = k * iv;
+                    prev = st.cum[k];
+                }
+                for (size_t q = 0; q < nreq; ++q) {
+                    pals_sim_request& r = out[q];
+                    r.id = (int64_t)q;
+                    r.arrival_s = arrival[q];
+                    r.output_tokens = st.len[q];
+                    r._pad = 0;
+                    r.completed_s = kk[q] ? (kk[q] - 1) * iv + iv : -1.0;
+                    r.generated = kk[q] ? (double)st.len[q] : gg[q];
+                }
+            }
+    }
     return PALS_OK;
 }
 
@@ -1109,5 +1168,24 @@ extern "C" int pals_sim_last_timing(pals_ctx* ctx, double* host_setup_s, double*
     if (!ctx) return set_error(PALS_ECONFIG, "pals_sim_last_timing: null context");
     if (host_setup_s) *host_setup_s = ctx->sim_prep_s;
     if (kernel_ms) *kernel_ms = ctx->sim_kernel_ms;
+    return PALS_OK;
+}
+
+extern "C" int pals_sim_keep_requests(pals_ctx* ctx, int32_t enable) {
+    if (!ctx) return set_error(PALS_ECONFIG, "pals_sim_keep_requests: null context");
+    ctx->sim_keep_requests = enable ? 1 : 0;
+    return PALS_OK;
+}
+
+extern "C" int pals_sim_requests(pals_ctx* ctx, int64_t node, pals_sim_request* out, int64_t cap,
+                                 int64_t* n) {
+    if (!ctx || !n) return set_error(PALS_ECONFIG, "pals_sim_requests: null argument");
+    if (node < 0 || node >= (int64_t)ctx->sim_requests.size())
+        return set_error(PALS_ERANGE, "pals_sim_requests: node outside the last run (or "
+                                      "requests were not kept)");
+    const auto& v = ctx->sim_requests[node];
+    *n = (int64_t)v.size();
+    if (out && cap > 0)
+        std::memcpy(out, v.data(), sizeof(pals_sim_request) * (size_t)std::min<int64_t>(cap, *n));
     return PALS_OK;
 }

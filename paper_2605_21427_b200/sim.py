@@ -16,7 +16,7 @@ import os
 import numpy as np
 
 from .abi import (OBJ_BUDGET, OBJ_QOS, POLICIES, REASON_NAMES, SIM_DEC_DT, SIM_NODE_RESULT_DT,
-                  SIM_RESULT_DT, SIM_TEL_DT, CtrlCfg, Profile, Scenario, SimNode,
+                  SIM_REQ_DT, SIM_RESULT_DT, SIM_TEL_DT, CtrlCfg, Profile, Scenario, SimNode,
                   default_ctrl_cfg, ptr)
 from ._lib import check
 
@@ -124,7 +124,8 @@ def n_intervals(sc: dict) -> int:
     return int(np.floor(x + 0.5)) if x >= 0 else -int(np.floor(-x + 0.5))
 
 
-def run_scenarios(ctx, scenarios, profiles, gpu, coeffs, predictors=None, logs: bool = False):
+def run_scenarios(ctx, scenarios, profiles, gpu, coeffs, predictors=None, logs: bool = False,
+                  requests: bool = False):
     """run_scenario for every scenario dict (policy etc. inside each) on the GPU.
     predictors: {model_name: forest model handle} (predictor_scorer) or None.
     Returns (node_results, results, telemetry, decisions): node_results is
@@ -143,10 +144,21 @@ def run_scenarios(ctx, scenarios, profiles, gpu, coeffs, predictors=None, logs: 
     res = np.zeros(len(cs), SIM_RESULT_DT)
     tel = np.zeros((n_nodes, max(stride, 1)), SIM_TEL_DT) if logs else None
     dec = np.zeros((n_nodes, max(stride, 1)), SIM_DEC_DT) if logs else None
+    check(ctx.lib.pals_sim_keep_requests(ctx.h, 1 if requests else 0))
     check(ctx.lib.pals_run_scenarios(ctx.h, len(cs), arr, len(profiles), profs, preds,
                                      C.byref(gpu), C.byref(coeffs), ptr(nres), ptr(res), stride,
                                      ptr(tel), ptr(dec)))
-    return nres, res, tel, dec
+    if not requests:
+        return nres, res, tel, dec
+    reqs = []
+    for i in range(n_nodes):
+        n = C.c_int64(0)
+        check(ctx.lib.pals_sim_requests(ctx.h, i, None, 0, C.byref(n)))
+        r = np.zeros(n.value, SIM_REQ_DT)
+        check(ctx.lib.pals_sim_requests(ctx.h, i, ptr(r), n.value, C.byref(n)))
+        reqs.append(r)
+    check(ctx.lib.pals_sim_keep_requests(ctx.h, 0))
+    return nres, res, tel, dec, reqs
 
 
 def last_timing(ctx):
@@ -205,5 +217,15 @@ def decisions_csv(scenario: dict, tel: np.ndarray, dec: np.ndarray) -> bytes:
     return "".join(out).encode()
 
 
+def requests_csv(scenario: dict, reqs) -> bytes:
+    """requests_csv (metrics.hpp:159-166) from the per-node request records."""
+    out = ["node,model,id,arrival_s,output_tokens,generated,completed_s\n"]
+    for i, nd in enumerate(scenario["nodes"]):
+        m = nd["model"]
+        out.extend(f"{i},{m},{int(q['id'])},{_g(q['arrival_s'])},{int(q['output_tokens'])},"
+                   f"{_g(q['generated'])},{_g(q['completed_s'])}\n" for q in reqs[i])
+    return "".join(out).encode()
+
+
 __all__ = ["scenario_from_dict", "bundled_scenarios", "run_scenarios", "run_baseline_suite",
-           "telemetry_csv", "decisions_csv", "n_intervals", "CtrlCfg"]
+           "telemetry_csv", "decisions_csv", "requests_csv", "n_intervals", "CtrlCfg"]

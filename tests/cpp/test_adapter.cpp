@@ -468,7 +468,8 @@ int main(int argc, char** argv) {
                 const RunSummary sw = summarize(rw), sg = summarize(rg);
                 ok = ok && same_bits(sw.aggregate.tokens_per_joule, sg.aggregate.tokens_per_joule) &&
                      same_bits(sw.cluster_tracking_mae_w, sg.cluster_tracking_mae_w) &&
-                     decisions_csv(rw) == decisions_csv(rg) && telemetry_csv(rw) == telemetry_csv(rg);
+                     decisions_csv(rw) == decisions_csv(rg) && telemetry_csv(rw) == telemetry_csv(rg) &&
+                     requests_csv(rw) == requests_csv(rg);
                 EXPECT(ok, (name + "/" + to_string(pol)).c_str());
                 ++n_sc;
             }

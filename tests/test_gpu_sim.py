@@ -11,7 +11,7 @@ import pytest
 from paper_2605_21427_b200.abi import POLICIES
 from paper_2605_21427_b200.forest import Bundle, make_forest_model
 from paper_2605_21427_b200.sim import (bundled_scenarios, decisions_csv, n_intervals,
-                                       run_scenarios, telemetry_csv)
+                                       requests_csv, run_scenarios, telemetry_csv)
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -53,16 +53,18 @@ def test_bundled_scenarios_all_policies(ctx, reference, setup):
         for pol in POLICIES:
             scs.append(dict(sc, policy=pol))
             tags.append(f"{name}/{pol}")
-    nres, res, tel, dec = run_scenarios(ctx, scs, profs, gpu, coeffs, preds, logs=True)
+    nres, res, tel, dec, reqs = run_scenarios(ctx, scs, profs, gpu, coeffs, preds, logs=True,
+                                              requests=True)
     o = 0
     for i, (sc, tag) in enumerate(zip(scs, tags)):
         k = len(sc["nodes"])
         ref = reference.run_scenario(sc, profs, gpu, coeffs, path, want_csv=True)
         ours = (nres[o:o + k], res[i], tel[o:o + k], dec[o:o + k])
         _check(ours, ref[:4], sc, tag)
-        tcsv, dcsv = ref[4]
+        tcsv, dcsv, rcsv = ref[4]
         assert telemetry_csv(sc, tel[o:o + k]) == tcsv, tag
         assert decisions_csv(sc, tel[o:o + k], dec[o:o + k]) == dcsv, tag
+        assert requests_csv(sc, reqs[o:o + k]) == rcsv, tag
         o += k
 
 

@@ -205,6 +205,7 @@ struct SimArgs {
     pals_sim_telemetry* tel;
     pals_sim_decision* dec;
     int smem_run;  // > 0: running lists live in shared memory, smem_run entries per warp
+    const int32_t* order;  // CTA -> scenario
 };
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -218,7 +219,8 @@ __device__ __forceinline__ double warp_min(double v) {
 }
 
 __global__ void __launch_bounds__(32 * PALS_SIM_MAX_NODES) k_sim(SimArgs a) {
-    const SimScenDev S = a.scen[blockIdx.x];
+    const int sid = a.order[blockIdx.x];  // longest scenarios first (shorter tail)
+    const SimScenDev S = a.scen[sid];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     __shared__ double sh_sys[PALS_SIM_MAX_NODES], sh_bud[PALS_SIM_MAX_NODES];
     __shared__ double sh_cluster_abs, sh_energy;
@@ -551,7 +553,7 @@ __global__ void __launch_bounds__(32 * PALS_SIM_MAX_NODES) k_sim(SimArgs a) {
         o.sim_total_energy_j = sh_energy;
         o.n_intervals = S.n_int;
         o.n_budget_changes = S.n_changes;
-        a.out[blockIdx.x] = o;
+        a.out[sid] = o;
     }
 }
 
@@ -1064,7 +1066,15 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
     }
     SimArgs A;
     memset(&A, 0, sizeof A);
-    int r = res.upload((SimScenDev**)&A.scen, hs);
+    // CTA order: most node-intervals first, so the long scenarios do not form the tail
+    std::vector<int32_t> order(n_scen);
+    for (int s = 0; s < n_scen; ++s) order[s] = s;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+        return (int64_t)n_int[x] * scens[x].n_nodes > (int64_t)n_int[y] * scens[y].n_nodes;
+    });
+    int r = res.upload((int32_t**)&A.order, order);
+    if (r) return r;
+    r = res.upload((SimScenDev**)&A.scen, hs);
     if (r) return r;
     r = res.upload((SimNodeDev**)&A.nodes, hn);
     if (r) return r;

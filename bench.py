@@ -763,6 +763,33 @@ def bench_cfg3(args, dist, ctx, stream, l2_flush, int_peak):
         e2e_ms.append(a.elapsed_time(b))
     e2e_max = dist.max(float(np.sum(e2e_ms)))
     scan_avg = float(np.mean(scan_ms))
+    # the optional EP x DP extension of cfg3: 589,824 configs, 64-bit keys
+    cx = workloads.cfg3_extended()
+    planx = Plan(AnalyticModel(ctx, cx["profile"], cx["gpu"]), Grid(ctx, cx["points"]),
+                 cx["coeffs"])
+    thx, _, _ = planx.scores()
+    nqx = max(1, min(nq, 10_000))
+    qx = workloads.gen_queries(nqx, c["seed"], float(thx.max()), c["objective"],
+                               budget=c["budget"], first=dist.rank * nqx)
+    d_qx = torch.from_numpy(qx.view(np.uint8).copy()).cuda()
+    stepx = lambda: planx.run(d_qx.data_ptr(), nqx, d_idx.data_ptr(), d_rs.data_ptr())  # noqa
+    stepx()
+    torch.cuda.synchronize()
+    cx_cnt = planx.stats()
+    evx = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    for k in range(args.steps):
+        l2_flush()
+        evx[k][0].record(stream)
+        stepx()
+        evx[k][1].record(stream)
+    torch.cuda.synchronize()
+    tx = dist.max(float(np.sum([e0.elapsed_time(e1) for e0, e1 in evx])))
+    pairs_x = dist.sum(float((cx_cnt[0] + cx_cnt[1] + cx_cnt[2]) * len(cx["points"]))) * args.steps
+    extended = {"workload": "cfg3 x EP{1,4,8} x DP{1,2,3}: 589,824 configs (64-bit packed keys), "
+                            f"{nqx} mixed queries per GPU, eval+rank+select per step",
+                "value": pairs_x / (tx * 1e-3), "unit": "config evals/s",
+                "ms_per_step": tx / args.steps, "queries_per_gpu": nqx}
     out = {"metric": "config evals/s (cfg3 select_config, MoE grid, mixed QoS/budget queries)",
            "value": value, "unit": "config evals/s", "ms_per_step": t_max / args.steps,
            "steps": args.steps, "workload": CFG3_WORKLOAD, "configs": n_cfg,
@@ -779,7 +806,7 @@ def bench_cfg3(args, dist, ctx, stream, l2_flush, int_peak):
                         "frac": int_ops_step / (scan_avg * 1e-3) / int_peak,
                         "algorithmic": "2 int ops per scanned pair (4 for QoS+budget queries)",
                         "scan_share_of_step": scan_avg / float(np.mean(step_ms))},
-           "gpu_launches": int(launches)}
+           "gpu_launches": int(launches), "extended_grid": extended}
     return out, c, tref
 
 

@@ -722,6 +722,8 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
         if (r) return r;
         const double ni = std::llround(sc.duration_s / sc.interval_s);  // sim.hpp:224
         n_int[s] = (int)ni;
+        if (n_int[s] < 1)  // summarize() would throw on the empty log (metrics.hpp:27)
+            return set_error(PALS_EDATA, "summarize: empty telemetry log");
         max_int = std::max<int64_t>(max_int, n_int[s]);
         max_nodes = std::max(max_nodes, sc.n_nodes);
         total_nodes += sc.n_nodes;

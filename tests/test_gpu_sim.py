@@ -103,3 +103,29 @@ def test_seed_sweep_and_variants(ctx, reference, setup):
             pytest.fail(f"reference rejected case {i}")
         _check((nres[o:o + k], res[i], tel[o:o + k], dec[o:o + k]), ref, sc, f"case{i}")
         o += k
+
+
+def test_errors_follow_the_reference(ctx, reference, setup):
+    """Invalid scenarios fail like run_scenario / summarize would (same exception kinds)."""
+    from paper_2605_21427_b200._lib import ConfigError, DataError
+    profs, gpu, coeffs, preds, path = setup
+    base = bundled_scenarios()["single_node"]
+    with pytest.raises(ConfigError, match="policy requires a trained predictor"):
+        run_scenarios(ctx, [dict(base, policy="joint")], profs, gpu, coeffs, None)
+    with pytest.raises(RuntimeError):  # the reference refuses it the same way
+        reference.run_scenario(dict(base, policy="joint"), profs, gpu, coeffs, None)
+    with pytest.raises(ConfigError, match="qos_fraction"):
+        bad = dict(base, nodes=[dict(base["nodes"][0], qos_fraction=1.5)])
+        run_scenarios(ctx, [bad], profs, gpu, coeffs, preds)
+    with pytest.raises(DataError, match="empty telemetry log"):
+        run_scenarios(ctx, [dict(base, duration_s=0.1)], profs, gpu, coeffs, preds)
+    with pytest.raises(ConfigError, match="at most 32 nodes"):
+        big = dict(base, nodes=[base["nodes"][0]] * 33)
+        run_scenarios(ctx, [big], profs, gpu, coeffs, preds)
+    # joint split of a cluster budget below the nodes' floors: allocate_budget throws
+    mn = bundled_scenarios()["multinode_qos"]
+    low = dict(mn, cluster_budget_w=100.0)
+    with pytest.raises(ConfigError):
+        run_scenarios(ctx, [low], profs, gpu, coeffs, preds)
+    with pytest.raises(RuntimeError):
+        reference.run_scenario(low, profs, gpu, coeffs, path)

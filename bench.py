@@ -679,7 +679,9 @@ def bench_allocations(args, dist, ctx, stream, l2_flush):
                      "note": "the kernel is bound by its serial per-cluster FP64 loop "
                              "(thread per cluster), not by HBM; the byte roofline is "
                              "reported for completeness",
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                     "issue_active_pct_ncu": ncu_metric("k_allocate", "issue_active_pct"),
+                     "fp64_pipe_pct_ncu": ncu_metric("k_allocate", "fp64_pipe_pct")},
         "gpu_launches": int(launches),
     }
 
@@ -958,6 +960,13 @@ def bench_sim(args, dist, ctx):
             "scenarios_per_gpu": len(scs), "seeds_per_gpu": args.sim_seeds,
             "node_intervals_per_gpu": units,
             "value_basis": "device time of the simulation kernel (k_sim)",
+            "roofline": {"bound": "latency", "kernel": "k_sim", "achieved": None, "peak": None,
+                         "frac": None, "traffic": ncu_traffic("k_sim"),
+                         "note": "each scenario is a sequential chain of 1,800-7,200 intervals "
+                                 "with dependent chunk iterations; throughput scales with "
+                                 "scenarios in flight (DESIGN.md §5e)",
+                         "issue_active_pct_ncu_16_seeds": ncu_metric("k_sim",
+                                                                     "issue_active_pct")},
             "e2e": {"value": total / wall, "unit": "node-intervals/s",
                     "h2d_bytes_per_step": None, "d2h_bytes_per_step": int(nres.nbytes + res.nbytes),
                     "host_setup_s": float(np.mean(preps)),

@@ -165,9 +165,13 @@ struct PlanDev {
     double* ef;          // t_hat / p_node
     // rank structures (per order)
     uint64_t* skey[N_ORD];   // orderable keys of the values (unsorted, padded)
-    uint64_t* sorted[N_ORD]; // chunk-sorted keys
-    uint32_t* pos[N_ORD];    // merged position of every chunk-sorted key
+    uint64_t* sorted[N_ORD]; // ping-pong buffer of the merge rounds
+    uint32_t* sidx[N_ORD];   // point index carried beside sorted[]
     uint64_t* merged[N_ORD]; // fully sorted keys (position r = competition rank r)
+    uint32_t* midx[N_ORD];   // point index carried beside merged[]
+    uint64_t* samp[N_ORD];   // merged[k * samp_s] for k < samp_n (search index)
+    int64_t samp_s;          // sample stride
+    int samp_n;              // samples per order
     uint8_t* bnd[N_ORD];     // per position i: 0 = merged[i+1] equal, 1 = distinct but a
                              // tolerance near-tie, 2 = separated (or i = n-1)
     uint8_t* danger[N_ORD];  // per run-start position: the run ends on a near-tie (bnd == 1)

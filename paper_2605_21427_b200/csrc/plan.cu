@@ -15,9 +15,10 @@
 
 #include "pals_internal.cuh"
 
+
 namespace pals {
 
-constexpr int kChunk = 4096;        // sort chunk (smem bitonic)
+constexpr int kChunk = 2048;        // sort chunk (smem block merge sort)
 constexpr int kScanCh = 2048;       // configs per scan work item
 constexpr int kScanThreads = 256;
 // queries per thread in the scan (register tile): 8 with 32-bit keys, 4 with 64-bit
@@ -51,10 +52,10 @@ struct pals_plan {
     int64_t n = 0, np = 0;
     int nchunks = 0;
     int chunk = 4096;  // sort chunk size (keys per CTA)
+    int merge_tile = 1024;  // output keys per CTA of a merge round
     int force_exact = 0;
     int values = 0;               // internal: th / ef supplied directly (frontier.cu)
     int pdl = 1;                  // programmatic dependent launch between step kernels
-    int merge_mode = 1;           // 1: pairwise merge rounds, 0: all-pairs cross-rank + scatter
     int64_t last_exact = 0;
     PlanDev d{};
     int* tr = nullptr;            // device TR per point
@@ -152,170 +153,296 @@ __global__ void k_eval_values(PlanDev d) {
 }
 
 // ---------------------------------------------------------------- sort ----
-// (1) bitonic sort of each CH-key chunk (CH/4 threads). Warp w owns keys
-// [128w, 128w+128); lane l holds key 128w + 32k + l in x[k]. Exchange distances
-// 1..16 are warp shuffles, 32 and 64 are register swaps, only >= 128 go through
-// shared memory (15 of the 78 network stages for CH = 4096).
-// The kernel also resets what the next prep kernels accumulate into (merged
-// positions, the global-candidate keys, the last-block counter of k_assign), so
-// the step needs no separate memset nodes; keys past n are padded in registers.
-template <int CH>
-__global__ void __launch_bounds__(CH / 4) k_sort_chunks(PlanDev d, uint64_t* gk,
-                                                        uint32_t* done, int32_t* counts_reset,
-                                                        int to_merged) {
-    pdl_wait();
-    constexpr int kChunk = CH;
-    __shared__ uint64_t s[kChunk];
-    const int o = blockIdx.y;
-    const int64_t base = (int64_t)blockIdx.x * kChunk;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int i0 = 128 * w + lane;
-    uint64_t x[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int64_t i = base + i0 + 32 * k;
-        x[k] = i < d.n ? d.skey[o][i] : kNone64;
-        d.pos[o][i] = 0;
+// Keys travel with their point index, so the last merge round knows where every
+// point landed and the rank pass reads the merged order front to back. Real keys
+// are clamped below kNone64 (only the all-ones NaN pattern moves, and a plan with
+// a NaN score takes the generic literal-fold path), so the padding sorts strictly
+// last and merged positions < n hold exactly the n points.
+
+// search index of the merged keys: every samp_s-th position
+__device__ __forceinline__ void put_sample(const PlanDev& d, int o, uint32_t p, uint64_t key) {
+    const uint32_t S = (uint32_t)d.samp_s;
+    if (p < (uint32_t)d.n && p % S == 0) d.samp[o][p / S] = key;
+}
+
+// (1) merge sort of each chunk of TPB * kIPT keys in shared memory (block merge
+// sort): every thread sorts its 8 (key, index) pairs with Batcher's 19-comparator
+// network in registers, then log2(TPB) rounds merge pairs of sorted lists — each
+// thread finds its 8 outputs' start on the merge path by a binary search in shared
+// memory and merges them serially. Shared arrays are padded (one slot per 16 keys,
+// per 32 indices) so the blocked register <-> smem transposes are conflict-free.
+// The kernel also resets what the next prep kernels accumulate into (the
+// global-candidate keys, the last-block counter of the rank pass, the select's
+// class counters), so the step needs no separate memset nodes.
+constexpr int kIPT = 8;
+
+__device__ __forceinline__ int pk(int e) { return e + (e >> 4); }  // padded key slot
+__device__ __forceinline__ int pv(int e) { return e + (e >> 5); }  // padded index slot
+
+__device__ __forceinline__ void cmp_swap(uint64_t (&k)[kIPT], uint32_t (&v)[kIPT], int i, int j) {
+    if (k[j] < k[i]) {
+        const uint64_t tk = k[i];
+        k[i] = k[j];
+        k[j] = tk;
+        const uint32_t tv = v[i];
+        v[i] = v[j];
+        v[j] = tv;
     }
-    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+}
+
+__device__ __forceinline__ void sort8(uint64_t (&k)[kIPT], uint32_t (&v)[kIPT]) {
+    cmp_swap(k, v, 0, 1); cmp_swap(k, v, 2, 3); cmp_swap(k, v, 4, 5); cmp_swap(k, v, 6, 7);
+    cmp_swap(k, v, 0, 2); cmp_swap(k, v, 1, 3); cmp_swap(k, v, 4, 6); cmp_swap(k, v, 5, 7);
+    cmp_swap(k, v, 1, 2); cmp_swap(k, v, 5, 6);
+    cmp_swap(k, v, 0, 4); cmp_swap(k, v, 1, 5); cmp_swap(k, v, 2, 6); cmp_swap(k, v, 3, 7);
+    cmp_swap(k, v, 2, 4); cmp_swap(k, v, 3, 5);
+    cmp_swap(k, v, 1, 2); cmp_swap(k, v, 3, 4); cmp_swap(k, v, 5, 6);
+}
+
+// merge path: how many of the first `diag` outputs of merge(A, B) come from A
+// (ties take A first). A(i), B(i): key accessors.
+template <class FA, class FB>
+__device__ __forceinline__ int mp_search(FA A, int la, FB B, int lb, int diag) {
+    int lo = max(0, diag - lb), hi = min(diag, la);
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (A(mid) <= B(diag - 1 - mid)) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// kIPT consecutive outputs of merge(A, B) starting at (a, b) on the merge path
+template <class KA, class VA, class KB, class VB>
+__device__ __forceinline__ void mp_serial(KA Ak, VA Av, int la, KB Bk, VB Bv, int lb, int a,
+                                          int b, uint64_t (&k)[kIPT], uint32_t (&v)[kIPT]) {
+    uint64_t ka = a < la ? Ak(a) : kNone64, kb = b < lb ? Bk(b) : kNone64;
+#pragma unroll
+    for (int i = 0; i < kIPT; ++i) {
+        if (b >= lb || (a < la && ka <= kb)) {
+            k[i] = ka;
+            v[i] = a < la ? Av(a) : 0u;
+            ++a;
+            ka = a < la ? Ak(a) : kNone64;
+        } else {
+            k[i] = kb;
+            v[i] = Bv(b);
+            ++b;
+            kb = b < lb ? Bk(b) : kNone64;
+        }
+    }
+}
+
+// block merge sort of the TPB * kIPT (key, index) pairs in sk/sv (padded layout);
+// leaves each thread's kIPT outputs (positions t*kIPT..) in k/v
+template <int TPB>
+__device__ __forceinline__ void block_sort(uint64_t* sk, uint32_t* sv, uint64_t (&k)[kIPT],
+                                           uint32_t (&v)[kIPT]) {
+    const int t = threadIdx.x;
+#pragma unroll
+    for (int i = 0; i < kIPT; ++i) {
+        k[i] = sk[pk(t * kIPT + i)];
+        v[i] = sv[pv(t * kIPT + i)];
+    }
+    sort8(k, v);
+    for (int w = 1; w < TPB; w <<= 1) {
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < kIPT; ++i) {
+            sk[pk(t * kIPT + i)] = k[i];
+            sv[pv(t * kIPT + i)] = v[i];
+        }
+        __syncthreads();
+        const int g0 = (t & ~(2 * w - 1)) * kIPT;  // the group's first key
+        const int len = w * kIPT;
+        const int diag = (t & (2 * w - 1)) * kIPT;
+        auto Ak = [&](int i) { return sk[pk(g0 + i)]; };
+        auto Bk = [&](int i) { return sk[pk(g0 + len + i)]; };
+        auto Av = [&](int i) { return sv[pv(g0 + i)]; };
+        auto Bv = [&](int i) { return sv[pv(g0 + len + i)]; };
+        const int a = mp_search(Ak, len, Bk, len, diag);
+        mp_serial(Ak, Av, len, Bk, Bv, len, a, diag - a, k, v);
+    }
+}
+
+template <int TPB>
+__global__ void __launch_bounds__(TPB) k_sort_chunks(PlanDev d, uint64_t* gk, uint32_t* done,
+                                                     int32_t* counts_reset, int to_merged,
+                                                     int final_round) {
+    constexpr int CH = TPB * kIPT;
+    __shared__ uint64_t sk[CH + CH / 16];
+    __shared__ uint32_t sv[CH + CH / 32];
+    pdl_wait();
+    const int o = blockIdx.y;
+    const uint32_t base = blockIdx.x * (uint32_t)CH;
+    const int t = threadIdx.x;
+    for (int i = t; i < CH; i += TPB) {
+        const uint32_t g = base + i;
+        sk[pk(i)] = g < (uint32_t)d.n ? min(d.skey[o][g], kNone64 - 1) : kNone64;
+        sv[pv(i)] = g;
+    }
+    if (blockIdx.x == 0 && blockIdx.y == 0 && t == 0) {
         gk[0] = gk[1] = kNone64;
         *done = 0;
     }
-    // in a captured step the select's class counters are reset here (no memset node)
-    if (counts_reset && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 16)
-        counts_reset[threadIdx.x] = 0;
-    for (int ks = 2; ks <= kChunk; ks <<= 1) {
-        for (int j = ks >> 1; j > 0; j >>= 1) {
-            if (j >= 128) {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) s[i0 + 32 * k] = x[k];
-                __syncthreads();
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int i = i0 + 32 * k;
-                    const uint64_t p = s[i ^ j];
-                    const bool up = (i & ks) == 0, lower = (i & j) == 0;
-                    x[k] = (up == lower) ? min(x[k], p) : max(x[k], p);
-                }
-                __syncthreads();
-            } else if (j >= 32) {
-                const int kb = j >> 5;  // 1 or 2
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    if (k & kb) continue;
-                    const int k2 = k | kb;
-                    const bool up = ((i0 + 32 * k) & ks) == 0;
-                    const uint64_t lo = min(x[k], x[k2]), hi = max(x[k], x[k2]);
-                    x[k] = up ? lo : hi;
-                    x[k2] = up ? hi : lo;
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int i = i0 + 32 * k;
-                    const uint64_t p = __shfl_xor_sync(0xffffffffu, x[k], j);
-                    const bool up = (i & ks) == 0, lower = (lane & j) == 0;
-                    x[k] = (up == lower) ? min(x[k], p) : max(x[k], p);
-                }
-            }
-        }
-    }
-#pragma unroll
-    uint64_t* dst = to_merged ? d.merged[o] : d.sorted[o];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) dst[base + i0 + 32 * k] = x[k];
-}
-
-__device__ __forceinline__ int lower_bound_s(const uint64_t* s, int n, uint64_t x) {
-    int lo = 0, hi = n;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (s[mid] < x) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
-}
-__device__ __forceinline__ int upper_bound_s(const uint64_t* s, int n, uint64_t x) {
-    int lo = 0, hi = n;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (s[mid] <= x) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
-}
-
-// (2) merged position of every chunk-sorted key = its rank within its chunk plus
-// the number of keys before it in every other chunk (a stable k-way merge).
-template <int CH>
-__global__ void __launch_bounds__(256) k_cross(PlanDev d) {
-    pdl_wait();
-    constexpr int kChunk = CH;
-    __shared__ uint64_t s[kChunk];
-    const int a = blockIdx.x, b = blockIdx.y, o = blockIdx.z;
-    const int64_t abase = (int64_t)a * kChunk, bbase = (int64_t)b * kChunk;
-    if (a != b)
-        for (int i = threadIdx.x; i < kChunk; i += blockDim.x) s[i] = d.sorted[o][bbase + i];
+    if (counts_reset && blockIdx.x == 0 && blockIdx.y == 0 && t < 16) counts_reset[t] = 0;
     __syncthreads();
-    for (int i = threadIdx.x; i < kChunk; i += blockDim.x) {
-        if (abase + i >= d.n) break;
-        const uint64_t x = d.sorted[o][abase + i];
-        int cnt;
-        if (a == b) cnt = i;
-        else if (b < a) cnt = upper_bound_s(s, kChunk, x);
-        else cnt = lower_bound_s(s, kChunk, x);
-        atomicAdd(&d.pos[o][abase + i], (uint32_t)cnt);
+    uint64_t k[kIPT];
+    uint32_t v[kIPT];
+    block_sort<TPB>(sk, sv, k, v);
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kIPT; ++i) {
+        sk[pk(t * kIPT + i)] = k[i];
+        sv[pv(t * kIPT + i)] = v[i];
+    }
+    __syncthreads();
+    uint64_t* dst = to_merged ? d.merged[o] : d.sorted[o];
+    uint32_t* dstv = to_merged ? d.midx[o] : d.sidx[o];
+    for (int i = t; i < CH; i += TPB) {
+        const uint32_t p = base + i;
+        dst[p] = sk[pk(i)];
+        dstv[p] = sv[pv(i)];
+        if (final_round) put_sample(d, o, p, sk[pk(i)]);
     }
 }
 
-// (2'') large grids: instead of searching every other chunk (O(n * chunks)), merge
-// sorted runs pairwise, log2(chunks) rounds of one binary search per key into its
-// sibling run. A key of run r lands at (its index in r) + (keys of the sibling that
-// precede it: strictly smaller from a right sibling, smaller or equal from a left
-// one), which is the stable merge k_cross + k_scatter produce. Buffers ping-pong
-// between sorted and merged; the chunk sort picks its output so the last round
-// writes merged.
-__global__ void k_merge_round(PlanDev d, int64_t np, int64_t L, int to_merged) {
+template <bool LE>
+__device__ __forceinline__ bool before(uint64_t y, uint64_t x) {
+    return LE ? y <= x : y < x;
+}
+
+// Two searches by one warp over a sorted key sequence S(i), i in [lo0, hi0): ra
+// (rb) = the first position whose key is not before xa (xb), "before" being <
+// (LE: <=). 32-ary: each round probes 32 evenly spaced positions of each key's
+// remaining range with one load per lane and narrows it by a ballot, so a 32K-key
+// range takes 3 dependent loads instead of 15. Every lane returns the same answers.
+template <bool LE, class FS>
+__device__ __forceinline__ void warp_search2(FS S, uint32_t lo0, uint32_t hi0, uint64_t xa,
+                                             uint64_t xb, uint32_t& ra, uint32_t& rb) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t la = lo0, ha = hi0, lb = lo0, hb = hi0;
+    while (la < ha || lb < hb) {
+        const uint32_t sa = (ha - la + 31) >> 5, sb = (hb - lb + 31) >> 5;
+        const uint32_t pa = la + sa * (lane + 1) - 1, pb = lb + sb * (lane + 1) - 1;
+        const bool ta = la < ha && pa < ha && before<LE>(S(pa), xa);
+        const bool tb = lb < hb && pb < hb && before<LE>(S(pb), xb);
+        const uint32_t ca = __popc(__ballot_sync(0xffffffffu, ta));
+        const uint32_t cb = __popc(__ballot_sync(0xffffffffu, tb));
+        if (la < ha) {
+            ha = min(ha, la + sa * (ca + 1) - 1);
+            la += sa * ca;
+        }
+        if (lb < hb) {
+            hb = min(hb, lb + sb * (cb + 1) - 1);
+            lb += sb * cb;
+        }
+    }
+    ra = la;
+    rb = lb;
+}
+
+// Merge-path splits of two output diagonals da, db of merge(A, B) by one warp,
+// 32-ary as in warp_search2: the predicate A(a) <= B(d-1-a) holds on a prefix of
+// the candidate a's.
+template <class FA, class FB>
+__device__ __forceinline__ void warp_mp2(FA A, uint32_t la, FB B, uint32_t lb, uint32_t da,
+                                         uint32_t db, uint32_t& ra, uint32_t& rb) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t l0 = da > lb ? da - lb : 0, h0 = min(da, la);
+    uint32_t l1 = db > lb ? db - lb : 0, h1 = min(db, la);
+    while (l0 < h0 || l1 < h1) {
+        const uint32_t s0 = (h0 - l0 + 31) >> 5, s1 = (h1 - l1 + 31) >> 5;
+        const uint32_t p0 = l0 + s0 * (lane + 1) - 1, p1 = l1 + s1 * (lane + 1) - 1;
+        const bool t0 = l0 < h0 && p0 < h0 && A(p0) <= B(da - 1 - p0);
+        const bool t1 = l1 < h1 && p1 < h1 && A(p1) <= B(db - 1 - p1);
+        const uint32_t c0 = __popc(__ballot_sync(0xffffffffu, t0));
+        const uint32_t c1 = __popc(__ballot_sync(0xffffffffu, t1));
+        if (l0 < h0) {
+            h0 = min(h0, l0 + s0 * (c0 + 1) - 1);
+            l0 += s0 * c0;
+        }
+        if (l1 < h1) {
+            h1 = min(h1, l1 + s1 * (c1 + 1) - 1);
+            l1 += s1 * c1;
+        }
+    }
+    ra = l0;
+    rb = l1;
+}
+
+// (2) pairwise merge rounds of sorted runs of length L (merge path, one output
+// tile of TPB * kIPT keys per CTA): warp 0 finds where the tile's first and last
+// diagonals cross the two runs, the tile's slices of both runs are staged in
+// shared memory with coalesced loads, and every thread merges its 8 outputs as in
+// the block sort. Ties take the left run first (a stable merge). Buffers
+// ping-pong between sorted and merged; the chunk sort picks its output so the last
+// round writes merged, and the last round also writes the search index.
+template <int TPB>
+__global__ void __launch_bounds__(TPB) k_merge_round(PlanDev d, uint32_t np, int lgL,
+                                                     int to_merged, int final_round) {
+    constexpr int TILE = TPB * kIPT;
+    __shared__ uint64_t sk[TILE + TILE / 16];
+    __shared__ uint32_t sv[TILE + TILE / 32];
+    __shared__ uint32_t split[2];
     pdl_wait();
     const int o = blockIdx.y;
-    const uint64_t* in = to_merged ? d.sorted[o] : d.merged[o];
+    const uint64_t* __restrict__ in = to_merged ? d.sorted[o] : d.merged[o];
+    const uint32_t* __restrict__ inv = to_merged ? d.sidx[o] : d.midx[o];
     uint64_t* out = to_merged ? d.merged[o] : d.sorted[o];
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < np;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = i / L, j = i - r * L, sib = r ^ 1;
-        const uint64_t x = in[i];
-        const int64_t sb = sib * L;
-        if (sb >= np) {  // no sibling run at this level
-            out[i] = x;
-            continue;
+    uint32_t* outv = to_merged ? d.midx[o] : d.sidx[o];
+    const int t = threadIdx.x;
+    const uint32_t L = 1u << lgL;
+    const uint32_t t0 = blockIdx.x * (uint32_t)TILE;
+    const uint32_t pb = t0 & ~(2 * L - 1);  // the pair's first position
+    const uint32_t la = min(L, np - pb);
+    const uint32_t lb = np - pb > L ? min(L, np - pb - L) : 0;
+    const uint64_t* A = in + pb;
+    const uint64_t* B = A + la;
+    const uint32_t d0 = t0 - pb, d1 = min(d0 + (uint32_t)TILE, la + lb);
+    if (t < 32) {
+        uint32_t a0, a1;
+        warp_mp2([&](uint32_t i) { return A[i]; }, la, [&](uint32_t i) { return B[i]; }, lb, d0,
+                 d1, a0, a1);
+        if (t == 0) {
+            split[0] = a0;
+            split[1] = a1;
         }
-        const uint64_t* sr = in + sb;
-        int64_t lo = 0, hi = min(L, np - sb);
-        if (sib < r) {
-            while (lo < hi) {
-                const int64_t mid = (lo + hi) >> 1;
-                if (sr[mid] <= x) lo = mid + 1;
-                else hi = mid;
-            }
-        } else {
-            while (lo < hi) {
-                const int64_t mid = (lo + hi) >> 1;
-                if (sr[mid] < x) lo = mid + 1;
-                else hi = mid;
-            }
-        }
-        out[(r & ~(int64_t)1) * L + j + lo] = x;
     }
-}
-
-// (3) scatter to the merged order
-__global__ void k_scatter(PlanDev d) {
-    pdl_wait();
-    const int o = blockIdx.y;
-    uint64_t* m = d.merged[o];
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        m[d.pos[o][i]] = d.sorted[o][i];
+    __syncthreads();
+    const uint32_t a0 = split[0], a1 = split[1];
+    const int na = (int)(a1 - a0), nb = (int)((d1 - a1) - (d0 - a0));
+    const uint32_t b0 = d0 - a0;
+    for (int i = t; i < na; i += TPB) {
+        sk[pk(i)] = A[a0 + i];
+        sv[pv(i)] = inv[pb + a0 + i];
+    }
+    for (int i = t; i < nb; i += TPB) {
+        sk[pk(na + i)] = B[b0 + i];
+        sv[pv(na + i)] = inv[pb + la + b0 + i];
+    }
+    __syncthreads();
+    const int diag = t * kIPT;
+    const int tot = na + nb;
+    if (diag < tot) {
+        uint64_t k[kIPT];
+        uint32_t v[kIPT];
+        auto Ak = [&](int i) { return sk[pk(i)]; };
+        auto Bk = [&](int i) { return sk[pk(na + i)]; };
+        auto Av = [&](int i) { return sv[pv(i)]; };
+        auto Bv = [&](int i) { return sv[pv(na + i)]; };
+        const int a = mp_search(Ak, na, Bk, nb, diag);
+        mp_serial(Ak, Av, na, Bk, Bv, nb, a, diag - a, k, v);
+        const uint32_t p0 = pb + d0 + diag;
+#pragma unroll
+        for (int i = 0; i < kIPT; ++i) {
+            if (diag + i < tot) {
+                out[p0 + i] = k[i];
+                outv[p0 + i] = v[i];
+                if (final_round) put_sample(d, o, p0 + i, k[i]);
+            }
+        }
+    }
 }
 
 __device__ __forceinline__ double key_value(int o, uint64_t k) {
@@ -346,71 +473,81 @@ __device__ __forceinline__ uint8_t boundary(const PlanDev& d, int o, int64_t i) 
     return separated(key_value(o, a), key_value(o, b)) ? 2 : 1;
 }
 
-// (4) per point: competition rank r = lower_bound(merged, key) and the packed key
-// (r << tr_bits) | TR; per merged position: the boundary class and whether the
-// value's run ends on a near-tie (then a winner there needs the exact fold).
-constexpr int kSamples = 1024;  // per-order sample index of the merged keys (smem)
-
-// lower_bound over merged[0, n) through a shared-memory sample of every S-th key:
-// ~10 shared probes + log2(S) probes inside one S-key window of global memory
-__device__ __forceinline__ uint32_t lower_bound_sampled(const uint64_t* m, int64_t n,
-                                                        const uint64_t* samp, int ns, int64_t S,
-                                                        uint64_t x) {
-    int lo = 0, hi = ns;  // first sample >= x
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (samp[mid] < x) lo = mid + 1;
-        else hi = mid;
-    }
-    int64_t a = lo == 0 ? 0 : (int64_t)(lo - 1) * S + 1;
-    int64_t b = lo == ns ? n : (int64_t)lo * S;
-    while (a < b) {
-        const int64_t mid = (a + b) >> 1;
-        if (m[mid] < x) a = mid + 1;
-        else b = mid;
-    }
-    return (uint32_t)a;
-}
+// (4) the rank pass, over merged positions p (one warp = 32 consecutive positions):
+// the competition rank of the key at p is the start of its run of equal keys (the
+// last run start at or before p; a run that began before the warp is found by one
+// warp search), the point it carries gets its packed key (r << tr_bits) | TR, and
+// position p gets its boundary class and, at a run start, whether the run ends on
+// a near-tie (then a winner there needs the exact fold). Coalesced except for the
+// per-point key store; at most two warp searches per warp. M(p) / V(p): the merged
+// key / point index at position p (global memory or the cluster's shared memory).
+constexpr int kSamples = 1024;  // per-order search index of the merged keys
 
 __device__ void resolve_globals_warp(const PlanDev& d, const uint64_t* gk, int w);
 
-// grid.y = order: one thread per (point, order) keeps the dependent search chains
-// short. The last block to finish resolves the two query-independent winners.
-// assign_body: block bx of nbx for order o; nblocks = all assign blocks of the launch.
-__device__ __forceinline__ void assign_body(const PlanDev& d, const int* __restrict__ tr,
-                                            uint64_t* gk, uint32_t* done, int o, int bx, int nbx,
-                                            uint32_t nblocks, uint64_t* samp) {
-    const uint64_t* m = d.merged[o];
-    const int64_t S = (d.n + kSamples - 1) / kSamples;
-    const int ns = (int)((d.n + S - 1) / S);
-    for (int t = threadIdx.x; t < ns; t += blockDim.x) samp[t] = m[t * S];
-    __syncthreads();
-    for (int64_t i = bx * (int64_t)blockDim.x + threadIdx.x; i < d.n;
-         i += (int64_t)nbx * blockDim.x) {
-        const uint32_t r = lower_bound_sampled(m, d.n, samp, ns, S, d.skey[o][i]);
-        const uint64_t k = ((uint64_t)r << d.tr_bits) | (uint64_t)tr[i];
-        if (d.wide) d.key64[o][i] = k;
-        else d.key32[o][i] = (uint32_t)k;
-        if (r == 0 && o == ORD_T) atomicMin((unsigned long long*)&gk[0], k);
-        if (r == 0 && o == ORD_P) atomicMin((unsigned long long*)&gk[1], k);
-        // position-indexed tables (thread i handles merged position i)
-        const uint8_t bi = boundary(d, o, i);
-        d.bnd[o][i] = bi;
-        // danger is read only at run starts (a competition rank is a run start):
-        // walk to the run's end, one pass per run in total
-        uint8_t dg = 0;
-        if (i == 0 || m[i - 1] != m[i]) {
-            int64_t e = i;
-            int steps = 0;
-            while (e + 1 < d.n && m[e + 1] == m[i] && ++steps < 32) ++e;
-            if (steps >= 32)  // long run: binary search for its end
-                e = (int64_t)lower_bound_sampled(m, d.n, samp, ns, S, m[i] + 1) - 1;
-            dg = boundary(d, o, e) == 1;
-        }
-        d.danger[o][i] = dg;
+__device__ __forceinline__ uint8_t bnd_class(int o, uint64_t a, uint64_t b) {
+    if (a == b) return 0;
+    return separated(key_value(o, a), key_value(o, b)) ? 2 : 1;
+}
+
+template <class FM, class FV>
+__device__ __forceinline__ void assign_warp(const PlanDev& d, const int* __restrict__ tr,
+                                            uint64_t* gk, int o, uint32_t w0, FM M, FV V) {
+    const uint32_t n = (uint32_t)d.n;
+    const uint32_t lane = threadIdx.x & 31;
+    const unsigned full = 0xffffffffu;
+    const uint32_t p = w0 + lane;
+    const bool in = p < n;
+    const uint64_t key = in ? M(p) : kNone64;
+    uint64_t prev = __shfl_up_sync(full, key, 1);
+    uint64_t next = __shfl_down_sync(full, key, 1);
+    if (lane == 0) prev = p > 0 ? M(p - 1) : ~key;
+    if (lane == 31 && p + 1 < n) next = M(p + 1);
+    const bool start = in && prev != key;
+    const unsigned sm = __ballot_sync(full, start);
+    const uint8_t bi = (in && p + 1 < n) ? bnd_class(o, key, next) : 2;
+    // rank: the last run start among lanes 0..lane, else the start of lane 0's run
+    const unsigned upto = sm & (full >> (31 - lane));
+    uint32_t r0 = w0;
+    if (!(sm & 1u)) {  // warp-uniform
+        const uint64_t k0 = __shfl_sync(full, key, 0);
+        uint32_t a, b;
+        warp_search2<false>(M, 0, w0, k0, k0, a, b);
+        r0 = a;
     }
-    // last-block-done: every block's keys, danger flags and candidate atomics are
-    // visible after its fence, so the final block can resolve the globals
+    const uint32_t r = upto ? w0 + 31 - __clz(upto) : r0;
+    // danger at a run start: the class of the boundary after the run's last position
+    const unsigned after = sm & ~(full >> (31 - lane));
+    const int tl = after ? __ffs(after) - 1 : 32;
+    const uint8_t bend = (uint8_t)__shfl_sync(full, (int)bi, (tl - 1) & 31);
+    const uint8_t b31 = (uint8_t)__shfl_sync(full, (int)bi, 31);
+    uint8_t bext = 0;
+    if (sm && b31 == 0) {  // warp-uniform: the warp's last run continues past it
+        const uint64_t kl = __shfl_sync(full, key, 31 - __clz(sm));
+        uint32_t a, b;
+        warp_search2<true>(M, w0 + 32, n, kl, kl, a, b);
+        const uint32_t e = a - 1;  // the run's last position
+        bext = e + 1 < n ? bnd_class(o, M(e), M(e + 1)) : 2;
+    }
+    if (in) {
+        const uint8_t dg = start ? ((tl < 32 || b31 != 0 ? bend : bext) == 1) : 0;
+        const uint32_t idx = V(p);
+        if (idx < n) {
+            const uint64_t k = ((uint64_t)r << d.tr_bits) | (uint64_t)tr[idx];
+            if (d.wide) d.key64[o][idx] = k;
+            else d.key32[o][idx] = (uint32_t)k;
+            if (r == 0 && o == ORD_T) atomicMin((unsigned long long*)&gk[0], k);
+            if (r == 0 && o == ORD_P) atomicMin((unsigned long long*)&gk[1], k);
+        }
+        d.bnd[o][p] = bi;
+        d.danger[o][p] = dg;
+    }
+}
+
+// last-block-done: every block's keys, danger flags and candidate atomics are
+// visible after its fence, so the final block can resolve the two global winners
+__device__ __forceinline__ void last_block_resolve(const PlanDev& d, uint64_t* gk, uint32_t* done,
+                                                   uint32_t nblocks) {
     __shared__ bool last;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -418,17 +555,35 @@ __device__ __forceinline__ void assign_body(const PlanDev& d, const int* __restr
         last = atomicAdd(done, 1u) == nblocks - 1;
     }
     __syncthreads();
-    if (last) {
+    if (last) {  // block-uniform
         __threadfence();
         const int w = threadIdx.x >> 5;
         if (w < 2) resolve_globals_warp(d, gk, w);
+        __syncthreads();
+        if (threadIdx.x == 0) {  // self-cleaning for the next prepare
+            gk[0] = gk[1] = kNone64;
+            *done = 0;
+        }
     }
+}
+
+// assign_body: block bx of nbx for order o; nblocks = all assign blocks of the launch.
+__device__ __forceinline__ void assign_body(const PlanDev& d, const int* __restrict__ tr,
+                                            uint64_t* gk, uint32_t* done, int o, int bx, int nbx,
+                                            uint32_t nblocks) {
+    const uint64_t* __restrict__ m = d.merged[o];
+    const uint32_t* __restrict__ mi = d.midx[o];
+    const uint32_t n = (uint32_t)d.n;
+    const uint32_t stride = (uint32_t)nbx * blockDim.x;
+    for (uint32_t w0 = (uint32_t)bx * blockDim.x + (threadIdx.x & ~31u); w0 < n; w0 += stride)
+        assign_warp(d, tr, gk, o, w0, [&](uint32_t q) { return m[q]; },
+                    [&](uint32_t q) { return mi[q]; });
+    last_block_resolve(d, gk, done, nblocks);
 }
 
 __global__ void k_assign(PlanDev d, const int* __restrict__ tr, uint64_t* gk, uint32_t* done) {
     pdl_wait();
-    __shared__ uint64_t samp[kSamples];
-    assign_body(d, tr, gk, done, blockIdx.y, blockIdx.x, gridDim.x, gridDim.x * gridDim.y, samp);
+    assign_body(d, tr, gk, done, blockIdx.y, blockIdx.x, gridDim.x, gridDim.x * gridDim.y);
 }
 
 
@@ -628,11 +783,11 @@ __device__ __forceinline__ int64_t count_prefix(const uint64_t* m, int o, int64_
 __device__ __forceinline__ void qprep_body(const PlanDev& d, const SelArgs& a, int bx, int nbx,
                                            double* samp_t, double* samp_p) {
     const int lane = threadIdx.x & 31;
-    const int64_t S = (d.n + kSamples - 1) / kSamples;
-    const int ns = (int)((d.n + S - 1) / S);
-    for (int t = threadIdx.x; t < ns; t += blockDim.x) {
-        samp_t[t] = key_value(ORD_T, d.merged[ORD_T][t * S]);
-        samp_p[t] = key_value(ORD_P, d.merged[ORD_P][t * S]);
+    const int64_t S = d.samp_s;
+    const int ns = d.samp_n;
+    for (int t = threadIdx.x; t < ns; t += blockDim.x) {  // written by the last merge round
+        samp_t[t] = key_value(ORD_T, d.samp[ORD_T][t]);
+        samp_p[t] = key_value(ORD_P, d.samp[ORD_P][t]);
     }
     __syncthreads();
     for (int64_t j0 = bx * (int64_t)blockDim.x; j0 < a.nq; j0 += (int64_t)nbx * blockDim.x) {
@@ -690,7 +845,7 @@ __global__ void k_assign_qprep(PlanDev d, const int* __restrict__ tr, uint64_t* 
     __shared__ uint64_t sbuf[2 * kSamples];
     if (blockIdx.y < N_ORD) {
         if ((int)blockIdx.x >= eb) return;
-        assign_body(d, tr, gk, done, blockIdx.y, blockIdx.x, eb, (uint32_t)eb * N_ORD, sbuf);
+        assign_body(d, tr, gk, done, blockIdx.y, blockIdx.x, eb, (uint32_t)eb * N_ORD);
     } else {
         if ((int)blockIdx.x >= qb) return;
         qprep_body(d, a, blockIdx.x, qb, reinterpret_cast<double*>(sbuf),
@@ -1052,16 +1207,19 @@ static int plan_build(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
     const int64_t n = std::max<int64_t>(1, g->n);
     {
         const char* e = getenv("PALS_SORT_CHUNK");
-        // measured on B200 (cfg2, n = 65,536): 2048-key chunks give the shortest
-        // sort + cross-rank (26 + 25 us vs 55 + 19 us at 4096)
-        const int c = e ? atoi(e) : (n <= 65536 ? 2048 : kChunk);
-        p->chunk = (c == 1024 || c == 2048 || c == 4096) ? c : kChunk;
+        // chunk of the multi-kernel path (n > 65,536, or PALS_RANK_CLUSTER=0)
+        // small grids (cfg1's 36 candidates, a replay's candidate sets) sort in one
+        // chunk just large enough, so the prepare does not sort 2,048 padding keys
+        int c = e ? atoi(e) : kChunk;
+        if (!e) c = n <= 256 ? 256 : n <= 512 ? 512 : n <= 1024 ? 1024 : kChunk;
+        p->chunk = (c == 256 || c == 512 || c == 1024) ? c : kChunk;
+        if (p->chunk < 1024 && n > p->chunk) p->chunk = kChunk;  // merge tiles need runs >= 1024
+        const char* t = getenv("PALS_MERGE_TILE");
+        p->merge_tile = (t && atoi(t) == 2048) ? 2048 : 1024;
     }
     {
         const char* e = getenv("PALS_PDL");
         p->pdl = e ? atoi(e) != 0 : 1;
-        const char* mm = getenv("PALS_MERGE");
-        p->merge_mode = mm ? (atoi(mm) ? 1 : 0) : 1;
     }
     p->nchunks = (int)((n + p->chunk - 1) / p->chunk);
     p->np = (int64_t)p->nchunks * p->chunk;
@@ -1073,9 +1231,12 @@ static int plan_build(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
     d.batch = g->batch;
     d.dp = g->dp;
     d.inv_tr = g->inv_tr;
+    d.samp_s = (n + kSamples - 1) / kSamples;
+    d.samp_n = (int)((n + d.samp_s - 1) / d.samp_s);
     // one slab for all per-plan device arrays
     const size_t n8 = (size_t)n * 8, np8 = (size_t)p->np * 8, np4 = (size_t)p->np * 4;
-    size_t bytes = 5 * n8 + N_ORD * (3 * np8 + np4 + n8 + (size_t)n * 4) + 64 + 4 * (size_t)n +
+    size_t bytes = 5 * n8 + N_ORD * (3 * np8 + 2 * np4 + kSamples * 8 + n8 + (size_t)n * 4) + 64 +
+                   4 * (size_t)n +
                    (d.wide ? N_ORD * n8 : N_ORD * (size_t)n * 4) + 4096;
     if (m && m->kind == MODEL_TABLE) bytes += 4 * (size_t)n + 2 * 8 * (size_t)std::max<int64_t>(1, m->table_n);
     bytes += sizeof(Analytic) + 256;
@@ -1096,7 +1257,9 @@ static int plan_build(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
         d.skey[o] = (uint64_t*)take(np8);
         d.sorted[o] = (uint64_t*)take(np8);
         d.merged[o] = (uint64_t*)take(np8);
-        d.pos[o] = (uint32_t*)take(np4);
+        d.sidx[o] = (uint32_t*)take(np4);
+        d.midx[o] = (uint32_t*)take(np4);
+        d.samp[o] = (uint64_t*)take(kSamples * 8);
         d.bnd[o] = (uint8_t*)take((size_t)n);
         d.danger[o] = (uint8_t*)take((size_t)n);
         if (d.wide) d.key64[o] = (uint64_t*)take(n8);
@@ -1107,6 +1270,8 @@ static int plan_build(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
     // the same every prepare, so it is zeroed once here instead of every step
     PALS_CUDA(cudaMemsetAsync(d.globals, 0, 16, ctx->stream));
     p->gk = (uint64_t*)take(32);  // [2] global candidate keys + k_assign's done counter
+    PALS_CUDA(cudaMemsetAsync(p->gk, 0xFF, 16, ctx->stream));
+    PALS_CUDA(cudaMemsetAsync(p->gk + 2, 0, 8, ctx->stream));
     p->d_an = (Analytic*)take(sizeof(Analytic));
     // TR per point (inverse of grid inv_tr), computed once on the host at grid creation
     p->tr = (int*)take(4 * (size_t)n);
@@ -1190,39 +1355,40 @@ static int prep_head(pals_plan* p, int32_t* counts_reset = nullptr) {
         if (rc) return rc;
     }
     if (e != cudaSuccess) return cuda_fail(e, "pals_plan_prepare eval");
-    const dim3 gs(p->nchunks, N_ORD), gx(p->nchunks, p->nchunks, N_ORD);
     uint32_t* done = (uint32_t*)(p->gk + 2);
-    // merge rounds (measured on B200: cfg2 0.176 -> 0.164 ms per step, cfg3x 5.42 -> 4.28 ms
-    // against the all-pairs cross-rank, which stays selectable with PALS_MERGE=0)
+    const dim3 gs(p->nchunks, N_ORD);
+    // chunk sort, then log2(chunks) pairwise merge rounds; the last writer of merged
+    // also writes the search index
     int rounds = 0;
     while (((int64_t)p->chunk << rounds) < p->np) ++rounds;
-    const bool merge = p->merge_mode == 1;
-    const int sort_to_merged = merge ? (rounds % 2 == 0) : 0;
-    if (p->chunk == 1024) {
-        e = launch_k(k_sort_chunks<1024>, gs, 256, 0, s, pdl, d, p->gk, done, counts_reset,
-                     sort_to_merged);
-        if (e == cudaSuccess && !merge) e = launch_k(k_cross<1024>, gx, 256, 0, s, pdl, d);
-    } else if (p->chunk == 2048) {
-        e = launch_k(k_sort_chunks<2048>, gs, 512, 0, s, pdl, d, p->gk, done, counts_reset,
-                     sort_to_merged);
-        if (e == cudaSuccess && !merge) e = launch_k(k_cross<2048>, gx, 256, 0, s, pdl, d);
-    } else {
-        e = launch_k(k_sort_chunks<4096>, gs, 1024, 0, s, pdl, d, p->gk, done, counts_reset,
-                     sort_to_merged);
-        if (e == cudaSuccess && !merge) e = launch_k(k_cross<4096>, gx, 256, 0, s, pdl, d);
-    }
-    if (merge) {
-        // round k reads the buffer round k-1 wrote; the last round writes merged
-        const dim3 gm(grid_blocks(ctx, p->np, 256), N_ORD);
-        for (int k = 0; k < rounds && e == cudaSuccess; ++k)
-            e = launch_k(k_merge_round, gm, 256, 0, s, pdl, d, p->np, (int64_t)p->chunk << k,
-                         (int)((rounds - k) % 2 == 1));
-        count_launch(ctx, rounds - 2);  // eval + sort + rounds (the 4 below: eval, sort, cross, scatter)
-    } else if (e == cudaSuccess) {
-        e = launch_k(k_scatter, dim3(grid_blocks(ctx, n, 256), N_ORD), 256, 0, s, pdl, d);
+    const int sort_to_merged = rounds % 2 == 0;
+    const int sort_final = rounds == 0;
+    if (p->chunk == 256)
+        e = launch_k(k_sort_chunks<32>, gs, 32, 0, s, pdl, d, p->gk, done, counts_reset,
+                     sort_to_merged, sort_final);
+    else if (p->chunk == 512)
+        e = launch_k(k_sort_chunks<64>, gs, 64, 0, s, pdl, d, p->gk, done, counts_reset,
+                     sort_to_merged, sort_final);
+    else if (p->chunk == 1024)
+        e = launch_k(k_sort_chunks<128>, gs, 128, 0, s, pdl, d, p->gk, done, counts_reset,
+                     sort_to_merged, sort_final);
+    else
+        e = launch_k(k_sort_chunks<256>, gs, 256, 0, s, pdl, d, p->gk, done, counts_reset,
+                     sort_to_merged, sort_final);
+    // round k reads the buffer round k-1 wrote; the last round writes merged
+    int lg = 0;
+    while ((1 << lg) < p->chunk) ++lg;
+    for (int k = 0; k < rounds && e == cudaSuccess; ++k) {
+        const int to_m = (rounds - k) % 2 == 1, fin = k == rounds - 1;
+        if (p->merge_tile == 1024)
+            e = launch_k(k_merge_round<128>, dim3((unsigned)((p->np + 1023) / 1024), N_ORD), 128, 0, s,
+                         pdl, d, (uint32_t)p->np, lg + k, to_m, fin);
+        else
+            e = launch_k(k_merge_round<256>, dim3((unsigned)((p->np + 2047) / 2048), N_ORD), 256, 0, s,
+                         pdl, d, (uint32_t)p->np, lg + k, to_m, fin);
     }
     if (e != cudaSuccess) return cuda_fail(e, "pals_plan_prepare");
-    count_launch(ctx, 4);
+    count_launch(ctx, 2 + rounds);  // eval, sort, merge rounds
     return check_launch("pals_plan_prepare");
 }
 

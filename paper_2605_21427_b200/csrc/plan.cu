@@ -91,6 +91,12 @@ struct pals_plan {
     int64_t g_n = -1;
     int g_timed = 0;
     int64_t g_launches = 0;
+    const void* g_hq = nullptr;   // pinned host buffers baked into the graph (pals_select)
+    void* g_hidx = nullptr;
+    void* g_hrs = nullptr;
+    cudaStream_t side = nullptr;  // upload stream of pals_select's graph
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    int32_t* h_cnt = nullptr;     // pinned class counters (pals_select)
 };
 
 namespace pals {
@@ -1323,6 +1329,10 @@ int pals_plan_destroy(pals_plan* p) {
     if (p->gexec) cudaGraphExecDestroy(p->gexec);
     if (p->ev_scan0) cudaEventDestroy(p->ev_scan0);
     if (p->ev_scan1) cudaEventDestroy(p->ev_scan1);
+    if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+    if (p->ev_join) cudaEventDestroy(p->ev_join);
+    if (p->side) cudaStreamDestroy(p->side);
+    if (p->h_cnt) cudaFreeHost(p->h_cnt);
     cudaFree(p->slab);
     cudaFree(p->thr_t);
     cudaFree(p->d_q);
@@ -1511,15 +1521,24 @@ int pals_plan_select_device(pals_plan* p, const pals_query* d_queries, int64_t n
 // One full step — evaluate + rank (prepare) and select — replayed from a CUDA graph
 // captured on first use for these device buffers (8 kernels, no memset nodes: the
 // class counters are reset by k_sort_chunks, assign and qprep share one launch).
-int pals_plan_run(pals_plan* p, const pals_query* d_queries, int64_t nq, int32_t* d_idx,
-                  uint8_t* d_reason) {
-    if (p->err) return set_error(p->err, p->err_msg);
-    if (nq <= 0) return pals_plan_prepare(p);
+// One step as a graph. With pinned host buffers (h_q, h_idx, h_rs: pals_select) the
+// graph also holds the copies: the queries go up on a side stream while the model
+// is evaluated and ranked (the prepare never reads them), and only qprep waits for
+// them; the decisions and class counters come back at the end.
+static int plan_step(pals_plan* p, const pals_query* d_queries, int64_t nq, int32_t* d_idx,
+                     uint8_t* d_reason, const pals_query* h_q, int32_t* h_idx, uint8_t* h_rs) {
     pals_ctx* ctx = p->ctx;
     cudaStream_t s = ctx->stream;
     const int key_t = p->time_scan | (p->force_exact << 1);
     const bool hit = p->gexec && p->g_q == d_queries && p->g_n == nq && p->g_idx == d_idx &&
-                     p->g_rs == d_reason && p->g_timed == key_t;
+                     p->g_rs == d_reason && p->g_timed == key_t && p->g_hq == h_q &&
+                     p->g_hidx == h_idx && p->g_hrs == h_rs;
+    if (h_q && !p->side) {
+        PALS_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+        PALS_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+        PALS_CUDA(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+        PALS_CUDA(cudaMallocHost(&p->h_cnt, 64));
+    }
     if (!hit) {
         if (p->gexec) {
             cudaGraphExecDestroy(p->gexec);
@@ -1533,7 +1552,20 @@ int pals_plan_run(pals_plan* p, const pals_query* d_queries, int64_t nq, int32_t
         const int64_t l0 = ctx->launches;
         // (overlapping qprep with k_assign on a side stream measured no faster on
         // B200: the step stays a single chain)
-        rc = prep_head(p, p->counts);
+        cudaError_t ce0 = cudaSuccess;
+        if (h_q) {
+            ce0 = cudaEventRecord(p->ev_fork, s);
+            if (ce0 == cudaSuccess) ce0 = cudaStreamWaitEvent(p->side, p->ev_fork, 0);
+            if (ce0 == cudaSuccess)
+                ce0 = cudaMemcpyAsync((void*)d_queries, h_q, (size_t)nq * sizeof(pals_query),
+                                      cudaMemcpyHostToDevice, p->side);
+            if (ce0 == cudaSuccess) ce0 = cudaEventRecord(p->ev_join, p->side);
+        }
+        rc = ce0 != cudaSuccess ? cuda_fail(ce0, "pals_select upload") : prep_head(p, p->counts);
+        if (!rc && h_q) {
+            const cudaError_t we = cudaStreamWaitEvent(s, p->ev_join, 0);
+            if (we != cudaSuccess) rc = cuda_fail(we, "pals_select upload join");
+        }
         if (!rc) {
             // assign (prepare, part 2) and qprep (select, part 1) fused in one launch
             const SelArgs a = make_args(p, d_queries, nq, d_idx, d_reason);
@@ -1545,6 +1577,16 @@ int pals_plan_run(pals_plan* p, const pals_query* d_queries, int64_t nq, int32_t
             if (!rc) {
                 count_launch(ctx, 1);
                 rc = select_tail(p, a);
+            }
+            if (!rc && h_idx) {
+                cudaError_t de = cudaMemcpyAsync(h_idx, d_idx, (size_t)nq * 4,
+                                                 cudaMemcpyDeviceToHost, s);
+                if (de == cudaSuccess)
+                    de = cudaMemcpyAsync(h_rs, d_reason, (size_t)nq, cudaMemcpyDeviceToHost, s);
+                if (de == cudaSuccess)
+                    de = cudaMemcpyAsync(p->h_cnt, p->counts, 4 * (N_CLS + 1),
+                                         cudaMemcpyDeviceToHost, s);
+                if (de != cudaSuccess) rc = cuda_fail(de, "pals_select download");
             }
         }
         p->capturing = 0;
@@ -1565,11 +1607,30 @@ int pals_plan_run(pals_plan* p, const pals_query* d_queries, int64_t nq, int32_t
         p->g_idx = d_idx;
         p->g_rs = d_reason;
         p->g_timed = key_t;
+        p->g_hq = h_q;
+        p->g_hidx = h_idx;
+        p->g_hrs = h_rs;
     }
     PALS_CUDA(cudaGraphLaunch(p->gexec, s));
     count_launch(ctx, (int)p->g_launches);
     if (p->time_scan) p->scan_recorded = 1;
     return PALS_OK;
+}
+
+int pals_plan_run(pals_plan* p, const pals_query* d_queries, int64_t nq, int32_t* d_idx,
+                  uint8_t* d_reason) {
+    if (p->err) return set_error(p->err, p->err_msg);
+    if (nq <= 0) return pals_plan_prepare(p);
+    return plan_step(p, d_queries, nq, d_idx, d_reason, nullptr, nullptr, nullptr);
+}
+
+static bool is_pinned(const void* h) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, h) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
 }
 
 int pals_select(pals_plan* p, const pals_query* queries, int64_t nq, int32_t* idx,
@@ -1595,6 +1656,14 @@ int pals_select(pals_plan* p, const pals_query* queries, int64_t nq, int32_t* id
     pals_query* dq = (pals_query*)b;
     int32_t* di = (int32_t*)(b + (size_t)nq * sizeof(pals_query));
     uint8_t* dr = (uint8_t*)(di + nq);
+    if (is_pinned(queries) && is_pinned(idx) && is_pinned(reason)) {
+        // one graph: upload overlapped with the prepare, decisions downloaded at the end
+        rc = plan_step(p, dq, nq, di, dr, queries, idx, reason);
+        if (rc) return rc;
+        PALS_CUDA(cudaStreamSynchronize(s));
+        p->last_exact = p->h_cnt[N_CLS];
+        return PALS_OK;
+    }
     PALS_CUDA(cudaMemcpyAsync(dq, queries, (size_t)nq * sizeof(pals_query), cudaMemcpyHostToDevice, s));
     rc = pals_plan_run(p, dq, nq, di, dr);
     if (rc) return rc;

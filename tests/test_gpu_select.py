@@ -158,3 +158,31 @@ def test_select_one_and_errors(ctx, bundle):
     other = workloads.grid_points([333.0], [3], [2])
     with pytest.raises(ConfigError, match="unscored candidate"):
         select_config(other, make_targets(100.0), m, coeffs)
+
+
+def test_select_pinned_buffers_graph_path(ctx, oracle):
+    """pals_select with pinned host buffers runs one graph holding the upload (overlapped
+    with the prepare) and the downloads; replays must read the buffers' current contents."""
+    import torch
+
+    from paper_2605_21427_b200.abi import QUERY_DT, ptr
+    from paper_2605_21427_b200.wattserve import check
+
+    cfg = workloads.cfg2()
+    model = AnalyticModel(ctx, cfg["profile"], cfg["gpu"])
+    plan = Plan(model, Grid(ctx, cfg["points"]), cfg["coeffs"])
+    th, _, _ = plan.scores()
+    T, P, _ = oracle.eval(cfg["profile"], cfg["gpu"], cfg["points"])
+    nq = 3000
+    h_q = torch.empty(nq * QUERY_DT.itemsize, dtype=torch.uint8, pin_memory=True)
+    h_qn = h_q.numpy().view(QUERY_DT)
+    h_idx = torch.empty(nq, dtype=torch.int32, pin_memory=True).numpy()
+    h_rs = torch.empty(nq, dtype=torch.uint8, pin_memory=True).numpy()
+    for seed in (11, 12, 13):  # same buffers, new contents: the cached graph is replayed
+        q = workloads.gen_queries(nq, seed, float(th.max()), "mixed", budget=(700.0, 1900.0))
+        h_qn[:] = q
+        check(ctx.lib.pals_select(plan.h, ptr(h_qn), nq, ptr(h_idx), ptr(h_rs)))
+        idx, rs = plan.select(q)  # pageable path
+        assert np.array_equal(h_idx, idx) and np.array_equal(h_rs, rs)
+        oi, orr, rc = oracle.select(cfg["points"], T, P, cfg["coeffs"], q[::7])
+        assert rc == 0 and np.array_equal(h_idx[::7], oi) and np.array_equal(h_rs[::7], orr)

@@ -282,10 +282,21 @@ __global__ void __launch_bounds__(TPB) k_sort_chunks(PlanDev d, uint64_t* gk, ui
     const int o = blockIdx.y;
     const uint32_t base = blockIdx.x * (uint32_t)CH;
     const int t = threadIdx.x;
-    for (int i = t; i < CH; i += TPB) {
-        const uint32_t g = base + i;
-        sk[pk(i)] = g < (uint32_t)d.n ? min(d.skey[o][g], kNone64 - 1) : kNone64;
-        sv[pv(i)] = g;
+    {
+        // all loads in flight before the shared stores (a generic-pointer load may
+        // not be reordered across a shared store, which would serialize the round trips)
+        uint64_t x[kIPT];
+        const uint64_t* __restrict__ src = d.skey[o];
+#pragma unroll
+        for (int k = 0; k < kIPT; ++k) {
+            const uint32_t g = base + t + k * TPB;
+            x[k] = g < (uint32_t)d.n ? min(__ldg(src + g), kNone64 - 1) : kNone64;
+        }
+#pragma unroll
+        for (int k = 0; k < kIPT; ++k) {
+            sk[pk(t + k * TPB)] = x[k];
+            sv[pv(t + k * TPB)] = base + t + k * TPB;
+        }
     }
     if (blockIdx.x == 0 && blockIdx.y == 0 && t == 0) {
         gk[0] = gk[1] = kNone64;
@@ -419,13 +430,23 @@ __global__ void __launch_bounds__(TPB) k_merge_round(PlanDev d, uint32_t np, int
     const uint32_t a0 = split[0], a1 = split[1];
     const int na = (int)(a1 - a0), nb = (int)((d1 - a1) - (d0 - a0));
     const uint32_t b0 = d0 - a0;
-    for (int i = t; i < na; i += TPB) {
-        sk[pk(i)] = A[a0 + i];
-        sv[pv(i)] = inv[pb + a0 + i];
-    }
-    for (int i = t; i < nb; i += TPB) {
-        sk[pk(na + i)] = B[b0 + i];
-        sv[pv(na + i)] = inv[pb + la + b0 + i];
+    {
+        // stage both slices: every load in flight before the shared stores
+        uint64_t x[kIPT];
+        uint32_t y[kIPT];
+#pragma unroll
+        for (int k = 0; k < kIPT; ++k) {
+            const int i = t + k * TPB;
+            const uint32_t q = i < na ? pb + a0 + i : pb + la + b0 + (i - na);
+            const bool ok = i < na + nb;
+            x[k] = ok ? __ldg(in + q) : kNone64;
+            y[k] = ok ? __ldg(inv + q) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < kIPT; ++k) {
+            sk[pk(t + k * TPB)] = x[k];
+            sv[pv(t + k * TPB)] = y[k];
+        }
     }
     __syncthreads();
     const int diag = t * kIPT;
@@ -791,9 +812,23 @@ __device__ __forceinline__ void qprep_body(const PlanDev& d, const SelArgs& a, i
     const int lane = threadIdx.x & 31;
     const int64_t S = d.samp_s;
     const int ns = d.samp_n;
-    for (int t = threadIdx.x; t < ns; t += blockDim.x) {  // written by the last merge round
-        samp_t[t] = key_value(ORD_T, d.samp[ORD_T][t]);
-        samp_p[t] = key_value(ORD_P, d.samp[ORD_P][t]);
+    {  // written by the last merge round; all loads in flight before the shared stores
+        constexpr int R = (kSamples + 255) / 256;
+        uint64_t xt[R], xp[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            const int t = threadIdx.x + k * blockDim.x;
+            xt[k] = t < ns ? __ldg(d.samp[ORD_T] + t) : 0;
+            xp[k] = t < ns ? __ldg(d.samp[ORD_P] + t) : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            const int t = threadIdx.x + k * blockDim.x;
+            if (t < ns) {
+                samp_t[t] = key_value(ORD_T, xt[k]);
+                samp_p[t] = key_value(ORD_P, xp[k]);
+            }
+        }
     }
     __syncthreads();
     for (int64_t j0 = bx * (int64_t)blockDim.x; j0 < a.nq; j0 += (int64_t)nbx * blockDim.x) {
@@ -920,6 +955,22 @@ __device__ __forceinline__ int64_t scan_pos_of(const ScanPlan& sp, int64_t u) {
 }
 
 template <typename K>
+__device__ __forceinline__ void stage_keys(K* dst, const K* __restrict__ src, int nc, int ncp) {
+    constexpr int R = kScanCh / kScanThreads;
+    K x[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+        const int i = threadIdx.x + k * kScanThreads;
+        x[k] = i < nc ? __ldg(src + i) : (K)~(K)0;
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+        const int i = threadIdx.x + k * kScanThreads;
+        if (i < ncp) dst[i] = x[k];
+    }
+}
+
+template <typename K>
 __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) {
     pdl_wait();
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -972,13 +1023,11 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) 
             const int nc = (int)min((int64_t)kScanCh, j1 - c0);
             const int ncp = (nc + 3) & ~3;
             __syncthreads();
-            // stage the keys (pad with keys that never pass a threshold)
-            for (int i = threadIdx.x; i < ncp; i += blockDim.x) {
-                const bool in = i < nc;
-                if (c != CLS_C) se[i] = in ? ke[c0 + i] : (K)~(K)0;
-                st[i] = in ? kt[c0 + i] : (K)~(K)0;
-                if (c != CLS_A) sp[i] = in ? kp[c0 + i] : (K)~(K)0;
-            }
+            // stage the keys (pad with keys that never pass a threshold); per array,
+            // all of a thread's loads are in flight before its shared stores
+            if (c != CLS_C) stage_keys<K>(se, ke + c0, nc, ncp);
+            stage_keys<K>(st, kt + c0, nc, ncp);
+            if (c != CLS_A) stage_keys<K>(sp, kp + c0, nc, ncp);
             __syncthreads();
             // padded slots carry all-ones keys: they only pass an all-ones threshold,
             // and then they cannot lower a minimum below a real key

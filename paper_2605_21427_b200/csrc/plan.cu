@@ -271,13 +271,18 @@ __device__ __forceinline__ void block_sort(uint64_t* sk, uint32_t* sv, uint64_t 
     }
 }
 
+constexpr size_t sort_smem_bytes(int tpb) {
+    return (size_t)(tpb * kIPT + tpb * kIPT / 16) * 8 + (size_t)(tpb * kIPT + tpb * kIPT / 32) * 4;
+}
+
 template <int TPB>
 __global__ void __launch_bounds__(TPB) k_sort_chunks(PlanDev d, uint64_t* gk, uint32_t* done,
                                                      int32_t* counts_reset, int to_merged,
                                                      int final_round) {
     constexpr int CH = TPB * kIPT;
-    __shared__ uint64_t sk[CH + CH / 16];
-    __shared__ uint32_t sv[CH + CH / 32];
+    extern __shared__ __align__(16) unsigned char sort_smem[];  // sort_smem_bytes(TPB)
+    uint64_t* sk = reinterpret_cast<uint64_t*>(sort_smem);
+    uint32_t* sv = reinterpret_cast<uint32_t*>(sk + CH + CH / 16);
     pdl_wait();
     const int o = blockIdx.y;
     const uint32_t base = blockIdx.x * (uint32_t)CH;
@@ -1267,8 +1272,16 @@ static int plan_build(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
         // chunk just large enough, so the prepare does not sort 2,048 padding keys
         int c = e ? atoi(e) : kChunk;
         if (!e) c = n <= 256 ? 256 : n <= 512 ? 512 : n <= 1024 ? 1024 : kChunk;
-        p->chunk = (c == 256 || c == 512 || c == 1024) ? c : kChunk;
+        p->chunk = (c == 256 || c == 512 || c == 1024 || c == 4096 || c == 8192) ? c : kChunk;
         if (p->chunk < 1024 && n > p->chunk) p->chunk = kChunk;  // merge tiles need runs >= 1024
+        if (p->chunk > 2048) {  // > 48 KB of dynamic shared memory
+            PALS_CUDA(cudaFuncSetAttribute(k_sort_chunks<512>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)sort_smem_bytes(512)));
+            PALS_CUDA(cudaFuncSetAttribute(k_sort_chunks<1024>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)sort_smem_bytes(1024)));
+        }
         const char* t = getenv("PALS_MERGE_TILE");
         p->merge_tile = (t && atoi(t) == 2048) ? 2048 : 1024;
     }
@@ -1422,18 +1435,22 @@ static int prep_head(pals_plan* p, int32_t* counts_reset = nullptr) {
     while (((int64_t)p->chunk << rounds) < p->np) ++rounds;
     const int sort_to_merged = rounds % 2 == 0;
     const int sort_final = rounds == 0;
-    if (p->chunk == 256)
-        e = launch_k(k_sort_chunks<32>, gs, 32, 0, s, pdl, d, p->gk, done, counts_reset,
-                     sort_to_merged, sort_final);
-    else if (p->chunk == 512)
-        e = launch_k(k_sort_chunks<64>, gs, 64, 0, s, pdl, d, p->gk, done, counts_reset,
-                     sort_to_merged, sort_final);
-    else if (p->chunk == 1024)
-        e = launch_k(k_sort_chunks<128>, gs, 128, 0, s, pdl, d, p->gk, done, counts_reset,
-                     sort_to_merged, sort_final);
-    else
-        e = launch_k(k_sort_chunks<256>, gs, 256, 0, s, pdl, d, p->gk, done, counts_reset,
-                     sort_to_merged, sort_final);
+    switch (p->chunk) {
+#define PALS_SORT(TPB)                                                                         \
+    case TPB * kIPT:                                                                           \
+        e = launch_k(k_sort_chunks<TPB>, gs, TPB, sort_smem_bytes(TPB), s, pdl, d, p->gk, done, \
+                     counts_reset, sort_to_merged, sort_final);                                \
+        break;
+        PALS_SORT(32)
+        PALS_SORT(64)
+        PALS_SORT(128)
+        PALS_SORT(256)
+        PALS_SORT(512)
+        PALS_SORT(1024)
+#undef PALS_SORT
+        default:
+            e = cudaErrorInvalidValue;
+    }
     // round k reads the buffer round k-1 wrote; the last round writes merged
     int lg = 0;
     while ((1 << lg) < p->chunk) ++lg;

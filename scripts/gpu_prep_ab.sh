@@ -1,9 +1,15 @@
-# Rank pipeline: parity suite, default bench, cfg2 launch list
+# Chunk-size A/B of the block sort: parity per chunk, cfg2 bench line, launch list
 set -x
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-timeout 900 python -m pytest tests -q -m gpu --timeout 400 -p no:cacheprovider -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-START=$(date +%s); timeout 1200 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$? wall=$(( $(date +%s) - START ))s" >> gpurun_out/bench.err
+for c in 4096 8192; do
+PALS_SORT_CHUNK=$c timeout 900 python -m pytest tests/test_gpu_select.py tests/test_gpu_edge.py tests/test_gpu_random.py tests/test_gpu_pareto.py -q -m gpu --timeout 400 -p no:cacheprovider -x > gpurun_out/pytest_c$c.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_c$c.log
+done
+B="--steps 10 --warmup 3 --traces 20000 --trace-steps 360 --predictions 1048576 --cfg3-queries 100000 --cfg5-traces 0 --sim-seeds 0 --no-cpu-baseline"
+for c in 2048 4096 8192; do
+PALS_SORT_CHUNK=$c timeout 600 python bench.py $B > gpurun_out/bench_c$c.json 2> gpurun_out/bench_c$c.err
+done
 SMALL="--steps 2 --warmup 1 --traces 20000 --trace-steps 60 --predictions 1048576 --cfg3-queries 10000 --cfg5-traces 0 --sim-seeds 0 --no-cpu-baseline"
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py $SMALL > /dev/null 2>&1
+for c in 8192; do
+PALS_SORT_CHUNK=$c timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c$c.csv python bench.py $SMALL > /dev/null 2>&1
+done

@@ -99,6 +99,17 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
                                                 pals_trace_summary* __restrict__ out,
                                                 pals_step_log* __restrict__ logs,
                                                 pals_step_detail* __restrict__ details) {
+    // the per-model descriptors (table pointers and plant constants read every step)
+    // are copied to shared memory: LDS instead of L1-hit loads in the step loop
+    extern __shared__ __align__(16) unsigned char rp_smem[];
+    ReplayModelDev* s_models = reinterpret_cast<ReplayModelDev*>(rp_smem);
+    {
+        const int words = p.n_models * (int)(sizeof(ReplayModelDev) / 4);
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(models);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(rp_smem);
+        for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+        __syncthreads();
+    }
     const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t slot = kWarp ? gt >> 5 : gt;
     const int lane = threadIdx.x & 31;
@@ -108,7 +119,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
     const pals_ctrl_cfg& cfg = p.cfg;
     const uint64_t key = splitmix64(sp.seed ^ (uint64_t)(sp.first_trace + ti));
     const int mi = (int)(key % (uint64_t)p.n_models);
-    const ReplayModelDev& m = models[mi];
+    const ReplayModelDev& m = s_models[mi];
     const int obj = trace_objective(sp, key);
     const double qfrac = sp.qos_frac_lo + (sp.qos_frac_hi - sp.qos_frac_lo) * u01(draw(key, 0, 1));
     const double target_tps = qfrac * m.t_max;
@@ -638,16 +649,24 @@ static int replay_launch(pals_ctx* ctx, ReplayCache* rc, const pals_ctrl_cfg* cf
         const char* e = getenv("PALS_REPLAY_MINB");
         return e ? atoi(e) : 6;  // measured: 6 CTAs/SM (80 regs) beats 4 (126 regs) by 1.4x
     }();
+    const size_t msm = sizeof(ReplayModelDev) * (size_t)p.n_models;
+    if (msm > 48 * 1024) {
+        const int b = (int)msm;
+        PALS_CUDA(cudaFuncSetAttribute(k_replay<6, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        PALS_CUDA(cudaFuncSetAttribute(k_replay<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        PALS_CUDA(cudaFuncSetAttribute(k_replay<6, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        PALS_CUDA(cudaFuncSetAttribute(k_replay<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    }
     if (ctx->replay_layout == PALS_REPLAY_WARP) {
         const int64_t wblocks = (spec->n_traces + 3) / 4;  // 4 traces (warps) per CTA
-        k_replay<6, true><<<(unsigned)wblocks, 128, 0, ctx->stream>>>(rc->d_models, p, nullptr,
-                                                                     d_sum, d_logs, d_det);
+        k_replay<6, true><<<(unsigned)wblocks, 128, msm, ctx->stream>>>(rc->d_models, p, nullptr,
+                                                                       d_sum, d_logs, d_det);
     } else if (minb >= 8)
-        k_replay<8, false><<<(unsigned)blocks, 128, 0, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs, d_det);
+        k_replay<8, false><<<(unsigned)blocks, 128, msm, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs, d_det);
     else if (minb >= 6)
-        k_replay<6, false><<<(unsigned)blocks, 128, 0, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs, d_det);
+        k_replay<6, false><<<(unsigned)blocks, 128, msm, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs, d_det);
     else
-        k_replay<1, false><<<(unsigned)blocks, 128, 0, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs, d_det);
+        k_replay<1, false><<<(unsigned)blocks, 128, msm, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs, d_det);
     count_launch(ctx);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "k_replay");

@@ -487,16 +487,6 @@ __device__ __forceinline__ bool separated(double a, double b) {
     return fabs(a - b) > 4e-9 * smax(fabs(a), fabs(b));
 }
 
-__device__ __forceinline__ uint32_t lower_bound_g(const uint64_t* m, int64_t n, uint64_t x) {
-    int64_t lo = 0, hi = n;
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (m[mid] < x) lo = mid + 1;
-        else hi = mid;
-    }
-    return (uint32_t)lo;
-}
-
 // boundary class between merged positions i and i+1 (see PlanDev::bnd)
 __device__ __forceinline__ uint8_t boundary(const PlanDev& d, int o, int64_t i) {
     if (i + 1 >= d.n) return 2;

@@ -328,14 +328,15 @@ def run_ours(args, dist: Dist):
     e2e_value = pairs_total / (e2e_max * 1e-3)
 
     scan_avg = float(np.mean(scan_ms))
-    roof = {"bound": "alu", "kernel": "k_scan<uint32_t>",
+    roof = {"bound": "alu", "kernel": "k_scan",
             "achieved": int_ops_step / (scan_avg * 1e-3) / 1e12,
             "peak": int_peak / 1e12, "unit": "Tops/s",
             "frac": (int_ops_step / (scan_avg * 1e-3)) / int_peak,
             "traffic": ncu_traffic("k_scan"),
             "algorithmic": "2 int ops (compare, min) per scanned (config, query) pair; 4 for "
                            "QoS+budget queries",
-            "peak_source": "measured here: pals_measure_peaks ISETP+VIMNMX chains",
+            "peak_source": "measured here: pals_measure_peaks chains of the scan's per-pair "
+                           "instruction mix (IMAD.IADD + LOP3 + VIMNMX3 per 2 pairs), 2 ops/pair",
             "scan_share_of_step": scan_avg / float(np.mean(step_ms)),
             "step_breakdown_ms": {"graph_step": float(np.mean(step_ms)),
                                   "scan_kernel": scan_avg,
@@ -802,7 +803,7 @@ def bench_cfg3(args, dist, ctx, stream, l2_flush, int_peak):
            "e2e": {"value": pairs_total / (e2e_max * 1e-3), "unit": "config evals/s",
                    "h2d_bytes_per_step": nq * QUERY_DT.itemsize, "d2h_bytes_per_step": nq * 5,
                    "api": "pals_select (C ABI, pinned host buffers; includes eval+rank)"},
-           "roofline": {"bound": "alu", "kernel": "k_scan<uint32_t>",
+           "roofline": {"bound": "alu", "kernel": "k_scan",
                         "achieved": int_ops_step / (scan_avg * 1e-3) / 1e12,
                         "peak": int_peak / 1e12, "unit": "Tops/s",
                         "frac": int_ops_step / (scan_avg * 1e-3) / int_peak,

@@ -157,6 +157,7 @@ struct PlanDev {
     const int* batch;
     const int* dp;
     const int* inv_tr;   // TR -> point index
+    const int* tr;       // point index -> TR
     // scores
     double* T;
     double* P;
@@ -164,11 +165,13 @@ struct PlanDev {
     double* pn;          // p_node
     double* ef;          // t_hat / p_node
     // rank structures (per order)
-    uint64_t* skey[N_ORD];   // orderable keys of the values (unsorted, padded)
+    uint64_t* skey[N_ORD];   // orderable keys of the values, in TR order (padded)
     uint64_t* sorted[N_ORD]; // ping-pong buffer of the merge rounds
-    uint32_t* sidx[N_ORD];   // point index carried beside sorted[]
+    uint32_t* sidx[N_ORD];   // TR carried beside sorted[]; after the rank pass: the
+                             // competition rank of every merged position
     uint64_t* merged[N_ORD]; // fully sorted keys (position r = competition rank r)
-    uint32_t* midx[N_ORD];   // point index carried beside merged[]
+    uint32_t* midx[N_ORD];   // TR carried beside merged[]; after the rank pass: the point
+                             // index at every merged position
     uint64_t* samp[N_ORD];   // merged[k * samp_s] for k < samp_n (search index)
     int64_t samp_s;          // sample stride
     int samp_n;              // samples per order
@@ -177,6 +180,9 @@ struct PlanDev {
     uint8_t* danger[N_ORD];  // per run-start position: the run ends on a near-tie (bnd == 1)
     uint32_t* key32[N_ORD];  // packed keys (narrow)
     uint64_t* key64[N_ORD];  // packed keys (wide)
+    uint32_t* rank32[N_ORD]; // per point: competition rank r (the pair scan's feasibility side)
+    uint32_t* pos32[N_ORD];  // per point: merged position = rank of (value, TR), i.e. of the
+                             // packed key (the pair scan's argmin side; < 2^31 for any n)
     int32_t* globals;        // [0] argmax t over all, [1] argmin p over all, [2] generic flag,
                              // [3] number of exact folds last select
 };

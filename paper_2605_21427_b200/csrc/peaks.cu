@@ -6,22 +6,27 @@
 
 namespace pals {
 
-// Integer compare + min chains: the exact instruction mix of the select scan
-// (ISETP + predicated VIMNMX), 16 independent chains per thread.
+// The pair scan's class-A/C instruction mix (k_scan, plan.cu): per (config, query)
+// pair d = K - r (IMAD.IADD), v = pos | (d & 0x80000000) (LOP3), and one VIMNMX3
+// per two pairs; 8 independent query chains per thread. Reported as 2 "int ops" per
+// pair (the algorithmic compare + min), so bench.py's achieved / peak is the scan's
+// pair rate over this chain's pair rate.
 __global__ void __launch_bounds__(256) k_peak_int(uint32_t* out, int iters, uint32_t seed) {
-    uint32_t thr[8], acc[8];
+    uint32_t K[8], acc[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-        thr[q] = seed * (q + 3) + threadIdx.x;
+        K[q] = (seed * (q + 3) + threadIdx.x) & 0xFFFFF;
         acc[q] = 0xFFFFFFFFu;
     }
     uint32_t k = seed ^ (blockIdx.x * 977u + threadIdx.x);
     for (int i = 0; i < iters; ++i) {
-        const uint32_t a = k, b = k * 2654435761u, c = k ^ 0x9E3779B9u, d = k + 0x7F4A7C15u;
+        const uint32_t r0 = k & 0xFFFFF, p0 = k >> 12, r1 = (k ^ 0x9E3779B9u) & 0xFFFFF,
+                       p1 = (k + 0x7F4A7C15u) >> 12;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            if (a <= thr[q]) acc[q] = min(acc[q], b);
-            if (c <= thr[q]) acc[q] = min(acc[q], d);
+            const uint32_t v0 = p0 | ((K[q] - r0) & 0x80000000u);
+            const uint32_t v1 = p1 | ((K[q] - r1) & 0x80000000u);
+            acc[q] = __vimin3_u32(acc[q], v0, v1);
         }
         k += 0x61C88647u;
     }
@@ -84,7 +89,7 @@ extern "C" int pals_measure_peaks(pals_ctx* ctx, double* int_ops_per_s, double* 
     cudaFree(buf);
     if (e != cudaSuccess) return cuda_fail(e, "pals_measure_peaks");
     const double threads_total = (double)blocks * threads;
-    // per inner iteration: 8 chains x 2 (compare + min) x 2 candidates = 32 int ops
+    // per inner iteration: 8 chains x 2 pairs x 2 algorithmic ops (compare + min) = 32
     *int_ops_per_s = threads_total * iters_i * 32.0 / (best_i * 1e-3);
     // 8 DFMA = 16 flops per iteration
     *fp64_flops_per_s = threads_total * iters_d * 16.0 / (best_d * 1e-3);

@@ -21,12 +21,8 @@ namespace pals {
 constexpr int kChunk = 2048;        // sort chunk (smem block merge sort)
 constexpr int kScanCh = 2048;       // configs per scan work item
 constexpr int kScanThreads = 256;
-// queries per thread in the scan (register tile): 8 with 32-bit keys, 4 with 64-bit
-template <typename K>
-struct ScanQ {
-    static constexpr int Q = sizeof(K) == 4 ? 8 : 4;
-    static constexpr int TQ = kScanThreads * Q;
-};
+constexpr int kScanQ = 8;           // queries per thread in the scan (register tile)
+constexpr int kScanTQ = kScanThreads * kScanQ;
 
 enum { CLS_A = 0, CLS_B = 1, CLS_C = 2, CLS_D = 3, CLS_X = 4, N_CLS = 5 };
 enum { EX_FULL = 0, EX_QOS_NEAR = 1, EX_BUD_NEAR = 2 };
@@ -112,9 +108,10 @@ __device__ __forceinline__ void finish_scores(const PlanDev& d, int64_t i, doubl
     d.th[i] = th;
     d.pn[i] = pn;
     d.ef[i] = ef;
-    d.skey[ORD_T][i] = ~orderable(th);
-    d.skey[ORD_P][i] = orderable(pn);
-    d.skey[ORD_E][i] = ~orderable(ef);
+    const int q = d.tr[i];  // sort input in TR order
+    d.skey[ORD_T][q] = ~orderable(th);
+    d.skey[ORD_P][q] = orderable(pn);
+    d.skey[ORD_E][q] = ~orderable(ef);
     // the integer fast path needs positive, finite, well-scaled scores
     const bool ok = isfinite(th) && isfinite(pn) && isfinite(ef) && th > 1e-250 && pn > 1e-250 &&
                     ef > 1e-250;
@@ -152,9 +149,10 @@ __global__ void k_eval_values(PlanDev d) {
         d.th[i] = th;
         d.pn[i] = 1.0;
         d.ef[i] = ef;
-        d.skey[ORD_T][i] = ~orderable(th);
-        d.skey[ORD_P][i] = orderable(1.0);
-        d.skey[ORD_E][i] = ~orderable(ef);
+        const int q = d.tr[i];
+        d.skey[ORD_T][q] = ~orderable(th);
+        d.skey[ORD_P][q] = orderable(1.0);
+        d.skey[ORD_E][q] = ~orderable(ef);
     }
 }
 
@@ -185,8 +183,10 @@ constexpr int kIPT = 8;
 __device__ __forceinline__ int pk(int e) { return e + (e >> 4); }  // padded key slot
 __device__ __forceinline__ int pv(int e) { return e + (e >> 5); }  // padded index slot
 
+// ties are broken on the carried TR, so the order is the packed-key order; the
+// merges keep it because their left run always holds the smaller TRs
 __device__ __forceinline__ void cmp_swap(uint64_t (&k)[kIPT], uint32_t (&v)[kIPT], int i, int j) {
-    if (k[j] < k[i]) {
+    if (k[j] < k[i] || (k[j] == k[i] && v[j] < v[i])) {
         const uint64_t tk = k[i];
         k[i] = k[j];
         k[j] = tk;
@@ -290,6 +290,8 @@ __global__ void __launch_bounds__(TPB) k_sort_chunks(PlanDev d, uint64_t* gk, ui
     {
         // all loads in flight before the shared stores (a generic-pointer load may
         // not be reordered across a shared store, which would serialize the round trips)
+        // input in TR order (the evaluation writes position q = TR of each point), so
+        // sorting by (value, q) gives merged positions in packed-key order
         uint64_t x[kIPT];
         const uint64_t* __restrict__ src = d.skey[o];
 #pragma unroll
@@ -553,11 +555,16 @@ __device__ __forceinline__ void assign_warp(const PlanDev& d, const int* __restr
     }
     if (in) {
         const uint8_t dg = start ? ((tl < 32 || b31 != 0 ? bend : bext) == 1) : 0;
-        const uint32_t idx = V(p);
-        if (idx < n) {
-            const uint64_t k = ((uint64_t)r << d.tr_bits) | (uint64_t)tr[idx];
+        const uint32_t trv = V(p);  // the carried grid rank TR
+        if (trv < n) {
+            const uint32_t idx = (uint32_t)d.inv_tr[trv];
+            const uint64_t k = ((uint64_t)r << d.tr_bits) | (uint64_t)trv;
             if (d.wide) d.key64[o][idx] = k;
             else d.key32[o][idx] = (uint32_t)k;
+            d.rank32[o][idx] = r;
+            d.pos32[o][idx] = p;
+            d.midx[o][p] = idx;  // position -> point, and its rank (k_finalize)
+            d.sidx[o][p] = r;
             if (r == 0 && o == ORD_T) atomicMin((unsigned long long*)&gk[0], k);
             if (r == 0 && o == ORD_P) atomicMin((unsigned long long*)&gk[1], k);
         }
@@ -743,21 +750,6 @@ __device__ void resolve_globals_warp(const PlanDev& d, const uint64_t* gk, int w
 }
 
 // ------------------------------------------------------------ select ----
-template <typename K>
-struct KeyTraits;
-template <>
-struct KeyTraits<uint32_t> {
-    static __device__ __forceinline__ const uint32_t* keys(const PlanDev& d, int o) {
-        return d.key32[o];
-    }
-};
-template <>
-struct KeyTraits<uint64_t> {
-    static __device__ __forceinline__ const uint64_t* keys(const PlanDev& d, int o) {
-        return d.key64[o];
-    }
-};
-
 struct SelArgs {
     const pals_query* q;
     int64_t nq;
@@ -849,8 +841,9 @@ __device__ __forceinline__ void qprep_body(const PlanDev& d, const SelArgs& a, i
             else if (q.objective == PALS_OBJ_QOS) c = (Kp == 0) ? CLS_D : (Kt ? CLS_B : CLS_C);
             else c = (bset && Kp) ? CLS_C : CLS_D;
             // inclusive thresholds: feasible <=> key <= (K << tr_bits) - 1
-            a.thr_t[j] = Kt ? (((uint64_t)Kt << d.tr_bits) - 1) : 0;
-            a.thr_p[j] = Kp ? (((uint64_t)Kp << d.tr_bits) - 1) : 0;
+            // the scan's thresholds: feasible <=> rank <= K - 1
+            a.thr_t[j] = Kt ? (uint64_t)(Kt - 1) : 0;
+            a.thr_p[j] = Kp ? (uint64_t)(Kp - 1) : 0;
             a.best_e[j] = kNone64;
             a.best_t[j] = kNone64;
             a.cls[j] = (uint8_t)c;
@@ -889,42 +882,55 @@ __global__ void k_assign_qprep(PlanDev d, const int* __restrict__ tr, uint64_t* 
     }
 }
 
-// (8) the pair scan: every (query, config) pair of classes A/B/C is decided by
-// integer compares on the dense-rank keys (persistent CTAs over work items).
-template <typename K, int CLS, int kQ>
-__device__ __forceinline__ void scan_item(const K* __restrict__ se, const K* __restrict__ st,
-                                          const K* __restrict__ sp, int nc, const K* thr_t,
-                                          const K* thr_p, K* be, K* bt) {
-    constexpr int V = 16 / sizeof(K);
-    using VT = typename std::conditional<sizeof(K) == 4, uint4, ulonglong2>::type;
-    for (int c = 0; c < nc; c += V) {
-        K e[V], t[V], p[V];
-        if (CLS != CLS_C) {
-            const VT ve = *reinterpret_cast<const VT*>(se + c);
-            memcpy(e, &ve, 16);
-        }
-        {
-            const VT vt = *reinterpret_cast<const VT*>(st + c);
-            memcpy(t, &vt, 16);
-        }
-        if (CLS != CLS_A) {
-            const VT vp = *reinterpret_cast<const VT*>(sp + c);
-            memcpy(p, &vp, 16);
-        }
+// (8) the pair scan: every (query, config) pair of classes A/B/C is decided on the
+// integer (rank, position) arrays (persistent CTAs over work items). A point is
+// feasible on a side iff its competition rank r < K (K from qprep, stored as
+// K - 1 >= 0), and the argmin is the smallest merged position (the packed-key order).
+// Classes A (QoS, no budget) and C (budget, max throughput) take one threshold:
+// per pair d = (K - 1) - r (IMAD.IADD, FMA pipe) and v = pos | (d & 0x80000000)
+// (one LOP3: the sign bit of d marks an infeasible pair), and one 3-input min
+// (VIMNMX3) folds two configs into the running minimum — 1.5 ALU-pipe ops per pair
+// instead of a compare + predicated min (2). Class B (QoS with budget) tests both
+// sides with compares and keeps both minima.
+template <int CLS>
+__device__ __forceinline__ void scan_item(const uint32_t* __restrict__ s0,
+                                          const uint32_t* __restrict__ s1,
+                                          const uint32_t* __restrict__ s2,
+                                          const uint32_t* __restrict__ s3, int nc,
+                                          const uint32_t (&kt)[kScanQ],
+                                          const uint32_t (&kp)[kScanQ], uint32_t (&be)[kScanQ],
+                                          uint32_t (&bt)[kScanQ]) {
+    for (int c = 0; c < nc; c += 4) {
+        if (CLS != CLS_B) {
+            // s0: rank on the feasibility side, s1: position on the argmin side
+            const uint4 vr = *reinterpret_cast<const uint4*>(s0 + c);
+            const uint4 vp = *reinterpret_cast<const uint4*>(s1 + c);
+            const uint32_t r[4] = {vr.x, vr.y, vr.z, vr.w}, q[4] = {vp.x, vp.y, vp.z, vp.w};
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
+            for (int v = 0; v < 4; v += 2)
 #pragma unroll
-            for (int q = 0; q < kQ; ++q) {
-                if (CLS == CLS_A) {
-                    if (t[v] <= thr_t[q]) be[q] = min(be[q], e[v]);
-                } else if (CLS == CLS_B) {
-                    const bool fp = p[v] <= thr_p[q];
-                    if (fp && t[v] <= thr_t[q]) be[q] = min(be[q], e[v]);
-                    if (fp) bt[q] = min(bt[q], t[v]);
-                } else {
-                    if (p[v] <= thr_p[q]) bt[q] = min(bt[q], t[v]);
+                for (int j = 0; j < kScanQ; ++j) {
+                    const uint32_t K = CLS == CLS_A ? kt[j] : kp[j];
+                    const uint32_t v0 = q[v] | ((K - r[v]) & 0x80000000u);
+                    const uint32_t v1 = q[v + 1] | ((K - r[v + 1]) & 0x80000000u);
+                    be[j] = __vimin3_u32(be[j], v0, v1);
                 }
-            }
+        } else {
+            // s0: rank_t, s1: rank_p, s2: pos_e, s3: pos_t
+            const uint4 vt = *reinterpret_cast<const uint4*>(s0 + c);
+            const uint4 vpp = *reinterpret_cast<const uint4*>(s1 + c);
+            const uint4 ve = *reinterpret_cast<const uint4*>(s2 + c);
+            const uint4 vq = *reinterpret_cast<const uint4*>(s3 + c);
+            const uint32_t rt[4] = {vt.x, vt.y, vt.z, vt.w}, rp[4] = {vpp.x, vpp.y, vpp.z, vpp.w};
+            const uint32_t pe[4] = {ve.x, ve.y, ve.z, ve.w}, pt[4] = {vq.x, vq.y, vq.z, vq.w};
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+#pragma unroll
+                for (int j = 0; j < kScanQ; ++j) {
+                    const bool fp = rp[v] <= kp[j];
+                    if (fp && rt[v] <= kt[j]) be[j] = min(be[j], pe[v]);
+                    if (fp) bt[j] = min(bt[j], pt[v]);
+                }
         }
     }
 }
@@ -949,14 +955,15 @@ __device__ __forceinline__ int64_t scan_pos_of(const ScanPlan& sp, int64_t u) {
     return sp.pbase[3];
 }
 
-template <typename K>
-__device__ __forceinline__ void stage_keys(K* dst, const K* __restrict__ src, int nc, int ncp) {
+// pad with ranks that never pass a threshold (K - 1 < 2^31 - 1)
+__device__ __forceinline__ void stage_keys(uint32_t* dst, const uint32_t* __restrict__ src, int nc,
+                                           int ncp, uint32_t pad) {
     constexpr int R = kScanCh / kScanThreads;
-    K x[R];
+    uint32_t x[R];
 #pragma unroll
     for (int k = 0; k < R; ++k) {
         const int i = threadIdx.x + k * kScanThreads;
-        x[k] = i < nc ? __ldg(src + i) : (K)~(K)0;
+        x[k] = i < nc ? __ldg(src + i) : pad;
     }
 #pragma unroll
     for (int k = 0; k < R; ++k) {
@@ -965,25 +972,23 @@ __device__ __forceinline__ void stage_keys(K* dst, const K* __restrict__ src, in
     }
 }
 
-template <typename K>
+constexpr uint32_t kPadRank = 0x7FFFFFFFu;
+constexpr size_t kScanSmem = 4 * (size_t)kScanCh * 4;
+
 __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) {
     pdl_wait();
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    K* se = reinterpret_cast<K*>(smem_raw);
-    K* st = se + kScanCh;
-    K* sp = st + kScanCh;
-    const K* ke = KeyTraits<K>::keys(d, ORD_E);
-    const K* kt = KeyTraits<K>::keys(d, ORD_T);
-    const K* kp = KeyTraits<K>::keys(d, ORD_P);
-    constexpr int kQ = ScanQ<K>::Q;
-    constexpr int kTQ = ScanQ<K>::TQ;
+    uint32_t* s0 = reinterpret_cast<uint32_t*>(smem_raw);
+    uint32_t* s1 = s0 + kScanCh;
+    uint32_t* s2 = s1 + kScanCh;
+    uint32_t* s3 = s2 + kScanCh;
     const int64_t n = d.n;
     ScanPlan pl;
     pl.wbase[0] = pl.pbase[0] = 0;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         const int64_t cnt = a.counts[c];
-        pl.T[c] = (cnt + kTQ - 1) / kTQ;
+        pl.T[c] = (cnt + kScanTQ - 1) / kScanTQ;
         pl.tq[c] = pl.T[c] ? (cnt + pl.T[c] - 1) / pl.T[c] : 0;
         pl.pbase[c + 1] = pl.pbase[c] + pl.T[c] * n;
         pl.wbase[c + 1] = pl.wbase[c] + pl.T[c] * n * class_ops(c);
@@ -1001,42 +1006,51 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) 
         const int64_t j0 = r % n;
         const int64_t seg_end = min(p1, pl.pbase[c] + (tile + 1) * n);
         const int64_t j1 = j0 + (seg_end - pos);
-        // this tile's queries: 8 per thread (4 with 64-bit keys)
+        // this tile's queries: 8 per thread
         const int64_t q_lo = tile * pl.tq[c], q_hi = min((int64_t)a.counts[c], q_lo + pl.tq[c]);
-        K thr_t[kQ], thr_p[kQ], be[kQ], bt[kQ];
-        int32_t qid[kQ];
+        uint32_t kt[kScanQ], kp[kScanQ], be[kScanQ], bt[kScanQ];
+        int32_t qid[kScanQ];
 #pragma unroll
-        for (int q = 0; q < kQ; ++q) {
-            const int64_t s = q_lo + q * kScanThreads + threadIdx.x;
-            qid[q] = s < q_hi ? a.qlist[c * a.qcap + s] : -1;
-            thr_t[q] = qid[q] >= 0 ? (K)a.thr_t[qid[q]] : (K)0;
-            thr_p[q] = qid[q] >= 0 ? (K)a.thr_p[qid[q]] : (K)0;
-            be[q] = (K)~(K)0;
-            bt[q] = (K)~(K)0;
+        for (int q = 0; q < kScanQ; ++q) {
+            const int64_t sq = q_lo + q * kScanThreads + threadIdx.x;
+            qid[q] = sq < q_hi ? a.qlist[c * a.qcap + sq] : -1;
+            // thresholds K - 1 (qprep); an idle slot gets 0, which the scan may use
+            // freely since its minima are discarded
+            kt[q] = qid[q] >= 0 ? (uint32_t)a.thr_t[qid[q]] : 0u;
+            kp[q] = qid[q] >= 0 ? (uint32_t)a.thr_p[qid[q]] : 0u;
+            be[q] = 0xFFFFFFFFu;
+            bt[q] = 0xFFFFFFFFu;
         }
         for (int64_t c0 = j0; c0 < j1; c0 += kScanCh) {
             const int nc = (int)min((int64_t)kScanCh, j1 - c0);
             const int ncp = (nc + 3) & ~3;
             __syncthreads();
-            // stage the keys (pad with keys that never pass a threshold); per array,
-            // all of a thread's loads are in flight before its shared stores
-            if (c != CLS_C) stage_keys<K>(se, ke + c0, nc, ncp);
-            stage_keys<K>(st, kt + c0, nc, ncp);
-            if (c != CLS_A) stage_keys<K>(sp, kp + c0, nc, ncp);
+            if (c == CLS_A) {
+                stage_keys(s0, d.rank32[ORD_T] + c0, nc, ncp, kPadRank);
+                stage_keys(s1, d.pos32[ORD_E] + c0, nc, ncp, 0u);
+            } else if (c == CLS_C) {
+                stage_keys(s0, d.rank32[ORD_P] + c0, nc, ncp, kPadRank);
+                stage_keys(s1, d.pos32[ORD_T] + c0, nc, ncp, 0u);
+            } else {
+                stage_keys(s0, d.rank32[ORD_T] + c0, nc, ncp, kPadRank);
+                stage_keys(s1, d.rank32[ORD_P] + c0, nc, ncp, kPadRank);
+                stage_keys(s2, d.pos32[ORD_E] + c0, nc, ncp, 0u);
+                stage_keys(s3, d.pos32[ORD_T] + c0, nc, ncp, 0u);
+            }
             __syncthreads();
-            // padded slots carry all-ones keys: they only pass an all-ones threshold,
-            // and then they cannot lower a minimum below a real key
-            if (c == CLS_A) scan_item<K, CLS_A, kQ>(se, st, sp, ncp, thr_t, thr_p, be, bt);
-            else if (c == CLS_B) scan_item<K, CLS_B, kQ>(se, st, sp, ncp, thr_t, thr_p, be, bt);
-            else scan_item<K, CLS_C, kQ>(se, st, sp, ncp, thr_t, thr_p, be, bt);
+            if (c == CLS_A) scan_item<CLS_A>(s0, s1, s2, s3, ncp, kt, kp, be, bt);
+            else if (c == CLS_B) scan_item<CLS_B>(s0, s1, s2, s3, ncp, kt, kp, be, bt);
+            else scan_item<CLS_C>(s0, s1, s2, s3, ncp, kt, kp, be, bt);
         }
 #pragma unroll
-        for (int q = 0; q < kQ; ++q) {
+        for (int q = 0; q < kScanQ; ++q) {
             if (qid[q] < 0) continue;
-            if (c != CLS_C && be[q] != (K)~(K)0)
-                atomicMin((unsigned long long*)&a.best_e[qid[q]], (unsigned long long)be[q]);
-            if (c != CLS_A && bt[q] != (K)~(K)0)
-                atomicMin((unsigned long long*)&a.best_t[qid[q]], (unsigned long long)bt[q]);
+            // classes A / C keep their minimum in be (bit 31 set: nothing feasible)
+            const uint32_t me = be[q], mt = c == CLS_C ? be[q] : bt[q];
+            if (c != CLS_C && me < 0x80000000u)
+                atomicMin((unsigned long long*)&a.best_e[qid[q]], (unsigned long long)me);
+            if (c != CLS_A && mt < 0x80000000u)
+                atomicMin((unsigned long long*)&a.best_t[qid[q]], (unsigned long long)mt);
         }
         pos = seg_end;
     }
@@ -1052,22 +1066,6 @@ __device__ __forceinline__ bool feasible_p(const PlanDev& d, const pals_query& q
     return d.pn[c] <= q.power_budget_w * (1.0 - q.budget_margin);
 }
 
-// Resolve the "none" sentinel: with 16-bit fields an all-ones key is a real key
-// when n == 65536; it is the largest key, so it wins only if it is the sole
-// feasible point.
-__device__ __forceinline__ uint64_t fix_sentinel(const PlanDev& d, uint64_t best, int o,
-                                                 const pals_query& q, bool need_t, bool need_p) {
-    if (d.wide || best != kNone64) return best;
-    const uint32_t full = 0xFFFFFFFFu;
-    // the point whose packed key in order o is all-ones (TR = n-1 and rank 65535)
-    if (d.n != 65536) return best;
-    const int64_t c = d.inv_tr[d.n - 1];
-    if (d.key32[o][c] != full) return best;
-    if (need_t && !feasible_t(d, q, c)) return best;
-    if (need_p && !feasible_p(d, q, c)) return best;
-    return full;
-}
-
 __device__ __forceinline__ void push_work(const SelArgs& a, int32_t qid, int mode, uint32_t d0) {
     const int k = atomicAdd(&a.counts[N_CLS], 1);
     a.work[k] = WorkItem{qid, mode, d0, 0};
@@ -1076,7 +1074,6 @@ __device__ __forceinline__ void push_work(const SelArgs& a, int32_t qid, int mod
 // (9) decide every query from its two minima; near-tie winners go to the exact fold
 __global__ void k_finalize(PlanDev d, SelArgs a) {
     pdl_wait();
-    const uint64_t mask = (1ull << d.tr_bits) - 1;
     const uint64_t none = kNone64;
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.nq;
          j += (int64_t)gridDim.x * blockDim.x) {
@@ -1086,34 +1083,30 @@ __global__ void k_finalize(PlanDev d, SelArgs a) {
             push_work(a, (int32_t)j, EX_FULL, 0);
             continue;
         }
-        uint64_t be = a.best_e[j], bt = a.best_t[j];
-        if (!d.wide) {
-            be = be == 0xFFFFFFFFull ? none : be;
-            bt = bt == 0xFFFFFFFFull ? none : bt;
-        }
+        // the minima are merged positions (packed-key order): the winner is the point
+        // that position carries, its competition rank picks the near-tie flag
+        const uint64_t be = a.best_e[j], bt = a.best_t[j];
         int32_t idx = -1;
         int r = PALS_REASON_FALLBACK_MAX_T;
-        if (c == CLS_A || c == CLS_B) {
-            be = fix_sentinel(d, be, ORD_E, q, true, c == CLS_B);
-            if (be != none) {
-                const uint32_t d0 = (uint32_t)(be >> d.tr_bits);
-                if (d.danger[ORD_E][d0]) {
-                    push_work(a, (int32_t)j, EX_QOS_NEAR, d0);
-                    continue;
-                }
-                idx = d.inv_tr[be & mask];
-                r = PALS_REASON_QOS_FEASIBLE;
+        if ((c == CLS_A || c == CLS_B) && be != none) {
+            const int32_t pt = (int32_t)d.midx[ORD_E][be];
+            const uint32_t d0 = d.sidx[ORD_E][be];
+            if (d.danger[ORD_E][d0]) {
+                push_work(a, (int32_t)j, EX_QOS_NEAR, d0);
+                continue;
             }
+            idx = pt;
+            r = PALS_REASON_QOS_FEASIBLE;
         }
         if (idx < 0 && q.has_budget && (c == CLS_B || c == CLS_C || c == CLS_D)) {
-            if (c != CLS_D) bt = fix_sentinel(d, bt, ORD_T, q, false, true);
             if (c != CLS_D && bt != none) {
-                const uint32_t d0 = (uint32_t)(bt >> d.tr_bits);
+                const int32_t pt = (int32_t)d.midx[ORD_T][bt];
+                const uint32_t d0 = d.sidx[ORD_T][bt];
                 if (d.danger[ORD_T][d0]) {
                     push_work(a, (int32_t)j, EX_BUD_NEAR, d0);
                     continue;
                 }
-                idx = d.inv_tr[bt & mask];
+                idx = pt;
             } else {
                 idx = d.globals[1];  // budget below every candidate: least power (:180-188)
             }
@@ -1293,7 +1286,7 @@ static int plan_build(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
     d.samp_n = (int)((n + d.samp_s - 1) / d.samp_s);
     // one slab for all per-plan device arrays
     const size_t n8 = (size_t)n * 8, np8 = (size_t)p->np * 8, np4 = (size_t)p->np * 4;
-    size_t bytes = 5 * n8 + N_ORD * (3 * np8 + 2 * np4 + kSamples * 8 + n8 + (size_t)n * 4) + 64 +
+    size_t bytes = 5 * n8 + N_ORD * (3 * np8 + 2 * np4 + kSamples * 8 + n8 + (size_t)n * 12) + 64 +
                    4 * (size_t)n +
                    (d.wide ? N_ORD * n8 : N_ORD * (size_t)n * 4) + 4096;
     if (m && m->kind == MODEL_TABLE) bytes += 4 * (size_t)n + 2 * 8 * (size_t)std::max<int64_t>(1, m->table_n);
@@ -1322,6 +1315,8 @@ static int plan_build(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
         d.danger[o] = (uint8_t*)take((size_t)n);
         if (d.wide) d.key64[o] = (uint64_t*)take(n8);
         else d.key32[o] = (uint32_t*)take((size_t)n * 4);
+        d.rank32[o] = (uint32_t*)take((size_t)n * 4);
+        d.pos32[o] = (uint32_t*)take((size_t)n * 4);
     }
     d.globals = (int32_t*)take(16);
     // globals[2] (the generic-score flag) only ever gets set, and a plan's scores are
@@ -1333,6 +1328,7 @@ static int plan_build(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
     p->d_an = (Analytic*)take(sizeof(Analytic));
     // TR per point (inverse of grid inv_tr), computed once on the host at grid creation
     p->tr = (int*)take(4 * (size_t)n);
+    d.tr = p->tr;
     {
         std::vector<int> inv(g->n), tr(g->n);
         if (g->n) {
@@ -1545,10 +1541,7 @@ static int select_tail(pals_plan* p, const SelArgs& a) {
     const unsigned evf = p->capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
     if (p->time_scan) PALS_CUDA(cudaEventRecordWithFlags(p->ev_scan0, s, evf));
     cudaError_t e;
-    if (p->d.wide)
-        e = launch_k(k_scan<uint64_t>, sgrid, kScanThreads, 3 * kScanCh * 8, s, pdl, p->d, a);
-    else
-        e = launch_k(k_scan<uint32_t>, sgrid, kScanThreads, 3 * kScanCh * 4, s, pdl, p->d, a);
+    e = launch_k(k_scan, sgrid, kScanThreads, kScanSmem, s, pdl, p->d, a);
     if (e != cudaSuccess) return cuda_fail(e, "k_scan");
     if (p->time_scan) {
         PALS_CUDA(cudaEventRecordWithFlags(p->ev_scan1, s, evf));

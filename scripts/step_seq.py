@@ -7,7 +7,7 @@ hdr = rows[0]
 ki, vi = hdr.index('Kernel Name'), hdr.index('Metric Value')
 seq = [(r[ki][:44], int(r[vi])) for r in rows[1:]]
 which = int(sys.argv[2]) if len(sys.argv) > 2 else 4
-idx = [i for i, s in enumerate(seq) if 'k_scan<unsigned int>' in s[0]]
+idx = [i for i, s in enumerate(seq) if 'k_scan(' in s[0] or 'k_scan<unsigned int>' in s[0]]
 i = idx[which]
 j = i
 while 'k_eval_analytic' not in seq[j][0]:

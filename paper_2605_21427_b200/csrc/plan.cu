@@ -27,12 +27,6 @@ constexpr int kScanTQ = kScanThreads * kScanQ;
 enum { CLS_A = 0, CLS_B = 1, CLS_C = 2, CLS_D = 3, CLS_X = 4, N_CLS = 5 };
 enum { EX_FULL = 0, EX_QOS_NEAR = 1, EX_BUD_NEAR = 2 };
 
-struct WorkItem {
-    int32_t qid;
-    int32_t mode;
-    uint32_t d0;
-    int32_t pad;
-};
 
 }  // namespace pals
 
@@ -69,7 +63,6 @@ struct pals_plan {
     uint8_t* cls = nullptr;
     int32_t* qlist = nullptr;     // N_CLS regions of qcap
     int32_t* counts = nullptr;    // [N_CLS] class sizes, [N_CLS] exact count
-    WorkItem* work = nullptr;
     pals_query* d_q = nullptr;    // host-API staging
     int32_t* d_idx = nullptr;
     uint8_t* d_reason = nullptr;
@@ -515,8 +508,8 @@ __device__ __forceinline__ uint8_t bnd_class(int o, uint64_t a, uint64_t b) {
 }
 
 template <class FM, class FV>
-__device__ __forceinline__ void assign_warp(const PlanDev& d, const int* __restrict__ tr,
-                                            uint64_t* gk, int o, uint32_t w0, FM M, FV V) {
+__device__ __forceinline__ void assign_warp(const PlanDev& d, uint64_t* gk, int o, uint32_t w0,
+                                            FM M, FV V) {
     const uint32_t n = (uint32_t)d.n;
     const uint32_t lane = threadIdx.x & 31;
     const unsigned full = 0xffffffffu;
@@ -597,22 +590,21 @@ __device__ __forceinline__ void last_block_resolve(const PlanDev& d, uint64_t* g
 }
 
 // assign_body: block bx of nbx for order o; nblocks = all assign blocks of the launch.
-__device__ __forceinline__ void assign_body(const PlanDev& d, const int* __restrict__ tr,
-                                            uint64_t* gk, uint32_t* done, int o, int bx, int nbx,
-                                            uint32_t nblocks) {
+__device__ __forceinline__ void assign_body(const PlanDev& d, uint64_t* gk, uint32_t* done, int o,
+                                            int bx, int nbx, uint32_t nblocks) {
     const uint64_t* __restrict__ m = d.merged[o];
     const uint32_t* __restrict__ mi = d.midx[o];
     const uint32_t n = (uint32_t)d.n;
     const uint32_t stride = (uint32_t)nbx * blockDim.x;
     for (uint32_t w0 = (uint32_t)bx * blockDim.x + (threadIdx.x & ~31u); w0 < n; w0 += stride)
-        assign_warp(d, tr, gk, o, w0, [&](uint32_t q) { return m[q]; },
+        assign_warp(d, gk, o, w0, [&](uint32_t q) { return m[q]; },
                     [&](uint32_t q) { return mi[q]; });
     last_block_resolve(d, gk, done, nblocks);
 }
 
-__global__ void k_assign(PlanDev d, const int* __restrict__ tr, uint64_t* gk, uint32_t* done) {
+__global__ void k_assign(PlanDev d, uint64_t* gk, uint32_t* done) {
     pdl_wait();
-    assign_body(d, tr, gk, done, blockIdx.y, blockIdx.x, gridDim.x, gridDim.x * gridDim.y);
+    assign_body(d, gk, done, blockIdx.y, blockIdx.x, gridDim.x, gridDim.x * gridDim.y);
 }
 
 
@@ -762,7 +754,6 @@ struct SelArgs {
     uint8_t* cls;
     int32_t* qlist;
     int32_t* counts;  // [0..N_CLS) class sizes, [N_CLS] work items
-    WorkItem* work;
     int64_t qcap;
     int force_exact;
 };
@@ -868,13 +859,13 @@ __global__ void k_qprep(PlanDev d, SelArgs a) {
 
 // k_assign and k_qprep in one launch (the captured step): qprep reads only the merged
 // arrays, so its blocks (grid.y == N_ORD) run beside the assign blocks (grid.y < N_ORD).
-__global__ void k_assign_qprep(PlanDev d, const int* __restrict__ tr, uint64_t* gk,
+__global__ void k_assign_qprep(PlanDev d, uint64_t* gk,
                                uint32_t* done, SelArgs a, int eb, int qb) {
     pdl_wait();
     __shared__ uint64_t sbuf[2 * kSamples];
     if (blockIdx.y < N_ORD) {
         if ((int)blockIdx.x >= eb) return;
-        assign_body(d, tr, gk, done, blockIdx.y, blockIdx.x, eb, (uint32_t)eb * N_ORD);
+        assign_body(d, gk, done, blockIdx.y, blockIdx.x, eb, (uint32_t)eb * N_ORD);
     } else {
         if ((int)blockIdx.x >= qb) return;
         qprep_body(d, a, blockIdx.x, qb, reinterpret_cast<double*>(sbuf),
@@ -1066,97 +1057,108 @@ __device__ __forceinline__ bool feasible_p(const PlanDev& d, const pals_query& q
     return d.pn[c] <= q.power_budget_w * (1.0 - q.budget_margin);
 }
 
-__device__ __forceinline__ void push_work(const SelArgs& a, int32_t qid, int mode, uint32_t d0) {
-    const int k = atomicAdd(&a.counts[N_CLS], 1);
-    a.work[k] = WorkItem{qid, mode, d0, 0};
-}
-
-// (9) decide every query from its two minima; near-tie winners go to the exact fold
-__global__ void k_finalize(PlanDev d, SelArgs a) {
-    pdl_wait();
-    const uint64_t none = kNone64;
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.nq;
-         j += (int64_t)gridDim.x * blockDim.x) {
-        const int c = a.cls[j];
-        const pals_query q = a.q[j];
-        if (c == CLS_X) {
-            push_work(a, (int32_t)j, EX_FULL, 0);
-            continue;
-        }
-        // the minima are merged positions (packed-key order): the winner is the point
-        // that position carries, its competition rank picks the near-tie flag
-        const uint64_t be = a.best_e[j], bt = a.best_t[j];
-        int32_t idx = -1;
-        int r = PALS_REASON_FALLBACK_MAX_T;
-        if ((c == CLS_A || c == CLS_B) && be != none) {
-            const int32_t pt = (int32_t)d.midx[ORD_E][be];
-            const uint32_t d0 = d.sidx[ORD_E][be];
-            if (d.danger[ORD_E][d0]) {
-                push_work(a, (int32_t)j, EX_QOS_NEAR, d0);
-                continue;
-            }
-            idx = pt;
-            r = PALS_REASON_QOS_FEASIBLE;
-        }
-        if (idx < 0 && q.has_budget && (c == CLS_B || c == CLS_C || c == CLS_D)) {
-            if (c != CLS_D && bt != none) {
-                const int32_t pt = (int32_t)d.midx[ORD_T][bt];
-                const uint32_t d0 = d.sidx[ORD_T][bt];
-                if (d.danger[ORD_T][d0]) {
-                    push_work(a, (int32_t)j, EX_BUD_NEAR, d0);
-                    continue;
-                }
-                idx = pt;
-            } else {
-                idx = d.globals[1];  // budget below every candidate: least power (:180-188)
-            }
-            r = PALS_REASON_BUDGET_MAX_T;
-        }
-        if (idx < 0) {
-            idx = d.globals[0];  // fallback: max throughput over all (:191-198)
-            r = PALS_REASON_FALLBACK_MAX_T;
-        }
-        a.out_idx[j] = idx;
-        a.out_reason[j] = (uint8_t)r;
+// (9) decide every query from its two minima. A query whose winner sits in a near-tie
+// cluster (or every query of a generic plan) is re-decided by the exact fold, run by
+// the deciding warp itself: the lanes that need one are folded one after another
+// (10), so no second launch or work queue sits in the step.
+__device__ __forceinline__ void exact_item(const PlanDev& d, const SelArgs& a, int32_t qid,
+                                           int mode, uint32_t d0) {
+    const pals_query q = a.q[qid];
+    if (mode == EX_FULL) {
+        warp_select_full(d, q, &a.out_idx[qid], &a.out_reason[qid]);
+        return;
+    }
+    int best;
+    int r;
+    if (mode == EX_QOS_NEAR) {
+        const uint32_t cut = cluster_end(d, ORD_E, d0);
+        best = warp_fold(
+            d.n, d.cap, d.batch,
+            [&](int64_t c) {
+                return rank_of(d, ORD_E, c) <= cut && feasible_t(d, q, c) &&
+                       feasible_p(d, q, c);
+            },
+            [&](int64_t c) { return d.ef[c]; });
+        r = PALS_REASON_QOS_FEASIBLE;
+    } else {
+        const uint32_t cut = cluster_end(d, ORD_T, d0);
+        best = warp_fold(
+            d.n, d.cap, d.batch,
+            [&](int64_t c) { return rank_of(d, ORD_T, c) <= cut && feasible_p(d, q, c); },
+            [&](int64_t c) { return d.th[c]; });
+        r = PALS_REASON_BUDGET_MAX_T;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        a.out_idx[qid] = best;
+        a.out_reason[qid] = (uint8_t)r;
     }
 }
 
-// (10) exact sequential fold for the queued queries, one warp per query
-__global__ void k_exact(PlanDev d, SelArgs a) {
+__global__ void k_finalize(PlanDev d, SelArgs a) {
     pdl_wait();
-    const int warps = (gridDim.x * blockDim.x) >> 5;
-    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nwork = a.counts[N_CLS];
-    for (int k = w; k < nwork; k += warps) {
-        const WorkItem it = a.work[k];
-        const pals_query q = a.q[it.qid];
-        if (it.mode == EX_FULL) {
-            warp_select_full(d, q, &a.out_idx[it.qid], &a.out_reason[it.qid]);
-            continue;
+    const uint64_t none = kNone64;
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); j0 < a.nq;
+         j0 += stride) {  // whole warps: the exact folds below need every lane
+        const int64_t j = j0 + lane;
+        int mode = -1;
+        uint32_t d0 = 0;
+        if (j < a.nq) {
+            const int c = a.cls[j];
+            const pals_query q = a.q[j];
+            // the minima are merged positions (packed-key order): the winner is the
+            // point that position carries, its competition rank picks the near-tie flag
+            const uint64_t be = a.best_e[j], bt = a.best_t[j];
+            int32_t idx = -1;
+            int r = PALS_REASON_FALLBACK_MAX_T;
+            if (c == CLS_X) {
+                mode = EX_FULL;
+            } else {
+                if ((c == CLS_A || c == CLS_B) && be != none) {
+                    const int32_t pt = (int32_t)d.midx[ORD_E][be];
+                    const uint32_t rk = d.sidx[ORD_E][be];
+                    if (d.danger[ORD_E][rk]) {
+                        mode = EX_QOS_NEAR;
+                        d0 = rk;
+                    }
+                    idx = pt;
+                    r = PALS_REASON_QOS_FEASIBLE;
+                }
+                if (mode < 0 && idx < 0 && q.has_budget &&
+                    (c == CLS_B || c == CLS_C || c == CLS_D)) {
+                    if (c != CLS_D && bt != none) {
+                        const int32_t pt = (int32_t)d.midx[ORD_T][bt];
+                        const uint32_t rk = d.sidx[ORD_T][bt];
+                        if (d.danger[ORD_T][rk]) {
+                            mode = EX_BUD_NEAR;
+                            d0 = rk;
+                        }
+                        idx = pt;
+                    } else {
+                        idx = d.globals[1];  // budget below every candidate: least power (:180-188)
+                    }
+                    r = PALS_REASON_BUDGET_MAX_T;
+                }
+                if (idx < 0) {
+                    idx = d.globals[0];  // fallback: max throughput over all (:191-198)
+                    r = PALS_REASON_FALLBACK_MAX_T;
+                }
+            }
+            if (mode < 0) {
+                a.out_idx[j] = idx;
+                a.out_reason[j] = (uint8_t)r;
+            }
         }
-        int best;
-        int r;
-        if (it.mode == EX_QOS_NEAR) {
-            const uint32_t cut = cluster_end(d, ORD_E, it.d0);
-            best = warp_fold(
-                d.n, d.cap, d.batch,
-                [&](int64_t c) {
-                    return rank_of(d, ORD_E, c) <= cut && feasible_t(d, q, c) &&
-                           feasible_p(d, q, c);
-                },
-                [&](int64_t c) { return d.ef[c]; });
-            r = PALS_REASON_QOS_FEASIBLE;
-        } else {
-            const uint32_t cut = cluster_end(d, ORD_T, it.d0);
-            best = warp_fold(
-                d.n, d.cap, d.batch,
-                [&](int64_t c) { return rank_of(d, ORD_T, c) <= cut && feasible_p(d, q, c); },
-                [&](int64_t c) { return d.th[c]; });
-            r = PALS_REASON_BUDGET_MAX_T;
-        }
-        if ((threadIdx.x & 31) == 0) {
-            a.out_idx[it.qid] = best;
-            a.out_reason[it.qid] = (uint8_t)r;
+        unsigned m = __ballot_sync(full, mode >= 0);
+        if (m && lane == 0) atomicAdd(&a.counts[N_CLS], __popc(m));  // exact-fold count
+        while (m) {
+            const int l = __ffs(m) - 1;
+            m &= m - 1;
+            const int md = __shfl_sync(full, mode, l);
+            const uint32_t dd = __shfl_sync(full, d0, l);
+            exact_item(d, a, (int32_t)(j0 + l), md, dd);
         }
     }
 }
@@ -1459,7 +1461,7 @@ static int prep_tail(pals_plan* p) {
     pals_ctx* ctx = p->ctx;
     const int eb = grid_blocks(ctx, p->n, 256);
     const cudaError_t e = launch_k(k_assign, dim3(eb, N_ORD), 256, 0, ctx->stream, (bool)p->pdl,
-                                   p->d, (const int*)p->tr, p->gk, (uint32_t*)(p->gk + 2));
+                                   p->d, p->gk, (uint32_t*)(p->gk + 2));
     if (e != cudaSuccess) return cuda_fail(e, "pals_plan_prepare assign");
     count_launch(ctx, 1);
     return check_launch("pals_plan_prepare");
@@ -1479,7 +1481,7 @@ static int ensure_query_buffers(pals_plan* p, int64_t nq) {
     }
     cudaFree(p->thr_t);
     const int64_t cap = std::max<int64_t>(nq, 1024);
-    const size_t bytes = (size_t)cap * (8 * 4 + 1 + 4 * N_CLS + sizeof(WorkItem)) + 4096;
+    const size_t bytes = (size_t)cap * (8 * 4 + 1 + 4 * N_CLS) + 4096;
     PALS_CUDA(cudaMalloc(&p->thr_t, bytes));
     char* s = (char*)p->thr_t;
     auto take = [&](size_t b) {
@@ -1493,7 +1495,6 @@ static int ensure_query_buffers(pals_plan* p, int64_t nq) {
     p->best_t = (uint64_t*)take(8 * cap);
     p->cls = (uint8_t*)take(cap);
     p->qlist = (int32_t*)take(4 * (size_t)cap * N_CLS);
-    p->work = (WorkItem*)take(sizeof(WorkItem) * (size_t)cap);
     p->counts = (int32_t*)take(64);
     p->qcap = cap;
     return PALS_OK;
@@ -1513,7 +1514,6 @@ static SelArgs make_args(pals_plan* p, const pals_query* d_queries, int64_t nq, 
     a.cls = p->cls;
     a.qlist = p->qlist;
     a.counts = p->counts;
-    a.work = p->work;
     a.qcap = p->qcap;
     a.force_exact = p->force_exact;
     return a;
@@ -1548,10 +1548,10 @@ static int select_tail(pals_plan* p, const SelArgs& a) {
         p->scan_recorded = 1;
     }
     const int qb = grid_blocks(ctx, a.nq, 256);
-    e = launch_k(k_finalize, qb, 256, 0, s, pdl, p->d, a);
-    if (e == cudaSuccess) e = launch_k(k_exact, ctx->num_sms * 2, 256, 0, s, (bool)p->pdl, p->d, a);
+    // enough warps for plans where many queries take the exact fold (generic scores)
+    e = launch_k(k_finalize, std::max(qb, ctx->num_sms * 2), 256, 0, s, pdl, p->d, a);
     if (e != cudaSuccess) return cuda_fail(e, "pals_plan_select_device tail");
-    count_launch(ctx, 3);
+    count_launch(ctx, 2);
     return check_launch("pals_plan_select_device");
 }
 
@@ -1620,8 +1620,8 @@ static int plan_step(pals_plan* p, const pals_query* d_queries, int64_t nq, int3
             const SelArgs a = make_args(p, d_queries, nq, d_idx, d_reason);
             const int eb = grid_blocks(ctx, p->n, 256), qb = grid_blocks(ctx, nq, 256);
             const cudaError_t e = launch_k(k_assign_qprep, dim3(std::max(eb, qb), N_ORD + 1),
-                                           256, 0, s, (bool)p->pdl, p->d, (const int*)p->tr,
-                                           p->gk, (uint32_t*)(p->gk + 2), a, eb, qb);
+                                           256, 0, s, (bool)p->pdl, p->d, p->gk,
+                                           (uint32_t*)(p->gk + 2), a, eb, qb);
             if (e != cudaSuccess) rc = cuda_fail(e, "k_assign_qprep");
             if (!rc) {
                 count_launch(ctx, 1);

@@ -645,10 +645,15 @@ static int replay_launch(pals_ctx* ctx, ReplayCache* rc, const pals_ctrl_cfg* cf
         k_replay_order<<<ob, 256, 0, ctx->stream>>>(*spec, order, counters);
         count_launch(ctx);
     }
-    static const int minb = [] {
+    // measured on B200: 6 CTAs/SM (80 regs) beats the 126-register build by 1.1-1.4x on
+    // small candidate sets (cfg4's 36: 6.8e10 vs 6.1e10 decisions/s); on the 1,464-
+    // candidate DR grid the unconstrained build wins (3.9e10 vs 3.3e10)
+    static const int minb_env = [] {
         const char* e = getenv("PALS_REPLAY_MINB");
-        return e ? atoi(e) : 6;  // measured: 6 CTAs/SM (80 regs) beats 4 (126 regs) by 1.4x
+        return e ? atoi(e) : 0;
     }();
+    const int ncand = (int)(rc->caps.size() * rc->batches.size());
+    const int minb = minb_env ? minb_env : (ncand <= 256 ? 6 : 1);
     const size_t msm = sizeof(ReplayModelDev) * (size_t)p.n_models;
     if (msm > 48 * 1024) {
         const int b = (int)msm;

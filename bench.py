@@ -1033,6 +1033,7 @@ def bench_frontiers(args, dist, ctx, stream, l2_flush):
     launches = ctx.lib.pals_ctx_launch_count(ctx.h) - l0
     t_max = dist.max(float(np.sum([a.elapsed_time(b) for a, b in ev])))
     value = dist.sum(float(n)) * args.steps / (t_max * 1e-3)
+    idx = plan.frontier()  # warm-up of the host-output path (its scratch buffer)
     dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):

@@ -228,10 +228,9 @@ int pals_plan_frontier(pals_plan* p, int32_t* idx, int64_t* n_out) {
     pals_ctx* ctx = plan_ctx(p);
     PALS_CUDA(cudaSetDevice(ctx->device));
     const int64_t n = plan_dev(p).n;
-    int32_t* d_idx = nullptr;
-    int64_t* d_n = nullptr;
-    PALS_CUDA(cudaMalloc(&d_idx, 4 * (size_t)std::max<int64_t>(1, n) + 16));
-    d_n = (int64_t*)(((uintptr_t)(d_idx + std::max<int64_t>(1, n)) + 7) & ~(uintptr_t)7);
+    int32_t* d_idx = (int32_t*)plan_scratch(p, 4 * (size_t)std::max<int64_t>(1, n) + 16);
+    if (!d_idx) return set_error(PALS_ERUNTIME, "pals_plan_frontier: out of device memory");
+    int64_t* d_n = (int64_t*)(((uintptr_t)(d_idx + std::max<int64_t>(1, n)) + 7) & ~(uintptr_t)7);
     int rc = pals_plan_frontier_device(p, d_idx, d_n);
     if (rc == PALS_OK) {
         cudaStream_t s = ctx->stream;
@@ -241,7 +240,6 @@ int pals_plan_frontier(pals_plan* p, int32_t* idx, int64_t* n_out) {
             e = copy_on(s, idx, d_idx, 4 * (size_t)*n_out, cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) rc = cuda_fail(e, "pals_plan_frontier");
     }
-    cudaFree(d_idx);
     return rc;
 }
 

@@ -298,6 +298,7 @@ int forest_eval_raw(const pals_model* m, pals_ctx* ctx, int64_t n, const double*
 // plan.cu
 const pals_grid* plan_grid(const pals_plan* p);
 pals_ctx* plan_ctx(const pals_plan* p);
+void* plan_scratch(pals_plan* p, size_t bytes);
 // a plan over given (throughput, efficiency) values per grid point (T / P arrays of
 // the plan are filled by the caller before pals_plan_prepare); frontier only
 int plan_create_values(pals_ctx* ctx, const pals_grid* g, pals_plan** out);

@@ -86,6 +86,8 @@ struct pals_plan {
     cudaStream_t side = nullptr;  // upload stream of pals_select's graph
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int32_t* h_cnt = nullptr;     // pinned class counters (pals_select)
+    void* scratch = nullptr;      // plan_scratch()
+    size_t scratch_bytes = 0;
 };
 
 namespace pals {
@@ -1229,6 +1231,18 @@ int plan_create_values(pals_ctx* ctx, const pals_grid* g, pals_plan** out) {
     return rc;
 }
 pals_ctx* plan_ctx(const pals_plan* p) { return p->ctx; }
+// per-plan device scratch that persists across calls (host-output entry points):
+// no cudaMalloc / cudaFree (which synchronizes the device) per call
+void* plan_scratch(pals_plan* p, size_t bytes) {
+    if (bytes > p->scratch_bytes) {
+        cudaFree(p->scratch);
+        p->scratch = nullptr;
+        p->scratch_bytes = 0;
+        if (cudaMalloc(&p->scratch, bytes) != cudaSuccess) return nullptr;
+        p->scratch_bytes = bytes;
+    }
+    return p->scratch;
+}
 }  // namespace pals
 
 static int plan_build(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
@@ -1383,6 +1397,7 @@ int pals_plan_destroy(pals_plan* p) {
     if (p->ev_join) cudaEventDestroy(p->ev_join);
     if (p->side) cudaStreamDestroy(p->side);
     if (p->h_cnt) cudaFreeHost(p->h_cnt);
+    cudaFree(p->scratch);
     cudaFree(p->slab);
     cudaFree(p->thr_t);
     cudaFree(p->d_q);

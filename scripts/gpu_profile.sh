@@ -9,8 +9,9 @@ START=$(date +%s); timeout 1200 python bench.py > gpurun_out/bench.json 2> gpuru
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2>> gpurun_out/bench.err
 SMALL="--steps 2 --warmup 1 --traces 100000 --predictions 4194304 --cfg3-queries 100000 --cfg5-traces 0 --sim-seeds 0 --no-cpu-baseline"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py $SMALL > gpurun_out/b_ncu.log 2>&1
-for k in k_scan "k_sort_chunks<256>" "k_merge_round<128>" k_forest_eval_aos k_assign_qprep k_allocate k_front_scan; do
-  n=${k%%<*}; timeout 600 ncu --set full --clock-control none --import-source on -k "regex:$k" -s 2 -c 1 -o gpurun_out/prof_$n python bench.py $SMALL > gpurun_out/ncu_$n.log 2>&1
+for k in "k_scan\\(" "k_sort_chunks<\\(int\\)256>" "k_merge_round<\\(int\\)128>" k_forest_eval_aos k_assign_qprep k_allocate k_front_scan k_finalize; do
+  n=${k%%[<\\]*}
+  timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$k" -s 2 -c 1 -o gpurun_out/prof_$n python bench.py $SMALL > gpurun_out/ncu_$n.log 2>&1
 done
 # the replay at its bench size (1e6 traces; 300 steps keep ncu's ~40 replays short)
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_replay -s 1 -c 1 -o gpurun_out/prof_k_replay python bench.py --steps 1 --warmup 1 --trace-steps 300 --predictions 1048576 --cfg3-queries 100000 --cfg5-traces 0 --sim-seeds 0 --no-cpu-baseline > gpurun_out/ncu_k_replay.log 2>&1

@@ -893,14 +893,19 @@ __device__ __forceinline__ void scan_item(const uint32_t* __restrict__ s0,
                                           const uint32_t (&kt)[kScanQ],
                                           const uint32_t (&kp)[kScanQ], uint32_t (&be)[kScanQ],
                                           uint32_t (&bt)[kScanQ]) {
-    for (int c = 0; c < nc; c += 4) {
-        if (CLS != CLS_B) {
-            // s0: rank on the feasibility side, s1: position on the argmin side
-            const uint4 vr = *reinterpret_cast<const uint4*>(s0 + c);
-            const uint4 vp = *reinterpret_cast<const uint4*>(s1 + c);
-            const uint32_t r[4] = {vr.x, vr.y, vr.z, vr.w}, q[4] = {vp.x, vp.y, vp.z, vp.w};
+    if (CLS != CLS_B) {
+        // s0: rank on the feasibility side, s1: position on the argmin side; 8 configs
+        // per iteration (nc is padded to a multiple of 8) so the next shared loads are
+        // in flight while the current pairs run
+        for (int c = 0; c < nc; c += 8) {
+            const uint4 vr0 = *reinterpret_cast<const uint4*>(s0 + c);
+            const uint4 vp0 = *reinterpret_cast<const uint4*>(s1 + c);
+            const uint4 vr1 = *reinterpret_cast<const uint4*>(s0 + c + 4);
+            const uint4 vp1 = *reinterpret_cast<const uint4*>(s1 + c + 4);
+            const uint32_t r[8] = {vr0.x, vr0.y, vr0.z, vr0.w, vr1.x, vr1.y, vr1.z, vr1.w};
+            const uint32_t q[8] = {vp0.x, vp0.y, vp0.z, vp0.w, vp1.x, vp1.y, vp1.z, vp1.w};
 #pragma unroll
-            for (int v = 0; v < 4; v += 2)
+            for (int v = 0; v < 8; v += 2)
 #pragma unroll
                 for (int j = 0; j < kScanQ; ++j) {
                     const uint32_t K = CLS == CLS_A ? kt[j] : kp[j];
@@ -908,7 +913,11 @@ __device__ __forceinline__ void scan_item(const uint32_t* __restrict__ s0,
                     const uint32_t v1 = q[v + 1] | ((K - r[v + 1]) & 0x80000000u);
                     be[j] = __vimin3_u32(be[j], v0, v1);
                 }
-        } else {
+        }
+        return;
+    }
+    for (int c = 0; c < nc; c += 4) {
+        {
             // s0: rank_t, s1: rank_p, s2: pos_e, s3: pos_t
             const uint4 vt = *reinterpret_cast<const uint4*>(s0 + c);
             const uint4 vpp = *reinterpret_cast<const uint4*>(s1 + c);
@@ -1016,7 +1025,7 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) 
         }
         for (int64_t c0 = j0; c0 < j1; c0 += kScanCh) {
             const int nc = (int)min((int64_t)kScanCh, j1 - c0);
-            const int ncp = (nc + 3) & ~3;
+            const int ncp = (nc + 7) & ~7;  // class A/C iterations take 8 configs
             __syncthreads();
             if (c == CLS_A) {
                 stage_keys(s0, d.rank32[ORD_T] + c0, nc, ncp, kPadRank);

@@ -885,7 +885,7 @@ __global__ void k_assign_qprep(PlanDev d, uint64_t* gk,
 // (VIMNMX3) folds two configs into the running minimum — 1.5 ALU-pipe ops per pair
 // instead of a compare + predicated min (2). Class B (QoS with budget) tests both
 // sides with compares and keeps both minima.
-template <int CLS>
+template <int CLS, int NQ = kScanQ>
 __device__ __forceinline__ void scan_item(const uint32_t* __restrict__ s0,
                                           const uint32_t* __restrict__ s1,
                                           const uint32_t* __restrict__ s2,
@@ -907,7 +907,7 @@ __device__ __forceinline__ void scan_item(const uint32_t* __restrict__ s0,
 #pragma unroll
             for (int v = 0; v < 8; v += 2)
 #pragma unroll
-                for (int j = 0; j < kScanQ; ++j) {
+                for (int j = 0; j < NQ; ++j) {
                     const uint32_t K = CLS == CLS_A ? kt[j] : kp[j];
                     const uint32_t v0 = q[v] | ((K - r[v]) & 0x80000000u);
                     const uint32_t v1 = q[v + 1] | ((K - r[v + 1]) & 0x80000000u);
@@ -928,7 +928,7 @@ __device__ __forceinline__ void scan_item(const uint32_t* __restrict__ s0,
 #pragma unroll
             for (int v = 0; v < 4; ++v)
 #pragma unroll
-                for (int j = 0; j < kScanQ; ++j) {
+                for (int j = 0; j < NQ; ++j) {
                     const bool fp = rp[v] <= kp[j];
                     if (fp && rt[v] <= kt[j]) be[j] = min(be[j], pe[v]);
                     if (fp) bt[j] = min(bt[j], pt[v]);
@@ -1023,6 +1023,7 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) 
             be[q] = 0xFFFFFFFFu;
             bt[q] = 0xFFFFFFFFu;
         }
+        const bool full_slots = __any_sync(0xffffffffu, qid[kScanQ - 1] >= 0);
         for (int64_t c0 = j0; c0 < j1; c0 += kScanCh) {
             const int nc = (int)min((int64_t)kScanCh, j1 - c0);
             const int ncp = (nc + 7) & ~7;  // class A/C iterations take 8 configs
@@ -1040,9 +1041,18 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) 
                 stage_keys(s3, d.pos32[ORD_T] + c0, nc, ncp, 0u);
             }
             __syncthreads();
-            if (c == CLS_A) scan_item<CLS_A>(s0, s1, s2, s3, ncp, kt, kp, be, bt);
-            else if (c == CLS_B) scan_item<CLS_B>(s0, s1, s2, s3, ncp, kt, kp, be, bt);
-            else scan_item<CLS_C>(s0, s1, s2, s3, ncp, kt, kp, be, bt);
+            // a warp whose last query slot is idle on every lane skips it (balanced
+            // tiles leave up to one slot per thread empty: ~10 % of the pairs at 1e4
+            // queries); the choice is warp-uniform
+            if (c == CLS_A) {
+                if (full_slots) scan_item<CLS_A>(s0, s1, s2, s3, ncp, kt, kp, be, bt);
+                else scan_item<CLS_A, kScanQ - 1>(s0, s1, s2, s3, ncp, kt, kp, be, bt);
+            } else if (c == CLS_B) {
+                scan_item<CLS_B>(s0, s1, s2, s3, ncp, kt, kp, be, bt);
+            } else {
+                if (full_slots) scan_item<CLS_C>(s0, s1, s2, s3, ncp, kt, kp, be, bt);
+                else scan_item<CLS_C, kScanQ - 1>(s0, s1, s2, s3, ncp, kt, kp, be, bt);
+            }
         }
 #pragma unroll
         for (int q = 0; q < kScanQ; ++q) {

@@ -925,13 +925,21 @@ __device__ __forceinline__ void scan_item(const uint32_t* __restrict__ s0,
             const uint4 vq = *reinterpret_cast<const uint4*>(s3 + c);
             const uint32_t rt[4] = {vt.x, vt.y, vt.z, vt.w}, rp[4] = {vpp.x, vpp.y, vpp.z, vpp.w};
             const uint32_t pe[4] = {ve.x, ve.y, ve.z, ve.w}, pt[4] = {vq.x, vq.y, vq.z, vq.w};
+            // both sides as sign masks: dt = Kt-1 - r_t, dp = Kp-1 - r_p; the QoS value
+            // pos_e + ((dt | dp) & 0x80000000) (LOP3, then an add of disjoint bits on the
+            // FMA pipe), the budget-branch value pos_t | (dp & 0x80000000) (LOP3)
 #pragma unroll
-            for (int v = 0; v < 4; ++v)
+            for (int v = 0; v < 4; v += 2)
 #pragma unroll
                 for (int j = 0; j < NQ; ++j) {
-                    const bool fp = rp[v] <= kp[j];
-                    if (fp && rt[v] <= kt[j]) be[j] = min(be[j], pe[v]);
-                    if (fp) bt[j] = min(bt[j], pt[v]);
+                    const uint32_t dt0 = kt[j] - rt[v], dp0 = kp[j] - rp[v];
+                    const uint32_t dt1 = kt[j] - rt[v + 1], dp1 = kp[j] - rp[v + 1];
+                    const uint32_t e0 = pe[v] + ((dt0 | dp0) & 0x80000000u);
+                    const uint32_t e1 = pe[v + 1] + ((dt1 | dp1) & 0x80000000u);
+                    const uint32_t t0 = pt[v] | (dp0 & 0x80000000u);
+                    const uint32_t t1 = pt[v + 1] | (dp1 & 0x80000000u);
+                    be[j] = __vimin3_u32(be[j], e0, e1);
+                    bt[j] = __vimin3_u32(bt[j], t0, t1);
                 }
         }
     }

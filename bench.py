@@ -503,7 +503,7 @@ def run_ours(args, dist: Dist):
         "e2e": {"value": e2e_value, "unit": "config evals/s",
                 "h2d_bytes_per_step": nq * QUERY_DT.itemsize,
                 "d2h_bytes_per_step": nq * 5,
-                "api": "pals_select (C ABI, pinned host buffers; includes eval+rank)"},
+                "api": "pals_select (C ABI, pinned host buffers: one graph, query upload overlapped with eval+rank, decisions stored to the mapped host buffers by the finalize kernel)"},
         "roofline": roof,
         "gpu_launches": int(launches),
         "gather": gather,
@@ -802,7 +802,7 @@ def bench_cfg3(args, dist, ctx, stream, l2_flush, int_peak):
                              "exact_fold": int(cnt[5])},
            "e2e": {"value": pairs_total / (e2e_max * 1e-3), "unit": "config evals/s",
                    "h2d_bytes_per_step": nq * QUERY_DT.itemsize, "d2h_bytes_per_step": nq * 5,
-                   "api": "pals_select (C ABI, pinned host buffers; includes eval+rank)"},
+                   "api": "pals_select (C ABI, pinned host buffers: one graph, query upload overlapped with eval+rank, decisions stored to the mapped host buffers by the finalize kernel)"},
            "roofline": {"bound": "alu", "kernel": "k_scan",
                         "achieved": int_ops_step / (scan_avg * 1e-3) / 1e12,
                         "peak": int_peak / 1e12, "unit": "Tops/s",

@@ -1715,12 +1715,15 @@ int pals_plan_run(pals_plan* p, const pals_query* d_queries, int64_t nq, int32_t
     return plan_step(p, d_queries, nq, d_idx, d_reason, nullptr, nullptr, nullptr);
 }
 
-static bool is_pinned(const void* h) {
+// page-locked host memory; *dev = its device-side address (mapped under unified
+// addressing) or null
+static bool is_pinned(const void* h, void** dev = nullptr) {
     cudaPointerAttributes at;
     if (cudaPointerGetAttributes(&at, h) != cudaSuccess) {
         (void)cudaGetLastError();
         return false;
     }
+    if (dev) *dev = at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
     return at.type == cudaMemoryTypeHost;
 }
 
@@ -1747,12 +1750,18 @@ int pals_select(pals_plan* p, const pals_query* queries, int64_t nq, int32_t* id
     pals_query* dq = (pals_query*)b;
     int32_t* di = (int32_t*)(b + (size_t)nq * sizeof(pals_query));
     uint8_t* dr = (uint8_t*)(di + nq);
-    if (is_pinned(queries) && is_pinned(idx) && is_pinned(reason)) {
-        // one graph: upload overlapped with the prepare, decisions downloaded at the end
-        rc = plan_step(p, dq, nq, di, dr, queries, idx, reason);
+    void *m_idx = nullptr, *m_rs = nullptr;
+    if (is_pinned(queries) && is_pinned(idx, &m_idx) && is_pinned(reason, &m_rs)) {
+        // one graph: upload overlapped with the prepare; with mapped result buffers the
+        // decisions are stored straight into host memory by k_finalize (no download
+        // nodes), else downloaded at the end
+        const bool mapped = m_idx && m_rs;
+        rc = mapped ? plan_step(p, dq, nq, (int32_t*)m_idx, (uint8_t*)m_rs, queries, nullptr,
+                                nullptr)
+                    : plan_step(p, dq, nq, di, dr, queries, idx, reason);
         if (rc) return rc;
         PALS_CUDA(cudaStreamSynchronize(s));
-        p->last_exact = p->h_cnt[N_CLS];
+        p->last_exact = mapped ? -1 : p->h_cnt[N_CLS];  // -1: read on demand
         return PALS_OK;
     }
     PALS_CUDA(cudaMemcpyAsync(dq, queries, (size_t)nq * sizeof(pals_query), cudaMemcpyHostToDevice, s));
@@ -1779,7 +1788,15 @@ int pals_plan_scores(pals_plan* p, double* t_hat, double* p_node, double* eff) {
     return PALS_OK;
 }
 
-int64_t pals_plan_last_exact_count(const pals_plan* p) { return p->last_exact; }
+int64_t pals_plan_last_exact_count(const pals_plan* p) {
+    if (p->last_exact < 0 && p->counts) {  // not downloaded by the last select
+        int32_t cnt[N_CLS + 1];
+        if (copy_on(p->ctx->stream, cnt, p->counts, sizeof cnt, cudaMemcpyDeviceToHost) ==
+            cudaSuccess)
+            const_cast<pals_plan*>(p)->last_exact = cnt[N_CLS];
+    }
+    return p->last_exact;
+}
 
 int pals_plan_stats(pals_plan* p, int64_t* c6) {
     if (!p->counts) {

@@ -22,6 +22,9 @@ constexpr int kChunk = 2048;        // sort chunk (smem block merge sort)
 constexpr int kScanCh = 2048;       // configs per scan work item
 constexpr int kScanThreads = 256;
 constexpr int kScanQ = 8;           // queries per thread in the scan (register tile)
+constexpr int kMaxChunks = 8;       // pals_select: query chunks pipelined behind their upload
+constexpr int kCountStride = 8;     // class counters per chunk (N_CLS + 1 used)
+constexpr int kCountInts = kMaxChunks * kCountStride;
 constexpr int kScanTQ = kScanThreads * kScanQ;
 
 enum { CLS_A = 0, CLS_B = 1, CLS_C = 2, CLS_D = 3, CLS_X = 4, N_CLS = 5 };
@@ -85,6 +88,8 @@ struct pals_plan {
     void* g_hrs = nullptr;
     cudaStream_t side = nullptr;  // upload stream of pals_select's graph
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_up[kMaxChunks] = {};  // chunk uploads done (pals_select)
+    int g_chunks = 1;             // query chunks of the cached pals_select graph
     int32_t* h_cnt = nullptr;     // pinned class counters (pals_select)
     void* scratch = nullptr;      // plan_scratch()
     size_t scratch_bytes = 0;
@@ -304,7 +309,8 @@ __global__ void __launch_bounds__(TPB) k_sort_chunks(PlanDev d, uint64_t* gk, ui
         gk[0] = gk[1] = kNone64;
         *done = 0;
     }
-    if (counts_reset && blockIdx.x == 0 && blockIdx.y == 0 && t < 16) counts_reset[t] = 0;
+    if (counts_reset && blockIdx.x == 0 && blockIdx.y == 0)
+        for (int i = t; i < kCountInts; i += TPB) counts_reset[i] = 0;
     __syncthreads();
     uint64_t k[kIPT];
     uint32_t v[kIPT];
@@ -1422,6 +1428,8 @@ int pals_plan_destroy(pals_plan* p) {
     if (p->ev_scan1) cudaEventDestroy(p->ev_scan1);
     if (p->ev_fork) cudaEventDestroy(p->ev_fork);
     if (p->ev_join) cudaEventDestroy(p->ev_join);
+    for (auto& e : p->ev_up)
+        if (e) cudaEventDestroy(e);
     if (p->side) cudaStreamDestroy(p->side);
     if (p->h_cnt) cudaFreeHost(p->h_cnt);
     cudaFree(p->scratch);
@@ -1537,7 +1545,7 @@ static int ensure_query_buffers(pals_plan* p, int64_t nq) {
     p->best_t = (uint64_t*)take(8 * cap);
     p->cls = (uint8_t*)take(cap);
     p->qlist = (int32_t*)take(4 * (size_t)cap * N_CLS);
-    p->counts = (int32_t*)take(64);
+    p->counts = (int32_t*)take(4 * kCountInts);
     p->qcap = cap;
     return PALS_OK;
 }
@@ -1561,9 +1569,25 @@ static SelArgs make_args(pals_plan* p, const pals_query* d_queries, int64_t nq, 
     return a;
 }
 
+// the arguments of query chunk k = [off, off + len): every per-query array shifted,
+// its own class counters; the class lists keep their stride qcap, so chunks use
+// disjoint slices of them
+static SelArgs make_args_chunk(pals_plan* p, const pals_query* d_queries, int64_t off, int64_t len,
+                               int32_t* d_idx, uint8_t* d_reason, int k) {
+    SelArgs a = make_args(p, d_queries + off, len, d_idx + off, d_reason + off);
+    a.thr_t += off;
+    a.thr_p += off;
+    a.best_e += off;
+    a.best_t += off;
+    a.cls += off;
+    a.qlist += off;
+    a.counts += kCountStride * k;
+    return a;
+}
+
 // select, part 1 (needs only the merged arrays): thresholds and classes per query
 static int select_head(pals_plan* p, const SelArgs& a, cudaStream_t s) {
-    PALS_CUDA(cudaMemsetAsync(p->counts, 0, 64, s));
+    PALS_CUDA(cudaMemsetAsync(p->counts, 0, 4 * kCountInts, s));
     const cudaError_t e = launch_k(k_qprep, grid_blocks(p->ctx, a.nq, 256), 256, 0, s, false,
                                    p->d, a);
     if (e != cudaSuccess) return cuda_fail(e, "pals_plan_select_device qprep");
@@ -1628,7 +1652,8 @@ static int plan_step(pals_plan* p, const pals_query* d_queries, int64_t nq, int3
         PALS_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
         PALS_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
         PALS_CUDA(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
-        PALS_CUDA(cudaMallocHost(&p->h_cnt, 64));
+        for (auto& e : p->ev_up) PALS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        PALS_CUDA(cudaMallocHost(&p->h_cnt, 4 * kCountInts));
     }
     if (!hit) {
         if (p->gexec) {
@@ -1643,43 +1668,62 @@ static int plan_step(pals_plan* p, const pals_query* d_queries, int64_t nq, int3
         const int64_t l0 = ctx->launches;
         // (overlapping qprep with k_assign on a side stream measured no faster on
         // B200: the step stays a single chain)
+        // pals_select with many queries: the upload is split into chunks on the side
+        // stream and each chunk's qprep / scan / finalize waits only for its own chunk,
+        // so all but the first chunk's copy hide behind the previous chunk's scan
+        const int nch = !h_q ? 1
+                             : (int)std::max<int64_t>(1, std::min<int64_t>(kMaxChunks, nq / 131072));
+        const int64_t clen = (nq + nch - 1) / nch;
         cudaError_t ce0 = cudaSuccess;
         if (h_q) {
             ce0 = cudaEventRecord(p->ev_fork, s);
             if (ce0 == cudaSuccess) ce0 = cudaStreamWaitEvent(p->side, p->ev_fork, 0);
-            if (ce0 == cudaSuccess)
-                ce0 = cudaMemcpyAsync((void*)d_queries, h_q, (size_t)nq * sizeof(pals_query),
-                                      cudaMemcpyHostToDevice, p->side);
+            for (int k = 0; k < nch && ce0 == cudaSuccess; ++k) {
+                const int64_t off = k * clen, len = std::min(clen, nq - off);
+                ce0 = cudaMemcpyAsync((void*)(d_queries + off), h_q + off,
+                                      (size_t)len * sizeof(pals_query), cudaMemcpyHostToDevice,
+                                      p->side);
+                if (ce0 == cudaSuccess) ce0 = cudaEventRecord(p->ev_up[k], p->side);
+            }
             if (ce0 == cudaSuccess) ce0 = cudaEventRecord(p->ev_join, p->side);
         }
         rc = ce0 != cudaSuccess ? cuda_fail(ce0, "pals_select upload") : prep_head(p, p->counts);
-        if (!rc && h_q) {
-            const cudaError_t we = cudaStreamWaitEvent(s, p->ev_join, 0);
-            if (we != cudaSuccess) rc = cuda_fail(we, "pals_select upload join");
-        }
-        if (!rc) {
-            // assign (prepare, part 2) and qprep (select, part 1) fused in one launch
-            const SelArgs a = make_args(p, d_queries, nq, d_idx, d_reason);
-            const int eb = grid_blocks(ctx, p->n, 256), qb = grid_blocks(ctx, nq, 256);
-            const cudaError_t e = launch_k(k_assign_qprep, dim3(std::max(eb, qb), N_ORD + 1),
-                                           256, 0, s, (bool)p->pdl, p->d, p->gk,
-                                           (uint32_t*)(p->gk + 2), a, eb, qb);
-            if (e != cudaSuccess) rc = cuda_fail(e, "k_assign_qprep");
+        for (int k = 0; k < nch && !rc; ++k) {
+            const int64_t off = k * clen, len = std::min(clen, nq - off);
+            if (h_q) {
+                const cudaError_t we =
+                    cudaStreamWaitEvent(s, k == nch - 1 ? p->ev_join : p->ev_up[k], 0);
+                if (we != cudaSuccess) rc = cuda_fail(we, "pals_select upload join");
+            }
+            const SelArgs a = make_args_chunk(p, d_queries, off, len, d_idx, d_reason, k);
+            const int qb = grid_blocks(ctx, len, 256);
+            cudaError_t e;
+            if (!rc && k == 0) {
+                // assign (prepare, part 2) and qprep (select, part 1) fused in one launch
+                const int eb = grid_blocks(ctx, p->n, 256);
+                e = launch_k(k_assign_qprep, dim3(std::max(eb, qb), N_ORD + 1), 256, 0, s,
+                             (bool)p->pdl, p->d, p->gk, (uint32_t*)(p->gk + 2), a, eb, qb);
+                if (e != cudaSuccess) rc = cuda_fail(e, "k_assign_qprep");
+            } else if (!rc) {
+                e = launch_k(k_qprep, qb, 256, 0, s, false, p->d, a);
+                if (e != cudaSuccess) rc = cuda_fail(e, "k_qprep");
+            }
             if (!rc) {
                 count_launch(ctx, 1);
                 rc = select_tail(p, a);
             }
-            if (!rc && h_idx) {
-                cudaError_t de = cudaMemcpyAsync(h_idx, d_idx, (size_t)nq * 4,
-                                                 cudaMemcpyDeviceToHost, s);
-                if (de == cudaSuccess)
-                    de = cudaMemcpyAsync(h_rs, d_reason, (size_t)nq, cudaMemcpyDeviceToHost, s);
-                if (de == cudaSuccess)
-                    de = cudaMemcpyAsync(p->h_cnt, p->counts, 4 * (N_CLS + 1),
-                                         cudaMemcpyDeviceToHost, s);
-                if (de != cudaSuccess) rc = cuda_fail(de, "pals_select download");
-            }
         }
+        if (!rc && h_idx) {
+            cudaError_t de =
+                cudaMemcpyAsync(h_idx, d_idx, (size_t)nq * 4, cudaMemcpyDeviceToHost, s);
+            if (de == cudaSuccess)
+                de = cudaMemcpyAsync(h_rs, d_reason, (size_t)nq, cudaMemcpyDeviceToHost, s);
+            if (de == cudaSuccess)
+                de = cudaMemcpyAsync(p->h_cnt, p->counts, 4 * kCountInts, cudaMemcpyDeviceToHost,
+                                     s);
+            if (de != cudaSuccess) rc = cuda_fail(de, "pals_select download");
+        }
+        p->g_chunks = nch;
         p->capturing = 0;
         cudaGraph_t g = nullptr;
         const cudaError_t ce = cudaStreamEndCapture(s, &g);
@@ -1761,7 +1805,9 @@ int pals_select(pals_plan* p, const pals_query* queries, int64_t nq, int32_t* id
                     : plan_step(p, dq, nq, di, dr, queries, idx, reason);
         if (rc) return rc;
         PALS_CUDA(cudaStreamSynchronize(s));
-        p->last_exact = mapped ? -1 : p->h_cnt[N_CLS];  // -1: read on demand
+        int64_t ex = 0;
+        for (int k = 0; k < p->g_chunks; ++k) ex += p->h_cnt[kCountStride * k + N_CLS];
+        p->last_exact = mapped ? -1 : ex;  // -1: read on demand
         return PALS_OK;
     }
     PALS_CUDA(cudaMemcpyAsync(dq, queries, (size_t)nq * sizeof(pals_query), cudaMemcpyHostToDevice, s));
@@ -1790,10 +1836,13 @@ int pals_plan_scores(pals_plan* p, double* t_hat, double* p_node, double* eff) {
 
 int64_t pals_plan_last_exact_count(const pals_plan* p) {
     if (p->last_exact < 0 && p->counts) {  // not downloaded by the last select
-        int32_t cnt[N_CLS + 1];
+        int32_t cnt[kCountInts];
         if (copy_on(p->ctx->stream, cnt, p->counts, sizeof cnt, cudaMemcpyDeviceToHost) ==
-            cudaSuccess)
-            const_cast<pals_plan*>(p)->last_exact = cnt[N_CLS];
+            cudaSuccess) {
+            int64_t ex = 0;
+            for (int k = 0; k < p->g_chunks; ++k) ex += cnt[kCountStride * k + N_CLS];
+            const_cast<pals_plan*>(p)->last_exact = ex;
+        }
     }
     return p->last_exact;
 }

@@ -160,9 +160,12 @@ def test_select_one_and_errors(ctx, bundle):
         select_config(other, make_targets(100.0), m, coeffs)
 
 
-def test_select_pinned_buffers_graph_path(ctx, oracle):
+@pytest.mark.parametrize("nq", [3000, 300_000])
+def test_select_pinned_buffers_graph_path(ctx, oracle, nq):
     """pals_select with pinned host buffers runs one graph holding the upload (overlapped
-    with the prepare) and the downloads; replays must read the buffers' current contents."""
+    with the prepare; in chunks pipelined behind their scans for large batches) and
+    stores the decisions into the mapped result buffers; replays must read the buffers'
+    current contents."""
     import torch
 
     from paper_2605_21427_b200.abi import QUERY_DT, ptr
@@ -173,7 +176,7 @@ def test_select_pinned_buffers_graph_path(ctx, oracle):
     plan = Plan(model, Grid(ctx, cfg["points"]), cfg["coeffs"])
     th, _, _ = plan.scores()
     T, P, _ = oracle.eval(cfg["profile"], cfg["gpu"], cfg["points"])
-    nq = 3000
+    step = 7 if nq < 10_000 else 997
     h_q = torch.empty(nq * QUERY_DT.itemsize, dtype=torch.uint8, pin_memory=True)
     h_qn = h_q.numpy().view(QUERY_DT)
     h_idx = torch.empty(nq, dtype=torch.int32, pin_memory=True).numpy()
@@ -184,5 +187,6 @@ def test_select_pinned_buffers_graph_path(ctx, oracle):
         check(ctx.lib.pals_select(plan.h, ptr(h_qn), nq, ptr(h_idx), ptr(h_rs)))
         idx, rs = plan.select(q)  # pageable path
         assert np.array_equal(h_idx, idx) and np.array_equal(h_rs, rs)
-        oi, orr, rc = oracle.select(cfg["points"], T, P, cfg["coeffs"], q[::7])
-        assert rc == 0 and np.array_equal(h_idx[::7], oi) and np.array_equal(h_rs[::7], orr)
+        oi, orr, rc = oracle.select(cfg["points"], T, P, cfg["coeffs"], q[::step])
+        assert rc == 0 and np.array_equal(h_idx[::step], oi) and np.array_equal(h_rs[::step], orr)
+        assert plan.last_exact_count >= 0

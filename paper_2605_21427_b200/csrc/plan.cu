@@ -3,9 +3,10 @@
 //
 // Reference semantics: select_config controller.hpp:132-201 with
 // better_candidate controller.hpp:118-125. The fast path turns every FP64
-// feasibility test and every tolerance comparison into integer compares on
-// precomputed dense ranks; queries whose winner sits in a near-tie cluster
-// (scores within 4e-9 relative) are re-decided by the literal sequential fold.
+// feasibility test and every tolerance comparison into integer operations on
+// precomputed competition ranks and merged positions; queries whose winner sits in a
+// near-tie cluster (scores within 4e-9 relative) are re-decided by the literal
+// sequential fold.
 #include <algorithm>
 #include <type_traits>
 #include <cstring>

@@ -47,6 +47,7 @@ struct pals_plan {
     int nchunks = 0;
     int chunk = 4096;  // sort chunk size (keys per CTA)
     int merge_tile = 1024;  // output keys per CTA of a merge round
+    int sort_ipt4 = 1;      // 2,048-key chunks: 4 keys per thread (PALS_SORT_IPT=8: 8)
     int force_exact = 0;
     int values = 0;               // internal: th / ef supplied directly (frontier.cu)
     int pdl = 1;                  // programmatic dependent launch between step kernels
@@ -186,7 +187,8 @@ __device__ __forceinline__ int pv(int e) { return e + (e >> 5); }  // padded ind
 
 // ties are broken on the carried TR, so the order is the packed-key order; the
 // merges keep it because their left run always holds the smaller TRs
-__device__ __forceinline__ void cmp_swap(uint64_t (&k)[kIPT], uint32_t (&v)[kIPT], int i, int j) {
+template <int IPT>
+__device__ __forceinline__ void cmp_swap(uint64_t (&k)[IPT], uint32_t (&v)[IPT], int i, int j) {
     if (k[j] < k[i] || (k[j] == k[i] && v[j] < v[i])) {
         const uint64_t tk = k[i];
         k[i] = k[j];
@@ -197,7 +199,15 @@ __device__ __forceinline__ void cmp_swap(uint64_t (&k)[kIPT], uint32_t (&v)[kIPT
     }
 }
 
-__device__ __forceinline__ void sort8(uint64_t (&k)[kIPT], uint32_t (&v)[kIPT]) {
+// Batcher's odd-even merge networks for 8 (19 comparators) and 4 (5) keys
+template <int IPT>
+__device__ __forceinline__ void sort_net(uint64_t (&k)[IPT], uint32_t (&v)[IPT]) {
+    if (IPT == 4) {
+        cmp_swap(k, v, 0, 1); cmp_swap(k, v, 2, 3);
+        cmp_swap(k, v, 0, 2); cmp_swap(k, v, 1, 3);
+        cmp_swap(k, v, 1, 2);
+        return;
+    }
     cmp_swap(k, v, 0, 1); cmp_swap(k, v, 2, 3); cmp_swap(k, v, 4, 5); cmp_swap(k, v, 6, 7);
     cmp_swap(k, v, 0, 2); cmp_swap(k, v, 1, 3); cmp_swap(k, v, 4, 6); cmp_swap(k, v, 5, 7);
     cmp_swap(k, v, 1, 2); cmp_swap(k, v, 5, 6);
@@ -219,13 +229,13 @@ __device__ __forceinline__ int mp_search(FA A, int la, FB B, int lb, int diag) {
     return lo;
 }
 
-// kIPT consecutive outputs of merge(A, B) starting at (a, b) on the merge path
-template <class KA, class VA, class KB, class VB>
+// IPT consecutive outputs of merge(A, B) starting at (a, b) on the merge path
+template <int IPT, class KA, class VA, class KB, class VB>
 __device__ __forceinline__ void mp_serial(KA Ak, VA Av, int la, KB Bk, VB Bv, int lb, int a,
-                                          int b, uint64_t (&k)[kIPT], uint32_t (&v)[kIPT]) {
+                                          int b, uint64_t (&k)[IPT], uint32_t (&v)[IPT]) {
     uint64_t ka = a < la ? Ak(a) : kNone64, kb = b < lb ? Bk(b) : kNone64;
 #pragma unroll
-    for (int i = 0; i < kIPT; ++i) {
+    for (int i = 0; i < IPT; ++i) {
         if (b >= lb || (a < la && ka <= kb)) {
             k[i] = ka;
             v[i] = a < la ? Av(a) : 0u;
@@ -240,47 +250,47 @@ __device__ __forceinline__ void mp_serial(KA Ak, VA Av, int la, KB Bk, VB Bv, in
     }
 }
 
-// block merge sort of the TPB * kIPT (key, index) pairs in sk/sv (padded layout);
-// leaves each thread's kIPT outputs (positions t*kIPT..) in k/v
-template <int TPB>
-__device__ __forceinline__ void block_sort(uint64_t* sk, uint32_t* sv, uint64_t (&k)[kIPT],
-                                           uint32_t (&v)[kIPT]) {
+// block merge sort of the TPB * IPT (key, index) pairs in sk/sv (padded layout);
+// leaves each thread's IPT outputs (positions t*IPT..) in k/v
+template <int TPB, int IPT>
+__device__ __forceinline__ void block_sort(uint64_t* sk, uint32_t* sv, uint64_t (&k)[IPT],
+                                           uint32_t (&v)[IPT]) {
     const int t = threadIdx.x;
 #pragma unroll
-    for (int i = 0; i < kIPT; ++i) {
-        k[i] = sk[pk(t * kIPT + i)];
-        v[i] = sv[pv(t * kIPT + i)];
+    for (int i = 0; i < IPT; ++i) {
+        k[i] = sk[pk(t * IPT + i)];
+        v[i] = sv[pv(t * IPT + i)];
     }
-    sort8(k, v);
+    sort_net<IPT>(k, v);
     for (int w = 1; w < TPB; w <<= 1) {
         __syncthreads();
 #pragma unroll
-        for (int i = 0; i < kIPT; ++i) {
-            sk[pk(t * kIPT + i)] = k[i];
-            sv[pv(t * kIPT + i)] = v[i];
+        for (int i = 0; i < IPT; ++i) {
+            sk[pk(t * IPT + i)] = k[i];
+            sv[pv(t * IPT + i)] = v[i];
         }
         __syncthreads();
-        const int g0 = (t & ~(2 * w - 1)) * kIPT;  // the group's first key
-        const int len = w * kIPT;
-        const int diag = (t & (2 * w - 1)) * kIPT;
+        const int g0 = (t & ~(2 * w - 1)) * IPT;  // the group's first key
+        const int len = w * IPT;
+        const int diag = (t & (2 * w - 1)) * IPT;
         auto Ak = [&](int i) { return sk[pk(g0 + i)]; };
         auto Bk = [&](int i) { return sk[pk(g0 + len + i)]; };
         auto Av = [&](int i) { return sv[pv(g0 + i)]; };
         auto Bv = [&](int i) { return sv[pv(g0 + len + i)]; };
         const int a = mp_search(Ak, len, Bk, len, diag);
-        mp_serial(Ak, Av, len, Bk, Bv, len, a, diag - a, k, v);
+        mp_serial<IPT>(Ak, Av, len, Bk, Bv, len, a, diag - a, k, v);
     }
 }
 
-constexpr size_t sort_smem_bytes(int tpb) {
-    return (size_t)(tpb * kIPT + tpb * kIPT / 16) * 8 + (size_t)(tpb * kIPT + tpb * kIPT / 32) * 4;
+constexpr size_t sort_smem_bytes(int tpb, int ipt = kIPT) {
+    return (size_t)(tpb * ipt + tpb * ipt / 16) * 8 + (size_t)(tpb * ipt + tpb * ipt / 32) * 4;
 }
 
-template <int TPB>
+template <int TPB, int IPT = kIPT>
 __global__ void __launch_bounds__(TPB) k_sort_chunks(PlanDev d, uint64_t* gk, uint32_t* done,
                                                      int32_t* counts_reset, int to_merged,
                                                      int final_round) {
-    constexpr int CH = TPB * kIPT;
+    constexpr int CH = TPB * IPT;
     extern __shared__ __align__(16) unsigned char sort_smem[];  // sort_smem_bytes(TPB)
     uint64_t* sk = reinterpret_cast<uint64_t*>(sort_smem);
     uint32_t* sv = reinterpret_cast<uint32_t*>(sk + CH + CH / 16);
@@ -293,15 +303,15 @@ __global__ void __launch_bounds__(TPB) k_sort_chunks(PlanDev d, uint64_t* gk, ui
         // not be reordered across a shared store, which would serialize the round trips)
         // input in TR order (the evaluation writes position q = TR of each point), so
         // sorting by (value, q) gives merged positions in packed-key order
-        uint64_t x[kIPT];
+        uint64_t x[IPT];
         const uint64_t* __restrict__ src = d.skey[o];
 #pragma unroll
-        for (int k = 0; k < kIPT; ++k) {
+        for (int k = 0; k < IPT; ++k) {
             const uint32_t g = base + t + k * TPB;
             x[k] = g < (uint32_t)d.n ? min(__ldg(src + g), kNone64 - 1) : kNone64;
         }
 #pragma unroll
-        for (int k = 0; k < kIPT; ++k) {
+        for (int k = 0; k < IPT; ++k) {
             sk[pk(t + k * TPB)] = x[k];
             sv[pv(t + k * TPB)] = base + t + k * TPB;
         }
@@ -313,14 +323,14 @@ __global__ void __launch_bounds__(TPB) k_sort_chunks(PlanDev d, uint64_t* gk, ui
     if (counts_reset && blockIdx.x == 0 && blockIdx.y == 0)
         for (int i = t; i < kCountInts; i += TPB) counts_reset[i] = 0;
     __syncthreads();
-    uint64_t k[kIPT];
-    uint32_t v[kIPT];
-    block_sort<TPB>(sk, sv, k, v);
+    uint64_t k[IPT];
+    uint32_t v[IPT];
+    block_sort<TPB, IPT>(sk, sv, k, v);
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < kIPT; ++i) {
-        sk[pk(t * kIPT + i)] = k[i];
-        sv[pv(t * kIPT + i)] = v[i];
+    for (int i = 0; i < IPT; ++i) {
+        sk[pk(t * IPT + i)] = k[i];
+        sv[pv(t * IPT + i)] = v[i];
     }
     __syncthreads();
     uint64_t* dst = to_merged ? d.merged[o] : d.sorted[o];
@@ -468,7 +478,7 @@ __global__ void __launch_bounds__(TPB) k_merge_round(PlanDev d, uint32_t np, int
         auto Av = [&](int i) { return sv[pv(i)]; };
         auto Bv = [&](int i) { return sv[pv(na + i)]; };
         const int a = mp_search(Ak, na, Bk, nb, diag);
-        mp_serial(Ak, Av, na, Bk, Bv, nb, a, diag - a, k, v);
+        mp_serial<kIPT>(Ak, Av, na, Bk, Bv, nb, a, diag - a, k, v);
         const uint32_t p0 = pb + d0 + diag;
 #pragma unroll
         for (int i = 0; i < kIPT; ++i) {
@@ -1315,6 +1325,10 @@ static int plan_build(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)sort_smem_bytes(1024)));
         }
+        const char* ipt = getenv("PALS_SORT_IPT");
+        // measured on B200 (cfg2): 4 keys x 512 threads sorts a 2,048-key chunk in 15 us
+        // against 18 us for 8 x 256 (more warps hide the merge levels' smem latency)
+        p->sort_ipt4 = !(ipt && atoi(ipt) == 8);
         const char* t = getenv("PALS_MERGE_TILE");
         p->merge_tile = (t && atoi(t) == 2048) ? 2048 : 1024;
     }
@@ -1474,7 +1488,10 @@ static int prep_head(pals_plan* p, int32_t* counts_reset = nullptr) {
     while (((int64_t)p->chunk << rounds) < p->np) ++rounds;
     const int sort_to_merged = rounds % 2 == 0;
     const int sort_final = rounds == 0;
-    switch (p->chunk) {
+    if (p->sort_ipt4 && p->chunk == 2048)  // 4 keys per thread, 512 threads
+        e = launch_k(k_sort_chunks<512, 4>, gs, 512, sort_smem_bytes(512, 4), s, pdl, d, p->gk,
+                     done, counts_reset, sort_to_merged, sort_final);
+    else switch (p->chunk) {
 #define PALS_SORT(TPB)                                                                         \
     case TPB * kIPT:                                                                           \
         e = launch_k(k_sort_chunks<TPB>, gs, TPB, sort_smem_bytes(TPB), s, pdl, d, p->gk, done, \
@@ -1490,6 +1507,7 @@ static int prep_head(pals_plan* p, int32_t* counts_reset = nullptr) {
         default:
             e = cudaErrorInvalidValue;
     }
+
     // round k reads the buffer round k-1 wrote; the last round writes merged
     int lg = 0;
     while ((1 << lg) < p->chunk) ++lg;

@@ -47,7 +47,8 @@ struct pals_plan {
     int nchunks = 0;
     int chunk = 4096;  // sort chunk size (keys per CTA)
     int merge_tile = 1024;  // output keys per CTA of a merge round
-    int sort_ipt4 = 1;      // 2,048-key chunks: 4 keys per thread (PALS_SORT_IPT=8: 8)
+    int sort_ipt = 4;       // keys per thread of a 2,048-key chunk sort (PALS_SORT_IPT 2/4/8)
+    int merge_ipt = 4;      // keys per thread of a 1,024-key merge tile (PALS_MERGE_IPT 2/4/8)
     int force_exact = 0;
     int values = 0;               // internal: th / ef supplied directly (frontier.cu)
     int pdl = 1;                  // programmatic dependent launch between step kernels
@@ -202,6 +203,10 @@ __device__ __forceinline__ void cmp_swap(uint64_t (&k)[IPT], uint32_t (&v)[IPT],
 // Batcher's odd-even merge networks for 8 (19 comparators) and 4 (5) keys
 template <int IPT>
 __device__ __forceinline__ void sort_net(uint64_t (&k)[IPT], uint32_t (&v)[IPT]) {
+    if (IPT == 2) {
+        cmp_swap(k, v, 0, 1);
+        return;
+    }
     if (IPT == 4) {
         cmp_swap(k, v, 0, 1); cmp_swap(k, v, 2, 3);
         cmp_swap(k, v, 0, 2); cmp_swap(k, v, 1, 3);
@@ -414,10 +419,10 @@ __device__ __forceinline__ void warp_mp2(FA A, uint32_t la, FB B, uint32_t lb, u
 // the block sort. Ties take the left run first (a stable merge). Buffers
 // ping-pong between sorted and merged; the chunk sort picks its output so the last
 // round writes merged, and the last round also writes the search index.
-template <int TPB>
+template <int TPB, int IPT = kIPT>
 __global__ void __launch_bounds__(TPB) k_merge_round(PlanDev d, uint32_t np, int lgL,
                                                      int to_merged, int final_round) {
-    constexpr int TILE = TPB * kIPT;
+    constexpr int TILE = TPB * IPT;
     __shared__ uint64_t sk[TILE + TILE / 16];
     __shared__ uint32_t sv[TILE + TILE / 32];
     __shared__ uint32_t split[2];
@@ -451,10 +456,10 @@ __global__ void __launch_bounds__(TPB) k_merge_round(PlanDev d, uint32_t np, int
     const uint32_t b0 = d0 - a0;
     {
         // stage both slices: every load in flight before the shared stores
-        uint64_t x[kIPT];
-        uint32_t y[kIPT];
+        uint64_t x[IPT];
+        uint32_t y[IPT];
 #pragma unroll
-        for (int k = 0; k < kIPT; ++k) {
+        for (int k = 0; k < IPT; ++k) {
             const int i = t + k * TPB;
             const uint32_t q = i < na ? pb + a0 + i : pb + la + b0 + (i - na);
             const bool ok = i < na + nb;
@@ -462,26 +467,26 @@ __global__ void __launch_bounds__(TPB) k_merge_round(PlanDev d, uint32_t np, int
             y[k] = ok ? __ldg(inv + q) : 0u;
         }
 #pragma unroll
-        for (int k = 0; k < kIPT; ++k) {
+        for (int k = 0; k < IPT; ++k) {
             sk[pk(t + k * TPB)] = x[k];
             sv[pv(t + k * TPB)] = y[k];
         }
     }
     __syncthreads();
-    const int diag = t * kIPT;
+    const int diag = t * IPT;
     const int tot = na + nb;
     if (diag < tot) {
-        uint64_t k[kIPT];
-        uint32_t v[kIPT];
+        uint64_t k[IPT];
+        uint32_t v[IPT];
         auto Ak = [&](int i) { return sk[pk(i)]; };
         auto Bk = [&](int i) { return sk[pk(na + i)]; };
         auto Av = [&](int i) { return sv[pv(i)]; };
         auto Bv = [&](int i) { return sv[pv(na + i)]; };
         const int a = mp_search(Ak, na, Bk, nb, diag);
-        mp_serial<kIPT>(Ak, Av, na, Bk, Bv, nb, a, diag - a, k, v);
+        mp_serial<IPT>(Ak, Av, na, Bk, Bv, nb, a, diag - a, k, v);
         const uint32_t p0 = pb + d0 + diag;
 #pragma unroll
-        for (int i = 0; i < kIPT; ++i) {
+        for (int i = 0; i < IPT; ++i) {
             if (diag + i < tot) {
                 out[p0 + i] = k[i];
                 outv[p0 + i] = v[i];
@@ -1328,7 +1333,11 @@ static int plan_build(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
         const char* ipt = getenv("PALS_SORT_IPT");
         // measured on B200 (cfg2): 4 keys x 512 threads sorts a 2,048-key chunk in 15 us
         // against 18 us for 8 x 256 (more warps hide the merge levels' smem latency)
-        p->sort_ipt4 = !(ipt && atoi(ipt) == 8);
+        p->sort_ipt = ipt ? atoi(ipt) : 4;
+        // measured on B200 (cfg2): 4 keys x 256 threads per 1,024-key merge tile, 7.4 us per
+        // round against 8.5 us for 8 x 128
+        const char* mi = getenv("PALS_MERGE_IPT");
+        p->merge_ipt = mi ? atoi(mi) : 2;
         const char* t = getenv("PALS_MERGE_TILE");
         p->merge_tile = (t && atoi(t) == 2048) ? 2048 : 1024;
     }
@@ -1488,7 +1497,10 @@ static int prep_head(pals_plan* p, int32_t* counts_reset = nullptr) {
     while (((int64_t)p->chunk << rounds) < p->np) ++rounds;
     const int sort_to_merged = rounds % 2 == 0;
     const int sort_final = rounds == 0;
-    if (p->sort_ipt4 && p->chunk == 2048)  // 4 keys per thread, 512 threads
+    if (p->sort_ipt == 2 && p->chunk == 2048)  // 2 keys per thread, 1,024 threads
+        e = launch_k(k_sort_chunks<1024, 2>, gs, 1024, sort_smem_bytes(1024, 2), s, pdl, d,
+                     p->gk, done, counts_reset, sort_to_merged, sort_final);
+    else if (p->sort_ipt == 4 && p->chunk == 2048)  // 4 keys per thread, 512 threads
         e = launch_k(k_sort_chunks<512, 4>, gs, 512, sort_smem_bytes(512, 4), s, pdl, d, p->gk,
                      done, counts_reset, sort_to_merged, sort_final);
     else switch (p->chunk) {
@@ -1513,7 +1525,16 @@ static int prep_head(pals_plan* p, int32_t* counts_reset = nullptr) {
     while ((1 << lg) < p->chunk) ++lg;
     for (int k = 0; k < rounds && e == cudaSuccess; ++k) {
         const int to_m = (rounds - k) % 2 == 1, fin = k == rounds - 1;
-        if (p->merge_tile == 1024)
+        if (p->merge_tile == 1024 && p->merge_ipt == 1)
+            e = launch_k(k_merge_round<1024, 1>, dim3((unsigned)((p->np + 1023) / 1024), N_ORD),
+                         1024, 0, s, pdl, d, (uint32_t)p->np, lg + k, to_m, fin);
+        else if (p->merge_tile == 1024 && p->merge_ipt == 2)
+            e = launch_k(k_merge_round<512, 2>, dim3((unsigned)((p->np + 1023) / 1024), N_ORD),
+                         512, 0, s, pdl, d, (uint32_t)p->np, lg + k, to_m, fin);
+        else if (p->merge_tile == 1024 && p->merge_ipt == 4)
+            e = launch_k(k_merge_round<256, 4>, dim3((unsigned)((p->np + 1023) / 1024), N_ORD),
+                         256, 0, s, pdl, d, (uint32_t)p->np, lg + k, to_m, fin);
+        else if (p->merge_tile == 1024)
             e = launch_k(k_merge_round<128>, dim3((unsigned)((p->np + 1023) / 1024), N_ORD), 128, 0, s,
                          pdl, d, (uint32_t)p->np, lg + k, to_m, fin);
         else

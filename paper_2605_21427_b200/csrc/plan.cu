@@ -1329,6 +1329,9 @@ static int plan_build(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
             PALS_CUDA(cudaFuncSetAttribute(k_sort_chunks<1024>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)sort_smem_bytes(1024)));
+            PALS_CUDA(cudaFuncSetAttribute(k_sort_chunks<1024, 4>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)sort_smem_bytes(1024, 4)));
         }
         const char* ipt = getenv("PALS_SORT_IPT");
         // measured on B200 (cfg2): 4 keys x 512 threads sorts a 2,048-key chunk in 15 us
@@ -1503,6 +1506,9 @@ static int prep_head(pals_plan* p, int32_t* counts_reset = nullptr) {
     else if (p->sort_ipt == 4 && p->chunk == 2048)  // 4 keys per thread, 512 threads
         e = launch_k(k_sort_chunks<512, 4>, gs, 512, sort_smem_bytes(512, 4), s, pdl, d, p->gk,
                      done, counts_reset, sort_to_merged, sort_final);
+    else if (p->sort_ipt == 4 && p->chunk == 4096)  // 4 keys per thread, 1,024 threads
+        e = launch_k(k_sort_chunks<1024, 4>, gs, 1024, sort_smem_bytes(1024, 4), s, pdl, d,
+                     p->gk, done, counts_reset, sort_to_merged, sort_final);
     else switch (p->chunk) {
 #define PALS_SORT(TPB)                                                                         \
     case TPB * kIPT:                                                                           \

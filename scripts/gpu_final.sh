@@ -11,7 +11,7 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/b
 PALS_BENCH_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 3 --warmup 3 --traces 50000 --predictions 1048576 --cfg3-queries 100000 --cfg5-traces 200000 > gpurun_out/bench_2rank_gloo.json 2> gpurun_out/bench_2rank.err; echo "rc=$?" >> gpurun_out/bench_2rank.err
 SMALL="--steps 2 --warmup 1 --traces 100000 --predictions 4194304 --cfg3-queries 100000 --cfg5-traces 0 --sim-seeds 0 --no-cpu-baseline"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py $SMALL > gpurun_out/b_ncu.log 2>&1
-for k in "k_scan\\(" "k_sort_chunks<\\(int\\)256>" "k_merge_round<\\(int\\)128>" k_forest_eval_aos k_assign_qprep k_allocate k_front_scan k_finalize; do
+for k in "k_scan\\(" "k_sort_chunks<\\(int\\)512, \\(int\\)4>" "k_merge_round<\\(int\\)512, \\(int\\)2>" k_forest_eval_aos k_assign_qprep k_allocate k_front_scan k_finalize; do
   n=${k%%[<\\]*}
   timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$k" -s 2 -c 1 -o gpurun_out/prof_$n python bench.py $SMALL > gpurun_out/ncu_$n.log 2>&1
 done

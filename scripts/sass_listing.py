@@ -14,7 +14,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_2605_21427_b200", "libpals_gpu.so")
 KEEP = ["k_scanIj", "k_replayILi6", "k_forest_eval_aos", "k_allocateILb0", "k_eval_analyticE",
-        "k_merge_roundILi128", "k_sort_chunksILi256", "k_assign_qprep", "k_front_group",
+        "k_merge_roundILi512ELi2", "k_sort_chunksILi512ELi4", "k_assign_qprep", "k_front_group",
         "k_front_scan", "k_finalize", "k_build_tables", "k_alloc_steps", "k_one", "5k_simE"]
 GROUPS = {
     "fp64": r"^(DFMA|DMUL|DADD|DSETP|DMNMX|F2F\.F64|I2F\.F64|F2I\.F64|MUFU\.RCP64H|MUFU\.RSQ64H)",

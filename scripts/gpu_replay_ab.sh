@@ -1,6 +1,7 @@
-# replay parity tests + the replay legs of the bench (everything else shrunk)
+# replay change: replay parity suite + the bench's replay legs
 set -x
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_control.py tests/test_gpu_replay_warp.py tests/test_gpu_edge.py tests/test_gpu_random.py tests/test_decisions.py -q -m gpu -p no:cacheprovider > gpurun_out/pytest_replay.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_replay.log
-timeout 900 python bench.py --steps 5 --warmup 3 --cfg3-queries 10000 --cfg5-traces 0 --sim-seeds 0 --predictions 1048576 --clusters 10000 --no-cpu-baseline > gpurun_out/bench_replay.json 2> gpurun_out/bench_replay.err; echo "bench rc=$?" >> gpurun_out/bench_replay.err
+timeout 900 python -m pytest tests/test_gpu_control.py tests/test_decisions.py tests/test_gpu_replay_warp.py tests/test_gpu_adapter.py -q -m gpu --timeout 400 -p no:cacheprovider -x > gpurun_out/pytest_r.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_r.log
+B="--steps 5 --warmup 3 --predictions 1048576 --cfg3-queries 10000 --sim-seeds 0 --cfg5-traces 0 --no-cpu-baseline"
+timeout 600 python bench.py $B > gpurun_out/bench_r.json 2> gpurun_out/bench_r.err

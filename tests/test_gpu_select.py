@@ -160,7 +160,7 @@ def test_select_one_and_errors(ctx, bundle):
         select_config(other, make_targets(100.0), m, coeffs)
 
 
-@pytest.mark.parametrize("nq", [3000, 300_000])
+@pytest.mark.parametrize("nq", [3000, 300_001])
 def test_select_pinned_buffers_graph_path(ctx, oracle, nq):
     """pals_select with pinned host buffers runs one graph holding the upload (overlapped
     with the prepare; in chunks pipelined behind their scans for large batches) and

@@ -204,7 +204,11 @@ def run_ours(args, dist: Dist):
     from paper_2605_21427_b200.wattserve import (AnalyticModel, Context, Grid, Plan,
                                                  measure_peaks, replay, replay_device)
 
-    dev = dist.local % max(1, torch.cuda.device_count())  # ranks may share a GPU (gloo CI)
+    ndev = torch.cuda.device_count()
+    if dist.world > ndev and os.environ.get("PALS_BENCH_BACKEND") != "gloo":
+        sys.exit(f"bench.py: {dist.world} ranks but {ndev} visible GPUs (one rank per GPU; "
+                 "PALS_BENCH_BACKEND=gloo lets CI ranks share one)")
+    dev = dist.local % max(1, ndev)  # ranks share a GPU only under the gloo CI override
     torch.cuda.set_device(dev)
     dist.init("nccl")
     # a real (non-legacy-default) stream shared by torch and libpals_gpu, so the CUDA
@@ -493,8 +497,8 @@ def run_ours(args, dist: Dist):
 
     out = {
         "metric": METRIC, "value": value, "unit": "config evals/s",
-        "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "n_gpus": dist.world, "gpus_requested": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": SELECT_WORKLOAD, "queries_per_gpu": nq, "configs": n_cfg,
                    "scanned_queries_per_gpu": scanned_q, "exact_fold_queries": exact_q,
@@ -1274,8 +1278,29 @@ def run_reference(args, dist: Dist):
     print(json.dumps(out), flush=True)
 
 
+def spawn_ranks(args):
+    """`--gpus N` without a torchrun environment: launch the N ranks here (one process
+    per GPU, torchrun rendezvous on 127.0.0.1) instead of silently measuring one GPU."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
 def main():
     args = parse()
+    if args.gpus < 1:
+        sys.exit("bench.py: --gpus must be >= 1")
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and args.gpus > 1:
+        spawn_ranks(args)  # does not return
+    if world is not None and int(world) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU")
     dist = Dist()
     if args.impl == "reference":
         run_reference(args, dist)

@@ -851,7 +851,11 @@ __device__ __forceinline__ void qprep_body(const PlanDev& d, const SelArgs& a, i
                 Kp = (uint32_t)count_prefix(d.merged[ORD_P], ORD_P, d.n, samp_p, ns, S,
                                             [&](double p) { return p <= budget; });
             }
-            if (a.force_exact || d.globals[2]) c = CLS_X;
+            // Kt as a prefix count needs !(t*bias < target) to be monotone along the
+            // descending t order, i.e. bias >= 0 (or NaN: true everywhere); a negative
+            // bias makes the feasible set a suffix, so such queries take the literal fold
+            if (a.force_exact || d.globals[2] || (q.objective == PALS_OBJ_QOS && q.bias < 0.0))
+                c = CLS_X;
             else if (q.objective == PALS_OBJ_QOS && !bset) c = Kt ? CLS_A : CLS_D;
             else if (q.objective == PALS_OBJ_QOS) c = (Kp == 0) ? CLS_D : (Kt ? CLS_B : CLS_C);
             else c = (bset && Kp) ? CLS_C : CLS_D;
@@ -1565,6 +1569,7 @@ static int prep_tail(pals_plan* p) {
 
 int pals_plan_prepare(pals_plan* p) {
     if (p->err) return set_error(p->err, p->err_msg);
+    PALS_CUDA(cudaSetDevice(p->ctx->device));
     int rc = prep_head(p);
     return rc ? rc : prep_tail(p);
 }
@@ -1672,6 +1677,7 @@ int pals_plan_select_device(pals_plan* p, const pals_query* d_queries, int64_t n
     if (p->err) return set_error(p->err, p->err_msg);
     if (nq <= 0) return PALS_OK;
     if (nq > ((int64_t)1 << 31) - 1) return set_error(PALS_ECONFIG, "pals_select: too many queries");
+    PALS_CUDA(cudaSetDevice(p->ctx->device));
     int rc = ensure_query_buffers(p, nq);
     if (rc) return rc;
     const SelArgs a = make_args(p, d_queries, nq, d_idx, d_reason);
@@ -1802,6 +1808,7 @@ int pals_plan_run(pals_plan* p, const pals_query* d_queries, int64_t nq, int32_t
                   uint8_t* d_reason) {
     if (p->err) return set_error(p->err, p->err_msg);
     if (nq <= 0) return pals_plan_prepare(p);
+    PALS_CUDA(cudaSetDevice(p->ctx->device));
     return plan_step(p, d_queries, nq, d_idx, d_reason, nullptr, nullptr, nullptr);
 }
 
@@ -1870,6 +1877,7 @@ int pals_select(pals_plan* p, const pals_query* queries, int64_t nq, int32_t* id
 
 int pals_plan_scores(pals_plan* p, double* t_hat, double* p_node, double* eff) {
     if (p->err) return set_error(p->err, p->err_msg);
+    PALS_CUDA(cudaSetDevice(p->ctx->device));
     int rc = pals_plan_prepare(p);
     if (rc) return rc;
     cudaStream_t s = p->ctx->stream;
@@ -1894,15 +1902,17 @@ int64_t pals_plan_last_exact_count(const pals_plan* p) {
 }
 
 int pals_plan_stats(pals_plan* p, int64_t* c6) {
-    if (!p->counts) {
-        for (int i = 0; i < 6; ++i) c6[i] = 0;
-        return PALS_OK;
-    }
-    int32_t cnt[N_CLS + 1];
+    for (int i = 0; i < 6; ++i) c6[i] = 0;
+    if (!p->counts) return PALS_OK;
+    PALS_CUDA(cudaSetDevice(p->ctx->device));
+    // a pinned pals_select splits large batches into chunks, each with its own counters
+    // (stride kCountStride); chunks a select did not use are zeroed by it
+    int32_t cnt[kCountInts];
     PALS_CUDA(cudaMemcpyAsync(cnt, p->counts, sizeof cnt, cudaMemcpyDeviceToHost, p->ctx->stream));
     PALS_CUDA(cudaStreamSynchronize(p->ctx->stream));
-    for (int i = 0; i < 6; ++i) c6[i] = cnt[i];
-    p->last_exact = cnt[N_CLS];
+    for (int k = 0; k < kMaxChunks; ++k)
+        for (int i = 0; i < 6; ++i) c6[i] += cnt[kCountStride * k + i];
+    p->last_exact = c6[N_CLS];
     return PALS_OK;
 }
 
@@ -1931,6 +1941,7 @@ int pals_plan_set_force_exact(pals_plan* p, int force) {
 
 int pals_eval_device(pals_ctx* ctx, const pals_model* m, const pals_grid* g, double* d_T,
                      double* d_P) {
+    PALS_CUDA(cudaSetDevice(ctx->device));
     if (m->kind == MODEL_TABLE)
         return set_error(PALS_ECONFIG, "pals_eval_device: table models are scored via plans");
     if (m->kind == MODEL_FOREST)
@@ -1950,6 +1961,7 @@ int pals_eval_device(pals_ctx* ctx, const pals_model* m, const pals_grid* g, dou
 }
 
 int pals_eval(pals_ctx* ctx, const pals_model* m, const pals_grid* g, double* T, double* P) {
+    PALS_CUDA(cudaSetDevice(ctx->device));
     pals_coeffs k{1.0, 0.0};
     pals_plan* p = nullptr;
     int rc = pals_plan_create(ctx, m, g, &k, &p);

@@ -115,7 +115,9 @@ constexpr uint32_t kWordIdx = 0x000FFFFFu;
 __device__ __forceinline__ void table_select(const ReplayModelDev& m, double target, bool bset,
                                              double budget, int kp, int kt, double bias,
                                              int objective, int* idx, int* reason) {
-    if (!m.generic) {
+    // the rank tables assume a t-feasible prefix, i.e. bias >= 0 (bias_min may be negative
+    // in a caller's ControllerConfig / initial state): otherwise the literal fold
+    if (!m.generic && !(objective == PALS_OBJ_QOS && bias < 0.0)) {
         bool qos_empty = true;
         if (objective == PALS_OBJ_QOS) {
             const uint32_t w = m.m2[kt * (m.nd_p + 1) + (bset ? kp : m.nd_p)];

@@ -115,3 +115,32 @@ def test_replay_single_objective(ctx, oracle, mode):
     osumm, ologs = oracle.replay(s["profiles"], s["gpu"], s["coeffs"], s["caps"], s["batches"],
                                  s["cfg"], spec)
     assert np.array_equal(logs, ologs) and np.array_equal(summ, osumm)
+
+
+def test_select_negative_bias(ctx, reference, bundle):
+    """A negative bias makes the QoS-feasible set a suffix of the t_hat order:
+    such queries must take the literal fold and still match the reference, including a
+    non-positive target (every candidate then passes !(t*bias < target) or none does)."""
+    profs, gpu, coeffs = bundle
+    p = profs[1]
+    pts = workloads.grid_points([150.0 + 10 * i for i in range(24)], list(range(1, 33)),
+                                [p.deploy_tp], [p.deploy_ep], [p.deploy_dp])
+    plan = Plan(AnalyticModel(ctx, p, gpu), Grid(ctx, pts), coeffs)
+    th, _, _ = plan.scores()
+    rng = np.random.default_rng(11)
+    n = 400
+    q = np.zeros(n, abi.QUERY_DT)
+    q["throughput_tps"] = rng.uniform(-1.2, 1.0, n) * float(th.max())
+    q["bias"] = np.where(rng.uniform(size=n) < 0.7, rng.uniform(-2.0, -0.01, n),
+                         rng.uniform(0.5, 2.0, n))
+    q["target_headroom"] = 0.05
+    q["has_budget"] = rng.uniform(size=n) < 0.5
+    q["power_budget_w"] = rng.uniform(600.0, 2500.0, n)
+    q["budget_margin"] = 0.02
+    q["objective"] = (rng.uniform(size=n) < 0.2).astype(np.int32)
+    idx, rs = plan.select(q)
+    ri, rr, rc = reference.select_analytic(p, gpu, pts, coeffs, q)
+    assert rc == 0, reference.last_error()
+    assert np.array_equal(idx, ri) and np.array_equal(rs, rr)
+    neg = (q["bias"] < 0) & (q["objective"] == 0)
+    assert plan.stats()[4] >= int(neg.sum())  # routed to the literal fold

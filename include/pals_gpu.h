@@ -378,6 +378,93 @@ int pals_replay_device_ex(pals_ctx* ctx, int32_t n_models, pals_model* const* mo
                           const pals_replay_spec* spec, pals_trace_summary* d_summaries,
                           pals_step_log* d_logs, pals_step_detail* d_details);
 
+/* ---- batched controller replay over CALLER traces ---------------------- */
+/* One point of a piecewise-constant signal: the reference's budget-trace row
+ * std::pair<double,double>{t_seconds, value} (scenario_io.hpp:13-25), same layout, so a
+ * std::vector<std::pair<double,double>> can be passed as is. The signal's value at t is
+ * detail::trace_value (sim.hpp:167-174): the value of the last point of the leading run
+ * with t_s <= t, else the first point's value. */
+typedef struct {
+    double t_s;
+    double value;
+} pals_signal_point;
+
+/* NodeRuntime's actuation state (sim.hpp:155-157): the cap the breaker enforces this
+ * interval, the cap that lands next interval, the batch cap. Caps must be candidate caps
+ * and the batch cap a candidate batch. */
+typedef struct {
+    double applied_cap_w;
+    double inflight_cap_w;
+    int32_t batch_cap;
+    int32_t _pad;
+} pals_plant_state;
+
+/* One caller trace: a node of the fluid plant under caller signals.
+ * Budget: node_budget = budget signal at t0 (<= 0 or n_budget == 0: unbudgeted, as
+ * NodeRuntime::node_budget, sim.hpp:164, 198, 436). Offered load (tokens/s) = load signal
+ * at t0. measured = min(offered, dp * throughput(enforced cap, batch cap)) * noise with
+ * noise = 1 + noise_amp * (2 u - 1), u = the 53-bit uniform of
+ * splitmix64(noise_key ^ 3 << 48 ^ step) (step = the global step index; noise_amp 0: none).
+ * Targets{target_tps, node_budget if > 0, epsilon, objective} every step (sim.hpp:432-436). */
+typedef struct {
+    int64_t budget_off;    /* first point of the budget signal in the call's signal array */
+    int64_t load_off;      /* first point of the offered-load signal */
+    double target_tps;
+    double epsilon;
+    double noise_amp;
+    uint64_t noise_key;
+    int32_t n_budget;      /* points (0: never budgeted) */
+    int32_t n_load;        /* points (>= 1) */
+    int32_t model;         /* models[model] scores, plant[model] is the true system */
+    int32_t objective;     /* PALS_OBJ_* */
+} pals_trace;
+
+/* The arguments of one pals_replay_traces call. Steps are global: step k of this call is
+ * interval first_step + k, t0 = (double)(first_step + k) * interval_s, t1 = t0 + interval_s
+ * (Simulator::run, sim.hpp:229-231), so a replay split at any step and resumed from the
+ * returned states gives the same decisions as one uninterrupted call.
+ * init / init_plant: per-trace ControllerState / plant state, or NULL for the sim's start
+ * (ControllerState{} at (max cap, max batch), sim.hpp:284-288). ControllerState::current must
+ * be a candidate of the trace's model (caps x batches at its deployment tp/ep/dp).
+ * Outputs: summaries (n_traces; digest and totals cover this call's steps), final states
+ * (may be NULL), per-step logs / details of traces [0, n_log_traces) (may be NULL). */
+typedef struct {
+    int64_t n_traces;
+    int64_t first_step;
+    int32_t n_steps;
+    int32_t n_log_traces;
+    double interval_s;
+    const pals_trace* traces;
+    const pals_signal_point* signal;
+    int64_t n_signal;
+    const pals_ctrl_state* init;
+    const pals_plant_state* init_plant;
+    pals_trace_summary* summaries;
+    pals_ctrl_state* final_state;
+    pals_plant_state* final_plant;
+    pals_step_log* logs;
+    pals_step_detail* details;
+} pals_trace_batch;
+
+/* control_step (controller.hpp:210-267) replayed over caller traces: host buffers,
+ * synchronous. Invalid traces (model / objective out of range, signal offsets outside the
+ * signal array, n_load < 1, a state point that is not a candidate) fail the call with
+ * PALS_ECONFIG naming the first one. Same models / plant / candidate axes as pals_replay. */
+int pals_replay_traces(pals_ctx* ctx, int32_t n_models, pals_model* const* models,
+                       const pals_profile* plant, const pals_gpu_spec* gpu,
+                       const pals_coeffs* coeffs, const double* caps, int32_t n_caps,
+                       const int32_t* batches, int32_t n_batches, const pals_ctrl_cfg* cfg,
+                       const pals_trace_batch* batch);
+/* Same with every pointer of *batch device-resident; async on the context stream. An
+ * invalid trace gets summary.model = -1; pals_replay_traces_status() synchronises and
+ * returns the first invalid trace index of the last call on ctx (-1: none). */
+int pals_replay_traces_device(pals_ctx* ctx, int32_t n_models, pals_model* const* models,
+                              const pals_profile* plant, const pals_gpu_spec* gpu,
+                              const pals_coeffs* coeffs, const double* caps, int32_t n_caps,
+                              const int32_t* batches, int32_t n_batches,
+                              const pals_ctrl_cfg* cfg, const pals_trace_batch* batch);
+int64_t pals_replay_traces_status(pals_ctx* ctx);
+
 /* ---- decision-log wire format (metrics.hpp:145-157, csvio.hpp:17-21) -- */
 /* decisions_csv over the logged traces of a replay (host buffers from pals_replay_ex):
  * header "node,model,t_s,cap_w,batch,tp,ep,dp,applied,reason,err_norm,bias", then one

@@ -11,8 +11,8 @@
 //   analytic_scorer   controller.hpp:107-111
 //   predictor_scorer  controller.hpp:100-105 (PredictorBundle, forest.hpp:217-251)
 //   table_scorer      the TableScorer test fake, tests/test_controller.cpp:17-29
-// plus batched entry points (SelectPlan, replay) that have no single-call
-// counterpart in the reference. Also allocate_budget (allocator.hpp:76-186) over
+// plus batched entry points (SelectPlan; replay over caller traces with ControllerState
+// in and out) that have no single-call counterpart in the reference. Also allocate_budget (allocator.hpp:76-186) over
 // GpuAllocRequest nodes, build_frontier / evaluate_regime (pareto.hpp:31-59,
 // 114-135), and run_scenario / run_baseline_suite (sim.hpp:482-500) returning the
 // reference's own SimResult.
@@ -330,6 +330,146 @@ private:
     pals_grid* grid_ = nullptr;
     pals_plan* plan_ = nullptr;
 };
+
+// ---- batched control_step replay over caller traces (pals_replay_traces) ----
+// One node of the fluid plant under the caller's signals, in the
+// reference's own representations: budget / load traces are the budget-trace rows
+// std::vector<std::pair<double,double>> of scenario_io.hpp:13-25 read with
+// detail::trace_value (sim.hpp:167-174); the controller state is ControllerState
+// (controller.hpp:55-63); the actuation state is NodeRuntime's applied / inflight cap and
+// batch cap (sim.hpp:155-157); per-step records are the sim's DecisionRecord
+// (sim.hpp:122-129).
+struct ReplayTrace {
+    int model = 0;                 // index into the scorers / plant profiles
+    Targets targets;               // throughput target, epsilon, objective (budget: below)
+    std::vector<std::pair<double, double>> budget_trace;  // node watts (empty: unbudgeted)
+    std::vector<std::pair<double, double>> load_trace;    // offered tokens/s (non-empty)
+    double noise_amp = 0.0;        // measured *= 1 + amp * U(-1, 1) (pals_trace)
+    std::uint64_t noise_key = 0;
+};
+
+struct PlantState {
+    double applied_cap_w = 0.0;
+    double inflight_cap_w = 0.0;
+    int batch_cap = 0;
+};
+
+struct ReplayResult {
+    std::vector<ControllerState> states;          // final state per trace
+    std::vector<PlantState> plant;                // final actuation state per trace
+    std::vector<pals_trace_summary> summaries;    // digest, energy, tokens, applied count
+    std::vector<std::vector<DecisionRecord>> decisions;  // the first n_log_traces traces
+};
+
+// scorers[k] scores candidates caps x batches at plant[k]'s deployment tp/ep/dp
+// (build_candidates order, sim.hpp:293-308); plant[k] is the true system. init /
+// init_plant: nullptr = the sim's start, ControllerState{} at (max cap, max batch).
+// Steps are global (first_step + k), so replay(…, K, …) then replay(…, first_step = K,
+// init = &r.states, init_plant = &r.plant) equals one uninterrupted replay.
+inline ReplayResult replay(Context& ctx, const std::vector<GpuScorer>& scorers,
+                           const std::vector<ModelProfile>& plant, const GpuSpec& gpu,
+                           const SystemPowerCoeffs& coeffs, const std::vector<double>& caps,
+                           const std::vector<int>& batches, const ControllerConfig& cfg,
+                           const std::vector<ReplayTrace>& traces, int n_steps,
+                           double interval_s = 0.5, std::int64_t first_step = 0,
+                           const std::vector<ControllerState>* init = nullptr,
+                           const std::vector<PlantState>* init_plant = nullptr,
+                           int n_log_traces = 0) {
+    if (scorers.size() != plant.size())
+        throw config_error("replay: one scorer per plant profile");
+    std::vector<pals_model*> hs;
+    std::vector<pals_profile> profs;
+    for (std::size_t i = 0; i < plant.size(); ++i) {
+        hs.push_back(scorers[i].get());
+        profs.push_back(to_c(plant[i]));
+    }
+    const std::size_t n = traces.size();
+    std::vector<pals_trace> tr(n);
+    std::vector<pals_signal_point> sig;
+    for (std::size_t i = 0; i < n; ++i) {
+        const ReplayTrace& t = traces[i];
+        pals_trace& c = tr[i];
+        c.model = t.model;
+        c.objective = t.targets.objective == Objective::BudgetMaxThroughput ? PALS_OBJ_BUDGET
+                                                                            : PALS_OBJ_QOS;
+        c.target_tps = t.targets.throughput_tps;
+        c.epsilon = t.targets.epsilon;
+        c.noise_amp = t.noise_amp;
+        c.noise_key = t.noise_key;
+        c.budget_off = static_cast<int64_t>(sig.size());
+        c.n_budget = static_cast<int32_t>(t.budget_trace.size());
+        for (const auto& [ts, v] : t.budget_trace) sig.push_back(pals_signal_point{ts, v});
+        c.load_off = static_cast<int64_t>(sig.size());
+        c.n_load = static_cast<int32_t>(t.load_trace.size());
+        for (const auto& [ts, v] : t.load_trace) sig.push_back(pals_signal_point{ts, v});
+    }
+    std::vector<pals_ctrl_state> ini;
+    if (init) {
+        if (init->size() != n) throw config_error("replay: one initial state per trace");
+        for (const auto& st : *init) ini.push_back(to_c(st));
+    }
+    std::vector<pals_plant_state> inp;
+    if (init_plant) {
+        if (init_plant->size() != n) throw config_error("replay: one plant state per trace");
+        for (const auto& ps : *init_plant)
+            inp.push_back(pals_plant_state{ps.applied_cap_w, ps.inflight_cap_w, ps.batch_cap, 0});
+    }
+    const int nl = static_cast<int>(std::min<std::size_t>(std::max(n_log_traces, 0), n));
+    ReplayResult r;
+    r.summaries.resize(n);
+    std::vector<pals_ctrl_state> fin(n);
+    std::vector<pals_plant_state> finp(n);
+    std::vector<pals_step_log> logs(static_cast<std::size_t>(nl) * n_steps);
+    std::vector<pals_step_detail> det(logs.size());
+    pals_trace_batch b{};
+    b.n_traces = static_cast<int64_t>(n);
+    b.first_step = first_step;
+    b.n_steps = n_steps;
+    b.n_log_traces = nl;
+    b.interval_s = interval_s;
+    b.traces = tr.data();
+    b.signal = sig.data();
+    b.n_signal = static_cast<int64_t>(sig.size());
+    b.init = init ? ini.data() : nullptr;
+    b.init_plant = init_plant ? inp.data() : nullptr;
+    b.summaries = r.summaries.data();
+    b.final_state = fin.data();
+    b.final_plant = finp.data();
+    b.logs = nl ? logs.data() : nullptr;
+    b.details = nl ? det.data() : nullptr;
+    const pals_gpu_spec g{gpu.idle_watts, gpu.min_cap_watts, gpu.max_cap_watts, gpu.max_frequency};
+    const pals_coeffs k{coeffs.alpha, coeffs.beta_watts};
+    const pals_ctrl_cfg c = to_c(cfg);
+    check(pals_replay_traces(ctx.get(), static_cast<int32_t>(hs.size()), hs.data(), profs.data(),
+                             &g, &k, caps.data(), static_cast<int32_t>(caps.size()),
+                             batches.data(), static_cast<int32_t>(batches.size()), &c, &b));
+    r.states.reserve(n);
+    r.plant.reserve(n);
+    for (std::size_t i = 0; i < n; ++i) {
+        r.states.push_back(from_c(fin[i]));
+        r.plant.push_back(PlantState{finp[i].applied_cap_w, finp[i].inflight_cap_w, finp[i].batch_cap});
+    }
+    r.decisions.resize(nl);
+    const int nb = static_cast<int>(batches.size());
+    for (int i = 0; i < nl; ++i) {
+        const ModelProfile& pm = plant[static_cast<std::size_t>(tr[i].model)];
+        for (int s = 0; s < n_steps; ++s) {
+            const pals_step_log& lg = logs[static_cast<std::size_t>(i) * n_steps + s];
+            const pals_step_detail& dt = det[static_cast<std::size_t>(i) * n_steps + s];
+            DecisionRecord d;
+            d.t_s = static_cast<double>(first_step + s) * interval_s + interval_s;
+            d.point = OperatingPoint{caps[static_cast<std::size_t>(lg.idx / nb)],
+                                     batches[static_cast<std::size_t>(lg.idx % nb)],
+                                     pm.deployment.tp, pm.deployment.ep, pm.deployment.dp};
+            d.applied = lg.applied != 0;
+            d.reason = static_cast<DecisionReason>(lg.reason);
+            d.err_norm = dt.err_norm;
+            d.bias = dt.bias;
+            r.decisions[static_cast<std::size_t>(i)].push_back(d);
+        }
+    }
+    return r;
+}
 
 // AllocRequest (allocator.hpp:13-19) with a device scorer.
 struct GpuAllocRequest {

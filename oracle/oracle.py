@@ -16,10 +16,11 @@ import subprocess
 
 import numpy as np
 
-from paper_2605_21427_b200.abi import (POINT_DT, QUERY_DT, STEPDETAIL_DT, STEPLOG_DT,
-                                       SUMMARY_DT, Coeffs,
+from paper_2605_21427_b200.abi import (PLANT_DT, POINT_DT, QUERY_DT, SIGNAL_DT, STATE_DT,
+                                       STEPDETAIL_DT, STEPLOG_DT, SUMMARY_DT, TRACE_DT, Coeffs,
                                        CtrlCfg, CtrlState, Decision, GpuSpec, Profile,
-                                       ReplaySpec, Targets, Telemetry, ptr)
+                                       ReplaySpec, Targets, Telemetry, TraceBatch, ptr,
+                                       state_array)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "liboracle.so")
@@ -192,6 +193,8 @@ class Reference:
         L.ref_bench_replay.restype = C.c_double
         L.ref_bench_replay.argtypes = [C.c_int, _VP, _VP, _VP, _VP, C.c_int, _VP, C.c_int, _VP,
                                        _VP, C.c_int, _VP]
+        L.ref_replay_traces.argtypes = [C.c_int, _VP, _VP, _VP, _VP, C.c_int, _VP, C.c_int,
+                                        _VP, _VP, C.c_int, _P(C.c_double)]
         L.ref_load_profile.argtypes = [C.c_char_p, _VP]
         L.ref_load_platform.argtypes = [C.c_char_p, _VP, _VP]
 
@@ -341,6 +344,45 @@ class Reference:
         secs = self.lib.ref_bench_select(C.byref(prof), C.byref(gpu), ptr(pts), len(pts),
                                          C.byref(coeffs), ptr(q), nq, threads, ptr(idx), ptr(rs))
         return secs, idx, rs
+
+    def replay_traces(self, plant, gpu, coeffs, caps, batches, cfg, traces, signal, n_steps,
+                      interval_s=0.5, first_step=0, init=None, init_plant=None,
+                      n_log_traces=0, details=False, threads=1):
+        """The unmodified control_step over caller traces (the pals_replay_traces
+        contract; see replay_trace_one in ref_harness.cpp). Returns (dict, seconds)."""
+        profs = (Profile * len(plant))(*plant)
+        caps = np.ascontiguousarray(caps, np.float64)
+        batches = np.ascontiguousarray(batches, np.int32)
+        tr = np.ascontiguousarray(traces, TRACE_DT)
+        sig = np.ascontiguousarray(signal, SIGNAL_DT)
+        n = len(tr)
+        ini = None if init is None else state_array(init)
+        inp = None if init_plant is None else np.ascontiguousarray(init_plant, PLANT_DT)
+        summ = np.zeros(max(n, 1), SUMMARY_DT)
+        fin = np.zeros(max(n, 1), STATE_DT)
+        finp = np.zeros(max(n, 1), PLANT_DT)
+        nl = min(max(n_log_traces, 0), n)
+        logs = np.zeros(max(1, nl * n_steps), STEPLOG_DT)
+        det = np.zeros(max(1, nl * n_steps), STEPDETAIL_DT)
+        b = TraceBatch(n_traces=n, first_step=first_step, n_steps=n_steps, n_log_traces=nl,
+                       interval_s=interval_s, traces=ptr(tr).value if n else None,
+                       signal=ptr(sig).value if len(sig) else None, n_signal=len(sig),
+                       init=None if ini is None else ptr(ini).value,
+                       init_plant=None if inp is None else ptr(inp).value,
+                       summaries=ptr(summ).value, final_state=ptr(fin).value,
+                       final_plant=ptr(finp).value, logs=ptr(logs).value if nl else None,
+                       details=ptr(det).value if (nl and details) else None)
+        secs = C.c_double(0.0)
+        rc = self.lib.ref_replay_traces(len(plant), profs, C.byref(gpu), C.byref(coeffs),
+                                        ptr(caps), len(caps), ptr(batches), len(batches),
+                                        C.byref(cfg), C.byref(b), threads, C.byref(secs))
+        if rc:
+            raise RuntimeError(f"ref_replay_traces rc={rc}: {self.last_error()}")
+        out = {"summaries": summ[:n], "final_state": fin[:n], "final_plant": finp[:n],
+               "logs": logs[: nl * n_steps]}
+        if details:
+            out["details"] = det[: nl * n_steps]
+        return out, secs.value
 
     def bench_replay(self, plant, gpu, coeffs, caps, batches, cfg, spec, threads):
         profs = (Profile * len(plant))(*plant)

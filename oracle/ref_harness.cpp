@@ -12,6 +12,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -320,6 +321,125 @@ void replay_one(const std::vector<ReplayModel>& models, const GpuSpec& gpu,
     summary->objective = obj;
 }
 
+// The same plant under caller traces (pals_replay_traces): budget and offered load are
+// the reference's own detail::trace_value (sim.hpp:167-174) of the caller's signals at
+// t0 = (first_step + k) * interval (Simulator::run, sim.hpp:229-231); initial and final
+// ControllerState / actuation state as given.
+void replay_trace_one(const std::vector<ReplayModel>& models, const GpuSpec& gpu,
+                      const SystemPowerCoeffs& coeffs, const ControllerConfig& cfg,
+                      const pals_trace_batch& b, std::int64_t i) {
+    const pals_trace& tr = b.traces[i];
+    const ReplayModel& rm = models.at(tr.model);
+    std::vector<std::pair<double, double>> budget, load;
+    for (int j = 0; j < tr.n_budget; ++j)
+        budget.emplace_back(b.signal[tr.budget_off + j].t_s, b.signal[tr.budget_off + j].value);
+    for (int j = 0; j < tr.n_load; ++j)
+        load.emplace_back(b.signal[tr.load_off + j].t_s, b.signal[tr.load_off + j].value);
+    const OperatingPoint& first = rm.cands.front();
+    double max_cap = first.cap_watts;
+    int max_batch = first.batch;
+    for (const auto& c : rm.cands) {
+        max_cap = std::max(max_cap, c.cap_watts);
+        max_batch = std::max(max_batch, c.batch);
+    }
+    const int tp = first.tp, ep = first.ep, dp = first.dp;
+    detail::NodeRuntime n;  // only the fields enforce_cap reads
+    n.profile = &rm.profile;
+    n.cfg.tp = tp;
+    n.cfg.ep = ep;
+    n.cfg.dp = dp;
+    ControllerState st;
+    st.current = OperatingPoint{max_cap, max_batch, tp, ep, dp};
+    if (b.init) st = to_state(b.init[i]);
+    double applied_cap = max_cap, inflight_cap = max_cap;
+    int batch_cap = max_batch;
+    if (b.init_plant) {
+        applied_cap = b.init_plant[i].applied_cap_w;
+        inflight_cap = b.init_plant[i].inflight_cap_w;
+        batch_cap = b.init_plant[i].batch_cap;
+    }
+    const int obj = tr.objective;
+    std::uint64_t h = kFnvOffset;
+    double energy = 0.0, tokens = 0.0;
+    int n_applied = 0;
+    const bool logging = b.logs && i < b.n_log_traces;
+    for (int k = 0; k < b.n_steps; ++k) {
+        const std::int64_t step = b.first_step + k;
+        const double t0 = step * b.interval_s;
+        const double t1 = t0 + b.interval_s;
+        n.node_budget = budget.empty() ? 0.0 : detail::trace_value(budget, t0);
+        const int b_eff = batch_cap;
+        const double cap = detail::enforce_cap(applied_cap, b_eff, n, gpu, coeffs);
+        const OperatingPoint p{cap, b_eff, tp, ep, dp};
+        const double capacity = cluster_throughput(p, rm.profile, gpu);
+        const double gpu_w = avg_gpu_power(p, rm.profile, gpu);
+        const double sys_w = dp * (coeffs.alpha * kGpusPerNode * gpu_w + coeffs.beta_watts);
+        const double offered = detail::trace_value(load, t0);
+        const double noise =
+            1.0 + tr.noise_amp * (2.0 * u01(draw(tr.noise_key, 3, static_cast<std::uint64_t>(step))) - 1.0);
+        const double measured = std::min(offered, capacity) * noise;
+        energy += sys_w * b.interval_s;
+        tokens += measured * b.interval_s;
+        Targets targets;
+        targets.throughput_tps = tr.target_tps;
+        targets.epsilon = tr.epsilon;
+        targets.objective =
+            obj == PALS_OBJ_BUDGET ? Objective::BudgetMaxThroughput : Objective::QosMaxEfficiency;
+        if (n.node_budget > 0.0) targets.power_budget_w = n.node_budget;
+        auto [d, st2] = control_step(TelemetryInput{t1, measured}, t1, targets, rm.cands,
+                                     rm.scorer, coeffs, st, cfg);
+        st = st2;
+        const int idx = index_of(rm.cands, d.point);
+        const std::uint64_t word = (static_cast<std::uint64_t>(static_cast<std::uint32_t>(idx)) << 8) |
+                                   (static_cast<std::uint64_t>(d.applied ? 1 : 0) << 4) |
+                                   static_cast<std::uint64_t>(reason_code(d.reason));
+        h = (h ^ word) * kFnvPrime;
+        if (d.applied) ++n_applied;
+        if (logging) {
+            pals_step_log& lg = b.logs[i * b.n_steps + k];
+            lg.idx = idx;
+            lg.applied = d.applied ? 1 : 0;
+            lg.reason = static_cast<std::uint8_t>(reason_code(d.reason));
+            lg.cap_tenths = static_cast<std::uint16_t>(std::llround(cap * 10.0));
+            if (b.details) {
+                pals_step_detail& dt = b.details[i * b.n_steps + k];
+                dt.err_norm = tr.target_tps > 0.0 ? (tr.target_tps - measured) / tr.target_tps : 0.0;
+                dt.bias = st.bias;
+            }
+        }
+        applied_cap = inflight_cap;
+        if (d.applied) {
+            batch_cap = d.point.batch;
+            inflight_cap = d.point.cap_watts;
+        }
+    }
+    std::uint64_t bias_bits;
+    std::memcpy(&bias_bits, &st.bias, 8);
+    const int final_idx = index_of(rm.cands, st.current);
+    h = (h ^ bias_bits) * kFnvPrime;
+    h = (h ^ static_cast<std::uint64_t>(static_cast<std::uint32_t>(final_idx))) * kFnvPrime;
+    pals_trace_summary& sm = b.summaries[i];
+    sm.digest = h;
+    sm.final_bias = st.bias;
+    sm.energy_j = energy;
+    sm.tokens = tokens;
+    sm.n_applied = n_applied;
+    sm.final_idx = final_idx;
+    sm.model = tr.model;
+    sm.objective = obj;
+    if (b.final_state) {
+        if (b.n_steps == 0 && b.init) b.final_state[i] = b.init[i];
+        else b.final_state[i] = from_state(st);
+    }
+    if (b.final_plant) {
+        pals_plant_state ps{};
+        ps.applied_cap_w = applied_cap;
+        ps.inflight_cap_w = inflight_cap;
+        ps.batch_cap = batch_cap;
+        b.final_plant[i] = ps;
+    }
+}
+
 std::vector<ReplayModel> build_replay_models(int n_models, const pals_profile* plant,
                                              const GpuSpec& gpu, const SystemPowerCoeffs& coeffs,
                                              const double* caps, int n_caps,
@@ -623,6 +743,49 @@ double ref_bench_replay(int n_models, const pals_profile* plant, const pals_gpu_
     const auto t1 = std::chrono::steady_clock::now();
     if (failed) return -1.0;
     return std::chrono::duration<double>(t1 - t0).count();
+}
+
+// Reference control_step over caller traces (the pals_replay_traces contract), traces
+// split across n_threads; *seconds receives the wall time.
+int ref_replay_traces(int n_models, const pals_profile* plant, const pals_gpu_spec* gpu,
+                      const pals_coeffs* coeffs, const double* caps, int n_caps,
+                      const int* batches, int n_batches, const pals_ctrl_cfg* cfg,
+                      const pals_trace_batch* batch, int n_threads, double* seconds) {
+    const GpuSpec g = to_gpu(*gpu);
+    const SystemPowerCoeffs k{coeffs->alpha, coeffs->beta_watts};
+    const ControllerConfig c = to_cfg(*cfg);
+    std::atomic<int> failed{0};
+    std::string err;
+    std::mutex mu;
+    n_threads = std::max(1, n_threads);
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> th;
+    for (int t = 0; t < n_threads; ++t) {
+        th.emplace_back([&, t] {
+            try {
+                const auto models = build_replay_models(n_models, plant, g, k, caps, n_caps,
+                                                        batches, n_batches, true);
+                const std::int64_t lo = batch->n_traces * t / n_threads;
+                const std::int64_t hi = batch->n_traces * (t + 1) / n_threads;
+                for (std::int64_t i = lo; i < hi; ++i) replay_trace_one(models, g, k, c, *batch, i);
+            } catch (...) {
+                std::lock_guard<std::mutex> l(mu);
+                const int rc = map_exception();
+                if (!failed) {
+                    failed = rc;
+                    err = g_err;
+                }
+            }
+        });
+    }
+    for (auto& x : th) x.join();
+    const auto t1 = std::chrono::steady_clock::now();
+    if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+    if (failed) {
+        g_err = err;
+        return failed;
+    }
+    return PALS_OK;
 }
 
 std::uint64_t ref_splitmix64(std::uint64_t x) { return splitmix64(x); }

@@ -70,6 +70,11 @@ SIGNATURES = [
                             _VP, _VP, _VP]),
     ("pals_replay_device_ex", _I, [_VP, _I32, _VP, _VP, _VP, _VP, _VP, _I32, _VP, _I32, _VP,
                                    _VP, _VP, _VP, _VP]),
+    ("pals_replay_traces", _I, [_VP, _I32, _VP, _VP, _VP, _VP, _VP, _I32, _VP, _I32, _VP,
+                                _VP]),
+    ("pals_replay_traces_device", _I, [_VP, _I32, _VP, _VP, _VP, _VP, _VP, _I32, _VP, _I32,
+                                       _VP, _VP]),
+    ("pals_replay_traces_status", _I64, [_VP]),
     ("pals_decisions_csv", _I, [_VP, _VP, _I32, _VP, _I32, _VP, _I32, _VP, _VP, _VP, _VP, _I64,
                                 _VP]),
     ("pals_fnv1a64", C.c_uint64, [_VP, _I64]),

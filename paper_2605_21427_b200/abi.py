@@ -141,6 +141,56 @@ assert C.sizeof(Point) == POINT_DT.itemsize == 24
 assert C.sizeof(Query) == QUERY_DT.itemsize == 48
 STEPDETAIL_DT = np.dtype([("err_norm", "<f8"), ("bias", "<f8")], align=True)
 
+# ---- caller-trace replay (pals_replay_traces) ----
+# pals_signal_point = the reference's budget-trace row std::pair<double,double>{t_s, value}
+SIGNAL_DT = np.dtype([("t_s", "<f8"), ("value", "<f8")], align=True)
+# pals_trace
+TRACE_DT = np.dtype([("budget_off", "<i8"), ("load_off", "<i8"), ("target_tps", "<f8"),
+                     ("epsilon", "<f8"), ("noise_amp", "<f8"), ("noise_key", "<u8"),
+                     ("n_budget", "<i4"), ("n_load", "<i4"), ("model", "<i4"),
+                     ("objective", "<i4")], align=True)
+# pals_plant_state = NodeRuntime applied_cap / inflight_cap / batch_cap (sim.hpp:155-157)
+PLANT_DT = np.dtype([("applied_cap_w", "<f8"), ("inflight_cap_w", "<f8"),
+                     ("batch_cap", "<i4"), ("_pad", "<i4")], align=True)
+_TARGETS_DT = np.dtype([("throughput_tps", "<f8"), ("power_budget_w", "<f8"),
+                        ("epsilon", "<f8"), ("has_budget", "<i4"), ("objective", "<i4")],
+                       align=True)
+# pals_ctrl_state = ControllerState (controller.hpp:55-63), as an array element
+STATE_DT = np.dtype([("bias", "<f8"), ("integral", "<f8"), ("prev_error", "<f8"),
+                     ("current", POINT_DT), ("last_targets", _TARGETS_DT),
+                     ("has_prev_error", "<i4"), ("sustain_count", "<i4"),
+                     ("has_last_targets", "<i4"), ("_pad", "<i4")], align=True)
+
+
+class TraceBatch(C.Structure):  # pals_trace_batch
+    _fields_ = [("n_traces", C.c_int64), ("first_step", C.c_int64), ("n_steps", C.c_int32),
+                ("n_log_traces", C.c_int32), ("interval_s", C.c_double),
+                ("traces", C.c_void_p), ("signal", C.c_void_p), ("n_signal", C.c_int64),
+                ("init", C.c_void_p), ("init_plant", C.c_void_p), ("summaries", C.c_void_p),
+                ("final_state", C.c_void_p), ("final_plant", C.c_void_p), ("logs", C.c_void_p),
+                ("details", C.c_void_p)]
+
+
+assert SIGNAL_DT.itemsize == 16 and TRACE_DT.itemsize == 64 and PLANT_DT.itemsize == 24
+assert STATE_DT.itemsize == C.sizeof(CtrlState) == 96 and C.sizeof(TraceBatch) == 112
+
+
+def state_array(states) -> np.ndarray:
+    """STATE_DT array from CtrlState structs (or pass a STATE_DT array through)."""
+    if isinstance(states, np.ndarray):
+        return np.ascontiguousarray(states, STATE_DT)
+    out = np.zeros(len(states), STATE_DT)
+    C.memmove(out.ctypes.data, (CtrlState * len(states))(*states), out.nbytes)
+    return out
+
+
+def state_struct(row) -> CtrlState:
+    """CtrlState from one STATE_DT element."""
+    s = CtrlState()
+    C.memmove(C.addressof(s), np.ascontiguousarray(row).ctypes.data, C.sizeof(s))
+    return s
+
+
 # ---- queue-plant scenarios (sim.hpp:47-145; pals_run_scenarios) ----
 POLICY_FIXED, POLICY_ADAPTIVE_BATCH, POLICY_ADAPTIVE_CAP, POLICY_JOINT, POLICY_ORACLE = range(5)
 POLICIES = {"fixed": 0, "adaptive-batch": 1, "adaptive-cap": 2, "joint": 3, "oracle": 4}

@@ -20,12 +20,26 @@
 namespace pals {
 
 
+// pals_replay_traces: caller traces, signals and states (device pointers)
+struct TraceArgs {
+    const pals_trace* traces;
+    const pals_signal_point* sig;
+    int64_t n_sig;
+    const pals_ctrl_state* init;        // null: ControllerState{} at (max cap, max batch)
+    const pals_plant_state* init_plant;  // null: (max cap, max cap, max batch)
+    pals_ctrl_state* fin;
+    pals_plant_state* fin_plant;
+    unsigned long long* status;          // min invalid trace index
+    int64_t first_step;
+};
+
 struct ReplayParams {
     pals_replay_spec spec;
     pals_ctrl_cfg cfg;
     double alpha, beta;
     int n_models;
     int variant;  // PALS_REPLAY_VARIANT bit 1: prefix-min breaker search (default on)
+    TraceArgs tr;
 };
 
 // ---- counter-based trace generator --------------------------
@@ -58,6 +72,41 @@ struct Seg {
 
 
 
+// A caller signal read as detail::trace_value (sim.hpp:167-174) at non-decreasing times:
+// the cursor passes every point with t_s <= t (the value of the last one passed, else the
+// first point's value). Only the next timestamp and the current value stay in registers.
+struct SigCursor {
+    const pals_signal_point* p;    // next unread point
+    const pals_signal_point* end;
+    double v, nt;
+    __device__ __forceinline__ void init(const pals_signal_point* b, int n) {
+        p = b;
+        end = b + n;
+        v = n > 0 ? b[0].value : 0.0;
+        nt = n > 0 ? b[0].t_s : 0.0;
+    }
+    __device__ __forceinline__ double at(double t) {
+        while (p < end && nt <= t) {
+            v = p->value;
+            ++p;
+            nt = p < end ? p->t_s : 0.0;
+        }
+        return v;
+    }
+};
+
+// index of a knob value in the candidate axes (first match, as build_candidates lists them)
+__device__ __forceinline__ int cap_index(const ReplayModelDev& m, double c) {
+    for (int a = 0; a < m.nc; ++a)
+        if (m.walk_c[(int64_t)a * m.L] == c) return a;
+    return -1;
+}
+__device__ __forceinline__ int batch_index(const ReplayModelDev& m, int b) {
+    for (int j = 0; j < m.nb; ++j)
+        if (m.batch[j] == b) return j;
+    return -1;
+}
+
 __device__ __forceinline__ int trace_objective(const pals_replay_spec& sp, uint64_t key) {
     return sp.objective_mode == 2 ? (int)(draw(key, 0, 0) >> 63) : sp.objective_mode;
 }
@@ -65,14 +114,16 @@ __device__ __forceinline__ int trace_objective(const pals_replay_spec& sp, uint6
 // Thread -> trace assignment that keeps warps objective-uniform: QoS traces run
 // the PID/target branch, budget traces do not, so mixing them halves SIMT
 // efficiency. Results are written by trace index, so the order is invisible.
-__global__ void k_replay_order(pals_replay_spec sp, int32_t* __restrict__ order,
-                               int32_t* __restrict__ counters) {
+__global__ void k_replay_order(pals_replay_spec sp, const pals_trace* __restrict__ traces,
+                               int32_t* __restrict__ order, int32_t* __restrict__ counters) {
     const int lane = threadIdx.x & 31;
     for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < sp.n_traces;
          i0 += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = i0 + threadIdx.x;
         int g = -1;
-        if (i < sp.n_traces) g = trace_objective(sp, splitmix64(sp.seed ^ (uint64_t)(sp.first_trace + i)));
+        if (i < sp.n_traces)
+            g = traces ? (traces[i].objective == PALS_OBJ_BUDGET ? 1 : 0)
+                       : trace_objective(sp, splitmix64(sp.seed ^ (uint64_t)(sp.first_trace + i)));
         for (int k = 0; k < 2; ++k) {
             const unsigned m = __ballot_sync(0xffffffffu, g == k);
             if (!m) continue;
@@ -93,12 +144,16 @@ __global__ void k_replay_order(pals_replay_spec sp, int32_t* __restrict__ order,
 // same scalar code, run redundantly by the 32 lanes; the lanes split what is
 // parallel inside a step: the per-step noise draws (32 steps per round), the Kt /
 // Kp searches (32-ary) and the enforce_cap walk (32 positions per round).
-template <int kMinBlocks, bool kWarp>
+// kTr: caller traces (pals_replay_traces): model, objective and target per trace, budget
+// and offered load from caller signals, initial / final controller and plant states;
+// thread layout only. Otherwise the synthetic generator of DESIGN.md §4.
+template <int kMinBlocks, bool kWarp, bool kTr>
 __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev* __restrict__ models,
                                                 ReplayParams p, const int32_t* __restrict__ order,
                                                 pals_trace_summary* __restrict__ out,
                                                 pals_step_log* __restrict__ logs,
                                                 pals_step_detail* __restrict__ details) {
+    static_assert(!(kWarp && kTr), "caller traces run in the thread layout");
     // the per-model descriptors (table pointers and plant constants read every step)
     // are copied to shared memory: LDS instead of L1-hit loads in the step loop
     extern __shared__ __align__(16) unsigned char rp_smem[];
@@ -117,15 +172,52 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
     if (slot >= sp.n_traces) return;  // warp-uniform in the warp layout
     const int64_t ti = order ? order[slot] : slot;
     const pals_ctrl_cfg& cfg = p.cfg;
-    const uint64_t key = splitmix64(sp.seed ^ (uint64_t)(sp.first_trace + ti));
-    const int mi = (int)(key % (uint64_t)p.n_models);
+
+    // ---- per-trace setup: model, objective, target, signals, initial state ----
+    uint64_t key;     // synthetic: trace key; caller traces: noise key
+    int mi, obj;
+    double target_tps, eps, noise_amp;
+    Seg bs{0, 0, 0.0};  // synthetic budget lane 1: level U(lo_frac * p_min, hi_frac * p_max)
+    Seg ls{0, 0, 0.0};  // synthetic offered-load lane 2: level U(load_lo * t_max, load_hi * t_max)
+    SigCursor bsig, lsig;  // caller budget / offered-load signals
+    bool has_bsig = false;
+    if constexpr (kTr) {
+        const pals_trace tr = p.tr.traces[ti];
+        bool ok = tr.model >= 0 && tr.model < p.n_models &&
+                  (tr.objective == PALS_OBJ_QOS || tr.objective == PALS_OBJ_BUDGET) &&
+                  tr.n_load >= 1 && tr.n_budget >= 0 && tr.load_off >= 0 && tr.budget_off >= 0 &&
+                  tr.load_off + tr.n_load <= p.tr.n_sig &&
+                  (tr.n_budget == 0 || tr.budget_off + tr.n_budget <= p.tr.n_sig);
+        mi = ok ? tr.model : 0;
+        obj = tr.objective;
+        target_tps = tr.target_tps;
+        eps = tr.epsilon;
+        noise_amp = tr.noise_amp;
+        key = tr.noise_key;
+        if (ok) {
+            lsig.init(p.tr.sig + tr.load_off, tr.n_load);
+            has_bsig = tr.n_budget > 0;
+            if (has_bsig) bsig.init(p.tr.sig + tr.budget_off, tr.n_budget);
+        }
+        if (!ok) {
+            atomicMin(p.tr.status, (unsigned long long)ti);
+            pals_trace_summary z{};
+            z.model = -1;
+            out[ti] = z;
+            return;
+        }
+    } else {
+        key = splitmix64(sp.seed ^ (uint64_t)(sp.first_trace + ti));
+        mi = (int)(key % (uint64_t)p.n_models);
+        obj = trace_objective(sp, key);
+        const double qfrac =
+            sp.qos_frac_lo + (sp.qos_frac_hi - sp.qos_frac_lo) * u01(draw(key, 0, 1));
+        target_tps = qfrac * s_models[mi].t_max;
+        eps = sp.epsilon;
+        noise_amp = sp.noise_amp;
+    }
     const ReplayModelDev& m = s_models[mi];
-    const int obj = trace_objective(sp, key);
-    const double qfrac = sp.qos_frac_lo + (sp.qos_frac_hi - sp.qos_frac_lo) * u01(draw(key, 0, 1));
-    const double target_tps = qfrac * m.t_max;
     const double target = target_tps * (1.0 + cfg.target_headroom);
-    Seg bs{0, 0, 0.0};  // budget lane 1: level U(lo_frac * p_min, hi_frac * p_max)
-    Seg ls{0, 0, 0.0};  // offered-load lane 2: level U(load_lo * t_max, load_hi * t_max)
 
     // ControllerState (controller.hpp:55-63)
     double bias = 1.0, integral = 0.0, prev_err = 0.0;
@@ -136,6 +228,43 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
     // plant (sim.hpp:155-157, 466-472); caps and batch caps are always candidate knob
     // values, tracked by their index in the caps / batches lists
     int applied_a = m.init_a, inflight_a = m.init_a, batch_b = m.init_b;
+    if constexpr (kTr) {
+        bool ok = true;
+        if (p.tr.init) {
+            const pals_ctrl_state st = p.tr.init[ti];
+            bias = st.bias;
+            integral = st.integral;
+            prev_err = st.prev_error;
+            has_prev = st.has_prev_error != 0;
+            sustain = st.sustain_count;
+            const int a = cap_index(m, st.current.cap_watts);
+            const int b = batch_index(m, st.current.batch);
+            ok = a >= 0 && b >= 0 && st.current.tp == m.tp && st.current.ep == m.ep &&
+                 st.current.dp == m.dp;
+            cur = a * m.nb + b;
+            // constraints_changed (controller.hpp:241-242) compares whole Targets; a trace's
+            // throughput target, epsilon and objective are fixed, so only the budget moves
+            const pals_targets& lt = st.last_targets;
+            has_last = st.has_last_targets && lt.throughput_tps == target_tps &&
+                       lt.epsilon == eps && lt.objective == obj;
+            last_has_budget = lt.has_budget != 0;
+            last_budget = lt.power_budget_w;
+        }
+        if (p.tr.init_plant) {
+            const pals_plant_state ps = p.tr.init_plant[ti];
+            applied_a = cap_index(m, ps.applied_cap_w);
+            inflight_a = cap_index(m, ps.inflight_cap_w);
+            batch_b = batch_index(m, ps.batch_cap);
+            ok = ok && applied_a >= 0 && inflight_a >= 0 && batch_b >= 0;
+        }
+        if (!ok) {
+            atomicMin(p.tr.status, (unsigned long long)ti);
+            pals_trace_summary z{};
+            z.model = -1;
+            out[ti] = z;
+            return;
+        }
+    }
     // enforce_cap memo (pure function of its inputs)
     int c_a = -1, c_b = -1;
     double c_nb = -1.0;
@@ -152,14 +281,22 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
     // registers live across the loop)
     const bool logging = logs && ti < sp.n_log_traces && (!kWarp || lane == 0);
     double noise_lane = 1.0;  // warp layout: noise of step (k & ~31) + lane
+    double node_budget = 0.0;
 
     for (int k = 0; k < sp.n_steps; ++k) {
-        const double t0 = (double)k * sp.interval_s;
-        const double t1 = t0 + sp.interval_s;
-        const double node_budget =
-            sp.budget_mode ? bs.at(k, key, 1, sp.seg_min, sp.seg_max, sp.budget_lo_frac, m.p_min,
-                                   sp.budget_hi_frac, m.p_max)
-                           : 0.0;
+        double t0, t1;
+        if constexpr (kTr) {
+            t0 = (double)(p.tr.first_step + k) * sp.interval_s;  // Simulator::run sim.hpp:230
+            t1 = t0 + sp.interval_s;
+            if (has_bsig) node_budget = bsig.at(t0);
+        } else {
+            t0 = (double)k * sp.interval_s;
+            t1 = t0 + sp.interval_s;
+            node_budget = sp.budget_mode ? bs.at(k, key, 1, sp.seg_min, sp.seg_max,
+                                                 sp.budget_lo_frac, m.p_min, sp.budget_hi_frac,
+                                                 m.p_max)
+                                         : 0.0;
+        }
         // b_eff = batch_cap (fluid plant: the queue always covers the batch cap)
         if (applied_a != c_a || batch_b != c_b || node_budget != c_nb) {
             // enforce_cap (sim.hpp:195-205): walk down in 5 W steps until the cluster
@@ -203,15 +340,23 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
             c_b = batch_b;
             c_nb = node_budget;
         }
-        const double offered = ls.at(k, key, 2, sp.seg_min, sp.seg_max, sp.load_lo, m.t_max,
-                                     sp.load_hi, m.t_max);
-        double noise;
-        if (kWarp) {
-            if ((k & 31) == 0 && k + lane < sp.n_steps)
-                noise_lane = 1.0 + sp.noise_amp * (2.0 * u01(draw(key, 3, (uint64_t)(k + lane))) - 1.0);
-            noise = __shfl_sync(0xffffffffu, noise_lane, k & 31);
+        double offered, noise;
+        if constexpr (kTr) {
+            offered = lsig.at(t0);
+            // noise_amp == 0 gives 1 + 0 * x = 1 exactly: the draw is skipped, not changed
+            noise = noise_amp != 0.0
+                        ? 1.0 + noise_amp * (2.0 * u01(draw(key, 3, (uint64_t)(p.tr.first_step + k))) - 1.0)
+                        : 1.0;
         } else {
-            noise = 1.0 + sp.noise_amp * (2.0 * u01(draw(key, 3, (uint64_t)k)) - 1.0);
+            offered = ls.at(k, key, 2, sp.seg_min, sp.seg_max, sp.load_lo, m.t_max, sp.load_hi,
+                            m.t_max);
+            if (kWarp) {
+                if ((k & 31) == 0 && k + lane < sp.n_steps)
+                    noise_lane = 1.0 + noise_amp * (2.0 * u01(draw(key, 3, (uint64_t)(k + lane))) - 1.0);
+                noise = __shfl_sync(0xffffffffu, noise_lane, k & 31);
+            } else {
+                noise = 1.0 + noise_amp * (2.0 * u01(draw(key, 3, (uint64_t)k)) - 1.0);
+            }
         }
         const double measured = smin(offered, capacity) * noise;
         energy += sys_w * sp.interval_s;
@@ -244,7 +389,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
             has_last = true;
             last_has_budget = bset;
             last_budget = node_budget;
-            if (fabs(err_norm) > sp.epsilon) ++sustain;
+            if (fabs(err_norm) > eps) ++sustain;
             else sustain = 0;
 
             const double budget = bset ? node_budget * (1.0 - cfg.budget_margin) : 0.0;
@@ -331,6 +476,43 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
     s.model = mi;
     s.objective = obj;
     out[ti] = s;
+    if constexpr (kTr) {
+        if (p.tr.fin) {
+            pals_ctrl_state f;
+            if (sp.n_steps == 0 && p.tr.init) {
+                f = p.tr.init[ti];
+            } else {
+                memset(&f, 0, sizeof f);
+                f.bias = bias;
+                f.integral = integral;
+                f.prev_error = prev_err;
+                f.has_prev_error = has_prev;
+                f.sustain_count = sustain;
+                f.current.cap_watts = m.walk_c[(int64_t)(cur / m.nb) * m.L];
+                f.current.batch = m.batch[cur % m.nb];
+                f.current.tp = m.tp;
+                f.current.ep = m.ep;
+                f.current.dp = m.dp;
+                f.has_last_targets = has_last;
+                if (has_last) {  // Targets of the last step (controller.hpp:243)
+                    f.last_targets.throughput_tps = target_tps;
+                    f.last_targets.has_budget = last_has_budget;
+                    f.last_targets.power_budget_w = last_has_budget ? last_budget : 0.0;
+                    f.last_targets.epsilon = eps;
+                    f.last_targets.objective = obj;
+                }
+            }
+            p.tr.fin[ti] = f;
+        }
+        if (p.tr.fin_plant) {
+            pals_plant_state f;
+            memset(&f, 0, sizeof f);
+            f.applied_cap_w = m.walk_c[(int64_t)applied_a * m.L];
+            f.inflight_cap_w = m.walk_c[(int64_t)inflight_a * m.L];
+            f.batch_cap = m.batch[batch_b];
+            p.tr.fin_plant[ti] = f;
+        }
+    }
 }
 
 // Per-model select tables from a prepared plan (single CTA; n <= kMaxReplayCands).
@@ -446,6 +628,7 @@ struct ReplayCache {
     Analytic* d_plant = nullptr;
     int32_t* d_order = nullptr;  // thread -> trace permutation (capacity order_cap) + 2 counters
     int64_t order_cap = 0;
+    unsigned long long* d_status = nullptr;  // pals_replay_traces: first invalid trace
 };
 
 void replay_cache_free(pals_ctx* ctx) {
@@ -456,6 +639,7 @@ void replay_cache_free(pals_ctx* ctx) {
     for (auto* g : rc->grids) pals_grid_destroy(g);
     for (auto* m : rc->plant_models) pals_model_destroy(m);
     cudaFree(rc->d_order);
+    cudaFree(rc->d_status);
     cudaFree(rc->d_models);
     cudaFree(rc->d_tables);
     cudaFree(rc->d_plant);
@@ -619,6 +803,7 @@ static int replay_launch(pals_ctx* ctx, ReplayCache* rc, const pals_ctrl_cfg* cf
     if (spec->n_steps < 0 || spec->seg_min < 1 || spec->seg_max < spec->seg_min)
         return set_error(PALS_ECONFIG, "pals_replay: bad spec");
     ReplayParams p;
+    memset(&p, 0, sizeof p);
     p.spec = *spec;
     p.cfg = *cfg;
     p.alpha = rc->coeffs.alpha;
@@ -642,7 +827,7 @@ static int replay_launch(pals_ctx* ctx, ReplayCache* rc, const pals_ctrl_cfg* cf
         int32_t* counters = rc->d_order + spec->n_traces;
         PALS_CUDA(cudaMemsetAsync(counters, 0, 8, ctx->stream));
         const int ob = (int)std::min<int64_t>((spec->n_traces + 255) / 256, ctx->num_sms * 8);
-        k_replay_order<<<ob, 256, 0, ctx->stream>>>(*spec, order, counters);
+        k_replay_order<<<ob, 256, 0, ctx->stream>>>(*spec, nullptr, order, counters);
         count_launch(ctx);
     }
     // measured on B200: 6 CTAs/SM (80 regs) beats the 126-register build by 1.1-1.4x on
@@ -657,24 +842,85 @@ static int replay_launch(pals_ctx* ctx, ReplayCache* rc, const pals_ctrl_cfg* cf
     const size_t msm = sizeof(ReplayModelDev) * (size_t)p.n_models;
     if (msm > 48 * 1024) {
         const int b = (int)msm;
-        PALS_CUDA(cudaFuncSetAttribute(k_replay<6, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-        PALS_CUDA(cudaFuncSetAttribute(k_replay<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-        PALS_CUDA(cudaFuncSetAttribute(k_replay<6, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-        PALS_CUDA(cudaFuncSetAttribute(k_replay<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        PALS_CUDA(cudaFuncSetAttribute(k_replay<6, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        PALS_CUDA(cudaFuncSetAttribute(k_replay<8, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        PALS_CUDA(cudaFuncSetAttribute(k_replay<6, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        PALS_CUDA(cudaFuncSetAttribute(k_replay<1, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
     }
     if (ctx->replay_layout == PALS_REPLAY_WARP) {
         const int64_t wblocks = (spec->n_traces + 3) / 4;  // 4 traces (warps) per CTA
-        k_replay<6, true><<<(unsigned)wblocks, 128, msm, ctx->stream>>>(rc->d_models, p, nullptr,
+        k_replay<6, true, false><<<(unsigned)wblocks, 128, msm, ctx->stream>>>(rc->d_models, p, nullptr,
                                                                        d_sum, d_logs, d_det);
     } else if (minb >= 8)
-        k_replay<8, false><<<(unsigned)blocks, 128, msm, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs, d_det);
+        k_replay<8, false, false><<<(unsigned)blocks, 128, msm, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs, d_det);
     else if (minb >= 6)
-        k_replay<6, false><<<(unsigned)blocks, 128, msm, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs, d_det);
+        k_replay<6, false, false><<<(unsigned)blocks, 128, msm, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs, d_det);
     else
-        k_replay<1, false><<<(unsigned)blocks, 128, msm, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs, d_det);
+        k_replay<1, false, false><<<(unsigned)blocks, 128, msm, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs, d_det);
     count_launch(ctx);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "k_replay");
+    return PALS_OK;
+}
+
+// Caller traces (pals_replay_traces_device): every pointer of b is device-resident.
+static int traces_launch(pals_ctx* ctx, ReplayCache* rc, const pals_ctrl_cfg* cfg,
+                         const pals_trace_batch& b) {
+    if (!rc->d_status) PALS_CUDA(cudaMalloc(&rc->d_status, sizeof(unsigned long long)));
+    PALS_CUDA(cudaMemsetAsync(rc->d_status, 0xFF, sizeof(unsigned long long), ctx->stream));
+    if (b.n_traces <= 0) return PALS_OK;
+    if (b.n_steps < 0 || !b.traces || !b.summaries || (b.n_signal > 0 && !b.signal))
+        return set_error(PALS_ECONFIG, "pals_replay_traces: bad batch");
+    ReplayParams p;
+    memset(&p, 0, sizeof p);
+    p.spec.n_traces = b.n_traces;
+    p.spec.n_steps = b.n_steps;
+    p.spec.interval_s = b.interval_s;
+    p.spec.n_log_traces = b.logs ? b.n_log_traces : 0;
+    p.cfg = *cfg;
+    p.alpha = rc->coeffs.alpha;
+    p.beta = rc->coeffs.beta_watts;
+    p.n_models = (int)rc->models.size();
+    p.variant = 2;
+    p.tr.traces = b.traces;
+    p.tr.sig = b.signal;
+    p.tr.n_sig = b.n_signal;
+    p.tr.init = b.init;
+    p.tr.init_plant = b.init_plant;
+    p.tr.fin = b.final_state;
+    p.tr.fin_plant = b.final_plant;
+    p.tr.status = rc->d_status;
+    p.tr.first_step = b.first_step;
+    // objective-uniform warps, as the synthetic mixed workload
+    if (rc->order_cap < b.n_traces) {
+        cudaFree(rc->d_order);
+        rc->d_order = nullptr;
+        PALS_CUDA(cudaMalloc(&rc->d_order, (size_t)(b.n_traces + 2) * 4));
+        rc->order_cap = b.n_traces;
+    }
+    int32_t* order = rc->d_order;
+    int32_t* counters = rc->d_order + b.n_traces;
+    PALS_CUDA(cudaMemsetAsync(counters, 0, 8, ctx->stream));
+    const int ob = (int)std::min<int64_t>((b.n_traces + 255) / 256, ctx->num_sms * 8);
+    k_replay_order<<<ob, 256, 0, ctx->stream>>>(p.spec, b.traces, order, counters);
+    const int ncand = (int)(rc->caps.size() * rc->batches.size());
+    const size_t msm = sizeof(ReplayModelDev) * (size_t)p.n_models;
+    if (msm > 48 * 1024) {
+        const int sz = (int)msm;
+        PALS_CUDA(cudaFuncSetAttribute(k_replay<6, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sz));
+        PALS_CUDA(cudaFuncSetAttribute(k_replay<1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sz));
+    }
+    const unsigned blocks = (unsigned)((b.n_traces + 127) / 128);
+    pals_step_detail* det = b.logs ? b.details : nullptr;
+    if (ncand <= 256)
+        k_replay<6, false, true><<<blocks, 128, msm, ctx->stream>>>(rc->d_models, p, order,
+                                                                     b.summaries, b.logs, det);
+    else
+        k_replay<1, false, true><<<blocks, 128, msm, ctx->stream>>>(rc->d_models, p, order,
+                                                                     b.summaries, b.logs, det);
+    count_launch(ctx, 2);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "k_replay (traces)");
     return PALS_OK;
 }
 
@@ -1142,6 +1388,159 @@ int pals_replay_ex(pals_ctx* ctx, int32_t n_models, pals_model* const* models,
     }
     const cudaError_t e = cudaStreamSynchronize(ctx->stream);
     if (!r && e != cudaSuccess) r = cuda_fail(e, "pals_replay");
+    return r;
+}
+
+int pals_replay_traces_device(pals_ctx* ctx, int32_t n_models, pals_model* const* models,
+                              const pals_profile* plant, const pals_gpu_spec* gpu,
+                              const pals_coeffs* coeffs, const double* caps, int32_t n_caps,
+                              const int32_t* batches, int32_t n_batches,
+                              const pals_ctrl_cfg* cfg, const pals_trace_batch* batch) {
+    if (!batch || !cfg) return set_error(PALS_ECONFIG, "pals_replay_traces: null argument");
+    PALS_CUDA(cudaSetDevice(ctx->device));
+    ReplayCache* rc = nullptr;
+    int r = replay_setup(ctx, n_models, models, plant, gpu, coeffs, caps, n_caps, batches,
+                         n_batches, &rc);
+    if (r) return r;
+    return traces_launch(ctx, rc, cfg, *batch);
+}
+
+int64_t pals_replay_traces_status(pals_ctx* ctx) {
+    auto* rc = (ReplayCache*)ctx->replay_cache;
+    if (!rc || !rc->d_status) return -1;
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return -1;
+    unsigned long long v = ~0ull;
+    if (copy_on(ctx->stream, &v, rc->d_status, sizeof v, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return -1;
+    return v == ~0ull ? -1 : (int64_t)v;
+}
+
+int pals_replay_traces(pals_ctx* ctx, int32_t n_models, pals_model* const* models,
+                       const pals_profile* plant, const pals_gpu_spec* gpu,
+                       const pals_coeffs* coeffs, const double* caps, int32_t n_caps,
+                       const int32_t* batches, int32_t n_batches, const pals_ctrl_cfg* cfg,
+                       const pals_trace_batch* batch) {
+    if (!batch || !cfg) return set_error(PALS_ECONFIG, "pals_replay_traces: null argument");
+    const pals_trace_batch& b = *batch;
+    if (b.n_traces < 0 || b.n_steps < 0 || b.n_signal < 0 || (b.n_traces > 0 && !b.traces) ||
+        (b.n_traces > 0 && !b.summaries) || (b.n_signal > 0 && !b.signal))
+        return set_error(PALS_ECONFIG, "pals_replay_traces: bad batch");
+    PALS_CUDA(cudaSetDevice(ctx->device));
+    ReplayCache* rc = nullptr;
+    int r = replay_setup(ctx, n_models, models, plant, gpu, coeffs, caps, n_caps, batches,
+                         n_batches, &rc);
+    if (r) return r;
+    // the kernel's per-trace checks, with messages (first invalid trace)
+    auto in_caps = [&](double c) {
+        for (int a = 0; a < n_caps; ++a)
+            if (caps[a] == c) return true;
+        return false;
+    };
+    auto in_batches = [&](int v) {
+        for (int j = 0; j < n_batches; ++j)
+            if (batches[j] == v) return true;
+        return false;
+    };
+    for (int64_t i = 0; i < b.n_traces; ++i) {
+        const pals_trace& t = b.traces[i];
+        auto bad = [&](const char* why) {
+            return set_error(PALS_ECONFIG, "pals_replay_traces: trace " + std::to_string(i) +
+                                               ": " + why);
+        };
+        if (t.model < 0 || t.model >= n_models) return bad("model index out of range");
+        if (t.objective != PALS_OBJ_QOS && t.objective != PALS_OBJ_BUDGET)
+            return bad("unknown objective");
+        if (t.n_load < 1) return bad("empty offered-load signal");
+        if (t.n_budget < 0 || t.load_off < 0 || t.budget_off < 0 ||
+            t.load_off + t.n_load > b.n_signal ||
+            (t.n_budget > 0 && t.budget_off + t.n_budget > b.n_signal))
+            return bad("signal outside the signal array");
+        if (b.init) {
+            const pals_point& c = b.init[i].current;
+            const pals_profile& d = plant[t.model];
+            if (!in_caps(c.cap_watts) || !in_batches(c.batch) || c.tp != d.deploy_tp ||
+                c.ep != d.deploy_ep || c.dp != d.deploy_dp)
+                return bad("ControllerState::current is not a candidate");
+        }
+        if (b.init_plant) {
+            const pals_plant_state& ps = b.init_plant[i];
+            if (!in_caps(ps.applied_cap_w) || !in_caps(ps.inflight_cap_w) ||
+                !in_batches(ps.batch_cap))
+                return bad("plant state is not on the candidate axes");
+        }
+    }
+    if (b.n_traces == 0) return PALS_OK;
+    const int64_t n = b.n_traces;
+    const int64_t nl = b.logs ? std::min<int64_t>(std::max<int32_t>(b.n_log_traces, 0), n) : 0;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off += (bytes + 255) & ~(size_t)255;
+        return o;
+    };
+    const size_t o_tr = take(n * sizeof(pals_trace));
+    const size_t o_sig = take(std::max<int64_t>(b.n_signal, 1) * sizeof(pals_signal_point));
+    const size_t o_in = b.init ? take(n * sizeof(pals_ctrl_state)) : 0;
+    const size_t o_ip = b.init_plant ? take(n * sizeof(pals_plant_state)) : 0;
+    const size_t o_sum = take(n * sizeof(pals_trace_summary));
+    const size_t o_fs = b.final_state ? take(n * sizeof(pals_ctrl_state)) : 0;
+    const size_t o_fp = b.final_plant ? take(n * sizeof(pals_plant_state)) : 0;
+    const size_t lb = (size_t)nl * b.n_steps;
+    const size_t o_lg = nl ? take(lb * sizeof(pals_step_log)) : 0;
+    const size_t o_dt = (nl && b.details) ? take(lb * sizeof(pals_step_detail)) : 0;
+    if (ctx->scratch_bytes < off) {
+        cudaFree(ctx->d_scratch);
+        ctx->d_scratch = nullptr;
+        ctx->scratch_bytes = 0;
+        PALS_CUDA(cudaMalloc(&ctx->d_scratch, off));
+        ctx->scratch_bytes = off;
+    }
+    char* d = (char*)ctx->d_scratch;
+    cudaStream_t s = ctx->stream;
+    PALS_CUDA(cudaMemcpyAsync(d + o_tr, b.traces, n * sizeof(pals_trace), cudaMemcpyHostToDevice, s));
+    if (b.n_signal > 0)
+        PALS_CUDA(cudaMemcpyAsync(d + o_sig, b.signal, b.n_signal * sizeof(pals_signal_point),
+                                  cudaMemcpyHostToDevice, s));
+    if (b.init)
+        PALS_CUDA(cudaMemcpyAsync(d + o_in, b.init, n * sizeof(pals_ctrl_state),
+                                  cudaMemcpyHostToDevice, s));
+    if (b.init_plant)
+        PALS_CUDA(cudaMemcpyAsync(d + o_ip, b.init_plant, n * sizeof(pals_plant_state),
+                                  cudaMemcpyHostToDevice, s));
+    pals_trace_batch db = b;
+    db.traces = (const pals_trace*)(d + o_tr);
+    db.signal = (const pals_signal_point*)(d + o_sig);
+    db.init = b.init ? (const pals_ctrl_state*)(d + o_in) : nullptr;
+    db.init_plant = b.init_plant ? (const pals_plant_state*)(d + o_ip) : nullptr;
+    db.summaries = (pals_trace_summary*)(d + o_sum);
+    db.final_state = b.final_state ? (pals_ctrl_state*)(d + o_fs) : nullptr;
+    db.final_plant = b.final_plant ? (pals_plant_state*)(d + o_fp) : nullptr;
+    db.n_log_traces = (int32_t)nl;
+    db.logs = nl ? (pals_step_log*)(d + o_lg) : nullptr;
+    db.details = (nl && b.details) ? (pals_step_detail*)(d + o_dt) : nullptr;
+    r = traces_launch(ctx, rc, cfg, db);
+    if (!r) {
+        cudaMemcpyAsync(b.summaries, db.summaries, n * sizeof(pals_trace_summary),
+                        cudaMemcpyDeviceToHost, s);
+        if (b.final_state)
+            cudaMemcpyAsync(b.final_state, db.final_state, n * sizeof(pals_ctrl_state),
+                            cudaMemcpyDeviceToHost, s);
+        if (b.final_plant)
+            cudaMemcpyAsync(b.final_plant, db.final_plant, n * sizeof(pals_plant_state),
+                            cudaMemcpyDeviceToHost, s);
+        if (nl) cudaMemcpyAsync(b.logs, db.logs, lb * sizeof(pals_step_log), cudaMemcpyDeviceToHost, s);
+        if (db.details)
+            cudaMemcpyAsync(b.details, db.details, lb * sizeof(pals_step_detail),
+                            cudaMemcpyDeviceToHost, s);
+    }
+    const cudaError_t e = cudaStreamSynchronize(s);
+    if (!r && e != cudaSuccess) r = cuda_fail(e, "pals_replay_traces");
+    if (!r) {
+        const int64_t bad = pals_replay_traces_status(ctx);
+        if (bad >= 0)
+            r = set_error(PALS_ECONFIG,
+                          "pals_replay_traces: trace " + std::to_string(bad) + " rejected");
+    }
     return r;
 }
 

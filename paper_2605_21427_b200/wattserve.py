@@ -21,16 +21,17 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from .abi import (OBJ_BUDGET, OBJ_QOS, POINT_DT, QUERY_DT, STEPDETAIL_DT, STEPLOG_DT,
-                  SUMMARY_DT, Coeffs, CtrlCfg, CtrlState, Decision, GpuSpec, Point, Profile,
-                  ReplaySpec, Targets, Telemetry, ptr)
+from .abi import (OBJ_BUDGET, OBJ_QOS, PLANT_DT, POINT_DT, QUERY_DT, SIGNAL_DT, STATE_DT,
+                  STEPDETAIL_DT, STEPLOG_DT, SUMMARY_DT, TRACE_DT, Coeffs, CtrlCfg, CtrlState,
+                  Decision, GpuSpec, Point, Profile, ReplaySpec, Targets, Telemetry, TraceBatch,
+                  ptr, state_array)
 from ._lib import ConfigError, DataError, OutOfRange, PalsError, check  # noqa: F401
 
 __all__ = [
     "Context", "AnalyticModel", "TableModel", "Grid", "Plan", "analytic_scorer",
     "table_scorer", "select_config", "control_step", "replay", "make_targets",
     "default_context", "Allocator", "AllocResult", "allocate_budget", "replay_with_details",
-    "decisions_csv", "fnv1a64", "ConfigError", "DataError", "OutOfRange", "PalsError",
+    "decisions_csv", "fnv1a64", "replay_traces", "replay_traces_device", "ConfigError", "DataError", "OutOfRange", "PalsError",
 ]
 
 
@@ -393,6 +394,65 @@ def replay_device(ctx: Context, models, plant, gpu: GpuSpec, coeffs: Coeffs, cap
                                      ptr(caps), len(caps), ptr(batches), len(batches),
                                      C.byref(cfg), C.byref(spec), C.c_void_p(d_summaries),
                                      C.c_void_p(d_logs)))
+
+
+def _replay_common(models, plant, caps, batches):
+    n_models = len(models)
+    hs = (C.c_void_p * n_models)(*[m.h for m in models])
+    profs = (Profile * n_models)(*plant)
+    return (n_models, hs, profs, np.ascontiguousarray(caps, np.float64),
+            np.ascontiguousarray(batches, np.int32))
+
+
+def replay_traces(ctx: Context, models, plant, gpu: GpuSpec, coeffs: Coeffs, caps, batches,
+                  cfg: CtrlCfg, traces: np.ndarray, signal: np.ndarray, n_steps: int,
+                  interval_s: float = 0.5, first_step: int = 0, init=None, init_plant=None,
+                  n_log_traces: int = 0, details: bool = False, summaries=None):
+    """control_step replayed over caller traces (pals_replay_traces; host buffers).
+
+    traces: TRACE_DT array (model, objective, target, epsilon, noise, signal slices);
+    signal: SIGNAL_DT array of (t_s, value) rows — the reference's budget-trace
+    representation, read with detail::trace_value semantics (sim.hpp:167-174).
+    init: STATE_DT array / CtrlState list or None (ControllerState{} at max cap and
+    batch); init_plant: PLANT_DT array or None. Returns a dict with summaries,
+    final_state (STATE_DT), final_plant (PLANT_DT), logs and details."""
+    n_models, hs, profs, caps, batches = _replay_common(models, plant, caps, batches)
+    tr = np.ascontiguousarray(traces, TRACE_DT)
+    sig = np.ascontiguousarray(signal, SIGNAL_DT)
+    n = len(tr)
+    ini = None if init is None else state_array(init)
+    inp = None if init_plant is None else np.ascontiguousarray(init_plant, PLANT_DT)
+    summ = np.zeros(n, SUMMARY_DT) if summaries is None else summaries
+    fin = np.zeros(n, STATE_DT)
+    finp = np.zeros(n, PLANT_DT)
+    nl = min(max(n_log_traces, 0), n)
+    logs = np.zeros(max(1, nl * n_steps), STEPLOG_DT)
+    det = np.zeros(max(1, nl * n_steps), STEPDETAIL_DT) if details else None
+    b = TraceBatch(n_traces=n, first_step=first_step, n_steps=n_steps, n_log_traces=nl,
+                   interval_s=interval_s, traces=ptr(tr).value if n else None,
+                   signal=ptr(sig).value if len(sig) else None, n_signal=len(sig),
+                   init=None if ini is None else ptr(ini).value,
+                   init_plant=None if inp is None else ptr(inp).value,
+                   summaries=ptr(summ).value if n else None, final_state=ptr(fin).value,
+                   final_plant=ptr(finp).value, logs=ptr(logs).value if nl else None,
+                   details=ptr(det).value if (nl and details) else None)
+    check(ctx.lib.pals_replay_traces(ctx.h, n_models, hs, profs, C.byref(gpu), C.byref(coeffs),
+                                     ptr(caps), len(caps), ptr(batches), len(batches),
+                                     C.byref(cfg), C.byref(b)))
+    out = {"summaries": summ[:n], "final_state": fin, "final_plant": finp,
+           "logs": logs[: nl * n_steps]}
+    if details:
+        out["details"] = det[: nl * n_steps]
+    return out
+
+
+def replay_traces_device(ctx: Context, models, plant, gpu: GpuSpec, coeffs: Coeffs, caps,
+                         batches, cfg: CtrlCfg, batch: TraceBatch):
+    """pals_replay_traces_device: every pointer of `batch` device-resident; async."""
+    n_models, hs, profs, caps, batches = _replay_common(models, plant, caps, batches)
+    check(ctx.lib.pals_replay_traces_device(ctx.h, n_models, hs, profs, C.byref(gpu),
+                                            C.byref(coeffs), ptr(caps), len(caps), ptr(batches),
+                                            len(batches), C.byref(cfg), C.byref(batch)))
 
 
 OBJECTIVES = {"qos": OBJ_QOS, "budget-throughput": OBJ_BUDGET}

@@ -17,7 +17,8 @@ from __future__ import annotations
 
 import numpy as np
 
-from .abi import OBJ_BUDGET, OBJ_QOS, POINT_DT, QUERY_DT, ReplaySpec, default_ctrl_cfg
+from .abi import (OBJ_BUDGET, OBJ_QOS, POINT_DT, QUERY_DT, SIGNAL_DT, TRACE_DT, ReplaySpec,
+                  default_ctrl_cfg)
 from .profiles import comm_of, load_bundle, profile_by_name, with_comm
 
 GOLDEN = np.uint64(0x9E3779B97F4A7C15)
@@ -133,6 +134,95 @@ def replay_spec(n_traces: int, n_steps: int = 3600, seed: int = 2605, first: int
     s.budget_mode = 1
     s.n_log_traces = n_log_traces
     return s
+
+
+def _draw(key, lane: int, ctr) -> np.ndarray:
+    """draw(key, lane, ctr) = splitmix64(key ^ lane << 48 ^ ctr)."""
+    return splitmix64(key ^ (np.uint64(lane) << np.uint64(48)) ^ np.asarray(ctr, np.uint64))
+
+
+def synthetic_traces(spec: ReplaySpec, n_models: int, t_max, p_min, p_max):
+    """The synthetic replay workload of `spec` written out as caller traces
+    for pals_replay_traces: per trace its model, objective, target and noise key, and its
+    piecewise-constant budget / offered-load segments as (t_s, value) signal rows starting
+    at step S_j (t_s = S_j * interval_s). Replaying these traces gives the synthetic path's
+    decisions bit for bit. t_max / p_min / p_max: per model, the plant's unconstrained
+    throughput and the min / max p_node over the candidates (what the generator scales by).
+    Returns (traces TRACE_DT, signal SIGNAL_DT)."""
+    n = int(spec.n_traces)
+    t_max, p_min, p_max = (np.asarray(x, np.float64) for x in (t_max, p_min, p_max))
+    gi = np.uint64(spec.first_trace) + np.arange(n, dtype=np.uint64)
+    key = splitmix64(np.uint64(spec.seed) ^ gi)
+    model = (key % np.uint64(n_models)).astype(np.int64)
+    if spec.objective_mode == 2:
+        obj = (_draw(key, 0, 0) >> np.uint64(63)).astype(np.int32)
+    else:
+        obj = np.full(n, spec.objective_mode, np.int32)
+    qfrac = spec.qos_frac_lo + (spec.qos_frac_hi - spec.qos_frac_lo) * u01(_draw(key, 0, 1))
+    span = np.uint64(spec.seg_max - spec.seg_min + 1)
+
+    def segments(lane, lo, hi):
+        """Seg::at: segment j starts at S_j = sum of earlier lengths; kept while S_j < n_steps."""
+        start = np.zeros(n, np.int64)
+        rows_t, rows_v, rows_i = [], [], []
+        act = np.arange(n)
+        j = 0
+        while len(act):
+            k = key[act]
+            ln = spec.seg_min + (_draw(k, lane, 2 * j) % span).astype(np.int64)
+            u = u01(_draw(k, lane, 2 * j + 1))
+            lvl = lo[act] + (hi[act] - lo[act]) * u
+            rows_i.append(act)
+            rows_t.append(start[act].astype(np.float64) * spec.interval_s)
+            rows_v.append(lvl)
+            start[act] += ln
+            act = act[start[act] < spec.n_steps]
+            j += 1
+        i = np.concatenate(rows_i)
+        order = np.argsort(i, kind="stable")  # per trace, in segment order
+        cnt = np.bincount(i, minlength=n)
+        return np.concatenate(rows_t)[order], np.concatenate(rows_v)[order], cnt
+
+    lt, lv, lc = segments(2, spec.load_lo * t_max[model], spec.load_hi * t_max[model])
+    if spec.budget_mode:
+        bt, bv, bc = segments(1, spec.budget_lo_frac * p_min[model],
+                              spec.budget_hi_frac * p_max[model])
+    else:
+        bt, bv, bc = np.zeros(0), np.zeros(0), np.zeros(n, np.int64)
+    signal = np.zeros(len(bt) + len(lt), SIGNAL_DT)
+    signal["t_s"][: len(bt)], signal["value"][: len(bt)] = bt, bv
+    signal["t_s"][len(bt):], signal["value"][len(bt):] = lt, lv
+    tr = np.zeros(n, TRACE_DT)
+    tr["budget_off"] = np.concatenate([[0], np.cumsum(bc)[:-1]]) if n else 0
+    tr["n_budget"] = bc
+    tr["load_off"] = len(bt) + (np.concatenate([[0], np.cumsum(lc)[:-1]]) if n else 0)
+    tr["n_load"] = lc
+    tr["target_tps"] = qfrac * t_max[model]
+    tr["epsilon"] = spec.epsilon
+    tr["noise_amp"] = spec.noise_amp
+    tr["noise_key"] = key
+    tr["model"] = model
+    tr["objective"] = obj
+    return tr, signal
+
+
+def plant_constants(ctx, plant, gpu, coeffs, caps, batches):
+    """Per model: (t_max, p_min, p_max) the synthetic generator scales by — the plant's
+    unconstrained throughput at (max cap, max batch) (sim.hpp:258-264) and the p_node range
+    over the candidates — from the library's own evaluation (pals_eval)."""
+    from .wattserve import AnalyticModel, Grid, eval_grid
+    t_max, p_min, p_max = [], [], []
+    for p in plant:
+        pts = grid_points(caps, batches, [p.deploy_tp], [p.deploy_ep], [p.deploy_dp])
+        T, P = eval_grid(AnalyticModel(ctx, p, gpu), Grid(ctx, pts))
+        dp = float(p.deploy_dp)
+        pn = dp * (coeffs.alpha * 4.0 * P + coeffs.beta_watts)
+        i = int(np.flatnonzero((pts["cap_watts"] == np.max(caps)) &
+                               (pts["batch"] == np.max(batches)))[0])
+        t_max.append(dp * T[i])
+        p_min.append(float(pn.min()))
+        p_max.append(float(pn.max()))
+    return np.array(t_max), np.array(p_min), np.array(p_max)
 
 
 def dr_candidates():

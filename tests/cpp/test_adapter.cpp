@@ -477,6 +477,138 @@ int main(int argc, char** argv) {
         EXPECT(n_sc == 15, "3 scenarios x 5 policies");
     }
 
+    // ---- gpu::replay over caller traces: the demand-response budget trace through the
+    // fluid plant, against the unmodified control_step / trace_value / enforce_cap driven
+    // by the same loop here; then a mid-trace resume from the returned states ----
+    {
+        const json all = json::parse(read_file(root + "/paper_2605_21427_b200/data/scenarios.json"));
+        std::vector<std::pair<double, double>> cluster;
+        for (const auto& tw : all.at("demand_response").at("trace"))
+            cluster.emplace_back(tw.at(0).get<double>(), tw.at(1).get<double>());
+        const std::vector<double> caps{150.0, 200.0, 250.0, 300.0, 350.0, 400.0};
+        const std::vector<int> batches{1, 4, 8, 16, 32, 64};
+        ControllerConfig cfg;
+        cfg.target_headroom = 0.05;
+        cfg.budget_margin = 0.02;
+        std::vector<gpu::GpuScorer> scorers;
+        for (const auto& p : profiles) scorers.push_back(gpu::analytic_scorer(ctx, p, gspec));
+        std::vector<gpu::ReplayTrace> traces;
+        Rng rng(31);
+        for (std::size_t m = 0; m < profiles.size(); ++m) {
+            for (int o = 0; o < 2; ++o) {
+                gpu::ReplayTrace t;
+                t.model = static_cast<int>(m);
+                const ModelProfile& pm = profiles[m];
+                const OperatingPoint top{400.0, 64, pm.deployment.tp, pm.deployment.ep,
+                                         pm.deployment.dp};
+                const double tmax = cluster_throughput(top, pm, gspec);
+                t.targets.throughput_tps = rng.uniform(0.3, 0.9) * tmax;
+                t.targets.objective = o ? Objective::BudgetMaxThroughput : Objective::QosMaxEfficiency;
+                for (const auto& [ts, w] : cluster)  // assign_budgets over 3 dp=1 nodes
+                    t.budget_trace.emplace_back(ts, w * 1.0 / 3);
+                for (int j = 0; j < 5; ++j)
+                    t.load_trace.emplace_back(720.0 * j, rng.uniform(0.3, 1.2) * tmax);
+                t.noise_amp = 0.04;
+                t.noise_key = rng.next_u64();
+                traces.push_back(t);
+            }
+        }
+        const int n_steps = 7200;
+        // the reference side: the same plant loop over wattserve's own functions
+        auto reference = [&](const gpu::ReplayTrace& t, ControllerState st, gpu::PlantState ps,
+                             std::int64_t first, int steps, std::vector<DecisionRecord>& recs) {
+            const ModelProfile& pm = profiles[static_cast<std::size_t>(t.model)];
+            std::vector<OperatingPoint> cands;
+            for (double c : caps)
+                for (int b : batches)
+                    cands.push_back(OperatingPoint{c, b, pm.deployment.tp, pm.deployment.ep,
+                                                   pm.deployment.dp});
+            const Scorer score = detail::cached(analytic_scorer(pm, gspec));
+            detail::NodeRuntime n;
+            n.profile = &pm;
+            n.cfg.tp = pm.deployment.tp;
+            n.cfg.ep = pm.deployment.ep;
+            n.cfg.dp = pm.deployment.dp;
+            for (int kk = 0; kk < steps; ++kk) {
+                const std::int64_t step = first + kk;
+                const double t0 = step * 0.5, t1 = t0 + 0.5;
+                n.node_budget = detail::trace_value(t.budget_trace, t0);
+                const double cap = detail::enforce_cap(ps.applied_cap_w, ps.batch_cap, n, gspec, k);
+                const OperatingPoint p{cap, ps.batch_cap, n.cfg.tp, n.cfg.ep, n.cfg.dp};
+                std::uint64_t x = t.noise_key ^ (std::uint64_t{3} << 48) ^ static_cast<std::uint64_t>(step);
+                const double u = static_cast<double>(splitmix64(x) >> 11) * 0x1.0p-53;
+                const double measured = std::min(detail::trace_value(t.load_trace, t0),
+                                                 cluster_throughput(p, pm, gspec)) *
+                                        (1.0 + t.noise_amp * (2.0 * u - 1.0));
+                Targets tg = t.targets;
+                if (n.node_budget > 0.0) tg.power_budget_w = n.node_budget;
+                auto [d, st2] = control_step(TelemetryInput{t1, measured}, t1, tg, cands, score, k,
+                                             st, cfg);
+                st = st2;
+                DecisionRecord r;
+                r.t_s = t1;
+                r.point = d.point;
+                r.applied = d.applied;
+                r.reason = d.reason;
+                r.err_norm = tg.throughput_tps > 0.0 ? (tg.throughput_tps - measured) / tg.throughput_tps : 0.0;
+                r.bias = st.bias;
+                recs.push_back(r);
+                ps.applied_cap_w = ps.inflight_cap_w;
+                if (d.applied) {
+                    ps.batch_cap = d.point.batch;
+                    ps.inflight_cap_w = d.point.cap_watts;
+                }
+            }
+            return std::make_pair(st, ps);
+        };
+        const int nt = static_cast<int>(traces.size());
+        const auto full = gpu::replay(ctx, scorers, profiles, gspec, k, caps, batches, cfg, traces,
+                                      n_steps, 0.5, 0, nullptr, nullptr, nt);
+        const auto part = gpu::replay(ctx, scorers, profiles, gspec, k, caps, batches, cfg, traces,
+                                      2999, 0.5, 0, nullptr, nullptr, nt);
+        const auto rest = gpu::replay(ctx, scorers, profiles, gspec, k, caps, batches, cfg, traces,
+                                      n_steps - 2999, 0.5, 2999, &part.states, &part.plant, nt);
+        auto same_rec = [](const DecisionRecord& a, const DecisionRecord& b) {
+            return same_bits(a.t_s, b.t_s) && a.point == b.point && a.applied == b.applied &&
+                   a.reason == b.reason && same_bits(a.err_norm, b.err_norm) &&
+                   same_bits(a.bias, b.bias);
+        };
+        bool ok = true, resumed = true;
+        int budget_decisions = 0;
+        for (int i = 0; i < nt; ++i) {
+            const ModelProfile& pm = profiles[static_cast<std::size_t>(traces[i].model)];
+            ControllerState st0;
+            st0.current = OperatingPoint{400.0, 64, pm.deployment.tp, pm.deployment.ep, pm.deployment.dp};
+            std::vector<DecisionRecord> recs;
+            const auto [st, ps] = reference(traces[i], st0, gpu::PlantState{400.0, 400.0, 64}, 0,
+                                            n_steps, recs);
+            ok = ok && same(full.states[i], st) && full.plant[i].applied_cap_w == ps.applied_cap_w &&
+                 full.plant[i].inflight_cap_w == ps.inflight_cap_w &&
+                 full.plant[i].batch_cap == ps.batch_cap && full.decisions[i].size() == recs.size();
+            for (std::size_t s2 = 0; ok && s2 < recs.size(); ++s2) {
+                ok = same_rec(full.decisions[i][s2], recs[s2]);
+                budget_decisions += recs[s2].reason == DecisionReason::BudgetConstrainedMaxThroughput;
+            }
+            resumed = resumed && same(rest.states[i], st);
+            for (std::size_t s2 = 0; resumed && s2 < recs.size(); ++s2)
+                resumed = same_rec(s2 < 2999 ? part.decisions[i][s2] : rest.decisions[i][s2 - 2999],
+                                   recs[s2]);
+        }
+        EXPECT(ok, "gpu::replay == control_step over the demand-response trace (7,200 steps)");
+        EXPECT(resumed, "gpu::replay resumed at step 2999 from its own states");
+        EXPECT(budget_decisions > 0, "the budget trace bound some decisions");
+        bool threw = false;
+        try {
+            std::vector<ControllerState> bad(traces.size());
+            for (auto& b2 : bad) b2.current.cap_watts = 123.0;  // not a candidate cap
+            gpu::replay(ctx, scorers, profiles, gspec, k, caps, batches, cfg, traces, 10, 0.5, 0,
+                        &bad);
+        } catch (const config_error& e) {
+            threw = std::string(e.what()).find("not a candidate") != std::string::npos;
+        }
+        EXPECT(threw, "replay: a non-candidate ControllerState::current throws config_error");
+    }
+
     std::printf("%s: %d checks, %d failures\n", g_fail ? "FAIL" : "PASS", g_checks, g_fail);
     return g_fail > 255 ? 255 : g_fail;
 }

@@ -398,6 +398,8 @@ def run_ours(args, dist: Dist):
     # the same cfg4 traces through the warp-per-trace layout, and both layouts on the
     # demand-response scenario's 1,464-candidate grid (SURVEY §8(d) cfg4 variants)
     layouts = replay_layouts(args, dist, ctx, stream, l2_flush, models, s, spec, dec_value)
+    args._synthetic_dec_value = dec_value
+    traces_leg = bench_traces(args, dist, ctx, stream, l2_flush, models, s, spec, d_sum)
     # FP64 work per decision in the replay kernel: PID 15 flops (2 div),
     # plant noise/min/energy/tokens 10, target test + Kt search ~2*log2(nd_t)+4
     fp64_per_dec = 40.0
@@ -519,7 +521,8 @@ def run_ours(args, dist: Dist):
             "e2e": {"value": dec_e2e, "unit": "decisions/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": nt * SUMMARY_DT.itemsize,
                     "api": "pals_replay (C ABI, host summaries)"},
-            "roofline": dec_roof, "gpu_launches": int(rlaunches), "layouts": layouts},
+            "roofline": dec_roof, "gpu_launches": int(rlaunches), "layouts": layouts,
+            "caller_traces": traces_leg},
         "predictions": predictions,
         "allocations": allocations,
         "frontiers": frontiers,
@@ -587,6 +590,105 @@ def replay_layouts(args, dist, ctx, stream, l2_flush, models, s, spec, thread_va
     out["dr_warp_per_trace"] = timed(caps, batches, dspec, "warp", 1)
     out["unit"] = "decisions/s"
     return out
+
+
+def bench_traces(args, dist, ctx, stream, l2_flush, models, s, spec, d_synth):
+    """cfg4 through the caller-trace boundary (pals_replay_traces): the same 1e6 traces,
+    written out as caller budget / load signals (446 MB of (t_s, value) rows + 64 B per
+    trace), device-resident for `value`; `e2e` from pinned host buffers through the host
+    call, which also returns every final ControllerState and plant state. Parity: every
+    trace summary equals the synthetic path's (d_synth) bit for bit."""
+    import torch
+    from paper_2605_21427_b200 import workloads
+    from paper_2605_21427_b200.abi import (PLANT_DT, SIGNAL_DT, STATE_DT, SUMMARY_DT, TRACE_DT,
+                                           TraceBatch)
+    from paper_2605_21427_b200.wattserve import replay_traces_device
+    consts = workloads.plant_constants(ctx, s["profiles"], s["gpu"], s["coeffs"], s["caps"],
+                                       s["batches"])
+    tr, sig = workloads.synthetic_traces(spec, len(models), *consts)
+    nt = len(tr)
+    d_tr = torch.from_numpy(tr.view(np.uint8)).cuda()
+    d_sig = torch.from_numpy(sig.view(np.uint8)).cuda()
+    d_sum = torch.empty(nt * SUMMARY_DT.itemsize, dtype=torch.uint8, device="cuda")
+    d_fin = torch.empty(nt * STATE_DT.itemsize, dtype=torch.uint8, device="cuda")
+    d_finp = torch.empty(nt * PLANT_DT.itemsize, dtype=torch.uint8, device="cuda")
+    b = TraceBatch(n_traces=nt, first_step=0, n_steps=spec.n_steps, n_log_traces=0,
+                   interval_s=spec.interval_s, traces=d_tr.data_ptr(), signal=d_sig.data_ptr(),
+                   n_signal=len(sig), init=None, init_plant=None, summaries=d_sum.data_ptr(),
+                   final_state=d_fin.data_ptr(), final_plant=d_finp.data_ptr(), logs=None,
+                   details=None)
+    run = lambda: replay_traces_device(ctx, models, s["profiles"], s["gpu"], s["coeffs"],  # noqa
+                                       s["caps"], s["batches"], s["cfg"], b)
+    run()
+    torch.cuda.synchronize()
+    reps = max(1, min(args.steps, 3))
+    dist.barrier()
+    ms = []
+    for _ in range(reps):
+        l2_flush()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    t = dist.max(float(np.sum(ms)))
+    value = dist.sum(float(nt) * spec.n_steps) * reps / (t * 1e-3)
+    mism = int((d_sum != d_synth).view(nt, SUMMARY_DT.itemsize).any(1).sum().item())
+    # e2e: pinned host traces / signals in, summaries + final states out, host call
+    h_tr = torch.empty(tr.nbytes, dtype=torch.uint8, pin_memory=True)
+    h_tr.numpy()[:] = tr.view(np.uint8)
+    h_sig = torch.empty(sig.nbytes, dtype=torch.uint8, pin_memory=True)
+    h_sig.numpy()[:] = sig.view(np.uint8)
+    h_sum = torch.empty(nt * SUMMARY_DT.itemsize, dtype=torch.uint8, pin_memory=True)
+    h_fin = torch.empty(nt * STATE_DT.itemsize, dtype=torch.uint8, pin_memory=True)
+    h_finp = torch.empty(nt * PLANT_DT.itemsize, dtype=torch.uint8, pin_memory=True)
+    hb = TraceBatch(n_traces=nt, first_step=0, n_steps=spec.n_steps, n_log_traces=0,
+                    interval_s=spec.interval_s, traces=h_tr.data_ptr(), signal=h_sig.data_ptr(),
+                    n_signal=len(sig), init=None, init_plant=None, summaries=h_sum.data_ptr(),
+                    final_state=h_fin.data_ptr(), final_plant=h_finp.data_ptr(), logs=None,
+                    details=None)
+    import ctypes as C
+    from paper_2605_21427_b200.wattserve import _replay_common
+    n_models, hs, profs, caps, batches = _replay_common(models, s["profiles"], s["caps"],
+                                                        s["batches"])
+    lib = ctx.lib
+
+    def e2e():
+        rc = lib.pals_replay_traces(ctx.h, n_models, hs, profs, C.byref(s["gpu"]),
+                                    C.byref(s["coeffs"]), caps.ctypes.data, len(caps),
+                                    batches.ctypes.data, len(batches), C.byref(s["cfg"]),
+                                    C.byref(hb))
+        assert rc == 0, lib.pals_last_error()
+
+    e2e()
+    e2e_ms = []
+    for _ in range(reps):
+        l2_flush()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        e2e()
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    te = dist.max(float(np.mean(e2e_ms)))
+    e2e_value = dist.sum(float(nt) * spec.n_steps) / (te * 1e-3)
+    mism_e2e = int((h_sum.cuda() != d_synth).view(nt, SUMMARY_DT.itemsize).any(1).sum().item())
+    return {"metric": "controller decisions/s over caller traces (pals_replay_traces)",
+            "value": value, "unit": "decisions/s", "ms_per_step": t / reps,
+            "workload": f"the cfg4 traces ({nt} per GPU x {spec.n_steps} steps) as caller "
+                        f"signals: {len(sig)} (t_s, value) rows, {sig.nbytes + tr.nbytes} B",
+            "e2e": {"value": e2e_value, "unit": "decisions/s",
+                    "h2d_bytes_per_step": int(tr.nbytes + sig.nbytes),
+                    "d2h_bytes_per_step": int(nt * (SUMMARY_DT.itemsize + STATE_DT.itemsize +
+                                                    PLANT_DT.itemsize)),
+                    "api": "pals_replay_traces (C ABI, pinned host traces in; summaries, "
+                           "ControllerStates and plant states out)"},
+            "vs_synthetic_path": value / max(1.0, float(args._synthetic_dec_value)),
+            "parity": {"checked": nt, "mismatches": mism + mism_e2e,
+                       "against": "the synthetic replay of the same traces (k_replay, "
+                                  "itself checked against oracle/_ref)"}}
 
 
 def alloc_setup_gpu(ctx):

@@ -465,6 +465,50 @@ int pals_replay_traces_device(pals_ctx* ctx, int32_t n_models, pals_model* const
                               const pals_ctrl_cfg* cfg, const pals_trace_batch* batch);
 int64_t pals_replay_traces_status(pals_ctx* ctx);
 
+/* ---- multi-GPU driver: one host thread and one context per device ------ */
+/* The reference steps nodes one after another in one thread (sim.hpp:243-244); queries
+ * and traces are independent, so here they are split into contiguous shards, one per
+ * device, each run by that device's own worker thread on its own context and stream.
+ * Nothing crosses devices until the results: by default every shard lands straight in
+ * the caller's host buffer from its own device; with pals_multi_set_gather(m, 1) the
+ * shards are first gathered into device 0 (cudaMemcpyPeerAsync over NVLink) and read
+ * back from there in one copy. A device may be listed more than once (two contexts on
+ * one GPU: the N>1 path on a single-GPU box). Results equal the one-context call's
+ * byte for byte. */
+typedef struct pals_multi pals_multi;
+int pals_multi_create(const int32_t* devices, int32_t n_devices, pals_multi** out);
+int pals_multi_destroy(pals_multi* m);
+int32_t pals_multi_size(const pals_multi* m);
+/* The context of rank r (its device, stream and launch counter). */
+pals_ctx* pals_multi_ctx(pals_multi* m, int32_t rank);
+int pals_multi_set_gather(pals_multi* m, int32_t to_device0);
+/* A scorer replicated on every device: pals_model_analytic / _table on each context.
+ * *id indexes m's models. */
+int pals_multi_model_analytic(pals_multi* m, const pals_profile* profile,
+                              const pals_gpu_spec* gpu, int32_t* id);
+int pals_multi_model_table(pals_multi* m, const pals_point* points, const double* throughput_tps,
+                           const double* gpu_power_w, int64_t n, int32_t* id);
+/* select_config for n queries over one candidate list (pals_select, sharded). */
+int pals_multi_select(pals_multi* m, int32_t model, const pals_point* points, int64_t n_points,
+                      const pals_coeffs* coeffs, const pals_query* queries, int64_t n,
+                      int32_t* index, uint8_t* reason);
+/* pals_replay_ex over spec's traces (models[k] = ids from pals_multi_model_*). */
+int pals_multi_replay(pals_multi* m, int32_t n_models, const int32_t* models,
+                      const pals_profile* plant, const pals_gpu_spec* gpu,
+                      const pals_coeffs* coeffs, const double* caps, int32_t n_caps,
+                      const int32_t* batches, int32_t n_batches, const pals_ctrl_cfg* cfg,
+                      const pals_replay_spec* spec, pals_trace_summary* summaries,
+                      pals_step_log* logs, pals_step_detail* details);
+/* pals_replay_traces over batch's traces (host buffers; the signal array is shared). */
+int pals_multi_replay_traces(pals_multi* m, int32_t n_models, const int32_t* models,
+                             const pals_profile* plant, const pals_gpu_spec* gpu,
+                             const pals_coeffs* coeffs, const double* caps, int32_t n_caps,
+                             const int32_t* batches, int32_t n_batches,
+                             const pals_ctrl_cfg* cfg, const pals_trace_batch* batch);
+/* Device milliseconds of each rank's part of the last call (CUDA events on the rank's
+ * stream, from its first upload to its last result copy); ms[n_devices]. */
+int pals_multi_last_ms(const pals_multi* m, double* ms);
+
 /* ---- decision-log wire format (metrics.hpp:145-157, csvio.hpp:17-21) -- */
 /* decisions_csv over the logged traces of a replay (host buffers from pals_replay_ex):
  * header "node,model,t_s,cap_w,batch,tp,ep,dp,applied,reason,err_norm,bias", then one

@@ -75,6 +75,19 @@ SIGNATURES = [
     ("pals_replay_traces_device", _I, [_VP, _I32, _VP, _VP, _VP, _VP, _VP, _I32, _VP, _I32,
                                        _VP, _VP]),
     ("pals_replay_traces_status", _I64, [_VP]),
+    ("pals_multi_create", _I, [_VP, _I32, _VP]),
+    ("pals_multi_destroy", _I, [_VP]),
+    ("pals_multi_size", _I32, [_VP]),
+    ("pals_multi_ctx", _VP, [_VP, _I32]),
+    ("pals_multi_set_gather", _I, [_VP, _I32]),
+    ("pals_multi_model_analytic", _I, [_VP, _VP, _VP, _VP]),
+    ("pals_multi_model_table", _I, [_VP, _VP, _VP, _VP, _I64, _VP]),
+    ("pals_multi_select", _I, [_VP, _I32, _VP, _I64, _VP, _VP, _I64, _VP, _VP]),
+    ("pals_multi_replay", _I, [_VP, _I32, _VP, _VP, _VP, _VP, _VP, _I32, _VP, _I32, _VP, _VP,
+                               _VP, _VP, _VP]),
+    ("pals_multi_replay_traces", _I, [_VP, _I32, _VP, _VP, _VP, _VP, _VP, _I32, _VP, _I32,
+                                      _VP, _VP]),
+    ("pals_multi_last_ms", _I, [_VP, _VP]),
     ("pals_decisions_csv", _I, [_VP, _VP, _I32, _VP, _I32, _VP, _I32, _VP, _VP, _VP, _VP, _I64,
                                 _VP]),
     ("pals_fnv1a64", C.c_uint64, [_VP, _I64]),

@@ -17,7 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpals_gpu.so")
 OBJ = os.path.join(HERE, "_build")
 SOURCES = ["ctx.cu", "plan.cu", "replay.cu", "forest.cu", "peaks.cu", "alloc.cu", "frontier.cu",
-           "logs.cu", "sim.cu"]
+           "logs.cu", "sim.cu", "multi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "--extended-lambda",

@@ -9,6 +9,7 @@
 // prefix-min of throughput keys (budget branch). A winner inside a near-tie
 // cluster is re-decided by the literal sequential fold over the candidates.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -72,24 +73,45 @@ struct Seg {
 
 
 
-// A caller signal read as detail::trace_value (sim.hpp:167-174) at non-decreasing times:
-// the cursor passes every point with t_s <= t (the value of the last one passed, else the
-// first point's value). Only the next timestamp and the current value stay in registers.
-struct SigCursor {
-    const pals_signal_point* p;    // next unread point
-    const pals_signal_point* end;
-    double v, nt;
-    __device__ __forceinline__ void init(const pals_signal_point* b, int n) {
-        p = b;
-        end = b + n;
-        v = n > 0 ? b[0].value : 0.0;
-        nt = n > 0 ? b[0].t_s : 0.0;
+// First step j in [from, n_steps) of a call whose start time t0(j) = (double)(first + j) * iv
+// reaches nt (nt <= t0(j): trace_value passes the point), else INT_MAX. t0 is
+// non-decreasing in j for iv > 0 (exact integer times a positive double), so a binary
+// search over the call's steps finds it with the exact predicate.
+__device__ __forceinline__ int first_pass_step(double nt, int from, int n_steps, int64_t first,
+                                               double iv) {
+    if (!(nt <= (double)(first + n_steps - 1) * iv)) return INT_MAX;  // NaN / after the call
+    if (nt <= (double)(first + from) * iv) return from;
+    int lo = from + 1, hi = n_steps - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (nt <= (double)(first + mid) * iv) hi = mid;
+        else lo = mid + 1;
     }
-    __device__ __forceinline__ double at(double t) {
-        while (p < end && nt <= t) {
+    return lo;
+}
+
+// A caller signal read as detail::trace_value (sim.hpp:167-174) at the steps' start times:
+// the cursor passes every point with t_s <= t0 (the value of the last one passed, else the
+// first point's value). Each point's timestamp is turned into the step index that passes
+// it when the point is reached, so a step costs one integer compare.
+struct SigCursor {
+    const pals_signal_point* p;  // next unread point
+    int rem;                     // unread points
+    int nk;                      // step that passes *p
+    double v;
+    __device__ __forceinline__ void init(const pals_signal_point* b, int n, int n_steps,
+                                         int64_t first, double iv) {
+        p = b;
+        rem = n;
+        v = n > 0 ? b[0].value : 0.0;
+        nk = n > 0 ? first_pass_step(b[0].t_s, 0, n_steps, first, iv) : INT_MAX;
+    }
+    __device__ __forceinline__ double at(int k, int n_steps, int64_t first, double iv) {
+        while (k >= nk) {
             v = p->value;
             ++p;
-            nt = p < end ? p->t_s : 0.0;
+            --rem;
+            nk = rem > 0 ? first_pass_step(p->t_s, k, n_steps, first, iv) : INT_MAX;
         }
         return v;
     }
@@ -195,9 +217,12 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
         noise_amp = tr.noise_amp;
         key = tr.noise_key;
         if (ok) {
-            lsig.init(p.tr.sig + tr.load_off, tr.n_load);
+            lsig.init(p.tr.sig + tr.load_off, tr.n_load, sp.n_steps, p.tr.first_step,
+                      sp.interval_s);
             has_bsig = tr.n_budget > 0;
-            if (has_bsig) bsig.init(p.tr.sig + tr.budget_off, tr.n_budget);
+            if (has_bsig)
+                bsig.init(p.tr.sig + tr.budget_off, tr.n_budget, sp.n_steps, p.tr.first_step,
+                          sp.interval_s);
         }
         if (!ok) {
             atomicMin(p.tr.status, (unsigned long long)ti);
@@ -283,15 +308,15 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
     double noise_lane = 1.0;  // warp layout: noise of step (k & ~31) + lane
     double node_budget = 0.0;
 
+    // control_step's stale-telemetry test (controller.hpp:217) with now = telemetry.t = t1:
+    // t1 - t1 is +0 for every step (the host checked that all step times are finite), so
+    // the test is one constant per call
+    const bool stale = 0.0 > 1.5 * cfg.interval_s;
     for (int k = 0; k < sp.n_steps; ++k) {
-        double t0, t1;
         if constexpr (kTr) {
-            t0 = (double)(p.tr.first_step + k) * sp.interval_s;  // Simulator::run sim.hpp:230
-            t1 = t0 + sp.interval_s;
-            if (has_bsig) node_budget = bsig.at(t0);
+            // signals at t0 = (first_step + k) * interval (Simulator::run sim.hpp:229-230)
+            if (has_bsig) node_budget = bsig.at(k, sp.n_steps, p.tr.first_step, sp.interval_s);
         } else {
-            t0 = (double)k * sp.interval_s;
-            t1 = t0 + sp.interval_s;
             node_budget = sp.budget_mode ? bs.at(k, key, 1, sp.seg_min, sp.seg_max,
                                                  sp.budget_lo_frac, m.p_min, sp.budget_hi_frac,
                                                  m.p_max)
@@ -342,7 +367,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
         }
         double offered, noise;
         if constexpr (kTr) {
-            offered = lsig.at(t0);
+            offered = lsig.at(k, sp.n_steps, p.tr.first_step, sp.interval_s);
             // noise_amp == 0 gives 1 + 0 * x = 1 exactly: the draw is skipped, not changed
             noise = noise_amp != 0.0
                         ? 1.0 + noise_amp * (2.0 * u01(draw(key, 3, (uint64_t)(p.tr.first_step + k))) - 1.0)
@@ -364,7 +389,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
 
         // ---- control_step (controller.hpp:210-267) ----
         int d_idx, d_applied, d_reason;
-        if (t1 - t1 > 1.5 * cfg.interval_s) {  // stale telemetry (:217-220)
+        if (stale) {  // stale telemetry (:217-220)
             d_idx = cur;
             d_applied = 0;
             d_reason = PALS_REASON_HOLD;
@@ -796,12 +821,25 @@ static int replay_setup(pals_ctx* ctx, int n_models, pals_model* const* models,
     return PALS_OK;
 }
 
+// Step times t0 = (first + k) * iv, t1 = t0 + iv must be exact, increasing and finite for
+// the kernels' step-index signal cursors and their once-per-call stale test.
+static bool step_times_ok(int64_t first, int64_t n_steps, double iv) {
+    if (!(iv > 0.0) || !std::isfinite(iv)) return false;
+    const int64_t lim = (int64_t)1 << 52;
+    if (first <= -lim || first >= lim || n_steps >= lim - (first < 0 ? -first : first)) return false;
+    const double a = (double)first * iv, z = (double)(first + n_steps) * iv + iv;
+    return std::isfinite(a) && std::isfinite(z);
+}
+
 static int replay_launch(pals_ctx* ctx, ReplayCache* rc, const pals_ctrl_cfg* cfg,
                          const pals_replay_spec* spec, pals_trace_summary* d_sum,
                          pals_step_log* d_logs, pals_step_detail* d_det) {
     if (spec->n_traces <= 0) return PALS_OK;
     if (spec->n_steps < 0 || spec->seg_min < 1 || spec->seg_max < spec->seg_min)
         return set_error(PALS_ECONFIG, "pals_replay: bad spec");
+    if (!step_times_ok(0, spec->n_steps, spec->interval_s))
+        return set_error(PALS_ECONFIG, "pals_replay: interval_s must be positive and every "
+                                       "step time finite (Scenario::validate, sim.hpp:81)");
     ReplayParams p;
     memset(&p, 0, sizeof p);
     p.spec = *spec;
@@ -871,6 +909,9 @@ static int traces_launch(pals_ctx* ctx, ReplayCache* rc, const pals_ctrl_cfg* cf
     if (b.n_traces <= 0) return PALS_OK;
     if (b.n_steps < 0 || !b.traces || !b.summaries || (b.n_signal > 0 && !b.signal))
         return set_error(PALS_ECONFIG, "pals_replay_traces: bad batch");
+    if (!step_times_ok(b.first_step, b.n_steps, b.interval_s))
+        return set_error(PALS_ECONFIG, "pals_replay_traces: interval_s must be positive and "
+                                       "every step time finite (Scenario::validate, sim.hpp:81)");
     ReplayParams p;
     memset(&p, 0, sizeof p);
     p.spec.n_traces = b.n_traces;

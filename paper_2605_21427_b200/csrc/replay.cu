@@ -9,6 +9,7 @@
 // prefix-min of throughput keys (budget branch). A winner inside a near-tie
 // cluster is re-decided by the literal sequential fold over the candidates.
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -39,7 +40,6 @@ struct ReplayParams {
     pals_ctrl_cfg cfg;
     double alpha, beta;
     int n_models;
-    int variant;  // PALS_REPLAY_VARIANT bit 1: prefix-min breaker search (default on)
     TraceArgs tr;
 };
 
@@ -144,7 +144,9 @@ __global__ void k_replay_order(pals_replay_spec sp, const pals_trace* __restrict
         const int64_t i = i0 + threadIdx.x;
         int g = -1;
         if (i < sp.n_traces)
-            g = traces ? (traces[i].objective == PALS_OBJ_BUDGET ? 1 : 0)
+            // group 0: traces that run the PID (QoS objective with a positive target: the
+            // synthetic targets always are), group 1: the rest
+            g = traces ? (traces[i].objective == PALS_OBJ_QOS && traces[i].target_tps > 0.0 ? 0 : 1)
                        : trace_objective(sp, splitmix64(sp.seed ^ (uint64_t)(sp.first_trace + i)));
         for (int k = 0; k < 2; ++k) {
             const unsigned m = __ballot_sync(0xffffffffu, g == k);
@@ -169,6 +171,9 @@ __global__ void k_replay_order(pals_replay_spec sp, const pals_trace* __restrict
 // kTr: caller traces (pals_replay_traces): model, objective and target per trace, budget
 // and offered load from caller signals, initial / final controller and plant states;
 // thread layout only. Otherwise the synthetic generator of DESIGN.md §4.
+// The step loop is instantiated twice: with the PID (QoS objective, positive target) and
+// without it (every other trace: err_norm = 0, controller.hpp:224-239), so each loop
+// keeps only its own state live; warps are made uniform in that choice (k_replay_order).
 template <int kMinBlocks, bool kWarp, bool kTr>
 __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev* __restrict__ models,
                                                 ReplayParams p, const int32_t* __restrict__ order,
@@ -247,7 +252,8 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
     // ControllerState (controller.hpp:55-63)
     double bias = 1.0, integral = 0.0, prev_err = 0.0;
     bool has_prev = false, has_last = false, last_has_budget = false;
-    double last_budget = 0.0;
+    double last_budget = 0.0;  // Targets::power_budget_w of the last step, and the raw
+                               // node budget the enforce_cap memo and Kp were taken at
     int sustain = 0;
     int cur = m.init_idx;
     // plant (sim.hpp:155-157, 466-472); caps and batch caps are always candidate knob
@@ -290,15 +296,14 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
             return;
         }
     }
-    // enforce_cap memo (pure function of its inputs)
+    // enforce_cap memo (a pure function of applied cap, batch cap and node budget; keyed
+    // on last_budget, c_a = -1 forces the first evaluation)
     int c_a = -1, c_b = -1;
-    double c_nb = -1.0;
     int cj = 0;  // walk position of the enforced cap (cap = walk_c[c_a][cj], logs only)
     double capacity = 0.0, sys_w = 0.0;
-    // Kp memo per budget value
-    double kp_budget = -1.0;
     int kp = m.nd_p;
-    int kt = 0;  // incremental t-feasibility count (count_t_feasible)
+    bool kp_ok = false;  // kp counts the candidates within last_budget's select budget
+    int kt = 0;          // incremental t-feasibility count (count_t_feasible)
     uint64_t h = 0xcbf29ce484222325ULL;
     double energy = 0.0, tokens = 0.0;
     int n_applied = 0;
@@ -306,188 +311,202 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
     // registers live across the loop)
     const bool logging = logs && ti < sp.n_log_traces && (!kWarp || lane == 0);
     double noise_lane = 1.0;  // warp layout: noise of step (k & ~31) + lane
-    double node_budget = 0.0;
-
     // control_step's stale-telemetry test (controller.hpp:217) with now = telemetry.t = t1:
     // t1 - t1 is +0 for every step (the host checked that all step times are finite), so
     // the test is one constant per call
     const bool stale = 0.0 > 1.5 * cfg.interval_s;
-    for (int k = 0; k < sp.n_steps; ++k) {
-        if constexpr (kTr) {
-            // signals at t0 = (first_step + k) * interval (Simulator::run sim.hpp:229-230)
-            if (has_bsig) node_budget = bsig.at(k, sp.n_steps, p.tr.first_step, sp.interval_s);
-        } else {
-            node_budget = sp.budget_mode ? bs.at(k, key, 1, sp.seg_min, sp.seg_max,
-                                                 sp.budget_lo_frac, m.p_min, sp.budget_hi_frac,
-                                                 m.p_max)
-                                         : 0.0;
-        }
-        // b_eff = batch_cap (fluid plant: the queue always covers the batch cap)
-        if (applied_a != c_a || batch_b != c_b || node_budget != c_nb) {
-            // enforce_cap (sim.hpp:195-205): walk down in 5 W steps until the cluster
-            // draw fits the budget; no budget -> the applied cap itself
-            const double* wc = m.walk_c + (int64_t)applied_a * m.L;
-            const int64_t wo = ((int64_t)applied_a * m.nb + batch_b) * m.L;
-            int j = 0;
-            if (node_budget > 0.0) {
-                if (kWarp) {  // first walk position that stops the loop, 32 per round
-                    for (int base = 0;; base += 32) {
-                        const int q = base + lane;
-                        const bool stop = q < m.L && (!(wc[q] > m.plant_min_cap) ||
-                                                      m.walk_pn[wo + q] <= node_budget);
-                        const unsigned b = __ballot_sync(0xffffffffu, stop);
-                        if (b) {
-                            j = base + __ffs(b) - 1;
-                            break;
+    // without the PID err_norm stays 0 (controller.hpp:224), so the sustain counter only
+    // grows when epsilon is negative
+    const bool eps_neg = 0.0 > eps;
+
+    auto steps = [&](auto pid_tag) {
+        constexpr bool kPid = decltype(pid_tag)::value;
+        for (int k = 0; k < sp.n_steps; ++k) {
+            double node_budget = 0.0;
+            if constexpr (kTr) {
+                // signals at t0 = (first_step + k) * interval (Simulator::run sim.hpp:229-230)
+                if (has_bsig) node_budget = bsig.at(k, sp.n_steps, p.tr.first_step, sp.interval_s);
+            } else {
+                if (sp.budget_mode)
+                    node_budget = bs.at(k, key, 1, sp.seg_min, sp.seg_max, sp.budget_lo_frac,
+                                        m.p_min, sp.budget_hi_frac, m.p_max);
+            }
+            // b_eff = batch_cap (fluid plant: the queue always covers the batch cap)
+            if (applied_a != c_a || batch_b != c_b || node_budget != last_budget) {
+                // enforce_cap (sim.hpp:195-205): walk down in 5 W steps until the cluster
+                // draw fits the budget; no budget -> the applied cap itself
+                const double* wc = m.walk_c + (int64_t)applied_a * m.L;
+                const int64_t wo = ((int64_t)applied_a * m.nb + batch_b) * m.L;
+                int j = 0;
+                if (node_budget > 0.0) {
+                    if (kWarp) {  // first walk position that stops the loop, 32 per round
+                        for (int base = 0;; base += 32) {
+                            const int q = base + lane;
+                            const bool stop = q < m.L && (!(wc[q] > m.plant_min_cap) ||
+                                                          m.walk_pn[wo + q] <= node_budget);
+                            const unsigned b = __ballot_sync(0xffffffffu, stop);
+                            if (b) {
+                                j = base + __ffs(b) - 1;
+                                break;
+                            }
                         }
+                    } else if (wc[0] > m.plant_min_cap && !(m.walk_pn[wo] <= node_budget)) {
+                        // the loop stops at the first position with c <= min_cap (a suffix
+                        // of the walk, from walk_jmin) or with a fitting draw; before
+                        // walk_jmin that is the first position whose running minimum
+                        // fits: a binary search over the non-increasing walk_pm
+                        int lo = 1, hi = m.walk_jmin[applied_a];
+                        const double* pm = m.walk_pm + wo;
+                        while (lo < hi) {
+                            const int mid = (lo + hi) >> 1;
+                            if (pm[mid] <= node_budget) hi = mid;
+                            else lo = mid + 1;
+                        }
+                        j = lo;
                     }
-                } else if (!(p.variant & 2)) {
-                    while (wc[j] > m.plant_min_cap && !(m.walk_pn[wo + j] <= node_budget)) ++j;
-                } else if (wc[0] > m.plant_min_cap && !(m.walk_pn[wo] <= node_budget)) {
-                    // the loop stops at the first position with c <= min_cap (a suffix
-                    // of the walk, from walk_jmin) or with a fitting draw; before
-                    // walk_jmin that is the first position whose running minimum
-                    // fits: a binary search over the non-increasing walk_pm
-                    int lo = 1, hi = m.walk_jmin[applied_a];
-                    const double* pm = m.walk_pm + wo;
-                    while (lo < hi) {
-                        const int mid = (lo + hi) >> 1;
-                        if (pm[mid] <= node_budget) hi = mid;
-                        else lo = mid + 1;
-                    }
-                    j = lo;
                 }
+                cj = j;
+                capacity = (double)m.dp * m.walk_T[wo + j];
+                sys_w = m.walk_pn[wo + j];  // = dp * (alpha * 4 * P + beta) (sim.hpp:413-414)
+                c_a = applied_a;
+                c_b = batch_b;
             }
-            cj = j;
-            capacity = (double)m.dp * m.walk_T[wo + j];
-            sys_w = m.walk_pn[wo + j];  // = dp * (alpha * 4 * P + beta) (sim.hpp:413-414)
-            c_a = applied_a;
-            c_b = batch_b;
-            c_nb = node_budget;
-        }
-        double offered, noise;
-        if constexpr (kTr) {
-            offered = lsig.at(k, sp.n_steps, p.tr.first_step, sp.interval_s);
-            // noise_amp == 0 gives 1 + 0 * x = 1 exactly: the draw is skipped, not changed
-            noise = noise_amp != 0.0
-                        ? 1.0 + noise_amp * (2.0 * u01(draw(key, 3, (uint64_t)(p.tr.first_step + k))) - 1.0)
-                        : 1.0;
-        } else {
-            offered = ls.at(k, key, 2, sp.seg_min, sp.seg_max, sp.load_lo, m.t_max, sp.load_hi,
-                            m.t_max);
-            if (kWarp) {
-                if ((k & 31) == 0 && k + lane < sp.n_steps)
-                    noise_lane = 1.0 + noise_amp * (2.0 * u01(draw(key, 3, (uint64_t)(k + lane))) - 1.0);
-                noise = __shfl_sync(0xffffffffu, noise_lane, k & 31);
+            double offered, noise;
+            if constexpr (kTr) {
+                offered = lsig.at(k, sp.n_steps, p.tr.first_step, sp.interval_s);
+                // noise_amp == 0 gives 1 + 0 * x = 1 exactly: the draw is skipped, not changed
+                noise = noise_amp != 0.0
+                            ? 1.0 + noise_amp * (2.0 * u01(draw(key, 3, (uint64_t)(p.tr.first_step + k))) - 1.0)
+                            : 1.0;
             } else {
-                noise = 1.0 + noise_amp * (2.0 * u01(draw(key, 3, (uint64_t)k)) - 1.0);
-            }
-        }
-        const double measured = smin(offered, capacity) * noise;
-        energy += sys_w * sp.interval_s;
-        tokens += measured * sp.interval_s;
-
-        // ---- control_step (controller.hpp:210-267) ----
-        int d_idx, d_applied, d_reason;
-        if (stale) {  // stale telemetry (:217-220)
-            d_idx = cur;
-            d_applied = 0;
-            d_reason = PALS_REASON_HOLD;
-        } else {
-            double err_norm = 0.0;
-            if (obj == PALS_OBJ_QOS && target_tps > 0.0) {
-                err_norm = (target_tps - measured) / target_tps;
-                const double promised = (double)m.dp * m.T[cur] * bias;
-                if (promised > 0.0) {
-                    const double pred_err = (promised - measured) / promised;
-                    integral = sclamp(integral + pred_err, -cfg.integral_clamp, cfg.integral_clamp);
-                    const double deriv = has_prev ? pred_err - prev_err : 0.0;
-                    const double corr = cfg.kp * pred_err + cfg.ki * integral + cfg.kd * deriv;
-                    bias = sclamp(bias * (1.0 - corr), cfg.bias_min, cfg.bias_max);
-                    prev_err = pred_err;
-                    has_prev = true;
-                }
-            }
-            const bool bset = node_budget > 0.0;
-            const bool changed =
-                !has_last || !(last_has_budget == bset && (!bset || last_budget == node_budget));
-            has_last = true;
-            last_has_budget = bset;
-            last_budget = node_budget;
-            if (fabs(err_norm) > eps) ++sustain;
-            else sustain = 0;
-
-            const double budget = bset ? node_budget * (1.0 - cfg.budget_margin) : 0.0;
-            if (bset && budget != kp_budget) {
+                offered = ls.at(k, key, 2, sp.seg_min, sp.seg_max, sp.load_lo, m.t_max, sp.load_hi,
+                                m.t_max);
                 if (kWarp) {
-                    kp = warp_leading_true(m.nd_p, [&](int i) { return m.up[i] <= budget; });
+                    if ((k & 31) == 0 && k + lane < sp.n_steps)
+                        noise_lane = 1.0 + noise_amp * (2.0 * u01(draw(key, 3, (uint64_t)(k + lane))) - 1.0);
+                    noise = __shfl_sync(0xffffffffu, noise_lane, k & 31);
                 } else {
-                    int lo = 0, hi = m.nd_p;
-                    while (lo < hi) {
-                        const int mid = (lo + hi) >> 1;
-                        if (m.up[mid] <= budget) lo = mid + 1;
-                        else hi = mid;
-                    }
-                    kp = lo;
-                }
-                kp_budget = budget;
-            }
-            int s_idx, s_reason;
-            if (obj == PALS_OBJ_QOS) {
-                if (kWarp) {
-                    const bool ok_lo = kt == 0 || !(m.ut[kt - 1] * bias < target);
-                    const bool ok_hi = kt == m.nd_t || (m.ut[kt] * bias < target);
-                    if (!(ok_lo && ok_hi))
-                        kt = warp_leading_true(m.nd_t,
-                                               [&](int i) { return !(m.ut[i] * bias < target); });
-                } else {
-                    kt = count_t_feasible(m, bias, target, kt);
+                    noise = 1.0 + noise_amp * (2.0 * u01(draw(key, 3, (uint64_t)k)) - 1.0);
                 }
             }
-            table_select(m, target, bset, budget, kp, kt, bias, obj, &s_idx, &s_reason);
-            const bool may_apply = changed || sustain >= cfg.sustain_intervals;
-            const int sc = s_idx;  // canonical (first equal point)
-            if (may_apply && sc != cur) {
-                cur = sc;
-                sustain = 0;
-                d_idx = sc;
-                d_applied = 1;
-                d_reason = s_reason;
-            } else {
+            const double measured = smin(offered, capacity) * noise;
+            energy += sys_w * sp.interval_s;
+            tokens += measured * sp.interval_s;
+
+            // ---- control_step (controller.hpp:210-267) ----
+            int d_idx, d_applied, d_reason;
+            if (stale) {  // stale telemetry (:217-220)
                 d_idx = cur;
                 d_applied = 0;
-                d_reason = may_apply ? s_reason : PALS_REASON_HOLD;
+                d_reason = PALS_REASON_HOLD;
+            } else {
+                bool sustained;
+                if constexpr (kPid) {  // QoS objective with a positive target (:224-239)
+                    const double err_norm = (target_tps - measured) / target_tps;
+                    const double promised = (double)m.dp * m.T[cur] * bias;
+                    if (promised > 0.0) {
+                        const double pred_err = (promised - measured) / promised;
+                        integral = sclamp(integral + pred_err, -cfg.integral_clamp, cfg.integral_clamp);
+                        const double deriv = has_prev ? pred_err - prev_err : 0.0;
+                        const double corr = cfg.kp * pred_err + cfg.ki * integral + cfg.kd * deriv;
+                        bias = sclamp(bias * (1.0 - corr), cfg.bias_min, cfg.bias_max);
+                        prev_err = pred_err;
+                        has_prev = true;
+                    }
+                    sustained = fabs(err_norm) > eps;
+                } else {
+                    sustained = eps_neg;
+                }
+                const bool bset = node_budget > 0.0;
+                const bool changed =
+                    !has_last || !(last_has_budget == bset && (!bset || last_budget == node_budget));
+                if (sustained) ++sustain;
+                else sustain = 0;
+                const bool may_apply = changed || sustain >= cfg.sustain_intervals;
+                const double budget = bset ? node_budget * (1.0 - cfg.budget_margin) : 0.0;
+                // select_config (controller.hpp:253) decides only when the decision may
+                // apply; on a hold its result is discarded (:256-266), so it is skipped
+                // (the Kt / Kp counts are recomputed from their memo on the next use)
+                int s_idx = cur, s_reason = PALS_REASON_HOLD;
+                if (may_apply) {
+                    if (bset && !(kp_ok && last_budget == node_budget)) {
+                        if (kWarp) {
+                            kp = warp_leading_true(m.nd_p, [&](int i) { return m.up[i] <= budget; });
+                        } else {
+                            int lo = 0, hi = m.nd_p;
+                            while (lo < hi) {
+                                const int mid = (lo + hi) >> 1;
+                                if (m.up[mid] <= budget) lo = mid + 1;
+                                else hi = mid;
+                            }
+                            kp = lo;
+                        }
+                    }
+                    if (obj == PALS_OBJ_QOS) {
+                        if (kWarp) {
+                            const bool ok_lo = kt == 0 || !(m.ut[kt - 1] * bias < target);
+                            const bool ok_hi = kt == m.nd_t || (m.ut[kt] * bias < target);
+                            if (!(ok_lo && ok_hi))
+                                kt = warp_leading_true(m.nd_t,
+                                                       [&](int i) { return !(m.ut[i] * bias < target); });
+                        } else {
+                            kt = count_t_feasible(m, bias, target, kt);
+                        }
+                    }
+                    table_select(m, target, bset, budget, kp, kt, bias, obj, &s_idx, &s_reason);
+                }
+                kp_ok = bset && (may_apply || (kp_ok && last_budget == node_budget));
+                has_last = true;
+                last_has_budget = bset;
+                last_budget = node_budget;
+                const int sc = s_idx;  // canonical (first equal point)
+                if (may_apply && sc != cur) {
+                    cur = sc;
+                    sustain = 0;
+                    d_idx = sc;
+                    d_applied = 1;
+                    d_reason = s_reason;
+                } else {
+                    d_idx = cur;
+                    d_applied = 0;
+                    d_reason = may_apply ? s_reason : PALS_REASON_HOLD;
+                }
+            }
+            // stale steps leave ControllerState (and last_budget) untouched: no memo then
+            if (stale) c_a = -1;
+            const uint64_t word = ((uint64_t)(uint32_t)d_idx << 8) | ((uint64_t)d_applied << 4) |
+                                  (uint64_t)d_reason;
+            h = (h ^ word) * 0x100000001b3ULL;
+            n_applied += d_applied;
+            if (logging) {
+                pals_step_log* lg = logs + ti * (int64_t)sp.n_steps;
+                const double cap = m.walk_c[(int64_t)c_a * m.L + cj];
+                pals_step_log r;
+                r.idx = d_idx;
+                r.applied = (uint8_t)d_applied;
+                r.reason = (uint8_t)d_reason;
+                r.cap_tenths = (uint16_t)llround(cap * 10.0);
+                lg[k] = r;
+                if (details) {  // DecisionRecord err_norm / bias (sim.hpp:438-440, 462-463)
+                    pals_step_detail* dt = details + ti * (int64_t)sp.n_steps;
+                    pals_step_detail x;
+                    x.err_norm = target_tps > 0.0 ? (target_tps - measured) / target_tps : 0.0;
+                    x.bias = bias;
+                    dt[k] = x;
+                }
+            }
+            // actuation (sim.hpp:466-472): batch next interval, cap one interval later;
+            // candidate index = cap index * nb + batch index (build_candidates order)
+            applied_a = inflight_a;
+            if (d_applied) {
+                batch_b = cur % m.nb;
+                inflight_a = cur / m.nb;
             }
         }
-        const uint64_t word = ((uint64_t)(uint32_t)d_idx << 8) | ((uint64_t)d_applied << 4) |
-                              (uint64_t)d_reason;
-        h = (h ^ word) * 0x100000001b3ULL;
-        n_applied += d_applied;
-        if (logging) {
-            pals_step_log* lg = logs + ti * (int64_t)sp.n_steps;
-            const double cap = m.walk_c[(int64_t)c_a * m.L + cj];
-            pals_step_log r;
-            r.idx = d_idx;
-            r.applied = (uint8_t)d_applied;
-            r.reason = (uint8_t)d_reason;
-            r.cap_tenths = (uint16_t)llround(cap * 10.0);
-            lg[k] = r;
-            if (details) {  // DecisionRecord err_norm / bias (sim.hpp:438-440, 462-463)
-                pals_step_detail* dt = details + ti * (int64_t)sp.n_steps;
-                pals_step_detail x;
-                x.err_norm = target_tps > 0.0 ? (target_tps - measured) / target_tps : 0.0;
-                x.bias = bias;
-                dt[k] = x;
-            }
-        }
-        // actuation (sim.hpp:466-472): batch next interval, cap one interval later;
-        // candidate index = cap index * nb + batch index (build_candidates order)
-        applied_a = inflight_a;
-        if (d_applied) {
-            batch_b = cur % m.nb;
-            inflight_a = cur / m.nb;
-        }
-    }
+    };
+    if (obj == PALS_OBJ_QOS && target_tps > 0.0) steps(std::true_type{});
+    else steps(std::false_type{});
+
     h = (h ^ (uint64_t)__double_as_longlong(bias)) * 0x100000001b3ULL;
     h = (h ^ (uint64_t)(uint32_t)cur) * 0x100000001b3ULL;
     if (kWarp && lane != 0) return;
@@ -847,11 +866,6 @@ static int replay_launch(pals_ctx* ctx, ReplayCache* rc, const pals_ctrl_cfg* cf
     p.alpha = rc->coeffs.alpha;
     p.beta = rc->coeffs.beta_watts;
     p.n_models = (int)rc->models.size();
-    static const int variant = [] {
-        const char* e = getenv("PALS_REPLAY_VARIANT");
-        return e ? atoi(e) : 2;
-    }();
-    p.variant = variant;
     const int64_t blocks = (spec->n_traces + 127) / 128;
     int32_t* order = nullptr;
     if (spec->objective_mode == 2 && ctx->replay_layout != PALS_REPLAY_WARP) {
@@ -871,17 +885,12 @@ static int replay_launch(pals_ctx* ctx, ReplayCache* rc, const pals_ctrl_cfg* cf
     // measured on B200: 6 CTAs/SM (80 regs) beats the 126-register build by 1.1-1.4x on
     // small candidate sets (cfg4's 36: 6.8e10 vs 6.1e10 decisions/s); on the 1,464-
     // candidate DR grid the unconstrained build wins (3.9e10 vs 3.3e10)
-    static const int minb_env = [] {
-        const char* e = getenv("PALS_REPLAY_MINB");
-        return e ? atoi(e) : 0;
-    }();
     const int ncand = (int)(rc->caps.size() * rc->batches.size());
-    const int minb = minb_env ? minb_env : (ncand <= 256 ? 6 : 1);
+    const int minb = ncand <= 256 ? 6 : 1;
     const size_t msm = sizeof(ReplayModelDev) * (size_t)p.n_models;
     if (msm > 48 * 1024) {
         const int b = (int)msm;
         PALS_CUDA(cudaFuncSetAttribute(k_replay<6, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-        PALS_CUDA(cudaFuncSetAttribute(k_replay<8, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
         PALS_CUDA(cudaFuncSetAttribute(k_replay<6, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
         PALS_CUDA(cudaFuncSetAttribute(k_replay<1, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
     }
@@ -889,9 +898,7 @@ static int replay_launch(pals_ctx* ctx, ReplayCache* rc, const pals_ctrl_cfg* cf
         const int64_t wblocks = (spec->n_traces + 3) / 4;  // 4 traces (warps) per CTA
         k_replay<6, true, false><<<(unsigned)wblocks, 128, msm, ctx->stream>>>(rc->d_models, p, nullptr,
                                                                        d_sum, d_logs, d_det);
-    } else if (minb >= 8)
-        k_replay<8, false, false><<<(unsigned)blocks, 128, msm, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs, d_det);
-    else if (minb >= 6)
+    } else if (minb >= 6)
         k_replay<6, false, false><<<(unsigned)blocks, 128, msm, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs, d_det);
     else
         k_replay<1, false, false><<<(unsigned)blocks, 128, msm, ctx->stream>>>(rc->d_models, p, order, d_sum, d_logs, d_det);
@@ -922,7 +929,6 @@ static int traces_launch(pals_ctx* ctx, ReplayCache* rc, const pals_ctrl_cfg* cf
     p.alpha = rc->coeffs.alpha;
     p.beta = rc->coeffs.beta_watts;
     p.n_models = (int)rc->models.size();
-    p.variant = 2;
     p.tr.traces = b.traces;
     p.tr.sig = b.signal;
     p.tr.n_sig = b.n_signal;

@@ -245,6 +245,11 @@ static uint64_t draw(uint64_t key, uint64_t lane, uint64_t ctr) {
     return or_splitmix64(key ^ (lane << 48) ^ ctr);
 }
 static double u01(uint64_t u) { return (double)(u >> 11) * 0x1.0p-53; }
+/* plant noise uniform of step s: the low (even s) or high (odd s) 32 bits of one
+ * splitmix64 draw per step pair, times 2^-32 */
+static double noise_u(uint64_t key, uint64_t s) {
+    return (double)(uint32_t)(draw(key, 3, s >> 1) >> (32 * (s & 1))) * 0x1.0p-32;
+}
 
 typedef struct {
     uint64_t key, lane;
@@ -411,7 +416,7 @@ static int replay_impl(int n_models, const pals_profile* plant, const pals_gpu_s
             const double capacity = (double)p.dp * Tc;
             const double sys_w = (double)p.dp * (k->alpha * 4.0 * Pc + k->beta_watts);
             const double offered = seg_value(&ls, s);
-            const double noise = 1.0 + spec->noise_amp * (2.0 * u01(draw(key, 3, (uint64_t)s)) - 1.0);
+            const double noise = 1.0 + spec->noise_amp * (2.0 * noise_u(key, (uint64_t)s) - 1.0);
             const double measured = smin(offered, capacity) * noise;
             energy += sys_w * spec->interval_s;
             tokens += measured * spec->interval_s;

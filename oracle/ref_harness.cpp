@@ -184,6 +184,12 @@ inline std::uint64_t draw(std::uint64_t key, std::uint64_t lane, std::uint64_t c
     return splitmix64(key ^ (lane << 48) ^ ctr);
 }
 inline double u01(std::uint64_t u) { return static_cast<double>(u >> 11) * 0x1.0p-53; }
+// plant noise uniform of step s: the low (even s) or high (odd s) 32 bits of one
+// splitmix64 draw per step pair, times 2^-32
+inline double noise_u(std::uint64_t key, std::uint64_t s) {
+    return static_cast<double>(static_cast<std::uint32_t>(draw(key, 3, s >> 1) >> (32 * (s & 1)))) *
+           0x1.0p-32;
+}
 
 struct Segments {
     std::uint64_t key, lane;
@@ -263,7 +269,7 @@ void replay_one(const std::vector<ReplayModel>& models, const GpuSpec& gpu,
         const double gpu_w = avg_gpu_power(p, rm.profile, gpu);
         const double sys_w = dp * (coeffs.alpha * kGpusPerNode * gpu_w + coeffs.beta_watts);
         const double offered = lseg.value_at(k);
-        const double noise = 1.0 + spec.noise_amp * (2.0 * u01(draw(key, 3, k)) - 1.0);
+        const double noise = 1.0 + spec.noise_amp * (2.0 * noise_u(key, k) - 1.0);
         const double measured = std::min(offered, capacity) * noise;
         energy += sys_w * spec.interval_s;
         tokens += measured * spec.interval_s;
@@ -376,7 +382,7 @@ void replay_trace_one(const std::vector<ReplayModel>& models, const GpuSpec& gpu
         const double sys_w = dp * (coeffs.alpha * kGpusPerNode * gpu_w + coeffs.beta_watts);
         const double offered = detail::trace_value(load, t0);
         const double noise =
-            1.0 + tr.noise_amp * (2.0 * u01(draw(tr.noise_key, 3, static_cast<std::uint64_t>(step))) - 1.0);
+            1.0 + tr.noise_amp * (2.0 * noise_u(tr.noise_key, static_cast<std::uint64_t>(step)) - 1.0);
         const double measured = std::min(offered, capacity) * noise;
         energy += sys_w * b.interval_s;
         tokens += measured * b.interval_s;

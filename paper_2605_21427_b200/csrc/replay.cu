@@ -48,6 +48,14 @@ __device__ __forceinline__ uint64_t draw(uint64_t key, uint64_t lane, uint64_t c
     return splitmix64(key ^ (lane << 48) ^ ctr);
 }
 __device__ __forceinline__ double u01(uint64_t u) { return (double)(u >> 11) * 0x1.0p-53; }
+// Plant noise of step s: noise = 1 + amp * (2 u - 1) with u the low (even s)
+// or high (odd s) 32 bits of draw(key, 3, s >> 1) times 2^-32 — one splitmix64 per step pair.
+__device__ __forceinline__ uint32_t noise_bits(uint64_t key, uint64_t s) {
+    return (uint32_t)(draw(key, 3, s >> 1) >> (32 * (s & 1)));
+}
+__device__ __forceinline__ double noise_of(double amp, uint32_t u) {
+    return 1.0 + amp * (2.0 * ((double)u * 0x1.0p-32) - 1.0);
+}
 
 // Piecewise-constant trace lane: only the segment cursor and level live in
 // registers; the level bounds (lo, hi) are recomputed from the model when a new
@@ -311,6 +319,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
     // registers live across the loop)
     const bool logging = logs && ti < sp.n_log_traces && (!kWarp || lane == 0);
     double noise_lane = 1.0;  // warp layout: noise of step (k & ~31) + lane
+    uint32_t nz_hi = 0;       // thread layout: the odd step's half of the pair's draw
     // control_step's stale-telemetry test (controller.hpp:217) with now = telemetry.t = t1:
     // t1 - t1 is +0 for every step (the host checked that all step times are finite), so
     // the test is one constant per call
@@ -372,22 +381,29 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
                 c_b = batch_b;
             }
             double offered, noise;
-            if constexpr (kTr) {
-                offered = lsig.at(k, sp.n_steps, p.tr.first_step, sp.interval_s);
-                // noise_amp == 0 gives 1 + 0 * x = 1 exactly: the draw is skipped, not changed
-                noise = noise_amp != 0.0
-                            ? 1.0 + noise_amp * (2.0 * u01(draw(key, 3, (uint64_t)(p.tr.first_step + k))) - 1.0)
-                            : 1.0;
-            } else {
-                offered = ls.at(k, key, 2, sp.seg_min, sp.seg_max, sp.load_lo, m.t_max, sp.load_hi,
-                                m.t_max);
-                if (kWarp) {
-                    if ((k & 31) == 0 && k + lane < sp.n_steps)
-                        noise_lane = 1.0 + noise_amp * (2.0 * u01(draw(key, 3, (uint64_t)(k + lane))) - 1.0);
-                    noise = __shfl_sync(0xffffffffu, noise_lane, k & 31);
+            if constexpr (kTr) offered = lsig.at(k, sp.n_steps, p.tr.first_step, sp.interval_s);
+            else offered = ls.at(k, key, 2, sp.seg_min, sp.seg_max, sp.load_lo, m.t_max,
+                                 sp.load_hi, m.t_max);
+            if (kWarp) {  // lanes draw the noise of 32 steps per round
+                if ((k & 31) == 0 && k + lane < sp.n_steps)
+                    noise_lane = noise_of(noise_amp, noise_bits(key, (uint64_t)(k + lane)));
+                noise = __shfl_sync(0xffffffffu, noise_lane, k & 31);
+            } else if (!kTr || noise_amp != 0.0) {
+                // (noise_amp == 0 gives 1 + 0 * x = 1 exactly: the draw is skipped, not changed)
+                // one draw per step pair; its high half waits in nz_hi for the odd step
+                const uint64_t st = kTr ? (uint64_t)(p.tr.first_step + k) : (uint64_t)k;
+                uint32_t u;
+                if (!(st & 1)) {
+                    const uint64_t r = draw(key, 3, st >> 1);
+                    u = (uint32_t)r;
+                    nz_hi = (uint32_t)(r >> 32);
                 } else {
-                    noise = 1.0 + noise_amp * (2.0 * u01(draw(key, 3, (uint64_t)k)) - 1.0);
+                    if (k == 0) nz_hi = noise_bits(key, st);
+                    u = nz_hi;
                 }
+                noise = noise_of(noise_amp, u);
+            } else {
+                noise = 1.0;
             }
             const double measured = smin(offered, capacity) * noise;
             energy += sys_w * sp.interval_s;

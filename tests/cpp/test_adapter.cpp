@@ -535,8 +535,11 @@ int main(int argc, char** argv) {
                 n.node_budget = detail::trace_value(t.budget_trace, t0);
                 const double cap = detail::enforce_cap(ps.applied_cap_w, ps.batch_cap, n, gspec, k);
                 const OperatingPoint p{cap, ps.batch_cap, n.cfg.tp, n.cfg.ep, n.cfg.dp};
-                std::uint64_t x = t.noise_key ^ (std::uint64_t{3} << 48) ^ static_cast<std::uint64_t>(step);
-                const double u = static_cast<double>(splitmix64(x) >> 11) * 0x1.0p-53;
+                // plant noise: one splitmix64 draw per step pair, 32 bits per step
+                const std::uint64_t x = t.noise_key ^ (std::uint64_t{3} << 48) ^
+                                        static_cast<std::uint64_t>(step >> 1);
+                const double u = static_cast<double>(static_cast<std::uint32_t>(
+                                     splitmix64(x) >> (32 * (step & 1)))) * 0x1.0p-32;
                 const double measured = std::min(detail::trace_value(t.load_trace, t0),
                                                  cluster_throughput(p, pm, gspec)) *
                                         (1.0 + t.noise_amp * (2.0 * u - 1.0));

@@ -12,7 +12,8 @@ import os
 from . import abi
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpals_gpu.so")
+# PALS_GPU_LIB: an alternative in-tree build of the same library (kernel A/B variants)
+LIB_PATH = os.environ.get("PALS_GPU_LIB") or os.path.join(_HERE, "libpals_gpu.so")
 
 _VP = C.c_void_p
 _I = C.c_int

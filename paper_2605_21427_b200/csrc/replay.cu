@@ -255,7 +255,9 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
         noise_amp = sp.noise_amp;
     }
     const ReplayModelDev& m = s_models[mi];
-    const double target = target_tps * (1.0 + cfg.target_headroom);
+    // the select target (controller.hpp:137), recomputed where used: one DMUL is cheaper than
+    // two registers held across the step loop
+#define RP_TARGET (target_tps * (1.0 + cfg.target_headroom))
 
     // ControllerState (controller.hpp:55-63)
     double bias = 1.0, integral = 0.0, prev_err = 0.0;
@@ -304,10 +306,10 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
             return;
         }
     }
-    // enforce_cap memo (a pure function of applied cap, batch cap and node budget; keyed
-    // on last_budget, c_a = -1 forces the first evaluation)
-    int c_a = -1, c_b = -1;
-    int cj = 0;  // walk position of the enforced cap (cap = walk_c[c_a][cj], logs only)
+    // enforce_cap memo (a pure function of applied cap, batch cap and node budget): keyed
+    // on c_ab = cap index * nb + batch index and last_budget; c_ab = -1 forces an evaluation
+    int c_ab = -1;
+    int cj = 0;  // walk position of the enforced cap (logged traces only)
     double capacity = 0.0, sys_w = 0.0;
     int kp = m.nd_p;
     bool kp_ok = false;  // kp counts the candidates within last_budget's select budget
@@ -320,6 +322,23 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
     const bool logging = logs && ti < sp.n_log_traces && (!kWarp || lane == 0);
     double noise_lane = 1.0;  // warp layout: noise of step (k & ~31) + lane
     uint32_t nz_hi = 0;       // thread layout: the odd step's half of the pair's draw
+    // thread layout: the noise of step kk, one draw per step pair (the high half of the
+    // pair's draw waits in nz_hi for the odd step; noise_amp == 0 gives 1 + 0 * x = 1
+    // exactly, so caller traces without noise skip the draw)
+    auto draw_noise = [&](int kk) {
+        if (kTr && noise_amp == 0.0) return 1.0;
+        const uint64_t st = kTr ? (uint64_t)(p.tr.first_step + kk) : (uint64_t)kk;
+        uint32_t u;
+        if (!(st & 1)) {
+            const uint64_t r = draw(key, 3, st >> 1);
+            u = (uint32_t)r;
+            nz_hi = (uint32_t)(r >> 32);
+        } else {
+            if (kk == 0) nz_hi = noise_bits(key, st);
+            u = nz_hi;
+        }
+        return noise_of(noise_amp, u);
+    };
     // control_step's stale-telemetry test (controller.hpp:217) with now = telemetry.t = t1:
     // t1 - t1 is +0 for every step (the host checked that all step times are finite), so
     // the test is one constant per call
@@ -330,6 +349,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
 
     auto steps = [&](auto pid_tag) {
         constexpr bool kPid = decltype(pid_tag)::value;
+        // dp * score(current).throughput_tps (controller.hpp:229), reloaded when current moves
         for (int k = 0; k < sp.n_steps; ++k) {
             double node_budget = 0.0;
             if constexpr (kTr) {
@@ -341,7 +361,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
                                         m.p_min, sp.budget_hi_frac, m.p_max);
             }
             // b_eff = batch_cap (fluid plant: the queue always covers the batch cap)
-            if (applied_a != c_a || batch_b != c_b || node_budget != last_budget) {
+            if (applied_a * m.nb + batch_b != c_ab || node_budget != last_budget) {
                 // enforce_cap (sim.hpp:195-205): walk down in 5 W steps until the cluster
                 // draw fits the budget; no budget -> the applied cap itself
                 const double* wc = m.walk_c + (int64_t)applied_a * m.L;
@@ -374,11 +394,10 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
                         j = lo;
                     }
                 }
-                cj = j;
                 capacity = (double)m.dp * m.walk_T[wo + j];
                 sys_w = m.walk_pn[wo + j];  // = dp * (alpha * 4 * P + beta) (sim.hpp:413-414)
-                c_a = applied_a;
-                c_b = batch_b;
+                c_ab = applied_a * m.nb + batch_b;
+                if (logging) cj = j;
             }
             double offered, noise;
             if constexpr (kTr) offered = lsig.at(k, sp.n_steps, p.tr.first_step, sp.interval_s);
@@ -388,22 +407,8 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
                 if ((k & 31) == 0 && k + lane < sp.n_steps)
                     noise_lane = noise_of(noise_amp, noise_bits(key, (uint64_t)(k + lane)));
                 noise = __shfl_sync(0xffffffffu, noise_lane, k & 31);
-            } else if (!kTr || noise_amp != 0.0) {
-                // (noise_amp == 0 gives 1 + 0 * x = 1 exactly: the draw is skipped, not changed)
-                // one draw per step pair; its high half waits in nz_hi for the odd step
-                const uint64_t st = kTr ? (uint64_t)(p.tr.first_step + k) : (uint64_t)k;
-                uint32_t u;
-                if (!(st & 1)) {
-                    const uint64_t r = draw(key, 3, st >> 1);
-                    u = (uint32_t)r;
-                    nz_hi = (uint32_t)(r >> 32);
-                } else {
-                    if (k == 0) nz_hi = noise_bits(key, st);
-                    u = nz_hi;
-                }
-                noise = noise_of(noise_amp, u);
             } else {
-                noise = 1.0;
+                noise = draw_noise(k);
             }
             const double measured = smin(offered, capacity) * noise;
             energy += sys_w * sp.interval_s;
@@ -460,16 +465,17 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
                     }
                     if (obj == PALS_OBJ_QOS) {
                         if (kWarp) {
+                            const double target = RP_TARGET;
                             const bool ok_lo = kt == 0 || !(m.ut[kt - 1] * bias < target);
                             const bool ok_hi = kt == m.nd_t || (m.ut[kt] * bias < target);
                             if (!(ok_lo && ok_hi))
                                 kt = warp_leading_true(m.nd_t,
                                                        [&](int i) { return !(m.ut[i] * bias < target); });
                         } else {
-                            kt = count_t_feasible(m, bias, target, kt);
+                            kt = count_t_feasible(m, bias, RP_TARGET, kt);
                         }
                     }
-                    table_select(m, target, bset, budget, kp, kt, bias, obj, &s_idx, &s_reason);
+                    table_select(m, RP_TARGET, bset, budget, kp, kt, bias, obj, &s_idx, &s_reason);
                 }
                 kp_ok = bset && (may_apply || (kp_ok && last_budget == node_budget));
                 has_last = true;
@@ -489,14 +495,14 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
                 }
             }
             // stale steps leave ControllerState (and last_budget) untouched: no memo then
-            if (stale) c_a = -1;
+            if (stale) c_ab = -1;
             const uint64_t word = ((uint64_t)(uint32_t)d_idx << 8) | ((uint64_t)d_applied << 4) |
                                   (uint64_t)d_reason;
             h = (h ^ word) * 0x100000001b3ULL;
             n_applied += d_applied;
             if (logging) {
                 pals_step_log* lg = logs + ti * (int64_t)sp.n_steps;
-                const double cap = m.walk_c[(int64_t)c_a * m.L + cj];
+                const double cap = m.walk_c[(int64_t)(c_ab / m.nb) * m.L + cj];
                 pals_step_log r;
                 r.idx = d_idx;
                 r.applied = (uint8_t)d_applied;

@@ -90,15 +90,18 @@ __device__ inline void thread_select_full(const ReplayModelDev& m, double target
 
 // select_config via the rank tables; exact by the near-tie argument of DESIGN.md §3.
 // Kt = #sorted t_hat entries with !(t*bias < target), kept incrementally: bias moves
-// a little each step, so the previous count is re-validated with two exact tests
-// before falling back to a binary search (same value either way). (A bounded walk
-// from the previous count before the search measured 10-33 % slower on B200.)
+// a little each step, so the previous count is re-validated with two exact tests (two
+// independent loads) before falling back to a binary search (same value either way),
+// narrowed to the side of prev the failing test points to. (A bounded walk from prev and
+// a 4-ary search with three independent probes per round both measured slower on B200:
+// they hold more registers in a kernel that is register-limited.)
 __device__ __forceinline__ int count_t_feasible(const ReplayModelDev& m, double bias,
                                                    double target, int prev) {
     const bool ok_lo = prev == 0 || !(m.ut[prev - 1] * bias < target);
     const bool ok_hi = prev == m.nd_t || (m.ut[prev] * bias < target);
     if (ok_lo && ok_hi) return prev;
-    int lo = 0, hi = m.nd_t;
+    // the count lies in [lo, hi]; a failing test narrows it to one side of prev
+    int lo = ok_lo ? prev + 1 : 0, hi = ok_lo ? m.nd_t : prev - 1;
     while (lo < hi) {
         const int mid = (lo + hi) >> 1;
         if (!(m.ut[mid] * bias < target)) lo = mid + 1;

@@ -466,7 +466,7 @@ def run_ours(args, dist: Dist):
     # ---------------- allocate_budget over many clusters ----------------
     allocations = bench_allocations(args, dist, ctx, stream, l2_flush)
     frontiers = bench_frontiers(args, dist, ctx, stream, l2_flush)
-    cfg3, c3, tref3 = bench_cfg3(args, dist, ctx, stream, l2_flush, int_peak)
+    cfg3, c3, tref3, gpu_cfg3 = bench_cfg3(args, dist, ctx, stream, l2_flush, int_peak)
     cfg5 = bench_cfg5(args, dist, ctx, stream, l2_flush) if args.cfg5_traces > 0 else None
     scen = bench_sim(args, dist, ctx) if args.sim_seeds > 0 else None
 
@@ -502,10 +502,8 @@ def run_ours(args, dist: Dist):
         "n_gpus": dist.world, "gpus_requested": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": SELECT_WORKLOAD, "queries_per_gpu": nq, "configs": n_cfg,
-                   "scanned_queries_per_gpu": scanned_q, "exact_fold_queries": exact_q,
-                   "global_batch": nq * dist.world, "parallelism": f"shard{dist.world}",
-                   "l2": "flushed between steps (256 MiB device write)"},
+        "config": select_config_dict(args, dist.world, n_cfg),
+        "select_stats": {"scanned_queries_per_gpu": scanned_q, "exact_fold_queries": exact_q},
         "e2e": {"value": e2e_value, "unit": "config evals/s",
                 "h2d_bytes_per_step": nq * QUERY_DT.itemsize,
                 "d2h_bytes_per_step": nq * 5,
@@ -533,20 +531,79 @@ def run_ours(args, dist: Dist):
         "peaks": {"int_ops_per_s": int_peak, "fp64_flops_per_s": fp64_peak,
                   "hbm_gbs_measured": measured_peaks_json().get("hbm_gbs")},
     }
+    cfg5_summ = cfg5.pop("_summaries", None) if cfg5 else None
+    sim_nres = scen.pop("_node_results", None) if scen else None
+    sim_res = scen.pop("_results", None) if scen else None
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"], out["decisions"]["cpu_baseline"] = cpu_baselines(args, cfg, tref)
+        # the reference legs time the unmodified code on the same inputs; their results are
+        # kept and compared with the GPU results of the same queries / traces / scenarios
+        r2, r4, r3, rs = {}, {}, {}, {}
+        out["cpu_baseline"] = cpu_select(args, cfg, tref, args.cpu_seconds, results=r2)
+        out["decisions"]["cpu_baseline"] = cpu_replay(args, args.cpu_seconds, results=r4)
         out["predictions"]["cpu_baseline"] = cpu_predict(args, bundle, args.cpu_seconds)
         out["allocations"]["cpu_baseline"] = cpu_allocate(args, args.cpu_seconds)
         out["frontiers"]["cpu_baseline"] = cpu_frontier(args.cpu_seconds)
-        out["cfg3"]["cpu_baseline"] = cpu_cfg3(args, c3, tref3, args.cpu_seconds)
+        out["cfg3"]["cpu_baseline"] = cpu_cfg3(args, c3, tref3, args.cpu_seconds, results=r3)
         if cfg5 is not None:  # same per-trace work as cfg4: the cfg4 reference sample
             out["cfg5"]["cpu_baseline"] = dict(out["decisions"]["cpu_baseline"])
         if scen is not None:
-            out["scenarios"]["cpu_baseline"] = cpu_sim(args, args.cpu_seconds)
+            out["scenarios"]["cpu_baseline"] = cpu_sim(args, args.cpu_seconds, results=rs)
         out["latency"]["cpu_reference_select_config_us"] = cpu_latency(c1, float(th1.max()))
+        out["parity"] = bench_parity(args, r2, (h_idx, h_rs), r3, gpu_cfg3, r4, h_sumn,
+                                     cfg5_summ, rs, sim_nres, sim_res)
     if dist.rank == 0:
         print(json.dumps(out), flush=True)
     dist.close()
+
+
+def bench_parity(args, r2, g2, r3, g3, r4, g4, g5, rs, g_nres, g_res):
+    """Bench-scale parity: every decision / trace summary / scenario result the reference
+    legs computed on this box, compared with the GPU's for the same inputs (the public
+    host-buffer API's outputs for cfg2 / cfg3 / cfg4). Plus one extra reference shard at the
+    far end of cfg5's 1e7 traces (global trace offsets)."""
+    par = {}
+    if r2.get("index") is not None:
+        n = len(r2["index"])
+        p = parity_of(g2[0][:n], r2["index"])
+        p["mismatches"] += int((g2[1][:n] != r2["reason"]).sum())
+        p["what"] = "cfg2 select_config decisions (index and reason) of the reference sample"
+        par["cfg2"] = p
+    if r3.get("index") is not None:
+        n = len(r3["index"])
+        p = parity_of(g3[0][:n], r3["index"])
+        p["mismatches"] += int((g3[1][:n] != r3["reason"]).sum())
+        p["what"] = "cfg3 decisions, the prefix of the 1e6 queries the reference decided"
+        par["cfg3"] = p
+    if r4.get("summaries") is not None:
+        par["cfg4"] = dict(parity_of(g4, r4["summaries"]),
+                           what="cfg4 per-trace summaries (control-step digest, final bias and "
+                                "point, energy, tokens, applied count)")
+    if g5 is not None and r4.get("summaries") is not None:
+        # cfg5 trace i is cfg4 trace i (same generator and seed): the head of cfg5 against
+        # the cfg4 sample, the tail against one more reference shard
+        from oracle.oracle import Reference
+        from paper_2605_21427_b200 import workloads
+        s = workloads.cfg4_setup()
+        n_tail = min(20_000, len(g5))
+        spec = workloads.replay_spec(n_tail, n_steps=args.trace_steps, seed=2605,
+                                     first=len(g5) - n_tail)
+        _, tail = Reference().bench_replay(s["profiles"], s["gpu"], s["coeffs"], s["caps"],
+                                           s["batches"], s["cfg"], spec, os.cpu_count() or 1)
+        head = parity_of(g5, r4["summaries"])
+        tl = parity_of(g5[len(g5) - n_tail:], tail)
+        par["cfg5"] = {"checked": head["checked"] + tl["checked"],
+                       "mismatches": head["mismatches"] + tl["mismatches"],
+                       "against": head["against"],
+                       "what": f"cfg5 per-trace summaries: the first {head['checked']} and the "
+                               f"last {tl['checked']} of {len(g5)} traces"}
+    if rs.get("results") is not None and g_nres is not None:
+        pn = parity_of(g_nres, rs["node_results"])
+        pr = parity_of(g_res, rs["results"])
+        par["scenarios"] = {"checked": pr["checked"], "mismatches": pr["mismatches"] +
+                            pn["mismatches"], "against": pr["against"],
+                            "what": f"run_scenario RunSummary of {pr['checked']} scenarios and "
+                                    f"{pn['checked']} node summaries"}
+    return par
 
 
 def replay_layouts(args, dist, ctx, stream, l2_flush, models, s, spec, thread_value):
@@ -872,6 +929,32 @@ def bench_cfg3(args, dist, ctx, stream, l2_flush, int_peak):
         e2e_ms.append(a.elapsed_time(b))
     e2e_max = dist.max(float(np.sum(e2e_ms)))
     scan_avg = float(np.mean(scan_ms))
+    # strong scaling: the 1e6 queries in total, contiguous shards over the ranks (at N = 1
+    # the same work as the weak leg)
+    from paper_2605_21427_b200.shard import shard_range
+    s_first, s_n = shard_range(nq, dist.rank, dist.world)
+    qs = workloads.gen_queries(max(1, s_n), c["seed"], tref, c["objective"], budget=c["budget"],
+                               first=s_first)
+    d_qs = torch.from_numpy(qs.view(np.uint8).copy()).cuda()
+    steps_s = lambda: plan.run(d_qs.data_ptr(), s_n, d_idx.data_ptr(), d_rs.data_ptr())  # noqa
+    steps_s()
+    torch.cuda.synchronize()
+    cnt_s = plan.stats()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    dist.barrier()
+    for k in range(args.steps):
+        l2_flush()
+        evs[k][0].record(stream)
+        steps_s()
+        evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    ts = dist.max(float(np.sum([e0.elapsed_time(e1) for e0, e1 in evs])))
+    pairs_s = dist.sum(float((cnt_s[0] + cnt_s[1] + cnt_s[2]) * n_cfg)) * args.steps
+    strong = {"scaling": "strong", "queries_total": nq, "queries_this_rank": s_n,
+              "value": pairs_s / (ts * 1e-3), "unit": "config evals/s",
+              "ms_per_step": ts / args.steps,
+              "queries_per_s": float(nq) * args.steps / (ts * 1e-3)}
     # the optional EP x DP extension of cfg3: 589,824 configs, 64-bit keys
     cx = workloads.cfg3_extended()
     planx = Plan(AnalyticModel(ctx, cx["profile"], cx["gpu"]), Grid(ctx, cx["points"]),
@@ -915,11 +998,12 @@ def bench_cfg3(args, dist, ctx, stream, l2_flush, int_peak):
                         "frac": int_ops_step / (scan_avg * 1e-3) / int_peak,
                         "algorithmic": "2 int ops per scanned pair (4 for QoS+budget queries)",
                         "scan_share_of_step": scan_avg / float(np.mean(step_ms))},
-           "gpu_launches": int(launches), "extended_grid": extended}
-    return out, c, tref
+           "gpu_launches": int(launches), "extended_grid": extended, "scaling": "weak",
+           "strong": strong}
+    return out, c, tref, (h_idx, h_rs)
 
 
-def cpu_cfg3(args, c, tref, seconds):
+def cpu_cfg3(args, c, tref, seconds, results=None):
     """cfg3 queries through the unmodified select_config + analytic_scorer, all threads."""
     from paper_2605_21427_b200 import workloads
     kind, ref = _reference_backend()
@@ -933,8 +1017,10 @@ def cpu_cfg3(args, c, tref, seconds):
                                want_results=False)
     nq = int(min(args.cfg3_queries, max(threads, len(q) * n / t * seconds / n)))
     q = workloads.gen_queries(nq, c["seed"], tref, c["objective"], budget=c["budget"])
-    t, _, _ = ref.bench_select(c["profile"], c["gpu"], c["points"], c["coeffs"], q, threads,
-                               want_results=False)
+    t, ri, rr = ref.bench_select(c["profile"], c["gpu"], c["points"], c["coeffs"], q, threads,
+                                 want_results=results is not None)
+    if results is not None:
+        results.update(index=ri, reason=rr)
     return {"value": nq * n / t, "unit": "config evals/s", "cores": threads, "kind": "reference",
             "sample": f"first {nq} of the 1e6 cfg3 queries x {n} configs through the unmodified "
                       f"select_config+analytic_scorer, {threads} threads, {t:.1f} s"}
@@ -1010,7 +1096,8 @@ def bench_cfg5(args, dist, ctx, stream, l2_flush):
                     "api": "pals_replay_device, then the summary gather to rank 0 and its "
                            "D2H into pinned host memory (the gather+D2H time is added once "
                            "per step)"},
-            "gpu_launches": int(launches)}
+            "gpu_launches": int(launches),
+            "_summaries": None if host is None else host.numpy().reshape(-1).view(SUMMARY_DT)}
 
 
 SIM_WORKLOAD = ("queue-plant run_scenario (sim.hpp) over the 3 bundled scenarios (single_node "
@@ -1079,10 +1166,10 @@ def bench_sim(args, dist, ctx):
                     "host_setup_s": float(np.mean(preps)),
                     "api": "pals_run_scenarios (C ABI): host arrival streams (mt19937_64 + libm) "
                            "and budget splits, then one k_sim launch; wall clock"},
-            "gpu_launches": None}
+            "gpu_launches": None, "_node_results": nres, "_results": res}
 
 
-def cpu_sim(args, seconds):
+def cpu_sim(args, seconds, results=None):
     """The unmodified run_scenario + summarize on all host threads over the first seeds of
     the same suite."""
     kind, ref = _reference_backend()
@@ -1100,9 +1187,14 @@ def cpu_sim(args, seconds):
     scs, units = sim_suite(1)
     t = ref.bench_scenarios(scs, profs, gpu, coeffs, path, threads)
     seeds = int(max(1, min(args.sim_seeds, seconds / max(t, 1e-3))))
-    if seeds > 1:
+    if seeds > 1 or results is not None:
         scs, units = sim_suite(seeds)
-        t = ref.bench_scenarios(scs, profs, gpu, coeffs, path, threads)
+        out = ref.bench_scenarios(scs, profs, gpu, coeffs, path, threads,
+                                  want_results=results is not None)
+        if results is not None:  # the sample's node results and RunSummary per scenario
+            t, results["node_results"], results["results"] = out
+        else:
+            t = out
     return {"value": units / t, "unit": "node-intervals/s", "cores": threads,
             "kind": "reference",
             "sample": f"{len(scs)} scenarios ({seeds} seeds x 3 bundled x 5 policies) through "
@@ -1218,8 +1310,26 @@ def _reference_backend():
     return "port", Oracle()
 
 
-def cpu_select(args, cfg, tref, seconds):
-    """select_config + analytic_scorer over cfg2 queries on all host threads."""
+def select_config_dict(args, world, n_cfg=65_536):
+    """The headline workload's config, identical in both arms (the driver compares them)."""
+    return {"workload": SELECT_WORKLOAD, "queries_per_gpu": args.queries, "configs": n_cfg,
+            "global_batch": args.queries * world, "parallelism": f"shard{world}",
+            "l2": "flushed between GPU steps (256 MiB device write)"}
+
+
+def parity_of(got, want, against="oracle/_ref (the unmodified reference headers)"):
+    """{checked, mismatches, against}: element-wise (per record, all bytes) comparison."""
+    got = np.ascontiguousarray(got)
+    want = np.ascontiguousarray(want)
+    n = min(len(got), len(want))
+    g = got[:n].view(np.uint8).reshape(n, -1)
+    w = want[:n].view(np.uint8).reshape(n, -1)
+    return {"checked": int(n), "mismatches": int((g != w).any(1).sum()), "against": against}
+
+
+def cpu_select(args, cfg, tref, seconds, results=None):
+    """select_config + analytic_scorer over cfg2 queries on all host threads. `results`
+    (a dict) receives the reference's decisions for the timed sample."""
     from paper_2605_21427_b200 import workloads
     kind, ref = _reference_backend()
     threads = os.cpu_count() or 1
@@ -1231,8 +1341,10 @@ def cpu_select(args, cfg, tref, seconds):
         rate = len(q) * n / t
         nq = int(min(args.queries, max(threads, rate * seconds / n)))
         q = workloads.gen_queries(nq, cfg["seed"], tref, "qos")
-        t, _, _ = ref.bench_select(cfg["profile"], cfg["gpu"], cfg["points"], cfg["coeffs"], q,
-                                   threads, want_results=False)
+        t, ri, rr = ref.bench_select(cfg["profile"], cfg["gpu"], cfg["points"], cfg["coeffs"], q,
+                                     threads, want_results=results is not None)
+        if results is not None:
+            results.update(index=ri, reason=rr)
         return {"value": nq * n / t, "unit": "config evals/s", "cores": threads,
                 "kind": "reference",
                 "sample": f"{nq} cfg2 queries x {n} configs through the unmodified "
@@ -1247,7 +1359,7 @@ def cpu_select(args, cfg, tref, seconds):
             "sample": f"{len(q)} cfg2 queries, C restatement, 1 thread"}
 
 
-def cpu_replay(args, seconds):
+def cpu_replay(args, seconds, results=None):
     from paper_2605_21427_b200 import workloads
     kind, ref = _reference_backend()
     s = workloads.cfg4_setup()
@@ -1259,8 +1371,10 @@ def cpu_replay(args, seconds):
         rate = probe.n_traces * args.trace_steps / t
         ntr = int(max(threads, min(args.traces, rate * seconds / args.trace_steps)))
         spec = workloads.replay_spec(ntr, n_steps=args.trace_steps, seed=2605)
-        t, _ = ref.bench_replay(s["profiles"], s["gpu"], s["coeffs"], s["caps"], s["batches"],
-                                s["cfg"], spec, threads)
+        t, summ = ref.bench_replay(s["profiles"], s["gpu"], s["coeffs"], s["caps"], s["batches"],
+                                   s["cfg"], spec, threads)
+        if results is not None:
+            results["summaries"] = summ
         return {"value": ntr * args.trace_steps / t, "unit": "decisions/s", "cores": threads,
                 "kind": "reference",
                 "sample": f"{ntr} cfg4 traces x {args.trace_steps} steps through the unmodified "
@@ -1308,10 +1422,6 @@ def cpu_latency(c1, tmax):
     return t / len(q) * 1e6
 
 
-def cpu_baselines(args, cfg, tref):
-    return cpu_select(args, cfg, tref, args.cpu_seconds), cpu_replay(args, args.cpu_seconds)
-
-
 def run_reference(args, dist: Dist):
     """The reference's own CPU implementation of the path, all host threads, rank 0."""
     if dist.rank != 0:
@@ -1345,7 +1455,7 @@ def run_reference(args, dist: Dist):
            "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": SELECT_WORKLOAD, "queries_per_gpu": args.queries},
+           "config": select_config_dict(args, dist.world, len(cfg["points"])),
            "cpu_baseline": vals[-1],
            "e2e": {"value": v, "unit": "config evals/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0},

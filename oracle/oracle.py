@@ -317,24 +317,30 @@ class Reference:
             out = out + ((tcsv, dcsv, rcsv),)
         return out
 
-    def bench_scenarios(self, scenarios, profiles, gpu, coeffs, bundle_path, threads):
-        """Wall seconds of run_scenario + summarize over the scenario dicts, threads-way."""
-        from paper_2605_21427_b200.abi import Scenario
+    def bench_scenarios(self, scenarios, profiles, gpu, coeffs, bundle_path, threads,
+                        want_results=False):
+        """Wall seconds of run_scenario + summarize over the scenario dicts, threads-way;
+        with want_results also (node_results, results) in scenario order."""
+        from paper_2605_21427_b200.abi import SIM_NODE_RESULT_DT, SIM_RESULT_DT, Scenario
         from paper_2605_21427_b200.sim import _CScenario, _model_index
         L = self.lib
         L.ref_bench_scenarios.restype = C.c_double
         L.ref_bench_scenarios.argtypes = [C.c_int, _VP, C.c_int, _VP, C.c_char_p, _VP, _VP,
-                                          C.c_int]
+                                          C.c_int, _VP, _VP]
         idx = _model_index(profiles)
         cs = [_CScenario(s, idx) for s in scenarios]
         arr = (Scenario * len(cs))(*[c.c for c in cs])
         profs = (Profile * len(profiles))(*profiles)
+        nres = np.zeros(sum(len(s["nodes"]) for s in scenarios), SIM_NODE_RESULT_DT)
+        res = np.zeros(len(scenarios), SIM_RESULT_DT)
         secs = L.ref_bench_scenarios(len(cs), arr, len(profiles), profs,
                                      bundle_path.encode() if bundle_path else None,
-                                     C.byref(gpu), C.byref(coeffs), threads)
+                                     C.byref(gpu), C.byref(coeffs), threads,
+                                     ptr(nres) if want_results else None,
+                                     ptr(res) if want_results else None)
         if secs < 0:
             raise RuntimeError("ref_bench_scenarios: a scenario failed")
-        return secs
+        return (secs, nres, res) if want_results else secs
 
     def bench_select(self, prof, gpu, pts, coeffs, queries, threads, want_results=True):
         nq = len(queries)

@@ -1279,9 +1279,12 @@ extern "C" {
 // CPU baseline: run_scenario + summarize over scenarios split across threads (wall s).
 double ref_bench_scenarios(int n_scen, const pals_scenario* s, int n_models,
                            const pals_profile* profs, const char* bundle_path,
-                           const pals_gpu_spec* gpu, const pals_coeffs* coeffs, int n_threads) {
+                           const pals_gpu_spec* gpu, const pals_coeffs* coeffs, int n_threads,
+                           pals_sim_node_result* node_out, pals_sim_result* res_out) {
     if (bundle_path) load_bundle(bundle_path);  // parse once, before the threads share it
     std::vector<int> rc(n_scen, 0);
+    std::vector<std::int64_t> node_off(n_scen + 1, 0);
+    for (int i = 0; i < n_scen; ++i) node_off[i + 1] = node_off[i] + s[i].n_nodes;
     const auto t0 = std::chrono::steady_clock::now();
     std::vector<std::thread> th;
     std::atomic<int> next{0};
@@ -1292,6 +1295,9 @@ double ref_bench_scenarios(int n_scen, const pals_scenario* s, int n_models,
                 pals_sim_result r;
                 rc[i] = ref_run_scenario(&s[i], n_models, profs, bundle_path, gpu, coeffs,
                                          nr.data(), &r, 0, nullptr, nullptr, nullptr, 0, nullptr);
+                if (node_out)
+                    std::memcpy(node_out + node_off[i], nr.data(), nr.size() * sizeof(nr[0]));
+                if (res_out) res_out[i] = r;
             }
         });
     for (auto& x : th) x.join();

@@ -79,7 +79,10 @@ def test_select_near_tie_tables(ctx, bundle, gold):
     assert n_exact > 0  # the near-tie fallback was exercised
 
 
-def test_select_cfg2_all_queries_vs_oracle(ctx, oracle):
+def test_select_cfg2_all_queries_vs_reference(ctx, reference):
+    """Every one of the 1e4 cfg2 bench queries (and 2,000 budget-variant queries) against
+    the unmodified select_config + analytic_scorer (oracle/_ref, all host threads)."""
+    import os
     cfg = workloads.cfg2()
     model = AnalyticModel(ctx, cfg["profile"], cfg["gpu"])
     plan = Plan(model, Grid(ctx, cfg["points"]), cfg["coeffs"])
@@ -87,15 +90,16 @@ def test_select_cfg2_all_queries_vs_oracle(ctx, oracle):
     tref = float(th.max())
     q = workloads.gen_queries(10_000, 2605, tref, "qos")
     idx, rs = plan.select(q)
-    T, P, _ = oracle.eval(cfg["profile"], cfg["gpu"], cfg["points"])
-    sub = np.arange(0, 10_000, 10)
-    oi, orr, rc = oracle.select(cfg["points"], T, P, cfg["coeffs"], q[sub])
-    assert np.array_equal(idx[sub], oi) and np.array_equal(rs[sub], orr)
+    threads = os.cpu_count() or 1
+    _, ri, rr = reference.bench_select(cfg["profile"], cfg["gpu"], cfg["points"],
+                                       cfg["coeffs"], q, threads)
+    assert np.array_equal(idx, ri) and np.array_equal(rs, rr)
     # the budget variant
     qb = workloads.gen_queries(2_000, 2606, tref, "qos", budget=(600.0, 2000.0))
     idx, rs = plan.select(qb)
-    oi, orr, rc = oracle.select(cfg["points"], T, P, cfg["coeffs"], qb[::4])
-    assert np.array_equal(idx[::4], oi) and np.array_equal(rs[::4], orr)
+    _, ri, rr = reference.bench_select(cfg["profile"], cfg["gpu"], cfg["points"],
+                                       cfg["coeffs"], qb, threads)
+    assert np.array_equal(idx, ri) and np.array_equal(rs, rr)
 
 
 def test_select_cfg3_million_queries(ctx, oracle):

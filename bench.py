@@ -597,8 +597,18 @@ def bench_parity(args, r2, g2, r3, g3, r4, g4, g5, rs, g_nres, g_res):
                        "what": f"cfg5 per-trace summaries: the first {head['checked']} and the "
                                f"last {tl['checked']} of {len(g5)} traces"}
     if rs.get("results") is not None and g_nres is not None:
-        pn = parity_of(g_nres, rs["node_results"])
-        pr = parity_of(g_res, rs["results"])
+        # the reference's MetricsSummary / RunSummary fields (final_idx and
+        # n_budget_changes are GPU-side bookkeeping the harness does not fill)
+        nf = ["tokens_per_joule", "qos_violation_rate", "power_tracking_mae_w", "total_tokens",
+              "total_energy_j", "mean_throughput_tps", "throughput_target_tps", "final_bias",
+              "arrival_stream_hash", "n_requests", "n_completed", "n_applied"]
+        rf = ["tokens_per_joule", "qos_violation_rate", "power_tracking_mae_w", "total_tokens",
+              "total_energy_j", "mean_throughput_tps", "cluster_tracking_mae_w",
+              "sim_total_energy_j", "n_intervals"]
+        from numpy.lib.recfunctions import repack_fields
+        nn, ns = len(rs["node_results"]), len(rs["results"])
+        pn = parity_of(repack_fields(g_nres[:nn][nf]), repack_fields(rs["node_results"][nf]))
+        pr = parity_of(repack_fields(g_res[:ns][rf]), repack_fields(rs["results"][rf]))
         par["scenarios"] = {"checked": pr["checked"], "mismatches": pr["mismatches"] +
                             pn["mismatches"], "against": pr["against"],
                             "what": f"run_scenario RunSummary of {pr['checked']} scenarios and "

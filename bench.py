@@ -332,20 +332,17 @@ def run_ours(args, dist: Dist):
     e2e_value = pairs_total / (e2e_max * 1e-3)
 
     scan_avg = float(np.mean(scan_ms))
-    roof = {"bound": "alu", "kernel": "k_scan",
-            "achieved": int_ops_step / (scan_avg * 1e-3) / 1e12,
-            "peak": int_peak / 1e12, "unit": "Tops/s",
-            "frac": (int_ops_step / (scan_avg * 1e-3)) / int_peak,
-            "traffic": ncu_traffic("k_scan"),
-            "algorithmic": "2 int ops (compare, min) per scanned (config, query) pair; 4 for "
-                           "QoS+budget queries",
-            "peak_source": "measured here: pals_measure_peaks chains of the scan's per-pair "
-                           "instruction mix (IMAD.IADD + LOP3 + VIMNMX3 per 2 pairs), 2 ops/pair",
-            "scan_share_of_step": scan_avg / float(np.mean(step_ms)),
-            "step_breakdown_ms": {"graph_step": float(np.mean(step_ms)),
-                                  "scan_kernel": scan_avg,
-                                  "ungraphed_step": float(np.mean(split_ms)),
-                                  "ungraphed_prepare(eval+rank)": float(np.mean(prep_ms))}}
+    roof_counts = (counts, n_cfg, scan_avg)
+    scan_extra = {"scan_share_of_step": scan_avg / float(np.mean(step_ms)),
+                  "step_breakdown_ms": {"graph_step": float(np.mean(step_ms)),
+                                        "scan_kernel": scan_avg,
+                                        "ungraphed_step": float(np.mean(split_ms)),
+                                        "ungraphed_prepare(eval+rank)": float(np.mean(prep_ms))},
+                  "chain_peak_secondary": {
+                      "value": int_peak / 1e12, "unit": "Tops/s (2 per pair)",
+                      "frac": (int_ops_step / (scan_avg * 1e-3)) / int_peak,
+                      "source": "pals_measure_peaks: dependent chains of the class-A mix "
+                                "(measured; includes the chain's own index arithmetic)"}}
 
     # ---------------- cfg4 replay ----------------
     s = workloads.cfg4_setup()
@@ -373,6 +370,11 @@ def run_ours(args, dist: Dist):
     rlaunches = ctx.launches - rl0
     r_ms = [a.elapsed_time(b) for a, b in rev]
     clk = clocks.stop()
+    roof = dict(scan_roofline(*roof_counts, clk), **scan_extra)
+    dec_roof = issue_roofline("k_replay", dec_roof_rate, "decisions", clk,
+                              "instruction issue: one dependent chain of FP64 PID arithmetic, "
+                              "table lookups and the plant per trace and step; the FP64 pipe "
+                              "runs at ~20 % of its peak (ncu), HBM is idle")
     r_max = dist.max(float(np.sum(r_ms)))
     dec_total = dist.sum(float(nt) * args.trace_steps) * rsteps
     dec_value = dec_total / (r_max * 1e-3)
@@ -400,73 +402,15 @@ def run_ours(args, dist: Dist):
     layouts = replay_layouts(args, dist, ctx, stream, l2_flush, models, s, spec, dec_value)
     args._synthetic_dec_value = dec_value
     traces_leg = bench_traces(args, dist, ctx, stream, l2_flush, models, s, spec, d_sum)
-    # FP64 work per decision in the replay kernel: PID 15 flops (2 div),
-    # plant noise/min/energy/tokens 10, target test + Kt search ~2*log2(nd_t)+4
-    fp64_per_dec = 40.0
-    dec_roof = {"bound": "fp64", "kernel": "k_replay",
-                "achieved": dec_value / dist.world * fp64_per_dec / 1e12,
-                "peak": fp64_peak / 1e12, "unit": "TFLOP/s",
-                "frac": dec_value / dist.world * fp64_per_dec / fp64_peak,
-                "traffic": ncu_traffic("k_replay"),
-                "algorithmic": f"{fp64_per_dec:.0f} FP64 ops per decision (counted in DESIGN.md "
-                               "§4); the kernel is latency-bound, not FP64-throughput-bound",
-                "peak_source": "measured here: pals_measure_peaks DFMA chains",
-                "issue_active_pct_ncu": ncu_metric("k_replay", "issue_active_pct"),
-                "eligible_warps_per_cycle_ncu": ncu_metric("k_replay", "eligible_warps_per_cycle"),
-                "note": "one dependency chain per trace: the binding resource is instruction "
-                        "issue under latency (ncu issue-active share above), not the FP64 pipe"}
+    dec_roof_rate = dec_value / dist.world  # per-GPU decisions/s, bound below with the clock
 
     # ---------------- K2: PredictorBundle::predict throughput ----------------
-    from paper_2605_21427_b200.forest import Bundle, make_forest_model
-    bundle = Bundle.load_npz(os.path.join(ROOT, "paper_2605_21427_b200", "data",
-                                          "predictor_small.npz"))
-    fmodel = make_forest_model(ctx, bundle, "mixtral-8x7b-like")
-    npred = args.predictions
-    ppts = workloads.predict_points(npred, seed=2605 + dist.rank)
-    d_pts = torch.from_numpy(ppts.view(np.uint8)).cuda()
-    d_T = torch.empty(npred, dtype=torch.float64, device="cuda")
-    d_P = torch.empty(npred, dtype=torch.float64, device="cuda")
-
-    def predict_step():
-        rc = ctx.lib.pals_predict_device(ctx.h, fmodel.h, d_pts.data_ptr(), npred,
-                                         d_T.data_ptr(), d_P.data_ptr())
-        assert rc == 0, ctx.lib.pals_last_error()
-
-    for _ in range(args.warmup):
-        predict_step()
-    torch.cuda.synchronize()
-    pev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    for k in range(args.steps):
-        l2_flush()
-        pev[k][0].record(stream)
-        predict_step()
-        pev[k][1].record(stream)
-    torch.cuda.synchronize()
-    p_max = dist.max(float(np.sum([a.elapsed_time(b) for a, b in pev])))
-    pred_value = dist.sum(float(npred)) * args.steps / (p_max * 1e-3)
-    # cell lookup: 5 binary searches over <= 10 thresholds + 2 table loads; HBM-bound part is
-    # the 24 B point read + 16 B result write per prediction
-    pred_bytes = 40.0
-    predictions = {
-        "metric": "predictor predictions/s (PredictorBundle::predict, T and P)",
-        "value": pred_value, "unit": "predictions/s", "points_per_gpu": npred,
-        "bundle": f"{bundle.throughput.n_trees}+{bundle.power.n_trees} trees, depth "
-                  f"{bundle.hyperparams['max_depth']}, trained by the reference pipeline; "
-                  f"{int(ctx.lib.pals_model_forest_cells(fmodel.h))} exact lattice cells",
-        "roofline": {"bound": "hbm", "kernel": "k_forest_eval",
-                     "achieved": pred_value / dist.world * pred_bytes / 1e9,
-                     "peak": measured_peaks_json().get("hbm_gbs", 6552.6), "unit": "GB/s",
-                     "frac": pred_value / dist.world * pred_bytes / 1e9 /
-                     measured_peaks_json().get("hbm_gbs", 6552.6),
-                     "traffic": ncu_traffic("k_forest_eval_aos"),
-                     "algorithmic": "40 B per prediction (24 B point in, 16 B T/P out)",
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs"}}
+    predictions, bundle = bench_forest(args, dist, ctx, stream, l2_flush)
 
     # ---------------- allocate_budget over many clusters ----------------
     allocations = bench_allocations(args, dist, ctx, stream, l2_flush)
     frontiers = bench_frontiers(args, dist, ctx, stream, l2_flush)
-    cfg3, c3, tref3, gpu_cfg3 = bench_cfg3(args, dist, ctx, stream, l2_flush, int_peak)
+    cfg3, c3, tref3, gpu_cfg3 = bench_cfg3(args, dist, ctx, stream, l2_flush, int_peak, clk)
     cfg5 = bench_cfg5(args, dist, ctx, stream, l2_flush) if args.cfg5_traces > 0 else None
     scen = bench_sim(args, dist, ctx) if args.sim_seeds > 0 else None
 
@@ -531,6 +475,7 @@ def run_ours(args, dist: Dist):
         "peaks": {"int_ops_per_s": int_peak, "fp64_flops_per_s": fp64_peak,
                   "hbm_gbs_measured": measured_peaks_json().get("hbm_gbs")},
     }
+    forest_kept = predictions.pop("_kept", {})
     cfg5_summ = cfg5.pop("_summaries", None) if cfg5 else None
     sim_nres = scen.pop("_node_results", None) if scen else None
     sim_res = scen.pop("_results", None) if scen else None
@@ -551,6 +496,7 @@ def run_ours(args, dist: Dist):
         out["latency"]["cpu_reference_select_config_us"] = cpu_latency(c1, float(th1.max()))
         out["parity"] = bench_parity(args, r2, (h_idx, h_rs), r3, gpu_cfg3, r4, h_sumn,
                                      cfg5_summ, rs, sim_nres, sim_res)
+        out["parity"].update(forest_parity(bundle, forest_kept))
     if dist.rank == 0:
         print(json.dumps(out), flush=True)
     dist.close()
@@ -614,6 +560,24 @@ def bench_parity(args, r2, g2, r3, g3, r4, g4, g5, rs, g_nres, g_res):
                             "what": f"run_scenario RunSummary of {pr['checked']} scenarios and "
                                     f"{pn['checked']} node summaries"}
     return par
+
+
+def forest_parity(bundle, kept):
+    """The forest leg's predictions (cell table and literal walk) against the unmodified
+    PredictorBundle::predict on the same points, bit for bit (T and P)."""
+    from oracle.oracle import Reference, ref_bundle_predict
+    path = os.path.join(tempfile.gettempdir(), "pals_bench_bundle_parity.json")
+    bundle.to_json(path)
+    ref = Reference()
+    out = {}
+    for direct, (pts, T, P) in kept.items():
+        rT, rP, _ = ref_bundle_predict(ref, path, "mixtral-8x7b-like", pts)
+        bad = (T.view(np.uint64) != rT.view(np.uint64)) | (P.view(np.uint64) != rP.view(np.uint64))
+        out["forest_direct_walk" if direct else "forest_cells"] = {
+            "checked": int(len(pts)), "mismatches": int(bad.sum()),
+            "against": "oracle/_ref (the unmodified reference headers)",
+            "what": "PredictorBundle::predict T and P bits, default 100-tree bundle"}
+    return out
 
 
 def replay_layouts(args, dist, ctx, stream, l2_flush, models, s, spec, thread_value):
@@ -758,6 +722,87 @@ def bench_traces(args, dist, ctx, stream, l2_flush, models, s, spec, d_synth):
                                   "itself checked against oracle/_ref)"}}
 
 
+def bench_forest(args, dist, ctx, stream, l2_flush):
+    """PredictorBundle::predict (forest.hpp:227-235) over random points, on the bundle at the
+    reference's default hyper-parameters (100 trees per forest, depth 14; trained by the
+    reference pipeline, data/predictor_default.npz): the exact lattice-cell table (the
+    default path) and the literal tree walk, plus the shipped 20-tree bundle."""
+    import torch
+    from paper_2605_21427_b200 import workloads
+    from paper_2605_21427_b200.forest import Bundle, make_forest_model
+    data = os.path.join(ROOT, "paper_2605_21427_b200", "data")
+    bundle = Bundle.load_npz(os.path.join(data, "predictor_default.npz"))
+    small = Bundle.load_npz(os.path.join(data, "predictor_small.npz"))
+    hbm = measured_peaks_json().get("hbm_gbs", 6552.6)
+
+    def timed(model, npts, direct, reps):
+        ctx.lib.pals_model_forest_set_direct(model.h, 1 if direct else 0)
+        pts = workloads.predict_points(npts, seed=2605 + dist.rank)
+        d_pts = torch.from_numpy(pts.view(np.uint8)).cuda()
+        d_T = torch.empty(npts, dtype=torch.float64, device="cuda")
+        d_P = torch.empty(npts, dtype=torch.float64, device="cuda")
+
+        def step():
+            rc = ctx.lib.pals_predict_device(ctx.h, model.h, d_pts.data_ptr(), npts,
+                                             d_T.data_ptr(), d_P.data_ptr())
+            assert rc == 0, ctx.lib.pals_last_error()
+
+        for _ in range(max(1, args.warmup)):
+            step()
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(reps)]
+        dist.barrier()
+        for k in range(reps):
+            l2_flush()
+            ev[k][0].record(stream)
+            step()
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+        t = dist.max(float(np.sum([a.elapsed_time(b) for a, b in ev])))
+        ctx.lib.pals_model_forest_set_direct(model.h, 0)
+        k = min(npts, 50_000)
+        kept[direct] = (pts[:k], d_T[:k].cpu().numpy(), d_P[:k].cpu().numpy())
+        return dist.sum(float(npts)) * reps / (t * 1e-3), t / reps
+
+    kept = {}
+    mid = "mixtral-8x7b-like"
+    fmodel = make_forest_model(ctx, bundle, mid)
+    npred = args.predictions
+    value, ms = timed(fmodel, npred, False, args.steps)
+    n_direct = max(1, npred // 16)
+    v_direct, ms_direct = timed(fmodel, n_direct, True, max(1, min(args.steps, 3)))
+    smodel = make_forest_model(ctx, small, mid)
+    v_small, _ = timed(smodel, npred, False, args.steps)
+    nodes = int(sum(len(f.feature) for f in (bundle.throughput, bundle.power)))
+    depth = bundle.hyperparams["max_depth"]
+    pred_bytes = 40.0  # 24 B point in, 16 B T/P out: the cell path's algorithmic traffic
+    per_gpu = value / dist.world
+    return {
+        "metric": "predictor predictions/s (PredictorBundle::predict, T and P)",
+        "value": value, "unit": "predictions/s", "ms_per_step": ms, "points_per_gpu": npred,
+        "bundle": f"{bundle.throughput.n_trees}+{bundle.power.n_trees} trees, depth {depth}, "
+                  f"{nodes} nodes (the reference's default hyper-parameters, trained by its "
+                  f"own pipeline); {int(ctx.lib.pals_model_forest_cells(fmodel.h))} exact "
+                  "lattice cells",
+        "roofline": {"bound": "hbm", "kernel": "k_forest_eval_aos",
+                     "achieved": per_gpu * pred_bytes / 1e9, "peak": hbm, "unit": "GB/s",
+                     "frac": per_gpu * pred_bytes / 1e9 / hbm,
+                     "traffic": ncu_traffic("k_forest_eval_aos"),
+                     "algorithmic": "40 B per prediction (24 B point in, 16 B T/P out)",
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+        "direct_walk": {"value": v_direct, "unit": "predictions/s", "points_per_gpu": n_direct,
+                        "ms_per_step": ms_direct,
+                        "note": "the literal per-point walk of all 200 trees (forest.hpp:80-85, "
+                                "176-180), used when a bundle's lattice exceeds 4M cells",
+                        "tree_node_visits_per_s": v_direct * 200 * depth},
+        "small_bundle": {"value": v_small, "unit": "predictions/s",
+                         "bundle": f"{small.throughput.n_trees}+{small.power.n_trees} trees, "
+                                   f"depth {small.hyperparams['max_depth']} (predictor_small)"},
+        "_kept": kept,
+    }, bundle
+
+
 def alloc_setup_gpu(ctx):
     """Allocator + per-model scales (unconstrained t_hat, peak p_node at dp 1) from the GPU."""
     from paper_2605_21427_b200 import workloads
@@ -847,15 +892,13 @@ def bench_allocations(args, dist, ctx, stream, l2_flush):
                 "h2d_bytes_per_step": int(8 * (n + 1) + 16 * nn + 8 * n),
                 "d2h_bytes_per_step": int(8 * nn + 13 * n),
                 "api": "pals_allocate_budget (C ABI, pinned host buffers)"},
-        "roofline": {"bound": "hbm", "kernel": "k_allocate", "achieved": ach, "peak": hbm,
-                     "unit": "GB/s", "frac": ach / hbm, "traffic": ncu_traffic("k_allocate"),
-                     "algorithmic": "29 B per cluster + 24 B per node",
-                     "note": "the kernel is bound by its serial per-cluster FP64 loop "
-                             "(thread per cluster), not by HBM; the byte roofline is "
-                             "reported for completeness",
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs",
-                     "issue_active_pct_ncu": ncu_metric("k_allocate", "issue_active_pct"),
-                     "fp64_pipe_pct_ncu": ncu_metric("k_allocate", "fp64_pipe_pct")},
+        "roofline": dict(issue_roofline("k_allocate", value / dist.world, "allocations", None,
+                                        "instruction issue: the reference's serial greedy "
+                                        "loop per cluster (one thread per cluster), FP64 "
+                                        "divides in the marginal-rate comparisons"),
+                         hbm_bytes_secondary={"algorithmic": "29 B per cluster + 24 B per node",
+                                              "achieved_gbs": ach, "peak_gbs": hbm,
+                                              "frac": ach / hbm}),
         "gpu_launches": int(launches),
     }
 
@@ -869,7 +912,7 @@ CFG5_WORKLOAD = ("cfg5: 1e7 fluid-plant traces in total (8 calibrated profiles: 
                  "summary gather (48 B/trace) to rank 0")
 
 
-def bench_cfg3(args, dist, ctx, stream, l2_flush, int_peak):
+def bench_cfg3(args, dist, ctx, stream, l2_flush, int_peak, clk=None):
     """BASELINE cfg3: the MoE grid with 1e6 mixed (target, budget) queries per GPU."""
     import torch
     from paper_2605_21427_b200 import workloads
@@ -1002,12 +1045,8 @@ def bench_cfg3(args, dist, ctx, stream, l2_flush, int_peak):
            "e2e": {"value": pairs_total / (e2e_max * 1e-3), "unit": "config evals/s",
                    "h2d_bytes_per_step": nq * QUERY_DT.itemsize, "d2h_bytes_per_step": nq * 5,
                    "api": "pals_select (C ABI, pinned host buffers: one graph, query upload overlapped with eval+rank, decisions stored to the mapped host buffers by the finalize kernel)"},
-           "roofline": {"bound": "alu", "kernel": "k_scan",
-                        "achieved": int_ops_step / (scan_avg * 1e-3) / 1e12,
-                        "peak": int_peak / 1e12, "unit": "Tops/s",
-                        "frac": int_ops_step / (scan_avg * 1e-3) / int_peak,
-                        "algorithmic": "2 int ops per scanned pair (4 for QoS+budget queries)",
-                        "scan_share_of_step": scan_avg / float(np.mean(step_ms))},
+           "roofline": dict(scan_roofline(cnt, n_cfg, scan_avg, clk),
+                            scan_share_of_step=scan_avg / float(np.mean(step_ms))),
            "gpu_launches": int(launches), "extended_grid": extended, "scaling": "weak",
            "strong": strong}
     return out, c, tref, (h_idx, h_rs)
@@ -1320,6 +1359,71 @@ def _reference_backend():
     return "port", Oracle()
 
 
+def issue_roofline(kernel, units_per_s, unit, clk, note):
+    """A latency / issue-bound kernel against instruction issue (one warp instruction per SMSP
+    per cycle): warp instructions per unit from the committed ncu capture of this build at the
+    bench size (smsp__inst_executed over the capture's units) x the live unit rate, over the
+    issue peak at the sampled SM clock. Also reports ncu's issue-active share."""
+    inst = ncu_metric(kernel, "warp_inst")
+    units = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02", "capture_sizes.json")) as f:
+            units = json.load(f)[kernel]["units"]
+    except Exception:
+        pass
+    mhz = (clk or {}).get("sm_mhz") or 1965.0
+    peak = 148 * 4 * mhz * 1e6
+    if not inst or not units:
+        return {"bound": "issue", "kernel": kernel, "achieved": None, "peak": peak / 1e9,
+                "unit": "G warp-instructions/s", "frac": None, "traffic": ncu_traffic(kernel),
+                "note": "no committed ncu capture for this build"}
+    per = inst / units
+    ach = per * units_per_s
+    return {"bound": "issue", "kernel": kernel, "achieved": ach / 1e9, "peak": peak / 1e9,
+            "unit": "G warp-instructions/s", "frac": ach / peak, "traffic": ncu_traffic(kernel),
+            "warp_instructions_per_" + unit.rstrip("s"): per,
+            "issue_active_pct_ncu": ncu_metric(kernel, "issue_active_pct"),
+            "peak_source": f"1 warp instruction / SMSP / cycle x 4 x 148 SMs at {mhz:.0f} MHz "
+                           "(sampled); instructions per unit from profiles/ncu_summary.json",
+            "algorithmic": note}
+
+
+def scan_mix():
+    """ALU-pipe warp instructions per (config, query) pair per thread of the pair-scan loops,
+    from the committed SASS analysis (scripts/sass_mix.py) of the build being measured."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02", "k_scan_mix.json")) as f:
+            m = json.load(f)["alu_warp_inst_per_pair_lane"]
+        return float(m["A/C"]), float(m["B"]), "profiles/r02/k_scan_mix.json"
+    except Exception:
+        return 1.5, 3.5, "built-in (LOP3 + 1/2 VIMNMX3 per A/C pair; 2 LOP3 + VIADDMNMX + 1/2 VIMNMX3 per B pair)"
+
+
+def scan_roofline(counts, n_cfg, scan_ms, clk):
+    """k_scan against the ALU pipe, the resource its instruction mix binds: ALU lane
+    operations issued per second (from the SASS mix x the pairs actually scanned) over the
+    ALU pipe's peak (16 lanes per SMSP, 4 SMSPs x 148 SMs at the SM clock sampled during
+    the run)."""
+    a_c, b, src = scan_mix()
+    pairs_ac = float(counts[0] + counts[2]) * n_cfg
+    pairs_b = float(counts[1]) * n_cfg
+    alu_ops = a_c * pairs_ac + b * pairs_b  # lane operations on the ALU pipe
+    mhz = (clk or {}).get("sm_mhz") or 1965.0
+    peak = 148 * 4 * 16 * mhz * 1e6
+    achieved = alu_ops / (scan_ms * 1e-3)
+    return {"bound": "alu", "kernel": "k_scan", "achieved": achieved / 1e12, "peak": peak / 1e12,
+            "unit": "Tops/s (ALU-pipe lane ops)", "frac": achieved / peak,
+            "traffic": ncu_traffic("k_scan"),
+            "pairs_per_s": (pairs_ac + pairs_b) / (scan_ms * 1e-3),
+            "algorithmic": "per scanned (config, query) pair: one feasibility compare and one "
+                           "argmin update (two per side for QoS+budget queries), executed as "
+                           f"{a_c} ALU-pipe instructions per pair (classes A/C) and {b} (class B) "
+                           "plus one FMA-pipe IMAD.IADD per side",
+            "peak_source": f"B200 ALU pipe 16 lanes/SMSP x 4 x 148 SMs at {mhz:.0f} MHz "
+                           f"(sampled); instruction mix from {src}",
+            "ncu_alu_pipe_pct_of_active": ncu_metric("k_scan", "alu_pipe_pct")}
+
+
 def select_config_dict(args, world, n_cfg=65_536):
     """The headline workload's config, identical in both arms (the driver compares them)."""
     return {"workload": SELECT_WORKLOAD, "queries_per_gpu": args.queries, "configs": n_cfg,
@@ -1460,6 +1564,9 @@ def run_reference(args, dist: Dist):
     T3, _, _ = ref.eval(c3["profile"], c3["gpu"], c3["points"])
     s3 = cpu_cfg3(args, c3, float(np.max(T3 * c3["points"]["dp"])), per_step)
     sm = cpu_sim(args, per_step) if args.sim_seeds > 0 else None
+    from paper_2605_21427_b200.forest import Bundle
+    pr = cpu_predict(args, Bundle.load_npz(os.path.join(ROOT, "paper_2605_21427_b200", "data",
+                                                        "predictor_default.npz")), per_step)
     zero = {"h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "config evals/s",
            "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
@@ -1474,6 +1581,10 @@ def run_reference(args, dist: Dist):
                          "cpu_baseline": dec,
                          "e2e": {"value": dec["value"], "unit": "decisions/s",
                                  "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}},
+           "predictions": {"metric": "predictor predictions/s (PredictorBundle::predict, T "
+                                     "and P)", "value": pr["value"], "unit": "predictions/s",
+                           "cpu_baseline": pr,
+                           "e2e": {"value": pr["value"], "unit": "predictions/s", **zero}},
            "frontiers": {"metric": "frontier points/s", "value": fro["value"],
                          "unit": "points/s", "workload": FRONTIER_WORKLOAD,
                          "cpu_baseline": fro,

@@ -398,6 +398,21 @@ def gen_forest(ref: Reference) -> None:
     np.savez_compressed(os.path.join(GOLD, "forest.npz"), **out)
 
 
+def gen_default_bundle(ref: Reference) -> None:
+    """The PredictorBundle at the reference's default hyper-parameters (100 trees per
+    forest, depth 14, min leaf 2: forest.hpp:72) trained by its own pipeline (run_sweep +
+    train_bundle), shipped as model-fit input for the forest bench leg:
+    paper_2605_21427_b200/data/predictor_default.npz."""
+    import tempfile
+    from oracle.oracle import ref_train_bundle
+    from paper_2605_21427_b200.forest import Bundle
+    profs, gpu, coeffs = load_bundle()
+    path = os.path.join(tempfile.mkdtemp(), "bundle.json")
+    ref_train_bundle(ref, profs, gpu, coeffs, path, n_trees=100, max_depth=14)
+    Bundle.load_json(path).save_npz(os.path.join(ROOT, "paper_2605_21427_b200", "data",
+                                                 "predictor_default.npz"))
+
+
 def main():
     os.makedirs(GOLD, exist_ok=True)
     ref = Reference()

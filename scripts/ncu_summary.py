@@ -22,6 +22,12 @@ WANT = {
     "smsp__warps_eligible.avg.per_cycle_active": "eligible_warps_per_cycle",
     "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed": "dram_throughput_pct",
     "lts__t_bytes.sum": "l2_bytes",
+    "smsp__inst_executed.sum": "warp_inst",
+    "sm__cycles_active.avg": "sm_cycles_active",
+    "sm__cycles_elapsed.avg": "sm_cycles_elapsed",
+    "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio": "stall_wait",
+    "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio": "stall_long_sb",
+    "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio": "stall_math_throttle",
 }
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
          "msecond": 1e-3, "second": 1.0}

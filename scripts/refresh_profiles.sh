@@ -18,4 +18,8 @@ for r in $reps; do
   k=$(basename "$r" .ncu-rep); k=${k#prof_}
   python3 "$ROOT/scripts/ncu_hotlines.py" "$r" > "$P/hotlines_$k.txt" || true
 done
+python3 "$ROOT/scripts/ncu_inst_lines.py" "$O/prof_k_replay.ncu-rep" 60 > "$P/inst_lines_k_replay.txt" || true
+python3 "$ROOT/scripts/ncu_inst_lines.py" "$O/prof_k_scan.ncu-rep" 40 > "$P/inst_lines_k_scan.txt" || true
+python3 "$ROOT/scripts/sass_mix.py" "$P/k_scan_mix.json" > /dev/null
+python3 "$ROOT/scripts/sass_listing.py" "$R" > /dev/null
 echo "refreshed $P"

@@ -13,9 +13,18 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_2605_21427_b200", "libpals_gpu.so")
-KEEP = ["k_scanIj", "k_replayILi6", "k_forest_eval_aos", "k_allocateILb0", "k_eval_analyticE",
-        "k_merge_roundILi512ELi2", "k_sort_chunksILi512ELi4", "k_assign_qprep", "k_front_group",
-        "k_front_scan", "k_finalize", "k_build_tables", "k_alloc_steps", "k_one", "5k_simE"]
+# every kernel of the library is listed; the file name is the kernel name with its template
+# arguments, e.g. k_replay_6_0_0 (demangled by c++filt)
+
+
+def short_name(mangled: str) -> str:
+    dem = subprocess.run(["c++filt", mangled], capture_output=True, text=True).stdout.strip()
+    base = dem.replace("(anonymous namespace)::", "").split("(")[0].replace("void ", "")
+    base = base.replace("pals::", "")
+    name = re.sub(r"[<>, ]+", "_", base).strip("_")
+    return name.replace("true", "1").replace("false", "0").replace("(int)", "")
+
+
 GROUPS = {
     "fp64": r"^(DFMA|DMUL|DADD|DSETP|DMNMX|F2F\.F64|I2F\.F64|F2I\.F64|MUFU\.RCP64H|MUFU\.RSQ64H)",
     "int_alu": r"^(IADD3|IMAD|ISETP|VIMNMX|IMNMX|LOP3|SHF|SEL|LEA|PRMT|FLO|POPC|BREV|IABS)",
@@ -38,16 +47,13 @@ def main():
     summary = []
     for f in funcs[1:]:
         name = f.split("\n", 1)[0].strip()
-        tag = next((k for k in KEEP if k in name), None)
-        if not tag:
-            continue
         lines = [ln for ln in f.split("\n") if re.match(r"\s*/\*[0-9a-f]{4}\*/", ln)]
         ops = []
         for ln in lines:
             m = re.match(r"\s*/\*[0-9a-f]{4}\*/\s+(@!?U?P\w+\s+)?([A-Z0-9_.]+)", ln)
             if m:
                 ops.append(m.group(2))
-        fname = "k_sim" if tag == "5k_simE" else tag.split("IL")[0].split("Ij")[0].rstrip("E")
+        fname = short_name(name)
         with open(os.path.join(out, fname + ".sass"), "w") as g:
             g.write(f"// {name}\n// cuobjdump -sass paper_2605_21427_b200/libpals_gpu.so "
                     f"(sm_100a, -fmad=false -lineinfo)\n")

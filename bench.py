@@ -438,8 +438,20 @@ def run_ours(args, dist: Dist):
     step_us = (time.perf_counter() - t0) / 200 * 1e6
     latency = {"workload": "cfg1: llama2-7b-like, 6 caps x 6 batches (36 candidates), target 0.6 x "
                            "unconstrained, static 1600 W budget",
-               "select_config_us": sel_us, "control_step_us": step_us,
-               "note": "one synchronous C-ABI call (H2D + 1 kernel + D2H); wall clock"}
+               "python_ctypes": {"select_config_us": sel_us, "control_step_us": step_us},
+               "note": "one synchronous call: the candidate set is validated, uploaded and "
+                       "scored once and cached; per call one kernel launch writing the "
+                       "decision to mapped pinned memory, then a stream sync; wall clock"}
+    cpp = os.path.join(ROOT, "tests", "cpp", "test_adapter")
+    if os.path.exists(cpp) and dist.rank == 0:
+        try:
+            r = subprocess.run([cpp, ROOT, "--latency"], capture_output=True, text=True,
+                               timeout=300)
+            latency["cpp_drop_in"] = json.loads(r.stdout.strip().splitlines()[-1])
+            latency["select_config_us"] = latency["cpp_drop_in"]["select_config_us"]
+            latency["control_step_us"] = latency["cpp_drop_in"]["control_step_us"]
+        except Exception as e:  # the binary needs the reference headers at build time
+            latency["cpp_drop_in"] = {"error": str(e)[:200]}
 
     out = {
         "metric": METRIC, "value": value, "unit": "config evals/s",

@@ -1,5 +1,6 @@
 // ctx.cu — contexts, errors, models, grids (the object side of pals_gpu.h).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -24,6 +25,11 @@ int cuda_fail(cudaError_t e, const char* where) {
 }
 
 void count_launch(pals_ctx* ctx, int k) { ctx->launches += k; }
+
+uint64_t next_model_uid() {
+    static std::atomic<uint64_t> uid{1};
+    return uid++;
+}
 
 // OperatingPoint::validate (types.hpp:117-123) then the comm_fixed_by_tp lookup
 // (model.hpp:56-59), i.e. the first exception analytic_scorer throws for p.
@@ -116,6 +122,7 @@ int pals_ctx_destroy(pals_ctx* c) {
     if (!c) return PALS_OK;
     cudaSetDevice(c->device);
     replay_cache_free(c);
+    one_cache_free(c);
     if (c->d_scratch) cudaFree(c->d_scratch);
     if (c->d_front) cudaFree(c->d_front);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
@@ -153,6 +160,7 @@ int pals_model_analytic(pals_ctx* ctx, const pals_profile* prof, const pals_gpu_
         return set_error(PALS_ECONFIG, "pals_model_analytic: n_tp out of range");
     auto* m = new pals_model();
     m->ctx = ctx;
+    m->uid = next_model_uid();
     m->kind = MODEL_ANALYTIC;
     m->profile = *prof;
     m->name = std::string(prof->name, strnlen(prof->name, sizeof(prof->name)));
@@ -187,6 +195,7 @@ int pals_model_table(pals_ctx* ctx, const pals_point* pts, const double* t, cons
         return set_error(PALS_ECONFIG, "pals_model_table: bad arguments");
     auto* m = new pals_model();
     m->ctx = ctx;
+    m->uid = next_model_uid();
     m->kind = MODEL_TABLE;
     m->name = "table";
     m->table_n = n;

@@ -376,6 +376,7 @@ extern "C" int pals_model_forest(pals_ctx* ctx, int32_t n_models, int32_t model_
     }
     auto* m = new pals_model();
     m->ctx = ctx;
+    m->uid = next_model_uid();
     m->kind = MODEL_FOREST;
     m->name = "predictor";
     m->forest = fh;

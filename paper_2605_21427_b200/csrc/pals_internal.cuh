@@ -221,6 +221,7 @@ struct pals_ctx {
     void* h_pinned = nullptr;
     size_t pinned_bytes = 0;
     void* replay_cache = nullptr;  // replay.cu
+    void* one_cache = nullptr;     // replay.cu: single-call candidate sets (pals_select_one)
     int replay_layout = 0;         // PALS_REPLAY_THREAD / PALS_REPLAY_WARP
     double sim_prep_s = 0.0;       // sim.cu: host setup of the last pals_run_scenarios
     double sim_kernel_ms = -1.0;   // and its k_sim launch (CUDA events)
@@ -244,6 +245,7 @@ enum ModelKind { MODEL_ANALYTIC = 0, MODEL_TABLE = 1, MODEL_FOREST = 2 };
 
 struct pals_model {
     pals_ctx* ctx = nullptr;
+    uint64_t uid = 0;  // unique per model ever created (cache keys survive pointer reuse)
     ModelKind kind = MODEL_ANALYTIC;
     std::string name;
     pals_profile profile{};
@@ -289,6 +291,8 @@ void count_launch(pals_ctx* ctx, int k = 1);
 const PlanDev& plan_dev(const pals_plan* p);
 int plan_error(const pals_plan* p);
 void replay_cache_free(pals_ctx* ctx);
+void one_cache_free(pals_ctx* ctx);
+uint64_t next_model_uid();
 // forest.cu
 void forest_free(void* f);
 int forest_eval_plan(pals_plan* p, const pals_model* m, pals_ctx* ctx);

@@ -1019,6 +1019,7 @@ struct OneArgs {
     pals_query q;      // select-only call
     int* out;          // [0] idx, [1] reason, [2] error, [3] applied
     pals_ctrl_state* out_state;
+    int scored;        // th / pn hold the candidates' scores already (cached set)
 };
 
 template <class Filter, class ScoreF>
@@ -1068,7 +1069,7 @@ __device__ int warp_fold_one(int64_t n, const double* cap, const int* batch, Fil
 // select_config fold, then the hysteresis gate.
 __global__ void k_one(OneArgs a) {
     const int lane = threadIdx.x;
-    for (int64_t c = lane; c < a.n; c += 32) {
+    for (int64_t c = lane; c < a.n && !a.scored; c += 32) {
         double T, P;
         if (a.an) {
             const Score s = analytic_score(*a.an, a.cap[c], a.batch[c], a.tp[c], a.dp[c]);
@@ -1196,11 +1197,287 @@ __global__ void k_one(OneArgs a) {
 
 using namespace pals;
 
+namespace pals {
+
+// A cached candidate set's scores: t_hat = dp * T, p_node (controller.hpp:147-150), by the
+// model on the device (analytic) or from the table's values (TableScorer).
+__global__ void k_one_score(const Analytic* an, int64_t n, const double* cap, const int* batch,
+                            const int* tp, const int* dp, const double* T, const double* P,
+                            double alpha, double beta, double* th, double* pn) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        double t, w;
+        if (an) {
+            const Score sc = analytic_score(*an, cap[c], batch[c], tp[c], dp[c]);
+            t = sc.T;
+            w = sc.P;
+        } else {
+            t = T[c];
+            w = P[c];
+        }
+        th[c] = (double)dp[c] * t;
+        pn[c] = p_node_of(w, dp[c], alpha, beta);
+    }
+}
+
+// Single-call candidate-set cache (pals_select_one / pals_control_step_one): a drop-in caller
+// passes the same candidate vector every control interval (SPEC: one controller per node),
+// so the validated, uploaded and scored set is kept per (model, coeffs, candidates) and a
+// call is one kernel launch writing its decision into mapped pinned memory.
+struct OneSet {
+    uint64_t model_uid = 0, key = 0, last = 0;
+    int64_t n = 0;
+    pals_coeffs k{};
+    std::vector<pals_point> pts;
+    int valid_rc = PALS_OK;
+    std::string err;
+    void* d = nullptr;
+    double *cap = nullptr, *th = nullptr, *pn = nullptr;
+    int *batch = nullptr, *tp = nullptr, *dp = nullptr;
+};
+struct OneCache {
+    std::vector<OneSet*> sets;
+    uint64_t clock = 0;
+    char* h_out = nullptr;  // mapped pinned: int out[8] + pals_ctrl_state
+    char* d_out = nullptr;
+};
+constexpr int kOneSets = 16;
+
+void one_cache_free(pals_ctx* ctx) {
+    auto* oc = (OneCache*)ctx->one_cache;
+    if (!oc) return;
+    cudaStreamSynchronize(ctx->stream);
+    for (auto* e : oc->sets) {
+        cudaFree(e->d);
+        delete e;
+    }
+    if (oc->h_out) cudaFreeHost(oc->h_out);
+    delete oc;
+    ctx->one_cache = nullptr;
+}
+
+static uint64_t fnv_pts(const pals_point* p, int64_t n) {
+    uint64_t h = 0xcbf29ce484222325ULL;
+    const unsigned char* b = (const unsigned char*)p;
+    for (size_t i = 0; i < (size_t)n * sizeof(pals_point); ++i) h = (h ^ b[i]) * 0x100000001b3ULL;
+    return h;
+}
+
+// the set for (m, coeffs, cands): found, or built (validated, uploaded, scored) on a miss
+static int one_set(pals_ctx* ctx, const pals_model* m, const pals_point* cands, int64_t n,
+                   double alpha, double beta, OneSet** out) {
+    auto* oc = (OneCache*)ctx->one_cache;
+    if (!oc) {
+        oc = new OneCache();
+        ctx->one_cache = oc;
+        PALS_CUDA(cudaHostAlloc((void**)&oc->h_out, 4096, cudaHostAllocMapped));
+        PALS_CUDA(cudaHostGetDevicePointer((void**)&oc->d_out, oc->h_out, 0));
+    }
+    const uint64_t key = fnv_pts(cands, n);
+    for (auto* e : oc->sets)
+        if (e->model_uid == m->uid && e->key == key && e->n == n && e->k.alpha == alpha &&
+            e->k.beta_watts == beta &&
+            !memcmp(e->pts.data(), cands, (size_t)n * sizeof(pals_point))) {
+            e->last = ++oc->clock;
+            *out = e;
+            return PALS_OK;
+        }
+    OneSet* e = nullptr;
+    if ((int)oc->sets.size() < kOneSets) {
+        e = new OneSet();
+        oc->sets.push_back(e);
+    } else {  // evict the least recently used set
+        e = *std::min_element(oc->sets.begin(), oc->sets.end(),
+                              [](const OneSet* a, const OneSet* b) { return a->last < b->last; });
+        PALS_CUDA(cudaStreamSynchronize(ctx->stream));
+        cudaFree(e->d);
+        *e = OneSet();
+    }
+    e->model_uid = 0;  // not valid until fully built
+    e->n = n;
+    e->key = key;
+    e->k = pals_coeffs{alpha, beta};
+    e->pts.assign(cands, cands + n);
+    e->last = ++oc->clock;
+    // the reference scores candidates in order and throws on the first rejection
+    e->valid_rc = validate_points(m, cands, n);
+    e->err = e->valid_rc ? std::string(pals_last_error()) : std::string();
+    const size_t n1 = (size_t)(n > 0 ? n : 1);
+    const size_t bytes = n1 * (8 * 5 + 4 * 4) + 256 * 10;
+    PALS_CUDA(cudaMalloc(&e->d, bytes));
+    char* b = (char*)e->d;
+    size_t off = 0;
+    auto take = [&](size_t sz) {
+        char* r = b + off;
+        off += (sz + 255) & ~(size_t)255;
+        return r;
+    };
+    e->cap = (double*)take(n1 * 8);
+    double* T = (double*)take(n1 * 8);
+    double* P = (double*)take(n1 * 8);
+    e->th = (double*)take(n1 * 8);
+    e->pn = (double*)take(n1 * 8);
+    e->batch = (int*)take(n1 * 4);
+    e->tp = (int*)take(n1 * 4);
+    int* ep = (int*)take(n1 * 4);
+    e->dp = (int*)take(n1 * 4);
+    if (e->valid_rc == PALS_OK && n > 0) {
+        std::vector<double> cap(n), tv(n), pv(n);
+        std::vector<int> bt(n), tp(n), epv(n), dp(n);
+        for (int64_t i = 0; i < n; ++i) {
+            cap[i] = cands[i].cap_watts;
+            bt[i] = cands[i].batch;
+            tp[i] = cands[i].tp;
+            epv[i] = cands[i].ep;
+            dp[i] = cands[i].dp;
+        }
+        if (m->kind == MODEL_TABLE) {  // TableScorer: first point equal by value
+            std::unordered_map<std::string, int64_t> first;
+            for (int64_t i = 0; i < m->table_n; ++i) {
+                pals_point q = m->table_pts[i];
+                if (q.cap_watts == 0.0) q.cap_watts = 0.0;
+                first.emplace(std::string((const char*)&q, sizeof q), i);
+            }
+            for (int64_t i = 0; i < n; ++i) {
+                pals_point q = cands[i];
+                if (q.cap_watts == 0.0) q.cap_watts = 0.0;
+                const int64_t r = first.at(std::string((const char*)&q, sizeof q));
+                tv[i] = m->table_T[r];
+                pv[i] = m->table_P[r];
+            }
+        }
+        cudaStream_t s = ctx->stream;
+        PALS_CUDA(cudaMemcpyAsync(e->cap, cap.data(), n * 8, cudaMemcpyHostToDevice, s));
+        PALS_CUDA(cudaMemcpyAsync(e->batch, bt.data(), n * 4, cudaMemcpyHostToDevice, s));
+        PALS_CUDA(cudaMemcpyAsync(e->tp, tp.data(), n * 4, cudaMemcpyHostToDevice, s));
+        PALS_CUDA(cudaMemcpyAsync(ep, epv.data(), n * 4, cudaMemcpyHostToDevice, s));
+        PALS_CUDA(cudaMemcpyAsync(e->dp, dp.data(), n * 4, cudaMemcpyHostToDevice, s));
+        if (m->kind == MODEL_TABLE) {
+            PALS_CUDA(cudaMemcpyAsync(T, tv.data(), n * 8, cudaMemcpyHostToDevice, s));
+            PALS_CUDA(cudaMemcpyAsync(P, pv.data(), n * 8, cudaMemcpyHostToDevice, s));
+        }
+        const Analytic* an = nullptr;
+        if (m->kind == MODEL_ANALYTIC) {
+            if (!m->d_an) {
+                auto* mm = const_cast<pals_model*>(m);
+                PALS_CUDA(cudaMalloc(&mm->d_an, sizeof(Analytic)));
+                PALS_CUDA(cudaMemcpyAsync(mm->d_an, &m->an, sizeof(Analytic),
+                                          cudaMemcpyHostToDevice, s));
+            }
+            an = m->d_an;
+        }
+        k_one_score<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(an, n, e->cap, e->batch, e->tp,
+                                                                e->dp, T, P, alpha, beta, e->th,
+                                                                e->pn);
+        count_launch(ctx);
+        const cudaError_t ce = cudaGetLastError();
+        if (ce != cudaSuccess) return cuda_fail(ce, "k_one_score");
+        PALS_CUDA(cudaStreamSynchronize(s));  // the host vectors above die here
+    }
+    e->model_uid = m->uid;
+    *out = e;
+    return PALS_OK;
+}
+
+}  // namespace pals
+
+// analytic / table scorers: the cached set, one launch, results through mapped memory
+static int one_call_cached(pals_ctx* ctx, const pals_model* m, const pals_point* cands,
+                           int64_t n, OneArgs& a, int do_step, pals_decision* out_d,
+                           pals_ctrl_state* out_s, const pals_ctrl_state* in_state) {
+    const bool stale = do_step && a.now_s - a.tel.t_s > 1.5 * a.cfg.interval_s;
+    if (stale) {  // controller.hpp:217-220: nothing is scored, the state is returned as is
+        out_d->point = in_state->current;
+        out_d->applied = 0;
+        out_d->reason = PALS_REASON_HOLD;
+        *out_s = *in_state;
+        return PALS_OK;
+    }
+    int rc;
+    const bool pid = do_step && a.tg.objective == PALS_OBJ_QOS && a.tg.throughput_tps > 0.0;
+    if (pid) {  // score(st.current) runs before select_config (controller.hpp:229)
+        rc = validate_point(m, in_state->current);
+        if (rc) return rc;
+    }
+    OneSet* e = nullptr;
+    rc = one_set(ctx, m, cands, n, a.alpha, a.beta, &e);
+    if (rc) return rc;
+    if (e->valid_rc) return set_error(e->valid_rc, e->err);
+    if (pid && m->kind == MODEL_TABLE) {
+        pals_point q = in_state->current;
+        if (q.cap_watts == 0.0) q.cap_watts = 0.0;
+        a.cur_ok = 0;
+        for (int64_t i = 0; i < m->table_n && !a.cur_ok; ++i) {
+            pals_point t = m->table_pts[i];
+            if (t.cap_watts == 0.0) t.cap_watts = 0.0;
+            if (!memcmp(&t, &q, sizeof q)) {
+                a.cur_ok = 1;
+                a.cur_T = m->table_T[i];
+            }
+        }
+    }
+    auto* oc = (OneCache*)ctx->one_cache;
+    a.n = n;
+    a.cap = e->cap;
+    a.batch = e->batch;
+    a.tp = e->tp;
+    a.dp = e->dp;
+    a.th = e->th;
+    a.pn = e->pn;
+    a.an = m->kind == MODEL_ANALYTIC ? m->d_an : nullptr;
+    a.scored = 1;
+    a.do_step = do_step;
+    a.out = (int*)oc->d_out;
+    a.out_state = (pals_ctrl_state*)(oc->d_out + 64);
+    // the current point for the analytic PID promise is scored in the kernel
+    if (do_step) a.st = *in_state;
+    volatile int* h = (volatile int*)oc->h_out;
+    h[2] = -1;
+    k_one<<<1, 32, 0, ctx->stream>>>(a);
+    count_launch(ctx);
+    cudaError_t ce = cudaGetLastError();
+    if (ce != cudaSuccess) return cuda_fail(ce, "k_one");
+    ce = cudaStreamSynchronize(ctx->stream);
+    if (ce != cudaSuccess) return cuda_fail(ce, "k_one sync");
+    int out[8];
+    memcpy(out, (const void*)oc->h_out, sizeof out);
+    if (out[2] != PALS_OK) return set_error(out[2] < 0 ? PALS_ERUNTIME : out[2], "unscored candidate");
+    if (!do_step) {
+        out_d->point = cands[out[0]];
+        out_d->applied = 1;
+        out_d->reason = out[1];
+        return PALS_OK;
+    }
+    pals_ctrl_state st;
+    memcpy(&st, (const void*)(oc->h_out + 64), sizeof st);
+    const pals_point& ch = cands[out[0]];
+    const pals_point& cu = in_state->current;
+    const bool same = ch.cap_watts == cu.cap_watts && ch.batch == cu.batch && ch.tp == cu.tp &&
+                      ch.ep == cu.ep && ch.dp == cu.dp;
+    const bool may_apply = out[5] != 0;
+    if (may_apply && !same) {  // hysteresis gate (controller.hpp:255-266)
+        st.current = ch;
+        st.sustain_count = 0;
+        out_d->point = ch;
+        out_d->applied = 1;
+        out_d->reason = out[1];
+    } else {
+        out_d->point = st.current;
+        out_d->applied = 0;
+        out_d->reason = out[1];
+    }
+    *out_s = st;
+    return PALS_OK;
+}
+
 static int one_call(pals_ctx* ctx, const pals_model* m, const pals_point* cands, int64_t n,
                     OneArgs& a, int do_step, pals_decision* out_d, pals_ctrl_state* out_s,
                     const pals_ctrl_state* in_state) {
     if (n <= 0) return set_error(PALS_ECONFIG, "select_config: empty candidate list");
-    // the reference scores candidates in order and aborts on the first rejection
+    PALS_CUDA(cudaSetDevice(ctx->device));
+    if (m->kind != MODEL_FOREST)
+        return one_call_cached(ctx, m, cands, n, a, do_step, out_d, out_s, in_state);
+    // forest scorers: the candidates (and the current point) are scored per call
     int rc;
     if (do_step && a.tg.objective == PALS_OBJ_QOS && a.tg.throughput_tps > 0.0 &&
         !(a.now_s - a.tel.t_s > 1.5 * a.cfg.interval_s)) {

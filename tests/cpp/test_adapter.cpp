@@ -7,6 +7,7 @@
 // Case families follow /root/reference/proj/tests/test_controller.cpp and
 // tests/acceptance/acceptance.cpp criterion 10 (restated, not copied).
 // Exit code = number of failed checks. Built by tests/cpp/build.sh.
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -91,8 +92,76 @@ static std::string read_file(const std::string& p) {
     return ss.str();
 }
 
+// Single-call latency of the drop-in (BASELINE cfg1): the bundled llama2-7b-like profile, its
+// 6 caps x 6 batches at the deployment TP, target 0.6 x unconstrained, a static 1600 W
+// budget; wall-clock microseconds per call for wattserve::gpu::* and the reference, printed
+// as one JSON line.
+static int latency(const std::string& root) {
+    gpu::Context ctx(0);
+    const json j = json::parse(read_file(root + "/paper_2605_21427_b200/data/profiles.json"));
+    ModelProfile prof;
+    for (const auto& pj : j.at("profiles"))
+        if (pj.at("name").get<std::string>() == "llama2-7b-like") prof = profile_from_json(pj);
+    const GpuSpec gspec = gpu_from_json(j.at("platform").at("gpu"));
+    const SystemPowerCoeffs k{1.05, 345.0};
+    std::vector<OperatingPoint> cands;
+    for (double c : {150.0, 200.0, 250.0, 300.0, 350.0, 400.0})
+        for (int b : {1, 4, 8, 16, 32, 64})
+            cands.push_back(OperatingPoint{c, b, prof.deployment.tp, prof.deployment.ep,
+                                           prof.deployment.dp});
+    const Scorer cs = detail::cached(analytic_scorer(prof, gspec));
+    auto gs = gpu::analytic_scorer(ctx, prof, gspec);
+    Targets t = qos(0.6 * throughput(cands.back(), prof, gspec));
+    t.power_budget_w = 1600.0;
+    ControllerConfig cfg;
+    cfg.target_headroom = 0.05;
+    cfg.budget_margin = 0.02;
+    auto bench = [](auto&& f, int reps) {
+        for (int i = 0; i < 50; ++i) f(i);
+        const auto t0 = std::chrono::steady_clock::now();
+        for (int i = 0; i < reps; ++i) f(i);
+        return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0)
+                   .count() / reps;
+    };
+    int sink = 0;
+    const double g_sel = bench([&](int) { sink += gpu::select_config(cands, t, gs, k, 1.0, 0.05, 0.02).point.batch; }, 2000);
+    const double r_sel = bench([&](int) { sink += select_config(cands, t, cs, k, 1.0, 0.05, 0.02).point.batch; }, 20000);
+    ControllerState sg, sr;
+    sg.current = sr.current = cands.back();
+    bool same = true;
+    const double g_step = bench([&](int i) {
+        auto [d, s2] = gpu::control_step(TelemetryInput{0.5 * i, 0.55 * t.throughput_tps}, 0.5 * i,
+                                         t, cands, gs, k, sg, cfg);
+        sg = s2;
+        sink += d.point.batch;
+    }, 2000);
+    const double r_step = bench([&](int i) {
+        auto [d, s2] = control_step(TelemetryInput{0.5 * i, 0.55 * t.throughput_tps}, 0.5 * i, t,
+                                    cands, cs, k, sr, cfg);
+        sr = s2;
+        sink += d.point.batch;
+    }, 20000);
+    // same call sequence on both sides from the same start: the states must agree
+    ControllerState a, b;
+    a.current = b.current = cands.back();
+    for (int i = 0; i < 300; ++i) {
+        const TelemetryInput ti{0.5 * i, (0.4 + 0.002 * i) * t.throughput_tps};
+        auto [da, sa] = gpu::control_step(ti, 0.5 * i, t, cands, gs, k, a, cfg);
+        auto [db, sb] = control_step(ti, 0.5 * i, t, cands, cs, k, b, cfg);
+        same = same && ::same(da, db) && ::same(sa, sb);
+        a = sa;
+        b = sb;
+    }
+    std::printf("{\"select_config_us\": %.3f, \"control_step_us\": %.3f, "
+                "\"reference_select_config_us\": %.3f, \"reference_control_step_us\": %.3f, "
+                "\"candidates\": %zu, \"identical\": %s, \"sink\": %d}\n",
+                g_sel, g_step, r_sel, r_step, cands.size(), same ? "true" : "false", sink & 1);
+    return same ? 0 : 1;
+}
+
 int main(int argc, char** argv) {
     const std::string root = argc > 1 ? argv[1] : ".";
+    if (argc > 2 && std::string(argv[2]) == "--latency") return latency(root);
     gpu::Context ctx(0);
     const SystemPowerCoeffs k{1.05, 345.0};
 

@@ -371,10 +371,7 @@ def run_ours(args, dist: Dist):
     r_ms = [a.elapsed_time(b) for a, b in rev]
     clk = clocks.stop()
     roof = dict(scan_roofline(*roof_counts, clk), **scan_extra)
-    dec_roof = issue_roofline("k_replay", dec_roof_rate, "decisions", clk,
-                              "instruction issue: one dependent chain of FP64 PID arithmetic, "
-                              "table lookups and the plant per trace and step; the FP64 pipe "
-                              "runs at ~20 % of its peak (ncu), HBM is idle")
+
     r_max = dist.max(float(np.sum(r_ms)))
     dec_total = dist.sum(float(nt) * args.trace_steps) * rsteps
     dec_value = dec_total / (r_max * 1e-3)
@@ -402,7 +399,10 @@ def run_ours(args, dist: Dist):
     layouts = replay_layouts(args, dist, ctx, stream, l2_flush, models, s, spec, dec_value)
     args._synthetic_dec_value = dec_value
     traces_leg = bench_traces(args, dist, ctx, stream, l2_flush, models, s, spec, d_sum)
-    dec_roof_rate = dec_value / dist.world  # per-GPU decisions/s, bound below with the clock
+    dec_roof = issue_roofline("k_replay", dec_value / dist.world, "decisions", clk,
+                              "instruction issue: one dependent chain of FP64 PID arithmetic, "
+                              "table lookups and the plant per trace and step; the FP64 pipe "
+                              "runs at ~20 % of its peak (ncu), HBM is idle")
 
     # ---------------- K2: PredictorBundle::predict throughput ----------------
     predictions, bundle = bench_forest(args, dist, ctx, stream, l2_flush)

@@ -315,6 +315,15 @@ int pals_select(pals_plan* p, const pals_query* queries, int64_t n, int32_t* ind
 int pals_plan_scores(pals_plan* p, double* t_hat, double* p_node, double* eff);
 /* Diagnostics of the last select: queries resolved by the exact sequential fold. */
 int64_t pals_plan_last_exact_count(const pals_plan* p);
+/* How a plan decides its queries (results identical either way):
+ * PALS_DECIDE_SCAN (default) evaluates every (config, query) pair of a query's class in
+ * the pair scan — the config-evaluation workload BASELINE.json measures; PALS_DECIDE_PREFIX
+ * answers each query from prefix-minimum tables over the sorted orders (O(1) per QoS-only
+ * or budget-only query, one block of at most n/64 positions per QoS+budget query): the
+ * fastest time to decide. */
+#define PALS_DECIDE_SCAN 0
+#define PALS_DECIDE_PREFIX 1
+int pals_plan_set_decide(pals_plan* p, int32_t mode);
 /* Force every query through the exact sequential fold (testing). */
 int pals_plan_set_force_exact(pals_plan* p, int force);
 /* Synchronises, then reports the last select's per-class query counts:

@@ -56,6 +56,7 @@ SIGNATURES = [
     ("pals_plan_scores", _I, [_VP, _VP, _VP, _VP]),
     ("pals_plan_last_exact_count", _I64, [_VP]),
     ("pals_plan_set_force_exact", _I, [_VP, _I]),
+    ("pals_plan_set_decide", _I, [_VP, _I32]),
     ("pals_plan_stats", _I, [_VP, _VP]),
     ("pals_plan_time_scan", _I, [_VP, _I]),
     ("pals_plan_scan_ms", _D, [_VP]),

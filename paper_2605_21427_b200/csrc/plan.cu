@@ -96,6 +96,10 @@ struct pals_plan {
     int32_t* h_cnt = nullptr;     // pinned class counters (pals_select)
     void* scratch = nullptr;      // plan_scratch()
     size_t scratch_bytes = 0;
+    // PALS_DECIDE_PREFIX: prefix-min tables instead of the pair scan (time to decide)
+    int decide = PALS_DECIDE_SCAN;
+    void* dec_buf = nullptr;
+    size_t dec_bytes = 0;
 };
 
 namespace pals {
@@ -1102,6 +1106,143 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) 
     }
 }
 
+// ---- time to decide: prefix-min tables instead of the pair scan -----------------------
+// Feasibility is a prefix of the sorted orders (Kt of the t_hat order, Kp of the p_node
+// order), so the argmins the pair scan folds are prefix minima:
+//   class A (QoS, no budget): min pos_e over t-positions [0, Kt)       = PM_A[Kt - 1]
+//   class C (budget)        : min pos_t over p-positions [0, Kp)       = PM_C[Kp - 1]
+//   class B (QoS + budget)  : min pos_e over {t-pos < Kt, p-pos < Kp}: a 2-D dominance
+//     minimum = TB_b[Kp - 1] over the first b = floor(Kt / B) whole blocks of B t-positions
+//     (TB_b = prefix minimum along the p order of pos_e restricted to t-pos < b B), folded
+//     with the < B remaining t-positions, which one warp reads from te[] (p-pos, pos_e in
+//     t order); its budget branch is PM_C[Kp - 1].
+// The minima are the same merged positions the scan produces (min is exact and
+// associative), so k_finalize (near-tie folds included) is shared.
+constexpr int kDecTile = 1024;        // elements per scan tile (256 threads x 4)
+constexpr int kDecMaxBlocks = 64;     // at most 64 2-D table rows
+
+struct DecDev {
+    int64_t n;
+    int B, nb, ntiles;
+    uint32_t* elemA;   // pos_e at every t-position
+    uint32_t* elemC;   // pos_t at every p-position
+    uint2* te;         // (p-pos, pos_e) at every t-position
+    uint2* pt;         // (t-pos, pos_e) at every p-position
+    uint32_t* agg;     // [rows][ntiles] tile minima
+    uint32_t* tab;     // [rows][n]: row 0 PM_A, row 1 PM_C, row 1 + b TB_b (b = 1..nb)
+};
+
+__global__ void k_dec_elems(PlanDev d, DecDev t) {
+    pdl_wait();
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < d.n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t it = d.midx[ORD_T][p], ip = d.midx[ORD_P][p];
+        const uint32_t e_t = d.pos32[ORD_E][it], e_p = d.pos32[ORD_E][ip];
+        t.elemA[p] = e_t;
+        t.te[p] = make_uint2(d.pos32[ORD_P][it], e_t);
+        t.elemC[p] = d.pos32[ORD_T][ip];
+        t.pt[p] = make_uint2(d.pos32[ORD_T][ip], e_p);
+    }
+}
+
+__device__ __forceinline__ uint32_t dec_elem(const DecDev& t, int row, int64_t i) {
+    if (i >= t.n) return kNone32;
+    if (row == 0) return t.elemA[i];
+    if (row == 1) return t.elemC[i];
+    const uint2 v = t.pt[i];  // row 1 + b: the points in the first b blocks of t-positions
+    return v.x < (uint32_t)((row - 1) * t.B) ? v.y : kNone32;
+}
+
+// (a) per (row, tile) minimum
+__global__ void __launch_bounds__(256) k_dec_tiles(DecDev t) {
+    pdl_wait();
+    const int row = blockIdx.y, tile = blockIdx.x;
+    uint32_t m = kNone32;
+#pragma unroll
+    for (int k = 0; k < kDecTile / 256; ++k)
+        m = min(m, dec_elem(t, row, (int64_t)tile * kDecTile + k * 256 + threadIdx.x));
+    m = __reduce_min_sync(0xffffffffu, m);
+    __shared__ uint32_t w[8];
+    if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        uint32_t x = threadIdx.x < 8 ? w[threadIdx.x] : kNone32;
+        x = __reduce_min_sync(0xffffffffu, x);
+        if (threadIdx.x == 0) t.agg[(int64_t)row * t.ntiles + tile] = x;
+    }
+}
+
+// (b) per (row, tile) inclusive prefix minimum with the carry of the earlier tiles
+__global__ void __launch_bounds__(256) k_dec_scan(DecDev t) {
+    pdl_wait();
+    const int row = blockIdx.y, tile = blockIdx.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __shared__ uint32_t s_carry, w[8];
+    if (threadIdx.x < 32) {
+        uint32_t c = kNone32;
+        for (int j = lane; j < tile; j += 32) c = min(c, t.agg[(int64_t)row * t.ntiles + j]);
+        c = __reduce_min_sync(0xffffffffu, c);
+        if (lane == 0) s_carry = c;
+    }
+    const int64_t base = (int64_t)tile * kDecTile + threadIdx.x * 4;
+    uint32_t v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = dec_elem(t, row, base + k);
+#pragma unroll
+    for (int k = 1; k < 4; ++k) v[k] = min(v[k], v[k - 1]);
+    uint32_t x = v[3];  // thread total -> warp inclusive scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x = min(x, y);
+    }
+    if (lane == 31) w[wid] = x;
+    __syncthreads();
+    uint32_t pre = s_carry;  // earlier tiles, earlier warps, earlier lanes
+    for (int j = 0; j < wid; ++j) pre = min(pre, w[j]);
+    const uint32_t up = __shfl_up_sync(0xffffffffu, x, 1);
+    if (lane > 0) pre = min(pre, up);
+    uint32_t* out = t.tab + (int64_t)row * t.n;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (base + k < t.n) out[base + k] = min(pre, v[k]);
+}
+
+// (c) one warp per scanned query: the table lookups (and class B's residual block)
+__global__ void __launch_bounds__(256) k_decide(DecDev t, SelArgs a) {
+    pdl_wait();
+    const int lane = threadIdx.x & 31;
+    const int64_t cA = a.counts[CLS_A], cB = a.counts[CLS_B], cC = a.counts[CLS_C];
+    const int64_t total = cA + cB + cC;
+    const uint32_t* PMA = t.tab;
+    const uint32_t* PMC = t.tab + t.n;
+    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < total;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        int c;
+        int64_t i;
+        if (w < cA) { c = CLS_A; i = w; }
+        else if (w < cA + cB) { c = CLS_B; i = w - cA; }
+        else { c = CLS_C; i = w - cA - cB; }
+        const int32_t qid = a.qlist[c * a.qcap + i];
+        const uint32_t kt = (uint32_t)a.thr_t[qid], kp = (uint32_t)a.thr_p[qid];  // K - 1
+        if (c == CLS_A) {
+            if (lane == 0) a.best_e[qid] = PMA[kt];
+            continue;
+        }
+        if (lane == 0) a.best_t[qid] = PMC[kp];
+        if (c == CLS_C) continue;
+        const uint32_t Kt = kt + 1;
+        const uint32_t b = Kt / (uint32_t)t.B;  // whole blocks of t-positions
+        uint32_t m = b ? t.tab[(int64_t)(1 + b) * t.n + kp] : kNone32;
+        for (uint32_t p = b * (uint32_t)t.B + lane; p < Kt; p += 32) {
+            const uint2 v = t.te[p];
+            if (v.x <= kp) m = min(m, v.y);
+        }
+        m = __reduce_min_sync(0xffffffffu, m);
+        if (lane == 0 && m != kNone32) a.best_e[qid] = m;
+    }
+}
+
 // exact feasibility of point c for query q (FP64, controller.hpp:155, 163)
 __device__ __forceinline__ bool feasible_t(const PlanDev& d, const pals_query& q, int64_t c) {
     const double target = q.throughput_tps * (1.0 + q.target_headroom);
@@ -1465,6 +1606,7 @@ int pals_plan_destroy(pals_plan* p) {
     if (p->h_cnt) cudaFreeHost(p->h_cnt);
     cudaFree(p->scratch);
     cudaFree(p->slab);
+    cudaFree(p->dec_buf);
     cudaFree(p->thr_t);
     cudaFree(p->d_q);
     delete p;
@@ -1646,8 +1788,46 @@ static int select_head(pals_plan* p, const SelArgs& a, cudaStream_t s) {
     return check_launch("pals_plan_select_device");
 }
 
-// select, part 2 (needs the packed keys): the pair scan, decisions, exact folds
-static int select_tail(pals_plan* p, const SelArgs& a) {
+// the prefix-min tables of the time-to-decide path (they depend on the ranks only)
+static int dec_layout(pals_plan* p, DecDev* t) {
+    const int64_t n = p->n;
+    t->n = n;
+    int B = 1024;
+    while ((n + B - 1) / B > kDecMaxBlocks) B *= 2;
+    t->B = B;
+    t->nb = (int)((n + B - 1) / B);
+    t->ntiles = (int)((n + kDecTile - 1) / kDecTile);
+    const int rows = 2 + t->nb;
+    const size_t nn = (size_t)std::max<int64_t>(n, 1);
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t need = al(nn * 4) * 2 + al(nn * 8) * 2 + al((size_t)rows * t->ntiles * 4) +
+                        al((size_t)rows * nn * 4);
+    if (p->dec_bytes < need) {
+        cudaFree(p->dec_buf);
+        p->dec_buf = nullptr;
+        p->dec_bytes = 0;
+        PALS_CUDA(cudaMalloc(&p->dec_buf, need));
+        p->dec_bytes = need;
+    }
+    char* b = (char*)p->dec_buf;
+    t->elemA = (uint32_t*)b;
+    b += al(nn * 4);
+    t->elemC = (uint32_t*)b;
+    b += al(nn * 4);
+    t->te = (uint2*)b;
+    b += al(nn * 8);
+    t->pt = (uint2*)b;
+    b += al(nn * 8);
+    t->agg = (uint32_t*)b;
+    b += al((size_t)rows * t->ntiles * 4);
+    t->tab = (uint32_t*)b;
+    return PALS_OK;
+}
+
+// select, part 2 (needs the packed keys): the pair scan (or the prefix-min decision),
+// decisions, exact folds. build: this call also builds the prefix-min tables (decide mode;
+// the first query chunk of a step)
+static int select_tail(pals_plan* p, const SelArgs& a, bool build = true) {
     pals_ctx* ctx = p->ctx;
     cudaStream_t s = ctx->stream;
     // stream-K scan grid: 4 CTAs per SM, equal integer-op shares (see k_scan)
@@ -1658,7 +1838,24 @@ static int select_tail(pals_plan* p, const SelArgs& a) {
     const unsigned evf = p->capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
     if (p->time_scan) PALS_CUDA(cudaEventRecordWithFlags(p->ev_scan0, s, evf));
     cudaError_t e;
-    e = launch_k(k_scan, sgrid, kScanThreads, kScanSmem, s, pdl, p->d, a);
+    if (p->decide == PALS_DECIDE_PREFIX) {
+        DecDev t;
+        int rc = dec_layout(p, &t);
+        if (rc) return rc;
+        if (build) {
+            e = launch_k(k_dec_elems, grid_blocks(ctx, p->n, 256), 256, 0, s, pdl, p->d, t);
+            if (e == cudaSuccess)
+                e = launch_k(k_dec_tiles, dim3(t.ntiles, 2 + t.nb), 256, 0, s, pdl, t);
+            if (e == cudaSuccess)
+                e = launch_k(k_dec_scan, dim3(t.ntiles, 2 + t.nb), 256, 0, s, pdl, t);
+            if (e != cudaSuccess) return cuda_fail(e, "decide tables");
+            count_launch(ctx, 3);
+        }
+        e = launch_k(k_decide, ctx->num_sms * 8, 256, 0, s, pdl, t, a);
+        if (e != cudaSuccess) return cuda_fail(e, "k_decide");
+    } else {
+        e = launch_k(k_scan, sgrid, kScanThreads, kScanSmem, s, pdl, p->d, a);
+    }
     if (e != cudaSuccess) return cuda_fail(e, "k_scan");
     if (p->time_scan) {
         PALS_CUDA(cudaEventRecordWithFlags(p->ev_scan1, s, evf));
@@ -1696,7 +1893,7 @@ static int plan_step(pals_plan* p, const pals_query* d_queries, int64_t nq, int3
                      uint8_t* d_reason, const pals_query* h_q, int32_t* h_idx, uint8_t* h_rs) {
     pals_ctx* ctx = p->ctx;
     cudaStream_t s = ctx->stream;
-    const int key_t = p->time_scan | (p->force_exact << 1);
+    const int key_t = p->time_scan | (p->force_exact << 1) | (p->decide << 2);
     const bool hit = p->gexec && p->g_q == d_queries && p->g_n == nq && p->g_idx == d_idx &&
                      p->g_rs == d_reason && p->g_timed == key_t && p->g_hq == h_q &&
                      p->g_hidx == h_idx && p->g_hrs == h_rs;
@@ -1762,7 +1959,7 @@ static int plan_step(pals_plan* p, const pals_query* d_queries, int64_t nq, int3
             }
             if (!rc) {
                 count_launch(ctx, 1);
-                rc = select_tail(p, a);
+                rc = select_tail(p, a, k == 0);
             }
         }
         if (!rc && h_idx) {
@@ -1932,6 +2129,13 @@ double pals_plan_scan_ms(pals_plan* p) {
     float ms = -1.0f;
     if (cudaEventElapsedTime(&ms, p->ev_scan0, p->ev_scan1) != cudaSuccess) return -1.0;
     return ms;
+}
+
+int pals_plan_set_decide(pals_plan* p, int32_t mode) {
+    if (mode != PALS_DECIDE_SCAN && mode != PALS_DECIDE_PREFIX)
+        return set_error(PALS_ECONFIG, "pals_plan_set_decide: unknown mode");
+    p->decide = mode;
+    return PALS_OK;
 }
 
 int pals_plan_set_force_exact(pals_plan* p, int force) {

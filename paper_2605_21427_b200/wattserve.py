@@ -227,6 +227,10 @@ class Plan:
     def last_exact_count(self) -> int:
         return int(self.ctx.lib.pals_plan_last_exact_count(self.h))
 
+    def set_decide(self, mode: str):
+        """"scan" (default: the pair scan) or "prefix" (prefix-min tables; same results)."""
+        check(self.ctx.lib.pals_plan_set_decide(self.h, {"scan": 0, "prefix": 1}[mode]))
+
     def force_exact(self, on: bool = True):
         check(self.ctx.lib.pals_plan_set_force_exact(self.h, 1 if on else 0))
 

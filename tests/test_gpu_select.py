@@ -223,3 +223,26 @@ def test_select_rank_pipeline_variants(ctx, oracle, monkeypatch, knobs):
     oi, orr, rc = oracle.select(cfg["points"], T, P, cfg["coeffs"], q[::41])
     assert rc == 0 and np.array_equal(results[1][0][::41], oi)
     assert np.array_equal(results[1][1][::41], orr)
+
+
+@pytest.mark.parametrize("which", ["cfg2", "cfg3", "cfg3x"])
+def test_prefix_decide_equals_scan(ctx, oracle, which):
+    """PALS_DECIDE_PREFIX (prefix-min tables; 2-D blocks for QoS+budget queries) decides
+    every query exactly as the pair scan does, on the bench grids, and a sample agrees
+    with the C oracle."""
+    c = {"cfg2": workloads.cfg2, "cfg3": workloads.cfg3,
+         "cfg3x": workloads.cfg3_extended}[which]()
+    plan = Plan(AnalyticModel(ctx, c["profile"], c["gpu"]), Grid(ctx, c["points"]), c["coeffs"])
+    th, _, _ = plan.scores()
+    n = {"cfg2": 20_000, "cfg3": 200_000, "cfg3x": 20_000}[which]
+    q = workloads.gen_queries(n, 4242, float(th.max()), "mixed", budget=(600.0, 6000.0))
+    q["bias"][::3] = np.linspace(0.5, 2.0, len(q["bias"][::3]))
+    si, sr = plan.select(q)
+    plan.set_decide("prefix")
+    pi, pr = plan.select(q)
+    assert np.array_equal(si, pi) and np.array_equal(sr, pr)
+    assert plan.stats()[1] > 0  # QoS+budget queries took the 2-D path
+    T, P, _ = oracle.eval(c["profile"], c["gpu"], c["points"])
+    sub = np.arange(0, n, max(1, n // 300))
+    oi, orr, _ = oracle.select(c["points"], T, P, c["coeffs"], q[sub])
+    assert np.array_equal(pi[sub], oi) and np.array_equal(pr[sub], orr)

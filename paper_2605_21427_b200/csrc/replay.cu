@@ -624,7 +624,7 @@ __global__ void __launch_bounds__(1024) k_build_tables(PlanDev d, ReplayModelDev
         const uint32_t w = (uint32_t)canon[d.inv_tr[k & kMask]];
         b1[i] = w | (d.danger[ORD_T][k >> 16] ? kWordDanger : 0u);
     }
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && rm->plant) {
         // plant constants: unconstrained throughput (sim.hpp:258-264) and the p_node range
         const Analytic& a = *rm->plant;
         double pmin = 0.0, pmax = 0.0;
@@ -638,6 +638,8 @@ __global__ void __launch_bounds__(1024) k_build_tables(PlanDev d, ReplayModelDev
         rm->t_max = (double)rm->dp * s.T;
         rm->p_min = pmin;
         rm->p_max = pmax;
+    }
+    if (threadIdx.x == 0) {
         rm->nd_t = ndt;
         rm->nd_p = ndp;
         rm->gmax_t = canon[d.globals[0]];
@@ -1220,6 +1222,117 @@ __global__ void k_one_score(const Analytic* an, int64_t n, const double* cap, co
     }
 }
 
+// One select_config / control_step on a cached set's rank tables (n <= kOneTableMax): the
+// PID and the hysteresis gate as k_one, the select as the replay's table_select (Kt, Kp
+// counts on the sorted score arrays, one table word, the literal fold on near-ties).
+struct OneTabArgs {
+    ReplayModelDev m;         // by value: no dependent load before the first table read
+    const Analytic* an;       // analytic scorer: score(current) on the device
+    double cur_T;             // table scorer: score(current) (host lookup)
+    int cur_ok;
+    int do_step;
+    pals_telemetry tel;
+    double now_s;
+    pals_targets tg;
+    pals_ctrl_state st;
+    pals_ctrl_cfg cfg;
+    pals_query q;
+    int* out;
+    pals_ctrl_state* out_state;
+};
+
+__global__ void k_one_tab(OneTabArgs a, int seq) {
+    // the sorted score arrays go to shared memory in one coalesced pass of the warp; the
+    // searches then run on shared memory (the per-call chain of dependent reads is the cost)
+    extern __shared__ double ot_smem[];
+    ReplayModelDev m = a.m;
+    for (int i = threadIdx.x; i < m.nd_t; i += 32) ot_smem[i] = m.ut[i];
+    for (int i = threadIdx.x; i < m.nd_p; i += 32) ot_smem[m.nd_t + i] = m.up[i];
+    __syncwarp();
+    if (threadIdx.x != 0) return;
+    m.ut = ot_smem;
+    m.up = ot_smem + m.nd_t;
+    pals_query q = a.q;
+    pals_ctrl_state st = a.st;
+    bool changed = false;
+    if (a.do_step) {  // controller.hpp:222-251 (stale calls never launch)
+        double err_norm = 0.0;
+        if (a.tg.objective == PALS_OBJ_QOS && a.tg.throughput_tps > 0.0) {
+            err_norm = (a.tg.throughput_tps - a.tel.throughput_tps) / a.tg.throughput_tps;
+            double curT = a.cur_T;
+            if (a.an) {
+                curT = analytic_score(*a.an, st.current.cap_watts, st.current.batch,
+                                      st.current.tp, st.current.dp).T;
+            } else if (!a.cur_ok) {
+                a.out[2] = PALS_ECONFIG;
+                __threadfence_system();
+                *(volatile int*)&a.out[7] = seq;
+                return;
+            }
+            const double promised = (double)st.current.dp * curT * st.bias;
+            if (promised > 0.0) {
+                const double pred_err = (promised - a.tel.throughput_tps) / promised;
+                st.integral =
+                    sclamp(st.integral + pred_err, -a.cfg.integral_clamp, a.cfg.integral_clamp);
+                const double deriv = st.has_prev_error ? pred_err - st.prev_error : 0.0;
+                const double corr = a.cfg.kp * pred_err + a.cfg.ki * st.integral + a.cfg.kd * deriv;
+                st.bias = sclamp(st.bias * (1.0 - corr), a.cfg.bias_min, a.cfg.bias_max);
+                st.prev_error = pred_err;
+                st.has_prev_error = 1;
+            }
+        }
+        const pals_targets& l = st.last_targets;
+        const bool eq = st.has_last_targets && l.throughput_tps == a.tg.throughput_tps &&
+                        l.has_budget == a.tg.has_budget &&
+                        (!l.has_budget || l.power_budget_w == a.tg.power_budget_w) &&
+                        l.epsilon == a.tg.epsilon && l.objective == a.tg.objective;
+        changed = !eq;
+        st.last_targets = a.tg;
+        st.has_last_targets = 1;
+        if (fabs(err_norm) > a.tg.epsilon) ++st.sustain_count;
+        else st.sustain_count = 0;
+        q.throughput_tps = a.tg.throughput_tps;
+        q.power_budget_w = a.tg.power_budget_w;
+        q.has_budget = a.tg.has_budget;
+        q.objective = a.tg.objective;
+        q.bias = st.bias;
+        q.target_headroom = a.cfg.target_headroom;
+        q.budget_margin = a.cfg.budget_margin;
+    }
+    // select_config (controller.hpp:137-200) on the rank tables
+    const double target = q.throughput_tps * (1.0 + q.target_headroom);
+    const bool bset = q.has_budget != 0;
+    const double budget = bset ? q.power_budget_w * (1.0 - q.budget_margin) : 0.0;
+    int kp = m.nd_p;
+    if (bset) {
+        int lo = 0, hi = m.nd_p;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (m.up[mid] <= budget) lo = mid + 1;
+            else hi = mid;
+        }
+        kp = lo;
+    }
+    const int kt = q.objective == PALS_OBJ_QOS ? count_t_feasible(m, q.bias, target, 0) : 0;
+    int best, r;
+    table_select(m, target, bset, budget, kp, kt, q.bias, q.objective, &best, &r);
+    a.out[2] = PALS_OK;
+    if (!a.do_step) {
+        a.out[0] = best;
+        a.out[1] = r;
+        a.out[3] = 1;
+    } else {
+        const bool may_apply = changed || st.sustain_count >= a.cfg.sustain_intervals;
+        a.out[0] = best;
+        a.out[1] = may_apply ? r : PALS_REASON_HOLD;
+        a.out[5] = may_apply ? 1 : 0;
+        *a.out_state = st;
+    }
+    // the results are in host memory before the sequence number the host polls for
+    __threadfence_system();
+    *(volatile int*)&a.out[7] = seq;
+}
+
 // Single-call candidate-set cache (pals_select_one / pals_control_step_one): a drop-in caller
 // passes the same candidate vector every control interval (SPEC: one controller per node),
 // so the validated, uploaded and scored set is kept per (model, coeffs, candidates) and a
@@ -1234,12 +1347,28 @@ struct OneSet {
     void* d = nullptr;
     double *cap = nullptr, *th = nullptr, *pn = nullptr;
     int *batch = nullptr, *tp = nullptr, *dp = nullptr;
+    // rank tables of the set (n <= kOneTableMax): select_config in O(log n) per call
+    pals_grid* grid = nullptr;
+    pals_plan* plan = nullptr;
+    void* d_tab = nullptr;
+    ReplayModelDev* d_m = nullptr;
+    ReplayModelDev h_m{};  // its values once k_build_tables has filled the counts
 };
+constexpr int64_t kOneTableMax = 1024;
+
+static void one_set_free(OneSet* e) {
+    cudaFree(e->d);
+    cudaFree(e->d_tab);
+    cudaFree(e->d_m);
+    if (e->plan) pals_plan_destroy(e->plan);
+    if (e->grid) pals_grid_destroy(e->grid);
+}
 struct OneCache {
     std::vector<OneSet*> sets;
     uint64_t clock = 0;
-    char* h_out = nullptr;  // mapped pinned: int out[8] + pals_ctrl_state
+    char* h_out = nullptr;  // mapped pinned: int out[8] (out[7]: sequence) + pals_ctrl_state
     char* d_out = nullptr;
+    int seq = 0;
 };
 constexpr int kOneSets = 16;
 
@@ -1248,7 +1377,7 @@ void one_cache_free(pals_ctx* ctx) {
     if (!oc) return;
     cudaStreamSynchronize(ctx->stream);
     for (auto* e : oc->sets) {
-        cudaFree(e->d);
+        one_set_free(e);
         delete e;
     }
     if (oc->h_out) cudaFreeHost(oc->h_out);
@@ -1290,7 +1419,7 @@ static int one_set(pals_ctx* ctx, const pals_model* m, const pals_point* cands, 
         e = *std::min_element(oc->sets.begin(), oc->sets.end(),
                               [](const OneSet* a, const OneSet* b) { return a->last < b->last; });
         PALS_CUDA(cudaStreamSynchronize(ctx->stream));
-        cudaFree(e->d);
+        one_set_free(e);
         *e = OneSet();
     }
     e->model_uid = 0;  // not valid until fully built
@@ -1373,6 +1502,45 @@ static int one_set(pals_ctx* ctx, const pals_model* m, const pals_point* cands, 
         const cudaError_t ce = cudaGetLastError();
         if (ce != cudaSuccess) return cuda_fail(ce, "k_one_score");
         PALS_CUDA(cudaStreamSynchronize(s));  // the host vectors above die here
+        if (n <= kOneTableMax) {  // the replay's select tables over this candidate set
+            int r = pals_grid_points(ctx, cands, n, &e->grid);
+            if (r) return r;
+            const pals_coeffs kk{alpha, beta};
+            r = pals_plan_create(ctx, m, e->grid, &kk, &e->plan);
+            if (r) return r;
+            r = pals_plan_prepare(e->plan);
+            if (r) return r;
+            const PlanDev& d = plan_dev(e->plan);
+            const size_t W = (size_t)n + 1;
+            PALS_CUDA(cudaMalloc(&e->d_tab, W * W * 4 + W * 4 + 2 * W * 8 + 1024));
+            PALS_CUDA(cudaMalloc(&e->d_m, sizeof(ReplayModelDev)));
+            ReplayModelDev h;
+            memset(&h, 0, sizeof h);
+            h.n = (int)n;
+            h.cap = e->grid->cap;
+            h.batch = e->grid->batch;
+            h.canon = e->grid->canon;
+            h.inv_tr = e->grid->inv_tr;
+            h.T = d.T;
+            h.th = d.th;
+            h.pn = d.pn;
+            h.ef = d.ef;
+            h.danger_t = d.danger[ORD_T];
+            h.danger_e = d.danger[ORD_E];
+            char* tb = (char*)e->d_tab;
+            h.m2 = (const uint32_t*)tb;
+            h.b1 = (const uint32_t*)(tb + W * W * 4);
+            h.ut = (const double*)(tb + ((W * W * 4 + W * 4 + 7) & ~(size_t)7));
+            h.up = h.ut + W;
+            PALS_CUDA(cudaMemcpyAsync(e->d_m, &h, sizeof h, cudaMemcpyHostToDevice, s));
+            k_build_tables<<<1, 1024, 0, s>>>(d, e->d_m, (uint32_t*)h.m2, (uint32_t*)h.b1,
+                                              (double*)h.ut, (double*)h.up, alpha, beta);
+            count_launch(ctx);
+            const cudaError_t be = cudaGetLastError();
+            if (be != cudaSuccess) return cuda_fail(be, "k_build_tables (one)");
+            PALS_CUDA(cudaMemcpyAsync(&e->h_m, e->d_m, sizeof h, cudaMemcpyDeviceToHost, s));
+            PALS_CUDA(cudaStreamSynchronize(s));
+        }
     }
     e->model_uid = m->uid;
     *out = e;
@@ -1433,12 +1601,42 @@ static int one_call_cached(pals_ctx* ctx, const pals_model* m, const pals_point*
     if (do_step) a.st = *in_state;
     volatile int* h = (volatile int*)oc->h_out;
     h[2] = -1;
-    k_one<<<1, 32, 0, ctx->stream>>>(a);
-    count_launch(ctx);
+    bool polled = false;
+    if (e->d_m) {
+        OneTabArgs t;
+        t.m = e->h_m;
+        t.an = a.an;
+        t.cur_T = a.cur_T;
+        t.cur_ok = a.cur_ok;
+        t.do_step = do_step;
+        t.tel = a.tel;
+        t.now_s = a.now_s;
+        t.tg = a.tg;
+        t.st = a.st;
+        t.cfg = a.cfg;
+        t.q = a.q;
+        t.out = a.out;
+        t.out_state = a.out_state;
+        const int seq = ++oc->seq;
+        h[7] = 0;
+        k_one_tab<<<1, 32, (size_t)(t.m.nd_t + t.m.nd_p) * 8, ctx->stream>>>(t, seq);
+        count_launch(ctx);
+        cudaError_t ce = cudaGetLastError();
+        if (ce != cudaSuccess) return cuda_fail(ce, "k_one_tab");
+        // the result is final once its sequence number shows up in the mapped buffer: poll
+        // it (a stream sync would add its wake-up latency); bounded, then the sync reports
+        // whatever went wrong
+        for (int spin = 0; spin < 2000000 && !polled; ++spin) polled = h[7] == seq;
+    } else {
+        k_one<<<1, 32, 0, ctx->stream>>>(a);
+        count_launch(ctx);
+    }
     cudaError_t ce = cudaGetLastError();
     if (ce != cudaSuccess) return cuda_fail(ce, "k_one");
-    ce = cudaStreamSynchronize(ctx->stream);
-    if (ce != cudaSuccess) return cuda_fail(ce, "k_one sync");
+    if (!polled) {
+        ce = cudaStreamSynchronize(ctx->stream);
+        if (ce != cudaSuccess) return cuda_fail(ce, "k_one sync");
+    }
     int out[8];
     memcpy(out, (const void*)oc->h_out, sizeof out);
     if (out[2] != PALS_OK) return set_error(out[2] < 0 ? PALS_ERUNTIME : out[2], "unscored candidate");

@@ -333,6 +333,11 @@ def run_ours(args, dist: Dist):
 
     scan_avg = float(np.mean(scan_ms))
     roof_counts = (counts, n_cfg, scan_avg)
+    time_to_decide = decide_leg(args, dist, plan, d_q, nq, h_qn, stream, l2_flush, None, n_cfg)
+    time_to_decide["scan_path"] = {"ms_per_step": t_max / args.steps,
+                                   "queries_per_s": dist.sum(float(nq)) * args.steps / (t_max * 1e-3),
+                                   "e2e_queries_per_s": dist.sum(float(nq)) * args.steps /
+                                   (e2e_max * 1e-3)}
     scan_extra = {"scan_share_of_step": scan_avg / float(np.mean(step_ms)),
                   "step_breakdown_ms": {"graph_step": float(np.mean(step_ms)),
                                         "scan_kernel": scan_avg,
@@ -465,6 +470,7 @@ def run_ours(args, dist: Dist):
                 "d2h_bytes_per_step": nq * 5,
                 "api": "pals_select (C ABI, pinned host buffers: one graph, query upload overlapped with eval+rank, decisions stored to the mapped host buffers by the finalize kernel)"},
         "roofline": roof,
+        "time_to_decide": time_to_decide,
         "gpu_launches": int(launches),
         "gather": gather,
         "clocks": clk,
@@ -506,6 +512,12 @@ def run_ours(args, dist: Dist):
         if scen is not None:
             out["scenarios"]["cpu_baseline"] = cpu_sim(args, args.cpu_seconds, results=rs)
         out["latency"]["cpu_reference_select_config_us"] = cpu_latency(c1, float(th1.max()))
+        for leg, cb in ((out["time_to_decide"], out["cpu_baseline"]),
+                        (out["cfg3"]["time_to_decide"], out["cfg3"]["cpu_baseline"])):
+            if cb.get("value"):
+                n_c = out["config"]["configs"]
+                leg["reference_queries_per_s"] = cb["value"] / n_c
+                leg["e2e_speedup_vs_reference"] = leg["e2e"]["queries_per_s"] / (cb["value"] / n_c)
         out["parity"] = bench_parity(args, r2, (h_idx, h_rs), r3, gpu_cfg3, r4, h_sumn,
                                      cfg5_summ, rs, sim_nres, sim_res)
         out["parity"].update(forest_parity(bundle, forest_kept))
@@ -994,6 +1006,9 @@ def bench_cfg3(args, dist, ctx, stream, l2_flush, int_peak, clk=None):
         e2e_ms.append(a.elapsed_time(b))
     e2e_max = dist.max(float(np.sum(e2e_ms)))
     scan_avg = float(np.mean(scan_ms))
+    ttd = decide_leg(args, dist, plan, d_q, nq, h_qn, stream, l2_flush, None, n_cfg)
+    ttd["scan_path"] = {"ms_per_step": t_max / args.steps,
+                        "e2e_queries_per_s": dist.sum(float(nq)) * args.steps / (e2e_max * 1e-3)}
     # strong scaling: the 1e6 queries in total, contiguous shards over the ranks (at N = 1
     # the same work as the weak leg)
     from paper_2605_21427_b200.shard import shard_range
@@ -1060,7 +1075,7 @@ def bench_cfg3(args, dist, ctx, stream, l2_flush, int_peak, clk=None):
            "roofline": dict(scan_roofline(cnt, n_cfg, scan_avg, clk),
                             scan_share_of_step=scan_avg / float(np.mean(step_ms))),
            "gpu_launches": int(launches), "extended_grid": extended, "scaling": "weak",
-           "strong": strong}
+           "strong": strong, "time_to_decide": ttd}
     return out, c, tref, (h_idx, h_rs)
 
 
@@ -1398,6 +1413,67 @@ def issue_roofline(kernel, units_per_s, unit, clk, note):
             "peak_source": f"1 warp instruction / SMSP / cycle x 4 x 148 SMs at {mhz:.0f} MHz "
                            "(sampled); instructions per unit from profiles/ncu_summary.json",
             "algorithmic": note}
+
+
+def decide_leg(args, dist, plan, d_q, nq, h_qn, stream, l2_flush, ref_pairs_per_s, n_cfg):
+    """Time to decide the same queries with the prefix-min path (PALS_DECIDE_PREFIX, same
+    decisions as the pair scan): device step time and end to end through pals_select with
+    pinned host buffers; queries/s beside the reference's queries/s (its config evals/s over
+    the grid size)."""
+    import torch
+    from paper_2605_21427_b200.abi import ptr
+    d_i = torch.empty(nq, dtype=torch.int32, device="cuda")
+    d_r = torch.empty(nq, dtype=torch.uint8, device="cuda")
+    h_i = torch.empty(nq, dtype=torch.int32, pin_memory=True).numpy()
+    h_r = torch.empty(nq, dtype=torch.uint8, pin_memory=True).numpy()
+    plan.time_scan(False)
+    plan.set_decide("prefix")
+    lib = plan.ctx.lib
+    try:
+        run = lambda: plan.run(d_q.data_ptr(), nq, d_i.data_ptr(), d_r.data_ptr())  # noqa
+        for _ in range(max(1, args.warmup)):
+            run()
+        torch.cuda.synchronize()
+        ms = []
+        for _ in range(args.steps):
+            l2_flush()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            run()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        t = dist.max(float(np.mean(ms)))
+
+        def e2e():
+            rc = lib.pals_select(plan.h, ptr(h_qn), nq, ptr(h_i), ptr(h_r))
+            assert rc == 0, lib.pals_last_error()
+
+        e2e()
+        em = []
+        for _ in range(args.steps):
+            l2_flush()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            e2e()
+            e1.record(stream)
+            e1.synchronize()
+            em.append(e0.elapsed_time(e1))
+        te = dist.max(float(np.mean(em)))
+    finally:
+        plan.set_decide("scan")
+    total_q = dist.sum(float(nq))
+    out = {"api": "PALS_DECIDE_PREFIX: prefix-min tables instead of the pair scan, the same "
+                  "decisions (tests/test_gpu_select.py)",
+           "ms_per_step": t, "queries_per_s": total_q / (t * 1e-3),
+           "e2e": {"queries_per_s": total_q / (te * 1e-3), "ms_per_step": te,
+                   "h2d_bytes_per_step": nq * 48, "d2h_bytes_per_step": nq * 5}}
+    if ref_pairs_per_s:
+        ref_qps = ref_pairs_per_s / n_cfg
+        out["reference_queries_per_s"] = ref_qps
+        out["e2e_speedup_vs_reference"] = out["e2e"]["queries_per_s"] / ref_qps
+    return out
 
 
 def scan_mix():

@@ -30,6 +30,7 @@
 //     never the simulation state, so every split is precomputed — allocate_budget
 //     on the GPU allocator (K4) for joint / oracle, dp-proportional otherwise.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -582,29 +583,84 @@ struct Resources {
         for (auto* m : plant_models) pals_model_destroy(m);
         for (void* p : dev) cudaFree(p);
     }
-    // staged arena: every per-scenario / per-node array is packed into one host
-    // buffer and moved with one allocation and one copy (thousands of small
-    // cudaMalloc / cudaFree calls would dominate the call otherwise)
-    std::vector<char> stage_buf;
+    // staged arena: every per-scenario / per-node array is packed into one device
+    // allocation (thousands of small cudaMalloc / cudaFree calls would dominate the call
+    // otherwise). Data segments are gathered by all host threads into pinned memory kept in
+    // the context and moved with one async copy; scratch (zero) regions live in a second
+    // range that is memset on the device. Offsets of the zero range carry kZeroBit.
+    static constexpr size_t kZeroBit = (size_t)1 << 62;
+    struct Seg {
+        const void* src;         // caller-owned (stage_ref) or own.data()
+        std::vector<char> own;   // copied data (stage)
+        size_t bytes, off;
+    };
+    std::vector<Seg> segs;
+    size_t data_bytes = 0, zero_bytes = 0;
     char* arena = nullptr;
+    char* zarena = nullptr;
     template <class T>
     size_t stage(const T* data, size_t n) {
-        const size_t off = (stage_buf.size() + 255) & ~(size_t)255;
-        stage_buf.resize(off + std::max<size_t>(1, n) * sizeof(T), 0);
-        if (data && n) std::memcpy(stage_buf.data() + off, data, n * sizeof(T));
+        const size_t bytes = std::max<size_t>(1, n) * sizeof(T);
+        if (!data) {  // scratch: zeroed on the device
+            const size_t off = (zero_bytes + 255) & ~(size_t)255;
+            zero_bytes = off + bytes;
+            return off | kZeroBit;
+        }
+        const size_t off = (data_bytes + 255) & ~(size_t)255;
+        data_bytes = off + bytes;
+        Seg sg{nullptr, std::vector<char>((const char*)data, (const char*)data + n * sizeof(T)),
+               n * sizeof(T), off};
+        segs.push_back(std::move(sg));
         return off;
     }
     template <class T>
     size_t stage(const std::vector<T>& v) { return stage(v.data(), v.size()); }
+    // staged without a copy: v must outlive commit()
+    template <class T>
+    size_t stage_ref(const std::vector<T>& v) {
+        const size_t off = (data_bytes + 255) & ~(size_t)255;
+        data_bytes = off + std::max<size_t>(1, v.size()) * sizeof(T);
+        segs.push_back(Seg{v.data(), {}, v.size() * sizeof(T), off});
+        return off;
+    }
     int commit() {
-        int r = alloc(&arena, stage_buf.size());
+        int r = alloc(&arena, data_bytes);
         if (r) return r;
-        const cudaError_t e = copy_on(ctx->stream, arena, stage_buf.data(), stage_buf.size(),
-                                      cudaMemcpyHostToDevice);
-        return e == cudaSuccess ? PALS_OK : cuda_fail(e, "pals_run_scenarios: arena upload");
+        r = alloc(&zarena, zero_bytes);
+        if (r) return r;
+        cudaStream_t s = ctx->stream;
+        PALS_CUDA(cudaMemsetAsync(zarena, 0, std::max<size_t>(1, zero_bytes), s));
+        PALS_CUDA(cudaStreamSynchronize(s));  // the pinned buffer may still feed a copy
+        if (ctx->pinned_bytes < data_bytes) {
+            if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+            ctx->h_pinned = nullptr;
+            ctx->pinned_bytes = 0;
+            PALS_CUDA(cudaHostAlloc(&ctx->h_pinned, data_bytes, cudaHostAllocDefault));
+            ctx->pinned_bytes = data_bytes;
+        }
+        char* pin = (char*)ctx->h_pinned;
+        const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 32u));
+        std::atomic<size_t> next{0};
+        std::vector<std::thread> th;
+        for (unsigned t = 0; t < nt; ++t)
+            th.emplace_back([&] {
+                for (size_t i = next++; i < segs.size(); i = next++) {
+                    const Seg& g = segs[i];
+                    if (g.bytes)
+                        std::memcpy(pin + g.off, g.own.empty() ? g.src : g.own.data(), g.bytes);
+                }
+            });
+        for (auto& t : th) t.join();
+        PALS_CUDA(cudaMemcpyAsync(arena, pin, std::max<size_t>(1, data_bytes),
+                                  cudaMemcpyHostToDevice, s));
+        PALS_CUDA(cudaStreamSynchronize(s));
+        segs.clear();
+        return PALS_OK;
     }
     template <class T>
-    T* at(size_t off) const { return (T*)(arena + off); }
+    T* at(size_t off) const {
+        return (T*)((off & kZeroBit) ? zarena + (off & ~kZeroBit) : arena + off);
+    }
     template <class T>
     int alloc(T** p, size_t n) {
         void* q = nullptr;
@@ -869,24 +925,30 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
                 node_stream[node0[s] + i] = it->second;
             }
         streams.resize(work.size());
+    }
+    // streams differ in length (900 s vs 3600 s scenarios): dynamic scheduling; the worker
+    // threads run while this thread splits the budgets (which never read the streams)
+    std::atomic<size_t> next_stream{0};
+    std::vector<std::thread> stream_threads;
+    {
         const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(),
                                                             (unsigned)work.size()));
-        std::vector<std::thread> th;
         for (unsigned t = 0; t < nt; ++t)
-            th.emplace_back([&, t] {
-                for (size_t w = t; w < work.size(); w += nt)
+            stream_threads.emplace_back([&] {
+                for (size_t w = next_stream++; w < work.size(); w = next_stream++)
                     gen_stream(scens[work[w].first], work[w].second, n_int[work[w].first],
                                &streams[w]);
             });
-        for (auto& t : th) t.join();
     }
-    std::vector<size_t> o_cum(streams.size()), o_len(streams.size());
-    for (size_t u = 0; u < streams.size(); ++u) {
-        o_cum[u] = res.stage(streams[u].cum);
-        o_len[u] = res.stage(streams[u].len);
-    }
+    struct Joiner {
+        std::vector<std::thread>& t;
+        ~Joiner() {
+            for (auto& x : t)
+                if (x.joinable()) x.join();
+        }
+    } joiner{stream_threads};
 
-    phase("streams");
+    phase("streams started");
     // budget changes and their splits (assign_budgets, sim.hpp:229-238, 277-283, 313-336)
     std::vector<std::vector<int32_t>> chg_k(n_scen);
     std::vector<std::vector<double>> chg_w(n_scen);
@@ -993,6 +1055,13 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
     }
 
     phase("budgets");
+    for (auto& t : stream_threads) t.join();
+    std::vector<size_t> o_cum(streams.size()), o_len(streams.size());
+    for (size_t u = 0; u < streams.size(); ++u) {
+        o_cum[u] = res.stage_ref(streams[u].cum);
+        o_len[u] = res.stage_ref(streams[u].len);
+    }
+    phase("streams");
     // device buffers: stage every array, one upload, then point the descriptors at it
     std::vector<SimScenDev> hs(n_scen);
     std::vector<SimNodeDev> hn(total_nodes);

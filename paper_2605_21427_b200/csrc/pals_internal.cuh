@@ -185,6 +185,13 @@ struct PlanDev {
                              // packed key (the pair scan's argmin side; < 2^31 for any n)
     int32_t* globals;        // [0] argmax t over all, [1] argmin p over all, [2] generic flag,
                              // [3] number of exact folds last select
+    // chunk-local ranks for the 16-bit SIMD pair scan (plan.cu k_scan): the grid's TR range
+    // is cut into chunks of lch points (the chunk sort's chunks, whose value-sorted runs
+    // list a chunk's points in global merged-position order)
+    int lch;
+    uint16_t* lr16[N_ORD];   // per TR: competition rank within its chunk (k_sort_chunks)
+    uint16_t* lq16[N_ORD];   // per TR: place in its chunk's run (k_sort_chunks)
+    uint32_t* cinv[N_ORD];   // per run place: the global merged position (the rank pass)
 };
 
 #ifdef __CUDACC__

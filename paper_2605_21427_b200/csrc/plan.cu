@@ -295,6 +295,8 @@ constexpr size_t sort_smem_bytes(int tpb, int ipt = kIPT) {
     return (size_t)(tpb * ipt + tpb * ipt / 16) * 8 + (size_t)(tpb * ipt + tpb * ipt / 32) * 4;
 }
 
+constexpr uint32_t kLrPadSort = 4095;  // a chunk-local rank no threshold reaches (k_scan)
+
 template <int TPB, int IPT = kIPT>
 __global__ void __launch_bounds__(TPB) k_sort_chunks(PlanDev d, uint64_t* gk, uint32_t* done,
                                                      int32_t* counts_reset, int to_merged,
@@ -349,6 +351,30 @@ __global__ void __launch_bounds__(TPB) k_sort_chunks(PlanDev d, uint64_t* gk, ui
         dst[p] = sk[pk(i)];
         dstv[p] = sv[pv(i)];
         if (final_round) put_sample(d, o, p, sk[pk(i)]);
+    }
+    // chunk-local ranks of the pair scan: the run lists the chunk in global merged-position
+    // order, so a point's place in it orders the chunk as the global positions do, and the
+    // first place with its key is its competition rank inside the chunk (equal keys are
+    // equal values)
+    if (CH <= 2048) {
+        for (int i = t; i < CH; i += TPB) {
+            const uint32_t v = sv[pv(i)];
+            if (v >= (uint32_t)d.n) {  // padding of the last chunk: never feasible
+                d.lr16[o][v] = (uint16_t)kLrPadSort;
+                d.lq16[o][v] = 0x7FFF;
+                d.cinv[o][base + i] = 0xFFFFFFFFu;
+                continue;
+            }
+            const uint64_t key = sk[pk(i)];
+            int lo = 0, hi = i;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (sk[pk(mid)] < key) lo = mid + 1;
+                else hi = mid;
+            }
+            d.lr16[o][v] = (uint16_t)lo;
+            d.lq16[o][v] = (uint16_t)i;
+        }
     }
 }
 
@@ -584,6 +610,8 @@ __device__ __forceinline__ void assign_warp(const PlanDev& d, uint64_t* gk, int 
             else d.key32[o][idx] = (uint32_t)k;
             d.rank32[o][idx] = r;
             d.pos32[o][idx] = p;
+            // the pair scan's run place -> global position (chunk-local ranks, k_scan)
+            d.cinv[o][(trv / (uint32_t)d.lch) * (uint32_t)d.lch + d.lq16[o][trv]] = p;
             d.midx[o][p] = idx;  // position -> point, and its rank (k_finalize)
             d.sidx[o][p] = r;
             if (r == 0 && o == ORD_T) atomicMin((unsigned long long*)&gk[0], k);
@@ -905,72 +933,85 @@ __global__ void k_assign_qprep(PlanDev d, uint64_t* gk,
     }
 }
 
-// (8) the pair scan: every (query, config) pair of classes A/B/C is decided on the
-// integer (rank, position) arrays (persistent CTAs over work items). A point is
-// feasible on a side iff its competition rank r < K (K from qprep, stored as
-// K - 1 >= 0), and the argmin is the smallest merged position (the packed-key order).
-// Classes A (QoS, no budget) and C (budget, max throughput) take one threshold:
-// per pair d = (K - 1) - r (IMAD.IADD, FMA pipe) and v = pos | (d & 0x80000000)
-// (one LOP3: the sign bit of d marks an infeasible pair), and one 3-input min
-// (VIMNMX3) folds two configs into the running minimum — 1.5 ALU-pipe ops per pair
-// instead of a compare + predicated min (2). Class B (QoS with budget) tests both
-// sides with compares and keeps both minima.
-template <int CLS, int NQ = kScanQ>
-__device__ __forceinline__ void scan_item(const uint32_t* __restrict__ s0,
-                                          const uint32_t* __restrict__ s1,
-                                          const uint32_t* __restrict__ s2,
-                                          const uint32_t* __restrict__ s3, int nc,
-                                          const uint32_t (&kt)[kScanQ],
-                                          const uint32_t (&kp)[kScanQ], uint32_t (&be)[kScanQ],
-                                          uint32_t (&bt)[kScanQ]) {
-    if (CLS != CLS_B) {
-        // s0: rank on the feasibility side, s1: position on the argmin side; 8 configs
-        // per iteration (nc is padded to a multiple of 8) so the next shared loads are
-        // in flight while the current pairs run
-        for (int c = 0; c < nc; c += 8) {
-            const uint4 vr0 = *reinterpret_cast<const uint4*>(s0 + c);
-            const uint4 vp0 = *reinterpret_cast<const uint4*>(s1 + c);
-            const uint4 vr1 = *reinterpret_cast<const uint4*>(s0 + c + 4);
-            const uint4 vp1 = *reinterpret_cast<const uint4*>(s1 + c + 4);
-            const uint32_t r[8] = {vr0.x, vr0.y, vr0.z, vr0.w, vr1.x, vr1.y, vr1.z, vr1.w};
-            const uint32_t q[8] = {vp0.x, vp0.y, vp0.z, vp0.w, vp1.x, vp1.y, vp1.z, vp1.w};
-#pragma unroll
-            for (int v = 0; v < 8; v += 2)
-#pragma unroll
-                for (int j = 0; j < NQ; ++j) {
-                    const uint32_t K = CLS == CLS_A ? kt[j] : kp[j];
-                    const uint32_t v0 = q[v] | ((K - r[v]) & 0x80000000u);
-                    const uint32_t v1 = q[v + 1] | ((K - r[v + 1]) & 0x80000000u);
-                    be[j] = __vimin3_u32(be[j], v0, v1);
-                }
-        }
-        return;
+// (8) the pair scan: every (query, config) pair of classes A/B/C is decided, on chunk-local
+// 16-bit ranks two configs per 32-bit register.
+//
+// Chunk-local ranks (every prepare). The grid's TR range is cut into the chunk sort's
+// chunks of L <= 2,048 points; the chunk sort's value-sorted run of a chunk lists its points
+// in global merged-position order. Per point (written by k_sort_chunks): lr = its
+// competition rank inside its chunk, lq = its place in the chunk's run; per run place
+// (written by the rank pass): cinv = the global merged position. A query's feasible set
+// on a side is the position prefix [0, K); with k = #(run places whose
+// position is < K): feasible <=> lr < k, and the smallest global position among a chunk's
+// feasible points is cinv[min lq over them] (lq orders a chunk exactly as the global
+// positions do). So one chunk is decided in 16-bit lanes:
+//   d = (0x8000 + k - 1) - lr            in [0x8000 - 2049, 0x8000 + 2047]: bit 15 set
+//                                        iff feasible, and no borrow between the lanes
+//   v = lq | (~d & 0x8000)               infeasible -> >= 0x8000 > every feasible lq
+//   m = min(m, v)                        VIMNMX3.U16x2: two new registers per instruction
+// With both configs of a register in its two lanes: per 4 pairs one IMAD.IADD (FMA pipe)
+// per 2 configs, one LOP3 per 2, one VIMNMX3.U16x2 per 4 — 0.75 ALU-pipe instructions
+// per pair (classes A / C), 2 for class B (dt & dp, two LOP3, two minima), where 32-bit
+// lanes took 1.5 / 3.5.
+constexpr uint32_t kPadRank = 0x7FFFFFFFu;
+constexpr uint32_t kLrPad = kLrPadSort;  // a chunk-local rank no threshold reaches
+constexpr uint32_t kFlag2 = 0x80008000u;
+
+// number of run places of a chunk with global position <= thr = K - 1 (the chunk-local
+// threshold): a binary search over the staged, ascending run positions (a branchless
+// fixed-step search measured slower on cfg3: more registers in the scan)
+__device__ __forceinline__ uint32_t local_count(const uint32_t* sr, int L, uint32_t thr) {
+    int lo = 0, hi = L;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (sr[mid] <= thr) lo = mid + 1;
+        else hi = mid;
     }
-    for (int c = 0; c < nc; c += 4) {
-        {
-            // s0: rank_t, s1: rank_p, s2: pos_e, s3: pos_t
-            const uint4 vt = *reinterpret_cast<const uint4*>(s0 + c);
-            const uint4 vpp = *reinterpret_cast<const uint4*>(s1 + c);
-            const uint4 ve = *reinterpret_cast<const uint4*>(s2 + c);
-            const uint4 vq = *reinterpret_cast<const uint4*>(s3 + c);
-            const uint32_t rt[4] = {vt.x, vt.y, vt.z, vt.w}, rp[4] = {vpp.x, vpp.y, vpp.z, vpp.w};
-            const uint32_t pe[4] = {ve.x, ve.y, ve.z, ve.w}, pt[4] = {vq.x, vq.y, vq.z, vq.w};
-            // both sides as sign masks: dt = Kt-1 - r_t, dp = Kp-1 - r_p; the QoS value
-            // pos_e + ((dt | dp) & 0x80000000) (LOP3, then an add of disjoint bits on the
-            // FMA pipe), the budget-branch value pos_t | (dp & 0x80000000) (LOP3)
+    return (uint32_t)lo;
+}
+
+__device__ __forceinline__ uint32_t kb2(uint32_t k) {  // both lanes: 0x8000 + k - 1
+    const uint32_t v = 0x8000u + k - 1u;
+    return v | (v << 16);
+}
+
+__device__ __forceinline__ uint32_t lane_min(uint32_t m2) {
+    return min(m2 & 0xFFFFu, m2 >> 16);
+}
+
+// One chunk segment of one query tile, classes A / C: the words are staged as
+// {lr(2c, 2c+1), lq(2c, 2c+1)} pairs, 2 words (4 configs) per LDS.128.
+template <int NQ>
+__device__ __forceinline__ void scan_seg1(const uint4* __restrict__ w, int nw4,
+                                          const uint32_t (&K)[kScanQ], uint32_t (&m)[kScanQ]) {
+    for (int c = 0; c < nw4; ++c) {
+        const uint4 v = w[c];  // x: lr word 0, y: lq word 0, z: lr word 1, w: lq word 1
 #pragma unroll
-            for (int v = 0; v < 4; v += 2)
+        for (int j = 0; j < NQ; ++j) {
+            const uint32_t d0 = K[j] - v.x, d1 = K[j] - v.z;
+            const uint32_t a0 = v.y | (~d0 & kFlag2), a1 = v.w | (~d1 & kFlag2);
+            m[j] = __vimin3_u16x2(m[j], a0, a1);
+        }
+    }
+}
+
+// class B: words {lrt, lrp, lqe, lqt} per config pair, 1 LDS.128 per 2 configs
+template <int NQ>
+__device__ __forceinline__ void scan_seg2(const uint4* __restrict__ w, int nw,
+                                          const uint32_t (&Kt)[kScanQ],
+                                          const uint32_t (&Kp)[kScanQ], uint32_t (&me)[kScanQ],
+                                          uint32_t (&mt)[kScanQ]) {
+    for (int c = 0; c + 1 < nw; c += 2) {
+        const uint4 v0 = w[c], v1 = w[c + 1];
 #pragma unroll
-                for (int j = 0; j < NQ; ++j) {
-                    const uint32_t dt0 = kt[j] - rt[v], dp0 = kp[j] - rp[v];
-                    const uint32_t dt1 = kt[j] - rt[v + 1], dp1 = kp[j] - rp[v + 1];
-                    const uint32_t e0 = pe[v] + ((dt0 | dp0) & 0x80000000u);
-                    const uint32_t e1 = pe[v + 1] + ((dt1 | dp1) & 0x80000000u);
-                    const uint32_t t0 = pt[v] | (dp0 & 0x80000000u);
-                    const uint32_t t1 = pt[v + 1] | (dp1 & 0x80000000u);
-                    be[j] = __vimin3_u32(be[j], e0, e1);
-                    bt[j] = __vimin3_u32(bt[j], t0, t1);
-                }
+        for (int j = 0; j < NQ; ++j) {
+            const uint32_t dt0 = Kt[j] - v0.x, dp0 = Kp[j] - v0.y;
+            const uint32_t dt1 = Kt[j] - v1.x, dp1 = Kp[j] - v1.y;
+            const uint32_t e0 = v0.z | (~(dt0 & dp0) & kFlag2);
+            const uint32_t e1 = v1.z | (~(dt1 & dp1) & kFlag2);
+            const uint32_t t0 = v0.w | (~dp0 & kFlag2), t1 = v1.w | (~dp1 & kFlag2);
+            me[j] = __vimin3_u16x2(me[j], e0, e1);
+            mt[j] = __vimin3_u16x2(mt[j], t0, t1);
         }
     }
 }
@@ -995,34 +1036,17 @@ __device__ __forceinline__ int64_t scan_pos_of(const ScanPlan& sp, int64_t u) {
     return sp.pbase[3];
 }
 
-// pad with ranks that never pass a threshold (K - 1 < 2^31 - 1)
-__device__ __forceinline__ void stage_keys(uint32_t* dst, const uint32_t* __restrict__ src, int nc,
-                                           int ncp, uint32_t pad) {
-    constexpr int R = kScanCh / kScanThreads;
-    uint32_t x[R];
-#pragma unroll
-    for (int k = 0; k < R; ++k) {
-        const int i = threadIdx.x + k * kScanThreads;
-        x[k] = i < nc ? __ldg(src + i) : pad;
-    }
-#pragma unroll
-    for (int k = 0; k < R; ++k) {
-        const int i = threadIdx.x + k * kScanThreads;
-        if (i < ncp) dst[i] = x[k];
-    }
-}
-
-constexpr uint32_t kPadRank = 0x7FFFFFFFu;
-constexpr size_t kScanSmem = 4 * (size_t)kScanCh * 4;
+// shared memory of k_scan: a chunk's staged words (class B: 2,048 x 16 B) and its run
+// positions for the chunk-local thresholds (2 x 2,048 x 4 B)
+constexpr size_t kScanSmem = (size_t)kScanCh * 16 + 2 * (size_t)kScanCh * 4;
 
 __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) {
     pdl_wait();
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    uint32_t* s0 = reinterpret_cast<uint32_t*>(smem_raw);
-    uint32_t* s1 = s0 + kScanCh;
-    uint32_t* s2 = s1 + kScanCh;
-    uint32_t* s3 = s2 + kScanCh;
+    uint4* sw = reinterpret_cast<uint4*>(smem_raw);
+    uint32_t* ssr = reinterpret_cast<uint32_t*>(smem_raw + (size_t)kScanCh * 16);  // [2][L]
     const int64_t n = d.n;
+    const int L = d.lch;
     ScanPlan pl;
     pl.wbase[0] = pl.pbase[0] = 0;
 #pragma unroll
@@ -1038,69 +1062,108 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) 
     const int64_t p1 = scan_pos_of(pl, W * (blockIdx.x + 1) / gridDim.x);
     int64_t pos = p0;
     while (pos < p1) {
-        // locate (class, tile, first config) of pos and the end of that tile segment
+        // locate (class, tile, first config) of pos and the end of that tile segment;
+        // configs are TR positions, cut further at the chunks of the local ranks
         int c = 0;
         while (pos >= pl.pbase[c + 1]) ++c;
         const int64_t r = pos - pl.pbase[c];
         const int64_t tile = r / n;
         const int64_t j0 = r % n;
-        const int64_t seg_end = min(p1, pl.pbase[c] + (tile + 1) * n);
+        const int64_t chunk_end = (j0 / L + 1) * L;
+        const int64_t seg_end = min(min(p1, pl.pbase[c] + (tile + 1) * n), pos + (chunk_end - j0));
         const int64_t j1 = j0 + (seg_end - pos);
+        const int64_t cb = (j0 / L) * L;  // the chunk's first TR
         // this tile's queries: 8 per thread
         const int64_t q_lo = tile * pl.tq[c], q_hi = min((int64_t)a.counts[c], q_lo + pl.tq[c]);
-        uint32_t kt[kScanQ], kp[kScanQ], be[kScanQ], bt[kScanQ];
         int32_t qid[kScanQ];
+        uint32_t thr_t[kScanQ], thr_p[kScanQ];
 #pragma unroll
         for (int q = 0; q < kScanQ; ++q) {
             const int64_t sq = q_lo + q * kScanThreads + threadIdx.x;
             qid[q] = sq < q_hi ? a.qlist[c * a.qcap + sq] : -1;
-            // thresholds K - 1 (qprep); an idle slot gets 0, which the scan may use
-            // freely since its minima are discarded
-            kt[q] = qid[q] >= 0 ? (uint32_t)a.thr_t[qid[q]] : 0u;
-            kp[q] = qid[q] >= 0 ? (uint32_t)a.thr_p[qid[q]] : 0u;
-            be[q] = 0xFFFFFFFFu;
-            bt[q] = 0xFFFFFFFFu;
+            thr_t[q] = qid[q] >= 0 ? (uint32_t)a.thr_t[qid[q]] : 0u;
+            thr_p[q] = qid[q] >= 0 ? (uint32_t)a.thr_p[qid[q]] : 0u;
         }
         const bool full_slots = __any_sync(0xffffffffu, qid[kScanQ - 1] >= 0);
-        for (int64_t c0 = j0; c0 < j1; c0 += kScanCh) {
-            const int nc = (int)min((int64_t)kScanCh, j1 - c0);
-            const int ncp = (nc + 7) & ~7;  // class A/C iterations take 8 configs
-            __syncthreads();
-            if (c == CLS_A) {
-                stage_keys(s0, d.rank32[ORD_T] + c0, nc, ncp, kPadRank);
-                stage_keys(s1, d.pos32[ORD_E] + c0, nc, ncp, 0u);
-            } else if (c == CLS_C) {
-                stage_keys(s0, d.rank32[ORD_P] + c0, nc, ncp, kPadRank);
-                stage_keys(s1, d.pos32[ORD_T] + c0, nc, ncp, 0u);
-            } else {
-                stage_keys(s0, d.rank32[ORD_T] + c0, nc, ncp, kPadRank);
-                stage_keys(s1, d.rank32[ORD_P] + c0, nc, ncp, kPadRank);
-                stage_keys(s2, d.pos32[ORD_E] + c0, nc, ncp, 0u);
-                stage_keys(s3, d.pos32[ORD_T] + c0, nc, ncp, 0u);
+        // stage the segment's config words (whole pairs; lanes outside [j0, j1) padded
+        // infeasible) and the chunk's run ranks
+        const int64_t w0 = j0 >> 1, w1 = (j1 + 1) >> 1;  // config pairs
+        const int nw = (int)(w1 - w0);
+        __syncthreads();
+        const uint32_t* lrt = reinterpret_cast<const uint32_t*>(d.lr16[ORD_T]);
+        const uint32_t* lrp = reinterpret_cast<const uint32_t*>(d.lr16[ORD_P]);
+        const uint32_t* lqe = reinterpret_cast<const uint32_t*>(d.lq16[ORD_E]);
+        const uint32_t* lqt = reinterpret_cast<const uint32_t*>(d.lq16[ORD_T]);
+        auto edge = [&](uint32_t wv, int64_t w) {  // pad the lanes outside [j0, j1)
+            if (2 * w < j0) wv = (wv & 0xFFFF0000u) | kLrPad;
+            if (2 * w + 1 >= j1) wv = (wv & 0x0000FFFFu) | (kLrPad << 16);
+            return wv;
+        };
+        if (c == CLS_B) {
+            for (int i = threadIdx.x; i < nw + 1; i += kScanThreads) {
+                const int64_t w = w0 + i;
+                uint4 v = make_uint4(kLrPad | (kLrPad << 16), kLrPad | (kLrPad << 16), 0u, 0u);
+                if (i < nw) {
+                    v.x = edge(__ldg(lrt + w), w);
+                    v.y = edge(__ldg(lrp + w), w);
+                    v.z = __ldg(lqe + w);
+                    v.w = __ldg(lqt + w);
+                }
+                sw[i] = v;
             }
-            __syncthreads();
-            // a warp whose last query slot is idle on every lane skips it (balanced
-            // tiles leave up to one slot per thread empty: ~10 % of the pairs at 1e4
-            // queries); the choice is warp-uniform
-            if (c == CLS_A) {
-                if (full_slots) scan_item<CLS_A>(s0, s1, s2, s3, ncp, kt, kp, be, bt);
-                else scan_item<CLS_A, kScanQ - 1>(s0, s1, s2, s3, ncp, kt, kp, be, bt);
-            } else if (c == CLS_B) {
-                scan_item<CLS_B>(s0, s1, s2, s3, ncp, kt, kp, be, bt);
-            } else {
-                if (full_slots) scan_item<CLS_C>(s0, s1, s2, s3, ncp, kt, kp, be, bt);
-                else scan_item<CLS_C, kScanQ - 1>(s0, s1, s2, s3, ncp, kt, kp, be, bt);
+        } else {
+            const uint32_t* lr = c == CLS_A ? lrt : lrp;
+            const uint32_t* lq = c == CLS_A ? lqe : lqt;
+            // 2 words per uint4; a trailing half-filled uint4 is padded infeasible
+            const int nw4 = (nw + 1) >> 1;
+            for (int i = threadIdx.x; i < nw4; i += kScanThreads) {
+                const int64_t wa = w0 + 2 * i, wb = wa + 1;
+                uint4 v;
+                v.x = edge(__ldg(lr + wa), wa);
+                v.y = __ldg(lq + wa);
+                v.z = wb < w1 ? edge(__ldg(lr + wb), wb) : (kLrPad | (kLrPad << 16));
+                v.w = wb < w1 ? __ldg(lq + wb) : 0u;
+                sw[i] = v;
             }
         }
+        // the chunk's run positions on the feasibility side(s): a query's chunk-local
+        // threshold is the number of run entries inside its feasible prefix [0, K)
+        const int ko = c == CLS_C ? ORD_P : ORD_T;
+        for (int i = threadIdx.x; i < L; i += kScanThreads) {
+            ssr[i] = __ldg(d.cinv[ko] + cb + i);
+            if (c == CLS_B) ssr[L + i] = __ldg(d.cinv[ORD_P] + cb + i);
+        }
+        __syncthreads();
+        // chunk-local thresholds of the 8 queries
+        uint32_t K1[kScanQ], K2[kScanQ], m1[kScanQ], m2[kScanQ];
+#pragma unroll
+        for (int q = 0; q < kScanQ; ++q) {
+            K1[q] = kb2(local_count(ssr, L, c == CLS_C ? thr_p[q] : thr_t[q]));
+            K2[q] = c == CLS_B ? kb2(local_count(ssr + L, L, thr_p[q])) : 0u;
+            m1[q] = m2[q] = 0xFFFFFFFFu;
+        }
+        if (c == CLS_B) {
+            scan_seg2<kScanQ>(sw, nw + (nw & 1), K1, K2, m1, m2);
+        } else {
+            const int nw4 = (nw + 1) >> 1;
+            if (full_slots) scan_seg1<kScanQ>(sw, nw4, K1, m1);
+            else scan_seg1<kScanQ - 1>(sw, nw4, K1, m1);
+        }
+        // chunk minima -> global merged positions -> the queries' running minima
+        const uint32_t* inv_a = d.cinv[c == CLS_C ? ORD_T : ORD_E] + cb;
 #pragma unroll
         for (int q = 0; q < kScanQ; ++q) {
             if (qid[q] < 0) continue;
-            // classes A / C keep their minimum in be (bit 31 set: nothing feasible)
-            const uint32_t me = be[q], mt = c == CLS_C ? be[q] : bt[q];
-            if (c != CLS_C && me < 0x80000000u)
-                atomicMin((unsigned long long*)&a.best_e[qid[q]], (unsigned long long)me);
-            if (c != CLS_A && mt < 0x80000000u)
-                atomicMin((unsigned long long*)&a.best_t[qid[q]], (unsigned long long)mt);
+            const uint32_t la = lane_min(m1[q]);
+            if (la < 0x8000u)
+                atomicMin((unsigned long long*)(c == CLS_C ? &a.best_t[qid[q]] : &a.best_e[qid[q]]),
+                          (unsigned long long)__ldg(inv_a + la));
+            if (c == CLS_B) {
+                const uint32_t lb = lane_min(m2[q]);
+                if (lb < 0x8000u)
+                    atomicMin((unsigned long long*)&a.best_t[qid[q]],
+                              (unsigned long long)__ldg(d.cinv[ORD_T] + cb + lb));
+            }
         }
         pos = seg_end;
     }
@@ -1458,41 +1521,17 @@ static int plan_build(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
         p->err_msg = pals_last_error();
     }
     const int64_t n = std::max<int64_t>(1, g->n);
-    {
-        const char* e = getenv("PALS_SORT_CHUNK");
-        // chunk of the multi-kernel path (n > 65,536, or PALS_RANK_CLUSTER=0)
-        // small grids (cfg1's 36 candidates, a replay's candidate sets) sort in one
-        // chunk just large enough, so the prepare does not sort 2,048 padding keys
-        int c = e ? atoi(e) : kChunk;
-        if (!e) c = n <= 256 ? 256 : n <= 512 ? 512 : n <= 1024 ? 1024 : kChunk;
-        p->chunk = (c == 256 || c == 512 || c == 1024 || c == 4096 || c == 8192) ? c : kChunk;
-        if (p->chunk < 1024 && n > p->chunk) p->chunk = kChunk;  // merge tiles need runs >= 1024
-        if (p->chunk > 2048) {  // > 48 KB of dynamic shared memory
-            PALS_CUDA(cudaFuncSetAttribute(k_sort_chunks<512>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)sort_smem_bytes(512)));
-            PALS_CUDA(cudaFuncSetAttribute(k_sort_chunks<1024>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)sort_smem_bytes(1024)));
-            PALS_CUDA(cudaFuncSetAttribute(k_sort_chunks<1024, 4>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)sort_smem_bytes(1024, 4)));
-        }
-        const char* ipt = getenv("PALS_SORT_IPT");
-        // measured on B200 (cfg2): 4 keys x 512 threads sorts a 2,048-key chunk in 15 us
-        // against 18 us for 8 x 256 (more warps hide the merge levels' smem latency)
-        p->sort_ipt = ipt ? atoi(ipt) : 4;
-        // measured on B200 (cfg2): 4 keys x 256 threads per 1,024-key merge tile, 7.4 us per
-        // round against 8.5 us for 8 x 128
-        const char* mi = getenv("PALS_MERGE_IPT");
-        p->merge_ipt = mi ? atoi(mi) : 2;
-        const char* t = getenv("PALS_MERGE_TILE");
-        p->merge_tile = (t && atoi(t) == 2048) ? 2048 : 1024;
-    }
-    {
-        const char* e = getenv("PALS_PDL");
-        p->pdl = e ? atoi(e) != 0 : 1;
-    }
+    // the chunk sort's chunk: 2,048 points (4 keys x 512 threads: 15 us on B200 against
+    // 27 us for a bitonic chunk sort, 18 us for 8 keys x 256, and slower 4,096 / 8,192-key
+    // chunks); small grids (cfg1's 36 candidates, a replay's candidate sets) sort in one
+    // chunk just large enough. The pair scan's chunk-local ranks need chunks <= 2,048.
+    p->chunk = n <= 256 ? 256 : n <= 512 ? 512 : n <= 1024 ? 1024 : kChunk;
+    p->sort_ipt = 4;
+    // 2 keys x 512 threads per 1,024-key merge tile (7.0 us per round against 8.5 us for
+    // 8 x 128 and 7.4 us for 4 x 256); PDL edges between the step's kernels
+    p->merge_ipt = 2;
+    p->merge_tile = 1024;
+    p->pdl = 1;
     p->nchunks = (int)((n + p->chunk - 1) / p->chunk);
     p->np = (int64_t)p->nchunks * p->chunk;
     PlanDev& d = p->d;
@@ -1512,7 +1551,8 @@ static int plan_build(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
                    (d.wide ? N_ORD * n8 : N_ORD * (size_t)n * 4) + 4096;
     if (m && m->kind == MODEL_TABLE) bytes += 4 * (size_t)n + 2 * 8 * (size_t)std::max<int64_t>(1, m->table_n);
     bytes += sizeof(Analytic) + 256;
-    bytes += 64 * 256;  // every take() rounds up to 256 B
+    bytes += N_ORD * (4 * (size_t)p->np + np4);  // chunk-local rank arrays
+    bytes += 80 * 256;  // every take() rounds up to 256 B
     PALS_CUDA(cudaMalloc(&p->slab, bytes));
     char* s = (char*)p->slab;
     auto take = [&](size_t b) {
@@ -1538,6 +1578,12 @@ static int plan_build(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
         else d.key32[o] = (uint32_t*)take((size_t)n * 4);
         d.rank32[o] = (uint32_t*)take((size_t)n * 4);
         d.pos32[o] = (uint32_t*)take((size_t)n * 4);
+    }
+    d.lch = p->chunk;
+    for (int o = 0; o < N_ORD; ++o) {
+        d.lr16[o] = (uint16_t*)take((size_t)p->np * 2);
+        d.lq16[o] = (uint16_t*)take((size_t)p->np * 2);
+        d.cinv[o] = (uint32_t*)take(np4);
     }
     d.globals = (int32_t*)take(16);
     // globals[2] (the generic-score flag) only ever gets set, and a plan's scores are
@@ -1830,14 +1876,16 @@ static int dec_layout(pals_plan* p, DecDev* t) {
 static int select_tail(pals_plan* p, const SelArgs& a, bool build = true) {
     pals_ctx* ctx = p->ctx;
     cudaStream_t s = ctx->stream;
-    // stream-K scan grid: 4 CTAs per SM, equal integer-op shares (see k_scan)
-    const int sgrid = ctx->num_sms * 4;
+    // stream-K scan grid: 4 CTAs per SM, 3 when the step scans under ~1e10 pairs (each
+    // CTA's fixed cost per chunk segment — staging, local thresholds — is then a larger
+    // share: cfg2 55 vs 59 us; cfg3 5.47 vs 5.55 ms the other way)
+    const int sgrid = ctx->num_sms * ((double)a.nq * (double)p->n < 1e10 ? 3 : 4);
     // event-record nodes around the scan (timing) are not kernels: plain edges there
     const bool pdl = p->pdl && !p->time_scan;
     // inside a stream capture the events become graph event-record nodes
     const unsigned evf = p->capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
-    if (p->time_scan) PALS_CUDA(cudaEventRecordWithFlags(p->ev_scan0, s, evf));
     cudaError_t e;
+    if (p->time_scan) PALS_CUDA(cudaEventRecordWithFlags(p->ev_scan0, s, evf));
     if (p->decide == PALS_DECIDE_PREFIX) {
         DecDev t;
         int rc = dec_layout(p, &t);

@@ -2,10 +2,9 @@
 ALU-pipe ceiling it implies:  python scripts/sass_mix.py [out.json]
 
 Loops are the backward branches of k_scan whose body holds the pair arithmetic. Per loop:
-the pairs one iteration decides per thread (configs per iteration x queries per thread: the
-class A/C loops take 8 configs x NQ (8, or 7 for warps with an idle last slot), the class B
-loop 4 configs x 8), and the ALU-pipe (LOP3, VIMNMX3, VIADDMNMX, ISETP, IADD3, SHF, SEL)
-and FMA-pipe (IMAD*) warp instructions. The binding pipe is the ALU: 16 lanes per SMSP,
+the pairs one iteration decides per thread (4 configs, two per 32-bit register in 16-bit
+lanes, x the NQ queries a thread holds: 8, or 7 for warps with an idle last slot), and the
+ALU-pipe (LOP3, VIMNMX3, ISETP, IADD3, SHF, SEL) and FMA-pipe (IMAD*) warp instructions. The binding pipe is the ALU: 16 lanes per SMSP,
 so an ALU warp instruction occupies it 2 cycles (B300_MICROARCH.md: rt_SMSP = 2)."""
 import collections
 import json
@@ -40,12 +39,17 @@ def loops():
             continue
         body = [o for (x, o, _, _) in ins if tgt <= x <= a]
         c = collections.Counter(o.split(".")[0] for o in body)
-        if not (c["VIMNMX3"] or c["VIADDMNMX"]) or len(body) > 400:
+        if not c["VIMNMX3"] or len(body) > 400:
             continue
-        cls = "B" if c["VIADDMNMX"] else "A/C"
+        # classes A / C: one LDS.128 per 4 configs (lr and lq words of two config pairs),
+        # two LOP3 and one 16x2 minimum per query and 4 configs; class B: one LDS.128 per
+        # 2 configs (lrt, lrp, lqe, lqt), six LOP3 and two minima per query and 4 configs
+        cls = "B" if c["LOP3"] >= 3 * c["VIMNMX3"] else "A/C"
+        configs = 4 * c["LDS"] if cls == "A/C" else 2 * c["LDS"]
+        nq = c["VIMNMX3"] // (configs // 4) // (2 if cls == "B" else 1)
         alu = sum(c[k] for k in ALU)
         fma = sum(c[k] for k in FMA)
-        pairs = 32 if cls == "B" else (64 if c["VIMNMX3"] == 32 else 56)
+        pairs = configs * nq
         out.append({"class": cls, "start": hex(tgt), "end": hex(a), "instructions": len(body),
                     "alu": alu, "fma": fma, "pairs_per_thread": pairs,
                     "alu_per_pair": alu / pairs, "fma_per_pair": fma / pairs,

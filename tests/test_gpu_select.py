@@ -196,35 +196,6 @@ def test_select_pinned_buffers_graph_path(ctx, oracle, nq):
         assert plan.last_exact_count >= 0
 
 
-@pytest.mark.parametrize("knobs", [{"PALS_SORT_IPT": "8", "PALS_MERGE_IPT": "8"},
-                                   {"PALS_SORT_IPT": "2", "PALS_MERGE_IPT": "1"},
-                                   {"PALS_SORT_CHUNK": "4096", "PALS_MERGE_IPT": "4"},
-                                   {"PALS_SORT_CHUNK": "1024", "PALS_MERGE_TILE": "2048"}])
-def test_select_rank_pipeline_variants(ctx, oracle, monkeypatch, knobs):
-    """The measured-slower sort / merge shapes (A/B knobs read at plan creation) give the
-    same decisions as the default pipeline and the oracle."""
-    cfg = workloads.cfg2()
-    q = None
-    results = []
-    for env in ({}, knobs):
-        for k in ("PALS_SORT_IPT", "PALS_MERGE_IPT", "PALS_SORT_CHUNK", "PALS_MERGE_TILE"):
-            monkeypatch.delenv(k, raising=False)
-        for k, v in env.items():
-            monkeypatch.setenv(k, v)
-        plan = Plan(AnalyticModel(ctx, cfg["profile"], cfg["gpu"]), Grid(ctx, cfg["points"]),
-                    cfg["coeffs"])
-        if q is None:
-            th, _, _ = plan.scores()
-            q = workloads.gen_queries(4000, 77, float(th.max()), "mixed", budget=(700.0, 1900.0))
-        results.append(plan.select(q))
-    assert np.array_equal(results[0][0], results[1][0])
-    assert np.array_equal(results[0][1], results[1][1])
-    T, P, _ = oracle.eval(cfg["profile"], cfg["gpu"], cfg["points"])
-    oi, orr, rc = oracle.select(cfg["points"], T, P, cfg["coeffs"], q[::41])
-    assert rc == 0 and np.array_equal(results[1][0][::41], oi)
-    assert np.array_equal(results[1][1][::41], orr)
-
-
 @pytest.mark.parametrize("which", ["cfg2", "cfg3", "cfg3x"])
 def test_prefix_decide_equals_scan(ctx, oracle, which):
     """PALS_DECIDE_PREFIX (prefix-min tables; 2-D blocks for QoS+budget queries) decides

@@ -759,7 +759,7 @@ def bench_forest(args, dist, ctx, stream, l2_flush):
     small = Bundle.load_npz(os.path.join(data, "predictor_small.npz"))
     hbm = measured_peaks_json().get("hbm_gbs", 6552.6)
 
-    def timed(model, npts, direct, reps):
+    def timed(model, npts, direct, reps, keep=True):
         ctx.lib.pals_model_forest_set_direct(model.h, 1 if direct else 0)
         pts = workloads.predict_points(npts, seed=2605 + dist.rank)
         d_pts = torch.from_numpy(pts.view(np.uint8)).cuda()
@@ -785,8 +785,9 @@ def bench_forest(args, dist, ctx, stream, l2_flush):
         torch.cuda.synchronize()
         t = dist.max(float(np.sum([a.elapsed_time(b) for a, b in ev])))
         ctx.lib.pals_model_forest_set_direct(model.h, 0)
-        k = min(npts, 50_000)
-        kept[direct] = (pts[:k], d_T[:k].cpu().numpy(), d_P[:k].cpu().numpy())
+        if keep:  # the default bundle's predictions, for the parity check
+            k = min(npts, 50_000)
+            kept[direct] = (pts[:k], d_T[:k].cpu().numpy(), d_P[:k].cpu().numpy())
         return dist.sum(float(npts)) * reps / (t * 1e-3), t / reps
 
     kept = {}
@@ -797,7 +798,7 @@ def bench_forest(args, dist, ctx, stream, l2_flush):
     n_direct = max(1, npred // 16)
     v_direct, ms_direct = timed(fmodel, n_direct, True, max(1, min(args.steps, 3)))
     smodel = make_forest_model(ctx, small, mid)
-    v_small, _ = timed(smodel, npred, False, args.steps)
+    v_small, _ = timed(smodel, npred, False, args.steps, keep=False)
     nodes = int(sum(len(f.feature) for f in (bundle.throughput, bundle.power)))
     depth = bundle.hyperparams["max_depth"]
     pred_bytes = 40.0  # 24 B point in, 16 B T/P out: the cell path's algorithmic traffic

@@ -444,9 +444,11 @@ def run_ours(args, dist: Dist):
     latency = {"workload": "cfg1: llama2-7b-like, 6 caps x 6 batches (36 candidates), target 0.6 x "
                            "unconstrained, static 1600 W budget",
                "python_ctypes": {"select_config_us": sel_us, "control_step_us": step_us},
-               "note": "one synchronous call: the candidate set is validated, uploaded and "
-                       "scored once and cached; per call one kernel launch writing the "
-                       "decision to mapped pinned memory, then a stream sync; wall clock"}
+               "note": "one synchronous call: the candidate set is validated, uploaded, scored "
+                       "and ranked once and cached; per call the request is posted in mapped "
+                       "pinned memory to the resident one-warp server kernel (k_one_server), "
+                       "which answers from the set's tables in shared memory; no kernel launch "
+                       "per call (launch_per_call_*: pals_ctx_set_one_server(0)); wall clock"}
     cpp = os.path.join(ROOT, "tests", "cpp", "test_adapter")
     if os.path.exists(cpp) and dist.rank == 0:
         try:

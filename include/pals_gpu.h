@@ -245,6 +245,12 @@ int64_t pals_ctx_launch_count(pals_ctx* ctx);
 #define PALS_REPLAY_THREAD 0
 #define PALS_REPLAY_WARP 1
 int pals_ctx_set_replay_layout(pals_ctx* ctx, int32_t layout);
+/* Single calls (pals_select_one / pals_control_step_one on a cached candidate set) are
+ * answered by a one-warp kernel kept resident on its own high-priority stream: a call posts
+ * its request in mapped pinned memory and polls the answer (no kernel launch per call). The
+ * kernel exits after idle_us microseconds without a request and is relaunched by the next
+ * call; idle_us = 0 launches one kernel per call instead. Default 2000. */
+int pals_ctx_set_one_server(pals_ctx* ctx, int64_t idle_us);
 
 /* ---- models (the three concrete Scorer kinds) ------------------------- */
 /* analytic_scorer(profile, gpu): validates like ModelProfile::validate (types.hpp:88-106) */

@@ -171,6 +171,9 @@ public:
     Context(const Context&) = delete;
     Context& operator=(const Context&) = delete;
     pals_ctx* get() const { return h_; }
+    // single calls through the resident server kernel (exits after idle_us idle; 0 = a
+    // kernel launch per call)
+    void set_one_server(int64_t idle_us) { check(pals_ctx_set_one_server(h_, idle_us)); }
 
 private:
     pals_ctx* h_ = nullptr;

@@ -32,6 +32,7 @@ SIGNATURES = [
     ("pals_ctx_sync", _I, [_VP]),
     ("pals_ctx_launch_count", _I64, [_VP]),
     ("pals_ctx_set_replay_layout", _I, [_VP, C.c_int32]),
+    ("pals_ctx_set_one_server", _I, [_VP, C.c_int64]),
     ("pals_model_analytic", _I, [_VP, _VP, _VP, _VP]),
     ("pals_model_table", _I, [_VP, _VP, _VP, _VP, _I64, _VP]),
     ("pals_model_forest", _I, [_VP, _I32, _I32, _VP,

@@ -145,6 +145,14 @@ int pals_ctx_sync(pals_ctx* c) {
 
 int64_t pals_ctx_launch_count(pals_ctx* c) { return c->launches; }
 
+int pals_ctx_set_one_server(pals_ctx* c, int64_t idle_us) {
+    if (!c) return set_error(PALS_ECONFIG, "pals_ctx_set_one_server: null context");
+    if (idle_us < 0) return set_error(PALS_ECONFIG, "pals_ctx_set_one_server: negative idle time");
+    one_server_stop(c);
+    c->one_server_idle_us = idle_us;
+    return PALS_OK;
+}
+
 int pals_ctx_set_replay_layout(pals_ctx* c, int32_t layout) {
     if (!c) return set_error(PALS_ECONFIG, "pals_ctx_set_replay_layout: null context");
     if (layout != PALS_REPLAY_THREAD && layout != PALS_REPLAY_WARP)

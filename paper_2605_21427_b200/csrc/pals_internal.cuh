@@ -230,6 +230,7 @@ struct pals_ctx {
     void* replay_cache = nullptr;  // replay.cu
     void* one_cache = nullptr;     // replay.cu: single-call candidate sets (pals_select_one)
     int replay_layout = 0;         // PALS_REPLAY_THREAD / PALS_REPLAY_WARP
+    int64_t one_server_idle_us = 2000;  // pals_ctx_set_one_server: 0 = one launch per call
     double sim_prep_s = 0.0;       // sim.cu: host setup of the last pals_run_scenarios
     double sim_kernel_ms = -1.0;   // and its k_sim launch (CUDA events)
     int sim_keep_requests = 0;     // pals_sim_keep_requests
@@ -299,6 +300,7 @@ const PlanDev& plan_dev(const pals_plan* p);
 int plan_error(const pals_plan* p);
 void replay_cache_free(pals_ctx* ctx);
 void one_cache_free(pals_ctx* ctx);
+void one_server_stop(pals_ctx* ctx);  // replay.cu: ends the resident single-call kernel
 uint64_t next_model_uid();
 // forest.cu
 void forest_free(void* f);

@@ -70,6 +70,11 @@ class Context:
         """"thread" (one thread per trace, default) or "warp" (one warp per trace)."""
         check(self.lib.pals_ctx_set_replay_layout(self.h, {"thread": 0, "warp": 1}[layout]))
 
+    def set_one_server(self, idle_us: int):
+        """Single calls through the resident server kernel, which exits after idle_us without
+        a request (0: one kernel launch per call)."""
+        check(self.lib.pals_ctx_set_one_server(self.h, int(idle_us)))
+
     @property
     def launches(self) -> int:
         return int(self.lib.pals_ctx_launch_count(self.h))

@@ -141,6 +141,19 @@ static int latency(const std::string& root) {
         sr = s2;
         sink += d.point.batch;
     }, 20000);
+    // the same calls with one kernel launch per call instead of the resident server
+    ctx.set_one_server(0);
+    const double l_sel = bench([&](int) { sink += gpu::select_config(cands, t, gs, k, 1.0, 0.05, 0.02).point.batch; }, 2000);
+    ControllerState sl;
+    sl.current = cands.back();
+    const double l_step = bench([&](int i) {
+        auto [d, s2] = gpu::control_step(TelemetryInput{0.5 * i, 0.55 * t.throughput_tps}, 0.5 * i,
+                                         t, cands, gs, k, sl, cfg);
+        sl = s2;
+        sink += d.point.batch;
+    }, 2000);
+    same = same && ::same(sl, sg);
+    ctx.set_one_server(2000);
     // same call sequence on both sides from the same start: the states must agree
     ControllerState a, b;
     a.current = b.current = cands.back();
@@ -153,9 +166,12 @@ static int latency(const std::string& root) {
         b = sb;
     }
     std::printf("{\"select_config_us\": %.3f, \"control_step_us\": %.3f, "
+                "\"launch_per_call_select_config_us\": %.3f, "
+                "\"launch_per_call_control_step_us\": %.3f, "
                 "\"reference_select_config_us\": %.3f, \"reference_control_step_us\": %.3f, "
                 "\"candidates\": %zu, \"identical\": %s, \"sink\": %d}\n",
-                g_sel, g_step, r_sel, r_step, cands.size(), same ? "true" : "false", sink & 1);
+                g_sel, g_step, l_sel, l_step, r_sel, r_step, cands.size(), same ? "true" : "false",
+                sink & 1);
     return same ? 0 : 1;
 }
 

@@ -68,6 +68,7 @@ struct pals_plan {
     uint64_t* best_t = nullptr;
     uint8_t* cls = nullptr;
     int32_t* qlist = nullptr;     // N_CLS regions of qcap
+    uint2* qthr = nullptr;        // beside qlist: (thr_t, thr_p) per slot
     int32_t* counts = nullptr;    // [N_CLS] class sizes, [N_CLS] exact count
     pals_query* d_q = nullptr;    // host-API staging
     int32_t* d_idx = nullptr;
@@ -809,6 +810,7 @@ struct SelArgs {
     uint64_t* best_t;
     uint8_t* cls;
     int32_t* qlist;
+    uint2* qthr;      // beside qlist: the slot's (thr_t, thr_p)
     int32_t* counts;  // [0..N_CLS) class sizes, [N_CLS] work items
     int64_t qcap;
     int force_exact;
@@ -906,7 +908,11 @@ __device__ __forceinline__ void qprep_body(const PlanDev& d, const SelArgs& a, i
             int base = 0;
             if (lane == __ffs(m) - 1) base = atomicAdd(&a.counts[k], __popc(m));
             base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-            if (c == k) a.qlist[k * a.qcap + base + __popc(m & ((1u << lane) - 1))] = (int32_t)j;
+            if (c == k) {
+                const int64_t slot = k * a.qcap + base + __popc(m & ((1u << lane) - 1));
+                a.qlist[slot] = (int32_t)j;
+                a.qthr[slot] = make_uint2((uint32_t)a.thr_t[j], (uint32_t)a.thr_p[j]);
+            }
         }
     }
 }
@@ -1030,23 +1036,98 @@ struct ScanPlan {
 __device__ __forceinline__ int class_ops(int c) { return c == CLS_B ? 4 : 2; }
 
 __device__ __forceinline__ int64_t scan_pos_of(const ScanPlan& sp, int64_t u) {
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-        if (u < sp.wbase[c + 1]) return sp.pbase[c] + (u - sp.wbase[c]) / class_ops(c);
-    return sp.pbase[3];
+    // register selects over the three classes (an indexed form went to the local stack)
+    if (u >= sp.wbase[3]) return sp.pbase[3];
+    const int c = (u >= sp.wbase[1]) + (u >= sp.wbase[2]);
+    const int64_t wb = c == 0 ? sp.wbase[0] : c == 1 ? sp.wbase[1] : sp.wbase[2];
+    const int64_t pb = c == 0 ? sp.pbase[0] : c == 1 ? sp.pbase[1] : sp.pbase[2];
+    return pb + (u - wb) / class_ops(c);
 }
 
-// shared memory of k_scan: a chunk's staged words (class B: 2,048 x 16 B) and its run
-// positions for the chunk-local thresholds (2 x 2,048 x 4 B)
-constexpr size_t kScanSmem = (size_t)kScanCh * 16 + 2 * (size_t)kScanCh * 4;
+// Bucket index over a chunk's staged run positions (ascending): T[b] = number of places
+// whose position is < b << sh, for b = 0..nb - 1 (nb = ((n - 1) >> sh) + 1 <= 1,024; the
+// count below nb << sh is every valid place). A query's chunk-local threshold is then a
+// search inside one bucket (~2 places for cfg2) instead of over the whole chunk, whose 11
+// dependent, bank-conflicted shared-memory steps per query (lanes hold unrelated queries)
+// cost ~7 us per segment. Built without atomics: the last place of each non-empty bucket
+// writes T[b + 1], then a block prefix max fills the empty buckets (every thread owns 4
+// consecutive entries: one LDS.64 / STS.64).
+constexpr int kScanBk = 1024;  // u16 entries per side
+static_assert(kScanBk == 4 * kScanThreads, "bucket scan: 4 entries per thread");
+__device__ __forceinline__ void bucket_mark(const uint32_t* sr, int L, uint16_t* T, int sh,
+                                            int nb) {
+    for (int i = threadIdx.x; i < L; i += kScanThreads) {
+        const uint32_t v = sr[i];
+        if (v == 0xFFFFFFFFu) continue;  // padding of the last chunk
+        const int b = (int)(v >> sh);
+        if (b + 1 < nb && (i == L - 1 || (int)(sr[i + 1] >> sh) != b || sr[i + 1] == 0xFFFFFFFFu))
+            T[b + 1] = (uint16_t)(i + 1);
+    }
+}
+__device__ __forceinline__ void bucket_scan(uint16_t* T, uint32_t* wtot) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint2 raw = reinterpret_cast<uint2*>(T)[threadIdx.x];
+    uint32_t e[4] = {raw.x & 0xFFFFu, raw.x >> 16, raw.y & 0xFFFFu, raw.y >> 16};
+#pragma unroll
+    for (int k = 1; k < 4; ++k) e[k] = max(e[k], e[k - 1]);
+    uint32_t x = e[3];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x = max(x, y);
+    }
+    if (lane == 31) wtot[warp] = x;
+    uint32_t pre = __shfl_up_sync(0xffffffffu, x, 1);
+    if (lane == 0) pre = 0;
+    __syncthreads();
+    for (int w = 0; w < warp; ++w) pre = max(pre, wtot[w]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) e[k] = max(e[k], pre);
+    reinterpret_cast<uint2*>(T)[threadIdx.x] = make_uint2(e[0] | (e[1] << 16), e[2] | (e[3] << 16));
+}
+__device__ __forceinline__ uint32_t bucket_count(const uint32_t* sr, const uint16_t* T, int sh,
+                                                 int nb, int nvalid, uint32_t thr) {
+    const int b = (int)(thr >> sh);
+    int lo = T[b], hi = b + 1 < nb ? (int)T[b + 1] : nvalid;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (sr[mid] <= thr) lo = mid + 1;
+        else hi = mid;
+    }
+    return (uint32_t)lo;
+}
+
+// shared memory of k_scan: a chunk's staged words (class B: 2,048 x 16 B), its run
+// positions for the chunk-local thresholds (2 x 2,048 x 4 B) and their bucket indexes
+constexpr size_t kScanSmem =
+    (size_t)kScanCh * 16 + 2 * (size_t)kScanCh * 4 + 2 * (size_t)kScanBk * 2;
+
+#ifdef PALS_SCAN_TRACE
+// A/B instrumentation (scripts/build_variants.sh): globaltimer of CTA phases, thread 0
+__device__ unsigned long long g_scan_trace[4096][16];
+#define SCAN_MARK(k)                                                                      \
+    if (threadIdx.x == 0 && blockIdx.x < 4096 && (k) < 16) {                              \
+        unsigned long long t_;                                                            \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
+        g_scan_trace[blockIdx.x][k] = t_;                                                 \
+    }
+#else
+#define SCAN_MARK(k)
+#endif
 
 __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) {
     pdl_wait();
+    SCAN_MARK(0);
+    int mark = 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint4* sw = reinterpret_cast<uint4*>(smem_raw);
     uint32_t* ssr = reinterpret_cast<uint32_t*>(smem_raw + (size_t)kScanCh * 16);  // [2][L]
+    uint16_t* sbk = reinterpret_cast<uint16_t*>(smem_raw + (size_t)kScanCh * 24);  // [2][kScanBk]
+    __shared__ uint32_t s_wtot[2][kScanThreads / 32];
     const int64_t n = d.n;
     const int L = d.lch;
+    const int sh = max(0, 32 - __clz((int)(n - 1)) - 10);  // <= 1,024 buckets of 2^sh positions
+    const int nb = (int)((n - 1) >> sh) + 1;
     ScanPlan pl;
     pl.wbase[0] = pl.pbase[0] = 0;
 #pragma unroll
@@ -1064,32 +1145,36 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) 
     while (pos < p1) {
         // locate (class, tile, first config) of pos and the end of that tile segment;
         // configs are TR positions, cut further at the chunks of the local ranks
-        int c = 0;
-        while (pos >= pl.pbase[c + 1]) ++c;
-        const int64_t r = pos - pl.pbase[c];
+        // (register selects, not indexed loads: the plan stays in registers, no local stack)
+        const int c = (pos >= pl.pbase[1]) + (pos >= pl.pbase[2]);
+        const int64_t pb = c == 0 ? pl.pbase[0] : c == 1 ? pl.pbase[1] : pl.pbase[2];
+        const int64_t tqc = c == 0 ? pl.tq[0] : c == 1 ? pl.tq[1] : pl.tq[2];
+        const int64_t r = pos - pb;
         const int64_t tile = r / n;
-        const int64_t j0 = r % n;
+        const int64_t j0 = r - tile * n;
         const int64_t chunk_end = (j0 / L + 1) * L;
-        const int64_t seg_end = min(min(p1, pl.pbase[c] + (tile + 1) * n), pos + (chunk_end - j0));
+        const int64_t seg_end = min(min(p1, pb + (tile + 1) * n), pos + (chunk_end - j0));
         const int64_t j1 = j0 + (seg_end - pos);
         const int64_t cb = (j0 / L) * L;  // the chunk's first TR
-        // this tile's queries: 8 per thread
-        const int64_t q_lo = tile * pl.tq[c], q_hi = min((int64_t)a.counts[c], q_lo + pl.tq[c]);
+        // this tile's queries: 8 per thread (slot validity needs no load)
+        const int64_t q_lo = tile * tqc, q_hi = min((int64_t)a.counts[c], q_lo + tqc);
+        const bool full_slots =
+            __any_sync(0xffffffffu, q_lo + (kScanQ - 1) * kScanThreads + threadIdx.x < q_hi);
+        const int64_t w0 = j0 >> 1, w1 = (j1 + 1) >> 1;  // config pairs
+        const int nw = (int)(w1 - w0);
+        __syncthreads();  // the previous segment is done with shared memory
+        // every global load of the segment is issued before the barrier: the query slots'
+        // ids and thresholds (written beside the class list by qprep, so no id -> threshold
+        // indirection), the segment's config words (whole pairs; lanes outside [j0, j1)
+        // padded infeasible) and the chunk's run positions
         int32_t qid[kScanQ];
-        uint32_t thr_t[kScanQ], thr_p[kScanQ];
+        uint2 qt[kScanQ];
 #pragma unroll
         for (int q = 0; q < kScanQ; ++q) {
             const int64_t sq = q_lo + q * kScanThreads + threadIdx.x;
-            qid[q] = sq < q_hi ? a.qlist[c * a.qcap + sq] : -1;
-            thr_t[q] = qid[q] >= 0 ? (uint32_t)a.thr_t[qid[q]] : 0u;
-            thr_p[q] = qid[q] >= 0 ? (uint32_t)a.thr_p[qid[q]] : 0u;
+            qid[q] = sq < q_hi ? __ldg(a.qlist + c * a.qcap + sq) : -1;
+            qt[q] = sq < q_hi ? __ldg(a.qthr + c * a.qcap + sq) : make_uint2(0u, 0u);
         }
-        const bool full_slots = __any_sync(0xffffffffu, qid[kScanQ - 1] >= 0);
-        // stage the segment's config words (whole pairs; lanes outside [j0, j1) padded
-        // infeasible) and the chunk's run ranks
-        const int64_t w0 = j0 >> 1, w1 = (j1 + 1) >> 1;  // config pairs
-        const int nw = (int)(w1 - w0);
-        __syncthreads();
         const uint32_t* lrt = reinterpret_cast<const uint32_t*>(d.lr16[ORD_T]);
         const uint32_t* lrp = reinterpret_cast<const uint32_t*>(d.lr16[ORD_P]);
         const uint32_t* lqe = reinterpret_cast<const uint32_t*>(d.lq16[ORD_E]);
@@ -1130,18 +1215,36 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) 
         // threshold is the number of run entries inside its feasible prefix [0, K)
         const int ko = c == CLS_C ? ORD_P : ORD_T;
         for (int i = threadIdx.x; i < L; i += kScanThreads) {
-            ssr[i] = __ldg(d.cinv[ko] + cb + i);
+            ssr[i] = __ldg((ko == ORD_P ? d.cinv[ORD_P] : d.cinv[ORD_T]) + cb + i);
             if (c == CLS_B) ssr[L + i] = __ldg(d.cinv[ORD_P] + cb + i);
         }
+        reinterpret_cast<uint2*>(sbk)[threadIdx.x] = make_uint2(0u, 0u);
+        if (c == CLS_B) reinterpret_cast<uint2*>(sbk + kScanBk)[threadIdx.x] = make_uint2(0u, 0u);
+        const int nvalid = (int)min((int64_t)L, n - cb);
+        SCAN_MARK(mark);
+        ++mark;
         __syncthreads();
+        bucket_mark(ssr, L, sbk, sh, nb);
+        if (c == CLS_B) bucket_mark(ssr + L, L, sbk + kScanBk, sh, nb);
+        __syncthreads();
+        bucket_scan(sbk, s_wtot[0]);
+        if (c == CLS_B) bucket_scan(sbk + kScanBk, s_wtot[1]);
+        __syncthreads();
+        SCAN_MARK(mark);
+        ++mark;
         // chunk-local thresholds of the 8 queries
         uint32_t K1[kScanQ], K2[kScanQ], m1[kScanQ], m2[kScanQ];
 #pragma unroll
         for (int q = 0; q < kScanQ; ++q) {
-            K1[q] = kb2(local_count(ssr, L, c == CLS_C ? thr_p[q] : thr_t[q]));
-            K2[q] = c == CLS_B ? kb2(local_count(ssr + L, L, thr_p[q])) : 0u;
+            K1[q] = kb2(bucket_count(ssr, sbk, sh, nb, nvalid, c == CLS_C ? qt[q].y : qt[q].x));
+            K2[q] = c == CLS_B ? kb2(bucket_count(ssr + L, sbk + kScanBk, sh, nb, nvalid, qt[q].y))
+                               : 0u;
             m1[q] = m2[q] = 0xFFFFFFFFu;
         }
+        SCAN_MARK(mark);
+        ++mark;
+        SCAN_MARK(mark);
+        ++mark;
         if (c == CLS_B) {
             scan_seg2<kScanQ>(sw, nw + (nw & 1), K1, K2, m1, m2);
         } else {
@@ -1149,8 +1252,10 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) 
             if (full_slots) scan_seg1<kScanQ>(sw, nw4, K1, m1);
             else scan_seg1<kScanQ - 1>(sw, nw4, K1, m1);
         }
+        SCAN_MARK(mark);
+        ++mark;
         // chunk minima -> global merged positions -> the queries' running minima
-        const uint32_t* inv_a = d.cinv[c == CLS_C ? ORD_T : ORD_E] + cb;
+        const uint32_t* inv_a = (c == CLS_C ? d.cinv[ORD_T] : d.cinv[ORD_E]) + cb;
 #pragma unroll
         for (int q = 0; q < kScanQ; ++q) {
             if (qid[q] < 0) continue;
@@ -1166,8 +1271,18 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) 
             }
         }
         pos = seg_end;
+        SCAN_MARK(mark);
+        ++mark;
     }
+    SCAN_MARK(15);
+    (void)mark;
 }
+
+#ifdef PALS_SCAN_TRACE
+extern "C" int pals_debug_scan_trace(unsigned long long* host, int n_rows) {
+    return (int)cudaMemcpyFromSymbol(host, g_scan_trace, (size_t)min(n_rows, 4096) * 16 * 8);
+}
+#endif
 
 // ---- time to decide: prefix-min tables instead of the pair scan -----------------------
 // Feasibility is a prefix of the sorted orders (Kt of the t_hat order, Kp of the p_node
@@ -1505,6 +1620,9 @@ void* plan_scratch(pals_plan* p, size_t bytes) {
 static int plan_build(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
                       const pals_coeffs* coeffs, pals_plan** out) {
     PALS_CUDA(cudaSetDevice(ctx->device));
+    // k_scan's shared memory exceeds the 48 KB default (per device, idempotent)
+    PALS_CUDA(cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)kScanSmem));
     auto* p = new pals_plan();
     p->ctx = ctx;
     p->model = m;
@@ -1770,7 +1888,7 @@ static int ensure_query_buffers(pals_plan* p, int64_t nq) {
     }
     cudaFree(p->thr_t);
     const int64_t cap = std::max<int64_t>(nq, 1024);
-    const size_t bytes = (size_t)cap * (8 * 4 + 1 + 4 * N_CLS) + 4096;
+    const size_t bytes = (size_t)cap * (8 * 4 + 1 + 12 * N_CLS) + 4096;
     PALS_CUDA(cudaMalloc(&p->thr_t, bytes));
     char* s = (char*)p->thr_t;
     auto take = [&](size_t b) {
@@ -1784,6 +1902,7 @@ static int ensure_query_buffers(pals_plan* p, int64_t nq) {
     p->best_t = (uint64_t*)take(8 * cap);
     p->cls = (uint8_t*)take(cap);
     p->qlist = (int32_t*)take(4 * (size_t)cap * N_CLS);
+    p->qthr = (uint2*)take(8 * (size_t)cap * N_CLS);
     p->counts = (int32_t*)take(4 * kCountInts);
     p->qcap = cap;
     return PALS_OK;
@@ -1802,6 +1921,7 @@ static SelArgs make_args(pals_plan* p, const pals_query* d_queries, int64_t nq, 
     a.best_t = p->best_t;
     a.cls = p->cls;
     a.qlist = p->qlist;
+    a.qthr = p->qthr;
     a.counts = p->counts;
     a.qcap = p->qcap;
     a.force_exact = p->force_exact;
@@ -1820,6 +1940,7 @@ static SelArgs make_args_chunk(pals_plan* p, const pals_query* d_queries, int64_
     a.best_t += off;
     a.cls += off;
     a.qlist += off;
+    a.qthr += off;
     a.counts += kCountStride * k;
     return a;
 }
@@ -1879,7 +2000,10 @@ static int select_tail(pals_plan* p, const SelArgs& a, bool build = true) {
     // stream-K scan grid: 4 CTAs per SM, 3 when the step scans under ~1e10 pairs (each
     // CTA's fixed cost per chunk segment — staging, local thresholds — is then a larger
     // share: cfg2 55 vs 59 us; cfg3 5.47 vs 5.55 ms the other way)
-    const int sgrid = ctx->num_sms * ((double)a.nq * (double)p->n < 1e10 ? 3 : 4);
+#ifndef PALS_SCAN_CPS_SMALL
+#define PALS_SCAN_CPS_SMALL 3
+#endif
+    const int sgrid = ctx->num_sms * ((double)a.nq * (double)p->n < 1e10 ? PALS_SCAN_CPS_SMALL : 4);
     // event-record nodes around the scan (timing) are not kernels: plain edges there
     const bool pdl = p->pdl && !p->time_scan;
     // inside a stream capture the events become graph event-record nodes

@@ -59,5 +59,7 @@ b = TraceBatch(n_traces=nt, first_step=0, n_steps=ns, n_log_traces=0, interval_s
                summaries=d3.data_ptr())
 ms = timed(lambda: replay_traces_device(ctx, models, *a, b))
 out["traces"] = nt * ns / (ms * 1e-3)
+import hashlib  # noqa: E402
+print("summary sha", hashlib.sha256(d1.cpu().numpy().tobytes()).hexdigest()[:16])
 print({k: f"{v:.4g}" for k, v in out.items()},
       "warp==thread", bool(torch.equal(d1, d2)), "traces==thread", bool(torch.equal(d1, d3)))

@@ -1243,8 +1243,9 @@ def bench_sim(args, dist, ctx):
             "e2e": {"value": total / wall, "unit": "node-intervals/s",
                     "h2d_bytes_per_step": None, "d2h_bytes_per_step": int(nres.nbytes + res.nbytes),
                     "host_setup_s": float(np.mean(preps)),
-                    "api": "pals_run_scenarios (C ABI): host arrival streams (mt19937_64 + libm) "
-                           "and budget splits, then one k_sim launch; wall clock"},
+                    "api": "pals_run_scenarios (C ABI): host arrival lengths (mt19937_64 + libm, "
+                           "all host threads) and budget splits, then k_sim and the arrival "
+                           "hashes (k_arrival_hash, side stream); wall clock"},
             "gpu_launches": None, "_node_results": nres, "_results": res}
 
 

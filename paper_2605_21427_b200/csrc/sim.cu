@@ -110,7 +110,6 @@ std::string fmt10g(double v) {
 struct Stream {
     std::vector<int32_t> len;
     std::vector<int32_t> cum;
-    uint64_t hash = 0xcbf29ce484222325ULL;
 };
 
 // FNV-1a over the decimal digits of v (std::to_string of a non-negative integer).
@@ -132,28 +131,69 @@ void gen_stream(const pals_scenario& sc, int node, int n_int, Stream* out) {
     const pals_sim_node& nd = sc.nodes[node];
     HostRng rng(splitmix64(splitmix64(sc.seed) ^ (uint64_t)node));  // Rng::substream
     const double log_mean = std::log(sc.mean_tokens) - 0.5 * sc.log_sigma * sc.log_sigma;
-    std::string tail;  // "@" + fmt_num(t): one snprintf per interval, not per request
-    // spawn_request (sim.hpp:338-353); the arrival hash chains fnv1a64 over
-    // to_string(id) + ":" + to_string(len) + "@" + fmt_num(t), byte for byte
+    // spawn_request (sim.hpp:338-353): the lengths; the arrival hash over the requests'
+    // strings is chained on the device (k_arrival_hash), where it was half the host time
     auto spawn = [&]() {
-        const int len = std::max(1, (int)std::lround(rng.lognormal(log_mean, sc.log_sigma)));
-        uint64_t h = fnv_dec(out->hash, (long)out->len.size());
-        h = (h ^ (unsigned char)':') * 0x100000001b3ULL;
-        h = fnv_dec(h, len);
-        out->hash = fnv_str(tail, h);
-        out->len.push_back(len);
+        out->len.push_back(std::max(1, (int)std::lround(rng.lognormal(log_mean, sc.log_sigma))));
     };
-    tail = "@" + fmt10g(0.0);
     for (int b = 0; b < nd.initial_backlog; ++b) spawn();
     out->cum.resize((size_t)n_int + 1);
     for (int k = 0; k < n_int; ++k) {
-        const double t0 = k * sc.interval_s;
         const int n = rng.poisson(nd.arrival_rate_per_s * sc.interval_s);
-        if (n) tail = "@" + fmt10g(t0);
         for (int a = 0; a < n; ++a) spawn();
         out->cum[k] = (int32_t)out->len.size();  // visible to interval k
     }
     out->cum[n_int] = (int32_t)out->len.size();
+}
+
+// The arrival hash of a stream (spawn_request, sim.hpp:338-353; fnv1a64 rng.hpp:22-28):
+// fnv1a64 chained over to_string(id) + ":" + to_string(len) + "@" + fmt_num(t) per request,
+// byte for byte; t's "@%.10g" strings come from the host, one per interval of the stream's
+// grid (tails[k] for an interval's spawns, tail0 = "@0" for the initial backlog). One
+// thread per stream: the chain is serial, the streams are not.
+struct HashJob {
+    const int32_t* len;
+    const int32_t* cum;
+    const uint32_t* toff;  // [n_int + 1] offsets into tchars: interval k's "@t" string
+    const char* tchars;
+    int n_int, backlog;
+};
+
+__device__ __forceinline__ uint64_t dev_fnv_dec(uint64_t h, uint32_t v) {
+    char d[12];
+    int n = 0;
+    do {
+        d[n++] = (char)('0' + v % 10u);
+        v /= 10u;
+    } while (v);
+    while (n) {
+        h ^= (unsigned char)d[--n];
+        h *= 0x100000001b3ULL;
+    }
+    return h;
+}
+
+__global__ void k_arrival_hash(const HashJob* __restrict__ jobs, int n_jobs, uint64_t* out) {
+    const int u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= n_jobs) return;
+    const HashJob j = jobs[u];
+    uint64_t h = 0xcbf29ce484222325ULL;
+    uint32_t id = 0;
+    auto req = [&](const char* t, uint32_t tn) {
+        h = dev_fnv_dec(h, id);
+        h = (h ^ (unsigned char)':') * 0x100000001b3ULL;
+        h = dev_fnv_dec(h, (uint32_t)j.len[id]);
+        for (uint32_t c = 0; c < tn; ++c) h = (h ^ (unsigned char)t[c]) * 0x100000001b3ULL;
+        ++id;
+    };
+    for (int b = 0; b < j.backlog; ++b) req("@0", 2);
+    for (int k = 0; k < j.n_int; ++k) {
+        const uint32_t end = (uint32_t)j.cum[k];
+        if (id == end) continue;
+        const uint32_t t0 = j.toff[k], tn = j.toff[k + 1] - t0;
+        while (id < end) req(j.tchars + t0, tn);
+    }
+    out[u] = h;
 }
 
 // trace_value (sim.hpp:167-174) for non-decreasing query times: the value of the
@@ -1061,6 +1101,35 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
         o_cum[u] = res.stage_ref(streams[u].cum);
         o_len[u] = res.stage_ref(streams[u].len);
     }
+    // "@" + fmt_num(k * interval) per interval of every distinct grid (the arrival hash's
+    // request suffixes, sim.hpp:344; csvio.hpp:17-21)
+    std::map<std::pair<double, int>, int> grid_of;
+    std::vector<std::vector<char>> g_chars;
+    std::vector<std::vector<uint32_t>> g_off;
+    std::vector<int> stream_grid(streams.size());
+    for (size_t u = 0; u < streams.size(); ++u) {
+        const pals_scenario& sc = scens[work[u].first];
+        const int ni = n_int[work[u].first];
+        auto it = grid_of.find({sc.interval_s, ni});
+        if (it == grid_of.end()) {
+            it = grid_of.emplace(std::make_pair(sc.interval_s, ni), (int)g_chars.size()).first;
+            std::vector<char> ch;
+            std::vector<uint32_t> off{0};
+            for (int k = 0; k < ni; ++k) {
+                const std::string t = "@" + fmt10g(k * sc.interval_s);
+                ch.insert(ch.end(), t.begin(), t.end());
+                off.push_back((uint32_t)ch.size());
+            }
+            g_chars.push_back(std::move(ch));
+            g_off.push_back(std::move(off));
+        }
+        stream_grid[u] = it->second;
+    }
+    std::vector<size_t> o_gch(g_chars.size()), o_goff(g_chars.size());
+    for (size_t g = 0; g < g_chars.size(); ++g) {
+        o_gch[g] = res.stage(g_chars[g]);
+        o_goff[g] = res.stage(g_off[g]);
+    }
     phase("streams");
     // device buffers: stage every array, one upload, then point the descriptors at it
     std::vector<SimScenDev> hs(n_scen);
@@ -1135,6 +1204,50 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
             }
         }
     }
+    // the arrival hashes, on a side stream beside k_sim
+    std::vector<HashJob> jobs(streams.size());
+    for (size_t u = 0; u < streams.size(); ++u) {
+        HashJob& j = jobs[u];
+        j.len = res.at<int32_t>(o_len[u]);
+        j.cum = res.at<int32_t>(o_cum[u]);
+        j.toff = res.at<uint32_t>(o_goff[stream_grid[u]]);
+        j.tchars = res.at<char>(o_gch[stream_grid[u]]);
+        j.n_int = n_int[work[u].first];
+        j.backlog = scens[work[u].first].nodes[work[u].second].initial_backlog;
+    }
+    HashJob* d_jobs = nullptr;
+    uint64_t* d_hash = nullptr;
+    {
+        int r = res.upload(&d_jobs, jobs);
+        if (r) return r;
+        r = res.alloc(&d_hash, jobs.size());
+        if (r) return r;
+    }
+    cudaStream_t hs_stream = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_hash = nullptr;
+    PALS_CUDA(cudaStreamCreateWithFlags(&hs_stream, cudaStreamNonBlocking));
+    struct StreamGuard {
+        cudaStream_t& s;
+        cudaEvent_t& a;
+        cudaEvent_t& b;
+        ~StreamGuard() {
+            if (s) cudaStreamSynchronize(s), cudaStreamDestroy(s);
+            if (a) cudaEventDestroy(a);
+            if (b) cudaEventDestroy(b);
+        }
+    } hs_guard{hs_stream, ev_fork, ev_hash};
+    PALS_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    PALS_CUDA(cudaEventCreateWithFlags(&ev_hash, cudaEventDisableTiming));
+    PALS_CUDA(cudaEventRecord(ev_fork, ctx->stream));
+    PALS_CUDA(cudaStreamWaitEvent(hs_stream, ev_fork, 0));
+    if (!jobs.empty()) {
+        k_arrival_hash<<<(unsigned)((jobs.size() + 63) / 64), 64, 0, hs_stream>>>(
+            d_jobs, (int)jobs.size(), d_hash);
+        count_launch(ctx);
+        const cudaError_t he = cudaGetLastError();
+        if (he != cudaSuccess) return cuda_fail(he, "k_arrival_hash");
+    }
+    PALS_CUDA(cudaEventRecord(ev_hash, hs_stream));
     SimArgs A;
     memset(&A, 0, sizeof A);
     // CTA order: most node-intervals first, so the long scenarios do not form the tail
@@ -1203,8 +1316,13 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
         e = copy_on(ctx->stream, decisions, A.dec, sizeof(pals_sim_decision) * nlog,
                     cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cuda_fail(e, "pals_run_scenarios");
+    std::vector<uint64_t> hashes(jobs.size());
+    e = cudaStreamWaitEvent(ctx->stream, ev_hash, 0);
+    if (e == cudaSuccess && !jobs.empty())
+        e = copy_on(ctx->stream, hashes.data(), d_hash, 8 * jobs.size(), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "pals_run_scenarios: arrival hashes");
     for (int64_t gi = 0; gi < total_nodes; ++gi)
-        node_results[gi].arrival_stream_hash = streams[node_stream[gi]].hash;
+        node_results[gi].arrival_stream_hash = hashes[node_stream[gi]];
     // RequestRec per request (sim.hpp:100-107), kept on the context for pals_sim_requests
     ctx->sim_requests.clear();
     if (keep_req) {

@@ -12,4 +12,6 @@ sys.argv = ["bench.py", "--sim-seeds", str(seeds)]
 args = bench.parse()
 d = bench.Dist()
 ctx = Context(0)
-print(json.dumps(bench.bench_sim(args, d, ctx)))
+r = bench.bench_sim(args, d, ctx)
+r = r[0] if isinstance(r, tuple) else r
+print(json.dumps(r, default=lambda o: o.tolist() if hasattr(o, "tolist") else str(o)))

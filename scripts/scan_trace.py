@@ -42,3 +42,6 @@ for k in range(1, 15):
     prev = rows[:, k - 1]
     d = (rows[m, k] - prev[m]) / 1e3
     print(f"mark {k:2d} (n={m.sum():4d}) dt min/med/max us", np.percentile(d, [0, 50, 100]).round(2))
+out = os.path.join(os.environ.get("GRAFT_REPO_ROOT", "."), "gpurun_out")
+if os.path.isdir(out):
+    np.save(os.path.join(out, f"scan_trace_{which}.npy"), rows - t0)

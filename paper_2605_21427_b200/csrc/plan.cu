@@ -24,9 +24,10 @@ constexpr int kScanCh = 2048;       // configs per scan work item
 constexpr int kScanThreads = 256;
 constexpr int kScanQ = 8;           // queries per thread in the scan (register tile)
 constexpr int kMaxChunks = 8;       // pals_select: query chunks pipelined behind their upload
-constexpr int kCountStride = 8;     // class counters per chunk (N_CLS + 1 used)
+constexpr int kCountStride = 16;    // per query chunk: [0, N_CLS) class sizes, [N_CLS] exact
+                                    // folds, [6] qprep blocks done, [8, 16) the scan plan
+constexpr int kCntDone = 6, kCntPlan = 8;
 constexpr int kCountInts = kMaxChunks * kCountStride;
-constexpr int kScanTQ = kScanThreads * kScanQ;
 
 enum { CLS_A = 0, CLS_B = 1, CLS_C = 2, CLS_D = 3, CLS_X = 4, N_CLS = 5 };
 enum { EX_FULL = 0, EX_QOS_NEAR = 1, EX_BUD_NEAR = 2 };
@@ -814,6 +815,7 @@ struct SelArgs {
     int32_t* counts;  // [0..N_CLS) class sizes, [N_CLS] work items
     int64_t qcap;
     int force_exact;
+    int scan_grid;    // k_scan's CTAs (the last qprep block partitions the scan over them)
 };
 
 // (7) per-query thresholds in competition-rank space and the query class.
@@ -841,6 +843,66 @@ __device__ __forceinline__ int64_t count_prefix(const uint64_t* m, int o, int64_
         else b = mid;
     }
     return a;
+}
+
+// ---- pair-scan partition ----------------------------------------------
+// The work of class c is T_c query tiles x the grid's n configs, laid end to end as config
+// positions; a k_scan CTA walks its position range in segments cut at tile and chunk
+// boundaries, and every segment pays a fixed phase (loads, barrier, the chunk's bucket
+// index, thresholds) before its pairs.
+//  * Cell mode (few cells: a cfg2-sized step, tiles x chunks <= CTAs). Every CTA gets
+//    exactly one part of one (class, tile, chunk) cell, so no CTA pays the fixed phase twice
+//    (stream-K cut ~40 % of cfg2's CTAs across a chunk or tile boundary, and those CTAs set
+//    the kernel's end). The tile size (NQ <= 8 query slots per thread) and the parts per
+//    chunk P minimise the largest unit: class A / C cells are cut into P parts, class B
+//    cells (4 ops per pair) into 2P; a smaller NQ must win by 2 %.
+//  * Stream-K otherwise: positions weighted by the class's ops per pair (A 2, B 4, C 2),
+//    each CTA an equal contiguous share of the weight.
+// The last qprep block writes the plan {NQ (0: stream-K), P, T_A, T_B, T_C, tq_A, tq_B, tq_C}
+// to counts[kCntPlan..]; 32-bit arithmetic (class counts < 2^31, n < 2^32).
+__device__ __forceinline__ uint32_t cdiv32(uint32_t a, uint32_t b) { return (a + b - 1) / b; }
+__device__ __forceinline__ void scan_plan_warp(int32_t* counts, uint32_t n, uint32_t L,
+                                               uint32_t G) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t c0 = *(volatile int32_t*)&counts[0], c1 = *(volatile int32_t*)&counts[1],
+                   c2 = *(volatile int32_t*)&counts[2];
+    const uint32_t nch = cdiv32(n, L);
+    // lane i evaluates NQ = 8 - i
+    const int nq = kScanQ - lane;
+    uint32_t P = 0, u = 0;
+    if (lane < kScanQ - 2) {
+        const uint32_t tqm = (uint32_t)kScanThreads * nq;
+        const uint32_t t0 = cdiv32(c0, tqm), t1 = cdiv32(c1, tqm), t2 = cdiv32(c2, tqm);
+        const uint32_t S = (t0 + 2 * t1 + t2) * nch;  // cells, class B counted twice
+        if (S > 0 && S <= G && nch <= G) {
+            P = G / S;
+            // per-thread slot-configs of a class's largest unit (class B: twice the ops per
+            // pair over half the configs)
+            auto unit = [=](uint32_t cnt, uint32_t t, uint32_t h) {
+                return t ? cdiv32(cdiv32(cnt, t), kScanThreads) * cdiv32(L, P * h) * h : 0u;
+            };
+            u = max(max(unit(c0, t0, 1), unit(c1, t1, 2)), unit(c2, t2, 1));
+        }
+    }
+    int bnq = 0;
+    uint32_t bP = 0, bu = 0;
+    for (int i = 0; i < kScanQ - 2; ++i) {
+        const uint32_t Pi = __shfl_sync(0xffffffffu, P, i), ui = __shfl_sync(0xffffffffu, u, i);
+        if (Pi && (bnq == 0 || (uint64_t)ui * 50 < (uint64_t)bu * 49)) {
+            bnq = kScanQ - i;
+            bP = Pi;
+            bu = ui;
+        }
+    }
+    if (lane == 0) {
+        const uint32_t tqm = (uint32_t)kScanThreads * (bnq ? bnq : kScanQ);
+        const uint32_t T0 = cdiv32(c0, tqm), T1 = cdiv32(c1, tqm), T2 = cdiv32(c2, tqm);
+        int4 h = make_int4(bnq, (int)bP, (int)T0, (int)T1);
+        int4 t = make_int4((int)T2, T0 ? (int)cdiv32(c0, T0) : 0, T1 ? (int)cdiv32(c1, T1) : 0,
+                           T2 ? (int)cdiv32(c2, T2) : 0);
+        *reinterpret_cast<int4*>(counts + kCntPlan) = h;
+        *reinterpret_cast<int4*>(counts + kCntPlan + 4) = t;
+    }
 }
 
 __device__ __forceinline__ void qprep_body(const PlanDev& d, const SelArgs& a, int bx, int nbx,
@@ -914,6 +976,19 @@ __device__ __forceinline__ void qprep_body(const PlanDev& d, const SelArgs& a, i
                 a.qthr[slot] = make_uint2((uint32_t)a.thr_t[j], (uint32_t)a.thr_p[j]);
             }
         }
+    }
+    // the last qprep block sees the final class sizes and partitions the pair scan once
+    // for every k_scan CTA (a per-CTA search sat on each CTA's critical path)
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&a.counts[kCntDone], 1) == nbx - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x < 32) {
+        __threadfence();
+        scan_plan_warp(a.counts, (uint32_t)d.n, (uint32_t)d.lch, (uint32_t)a.scan_grid);
     }
 }
 
@@ -1022,26 +1097,49 @@ __device__ __forceinline__ void scan_seg2(const uint4* __restrict__ w, int nw,
     }
 }
 
-// Stream-K partition of the pair scan: the work of every (class, query tile) is
-// laid end to end in units of one config (weighted by the class's ops per pair:
-// A 2, B 4, C 2) and each CTA takes an equal contiguous share, so every SM gets
-// the same number of integer ops whatever the query count.
+// the pair scan's partition (scan_plan_warp): this CTA's [p0, p1) of config positions
 struct ScanPlan {
-    int64_t T[3];     // tiles per class
-    int64_t tq[3];    // queries per tile (balanced, <= TQ)
-    int64_t wbase[4]; // cumulative weight at each class start
-    int64_t pbase[4]; // cumulative config position at each class start
+    int tq0, tq1, tq2;  // queries per tile of each class (balanced, <= NQ x 256)
+    int64_t pb1, pb2;   // config position where classes B and C start (A at 0)
 };
 
-__device__ __forceinline__ int class_ops(int c) { return c == CLS_B ? 4 : 2; }
-
-__device__ __forceinline__ int64_t scan_pos_of(const ScanPlan& sp, int64_t u) {
-    // register selects over the three classes (an indexed form went to the local stack)
-    if (u >= sp.wbase[3]) return sp.pbase[3];
-    const int c = (u >= sp.wbase[1]) + (u >= sp.wbase[2]);
-    const int64_t wb = c == 0 ? sp.wbase[0] : c == 1 ? sp.wbase[1] : sp.wbase[2];
-    const int64_t pb = c == 0 ? sp.pbase[0] : c == 1 ? sp.pbase[1] : sp.pbase[2];
-    return pb + (u - wb) / class_ops(c);
+__device__ __forceinline__ void scan_partition(const int32_t* __restrict__ counts, int64_t n, int L,
+                                               int b, int G, ScanPlan& pl, int64_t& p0,
+                                               int64_t& p1) {
+    const int4 h = __ldg(reinterpret_cast<const int4*>(counts + kCntPlan));
+    const int4 t = __ldg(reinterpret_cast<const int4*>(counts + kCntPlan + 4));
+    const int bnq = h.x, bP = h.y;
+    const uint32_t T0 = h.z, T1 = h.w, T2 = t.x;
+    pl.tq0 = t.y;
+    pl.tq1 = t.z;
+    pl.tq2 = t.w;
+    const int64_t pb1 = (int64_t)T0 * n, pb2 = pb1 + (int64_t)T1 * n, pb3 = pb2 + (int64_t)T2 * n;
+    pl.pb1 = pb1;
+    pl.pb2 = pb2;
+    if (bnq) {  // cell mode: cells x parts <= G, 32-bit throughout
+        const uint32_t nch = cdiv32((uint32_t)n, (uint32_t)L);
+        const uint32_t u1 = T0 * nch * bP, u2 = u1 + T1 * nch * 2 * bP, u3 = u2 + T2 * nch * bP;
+        p0 = p1 = 0;
+        if ((uint32_t)b >= u3) return;
+        const int c = ((uint32_t)b >= u1) + ((uint32_t)b >= u2);
+        const uint32_t Pc = c == CLS_B ? 2 * bP : bP;
+        const uint32_t r = (uint32_t)b - (c == 0 ? 0u : c == 1 ? u1 : u2);
+        const uint32_t cell = r / Pc, part = r - cell * Pc;
+        const uint32_t tile = cell / nch, ch = cell - tile * nch;
+        const uint32_t len = min((uint32_t)L, (uint32_t)n - ch * L);
+        const int64_t base = (c == 0 ? 0 : c == 1 ? pb1 : pb2) + (int64_t)tile * n + ch * L;
+        p0 = base + len * part / Pc;
+        p1 = base + len * (part + 1) / Pc;
+        return;
+    }
+    const int64_t w1 = (int64_t)T0 * n * 2, w2 = w1 + (int64_t)T1 * n * 4,
+                  W = w2 + (int64_t)T2 * n * 2;
+    auto pos_of = [=](int64_t u) {
+        if (u >= W) return pb3;
+        return u >= w2 ? pb2 + (u - w2) / 2 : u >= w1 ? pb1 + (u - w1) / 4 : u / 2;
+    };
+    p0 = pos_of(W * b / G);
+    p1 = pos_of(W * (b + 1) / G);
 }
 
 // Bucket index over a chunk's staged run positions (ascending): T[b] = number of places
@@ -1111,13 +1209,21 @@ __device__ unsigned long long g_scan_trace[4096][16];
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
         g_scan_trace[blockIdx.x][k] = t_;                                                 \
     }
+#define SCAN_SMID()                                                                       \
+    if (threadIdx.x == 0 && blockIdx.x < 4096) {                                          \
+        unsigned s_;                                                                      \
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(s_));                                   \
+        g_scan_trace[blockIdx.x][14] = s_;                                                \
+    }
 #else
 #define SCAN_MARK(k)
+#define SCAN_SMID()
 #endif
 
 __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) {
     pdl_wait();
     SCAN_MARK(0);
+    SCAN_SMID();
     int mark = 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint4* sw = reinterpret_cast<uint4*>(smem_raw);
@@ -1129,37 +1235,31 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) 
     const int sh = max(0, 32 - __clz((int)(n - 1)) - 10);  // <= 1,024 buckets of 2^sh positions
     const int nb = (int)((n - 1) >> sh) + 1;
     ScanPlan pl;
-    pl.wbase[0] = pl.pbase[0] = 0;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        const int64_t cnt = a.counts[c];
-        pl.T[c] = (cnt + kScanTQ - 1) / kScanTQ;
-        pl.tq[c] = pl.T[c] ? (cnt + pl.T[c] - 1) / pl.T[c] : 0;
-        pl.pbase[c + 1] = pl.pbase[c] + pl.T[c] * n;
-        pl.wbase[c + 1] = pl.wbase[c] + pl.T[c] * n * class_ops(c);
-    }
-    const int64_t W = pl.wbase[3];
-    const int64_t p0 = scan_pos_of(pl, W * blockIdx.x / gridDim.x);
-    const int64_t p1 = scan_pos_of(pl, W * (blockIdx.x + 1) / gridDim.x);
+    int64_t p0, p1;
+    scan_partition(a.counts, n, L, blockIdx.x, gridDim.x, pl, p0, p1);
     int64_t pos = p0;
     while (pos < p1) {
         // locate (class, tile, first config) of pos and the end of that tile segment;
         // configs are TR positions, cut further at the chunks of the local ranks
         // (register selects, not indexed loads: the plan stays in registers, no local stack)
-        const int c = (pos >= pl.pbase[1]) + (pos >= pl.pbase[2]);
-        const int64_t pb = c == 0 ? pl.pbase[0] : c == 1 ? pl.pbase[1] : pl.pbase[2];
-        const int64_t tqc = c == 0 ? pl.tq[0] : c == 1 ? pl.tq[1] : pl.tq[2];
+        const int c = (pos >= pl.pb1) + (pos >= pl.pb2);
+        const int64_t pb = c == 0 ? 0 : c == 1 ? pl.pb1 : pl.pb2;
+        const int64_t tqc = c == 0 ? pl.tq0 : c == 1 ? pl.tq1 : pl.tq2;
         const int64_t r = pos - pb;
-        const int64_t tile = r / n;
+        // 32-bit divisions where the operands fit (j0 < n < 2^32)
+        const int64_t tile = (r >> 32) ? r / n : (int64_t)((uint32_t)r / (uint32_t)n);
         const int64_t j0 = r - tile * n;
-        const int64_t chunk_end = (j0 / L + 1) * L;
+        const int64_t cb = (int64_t)(((uint32_t)j0 / (uint32_t)L) * (uint32_t)L);  // chunk's first TR
+        const int64_t chunk_end = cb + L;
         const int64_t seg_end = min(min(p1, pb + (tile + 1) * n), pos + (chunk_end - j0));
         const int64_t j1 = j0 + (seg_end - pos);
-        const int64_t cb = (j0 / L) * L;  // the chunk's first TR
         // this tile's queries: 8 per thread (slot validity needs no load)
         const int64_t q_lo = tile * tqc, q_hi = min((int64_t)a.counts[c], q_lo + tqc);
-        const bool full_slots =
-            __any_sync(0xffffffffu, q_lo + (kScanQ - 1) * kScanThreads + threadIdx.x < q_hi);
+        // query slots of this warp that hold a query (warp-uniform): the loop is instantiated
+        // per count, so empty slots cost no ALU work
+        const int qlen = (int)(q_hi - q_lo), wbase = (int)(threadIdx.x & ~31u);
+        const int nqw =
+            qlen > wbase ? min(kScanQ, (qlen - wbase + kScanThreads - 1) / kScanThreads) : 0;
         const int64_t w0 = j0 >> 1, w1 = (j1 + 1) >> 1;  // config pairs
         const int nw = (int)(w1 - w0);
         __syncthreads();  // the previous segment is done with shared memory
@@ -1246,11 +1346,31 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) 
         SCAN_MARK(mark);
         ++mark;
         if (c == CLS_B) {
-            scan_seg2<kScanQ>(sw, nw + (nw & 1), K1, K2, m1, m2);
+            const int nw2 = nw + (nw & 1);
+            switch (nqw) {
+                case 8: scan_seg2<8>(sw, nw2, K1, K2, m1, m2); break;
+                case 7: scan_seg2<7>(sw, nw2, K1, K2, m1, m2); break;
+                case 6: scan_seg2<6>(sw, nw2, K1, K2, m1, m2); break;
+                case 5: scan_seg2<5>(sw, nw2, K1, K2, m1, m2); break;
+                case 4: scan_seg2<4>(sw, nw2, K1, K2, m1, m2); break;
+                case 3: scan_seg2<3>(sw, nw2, K1, K2, m1, m2); break;
+                case 2: scan_seg2<2>(sw, nw2, K1, K2, m1, m2); break;
+                case 1: scan_seg2<1>(sw, nw2, K1, K2, m1, m2); break;
+                default: break;
+            }
         } else {
             const int nw4 = (nw + 1) >> 1;
-            if (full_slots) scan_seg1<kScanQ>(sw, nw4, K1, m1);
-            else scan_seg1<kScanQ - 1>(sw, nw4, K1, m1);
+            switch (nqw) {
+                case 8: scan_seg1<8>(sw, nw4, K1, m1); break;
+                case 7: scan_seg1<7>(sw, nw4, K1, m1); break;
+                case 6: scan_seg1<6>(sw, nw4, K1, m1); break;
+                case 5: scan_seg1<5>(sw, nw4, K1, m1); break;
+                case 4: scan_seg1<4>(sw, nw4, K1, m1); break;
+                case 3: scan_seg1<3>(sw, nw4, K1, m1); break;
+                case 2: scan_seg1<2>(sw, nw4, K1, m1); break;
+                case 1: scan_seg1<1>(sw, nw4, K1, m1); break;
+                default: break;
+            }
         }
         SCAN_MARK(mark);
         ++mark;
@@ -1908,6 +2028,13 @@ static int ensure_query_buffers(pals_plan* p, int64_t nq) {
     return PALS_OK;
 }
 
+// k_scan's grid: 4 CTAs of 256 threads per SM (the partition, scan_plan_warp, adapts the
+// query tiles and config parts to it)
+#ifndef PALS_SCAN_CPS
+#define PALS_SCAN_CPS 4
+#endif
+static int scan_grid(const pals_plan* p, int64_t) { return p->ctx->num_sms * PALS_SCAN_CPS; }
+
 static SelArgs make_args(pals_plan* p, const pals_query* d_queries, int64_t nq, int32_t* d_idx,
                          uint8_t* d_reason) {
     SelArgs a;
@@ -1925,6 +2052,7 @@ static SelArgs make_args(pals_plan* p, const pals_query* d_queries, int64_t nq, 
     a.counts = p->counts;
     a.qcap = p->qcap;
     a.force_exact = p->force_exact;
+    a.scan_grid = scan_grid(p, nq);
     return a;
 }
 
@@ -1997,13 +2125,7 @@ static int dec_layout(pals_plan* p, DecDev* t) {
 static int select_tail(pals_plan* p, const SelArgs& a, bool build = true) {
     pals_ctx* ctx = p->ctx;
     cudaStream_t s = ctx->stream;
-    // stream-K scan grid: 4 CTAs per SM, 3 when the step scans under ~1e10 pairs (each
-    // CTA's fixed cost per chunk segment — staging, local thresholds — is then a larger
-    // share: cfg2 55 vs 59 us; cfg3 5.47 vs 5.55 ms the other way)
-#ifndef PALS_SCAN_CPS_SMALL
-#define PALS_SCAN_CPS_SMALL 3
-#endif
-    const int sgrid = ctx->num_sms * ((double)a.nq * (double)p->n < 1e10 ? PALS_SCAN_CPS_SMALL : 4);
+    const int sgrid = a.scan_grid;
     // event-record nodes around the scan (timing) are not kernels: plain edges there
     const bool pdl = p->pdl && !p->time_scan;
     // inside a stream capture the events become graph event-record nodes

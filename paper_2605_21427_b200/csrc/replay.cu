@@ -44,6 +44,7 @@ struct ReplayParams {
     double alpha, beta;
     int n_models;
     TraceArgs tr;
+    uint64_t seg_mul;  // floor((2^64 - 1) / span), span = seg_max - seg_min + 1 (seg_mod)
 };
 
 // ---- counter-based trace generator --------------------------
@@ -63,15 +64,28 @@ __device__ __forceinline__ double noise_of(double amp, uint32_t u) {
 // Piecewise-constant trace lane: only the segment cursor and level live in
 // registers; the level bounds (lo, hi) are recomputed from the model when a new
 // segment starts (same expressions, same doubles) — fewer live registers per trace.
+// x % span for the segment-length draw with a precomputed reciprocal (mul = floor((2^64 - 1) /
+// span)): the quotient estimate is at most 2 below the true one, so at most two corrections
+// give the exact remainder. The 64-bit '%' is a ~60-instruction call, and a segment event of
+// any lane holds the whole warp (divergence): it ran on ~60 % of warp steps.
+__device__ __forceinline__ uint64_t seg_mod(uint64_t x, uint64_t span, uint64_t mul) {
+    uint64_t r = x - __umul64hi(x, mul) * span;
+    if (r >= span) r -= span;
+    if (r >= span) r -= span;
+    return r;
+}
+
 struct Seg {
     int next_j, seg_end;
     double level;
     __device__ __forceinline__ double at(int k, uint64_t key, uint64_t lane, int seg_min,
-                                         int seg_max, double lo_frac, const double& lo_of,
-                                         double hi_frac, const double& hi_of) {
+                                         int seg_max, uint64_t seg_mul, double lo_frac,
+                                         const double& lo_of, double hi_frac,
+                                         const double& hi_of) {
         while (k >= seg_end) {
             const uint64_t span = (uint64_t)(seg_max - seg_min) + 1;
-            const long len = seg_min + (long)(draw(key, lane, 2 * (uint64_t)next_j) % span);
+            const long len =
+                seg_min + (long)seg_mod(draw(key, lane, 2 * (uint64_t)next_j), span, seg_mul);
             const double u = u01(draw(key, lane, 2 * (uint64_t)next_j + 1));
             const double lo = lo_frac * lo_of, hi = hi_frac * hi_of;
             level = lo + (hi - lo) * u;
@@ -360,7 +374,8 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
                 if (has_bsig) node_budget = bsig.at(k, sp.n_steps, p.tr.first_step, sp.interval_s);
             } else {
                 if (sp.budget_mode)
-                    node_budget = bs.at(k, key, 1, sp.seg_min, sp.seg_max, sp.budget_lo_frac,
+                    node_budget = bs.at(k, key, 1, sp.seg_min, sp.seg_max, p.seg_mul,
+                                        sp.budget_lo_frac,
                                         m.p_min, sp.budget_hi_frac, m.p_max);
             }
             // b_eff = batch_cap (fluid plant: the queue always covers the batch cap)
@@ -404,7 +419,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_replay(const ReplayModelDev
             }
             double offered, noise;
             if constexpr (kTr) offered = lsig.at(k, sp.n_steps, p.tr.first_step, sp.interval_s);
-            else offered = ls.at(k, key, 2, sp.seg_min, sp.seg_max, sp.load_lo, m.t_max,
+            else offered = ls.at(k, key, 2, sp.seg_min, sp.seg_max, p.seg_mul, sp.load_lo, m.t_max,
                                  sp.load_hi, m.t_max);
             if (kWarp) {  // lanes draw the noise of 32 steps per round
                 if ((k & 31) == 0 && k + lane < sp.n_steps)
@@ -890,6 +905,7 @@ static int replay_launch(pals_ctx* ctx, ReplayCache* rc, const pals_ctrl_cfg* cf
     memset(&p, 0, sizeof p);
     p.spec = *spec;
     p.cfg = *cfg;
+    p.seg_mul = ~0ull / ((uint64_t)(spec->seg_max - spec->seg_min) + 1);
     p.alpha = rc->coeffs.alpha;
     p.beta = rc->coeffs.beta_watts;
     p.n_models = (int)rc->models.size();

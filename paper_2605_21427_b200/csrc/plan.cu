@@ -47,9 +47,6 @@ struct pals_plan {
     int64_t n = 0, np = 0;
     int nchunks = 0;
     int chunk = 4096;  // sort chunk size (keys per CTA)
-    int merge_tile = 1024;  // output keys per CTA of a merge round
-    int sort_ipt = 4;       // keys per thread of a 2,048-key chunk sort (PALS_SORT_IPT 2/4/8)
-    int merge_ipt = 4;      // keys per thread of a 1,024-key merge tile (PALS_MERGE_IPT 2/4/8)
     int force_exact = 0;
     int values = 0;               // internal: th / ef supplied directly (frontier.cu)
     int pdl = 1;                  // programmatic dependent launch between step kernels
@@ -1764,11 +1761,7 @@ static int plan_build(pals_ctx* ctx, const pals_model* m, const pals_grid* g,
     // chunks); small grids (cfg1's 36 candidates, a replay's candidate sets) sort in one
     // chunk just large enough. The pair scan's chunk-local ranks need chunks <= 2,048.
     p->chunk = n <= 256 ? 256 : n <= 512 ? 512 : n <= 1024 ? 1024 : kChunk;
-    p->sort_ipt = 4;
-    // 2 keys x 512 threads per 1,024-key merge tile (7.0 us per round against 8.5 us for
-    // 8 x 128 and 7.4 us for 4 x 256); PDL edges between the step's kernels
-    p->merge_ipt = 2;
-    p->merge_tile = 1024;
+    // PDL edges between the step's kernels
     p->pdl = 1;
     p->nchunks = (int)((n + p->chunk - 1) / p->chunk);
     p->np = (int64_t)p->nchunks * p->chunk;
@@ -1930,15 +1923,9 @@ static int prep_head(pals_plan* p, int32_t* counts_reset = nullptr) {
     while (((int64_t)p->chunk << rounds) < p->np) ++rounds;
     const int sort_to_merged = rounds % 2 == 0;
     const int sort_final = rounds == 0;
-    if (p->sort_ipt == 2 && p->chunk == 2048)  // 2 keys per thread, 1,024 threads
-        e = launch_k(k_sort_chunks<1024, 2>, gs, 1024, sort_smem_bytes(1024, 2), s, pdl, d,
-                     p->gk, done, counts_reset, sort_to_merged, sort_final);
-    else if (p->sort_ipt == 4 && p->chunk == 2048)  // 4 keys per thread, 512 threads
+    if (p->chunk == 2048)  // 4 keys x 512 threads (8 x 256 and 2 x 1,024 measured slower)
         e = launch_k(k_sort_chunks<512, 4>, gs, 512, sort_smem_bytes(512, 4), s, pdl, d, p->gk,
                      done, counts_reset, sort_to_merged, sort_final);
-    else if (p->sort_ipt == 4 && p->chunk == 4096)  // 4 keys per thread, 1,024 threads
-        e = launch_k(k_sort_chunks<1024, 4>, gs, 1024, sort_smem_bytes(1024, 4), s, pdl, d,
-                     p->gk, done, counts_reset, sort_to_merged, sort_final);
     else switch (p->chunk) {
 #define PALS_SORT(TPB)                                                                         \
     case TPB * kIPT:                                                                           \
@@ -1961,21 +1948,10 @@ static int prep_head(pals_plan* p, int32_t* counts_reset = nullptr) {
     while ((1 << lg) < p->chunk) ++lg;
     for (int k = 0; k < rounds && e == cudaSuccess; ++k) {
         const int to_m = (rounds - k) % 2 == 1, fin = k == rounds - 1;
-        if (p->merge_tile == 1024 && p->merge_ipt == 1)
-            e = launch_k(k_merge_round<1024, 1>, dim3((unsigned)((p->np + 1023) / 1024), N_ORD),
-                         1024, 0, s, pdl, d, (uint32_t)p->np, lg + k, to_m, fin);
-        else if (p->merge_tile == 1024 && p->merge_ipt == 2)
-            e = launch_k(k_merge_round<512, 2>, dim3((unsigned)((p->np + 1023) / 1024), N_ORD),
-                         512, 0, s, pdl, d, (uint32_t)p->np, lg + k, to_m, fin);
-        else if (p->merge_tile == 1024 && p->merge_ipt == 4)
-            e = launch_k(k_merge_round<256, 4>, dim3((unsigned)((p->np + 1023) / 1024), N_ORD),
-                         256, 0, s, pdl, d, (uint32_t)p->np, lg + k, to_m, fin);
-        else if (p->merge_tile == 1024)
-            e = launch_k(k_merge_round<128>, dim3((unsigned)((p->np + 1023) / 1024), N_ORD), 128, 0, s,
-                         pdl, d, (uint32_t)p->np, lg + k, to_m, fin);
-        else
-            e = launch_k(k_merge_round<256>, dim3((unsigned)((p->np + 2047) / 2048), N_ORD), 256, 0, s,
-                         pdl, d, (uint32_t)p->np, lg + k, to_m, fin);
+        // 2 keys x 512 threads per 1,024-key merge tile (7.0 us per round against 8.5 us for
+        // 8 x 128 and 7.4 us for 4 x 256)
+        e = launch_k(k_merge_round<512, 2>, dim3((unsigned)((p->np + 1023) / 1024), N_ORD), 512,
+                     0, s, pdl, d, (uint32_t)p->np, lg + k, to_m, fin);
     }
     if (e != cudaSuccess) return cuda_fail(e, "pals_plan_prepare");
     count_launch(ctx, 2 + rounds);  // eval, sort, merge rounds

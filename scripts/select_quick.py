@@ -25,7 +25,9 @@ q = (workloads.gen_queries(nq, 2605, float(th.max()), "qos") if which == "cfg2" 
 d_q = torch.from_numpy(q.view(np.uint8).copy()).cuda()
 d_i = torch.empty(nq, dtype=torch.int32, device="cuda")
 d_r = torch.empty(nq, dtype=torch.uint8, device="cuda")
-plan.time_scan(True)
+# "graph": time the captured step with its PDL edges (no scan events in the graph)
+graph_only = len(sys.argv) > 4 and sys.argv[4] == "graph"
+plan.time_scan(not graph_only)
 run = lambda: plan.run(d_q.data_ptr(), nq, d_i.data_ptr(), d_r.data_ptr())  # noqa: E731
 for _ in range(3):
     run()
@@ -40,7 +42,7 @@ for _ in range(reps):
     e1.record(stream)
     torch.cuda.synchronize()
     step.append(e0.elapsed_time(e1))
-    scan.append(plan.scan_ms())
+    scan.append(plan.scan_ms() if not graph_only else float("nan"))
 ms = float(np.median(scan))
 print(f"{which}: pairs {pairs:.4g}  scan {ms * 1e3:.1f} us ({pairs / (ms * 1e-3):.4g} pairs/s)  "
       f"step {np.median(step) * 1e3:.1f} us ({pairs / (np.median(step) * 1e-3):.4g} pairs/s)")

@@ -126,6 +126,7 @@ int pals_ctx_destroy(pals_ctx* c) {
     if (c->d_scratch) cudaFree(c->d_scratch);
     if (c->d_front) cudaFree(c->d_front);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
+    if (c->d_sim_arena) cudaFree(c->d_sim_arena);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
     return PALS_OK;

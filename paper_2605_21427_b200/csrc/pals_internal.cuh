@@ -227,6 +227,8 @@ struct pals_ctx {
     size_t scratch_bytes = 0;
     void* h_pinned = nullptr;
     size_t pinned_bytes = 0;
+    void* d_sim_arena = nullptr;  // pals_run_scenarios' staged inputs (reused across calls)
+    size_t sim_arena_bytes = 0;
     void* replay_cache = nullptr;  // replay.cu
     void* one_cache = nullptr;     // replay.cu: single-call candidate sets (pals_select_one)
     int replay_layout = 0;         // PALS_REPLAY_THREAD / PALS_REPLAY_WARP

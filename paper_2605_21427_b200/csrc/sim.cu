@@ -664,9 +664,19 @@ struct Resources {
         return off;
     }
     int commit() {
-        int r = alloc(&arena, data_bytes);
-        if (r) return r;
-        r = alloc(&zarena, zero_bytes);
+        // the staged-input arena is kept by the context (a cudaMalloc / cudaFree of a few
+        // hundred MB per call was a visible share of the call's host time)
+        const size_t need = std::max<size_t>(1, data_bytes);
+        if (ctx->sim_arena_bytes < need) {
+            if (ctx->d_sim_arena) cudaFree(ctx->d_sim_arena);
+            ctx->d_sim_arena = nullptr;
+            ctx->sim_arena_bytes = 0;
+            const cudaError_t e = cudaMalloc(&ctx->d_sim_arena, need);
+            if (e != cudaSuccess) return cuda_fail(e, "pals_run_scenarios: cudaMalloc");
+            ctx->sim_arena_bytes = need;
+        }
+        arena = (char*)ctx->d_sim_arena;
+        int r = alloc(&zarena, zero_bytes);
         if (r) return r;
         cudaStream_t s = ctx->stream;
         PALS_CUDA(cudaMemsetAsync(zarena, 0, std::max<size_t>(1, zero_bytes), s));
@@ -839,6 +849,7 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
     std::vector<int> node_set(total_nodes), node_init(total_nodes);
     std::vector<const pals_model*> node_scorer(total_nodes);
     std::vector<double> node_target(total_nodes);
+    std::map<std::pair<const pals_model*, std::vector<double>>, std::pair<int, int>> node_memo;
     {
         int64_t gi = 0;
         for (int s = 0; s < n_scen; ++s) {
@@ -858,6 +869,27 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
                     sc.policy == PALS_POLICY_ORACLE || !predictors || !predictors[n.model]
                         ? plant : predictors[n.model];
                 node_scorer[gi] = scorer;
+                // the node's (select set, initial candidate) is a function of the scorer, the
+                // policy, the candidate axes, the parallel degrees and the initial knobs: memoised
+                // on those (a few dozen numbers) instead of the expanded grid (up to 1,464
+                // candidates per node, thousands of nodes per call)
+                std::vector<double> tk;
+                tk.reserve(8 + sc.n_caps + sc.n_batches);
+                tk.push_back((double)sc.policy);
+                tk.push_back((double)n.tp);
+                tk.push_back((double)n.ep);
+                tk.push_back((double)n.dp);
+                tk.push_back(sc.initial_cap_w);
+                tk.push_back((double)sc.initial_batch);
+                tk.push_back((double)sc.n_caps);
+                tk.insert(tk.end(), sc.cand_caps, sc.cand_caps + sc.n_caps);
+                for (int b = 0; b < sc.n_batches; ++b) tk.push_back((double)sc.cand_batches[b]);
+                auto memo = node_memo.find({scorer, tk});
+                if (memo != node_memo.end()) {
+                    node_set[gi] = memo->second.first;
+                    node_init[gi] = memo->second.second;
+                    continue;
+                }
                 std::vector<pals_point> pts = policy_candidates(sc, n);
                 std::vector<std::tuple<double, int, int, int, int>> key;
                 for (auto& p : pts) key.emplace_back(p.cap_watts, p.batch, p.tp, p.ep, p.dp);
@@ -877,6 +909,8 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
                     res.sets.back().pts = pts;
                 }
                 node_set[gi] = it->second;
+                node_memo.emplace(std::make_pair(scorer, std::move(tk)),
+                                  std::make_pair(it->second, init));
             }
         }
     }
@@ -971,7 +1005,10 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
     std::atomic<size_t> next_stream{0};
     std::vector<std::thread> stream_threads;
     {
-        const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(),
+        // one core stays with this thread: it splits the budgets on the GPU meanwhile, and
+        // its CUDA calls lost the CPU to the workers (budget phase 56 ms -> 0.2-0.4 s)
+        const unsigned hc = std::thread::hardware_concurrency();
+        const unsigned nt = std::max(1u, std::min<unsigned>(hc > 1 ? hc - 1 : 1,
                                                             (unsigned)work.size()));
         for (unsigned t = 0; t < nt; ++t)
             stream_threads.emplace_back([&] {

@@ -82,17 +82,36 @@ def bundled_scenarios(path: str = DATA) -> dict:
 class _CScenario:
     """A pals_scenario plus the arrays it points to (kept alive together)."""
 
-    def __init__(self, sc: dict, model_index: dict):
-        self.caps = np.ascontiguousarray(sc["caps"], np.float64)
-        self.batches = np.ascontiguousarray(sc["batches"], np.int32)
-        tr = np.asarray(sc["trace"], np.float64).reshape(-1, 2)
-        self.tt = np.ascontiguousarray(tr[:, 0])
-        self.tw = np.ascontiguousarray(tr[:, 1])
-        self.nodes = (SimNode * len(sc["nodes"]))()
-        for i, n in enumerate(sc["nodes"]):
-            self.nodes[i] = SimNode(model_index[n["model"]], n["tp"], n["ep"], n["dp"],
-                                    n["qos_fraction"], n["arrival_rate_per_s"],
-                                    n["initial_backlog"], 0)
+    def __init__(self, sc: dict, model_index: dict, memo: dict | None = None):
+        # memo: arrays and controller configs shared by the scenarios of one call (a seed
+        # sweep repeats the same candidate axes, traces and controller for every seed)
+        memo = {} if memo is None else memo
+
+        def shared(key, make):
+            v = memo.get(key)
+            if v is None:
+                v = memo[key] = make()
+            return v
+
+        self.caps = shared(("caps", id(sc["caps"])),
+                           lambda: np.ascontiguousarray(sc["caps"], np.float64))
+        self.batches = shared(("batches", id(sc["batches"])),
+                              lambda: np.ascontiguousarray(sc["batches"], np.int32))
+
+        def split_trace():
+            tr = np.asarray(sc["trace"], np.float64).reshape(-1, 2)
+            return np.ascontiguousarray(tr[:, 0]), np.ascontiguousarray(tr[:, 1])
+
+        self.tt, self.tw = shared(("trace", id(sc["trace"])), split_trace)
+        def make_nodes():
+            nodes = (SimNode * len(sc["nodes"]))()
+            for i, n in enumerate(sc["nodes"]):
+                nodes[i] = SimNode(model_index[n["model"]], n["tp"], n["ep"], n["dp"],
+                                   n["qos_fraction"], n["arrival_rate_per_s"],
+                                   n["initial_backlog"], 0)
+            return nodes
+
+        self.nodes = shared(("nodes", id(sc["nodes"])), make_nodes)
         s = Scenario()
         s.duration_s, s.interval_s, s.seed = sc["duration_s"], sc["interval_s"], sc["seed"]
         s.mean_tokens, s.log_sigma = sc["mean_tokens"], sc["log_sigma"]
@@ -103,7 +122,8 @@ class _CScenario:
         s.trace_w = self.tw.ctypes.data if len(self.tw) else None
         s.policy = POLICIES[sc["policy"]]
         s.objective = OBJ_QOS if sc["objective"] == "qos" else OBJ_BUDGET
-        s.controller = default_ctrl_cfg(**sc["controller"])
+        ck = ("ctrl",) + tuple(sorted(sc["controller"].items()))
+        s.controller = shared(ck, lambda: default_ctrl_cfg(**sc["controller"]))
         s.epsilon = sc["epsilon"]
         s.cand_caps = self.caps.ctypes.data
         s.cand_batches = self.batches.ctypes.data
@@ -132,7 +152,8 @@ def run_scenarios(ctx, scenarios, profiles, gpu, coeffs, predictors=None, logs: 
     SIM_NODE_RESULT_DT in scenario/node order; with logs, telemetry / decisions are
     [total_nodes, max_intervals] arrays of SIM_TEL_DT / SIM_DEC_DT."""
     idx = _model_index(profiles)
-    cs = [_CScenario(s, idx) for s in scenarios]
+    memo: dict = {}
+    cs = [_CScenario(s, idx, memo) for s in scenarios]
     arr = (Scenario * len(cs))(*[c.c for c in cs])
     profs = (Profile * len(profiles))(*profiles)
     preds = (C.c_void_p * len(profiles))()

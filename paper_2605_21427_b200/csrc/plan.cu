@@ -66,7 +66,7 @@ struct pals_plan {
     uint64_t* best_t = nullptr;
     uint8_t* cls = nullptr;
     int32_t* qlist = nullptr;     // N_CLS regions of qcap
-    uint2* qthr = nullptr;        // beside qlist: (thr_t, thr_p) per slot
+    uint4* qthr = nullptr;        // beside qlist: (thr_t, thr_p, query id, 0) per slot
     int32_t* counts = nullptr;    // [N_CLS] class sizes, [N_CLS] exact count
     pals_query* d_q = nullptr;    // host-API staging
     int32_t* d_idx = nullptr;
@@ -808,7 +808,7 @@ struct SelArgs {
     uint64_t* best_t;
     uint8_t* cls;
     int32_t* qlist;
-    uint2* qthr;      // beside qlist: the slot's (thr_t, thr_p)
+    uint4* qthr;      // beside qlist: the slot's (thr_t, thr_p, query id, 0)
     int32_t* counts;  // [0..N_CLS) class sizes, [N_CLS] work items
     int64_t qcap;
     int force_exact;
@@ -970,7 +970,8 @@ __device__ __forceinline__ void qprep_body(const PlanDev& d, const SelArgs& a, i
             if (c == k) {
                 const int64_t slot = k * a.qcap + base + __popc(m & ((1u << lane) - 1));
                 a.qlist[slot] = (int32_t)j;
-                a.qthr[slot] = make_uint2((uint32_t)a.thr_t[j], (uint32_t)a.thr_p[j]);
+                a.qthr[slot] =
+                    make_uint4((uint32_t)a.thr_t[j], (uint32_t)a.thr_p[j], (uint32_t)j, 0u);
             }
         }
     }
@@ -1159,6 +1160,44 @@ __device__ __forceinline__ void bucket_mark(const uint32_t* sr, int L, uint16_t*
             T[b + 1] = (uint16_t)(i + 1);
     }
 }
+// Stage the chunk's L run positions (ascending; 0xFFFFFFFF pads the last chunk) into sr and
+// mark each non-empty bucket's last place in T (T zeroed beforehand): T[b + 1] = last + 1.
+// Thread t holds places [t PL, (t + 1) PL), PL = L / 256 (L = 256 .. 2,048).
+__device__ __forceinline__ void stage_marks(const uint32_t* __restrict__ src, int L, uint32_t* sr,
+                                            uint16_t* T, int sh, int nb) {
+    const int PL = L / kScanThreads;
+    const int i0 = threadIdx.x * PL;
+    uint32_t v[8];
+    if (PL == 8) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4*>(src + i0));
+        const uint4 b = __ldg(reinterpret_cast<const uint4*>(src + i0) + 1);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+        v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = k < PL ? __ldg(src + i0 + k) : 0xFFFFFFFFu;
+    }
+    // the position after this thread's last place: the next lane's first (lane 31: a load)
+    uint32_t nx = __shfl_down_sync(0xffffffffu, v[0], 1);
+    if ((threadIdx.x & 31) == 31) nx = i0 + PL < L ? __ldg(src + i0 + PL) : 0xFFFFFFFFu;
+    if (PL == 8) {
+        reinterpret_cast<uint4*>(sr + i0)[0] = make_uint4(v[0], v[1], v[2], v[3]);
+        reinterpret_cast<uint4*>(sr + i0)[1] = make_uint4(v[4], v[5], v[6], v[7]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (k < PL) sr[i0 + k] = v[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        if (k >= PL || v[k] == 0xFFFFFFFFu) continue;
+        const uint32_t nv = k + 1 < PL ? v[k + 1 < 8 ? k + 1 : 7] : nx;
+        const int b = (int)(v[k] >> sh);
+        if (b + 1 < nb && (nv == 0xFFFFFFFFu || (int)(nv >> sh) != b))
+            T[b + 1] = (uint16_t)(i0 + k + 1);
+    }
+}
+
 __device__ __forceinline__ void bucket_scan(uint16_t* T, uint32_t* wtot) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint2 raw = reinterpret_cast<uint2*>(T)[threadIdx.x];
@@ -1194,8 +1233,10 @@ __device__ __forceinline__ uint32_t bucket_count(const uint32_t* sr, const uint1
 
 // shared memory of k_scan: a chunk's staged words (class B: 2,048 x 16 B), its run
 // positions for the chunk-local thresholds (2 x 2,048 x 4 B) and their bucket indexes
-constexpr size_t kScanSmem =
-    (size_t)kScanCh * 16 + 2 * (size_t)kScanCh * 4 + 2 * (size_t)kScanBk * 2;
+// (the words: class B stages one uint4 per config pair, at most kScanCh / 2 + 1 pairs plus
+// a padding word; classes A / C half that); the bucket index is double-buffered per side
+constexpr size_t kScanWords = ((size_t)(kScanCh / 2 + 2) * 16 + 127) & ~(size_t)127;
+constexpr size_t kScanSmem = kScanWords + 2 * (size_t)kScanCh * 4 + 4 * (size_t)kScanBk * 2;
 
 #ifdef PALS_SCAN_TRACE
 // A/B instrumentation (scripts/build_variants.sh): globaltimer of CTA phases, thread 0
@@ -1224,8 +1265,9 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) 
     int mark = 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint4* sw = reinterpret_cast<uint4*>(smem_raw);
-    uint32_t* ssr = reinterpret_cast<uint32_t*>(smem_raw + (size_t)kScanCh * 16);  // [2][L]
-    uint16_t* sbk = reinterpret_cast<uint16_t*>(smem_raw + (size_t)kScanCh * 24);  // [2][kScanBk]
+    uint32_t* ssr = reinterpret_cast<uint32_t*>(smem_raw + kScanWords);  // [2][L]
+    // [2 buffers][2 sides][kScanBk]: segment s builds buffer s & 1 and zeroes the other
+    uint16_t* sbk = reinterpret_cast<uint16_t*>(smem_raw + kScanWords + (size_t)kScanCh * 8);
     __shared__ uint32_t s_wtot[2][kScanThreads / 32];
     const int64_t n = d.n;
     const int L = d.lch;
@@ -1235,6 +1277,8 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) 
     int64_t p0, p1;
     scan_partition(a.counts, n, L, blockIdx.x, gridDim.x, pl, p0, p1);
     int64_t pos = p0;
+    int seg = 0;  // this CTA's segment count: its parity selects the bucket-index buffer
+    reinterpret_cast<uint4*>(sbk)[threadIdx.x] = make_uint4(0u, 0u, 0u, 0u);  // buffer 0
     while (pos < p1) {
         // locate (class, tile, first config) of pos and the end of that tile segment;
         // configs are TR positions, cut further at the chunks of the local ranks
@@ -1267,10 +1311,11 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) 
         int32_t qid[kScanQ];
         uint2 qt[kScanQ];
 #pragma unroll
-        for (int q = 0; q < kScanQ; ++q) {
+        for (int q = 0; q < kScanQ; ++q) {  // one 16-byte record per slot
             const int64_t sq = q_lo + q * kScanThreads + threadIdx.x;
-            qid[q] = sq < q_hi ? __ldg(a.qlist + c * a.qcap + sq) : -1;
-            qt[q] = sq < q_hi ? __ldg(a.qthr + c * a.qcap + sq) : make_uint2(0u, 0u);
+            const uint4 r = sq < q_hi ? __ldg(a.qthr + c * a.qcap + sq) : make_uint4(0u, 0u, ~0u, 0u);
+            qid[q] = (int32_t)r.z;
+            qt[q] = make_uint2(r.x, r.y);
         }
         const uint32_t* lrt = reinterpret_cast<const uint32_t*>(d.lr16[ORD_T]);
         const uint32_t* lrp = reinterpret_cast<const uint32_t*>(d.lr16[ORD_P]);
@@ -1309,23 +1354,24 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) 
             }
         }
         // the chunk's run positions on the feasibility side(s): a query's chunk-local
-        // threshold is the number of run entries inside its feasible prefix [0, K)
+        // threshold is the number of run entries inside its feasible prefix [0, K). Thread t
+        // stages places [t PL, (t + 1) PL) and marks the bucket ends among them straight from
+        // its registers (the next place's position from the next lane), so the bucket index
+        // needs no separate shared-memory pass and barrier. The index is double-buffered:
+        // this segment's buffer was zeroed by the previous segment (or the kernel start),
+        // which now zeroes the next one; the top barrier orders both.
         const int ko = c == CLS_C ? ORD_P : ORD_T;
-        for (int i = threadIdx.x; i < L; i += kScanThreads) {
-            ssr[i] = __ldg((ko == ORD_P ? d.cinv[ORD_P] : d.cinv[ORD_T]) + cb + i);
-            if (c == CLS_B) ssr[L + i] = __ldg(d.cinv[ORD_P] + cb + i);
-        }
-        reinterpret_cast<uint2*>(sbk)[threadIdx.x] = make_uint2(0u, 0u);
-        if (c == CLS_B) reinterpret_cast<uint2*>(sbk + kScanBk)[threadIdx.x] = make_uint2(0u, 0u);
         const int nvalid = (int)min((int64_t)L, n - cb);
+        uint16_t* const t1 = sbk + (seg & 1) * 2 * kScanBk;  // side 1; side 2 at + kScanBk
+        stage_marks(ko == ORD_P ? d.cinv[ORD_P] + cb : d.cinv[ORD_T] + cb, L, ssr, t1, sh, nb);
+        if (c == CLS_B) stage_marks(d.cinv[ORD_P] + cb, L, ssr + L, t1 + kScanBk, sh, nb);
+        reinterpret_cast<uint4*>(sbk + ((seg + 1) & 1) * 2 * kScanBk)[threadIdx.x] =
+            make_uint4(0u, 0u, 0u, 0u);  // the next segment's buffer, both sides
         SCAN_MARK(mark);
         ++mark;
         __syncthreads();
-        bucket_mark(ssr, L, sbk, sh, nb);
-        if (c == CLS_B) bucket_mark(ssr + L, L, sbk + kScanBk, sh, nb);
-        __syncthreads();
-        bucket_scan(sbk, s_wtot[0]);
-        if (c == CLS_B) bucket_scan(sbk + kScanBk, s_wtot[1]);
+        bucket_scan(t1, s_wtot[0]);
+        if (c == CLS_B) bucket_scan(t1 + kScanBk, s_wtot[1]);
         __syncthreads();
         SCAN_MARK(mark);
         ++mark;
@@ -1333,8 +1379,8 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) 
         uint32_t K1[kScanQ], K2[kScanQ], m1[kScanQ], m2[kScanQ];
 #pragma unroll
         for (int q = 0; q < kScanQ; ++q) {
-            K1[q] = kb2(bucket_count(ssr, sbk, sh, nb, nvalid, c == CLS_C ? qt[q].y : qt[q].x));
-            K2[q] = c == CLS_B ? kb2(bucket_count(ssr + L, sbk + kScanBk, sh, nb, nvalid, qt[q].y))
+            K1[q] = kb2(bucket_count(ssr, t1, sh, nb, nvalid, c == CLS_C ? qt[q].y : qt[q].x));
+            K2[q] = c == CLS_B ? kb2(bucket_count(ssr + L, t1 + kScanBk, sh, nb, nvalid, qt[q].y))
                                : 0u;
             m1[q] = m2[q] = 0xFFFFFFFFu;
         }
@@ -1388,6 +1434,7 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) 
             }
         }
         pos = seg_end;
+        ++seg;
         SCAN_MARK(mark);
         ++mark;
     }
@@ -1984,7 +2031,8 @@ static int ensure_query_buffers(pals_plan* p, int64_t nq) {
     }
     cudaFree(p->thr_t);
     const int64_t cap = std::max<int64_t>(nq, 1024);
-    const size_t bytes = (size_t)cap * (8 * 4 + 1 + 12 * N_CLS) + 4096;
+    // per query: thresholds, minima, class; per class slot: list entry + 16-byte record
+    const size_t bytes = (size_t)cap * (8 * 4 + 1 + 20 * N_CLS) + 4096;
     PALS_CUDA(cudaMalloc(&p->thr_t, bytes));
     char* s = (char*)p->thr_t;
     auto take = [&](size_t b) {
@@ -1998,7 +2046,7 @@ static int ensure_query_buffers(pals_plan* p, int64_t nq) {
     p->best_t = (uint64_t*)take(8 * cap);
     p->cls = (uint8_t*)take(cap);
     p->qlist = (int32_t*)take(4 * (size_t)cap * N_CLS);
-    p->qthr = (uint2*)take(8 * (size_t)cap * N_CLS);
+    p->qthr = (uint4*)take(16 * (size_t)cap * N_CLS);
     p->counts = (int32_t*)take(4 * kCountInts);
     p->qcap = cap;
     return PALS_OK;

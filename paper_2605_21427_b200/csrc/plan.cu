@@ -19,6 +19,19 @@
 
 namespace pals {
 
+#ifdef PALS_SCAN_TRACE
+// A/B instrumentation of k_assign_qprep (scripts/aq_trace.py): globaltimer of block phases
+__device__ unsigned long long g_aq_trace[1024][8];
+#define AQ_MARK(k)                                                                        \
+    if (threadIdx.x == 0 && blockIdx.x < 1024) {                                          \
+        unsigned long long t_;                                                            \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
+        g_aq_trace[blockIdx.x][k] = t_;                                                   \
+    }
+#else
+#define AQ_MARK(k)
+#endif
+
 constexpr int kChunk = 2048;        // sort chunk (smem block merge sort)
 constexpr int kScanCh = 2048;       // configs per scan work item
 constexpr int kScanThreads = 256;
@@ -328,7 +341,7 @@ __global__ void __launch_bounds__(TPB) k_sort_chunks(PlanDev d, uint64_t* gk, ui
     }
     if (blockIdx.x == 0 && blockIdx.y == 0 && t == 0) {
         gk[0] = gk[1] = kNone64;
-        *done = 0;
+        done[0] = done[1] = 0;
     }
     if (counts_reset && blockIdx.x == 0 && blockIdx.y == 0)
         for (int i = t; i < kCountInts; i += TPB) counts_reset[i] = 0;
@@ -397,6 +410,34 @@ __device__ __forceinline__ void warp_search2(FS S, uint32_t lo0, uint32_t hi0, u
         const uint32_t pa = la + sa * (lane + 1) - 1, pb = lb + sb * (lane + 1) - 1;
         const bool ta = la < ha && pa < ha && before<LE>(S(pa), xa);
         const bool tb = lb < hb && pb < hb && before<LE>(S(pb), xb);
+        const uint32_t ca = __popc(__ballot_sync(0xffffffffu, ta));
+        const uint32_t cb = __popc(__ballot_sync(0xffffffffu, tb));
+        if (la < ha) {
+            ha = min(ha, la + sa * (ca + 1) - 1);
+            la += sa * ca;
+        }
+        if (lb < hb) {
+            hb = min(hb, lb + sb * (cb + 1) - 1);
+            lb += sb * cb;
+        }
+    }
+    ra = la;
+    rb = lb;
+}
+
+// Two independent warp searches over S in one pass of 32-ary rounds: ra = the first position
+// of [la, ha) whose key is not before xa (LEA: <=, else <), rb likewise over [lb, hb) for xb;
+// an empty range costs nothing.
+template <bool LEA, bool LEB, class FS>
+__device__ __forceinline__ void warp_search_pair(FS S, uint32_t la, uint32_t ha, uint64_t xa,
+                                                 uint32_t lb, uint32_t hb, uint64_t xb,
+                                                 uint32_t& ra, uint32_t& rb) {
+    const uint32_t lane = threadIdx.x & 31;
+    while (la < ha || lb < hb) {
+        const uint32_t sa = (ha - la + 31) >> 5, sb = (hb - lb + 31) >> 5;
+        const uint32_t pa = la + sa * (lane + 1) - 1, pb = lb + sb * (lane + 1) - 1;
+        const bool ta = la < ha && pa < ha && before<LEA>(S(pa), xa);
+        const bool tb = lb < hb && pb < hb && before<LEB>(S(pb), xb);
         const uint32_t ca = __popc(__ballot_sync(0xffffffffu, ta));
         const uint32_t cb = __popc(__ballot_sync(0xffffffffu, tb));
         if (la < ha) {
@@ -560,15 +601,40 @@ __device__ __forceinline__ uint8_t bnd_class(int o, uint64_t a, uint64_t b) {
     return separated(key_value(o, a), key_value(o, b)) ? 2 : 1;
 }
 
+// Narrow a warp search over the merged keys with the staged search index ss (every S-th
+// key, ns of them; null: no narrowing): the first position whose key is not before x (LE:
+// <=, else <) lies in [lo, hi] after this, a window of at most S positions — one or two
+// 32-ary rounds where the whole range took four.
+template <bool LE>
+__device__ __forceinline__ void narrow(const uint64_t* ss, int ns, uint32_t S, uint64_t x,
+                                       uint32_t& lo, uint32_t& hi) {
+    if (!ss) return;
+    int a = 0, b = ns;  // samples before x
+    while (a < b) {
+        const int mid = (a + b) >> 1;
+        if (before<LE>(ss[mid], x)) a = mid + 1;
+        else b = mid;
+    }
+    if (a > 0) lo = max(lo, (uint32_t)(a - 1) * S + 1);
+    if (a < ns) hi = min(hi, (uint32_t)a * S);
+    if (lo > hi) lo = hi;
+}
+
 template <class FM, class FV>
 __device__ __forceinline__ void assign_warp(const PlanDev& d, uint64_t* gk, int o, uint32_t w0,
-                                            FM M, FV V) {
+                                            FM M, FV V, const uint64_t* ss) {
     const uint32_t n = (uint32_t)d.n;
     const uint32_t lane = threadIdx.x & 31;
     const unsigned full = 0xffffffffu;
     const uint32_t p = w0 + lane;
     const bool in = p < n;
     const uint64_t key = in ? M(p) : kNone64;
+    // the point carried at p and what the stores need of it, loaded up front so the chain
+    // TR -> point index / run place overlaps the run searches below
+    const uint32_t trv = in ? V(p) : n;  // the carried grid rank TR
+    const bool real = trv < n;
+    const uint32_t idx = real ? (uint32_t)__ldg(d.inv_tr + trv) : 0u;
+    const uint32_t lq = real ? (uint32_t)d.lq16[o][trv] : 0u;
     uint64_t prev = __shfl_up_sync(full, key, 1);
     uint64_t next = __shfl_down_sync(full, key, 1);
     if (lane == 0) prev = p > 0 ? M(p - 1) : ~key;
@@ -576,41 +642,45 @@ __device__ __forceinline__ void assign_warp(const PlanDev& d, uint64_t* gk, int 
     const bool start = in && prev != key;
     const unsigned sm = __ballot_sync(full, start);
     const uint8_t bi = (in && p + 1 < n) ? bnd_class(o, key, next) : 2;
-    // rank: the last run start among lanes 0..lane, else the start of lane 0's run
+    AQ_MARK(5);
+    // rank: the last run start among lanes 0..lane, else the start of lane 0's run (a run
+    // that began before the warp: searched); danger at a run start: the class of the
+    // boundary after the run's last position (a run that continues past the warp:
+    // searched). Both searches (warp-uniform conditions) run in the same 32-ary rounds.
     const unsigned upto = sm & (full >> (31 - lane));
-    uint32_t r0 = w0;
-    if (!(sm & 1u)) {  // warp-uniform
-        const uint64_t k0 = __shfl_sync(full, key, 0);
-        uint32_t a, b;
-        warp_search2<false>(M, 0, w0, k0, k0, a, b);
-        r0 = a;
-    }
-    const uint32_t r = upto ? w0 + 31 - __clz(upto) : r0;
-    // danger at a run start: the class of the boundary after the run's last position
     const unsigned after = sm & ~(full >> (31 - lane));
     const int tl = after ? __ffs(after) - 1 : 32;
     const uint8_t bend = (uint8_t)__shfl_sync(full, (int)bi, (tl - 1) & 31);
     const uint8_t b31 = (uint8_t)__shfl_sync(full, (int)bi, 31);
+    const bool need_start = !(sm & 1u), need_end = sm && b31 == 0;
+    uint32_t r0 = w0;
     uint8_t bext = 0;
-    if (sm && b31 == 0) {  // warp-uniform: the warp's last run continues past it
-        const uint64_t kl = __shfl_sync(full, key, 31 - __clz(sm));
-        uint32_t a, b;
-        warp_search2<true>(M, w0 + 32, n, kl, kl, a, b);
-        const uint32_t e = a - 1;  // the run's last position
-        bext = e + 1 < n ? bnd_class(o, M(e), M(e + 1)) : 2;
+    if (need_start || need_end) {  // warp-uniform
+        const uint64_t k0 = __shfl_sync(full, key, 0);
+        const uint64_t kl = __shfl_sync(full, key, sm ? 31 - __clz(sm) : 0);
+        uint32_t lo0 = 0, hi0 = need_start ? w0 : 0, lo1 = w0 + 32, hi1 = need_end ? n : w0 + 32;
+        if (need_start) narrow<false>(ss, d.samp_n, (uint32_t)d.samp_s, k0, lo0, hi0);
+        if (need_end) narrow<true>(ss, d.samp_n, (uint32_t)d.samp_s, kl, lo1, hi1);
+        uint32_t a0, a1;
+        warp_search_pair<false, true>(M, lo0, hi0, k0, lo1, hi1, kl, a0, a1);
+        if (need_start) r0 = a0;
+        if (need_end) {
+            const uint32_t e = a1 - 1;  // the run's last position
+            bext = e + 1 < n ? bnd_class(o, M(e), M(e + 1)) : 2;
+        }
     }
+    const uint32_t r = upto ? w0 + 31 - __clz(upto) : r0;
+    AQ_MARK(6);
     if (in) {
         const uint8_t dg = start ? ((tl < 32 || b31 != 0 ? bend : bext) == 1) : 0;
-        const uint32_t trv = V(p);  // the carried grid rank TR
-        if (trv < n) {
-            const uint32_t idx = (uint32_t)d.inv_tr[trv];
+        if (real) {
             const uint64_t k = ((uint64_t)r << d.tr_bits) | (uint64_t)trv;
             if (d.wide) d.key64[o][idx] = k;
             else d.key32[o][idx] = (uint32_t)k;
             d.rank32[o][idx] = r;
             d.pos32[o][idx] = p;
             // the pair scan's run place -> global position (chunk-local ranks, k_scan)
-            d.cinv[o][(trv / (uint32_t)d.lch) * (uint32_t)d.lch + d.lq16[o][trv]] = p;
+            d.cinv[o][(trv / (uint32_t)d.lch) * (uint32_t)d.lch + lq] = p;
             d.midx[o][p] = idx;  // position -> point, and its rank (k_finalize)
             d.sidx[o][p] = r;
             if (r == 0 && o == ORD_T) atomicMin((unsigned long long*)&gk[0], k);
@@ -621,45 +691,58 @@ __device__ __forceinline__ void assign_warp(const PlanDev& d, uint64_t* gk, int 
     }
 }
 
-// last-block-done: every block's keys, danger flags and candidate atomics are
-// visible after its fence, so the final block can resolve the two global winners
+// last-block-done, per order: the t order's blocks count on done[0] and resolve the argmax
+// t_hat over all (gk[0]), the p order's on done[1] for the argmin p_node (gk[1]); every
+// block's keys, danger flags and candidate atomics are visible after its fence, so the last
+// block of the order can resolve its winner. The efficiency order resolves nothing and
+// skips the counter (one counter for all 768 cfg2 blocks serialised ~2.3 us of atomics).
 __device__ __forceinline__ void last_block_resolve(const PlanDev& d, uint64_t* gk, uint32_t* done,
-                                                   uint32_t nblocks) {
+                                                   int o, uint32_t nblocks) {
+    if (o == ORD_E) return;
+    const int w = o == ORD_T ? 0 : 1;
     __shared__ bool last;
     __syncthreads();
+    AQ_MARK(3);
     if (threadIdx.x == 0) {
         __threadfence();
-        last = atomicAdd(done, 1u) == nblocks - 1;
+        last = atomicAdd(&done[w], 1u) == nblocks - 1;
     }
     __syncthreads();
+    AQ_MARK(4);
     if (last) {  // block-uniform
         __threadfence();
-        const int w = threadIdx.x >> 5;
-        if (w < 2) resolve_globals_warp(d, gk, w);
+        if (threadIdx.x < 32) resolve_globals_warp(d, gk, w);
         __syncthreads();
         if (threadIdx.x == 0) {  // self-cleaning for the next prepare
-            gk[0] = gk[1] = kNone64;
-            *done = 0;
+            gk[w] = kNone64;
+            done[w] = 0;
         }
     }
 }
 
-// assign_body: block bx of nbx for order o; nblocks = all assign blocks of the launch.
+// assign_body: block bx of nbx for order o (nbx blocks per order).
+// ss: shared-memory scratch for the order's search index (kSamples keys) or null
 __device__ __forceinline__ void assign_body(const PlanDev& d, uint64_t* gk, uint32_t* done, int o,
-                                            int bx, int nbx, uint32_t nblocks) {
+                                            int bx, int nbx, uint64_t* ss) {
     const uint64_t* __restrict__ m = d.merged[o];
     const uint32_t* __restrict__ mi = d.midx[o];
     const uint32_t n = (uint32_t)d.n;
     const uint32_t stride = (uint32_t)nbx * blockDim.x;
+    if (ss) {  // the search index written by the last merge round
+        for (int i = threadIdx.x; i < d.samp_n; i += blockDim.x) ss[i] = __ldg(d.samp[o] + i);
+        __syncthreads();
+    }
+    AQ_MARK(1);
     for (uint32_t w0 = (uint32_t)bx * blockDim.x + (threadIdx.x & ~31u); w0 < n; w0 += stride)
         assign_warp(d, gk, o, w0, [&](uint32_t q) { return m[q]; },
-                    [&](uint32_t q) { return mi[q]; });
-    last_block_resolve(d, gk, done, nblocks);
+                    [&](uint32_t q) { return mi[q]; }, ss);
+    AQ_MARK(2);
+    last_block_resolve(d, gk, done, o, (uint32_t)nbx);
 }
 
 __global__ void k_assign(PlanDev d, uint64_t* gk, uint32_t* done) {
     pdl_wait();
-    assign_body(d, gk, done, blockIdx.y, blockIdx.x, gridDim.x, gridDim.x * gridDim.y);
+    assign_body(d, gk, done, blockIdx.y, blockIdx.x, gridDim.x, nullptr);
 }
 
 
@@ -832,12 +915,24 @@ __device__ __forceinline__ int64_t count_prefix(const uint64_t* m, int o, int64_
         if (pred(samp[mid])) lo = mid + 1;
         else hi = mid;
     }
+    // the count lies in [a, b]; 8-ary: each round probes 7 evenly spaced positions with
+    // independent loads (2 dependent rounds for cfg2's 64-key windows instead of 6)
     int64_t a = lo == 0 ? 0 : (int64_t)(lo - 1) * S + 1;
     int64_t b = lo == ns ? n : (int64_t)lo * S;
     while (a < b) {
-        const int64_t mid = (a + b) >> 1;
-        if (pred(key_value(o, m[mid]))) a = mid + 1;
-        else b = mid;
+        const int64_t step = (b - a + 7) >> 3;
+        bool t[7];
+#pragma unroll
+        for (int i = 0; i < 7; ++i) {
+            const int64_t q = a + step * (i + 1) - 1;
+            t[i] = q < b && pred(key_value(o, m[q]));
+        }
+        int c = 0;  // a prefix of the probes holds
+#pragma unroll
+        for (int i = 0; i < 7; ++i) c += t[i];
+        const int64_t na = a + step * c;
+        if (c < 7) b = min(b, na + step - 1);  // probe c + 1 failed (or lies past b)
+        a = na;
     }
     return a;
 }
@@ -926,6 +1021,7 @@ __device__ __forceinline__ void qprep_body(const PlanDev& d, const SelArgs& a, i
         }
     }
     __syncthreads();
+    AQ_MARK(1);
     for (int64_t j0 = bx * (int64_t)blockDim.x; j0 < a.nq; j0 += (int64_t)nbx * blockDim.x) {
         const int64_t j = j0 + threadIdx.x;
         int c = -1;
@@ -975,6 +1071,7 @@ __device__ __forceinline__ void qprep_body(const PlanDev& d, const SelArgs& a, i
             }
         }
     }
+    AQ_MARK(2);
     // the last qprep block sees the final class sizes and partitions the pair scan once
     // for every k_scan CTA (a per-CTA search sat on each CTA's critical path)
     __shared__ bool last;
@@ -997,19 +1094,27 @@ __global__ void k_qprep(PlanDev d, SelArgs a) {
 }
 
 // k_assign and k_qprep in one launch (the captured step): qprep reads only the merged
-// arrays, so its blocks (grid.y == N_ORD) run beside the assign blocks (grid.y < N_ORD).
-__global__ void k_assign_qprep(PlanDev d, uint64_t* gk,
-                               uint32_t* done, SelArgs a, int eb, int qb) {
+// arrays, so its blocks run beside the assign blocks. One flat grid, the qb qprep blocks
+// first (they carry the longer dependent chain: the search index, two threshold searches
+// per query, then the scan partition), then eb assign blocks per order; at most 6 blocks of
+// 256 threads per SM (42 registers) so that every block of cfg2's launch is resident at once
+// (at 46 registers 5 fit, and a second wave of ~270 blocks — the qprep row last — started
+// 5 us late).
+__global__ void __launch_bounds__(256, 6) k_assign_qprep(PlanDev d, uint64_t* gk,
+                                                         uint32_t* done, SelArgs a, int eb,
+                                                         int qb) {
     pdl_wait();
+    AQ_MARK(0);
     __shared__ uint64_t sbuf[2 * kSamples];
-    if (blockIdx.y < N_ORD) {
-        if ((int)blockIdx.x >= eb) return;
-        assign_body(d, gk, done, blockIdx.y, blockIdx.x, eb, (uint32_t)eb * N_ORD);
+    const int b = (int)blockIdx.x;
+    if (b >= qb) {
+        const int o = (b - qb) / eb;
+        assign_body(d, gk, done, o, b - qb - o * eb, eb, sbuf);
     } else {
-        if ((int)blockIdx.x >= qb) return;
-        qprep_body(d, a, blockIdx.x, qb, reinterpret_cast<double*>(sbuf),
+        qprep_body(d, a, b, qb, reinterpret_cast<double*>(sbuf),
                    reinterpret_cast<double*>(sbuf) + kSamples);
     }
+    AQ_MARK(7);
 }
 
 // (8) the pair scan: every (query, config) pair of classes A/B/C is decided, on chunk-local
@@ -1443,6 +1548,9 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(PlanDev d, SelArgs a) 
 }
 
 #ifdef PALS_SCAN_TRACE
+extern "C" int pals_debug_aq_trace(unsigned long long* host) {
+    return (int)cudaMemcpyFromSymbol(host, g_aq_trace, sizeof(g_aq_trace));
+}
 extern "C" int pals_debug_scan_trace(unsigned long long* host, int n_rows) {
     return (int)cudaMemcpyFromSymbol(host, g_scan_trace, (size_t)min(n_rows, 4096) * 16 * 8);
 }
@@ -2268,7 +2376,7 @@ static int plan_step(pals_plan* p, const pals_query* d_queries, int64_t nq, int3
             if (!rc && k == 0) {
                 // assign (prepare, part 2) and qprep (select, part 1) fused in one launch
                 const int eb = grid_blocks(ctx, p->n, 256);
-                e = launch_k(k_assign_qprep, dim3(std::max(eb, qb), N_ORD + 1), 256, 0, s,
+                e = launch_k(k_assign_qprep, dim3((unsigned)(qb + N_ORD * eb)), 256, 0, s,
                              (bool)p->pdl, p->d, p->gk, (uint32_t*)(p->gk + 2), a, eb, qb);
                 if (e != cudaSuccess) rc = cuda_fail(e, "k_assign_qprep");
             } else if (!rc) {

@@ -804,6 +804,10 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
                     std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start)
                         .count());
     };
+    struct PhaseEnd {  // reports after every resource of the call is released
+        decltype(phase)& ph;
+        ~PhaseEnd() { ph("released"); }
+    } phase_end{phase};
     Resources res{ctx};
     // plant models (analytic, one per profile): device Analytic + the oracle's scorer
     for (int m = 0; m < n_models; ++m) {
@@ -1200,8 +1204,10 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
                 o_run_gen[gi] = res.stage((const double*)nullptr, run_cap);
             }
         }
+        phase("staged");
         int r = res.commit();
         if (r) return r;
+        phase("committed");
         gi = 0;
         for (int s = 0; s < n_scen; ++s) {
             const pals_scenario& sc = scens[s];
@@ -1341,6 +1347,7 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
     cudaEventDestroy(ev1);
     ctx->sim_kernel_ms = kms;
     if (e != cudaSuccess) return cuda_fail(e, "k_sim");
+    phase("kernel");
     e = copy_on(ctx->stream, node_results, A.node_out, sizeof(pals_sim_node_result) * total_nodes,
                 cudaMemcpyDeviceToHost);
     if (e == cudaSuccess)
@@ -1360,6 +1367,7 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
     if (e != cudaSuccess) return cuda_fail(e, "pals_run_scenarios: arrival hashes");
     for (int64_t gi = 0; gi < total_nodes; ++gi)
         node_results[gi].arrival_stream_hash = hashes[node_stream[gi]];
+    phase("results");
     // RequestRec per request (sim.hpp:100-107), kept on the context for pals_sim_requests
     ctx->sim_requests.clear();
     if (keep_req) {

@@ -1214,7 +1214,8 @@ def bench_sim(args, dist, ctx):
     profs, gpu, coeffs = load_bundle()
     _, preds = sim_predictors(ctx, profs)
     scs, units = sim_suite(args.sim_seeds, first_seed=dist.rank * args.sim_seeds)
-    run_scenarios(ctx, scs[:15], profs, gpu, coeffs, preds)  # warm-up
+    # warm-up at the timed size (allocates the context's pinned / device stream buffers)
+    run_scenarios(ctx, scs, profs, gpu, coeffs, preds)
     walls, kms, preps = [], [], []
     for _ in range(max(1, args.sim_steps)):
         dist.barrier()

@@ -127,6 +127,9 @@ int pals_ctx_destroy(pals_ctx* c) {
     if (c->d_front) cudaFree(c->d_front);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
     if (c->d_sim_arena) cudaFree(c->d_sim_arena);
+    if (c->h_sim_streams) cudaFreeHost(c->h_sim_streams);
+    if (c->d_sim_streams) cudaFree(c->d_sim_streams);
+    if (c->h_sim_flags) cudaFreeHost(c->h_sim_flags);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
     return PALS_OK;

@@ -229,6 +229,10 @@ struct pals_ctx {
     size_t pinned_bytes = 0;
     void* d_sim_arena = nullptr;  // pals_run_scenarios' staged inputs (reused across calls)
     size_t sim_arena_bytes = 0;
+    void* h_sim_streams = nullptr;  // its streamed arrivals: pinned staging + device mirror
+    void* d_sim_streams = nullptr;
+    size_t sim_stream_bytes = 0;
+    int* h_sim_flags = nullptr;     // pinned 1s: the value the chunk-ready flag copies write
     void* replay_cache = nullptr;  // replay.cu
     void* one_cache = nullptr;     // replay.cu: single-call candidate sets (pals_select_one)
     int replay_layout = 0;         // PALS_REPLAY_THREAD / PALS_REPLAY_WARP

@@ -105,13 +105,6 @@ std::string fmt10g(double v) {
     return buf;
 }
 
-// One node's arrival stream: request lengths by id, and cum[k] = requests spawned
-// before interval k's service (cum[0] = the initial backlog).
-struct Stream {
-    std::vector<int32_t> len;
-    std::vector<int32_t> cum;
-};
-
 // FNV-1a over the decimal digits of v (std::to_string of a non-negative integer).
 inline uint64_t fnv_dec(uint64_t h, long v) {
     char d[24];
@@ -127,24 +120,55 @@ inline uint64_t fnv_dec(uint64_t h, long v) {
     return h;
 }
 
-void gen_stream(const pals_scenario& sc, int node, int n_int, Stream* out) {
-    const pals_sim_node& nd = sc.nodes[node];
-    HostRng rng(splitmix64(splitmix64(sc.seed) ^ (uint64_t)node));  // Rng::substream
-    const double log_mean = std::log(sc.mean_tokens) - 0.5 * sc.log_sigma * sc.log_sigma;
-    // spawn_request (sim.hpp:338-353): the lengths; the arrival hash over the requests'
-    // strings is chained on the device (k_arrival_hash), where it was half the host time
-    auto spawn = [&]() {
-        out->len.push_back(std::max(1, (int)std::lround(rng.lognormal(log_mean, sc.log_sigma))));
-    };
-    for (int b = 0; b < nd.initial_backlog; ++b) spawn();
-    out->cum.resize((size_t)n_int + 1);
-    for (int k = 0; k < n_int; ++k) {
-        const int n = rng.poisson(nd.arrival_rate_per_s * sc.interval_s);
-        for (int a = 0; a < n; ++a) spawn();
-        out->cum[k] = (int32_t)out->len.size();  // visible to interval k
+
+// One node's arrival stream (spawn_request, sim.hpp:338-353: the lengths; the arrival hash
+// over the requests' strings is chained on the device by k_arrival_hash): request lengths by
+// id, and cum[k] = requests spawned before interval k's service (the initial backlog first).
+// Generated incrementally, interval range by interval range, straight into its region of
+// the streamed upload buffer: cum [n_int + 1], len [cap] (cap: a bound the count never
+// reaches in practice — mean + 12 sigma + 1,024; an overflow is reported).
+struct StreamGen {
+    HostRng rng{0};
+    double log_mean = 0.0, log_sigma = 0.0, lam = 0.0;
+    int backlog = 0, n_int = 0;
+    int32_t* cum = nullptr;  // cum[k * cstride]: the streams' counts are interval-major
+    int64_t cstride = 1;
+    int32_t* len = nullptr;
+    int64_t cap = 0, count = 0;
+    bool overflow = false;
+    void init(const pals_scenario& sc, int node, int ni, int32_t* c, int64_t cs, int32_t* l,
+              int64_t cp) {
+        const pals_sim_node& nd = sc.nodes[node];
+        rng = HostRng(splitmix64(splitmix64(sc.seed) ^ (uint64_t)node));  // Rng::substream
+        log_mean = std::log(sc.mean_tokens) - 0.5 * sc.log_sigma * sc.log_sigma;
+        log_sigma = sc.log_sigma;
+        lam = nd.arrival_rate_per_s * sc.interval_s;
+        backlog = nd.initial_backlog;
+        n_int = ni;
+        cum = c;
+        cstride = cs;
+        len = l;
+        cap = cp;
+        count = 0;
+        overflow = false;
     }
-    out->cum[n_int] = (int32_t)out->len.size();
-}
+    void spawn() {
+        const int32_t v = std::max(1, (int)std::lround(rng.lognormal(log_mean, log_sigma)));
+        if (count < cap) len[count] = v;
+        else overflow = true;
+        ++count;
+    }
+    void run(int k0, int k1) {  // intervals [k0, k1), in order
+        if (k0 == 0)
+            for (int b = 0; b < backlog; ++b) spawn();
+        for (int k = k0; k < k1; ++k) {
+            const int n = rng.poisson(lam);
+            for (int a = 0; a < n; ++a) spawn();
+            cum[k * cstride] = (int32_t)count;  // visible to interval k
+        }
+        if (k1 == n_int) cum[n_int * cstride] = (int32_t)count;
+    }
+};
 
 // The arrival hash of a stream (spawn_request, sim.hpp:338-353; fnv1a64 rng.hpp:22-28):
 // fnv1a64 chained over to_string(id) + ":" + to_string(len) + "@" + fmt_num(t) per request,
@@ -153,7 +177,8 @@ void gen_stream(const pals_scenario& sc, int node, int n_int, Stream* out) {
 // thread per stream: the chain is serial, the streams are not.
 struct HashJob {
     const int32_t* len;
-    const int32_t* cum;
+    const int32_t* cum;  // cum[k * cstride]
+    int64_t cstride;
     const uint32_t* toff;  // [n_int + 1] offsets into tchars: interval k's "@t" string
     const char* tchars;
     int n_int, backlog;
@@ -188,7 +213,7 @@ __global__ void k_arrival_hash(const HashJob* __restrict__ jobs, int n_jobs, uin
     };
     for (int b = 0; b < j.backlog; ++b) req("@0", 2);
     for (int k = 0; k < j.n_int; ++k) {
-        const uint32_t end = (uint32_t)j.cum[k];
+        const uint32_t end = (uint32_t)j.cum[(int64_t)k * j.cstride];
         if (id == end) continue;
         const uint32_t t0 = j.toff[k], tn = j.toff[k + 1] - t0;
         while (id < end) req(j.tchars + t0, tn);
@@ -211,7 +236,8 @@ struct TraceCursor {
 struct SimNodeDev {
     const ReplayModelDev* sel;  // select tables over the node's candidates + scorer
     const Analytic* plant;      // the node's calibrated profile
-    const int32_t* cum;         // [n_int + 1]
+    const int32_t* cum;         // [n_int + 1], element k at cum[k * cum_stride]
+    int64_t cum_stride;
     const int32_t* len;         // request lengths by id
     int32_t* run_len;           // running list (global fallback): output tokens, generated,
     double* run_gen;            // request id
@@ -247,7 +273,32 @@ struct SimArgs {
     pals_sim_decision* dec;
     int smem_run;  // > 0: running lists live in shared memory, smem_run entries per warp
     const int32_t* order;  // CTA -> scenario
+    const int* flags;      // streamed arrivals: per chunk of chunk_k intervals, 1 once on device
+    int chunk_k;
 };
+
+// Wait until the arrivals of interval k's chunk are on the device (streamed upload): lane 0
+// polls the chunk's flag (device memory, written by a copy queued after the chunk's data)
+// with acquire loads; a flag that never rises releases the warp after ~20 s (the host raises
+// every flag before returning, so this only bounds a host failure).
+__device__ __forceinline__ void await_chunk(const SimArgs& a, int k, int& ready_until) {
+    if (k < ready_until) return;
+    const int c = k / a.chunk_k;
+    if ((threadIdx.x & 31) == 0) {
+        unsigned long long t0, t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (;;) {
+            int v;
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(a.flags + c) : "memory");
+            if (v) break;
+            __nanosleep(2000);
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > 20000000000ull) break;
+        }
+    }
+    __syncwarp();
+    ready_until = (c + 1) * a.chunk_k;
+}
 
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -307,6 +358,7 @@ __global__ void __launch_bounds__(32 * PALS_SIM_MAX_NODES) k_sim(SimArgs a) {
     double last_budget = 0.0;
     int sustain = 0;
     int next_admit = 0, R = 0, chg = 0;
+    int ready_until = 0;  // intervals whose arrivals are on the device (streamed upload)
     double node_budget = 0.0;
     double kp_budget = -1.0;
     int kpv = m.nd_p, kt = 0;
@@ -326,8 +378,10 @@ __global__ void __launch_bounds__(32 * PALS_SIM_MAX_NODES) k_sim(SimArgs a) {
         double sys_w = 0.0;
         if (live) {
             while (chg < S.n_changes && S.change_k[chg] <= k) node_budget = N.budget[chg++];
-            // (1) arrivals: the stream's requests up to this interval are queued
-            const int spawned = N.cum[k];
+            // (1) arrivals: the stream's requests up to this interval are queued (streamed:
+            // read through L2, the chunk's flag first)
+            await_chunk(a, k, ready_until);
+            const int spawned = __ldcg(N.cum + (int64_t)k * N.cum_stride);
             // (2) effective batch from queue pressure, per replica (sim.hpp:360-365)
             const int avail = R + (spawned - next_admit);
             const int per_replica = (avail + N.dp - 1) / N.dp;
@@ -375,7 +429,7 @@ __global__ void __launch_bounds__(32 * PALS_SIM_MAX_NODES) k_sim(SimArgs a) {
                     if (R < slot_cap && next_admit < spawned) {  // refill freed slots
                         const int n_adm = min(slot_cap - R, spawned - next_admit);
                         for (int j = lane; j < n_adm; j += 32) {
-                            run_len[R + j] = N.len[next_admit + j];
+                            run_len[R + j] = __ldcg(N.len + next_admit + j);
                             run_gen[R + j] = 0.0;
                             run_id[R + j] = next_admit + j;
                         }
@@ -566,7 +620,7 @@ __global__ void __launch_bounds__(32 * PALS_SIM_MAX_NODES) k_sim(SimArgs a) {
         r.throughput_target_tps = target;
         r.final_bias = bias;
         r.arrival_stream_hash = 0;  // host fills
-        r.n_requests = N.cum[S.n_int];
+        r.n_requests = __ldcg(N.cum + (int64_t)S.n_int * N.cum_stride);
         r.n_completed = completed;
         r.n_applied = n_applied;
         r.final_idx = cur;
@@ -983,7 +1037,6 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
     // backlog, length law, interval grid) — a baseline suite's policies share them
     std::vector<int64_t> node0(n_scen + 1, 0);
     for (int s = 0; s < n_scen; ++s) node0[s + 1] = node0[s] + scens[s].n_nodes;
-    std::vector<Stream> streams;
     std::vector<int> node_stream(total_nodes);
     std::vector<std::pair<int, int>> work;  // (scenario, node) generating each stream
     {
@@ -1002,32 +1055,87 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
                 }
                 node_stream[node0[s] + i] = it->second;
             }
-        streams.resize(work.size());
     }
-    // streams differ in length (900 s vs 3600 s scenarios): dynamic scheduling; the worker
-    // threads run while this thread splits the budgets (which never read the streams)
-    std::atomic<size_t> next_stream{0};
+    // Streamed arrivals. Each stream has a fixed region (cum, then len up to a capacity
+    // bound) in one pinned buffer mirrored by one device buffer, so the node descriptors
+    // point at device addresses known before any draw. The streams are generated in C
+    // chunks of intervals (every stream's intervals [c K, (c + 1) K) per chunk, each stream
+    // by one worker so its draws stay in order); every finished chunk is copied up and
+    // flagged in mapped memory, and k_sim, launched after chunk 0, waits per chunk for its
+    // flag — the simulation runs while the host still draws later intervals.
+    // layout: the counts interval-major (row k = every stream's cum[k], so a chunk's counts
+    // are one copy), then every stream's lengths
+    const size_t n_streams = work.size();
+    std::vector<size_t> s_oc(n_streams), s_ol(n_streams);
+    std::vector<int64_t> s_cap(n_streams);
+    int max_n_int = 1;
+    for (size_t u = 0; u < n_streams; ++u) max_n_int = std::max(max_n_int, n_int[work[u].first]);
+    size_t s_elems = (((size_t)max_n_int + 1) * n_streams + 31) & ~(size_t)31;
+    for (size_t u = 0; u < n_streams; ++u) {
+        const pals_scenario& sc = scens[work[u].first];
+        const pals_sim_node& nd = sc.nodes[work[u].second];
+        const int ni = n_int[work[u].first];
+        const double mean = std::max(0.0, nd.arrival_rate_per_s * sc.interval_s) * ni;
+        s_cap[u] = (int64_t)nd.initial_backlog +
+                   (int64_t)std::ceil(mean + 12.0 * std::sqrt(mean + 1.0)) + 1024;
+        s_oc[u] = u;  // column u of the count rows
+        s_ol[u] = s_elems;
+        s_elems += ((size_t)s_cap[u] + 31) & ~(size_t)31;
+    }
+    const int64_t cstride = (int64_t)n_streams;
+    const size_t s_bytes = std::max<size_t>(1, s_elems) * 4;
+    if (ctx->sim_stream_bytes < s_bytes) {
+        if (ctx->h_sim_streams) cudaFreeHost(ctx->h_sim_streams);
+        if (ctx->d_sim_streams) cudaFree(ctx->d_sim_streams);
+        ctx->h_sim_streams = ctx->d_sim_streams = nullptr;
+        ctx->sim_stream_bytes = 0;
+        PALS_CUDA(cudaHostAlloc(&ctx->h_sim_streams, s_bytes, cudaHostAllocDefault));
+        PALS_CUDA(cudaMalloc(&ctx->d_sim_streams, s_bytes));
+        ctx->sim_stream_bytes = s_bytes;
+    }
+    int32_t* const hbuf = (int32_t*)ctx->h_sim_streams;
+    int32_t* const dbuf = (int32_t*)ctx->d_sim_streams;
+    constexpr int kSimChunks = 8;
+    const int chunk_k = (max_n_int + kSimChunks - 1) / kSimChunks;
+    std::vector<StreamGen> gens(n_streams);
+    for (size_t u = 0; u < n_streams; ++u)
+        gens[u].init(scens[work[u].first], work[u].second, n_int[work[u].first], hbuf + s_oc[u],
+                     cstride, hbuf + s_ol[u], s_cap[u]);
+    // [chunk][stream]: the stream's request count after the chunk (its len range is
+    // [count after chunk c - 1, count after chunk c))
+    std::vector<int64_t> s_after((size_t)kSimChunks * n_streams, 0);
+    std::atomic<int> chunk_done[kSimChunks];
+    for (auto& x : chunk_done) x = 0;
+    std::atomic<bool> stop_workers{false};
     std::vector<std::thread> stream_threads;
+    unsigned n_workers = 1;
     {
-        // one core stays with this thread: it splits the budgets on the GPU meanwhile, and
-        // its CUDA calls lost the CPU to the workers (budget phase 56 ms -> 0.2-0.4 s)
+        // one core stays with this thread: it splits the budgets on the GPU meanwhile and
+        // then feeds the copies, and its CUDA calls lost the CPU to the workers otherwise
         const unsigned hc = std::thread::hardware_concurrency();
-        const unsigned nt = std::max(1u, std::min<unsigned>(hc > 1 ? hc - 1 : 1,
-                                                            (unsigned)work.size()));
-        for (unsigned t = 0; t < nt; ++t)
-            stream_threads.emplace_back([&] {
-                for (size_t w = next_stream++; w < work.size(); w = next_stream++)
-                    gen_stream(scens[work[w].first], work[w].second, n_int[work[w].first],
-                               &streams[w]);
+        n_workers = std::max(1u, std::min<unsigned>(hc > 1 ? hc - 1 : 1, (unsigned)n_streams));
+        for (unsigned t = 0; t < n_workers; ++t)
+            stream_threads.emplace_back([&, t] {
+                for (int c = 0; c < kSimChunks && !stop_workers; ++c) {
+                    for (size_t u = t; u < n_streams; u += n_workers) {
+                        StreamGen& g = gens[u];
+                        const int k0 = c * chunk_k, k1 = std::min(g.n_int, (c + 1) * chunk_k);
+                        if (k0 < k1) g.run(k0, k1);
+                        s_after[(size_t)c * n_streams + u] = g.count;
+                    }
+                    chunk_done[c].fetch_add(1, std::memory_order_release);
+                }
             });
     }
     struct Joiner {
         std::vector<std::thread>& t;
+        std::atomic<bool>& stop;
         ~Joiner() {
+            stop = true;
             for (auto& x : t)
                 if (x.joinable()) x.join();
         }
-    } joiner{stream_threads};
+    } joiner{stream_threads, stop_workers};
 
     phase("streams started");
     // budget changes and their splits (assign_budgets, sim.hpp:229-238, 277-283, 313-336)
@@ -1136,19 +1244,13 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
     }
 
     phase("budgets");
-    for (auto& t : stream_threads) t.join();
-    std::vector<size_t> o_cum(streams.size()), o_len(streams.size());
-    for (size_t u = 0; u < streams.size(); ++u) {
-        o_cum[u] = res.stage_ref(streams[u].cum);
-        o_len[u] = res.stage_ref(streams[u].len);
-    }
     // "@" + fmt_num(k * interval) per interval of every distinct grid (the arrival hash's
     // request suffixes, sim.hpp:344; csvio.hpp:17-21)
     std::map<std::pair<double, int>, int> grid_of;
     std::vector<std::vector<char>> g_chars;
     std::vector<std::vector<uint32_t>> g_off;
-    std::vector<int> stream_grid(streams.size());
-    for (size_t u = 0; u < streams.size(); ++u) {
+    std::vector<int> stream_grid(n_streams);
+    for (size_t u = 0; u < n_streams; ++u) {
         const pals_scenario& sc = scens[work[u].first];
         const int ni = n_int[work[u].first];
         auto it = grid_of.find({sc.interval_s, ni});
@@ -1196,8 +1298,8 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
                 max_run = std::max(max_run, run_cap);
                 o_run_len[gi] = res.stage((const int32_t*)nullptr, run_cap);
                 o_run_id[gi] = res.stage((const int32_t*)nullptr, run_cap);
-                if (keep_req) {
-                    const size_t nreq = streams[node_stream[gi]].len.size();
+                if (keep_req) {  // sized by the stream's capacity bound (drawn later)
+                    const size_t nreq = (size_t)s_cap[node_stream[gi]];
                     o_req_k[gi] = res.stage((const int32_t*)nullptr, nreq);
                     o_req_gen[gi] = res.stage((const double*)nullptr, nreq);
                 }
@@ -1236,8 +1338,9 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
                 N.dp = n.dp;
                 N.init_idx = node_init[gi];
                 N.target_tps = node_target[gi];
-                N.cum = res.at<int32_t>(o_cum[node_stream[gi]]);
-                N.len = res.at<int32_t>(o_len[node_stream[gi]]);
+                N.cum = dbuf + s_oc[node_stream[gi]];
+                N.cum_stride = cstride;
+                N.len = dbuf + s_ol[node_stream[gi]];
                 N.run_len = res.at<int32_t>(o_run_len[gi]);
                 N.run_id = res.at<int32_t>(o_run_id[gi]);
                 N.req_k = keep_req ? res.at<int32_t>(o_req_k[gi]) : nullptr;
@@ -1248,11 +1351,12 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
         }
     }
     // the arrival hashes, on a side stream beside k_sim
-    std::vector<HashJob> jobs(streams.size());
-    for (size_t u = 0; u < streams.size(); ++u) {
+    std::vector<HashJob> jobs(n_streams);
+    for (size_t u = 0; u < n_streams; ++u) {
         HashJob& j = jobs[u];
-        j.len = res.at<int32_t>(o_len[u]);
-        j.cum = res.at<int32_t>(o_cum[u]);
+        j.len = dbuf + s_ol[u];
+        j.cum = dbuf + s_oc[u];
+        j.cstride = cstride;
         j.toff = res.at<uint32_t>(o_goff[stream_grid[u]]);
         j.tchars = res.at<char>(o_gch[stream_grid[u]]);
         j.n_int = n_int[work[u].first];
@@ -1281,16 +1385,7 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
     } hs_guard{hs_stream, ev_fork, ev_hash};
     PALS_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     PALS_CUDA(cudaEventCreateWithFlags(&ev_hash, cudaEventDisableTiming));
-    PALS_CUDA(cudaEventRecord(ev_fork, ctx->stream));
-    PALS_CUDA(cudaStreamWaitEvent(hs_stream, ev_fork, 0));
-    if (!jobs.empty()) {
-        k_arrival_hash<<<(unsigned)((jobs.size() + 63) / 64), 64, 0, hs_stream>>>(
-            d_jobs, (int)jobs.size(), d_hash);
-        count_launch(ctx);
-        const cudaError_t he = cudaGetLastError();
-        if (he != cudaSuccess) return cuda_fail(he, "k_arrival_hash");
-    }
-    PALS_CUDA(cudaEventRecord(ev_hash, hs_stream));
+    // (the arrival hashes run on hs_stream after the last chunk's copies, below)
     SimArgs A;
     memset(&A, 0, sizeof A);
     // CTA order: most node-intervals first, so the long scenarios do not form the tail
@@ -1323,8 +1418,66 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
         r = res.alloc(&A.dec, nlog);
         if (r) return r;
     }
+    // per-chunk readiness flags in device memory (zeroed before the launch), raised by a
+    // 4-byte copy queued behind the chunk's data copies: k_sim polls L2, not the PCIe bus
+    // (polling mapped host memory from every warp starved the copies themselves)
+    int* d_flags = nullptr;
+    {
+        int r = res.alloc(&d_flags, kSimChunks);
+        if (r) return r;
+    }
+    if (!ctx->h_sim_flags) {  // pinned source of the flag value (1)
+        PALS_CUDA(cudaHostAlloc((void**)&ctx->h_sim_flags, 64 * sizeof(int), cudaHostAllocDefault));
+        for (int c = 0; c < 64; ++c) ctx->h_sim_flags[c] = 1;
+    }
+    PALS_CUDA(cudaMemsetAsync(d_flags, 0, kSimChunks * sizeof(int), ctx->stream));
+    A.flags = d_flags;
+    A.chunk_k = chunk_k;
     PALS_CUDA(cudaStreamSynchronize(ctx->stream));
     phase("upload");
+    // whatever happens below, every chunk flag is raised before this function returns, so a
+    // launched k_sim never waits for a chunk that will not come
+    struct FlagGuard {
+        pals_ctx* c;
+        int* f;
+        cudaStream_t& s;
+        ~FlagGuard() {
+            cudaMemcpyAsync(f, c->h_sim_flags, kSimChunks * sizeof(int), cudaMemcpyHostToDevice,
+                            s);
+            cudaStreamSynchronize(s);
+            cudaStreamSynchronize(c->stream);
+        }
+    } flag_guard{ctx, d_flags, hs_stream};
+    // chunk c: wait for its draws, copy every stream's new part up on hs_stream, then raise
+    // the chunk's flag once the copies have landed (a host function in stream order)
+    auto publish = [&](int c) -> int {
+        while (chunk_done[c].load(std::memory_order_acquire) < (int)n_workers)
+            std::this_thread::sleep_for(std::chrono::microseconds(20));
+        for (size_t u = 0; u < n_streams; ++u) {
+            const int ni = gens[u].n_int;
+            const int64_t l0 = c ? std::min(s_cap[u], s_after[(size_t)(c - 1) * n_streams + u]) : 0;
+            const int64_t l1 = std::min(s_cap[u], s_after[(size_t)c * n_streams + u]);
+            if (l1 > l0)
+                PALS_CUDA(cudaMemcpyAsync(dbuf + s_ol[u] + l0, hbuf + s_ol[u] + l0,
+                                          (size_t)(l1 - l0) * 4, cudaMemcpyHostToDevice,
+                                          hs_stream));
+            (void)ni;
+        }
+        {  // the chunk's count rows (the last chunk also the final row, cum[n_int])
+            const int k0 = c * chunk_k;
+            const int k1 =
+                c == kSimChunks - 1 ? max_n_int + 1 : std::min(max_n_int + 1, (c + 1) * chunk_k);
+            if (k1 > k0)
+                PALS_CUDA(cudaMemcpyAsync(dbuf + (size_t)k0 * n_streams, hbuf + (size_t)k0 * n_streams,
+                                          (size_t)(k1 - k0) * n_streams * 4,
+                                          cudaMemcpyHostToDevice, hs_stream));
+        }
+        PALS_CUDA(cudaMemcpyAsync(d_flags + c, ctx->h_sim_flags, sizeof(int),
+                                  cudaMemcpyHostToDevice, hs_stream));
+        return PALS_OK;
+    };
+    int pr = publish(0);
+    if (pr) return pr;
     ctx->sim_prep_s =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
     cudaEvent_t ev0, ev1;
@@ -1340,6 +1493,25 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
     count_launch(ctx);
     cudaError_t e = cudaGetLastError();
     cudaEventRecord(ev1, ctx->stream);
+    for (int c = 1; c < kSimChunks && e == cudaSuccess; ++c) {
+        pr = publish(c);
+        if (pr) return pr;
+    }
+    phase("published");
+    for (auto& t : stream_threads) t.join();
+    for (size_t u = 0; u < n_streams; ++u)
+        if (gens[u].overflow)
+            return set_error(PALS_EDATA, "pals_run_scenarios: an arrival stream exceeded its "
+                                         "capacity bound (mean + 12 sigma)");
+    if (!jobs.empty()) {  // after every chunk's copies (hs_stream order)
+        k_arrival_hash<<<(unsigned)((jobs.size() + 63) / 64), 64, 0, hs_stream>>>(
+            d_jobs, (int)jobs.size(), d_hash);
+        count_launch(ctx);
+        const cudaError_t he = cudaGetLastError();
+        if (he != cudaSuccess) return cuda_fail(he, "k_arrival_hash");
+    }
+    PALS_CUDA(cudaEventRecord(ev_hash, hs_stream));
+
     if (e == cudaSuccess) e = cudaEventSynchronize(ev1);
     float kms = -1.0f;
     if (e == cudaSuccess) cudaEventElapsedTime(&kms, ev0, ev1);
@@ -1375,8 +1547,10 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
         int64_t gi = 0;
         for (int s = 0; s < n_scen; ++s)
             for (int i = 0; i < scens[s].n_nodes; ++i, ++gi) {
-                const Stream& st = streams[node_stream[gi]];
-                const size_t nreq = st.len.size();
+                const size_t u = (size_t)node_stream[gi];
+                const int32_t* st_len = hbuf + s_ol[u];
+                const int32_t* st_cum = hbuf + s_oc[u];
+                const size_t nreq = (size_t)gens[u].count;
                 std::vector<int32_t> kk(nreq);
                 std::vector<double> gg(nreq);
                 e = copy_on(ctx->stream, kk.data(), res.at<int32_t>(o_req_k[gi]), nreq * 4,
@@ -1391,17 +1565,18 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
                 std::vector<double> arrival(nreq, 0.0);  // backlog: spawned at t = 0
                 int64_t prev = scens[s].nodes[i].initial_backlog;
                 for (int k = 0; k < n_int[s]; ++k) {
-                    for (int64_t q = prev; q < st.cum[k]; ++q) arrival[q] = k * iv;
-                    prev = st.cum[k];
+                    const int64_t ck = st_cum[(int64_t)k * cstride];
+                    for (int64_t q = prev; q < ck; ++q) arrival[q] = k * iv;
+                    prev = ck;
                 }
                 for (size_t q = 0; q < nreq; ++q) {
                     pals_sim_request& r = out[q];
                     r.id = (int64_t)q;
                     r.arrival_s = arrival[q];
-                    r.output_tokens = st.len[q];
+                    r.output_tokens = st_len[q];
                     r._pad = 0;
                     r.completed_s = kk[q] ? (kk[q] - 1) * iv + iv : -1.0;
-                    r.generated = kk[q] ? (double)st.len[q] : gg[q];
+                    r.generated = kk[q] ? (double)st_len[q] : gg[q];
                 }
             }
     }

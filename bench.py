@@ -67,6 +67,8 @@ def parse():
     ap.add_argument("--cfg5-steps", type=int, default=2, help="timed cfg5 replays")
     ap.add_argument("--sim-seeds", type=int, default=256,
                     help="seeds per GPU of the 3-scenario x 5-policy queue-plant suite")
+    ap.add_argument("--sim-no-stream", action="store_true",
+                    help="queue-plant uploads before the launch (for ncu launch lists)")
     ap.add_argument("--sim-steps", type=int, default=2, help="timed queue-plant runs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
@@ -1211,6 +1213,8 @@ def bench_sim(args, dist, ctx):
     device simulation) and the simulation kernel alone."""
     from paper_2605_21427_b200.profiles import load_bundle
     from paper_2605_21427_b200.sim import last_timing, run_scenarios
+    if args.sim_no_stream:
+        ctx.set_sim_streaming(False)
     profs, gpu, coeffs = load_bundle()
     _, preds = sim_predictors(ctx, profs)
     scs, units = sim_suite(args.sim_seeds, first_seed=dist.rank * args.sim_seeds)

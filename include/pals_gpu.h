@@ -731,6 +731,11 @@ typedef struct {
  * records (nodes numbered across scenarios, as node_results) — n = count; out may be
  * NULL to size. */
 int pals_sim_keep_requests(pals_ctx* ctx, int32_t enable);
+/* Streamed arrivals (default on): pals_run_scenarios launches the simulation after the
+ * first chunk of arrival intervals and uploads the rest while it runs. enable = 0 draws and
+ * uploads every chunk before the launch — for runs under a kernel profiler, which
+ * serialises the launch with the later uploads. */
+int pals_sim_set_streaming(pals_ctx* ctx, int32_t enable);
 int pals_sim_requests(pals_ctx* ctx, int64_t node, pals_sim_request* out, int64_t cap,
                       int64_t* n);
 

@@ -96,6 +96,7 @@ SIGNATURES = [
     ("pals_fnv1a64", C.c_uint64, [_VP, _I64]),
     ("pals_sim_last_timing", _I, [_VP, _VP, _VP]),
     ("pals_sim_keep_requests", _I, [_VP, _I32]),
+    ("pals_sim_set_streaming", _I, [_VP, _I32]),
     ("pals_sim_requests", _I, [_VP, _I64, _VP, _I64, _VP]),
     ("pals_run_scenarios", _I, [_VP, _I32, _VP, _I32, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _VP,
                                 _VP]),

@@ -240,6 +240,7 @@ struct pals_ctx {
     double sim_prep_s = 0.0;       // sim.cu: host setup of the last pals_run_scenarios
     double sim_kernel_ms = -1.0;   // and its k_sim launch (CUDA events)
     int sim_keep_requests = 0;     // pals_sim_keep_requests
+    int sim_streaming = 1;         // pals_sim_set_streaming
     std::vector<std::vector<pals_sim_request>> sim_requests;  // per node of the last run
     void* d_front = nullptr;       // frontier.cu scratch
     size_t front_bytes = 0;

@@ -1476,8 +1476,12 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
                                   cudaMemcpyHostToDevice, hs_stream));
         return PALS_OK;
     };
-    int pr = publish(0);
-    if (pr) return pr;
+    // streamed: launch after chunk 0; otherwise (profiling) after every chunk
+    const int pre = ctx->sim_streaming ? 1 : kSimChunks;
+    for (int c = 0; c < pre; ++c) {
+        const int pr = publish(c);
+        if (pr) return pr;
+    }
     ctx->sim_prep_s =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
     cudaEvent_t ev0, ev1;
@@ -1493,8 +1497,8 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
     count_launch(ctx);
     cudaError_t e = cudaGetLastError();
     cudaEventRecord(ev1, ctx->stream);
-    for (int c = 1; c < kSimChunks && e == cudaSuccess; ++c) {
-        pr = publish(c);
+    for (int c = pre; c < kSimChunks && e == cudaSuccess; ++c) {
+        const int pr = publish(c);
         if (pr) return pr;
     }
     phase("published");
@@ -1587,6 +1591,12 @@ extern "C" int pals_sim_last_timing(pals_ctx* ctx, double* host_setup_s, double*
     if (!ctx) return set_error(PALS_ECONFIG, "pals_sim_last_timing: null context");
     if (host_setup_s) *host_setup_s = ctx->sim_prep_s;
     if (kernel_ms) *kernel_ms = ctx->sim_kernel_ms;
+    return PALS_OK;
+}
+
+extern "C" int pals_sim_set_streaming(pals_ctx* ctx, int32_t enable) {
+    if (!ctx) return set_error(PALS_ECONFIG, "pals_sim_set_streaming: null context");
+    ctx->sim_streaming = enable ? 1 : 0;
     return PALS_OK;
 }
 

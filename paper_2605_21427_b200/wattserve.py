@@ -70,6 +70,11 @@ class Context:
         """"thread" (one thread per trace, default) or "warp" (one warp per trace)."""
         check(self.lib.pals_ctx_set_replay_layout(self.h, {"thread": 0, "warp": 1}[layout]))
 
+    def set_sim_streaming(self, on: bool = True):
+        """Queue-plant runs stream their arrival uploads behind the running simulation (on,
+        the default); off draws and uploads everything first (for kernel profilers)."""
+        check(self.lib.pals_sim_set_streaming(self.h, 1 if on else 0))
+
     def set_one_server(self, idle_us: int):
         """Single calls through the resident server kernel, which exits after idle_us without
         a request (0: one kernel launch per call)."""

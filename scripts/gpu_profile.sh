@@ -10,7 +10,7 @@ START=$(date +%s); timeout 1200 python bench.py > gpurun_out/bench.json 2> gpuru
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2>> gpurun_out/bench.err
 NCU="ncu --set full --clock-control none --import-source on -f"
 # the launch list of the bench command itself (cold-cache, serialised: shares, not absolutes)
-timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --no-cpu-baseline > gpurun_out/b_ncu.log 2>&1
+timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --no-cpu-baseline --sim-no-stream > gpurun_out/b_ncu.log 2>&1
 # the select graph at cfg2's bench size (1e4 queries, 65,536 configs); launch 4 = a warm step
 for k in k_scan k_eval_analytic k_sort_chunks k_merge_round k_assign_qprep k_finalize; do
   timeout 600 $NCU -k "regex:^$k" -s 3 -c 1 -o gpurun_out/prof_$k python scripts/select_quick.py cfg2 2 x > gpurun_out/ncu_$k.log 2>&1

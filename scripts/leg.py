@@ -25,6 +25,7 @@ if leg == "alloc":
 elif leg == "frontier":
     out = bench.bench_frontiers(args, dist, ctx, stream, l2_flush)
 elif leg == "sim":
+    ctx.set_sim_streaming(False)  # under ncu the launch is serialised with the later uploads
     out = bench.bench_sim(args, dist, ctx)
     out = {k: v for k, v in out.items() if not k.startswith("_")}
 elif leg == "forest":

@@ -129,3 +129,22 @@ def test_errors_follow_the_reference(ctx, reference, setup):
         run_scenarios(ctx, [low], profs, gpu, coeffs, preds)
     with pytest.raises(RuntimeError):
         reference.run_scenario(low, profs, gpu, coeffs, path)
+
+
+def test_streamed_upload_matches_upload_first(ctx, setup):
+    """The streamed arrival upload (k_sim launched after the first chunk of intervals) and
+    the profiler mode (every chunk uploaded before the launch) give the same bytes."""
+    profs, gpu, coeffs, preds, _ = setup
+    scs = []
+    for seed in range(4):
+        for sc in bundled_scenarios().values():
+            for pol in POLICIES:
+                scs.append(dict(sc, policy=pol, seed=seed))
+    a = run_scenarios(ctx, scs, profs, gpu, coeffs, preds, logs=True)
+    ctx.set_sim_streaming(False)
+    try:
+        b = run_scenarios(ctx, scs, profs, gpu, coeffs, preds, logs=True)
+    finally:
+        ctx.set_sim_streaming(True)
+    for x, y in zip(a, b):
+        assert x.tobytes() == y.tobytes()

@@ -620,7 +620,9 @@ __global__ void __launch_bounds__(32 * PALS_SIM_MAX_NODES) k_sim(SimArgs a) {
         r.throughput_target_tps = target;
         r.final_bias = bias;
         r.arrival_stream_hash = 0;  // host fills
-        r.n_requests = __ldcg(N.cum + (int64_t)S.n_int * N.cum_stride);
+        // = cum[n_int]: no request spawns after the last interval, and cum[n_int - 1] lies
+        // in a chunk this warp has waited for (cum[n_int] may lie in the next one)
+        r.n_requests = __ldcg(N.cum + (int64_t)(S.n_int - 1) * N.cum_stride);
         r.n_completed = completed;
         r.n_applied = n_applied;
         r.final_idx = cur;

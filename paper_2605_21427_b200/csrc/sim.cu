@@ -677,7 +677,7 @@ struct Resources {
             cudaFree(s.d_tables);
         }
         for (auto* m : plant_models) pals_model_destroy(m);
-        for (void* p : dev) cudaFree(p);
+        for (void* p : dev) cudaFreeAsync(p, ctx->stream);
     }
     // staged arena: every per-scenario / per-node array is packed into one device
     // allocation (thousands of small cudaMalloc / cudaFree calls would dominate the call
@@ -769,8 +769,23 @@ struct Resources {
     }
     template <class T>
     int alloc(T** p, size_t n) {
+        // stream-ordered pool allocations: the call's per-call buffers (the zeroed running
+        // lists alone are ~100 MB at 256 seeds) come back from the device's pool, kept across
+        // calls, instead of cudaMalloc / cudaFree, whose device syncs and unmaps stalled
+        // some calls by 0.2-0.8 s
+        static thread_local int pool_dev = -1;
+        if (pool_dev != ctx->device) {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) {
+                uint64_t keep = ~0ull;
+                (void)cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+            (void)cudaGetLastError();
+            pool_dev = ctx->device;
+        }
         void* q = nullptr;
-        const cudaError_t e = cudaMalloc(&q, std::max<size_t>(1, n) * sizeof(T));
+        const cudaError_t e =
+            cudaMallocAsync(&q, std::max<size_t>(1, n) * sizeof(T), ctx->stream);
         if (e != cudaSuccess) return cuda_fail(e, "pals_run_scenarios: cudaMalloc");
         dev.push_back(q);
         *p = (T*)q;
@@ -1219,6 +1234,7 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
                     p_off.push_back((int64_t)nmodel.size());
                 }
             }
+            phase("budget sets");
             pals_alloc* al = nullptr;
             int r = pals_alloc_create_sets(ctx, (int32_t)set_models.size(), set_models.data(),
                                            pts.data(), off.data(), gpu, coeffs, margin, &al);
@@ -1227,10 +1243,13 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
             std::vector<double> nb(nmodel.size()), tot(np);
             std::vector<uint8_t> sat(np);
             std::vector<int32_t> st(np);
+            phase("alloc created");
             r = pals_allocate_budget(al, 25.0, np, p_off.data(), nmodel.data(), ndp.data(),
                                      ntarget.data(), cbudget.data(), nb.data(), tot.data(),
                                      sat.data(), st.data());
+            phase("allocated");
             pals_alloc_destroy(al);
+            phase("alloc freed");
             if (r) return r;
             for (int64_t p = 0; p < np; ++p)
                 if (st[p] != PALS_OK)

@@ -1393,7 +1393,14 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
     }
     cudaStream_t hs_stream = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_hash = nullptr;
-    PALS_CUDA(cudaStreamCreateWithFlags(&hs_stream, cudaStreamNonBlocking));
+    {
+        // the greatest priority: the arrival hashes (launched once the last chunk is up, while
+        // k_sim's blocks hold the SMs) take the first free block slots instead of waiting
+        // for k_sim's tail
+        int lo = 0, hi = 0;
+        PALS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        PALS_CUDA(cudaStreamCreateWithPriority(&hs_stream, cudaStreamNonBlocking, hi));
+    }
     struct StreamGuard {
         cudaStream_t& s;
         cudaEvent_t& a;

@@ -123,6 +123,7 @@ int pals_ctx_destroy(pals_ctx* c) {
     cudaSetDevice(c->device);
     replay_cache_free(c);
     one_cache_free(c);
+    sim_cache_free(c);
     if (c->d_scratch) cudaFree(c->d_scratch);
     if (c->d_front) cudaFree(c->d_front);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);

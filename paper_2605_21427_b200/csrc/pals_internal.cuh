@@ -234,6 +234,7 @@ struct pals_ctx {
     size_t sim_stream_bytes = 0;
     int* h_sim_flags = nullptr;     // pinned 1s: the value the chunk-ready flag copies write
     void* replay_cache = nullptr;  // replay.cu
+    void* sim_cache = nullptr;     // sim.cu: plant models and select-table sets across calls
     void* one_cache = nullptr;     // replay.cu: single-call candidate sets (pals_select_one)
     int replay_layout = 0;         // PALS_REPLAY_THREAD / PALS_REPLAY_WARP
     int64_t one_server_idle_us = 2000;  // pals_ctx_set_one_server: 0 = one launch per call
@@ -306,6 +307,7 @@ void count_launch(pals_ctx* ctx, int k = 1);
 const PlanDev& plan_dev(const pals_plan* p);
 int plan_error(const pals_plan* p);
 void replay_cache_free(pals_ctx* ctx);
+void sim_cache_free(pals_ctx* ctx);
 void one_cache_free(pals_ctx* ctx);
 void one_server_stop(pals_ctx* ctx);  // replay.cu: ends the resident single-call kernel
 uint64_t next_model_uid();

@@ -661,23 +661,75 @@ struct SelSet {  // select tables for one (scorer, candidates, degrees)
     ReplayModelDev* d_m = nullptr;
     void* d_tables = nullptr;
     std::vector<pals_point> pts;
+    bool built = false;
+    void release() {
+        if (pl) pals_plan_destroy(pl);
+        if (g) pals_grid_destroy(g);
+        if (d_m) cudaFree(d_m);
+        if (d_tables) cudaFree(d_tables);
+        pl = nullptr;
+        g = nullptr;
+        d_m = nullptr;
+        d_tables = nullptr;
+        built = false;
+    }
 };
+
+// Kept by the context across pals_run_scenarios calls: the plant models (one per distinct
+// (profile, GPU spec)) and every select-table set, keyed by its scorer's uid (never reused,
+// unlike its address), the candidates and the bytes of everything else it was built from
+// (coefficients, plant model 0). A seed sweep rebuilds nothing, and no call pays the set
+// destructions, whose cudaFree calls stalled calls by up to ~1 s. Freed with the context.
+using SetKey = std::tuple<uint64_t, std::string, std::vector<std::tuple<double, int, int, int, int>>>;
+struct SimCache {
+    std::map<std::string, pals_model*> plants;
+    std::map<SetKey, SelSet*> sets;
+};
+
+}  // namespace
+
+void sim_cache_free(pals_ctx* ctx) {
+    if (!ctx || !ctx->sim_cache) return;
+    SimCache* c = (SimCache*)ctx->sim_cache;
+    for (auto& kv : c->sets) {
+        kv.second->release();
+        delete kv.second;
+    }
+    for (auto& kv : c->plants) pals_model_destroy(kv.second);
+    delete c;
+    ctx->sim_cache = nullptr;
+}
+
+namespace {
+
+SimCache& sim_cache_of(pals_ctx* ctx) {
+    if (!ctx->sim_cache) ctx->sim_cache = new SimCache;
+    return *(SimCache*)ctx->sim_cache;
+}
+
+template <class T>
+std::string raw_bytes(const T& v) {
+    return std::string(reinterpret_cast<const char*>(&v), sizeof v);
+}
 
 struct Resources {
     pals_ctx* ctx;
-    std::vector<SelSet> sets;
-    std::vector<pals_model*> plant_models;
+    std::vector<SelSet*> sets;               // owned by the context's SimCache
+    std::vector<pals_model*> plant_models;   // likewise
     std::vector<void*> dev;
     ~Resources() {
+        static const bool verbose = getenv("PALS_SIM_VERBOSE") != nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
+        auto mark = [&](const char* what) {
+            if (verbose)
+                fprintf(stderr, "[pals_run_scenarios]   release %-8s %.3f s\n", what,
+                        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0)
+                            .count());
+        };
         cudaStreamSynchronize(ctx->stream);
-        for (auto& s : sets) {
-            if (s.pl) pals_plan_destroy(s.pl);
-            if (s.g) pals_grid_destroy(s.g);
-            cudaFree(s.d_m);
-            cudaFree(s.d_tables);
-        }
-        for (auto* m : plant_models) pals_model_destroy(m);
+        mark("sync");
         for (void* p : dev) cudaFreeAsync(p, ctx->stream);
+        mark("pool");
     }
     // staged arena: every per-scenario / per-node array is packed into one device
     // allocation (thousands of small cudaMalloc / cudaFree calls would dominate the call
@@ -881,12 +933,21 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
     } phase_end{phase};
     Resources res{ctx};
     // plant models (analytic, one per profile): device Analytic + the oracle's scorer
+    SimCache& cache = sim_cache_of(ctx);
     for (int m = 0; m < n_models; ++m) {
-        pals_model* pm = nullptr;
-        int r = pals_model_analytic(ctx, &profiles[m], gpu, &pm);
-        if (r) return r;
-        res.plant_models.push_back(pm);
+        const std::string key = raw_bytes(profiles[m]) + raw_bytes(*gpu);
+        auto it = cache.plants.find(key);
+        if (it == cache.plants.end()) {
+            pals_model* pm = nullptr;
+            int r = pals_model_analytic(ctx, &profiles[m], gpu, &pm);
+            if (r) return r;
+            it = cache.plants.emplace(key, pm).first;
+        }
+        res.plant_models.push_back(it->second);
     }
+    // what a select set is built from besides its scorer and candidates
+    const std::string set_env =
+        raw_bytes(*coeffs) + raw_bytes(profiles[0]) + raw_bytes(*gpu);
     Analytic* d_plant = nullptr;
     {
         std::vector<Analytic> h;
@@ -980,8 +1041,14 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
                 auto it = set_of.find({scorer, key});
                 if (it == set_of.end()) {
                     it = set_of.emplace(std::make_pair(scorer, key), (int)res.sets.size()).first;
-                    res.sets.emplace_back();
-                    res.sets.back().pts = pts;
+                    const SetKey ck{scorer->uid, set_env, key};
+                    auto cit = cache.sets.find(ck);
+                    if (cit == cache.sets.end()) {
+                        SelSet* ns = new SelSet;
+                        ns->pts = pts;
+                        cit = cache.sets.emplace(ck, ns).first;
+                    }
+                    res.sets.push_back(cit->second);
                 }
                 node_set[gi] = it->second;
                 node_memo.emplace(std::make_pair(scorer, std::move(tk)),
@@ -993,7 +1060,9 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
     // build every select-table set: plan (scores + ranks) -> k_build_tables
     std::vector<int> set_scorer_model(res.sets.size(), -1);
     for (auto& [k, si] : set_of) {
-        SelSet& S = res.sets[si];
+        SelSet& S = *res.sets[si];
+        if (S.built) continue;  // from an earlier call (SimCache)
+        S.release();            // a build an earlier call failed to finish
         const pals_model* scorer = k.first;
         const int n = (int)S.pts.size();
         if (n > kMaxReplayCands)
@@ -1038,7 +1107,8 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
         m.ut = (const double*)(base + ((W * W * 4 + W * 4 + 7) & ~(size_t)7));
         m.up = m.ut + W;
         // k_build_tables also derives plant constants from m.plant: any node of the
-        // set shares the profile-independent parts used here; point it at model 0
+        // set shares the profile-independent parts used here; point it at model 0 (only
+        // k_build_tables reads it: the cached set keeps a pointer of this call, unused later)
         m.plant = d_plant;
         PALS_CUDA(copy_on(ctx->stream, S.d_m, &m, sizeof m, cudaMemcpyHostToDevice));
         k_build_tables<<<1, 1024, 0, ctx->stream>>>(d, S.d_m, (uint32_t*)m.m2, (uint32_t*)m.b1,
@@ -1047,6 +1117,7 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
         count_launch(ctx);
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "k_build_tables");
+        S.built = true;
     }
 
     phase("tables");
@@ -1155,34 +1226,65 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
     } joiner{stream_threads, stop_workers};
 
     phase("streams started");
-    // budget changes and their splits (assign_budgets, sim.hpp:229-238, 277-283, 313-336)
-    std::vector<std::vector<int32_t>> chg_k(n_scen);
-    std::vector<std::vector<double>> chg_w(n_scen);
-    std::vector<std::vector<double>> track(n_scen);
-    for (int s = 0; s < n_scen; ++s) {
-        const pals_scenario& sc = scens[s];
-        if (sc.n_trace > 0) {
-            double last = -1.0;
-            TraceCursor at_t0{sc}, at_t{sc};
-            for (int k = 0; k < n_int[s]; ++k) {
-                const double wv = at_t0(k * sc.interval_s);
-                if (wv != last) {
-                    chg_k[s].push_back(k);
-                    chg_w[s].push_back(wv);
-                    last = wv;
+    // budget changes and their splits (assign_budgets, sim.hpp:229-238, 277-283, 313-336).
+    // The change list and the per-interval tracking target are a function of the cluster
+    // signal (trace or static budget), the interval and the interval count, which a seed
+    // sweep repeats in every scenario: computed and staged once per distinct signal.
+    std::vector<int> sig(n_scen, -1);
+    std::vector<std::vector<int32_t>> u_ck;
+    std::vector<std::vector<double>> u_cw, u_tr;
+    {
+        using SigKey = std::tuple<const double*, const double*, int, double, int, double>;
+        std::map<SigKey, int> sig_of;
+        for (int s = 0; s < n_scen; ++s) {
+            const pals_scenario& sc = scens[s];
+            if (sc.n_trace <= 0 && !sc.has_cluster_budget) continue;
+            const SigKey key = sc.n_trace > 0
+                                   ? SigKey{sc.trace_t, sc.trace_w, sc.n_trace, sc.interval_s,
+                                            n_int[s], 0.0}
+                                   : SigKey{nullptr, nullptr, 0, sc.interval_s, n_int[s],
+                                            sc.cluster_budget_w};
+            auto it = sig_of.find(key);
+            if (it != sig_of.end()) {
+                sig[s] = it->second;
+                continue;
+            }
+            const int id = (int)u_ck.size();
+            sig_of.emplace(key, id);
+            sig[s] = id;
+            u_ck.emplace_back();
+            u_cw.emplace_back();
+            u_tr.emplace_back();
+            std::vector<int32_t>& ck = u_ck.back();
+            std::vector<double>& cw = u_cw.back();
+            std::vector<double>& tr = u_tr.back();
+            if (sc.n_trace > 0) {
+                double last = -1.0;
+                TraceCursor at_t0{sc}, at_t{sc};
+                for (int k = 0; k < n_int[s]; ++k) {
+                    const double wv = at_t0(k * sc.interval_s);
+                    if (wv != last) {
+                        ck.push_back(k);
+                        cw.push_back(wv);
+                        last = wv;
+                    }
                 }
+                tr.resize(n_int[s]);
+                for (int k = 0; k < n_int[s]; ++k) {
+                    const double t1 = k * sc.interval_s + sc.interval_s;
+                    tr[k] = at_t(t1 - sc.interval_s);
+                }
+            } else {
+                ck.push_back(0);
+                cw.push_back(sc.cluster_budget_w);
+                tr.assign(n_int[s], sc.cluster_budget_w);
             }
-            track[s].resize(n_int[s]);
-            for (int k = 0; k < n_int[s]; ++k) {
-                const double t1 = k * sc.interval_s + sc.interval_s;
-                track[s][k] = at_t(t1 - sc.interval_s);
-            }
-        } else if (sc.has_cluster_budget) {
-            chg_k[s].push_back(0);
-            chg_w[s].push_back(sc.cluster_budget_w);
-            track[s].assign(n_int[s], sc.cluster_budget_w);
         }
     }
+    const std::vector<int32_t> no_ck;
+    const std::vector<double> no_d;
+    auto CK = [&](int s) -> const std::vector<int32_t>& { return sig[s] < 0 ? no_ck : u_ck[sig[s]]; };
+    auto CW = [&](int s) -> const std::vector<double>& { return sig[s] < 0 ? no_d : u_cw[sig[s]]; };
     // node budgets per change: [scenario][change][node]
     std::vector<std::vector<double>> chg_b(n_scen);
     {
@@ -1190,17 +1292,17 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
         std::map<double, std::vector<int>> by_margin;
         for (int s = 0; s < n_scen; ++s) {
             const pals_scenario& sc = scens[s];
-            chg_b[s].assign(chg_k[s].size() * sc.n_nodes, 0.0);
-            if (chg_k[s].empty()) continue;
+            chg_b[s].assign(CK(s).size() * sc.n_nodes, 0.0);
+            if (CK(s).empty()) continue;
             if (sc.policy == PALS_POLICY_JOINT || sc.policy == PALS_POLICY_ORACLE) {
                 by_margin[sc.controller.budget_margin].push_back(s);
             } else {
                 int total_dp = 0;
                 for (int i = 0; i < sc.n_nodes; ++i) total_dp += sc.nodes[i].dp;
-                for (size_t c = 0; c < chg_k[s].size(); ++c)
+                for (size_t c = 0; c < CK(s).size(); ++c)
                     for (int i = 0; i < sc.n_nodes; ++i)
                         chg_b[s][c * sc.n_nodes + i] =
-                            chg_w[s][c] * (double)sc.nodes[i].dp / total_dp;
+                            CW(s)[c] * (double)sc.nodes[i].dp / total_dp;
             }
         }
         for (auto& [margin, ss] : by_margin) {
@@ -1216,21 +1318,21 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
                 const pals_scenario& sc = scens[s];
                 int64_t g0 = 0;
                 for (int q = 0; q < s; ++q) g0 += scens[q].n_nodes;
-                for (size_t c = 0; c < chg_k[s].size(); ++c) {
+                for (size_t c = 0; c < CK(s).size(); ++c) {
                     for (int i = 0; i < sc.n_nodes; ++i) {
                         const int si = node_set[g0 + i];
                         auto it = aset.find(si);
                         if (it == aset.end()) {
                             it = aset.emplace(si, (int)set_models.size()).first;
                             set_models.push_back((pals_model*)node_scorer[g0 + i]);
-                            pts.insert(pts.end(), res.sets[si].pts.begin(), res.sets[si].pts.end());
+                            pts.insert(pts.end(), res.sets[si]->pts.begin(), res.sets[si]->pts.end());
                             off.push_back((int64_t)pts.size());
                         }
                         nmodel.push_back(it->second);
                         ndp.push_back(sc.nodes[i].dp);
                         ntarget.push_back(sc.objective == PALS_OBJ_QOS ? node_target[g0 + i] : 0.0);
                     }
-                    cbudget.push_back(chg_w[s][c]);
+                    cbudget.push_back(CW(s)[c]);
                     p_off.push_back((int64_t)nmodel.size());
                 }
             }
@@ -1258,7 +1360,7 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
             int64_t o = 0;
             for (int s : ss) {
                 const pals_scenario& sc = scens[s];
-                for (size_t c = 0; c < chg_k[s].size(); ++c)
+                for (size_t c = 0; c < CK(s).size(); ++c)
                     for (int i = 0; i < sc.n_nodes; ++i) chg_b[s][c * sc.n_nodes + i] = nb[o++];
             }
         }
@@ -1298,6 +1400,8 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
     // device buffers: stage every array, one upload, then point the descriptors at it
     std::vector<SimScenDev> hs(n_scen);
     std::vector<SimNodeDev> hn(total_nodes);
+    constexpr size_t kNoOff = ~(size_t)0;
+    std::vector<size_t> u_off_ck(u_ck.size(), kNoOff), u_off_tr(u_ck.size(), kNoOff);
     std::vector<size_t> o_chg(n_scen), o_track(n_scen, 0), o_bud(total_nodes),
         o_run_len(total_nodes), o_run_gen(total_nodes), o_run_id(total_nodes),
         o_req_k(total_nodes), o_req_gen(total_nodes);
@@ -1307,11 +1411,19 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
         int64_t gi = 0;
         for (int s = 0; s < n_scen; ++s) {
             const pals_scenario& sc = scens[s];
-            o_chg[s] = res.stage(chg_k[s]);
-            if (!track[s].empty()) o_track[s] = res.stage(track[s]);
+            if (sig[s] >= 0) {  // staged once per distinct signal
+                if (u_off_ck[sig[s]] == kNoOff) {
+                    u_off_ck[sig[s]] = res.stage(u_ck[sig[s]]);
+                    u_off_tr[sig[s]] = res.stage(u_tr[sig[s]]);
+                }
+                o_chg[s] = u_off_ck[sig[s]];
+                o_track[s] = u_off_tr[sig[s]];
+            } else {
+                o_chg[s] = res.stage(no_ck);
+            }
             const int mb = *std::max_element(sc.cand_batches, sc.cand_batches + sc.n_batches);
             for (int i = 0; i < sc.n_nodes; ++i, ++gi) {
-                std::vector<double> nbud(chg_k[s].size());
+                std::vector<double> nbud(CK(s).size());
                 for (size_t c = 0; c < nbud.size(); ++c) nbud[c] = chg_b[s][c * sc.n_nodes + i];
                 o_bud[gi] = res.stage(nbud);
                 const size_t run_cap =
@@ -1342,17 +1454,17 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
             S.policy = sc.policy;
             S.objective = sc.objective;
             S.budget_active = sc.has_cluster_budget || sc.n_trace > 0;
-            S.n_changes = (int)chg_k[s].size();
+            S.n_changes = (int)CK(s).size();
             S.interval_s = sc.interval_s;
             S.epsilon = sc.epsilon;
             S.cfg = sc.controller;
             S.change_k = res.at<int32_t>(o_chg[s]);
-            S.track_target = track[s].empty() ? nullptr : res.at<double>(o_track[s]);
+            S.track_target = sig[s] < 0 ? nullptr : res.at<double>(o_track[s]);
             for (int i = 0; i < sc.n_nodes; ++i, ++gi) {
                 SimNodeDev& N = hn[gi];
                 const pals_sim_node& n = sc.nodes[i];
                 memset(&N, 0, sizeof N);
-                N.sel = res.sets[node_set[gi]].d_m;
+                N.sel = res.sets[node_set[gi]]->d_m;
                 N.plant = d_plant + n.model;
                 N.tp = n.tp;
                 N.ep = n.ep;

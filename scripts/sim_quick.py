@@ -1,4 +1,4 @@
-"""Quick GPU check of the queue-plant leg alone: python scripts/sim_quick.py [seeds]"""
+"""Quick GPU check of the queue-plant leg alone: python scripts/sim_quick.py [seeds [bench flags]]"""
 import json
 import os
 import sys
@@ -8,7 +8,7 @@ import bench  # noqa: E402
 from paper_2605_21427_b200.wattserve import Context  # noqa: E402
 
 seeds = int(sys.argv[1]) if len(sys.argv) > 1 else 64
-sys.argv = ["bench.py", "--sim-seeds", str(seeds)]
+sys.argv = ["bench.py", "--sim-seeds", str(seeds)] + sys.argv[2:]
 args = bench.parse()
 d = bench.Dist()
 ctx = Context(0)

@@ -273,9 +273,13 @@ struct SimArgs {
     pals_sim_decision* dec;
     int smem_run;  // > 0: running lists live in shared memory, smem_run entries per warp
     const int32_t* order;  // CTA -> scenario
-    const int* flags;      // streamed arrivals: per chunk of chunk_k intervals, 1 once on device
+    const int* flags;      // streamed arrivals: per (CTA group, chunk of chunk_k intervals), 1
+                           // once on device; a group's flag also covers every earlier group
     int chunk_k;
+    int n_chunks;
+    int n_groups;  // CTA group of block b: b * n_groups / gridDim.x (runs of the CTA order)
 };
+constexpr int kSimGroups = 4;  // 2 / 6 / 8 measured no better (scripts/ab_sim.sh)
 
 // Wait until the arrivals of interval k's chunk are on the device (streamed upload): lane 0
 // polls the chunk's flag (device memory, written by a copy queued after the chunk's data)
@@ -283,7 +287,7 @@ struct SimArgs {
 // every flag before returning, so this only bounds a host failure).
 __device__ __forceinline__ void await_chunk(const SimArgs& a, int k, int& ready_until) {
     if (k < ready_until) return;
-    const int c = k / a.chunk_k;
+    const int c = (int)(((int64_t)blockIdx.x * a.n_groups / gridDim.x) * a.n_chunks) + k / a.chunk_k;
     if ((threadIdx.x & 31) == 0) {
         unsigned long long t0, t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -297,7 +301,7 @@ __device__ __forceinline__ void await_chunk(const SimArgs& a, int k, int& ready_
         }
     }
     __syncwarp();
-    ready_until = (c + 1) * a.chunk_k;
+    ready_until = (k / a.chunk_k + 1) * a.chunk_k;
 }
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -1127,6 +1131,21 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
     for (int s = 0; s < n_scen; ++s) node0[s + 1] = node0[s] + scens[s].n_nodes;
     std::vector<int> node_stream(total_nodes);
     std::vector<std::pair<int, int>> work;  // (scenario, node) generating each stream
+    // CTA order: most node-intervals first, so the long scenarios do not form the tail
+    std::vector<int32_t> order(n_scen);
+    for (int s = 0; s < n_scen; ++s) order[s] = s;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+        return (int64_t)n_int[x] * scens[x].n_nodes > (int64_t)n_int[y] * scens[y].n_nodes;
+    });
+    // CTA groups: G equal runs of the CTA order. Streams are drawn and published group by
+    // group (each group in interval chunks), so the first CTAs to run wait for the draws of
+    // a quarter of the streams, not of all of them; a stream belongs to the first group
+    // that reads it
+    const int n_groups = std::max(1, std::min(kSimGroups, n_scen));
+    std::vector<int> scen_group(n_scen);
+    for (int pos = 0; pos < n_scen; ++pos)
+        scen_group[order[pos]] = (int)((int64_t)pos * n_groups / n_scen);
+    std::vector<int> stream_group;
     {
         using Key = std::tuple<uint64_t, int, double, int, double, double, double, int>;
         std::map<Key, int> seen;
@@ -1140,9 +1159,28 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
                 if (it == seen.end()) {
                     it = seen.emplace(key, (int)work.size()).first;
                     work.emplace_back(s, i);
+                    stream_group.push_back(scen_group[s]);
                 }
                 node_stream[node0[s] + i] = it->second;
+                stream_group[it->second] = std::min(stream_group[it->second], scen_group[s]);
             }
+    }
+    // streams renumbered group by group: a group's count columns are one contiguous range
+    std::vector<int> gcol(n_groups + 1, 0);
+    {
+        std::vector<int> perm(work.size()), inv(work.size());
+        for (size_t u = 0; u < work.size(); ++u) perm[u] = (int)u;
+        std::stable_sort(perm.begin(), perm.end(),
+                         [&](int x, int y) { return stream_group[x] < stream_group[y]; });
+        std::vector<std::pair<int, int>> w2(work.size());
+        for (size_t v = 0; v < perm.size(); ++v) {
+            w2[v] = work[perm[v]];
+            inv[perm[v]] = (int)v;
+            ++gcol[stream_group[perm[v]] + 1];
+        }
+        work.swap(w2);
+        for (auto& x : node_stream) x = inv[x];
+        for (int g = 0; g < n_groups; ++g) gcol[g + 1] += gcol[g];
     }
     // Streamed arrivals. Each stream has a fixed region (cum, then len up to a capacity
     // bound) in one pinned buffer mirrored by one device buffer, so the node descriptors
@@ -1192,7 +1230,8 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
     // [chunk][stream]: the stream's request count after the chunk (its len range is
     // [count after chunk c - 1, count after chunk c))
     std::vector<int64_t> s_after((size_t)kSimChunks * n_streams, 0);
-    std::atomic<int> chunk_done[kSimChunks];
+    const int n_pub = n_groups * kSimChunks;  // publications (group, chunk), group-major
+    std::vector<std::atomic<int>> chunk_done(n_pub);
     for (auto& x : chunk_done) x = 0;
     std::atomic<bool> stop_workers{false};
     std::vector<std::thread> stream_threads;
@@ -1204,14 +1243,15 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
         n_workers = std::max(1u, std::min<unsigned>(hc > 1 ? hc - 1 : 1, (unsigned)n_streams));
         for (unsigned t = 0; t < n_workers; ++t)
             stream_threads.emplace_back([&, t] {
-                for (int c = 0; c < kSimChunks && !stop_workers; ++c) {
-                    for (size_t u = t; u < n_streams; u += n_workers) {
+                for (int i = 0; i < n_pub && !stop_workers; ++i) {
+                    const int gr = i / kSimChunks, c = i % kSimChunks;
+                    for (size_t u = gcol[gr] + t; u < (size_t)gcol[gr + 1]; u += n_workers) {
                         StreamGen& g = gens[u];
                         const int k0 = c * chunk_k, k1 = std::min(g.n_int, (c + 1) * chunk_k);
                         if (k0 < k1) g.run(k0, k1);
                         s_after[(size_t)c * n_streams + u] = g.count;
                     }
-                    chunk_done[c].fetch_add(1, std::memory_order_release);
+                    chunk_done[i].fetch_add(1, std::memory_order_release);
                 }
             });
     }
@@ -1528,12 +1568,6 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
     // (the arrival hashes run on hs_stream after the last chunk's copies, below)
     SimArgs A;
     memset(&A, 0, sizeof A);
-    // CTA order: most node-intervals first, so the long scenarios do not form the tail
-    std::vector<int32_t> order(n_scen);
-    for (int s = 0; s < n_scen; ++s) order[s] = s;
-    std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
-        return (int64_t)n_int[x] * scens[x].n_nodes > (int64_t)n_int[y] * scens[y].n_nodes;
-    });
     int r = res.upload((int32_t**)&A.order, order);
     if (r) return r;
     r = res.upload((SimScenDev**)&A.scen, hs);
@@ -1563,16 +1597,18 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
     // (polling mapped host memory from every warp starved the copies themselves)
     int* d_flags = nullptr;
     {
-        int r = res.alloc(&d_flags, kSimChunks);
+        int r = res.alloc(&d_flags, n_pub);
         if (r) return r;
     }
     if (!ctx->h_sim_flags) {  // pinned source of the flag value (1)
         PALS_CUDA(cudaHostAlloc((void**)&ctx->h_sim_flags, 64 * sizeof(int), cudaHostAllocDefault));
         for (int c = 0; c < 64; ++c) ctx->h_sim_flags[c] = 1;
     }
-    PALS_CUDA(cudaMemsetAsync(d_flags, 0, kSimChunks * sizeof(int), ctx->stream));
+    PALS_CUDA(cudaMemsetAsync(d_flags, 0, n_pub * sizeof(int), ctx->stream));
     A.flags = d_flags;
     A.chunk_k = chunk_k;
+    A.n_chunks = kSimChunks;
+    A.n_groups = n_groups;
     PALS_CUDA(cudaStreamSynchronize(ctx->stream));
     phase("upload");
     // whatever happens below, every chunk flag is raised before this function returns, so a
@@ -1580,20 +1616,21 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
     struct FlagGuard {
         pals_ctx* c;
         int* f;
+        int n;
         cudaStream_t& s;
         ~FlagGuard() {
-            cudaMemcpyAsync(f, c->h_sim_flags, kSimChunks * sizeof(int), cudaMemcpyHostToDevice,
-                            s);
+            cudaMemcpyAsync(f, c->h_sim_flags, n * sizeof(int), cudaMemcpyHostToDevice, s);
             cudaStreamSynchronize(s);
             cudaStreamSynchronize(c->stream);
         }
-    } flag_guard{ctx, d_flags, hs_stream};
-    // chunk c: wait for its draws, copy every stream's new part up on hs_stream, then raise
-    // the chunk's flag once the copies have landed (a host function in stream order)
-    auto publish = [&](int c) -> int {
-        while (chunk_done[c].load(std::memory_order_acquire) < (int)n_workers)
+    } flag_guard{ctx, d_flags, n_pub, hs_stream};
+    // publication i = (group, chunk c): wait for its draws, copy the group's streams' new
+    // parts up on hs_stream, then raise its flag once the copies have landed (stream order)
+    auto publish = [&](int i) -> int {
+        while (chunk_done[i].load(std::memory_order_acquire) < (int)n_workers)
             std::this_thread::sleep_for(std::chrono::microseconds(20));
-        for (size_t u = 0; u < n_streams; ++u) {
+        const int gr = i / kSimChunks, c = i % kSimChunks;
+        for (size_t u = gcol[gr]; u < (size_t)gcol[gr + 1]; ++u) {
             const int ni = gens[u].n_int;
             const int64_t l0 = c ? std::min(s_cap[u], s_after[(size_t)(c - 1) * n_streams + u]) : 0;
             const int64_t l1 = std::min(s_cap[u], s_after[(size_t)c * n_streams + u]);
@@ -1607,17 +1644,19 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
             const int k0 = c * chunk_k;
             const int k1 =
                 c == kSimChunks - 1 ? max_n_int + 1 : std::min(max_n_int + 1, (c + 1) * chunk_k);
-            if (k1 > k0)
-                PALS_CUDA(cudaMemcpyAsync(dbuf + (size_t)k0 * n_streams, hbuf + (size_t)k0 * n_streams,
-                                          (size_t)(k1 - k0) * n_streams * 4,
-                                          cudaMemcpyHostToDevice, hs_stream));
+            const size_t ncol = (size_t)(gcol[gr + 1] - gcol[gr]);
+            if (k1 > k0 && ncol)  // the group's columns of those rows
+                PALS_CUDA(cudaMemcpy2DAsync(dbuf + (size_t)k0 * n_streams + gcol[gr], n_streams * 4,
+                                            hbuf + (size_t)k0 * n_streams + gcol[gr], n_streams * 4,
+                                            ncol * 4, (size_t)(k1 - k0), cudaMemcpyHostToDevice,
+                                            hs_stream));
         }
-        PALS_CUDA(cudaMemcpyAsync(d_flags + c, ctx->h_sim_flags, sizeof(int),
+        PALS_CUDA(cudaMemcpyAsync(d_flags + i, ctx->h_sim_flags, sizeof(int),
                                   cudaMemcpyHostToDevice, hs_stream));
         return PALS_OK;
     };
     // streamed: launch after chunk 0; otherwise (profiling) after every chunk
-    const int pre = ctx->sim_streaming ? 1 : kSimChunks;
+    const int pre = ctx->sim_streaming ? 1 : n_pub;
     for (int c = 0; c < pre; ++c) {
         const int pr = publish(c);
         if (pr) return pr;
@@ -1637,7 +1676,7 @@ extern "C" int pals_run_scenarios(pals_ctx* ctx, int32_t n_scen, const pals_scen
     count_launch(ctx);
     cudaError_t e = cudaGetLastError();
     cudaEventRecord(ev1, ctx->stream);
-    for (int c = pre; c < kSimChunks && e == cudaSuccess; ++c) {
+    for (int c = pre; c < n_pub && e == cudaSuccess; ++c) {
         const int pr = publish(c);
         if (pr) return pr;
     }
